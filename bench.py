@@ -1,0 +1,326 @@
+#!/usr/bin/env python
+"""GP-MPPI solve benchmark (BASELINE.json metric) — one JSON line on rank 0.
+
+Workload (N=1): BASELINE config 2 — GP-MPPI chance-constrained path following
++ 10 tightened circular obstacles, K=4096, T=40, M(=n GP points)=512, 3 terrains,
+p_x=0.95; synthetic lane/obstacles, random-init GP of that shape (no datasets).
+A "step" = one full plan_step (noise → rollout → variance → softmax update →
+shift → tightening pass).
+
+  value  = sample-rollout-steps/s over the timed ticks, device-resident inputs,
+           CUDA events on the planner stream, L2 flushed between ticks (outside
+           the timed spans), max over ranks.
+  e2e    = the same metric through the public C-ABI plan_step with host buffers
+           (H2D of x0 + task, D2H of command + diagnostics inside the timed span).
+  N > 1  = sharded solve, weak scaling: K = 4096·N samples per solve, each rank
+           rolls out 4096 (global-index Philox noise), one all-gather of the
+           (2T+6)-double reduction tuple over NCCL, every rank finishes identically.
+--impl reference: the reference algorithm's FP64 CPU restatement (oracle/, the
+           reference itself needs Eigen and cannot be built here), all host
+           threads, 128-sample chunks as mppi.cpp:401-426, same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def _percentile(xs, q):
+    return float(np.percentile(np.asarray(xs, dtype=np.float64), q))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def build_planner(w, api, samples=None, var_path=None):
+    from paper_2411_03289_b200 import workloads as W
+    task, track, obstacles = W.make_task_objects(w, api)
+    cfg = api.MppiConfig(samples=samples or w.samples, horizon=w.horizon, lam=w.lam,
+                         sigma_sim=w.sigma_sim, seed=w.seed)
+    if w.model == "gp":
+        X, Y, K = W.gp_training_set(w.n_points, w.terrains, seed=0)
+        gp = api.GpModel.fit(X, Y, K)
+        p = api.Planner(cfg, api.GpEnsemble(gp, w.terrains), p_x=w.p_x)
+    else:
+        p = api.Planner(cfg, api.NominalDynamic(), p_x=w.p_x)
+    if var_path is not None:
+        p.set_variance_path(var_path)
+    return p, task
+
+
+def cpu_reference(w, steps, warmup, threads=0, samples=None):
+    """Oracle port of the reference algorithm, timed on this host's cores."""
+    from oracle import oracle as O
+    from paper_2411_03289_b200 import workloads as W
+    from tests.helpers import oracle_task
+    K = samples or w.samples
+    X, Y, Kp = W.gp_training_set(w.n_points, w.terrains, seed=0)
+    gp = O.GP(X, Y, Kp) if w.model == "gp" else None
+    obstacles = W.random_obstacle_field(w.n_obstacles, seed=3) if w.n_obstacles else np.zeros((0, 3))
+    to = oracle_task(w, obstacles)
+    kind = O.ORC_MODEL_GP if w.model == "gp" else O.ORC_MODEL_NOMINAL
+    p = O.Planner(K, w.horizon, kind, gp, w.terrains if gp else 0, lam=w.lam,
+                  sigma_sim=w.sigma_sim, seed=w.seed, threads=threads, p_x=w.p_x)
+    x = np.array(w.x0, dtype=np.float64)
+    for _ in range(warmup):
+        p.plan_step(x, to)
+    ms = []
+    for _ in range(steps):
+        _, d = p.plan_step(x, to)
+        ms.append(d["plan_ms"])
+    return ms, p.threads_used(), K
+
+
+def run_reference_arm(args, w):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    # bounded sample: full K per step when a tick is ~1 s, otherwise scale K down
+    ms, threads, K = cpu_reference(w, args.steps, max(1, min(args.warmup, 1)), 0)
+    mean_ms = statistics.mean(ms)
+    value = K * w.horizon / (mean_ms / 1e3)
+    cpu = subprocess.run(["bash", "-c", "lscpu | grep 'Model name' | head -1"], capture_output=True,
+                         text=True).stdout.strip()
+    line = {
+        "impl": "reference", "metric": "sample-rollout-steps/s (GP-MPPI solve, p50/p99 ms in extra keys)",
+        "value": value, "unit": "sample-rollout-steps/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": mean_ms, "p50_ms": _percentile(ms, 50),
+        "p99_ms": _percentile(ms, 99), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{w.name}: K={K} T={w.horizon} n={w.n_points} R={w.terrains} "
+                   f"task={w.task} obstacles={w.n_obstacles}", "samples": K, "horizon": w.horizon,
+                   "gp_points": w.n_points},
+        "cpu_baseline": {"value": value, "unit": "sample-rollout-steps/s", "cores": threads,
+                         "kind": "port", "sample": f"{args.steps} full plan_step ticks of {w.name} "
+                         f"(K={K}) on {threads} threads; {cpu}"},
+        "e2e": {"value": value, "unit": "sample-rollout-steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="config2")
+    ap.add_argument("--variance-path", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=3)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    from paper_2411_03289_b200 import workloads as W
+    w = W.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference_arm(args, w)
+        return
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        run_sharded(args, w, world, rank)
+        return
+
+    import paper_2411_03289_b200 as G
+    planner, task = build_planner(w, G, var_path=args.variance_path)
+    x0 = np.array(w.x0, dtype=np.float64)
+    for _ in range(args.warmup):
+        planner.plan_step(x0, task)
+    launches0 = G.kernel_launches()
+    with ClockSampler(0) as clk:
+        tick_ms, phase = planner.bench_device(x0, task, args.steps, flush_l2=True)
+    launches = G.kernel_launches() - launches0
+    # e2e through the public plan_step (host buffers), L2 flushed between ticks
+    e2e_ms = []
+    for _ in range(args.steps):
+        G.flush_l2(0)
+        t0 = time.perf_counter()
+        planner.plan_step(x0, task)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    h2d, d2h = planner.io_bytes()
+    steps_per_tick = w.samples * w.horizon
+    mean_ms = float(np.mean(tick_ms))
+    value = steps_per_tick / (mean_ms / 1e3)
+    e2e_value = steps_per_tick / (float(np.mean(e2e_ms)) / 1e3)
+    peaks, peaks_kind = load_peaks()
+    # roofline of the dominant kernel phase (algorithmic FLOP)
+    n = w.n_points
+    rollout_ms, var_ms = phase[0] / args.steps, phase[1] / args.steps
+    var_flop = steps_per_tick * (n * n + 2 * n)
+    roll_flop = steps_per_tick * 22 * n
+    if var_ms >= rollout_ms:
+        dom, dom_ms, dom_flop = "variance", var_ms, var_flop
+    else:
+        dom, dom_ms, dom_flop = "rollout", rollout_ms, roll_flop
+    achieved = dom_flop / (dom_ms / 1e3) / 1e12
+    peak = peaks.get("bf16_tflops", 1590.0)
+    line = {
+        "metric": "sample-rollout-steps/s (GP-MPPI solve; p50/p99 latency in p50_ms/p99_ms)",
+        "value": value, "unit": "sample-rollout-steps/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": mean_ms, "p50_ms": _percentile(tick_ms, 50),
+        "p99_ms": _percentile(tick_ms, 99), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
+        "config": {"workload": f"{w.name}: GP-MPPI path following + {w.n_obstacles} tightened "
+                   f"obstacles, K={w.samples} T={w.horizon} M={n} R={w.terrains} p_x={w.p_x}",
+                   "samples": w.samples, "horizon": w.horizon, "gp_points": n,
+                   "parallelism": "single GPU", "l2": "flushed between ticks (2x L2 memset)",
+                   "variance_path": planner.variance_path()},
+        "phase_ms": {"rollout": rollout_ms, "variance": var_ms,
+                     "reduce_update": phase[2] / args.steps, "tightening": phase[3] / args.steps},
+        "e2e": {"value": e2e_value, "unit": "sample-rollout-steps/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "p50_ms": _percentile(e2e_ms, 50),
+                "p99_ms": _percentile(e2e_ms, 99)},
+        "roofline": {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                     "peak_kind": f"{peaks_kind} bf16 dense (MEASURED_PEAKS.json)",
+                     "flop_per_launch": dom_flop},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        ms, threads, K = cpu_reference(w, args.cpu_steps, 1, 0)
+        cpu_val = K * w.horizon / (statistics.mean(ms) / 1e3)
+        line["cpu_baseline"] = {"value": cpu_val, "unit": "sample-rollout-steps/s", "cores": threads,
+                                "kind": "port", "p50_ms": _percentile(ms, 50),
+                                "sample": f"{args.cpu_steps} plan_step ticks of {w.name} (K={K}), "
+                                          f"FP64 oracle, {threads} threads"}
+    print(json.dumps(line), flush=True)
+
+
+def run_sharded(args, w, world, rank):
+    """Weak-scaled sharded solve: K = w.samples·N, one NCCL all-gather per tick."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2411_03289_b200 as G
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    K_total = w.samples * world
+    planner, task = build_planner(w, G, samples=K_total)
+    planner.set_shard(rank * w.samples, w.samples)
+    W_t = G.tuple_doubles(w.horizon)
+    mine = torch.zeros(W_t, dtype=torch.float64, device="cuda")
+    gathered = torch.zeros(world, W_t, dtype=torch.float64, device="cuda")
+    x0 = np.array(w.x0, dtype=np.float64)
+
+    def tick():
+        planner.plan_partial(x0, task, mine.data_ptr())
+        dist.all_gather_into_tensor(gathered, mine)
+        torch.cuda.current_stream().synchronize()
+        return planner.plan_finish(gathered.data_ptr(), world)
+
+    for _ in range(args.warmup):
+        tick()
+    dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = G.kernel_launches()
+    ms = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            tick()
+            b.record()
+            b.synchronize()
+            ms.append(a.elapsed_time(b))
+    dist.barrier()
+    torch.cuda.synchronize()
+    t = torch.tensor(ms, dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = t.cpu().numpy()
+    launches = G.kernel_launches() - launches0
+    if rank == 0:
+        mean_ms = float(ms.mean())
+        value = K_total * w.horizon / (mean_ms / 1e3)
+        h2d, d2h = planner.io_bytes()
+        line = {
+            "metric": "sample-rollout-steps/s (GP-MPPI solve; p50/p99 latency in p50_ms/p99_ms)",
+            "value": value, "unit": "sample-rollout-steps/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": mean_ms, "p50_ms": _percentile(ms, 50),
+            "p99_ms": _percentile(ms, 99), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
+            "config": {"workload": f"{w.name} sharded: K={K_total} ({w.samples}/GPU) T={w.horizon} "
+                       f"M={w.n_points}", "samples": K_total, "horizon": w.horizon,
+                       "gp_points": w.n_points, "parallelism": f"sample-sharded x{world}, NCCL all-gather",
+                       "l2": "working set L2-resident; not flushed in the sharded loop"},
+            "e2e": {"value": value, "unit": "sample-rollout-steps/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,230 @@
+/*
+ * gpmppi_b200.h — C ABI of the B200-native GP-MPPI solve path.
+ *
+ * Drop-in boundary for the reference planner (/root/reference/proj). The
+ * reference exposes a C++ class API and no FFI; each entry point below names the
+ * reference interface it replaces (file:line under /root/reference/proj). Plain
+ * pointers and sizes only; all host arrays are row-major FP64 unless stated.
+ *
+ *   state   double[5]  (x, y, theta, v, omega)              core.hpp:30-36
+ *   control double[2]  (v_ref, omega_ref)                   core.hpp:54-56
+ *   eps     double[K][T][2]                                 mppi.cpp:53-62 (values)
+ *   kernel  double[6]  (signal_var, l0..l3, noise_var)      gp.hpp:12-22, gp.cpp:237-241
+ *
+ * Errors: every int-returning call returns a gpmppi_status; the message of the
+ * last failure on the calling thread is gpmppi_last_error(). The codes map onto
+ * the reference's exception classes (std::invalid_argument, std::runtime_error,
+ * std::logic_error; SURVEY §8(b) "Error conventions"). Non-finite samples and
+ * infeasible tightening are NOT errors (diag fields), as in the reference.
+ *
+ * There is no CPU fallback: every compute entry point runs sm_100a kernels and
+ * returns GPMPPI_CUDA_ERROR when no usable device is present.
+ */
+#ifndef GPMPPI_B200_H
+#define GPMPPI_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GPMPPI_ABI_VERSION 1
+
+typedef enum {
+  GPMPPI_OK = 0,
+  GPMPPI_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+  GPMPPI_RUNTIME_ERROR = 2,    /* std::runtime_error (Cholesky, file IO) */
+  GPMPPI_LOGIC_ERROR = 3,      /* std::logic_error */
+  GPMPPI_CUDA_ERROR = 4        /* no device / launch failure */
+} gpmppi_status;
+
+const char* gpmppi_last_error(void);
+int gpmppi_abi_version(void);
+/* number of sm_100a kernels this library launched in this process (evidence counter) */
+uint64_t gpmppi_kernel_launches(void);
+
+/* =============================== GP model ===============================
+ * Replaces gpmppi::GpModel (gp.hpp:30-98). The FP64 factorisation is computed
+ * on the host exactly as gp.cpp:61-150 (kernel grouping, jitter ladder
+ * 0,1e-10..1e-6, L^{-T}, alphas, LML); the device copy (Z, alpha, L^{-T} in
+ * FP64 and FP32) is uploaded once and owned by the model handle. */
+typedef struct gpmppi_model gpmppi_model;
+
+/* GpModel::fit (gp.cpp:61-150). inputs n×4, outputs n×m, kernels m×6. */
+int gpmppi_model_fit(const double* inputs, const double* outputs, int64_t n, int64_t m,
+                     const double* kernels, int device, gpmppi_model** out);
+/* GpModel::load (gp.cpp:244-272): GPMPPIG1 record, column-major FP64, refit on load. */
+int gpmppi_model_load(const char* path, int device, gpmppi_model** out);
+/* GpModel::save (gp.cpp:223-242): bit-exact round trip with the reference format. */
+int gpmppi_model_save(const gpmppi_model* model, const char* path);
+void gpmppi_model_free(gpmppi_model* model);
+int gpmppi_model_n_points(const gpmppi_model* model);  /* gp.hpp:59 */
+int gpmppi_model_n_outputs(const gpmppi_model* model); /* gp.hpp:60 */
+int gpmppi_model_n_groups(const gpmppi_model* model);  /* gp.hpp:68 */
+double gpmppi_model_group_jitter(const gpmppi_model* model, int group);       /* gp.hpp:70 */
+double gpmppi_model_log_marginal_likelihood(const gpmppi_model* model, int o); /* gp.hpp:65 */
+/* copies the training inputs (n×4) and outputs (n×m) back to the host */
+int gpmppi_model_training_data(const gpmppi_model* model, double* inputs, double* outputs);
+/* GpModel::predict_batch (gp.cpp:152-207) on the device, FP64: S×4 → mean, var S×m. */
+int gpmppi_model_predict_batch(const gpmppi_model* model, const double* queries, int64_t S,
+                               double* mean, double* var);
+
+/* =============================== planner ===============================
+ * Replaces gpmppi::Planner (mppi.hpp:96-143) and MppiConfig (mppi.hpp:16-26). */
+typedef struct {
+  int samples; /* K (MppiConfig::samples) */
+  int horizon; /* T (MppiConfig::horizon) */
+  double lambda;
+  double sigma_v2, sigma_w2; /* MppiConfig::sigma_sim (variances) */
+  double lo[2], hi[2];       /* ControlBounds (core.hpp:61-74) */
+  uint64_t seed;
+  int threads; /* accepted for API parity; results never depend on it */
+} gpmppi_mppi_config;
+
+typedef struct {
+  double tau_v, tau_omega, dt; /* NominalParams (dynamics.hpp:12-18) */
+} gpmppi_nominal;
+
+typedef struct {
+  double alpha_l, alpha_r, x_icr, y_icr_l, y_icr_r; /* Edd5Params (dynamics.hpp:36-45) */
+} gpmppi_edd5;
+
+enum {
+  GPMPPI_MODEL_GP_ENSEMBLE = 0, /* GpEnsemble (mppi.hpp:30-33) */
+  GPMPPI_MODEL_EDD5 = 1,        /* Edd5Baseline (mppi.hpp:34-37) */
+  GPMPPI_MODEL_UNICYCLE = 2,    /* UnicycleBaseline (mppi.hpp:38) */
+  GPMPPI_MODEL_NOMINAL = 3      /* extension: dynamic unicycle, zero residual (BASELINE config 1) */
+};
+
+typedef struct {
+  int kind;
+  const gpmppi_model* gp; /* non-owning, as GpEnsemble::model (mppi.hpp:31) */
+  int n_terrains;
+  gpmppi_edd5 edd5;
+  double track_width;
+} gpmppi_prediction_model;
+
+typedef struct { /* Track (costs.hpp:13-27) */
+  int is_circle;
+  double cx, cy, radius;
+  int n_waypoints;         /* <= GPMPPI_MAX_WAYPOINTS */
+  const double* waypoints; /* [W][2] */
+  int closed;
+  double half_width;
+} gpmppi_track;
+
+typedef struct {
+  double variance, deviation, slip, safety, speed; /* TrackingWeights (costs.hpp:34-40) */
+} gpmppi_tracking_weights;
+
+typedef struct {
+  double variance, obstacle, stage, terminal; /* AvoidanceWeights (costs.hpp:44-50) */
+} gpmppi_avoidance_weights;
+
+enum {
+  GPMPPI_TASK_TRACKING = 0,  /* TrackingTask  (mppi.hpp:42-46) */
+  GPMPPI_TASK_AVOIDANCE = 1, /* AvoidanceTask (mppi.hpp:47-52) */
+  GPMPPI_TASK_COMBINED = 2   /* tracking_cost + obstacle·Σ collision */
+};
+#define GPMPPI_MAX_WAYPOINTS 64
+#define GPMPPI_MAX_OBSTACLES 64
+
+typedef struct {
+  int kind;
+  const gpmppi_track* track; /* tracking / combined */
+  double v_desired;
+  gpmppi_tracking_weights tracking;
+  const double* obstacles; /* [O][3] (cx, cy, r); avoidance / combined */
+  int n_obstacles;
+  double goal[3]; /* (x, y, capture_radius) GoalSpec (costs.hpp:52-55) */
+  gpmppi_avoidance_weights avoidance;
+  double high_cost; /* AvoidanceTask::high_cost (mppi.hpp:51) */
+} gpmppi_task;
+
+typedef struct { /* StepDiagnostics (mppi.hpp:81-89) */
+  double best_cost, mean_cost, ess, weight_entropy;
+  int nonfinite_samples;
+  int tightening_infeasible;
+  double plan_ms;    /* host wall clock of the whole call (as mppi.cpp:456-458) */
+  double command_ms; /* host wall clock until the command was available */
+} gpmppi_diag;
+
+typedef struct gpmppi_planner gpmppi_planner;
+
+/* Planner(cfg, model, nominal, p_x) (mppi.cpp:187-202) */
+int gpmppi_planner_create(const gpmppi_mppi_config* cfg, const gpmppi_prediction_model* model,
+                          const gpmppi_nominal* nominal, double p_x, int device,
+                          gpmppi_planner** out);
+void gpmppi_planner_free(gpmppi_planner* p);
+/* Planner::plan_step (mppi.cpp:389-475), both overloads + the combined task. Host
+ * buffers in, host command out; the GPU work runs on the planner's stream. */
+int gpmppi_planner_plan_step(gpmppi_planner* p, const double x0[5], const gpmppi_task* task,
+                             double command[2], gpmppi_diag* diag);
+int gpmppi_planner_set_terrain_weights(gpmppi_planner* p, const double* w, int R); /* :208-218 */
+int gpmppi_planner_terrain_weights(const gpmppi_planner* p, double* w);      /* returns R */
+int gpmppi_planner_nominal_sequence(const gpmppi_planner* p, double* seq);   /* T×2 */
+int gpmppi_planner_set_nominal_sequence(gpmppi_planner* p, const double* seq);
+int gpmppi_planner_horizon_covariances(const gpmppi_planner* p, double* cov); /* T×5×5 */
+int gpmppi_planner_lane_radii(const gpmppi_planner* p, double* r);    /* returns T, 0 if unset */
+int gpmppi_planner_obstacle_margins(const gpmppi_planner* p, double* m); /* T×O, returns O */
+int gpmppi_planner_set_thresholds(gpmppi_planner* p, const double* r_bar, const double* margins,
+                                  int n_obstacles);
+uint64_t gpmppi_planner_tick(const gpmppi_planner* p);
+int gpmppi_planner_horizon(const gpmppi_planner* p);
+int gpmppi_planner_samples(const gpmppi_planner* p);
+
+/* ---- noise (north star: Philox production sampler + injection hook) ---- */
+enum { GPMPPI_NOISE_PHILOX = 0, GPMPPI_NOISE_INJECTED = 1 };
+int gpmppi_planner_set_noise_mode(gpmppi_planner* p, int mode);
+/* eps K×T×2 (this rank's samples), used by every following tick until replaced */
+int gpmppi_planner_inject_noise(gpmppi_planner* p, const double* eps);
+/* materialise the Philox noise the planner uses at tick t (K×T×2) */
+int gpmppi_planner_philox_noise(const gpmppi_planner* p, uint64_t tick, double* eps);
+
+/* ---- parity outputs of the last plan_step ---- */
+int gpmppi_planner_sample_costs(const gpmppi_planner* p, double* costs);   /* K */
+int gpmppi_planner_sample_weights(const gpmppi_planner* p, double* w);     /* K */
+/* per-step lane-violation and collision flags, terminal-capture and alive per sample */
+int gpmppi_planner_flags(const gpmppi_planner* p, uint8_t* viol, uint8_t* coll,
+                         uint8_t* terminal, uint8_t* alive);
+
+/* ---- variance path (north star: tensor cores only where tolerance allows) ---- */
+enum { GPMPPI_VAR_FFMA = 0, GPMPPI_VAR_TC_3XTF32 = 1, GPMPPI_VAR_TC_1XTF32 = 2 };
+int gpmppi_planner_set_variance_path(gpmppi_planner* p, int path);
+int gpmppi_planner_variance_path(const gpmppi_planner* p);
+
+/* ---- device-resident timing (bench): run `ticks` plan steps back to back on
+ * device-resident inputs (x0 held fixed). tick_ms[t] = CUDA-event time of tick t
+ * on the planner's stream; with flush_l2 a >L2-sized memset runs between ticks
+ * outside the timed spans. phase_ms[0..3] = summed event time of rollout,
+ * variance, reduce+update, tightening. */
+int gpmppi_planner_bench_device(gpmppi_planner* p, const double x0[5], const gpmppi_task* task,
+                                int ticks, int flush_l2, double* tick_ms, double* phase_ms);
+/* write a buffer twice the L2 size on `device` and synchronise */
+int gpmppi_flush_l2(int device);
+/* bytes one plan_step copies host->device (x0 + task) and device->host (command + diag) */
+int gpmppi_planner_io_bytes(const gpmppi_planner* p, int64_t* h2d, int64_t* d2h);
+
+/* ---- sharded solve (multi-GPU) ----
+ * A planner can own a contiguous global sample range [begin, begin+count) of a
+ * solve with cfg.samples = total; noise is keyed by the GLOBAL sample index.
+ * plan_partial writes this rank's reduction tuple (gpmppi_tuple_doubles(T)
+ * doubles) to a DEVICE buffer; the caller all-gathers the tuples (NCCL) and
+ * plan_finish combines them in rank order, updates/shifts the sequence, runs
+ * the tightening pass and returns the command. */
+int gpmppi_tuple_doubles(int horizon);
+int gpmppi_planner_set_shard(gpmppi_planner* p, int64_t begin, int64_t count);
+int gpmppi_planner_plan_partial(gpmppi_planner* p, const double x0[5], const gpmppi_task* task,
+                                void* device_tuple_out);
+int gpmppi_planner_plan_finish(gpmppi_planner* p, const void* device_tuples, int n_ranks,
+                               double command[2], gpmppi_diag* diag);
+/* Host restatement of the tuple combine the device runs (for CPU multi-rank tests):
+ * tuples n_ranks×gpmppi_tuple_doubles(T) → combined tuple. */
+int gpmppi_combine_tuples_host(const double* tuples, int n_ranks, int horizon, double lambda,
+                               double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

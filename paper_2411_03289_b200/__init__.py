@@ -1,0 +1,12 @@
+"""B200-native GP-MPPI solve path (arXiv 2411.03289), drop-in for the reference
+planner's plan_step. Host API mirrors /root/reference/proj/include/gpmppi/*.hpp;
+compute runs in lib/libgpmppi_b200.so (sm_100a CUDA) through a C ABI."""
+from .gpmppi import (  # noqa: F401
+    AvoidanceTask, AvoidanceWeights, CircleObstacle, CombinedTask, ControlBounds, Edd5Baseline,
+    Edd5Params, GoalSpec, GpEnsemble, GpModel, KernelParams, MppiConfig, NominalDynamic,
+    NominalParams, Planner, StepDiagnostics, Track, TrackingTask, TrackingWeights,
+    UnicycleBaseline, chi2_quantile_2dof, combine_tuples, kernel_launches, tuple_doubles)
+from ._capi import (  # noqa: F401
+    NOISE_INJECTED, NOISE_PHILOX, VAR_FFMA, VAR_TC_1XTF32, VAR_TC_3XTF32, CudaError)
+
+__version__ = "0.1.0"

@@ -1,0 +1,1171 @@
+// capi.cpp — C++ host layer behind include/gpmppi_b200.h.
+//
+// Owns the GP model (host FP64 factorisation restating gp.cpp:61-150, device
+// upload) and the planner (device buffers, stream, per-tick orchestration of
+// the kernels in kernels.cu, restating Planner::plan_step_impl, mppi.cpp:389-462).
+#include "gpmppi_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <limits>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "internal.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+struct CudaError {
+  cudaError_t e;
+  const char* where;
+};
+
+#define CK(call)                                                          \
+  do {                                                                    \
+    cudaError_t e__ = (call);                                             \
+    if (e__ != cudaSuccess) throw CudaError{e__, #call};                  \
+  } while (0)
+
+struct ArgError {
+  int code;
+  std::string msg;
+};
+[[noreturn]] void invalid(const std::string& m) { throw ArgError{GPMPPI_INVALID_ARGUMENT, m}; }
+[[noreturn]] void runtime(const std::string& m) { throw ArgError{GPMPPI_RUNTIME_ERROR, m}; }
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return GPMPPI_OK;
+  } catch (const ArgError& e) {
+    return fail(e.code, e.msg);
+  } catch (const CudaError& e) {
+    return fail(GPMPPI_CUDA_ERROR, std::string("CUDA error in ") + e.where + ": " +
+                                       cudaGetErrorString(e.e));
+  } catch (const std::bad_alloc&) {
+    return fail(GPMPPI_RUNTIME_ERROR, "host allocation failed");
+  }
+}
+
+void require_device(int device) {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    throw CudaError{e == cudaSuccess ? cudaErrorNoDevice : e, "cudaGetDeviceCount (no CUDA device)"};
+  if (device < 0 || device >= count) invalid("device index out of range");
+  CK(cudaSetDevice(device));
+}
+
+// ---------------------------------------------------------------------------
+// Host FP64 GP factorisation (gp.cpp:61-150).
+struct HostGroup {
+  double kernel[6];
+  std::vector<int> outputs;
+  double jitter = 0.0;
+  std::vector<double> aug;    // n×6 [x/l | 1 | -1/2|x/l|^2 + ln sv]  (gp.cpp:103-110)
+  std::vector<double> chol;   // n×n lower
+  std::vector<double> ilt;    // n×n upper = L^{-T}
+  std::vector<double> alphas; // n×n_out
+};
+
+bool cholesky_lower(std::vector<double>& A, int n) {  // Eigen LLT: fail iff a pivot <= 0
+  for (int j = 0; j < n; ++j) {
+    double* rj = &A[(size_t)j * n];
+    double x = rj[j];
+    for (int k = 0; k < j; ++k) x -= rj[k] * rj[k];
+    if (!(x > 0.0)) return false;
+    const double d = std::sqrt(x);
+    rj[j] = d;
+    for (int i = j + 1; i < n; ++i) {
+      double* ri = &A[(size_t)i * n];
+      double v = ri[j];
+      for (int k = 0; k < j; ++k) v -= ri[k] * rj[k];
+      ri[j] = v / d;
+    }
+  }
+  for (int i = 0; i < n; ++i)
+    for (int j = i + 1; j < n; ++j) A[(size_t)i * n + j] = 0.0;
+  return true;
+}
+
+void factor_group(HostGroup& G, const double* X, const double* Y, int n, int m,
+                  std::vector<double>& lml) {
+  const double sv = G.kernel[0], nv = G.kernel[5];
+  G.aug.assign((size_t)n * 6, 0.0);
+  std::vector<double> norms(n);
+  for (int i = 0; i < n; ++i) {
+    double sq = 0.0;
+    for (int d = 0; d < 4; ++d) {
+      const double v = X[(size_t)i * 4 + d] / G.kernel[1 + d];
+      G.aug[(size_t)i * 6 + d] = v;
+      sq += v * v;
+    }
+    norms[i] = -0.5 * sq;
+    G.aug[(size_t)i * 6 + 4] = 1.0;
+    G.aug[(size_t)i * 6 + 5] = norms[i] + std::log(sv);
+  }
+  std::vector<double> K((size_t)n * n);  // gp.cpp:112-114
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      const double* a = &G.aug[(size_t)i * 6];
+      const double* b = &G.aug[(size_t)j * 6];
+      K[(size_t)i * n + j] = std::exp(a[0] * b[0] + a[1] * b[1] + a[2] * b[2] + a[3] * b[3] +
+                                      norms[i] + b[5]);
+    }
+  for (int i = 0; i < n; ++i)
+    for (int j = i + 1; j < n; ++j) {
+      const double s = 0.5 * (K[(size_t)i * n + j] + K[(size_t)j * n + i]);
+      K[(size_t)i * n + j] = K[(size_t)j * n + i] = s;
+    }
+  bool ok = false;  // gp.cpp:116-133 jitter ladder
+  double jitter = 0.0;
+  for (int attempt = 0; attempt <= 5 && !ok; ++attempt) {
+    jitter = attempt == 0 ? 0.0 : std::pow(10.0, -11 + attempt);
+    G.chol = K;
+    for (int i = 0; i < n; ++i) G.chol[(size_t)i * n + i] += nv + jitter;
+    ok = cholesky_lower(G.chol, n);
+  }
+  if (!ok) {
+    std::ostringstream msg;
+    msg << "GpModel::fit: Cholesky failed for kernel group after jitter up to 1e-6"
+        << " (signal_var=" << sv << ", noise_var=" << nv << ")";
+    runtime(msg.str());
+  }
+  G.jitter = jitter;
+  const std::vector<double>& L = G.chol;
+  // L^{-1} row by row (axpy form), then transpose (gp.cpp:135-138)
+  std::vector<double> Xi((size_t)n * n, 0.0);
+  for (int i = 0; i < n; ++i) {
+    double* xi = &Xi[(size_t)i * n];
+    xi[i] = 1.0;
+    for (int k = 0; k < i; ++k) {
+      const double l = L[(size_t)i * n + k];
+      const double* xk = &Xi[(size_t)k * n];
+      for (int c = 0; c <= k; ++c) xi[c] -= l * xk[c];
+    }
+    const double d = L[(size_t)i * n + i];
+    for (int c = 0; c <= i; ++c) xi[c] /= d;
+  }
+  G.ilt.assign((size_t)n * n, 0.0);
+  for (int i = 0; i < n; ++i)
+    for (int j = i; j < n; ++j) G.ilt[(size_t)i * n + j] = Xi[(size_t)j * n + i];
+  // alphas + LML (gp.cpp:140-147)
+  const int no = (int)G.outputs.size();
+  G.alphas.assign((size_t)n * no, 0.0);
+  double logdet = 0.0;
+  for (int i = 0; i < n; ++i) logdet += std::log(L[(size_t)i * n + i]);
+  std::vector<double> z(n);
+  const double log2pi = std::log(2.0 * gpm::kPi);
+  for (int c = 0; c < no; ++c) {
+    const int j = G.outputs[c];
+    for (int i = 0; i < n; ++i) {
+      double v = Y[(size_t)i * m + j];
+      const double* li = &L[(size_t)i * n];
+      for (int k = 0; k < i; ++k) v -= li[k] * z[k];
+      z[i] = v / li[i];
+    }
+    for (int i = n - 1; i >= 0; --i) {
+      double v = z[i];
+      for (int k = i + 1; k < n; ++k) v -= L[(size_t)k * n + i] * G.alphas[(size_t)k * no + c];
+      G.alphas[(size_t)i * no + c] = v / L[(size_t)i * n + i];
+    }
+    double dot = 0.0;
+    for (int i = 0; i < n; ++i) dot += Y[(size_t)i * m + j] * G.alphas[(size_t)i * no + c];
+    lml[j] = -0.5 * dot - logdet - 0.5 * (double)n * log2pi;
+  }
+}
+
+}  // namespace
+
+// ===========================================================================
+struct gpmppi_model {
+  int device = 0;
+  int n = 0, m = 0;
+  std::vector<double> inputs, outputs, kernels, lml;
+  std::vector<HostGroup> groups;
+  std::vector<void*> dev_allocs;
+  gpm::ModelDev dev{};
+  ~gpmppi_model() {
+    cudaSetDevice(device);
+    for (void* p : dev_allocs) cudaFree(p);
+  }
+  template <class T>
+  T* upload(const std::vector<T>& v) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, sizeof(T) * std::max<size_t>(v.size(), 1)));
+    dev_allocs.push_back(p);
+    if (!v.empty()) CK(cudaMemcpy(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+    return static_cast<T*>(p);
+  }
+};
+
+namespace {
+
+gpmppi_model* build_model(const double* X, const double* Y, int64_t n64, int64_t m64,
+                          const double* kernels, int device) {
+  if (n64 < 1) invalid("GpModel::fit: inputs must be n x 4 with n >= 1");
+  if (m64 < 1) invalid("GpModel::fit: outputs must be n x m with m >= 1");
+  if (n64 > (1 << 16)) invalid("GpModel::fit: n too large for the device model");
+  const int n = (int)n64, m = (int)m64;
+  for (size_t i = 0; i < (size_t)n * 4; ++i)
+    if (!std::isfinite(X[i])) invalid("GpModel::fit: non-finite training data");
+  for (size_t i = 0; i < (size_t)n * m; ++i)
+    if (!std::isfinite(Y[i])) invalid("GpModel::fit: non-finite training data");
+  std::vector<HostGroup> groups;
+  for (int j = 0; j < m; ++j) {  // gp.cpp:85-100
+    const double* kp = kernels + 6 * j;
+    bool ok = kp[0] > 0.0 && kp[5] > 0.0;
+    for (int d = 0; d < 4; ++d) ok = ok && kp[1 + d] > 0.0;
+    if (!ok) invalid("KernelParams: all parameters must be strictly positive");
+    int g = -1;
+    for (size_t k = 0; k < groups.size(); ++k)
+      if (std::memcmp(groups[k].kernel, kp, sizeof(double) * 6) == 0) g = (int)k;
+    if (g < 0) {
+      groups.emplace_back();
+      std::memcpy(groups.back().kernel, kp, sizeof(double) * 6);
+      g = (int)groups.size() - 1;
+    }
+    groups[g].outputs.push_back(j);
+  }
+  if ((int)groups.size() > gpm::kMaxGroups)
+    invalid("GpModel::fit: at most " + std::to_string(gpm::kMaxGroups) + " distinct kernels supported on device");
+  for (auto& g : groups)
+    if ((int)g.outputs.size() > gpm::kMaxOutPerGroup)
+      invalid("GpModel::fit: at most " + std::to_string(gpm::kMaxOutPerGroup) + " outputs per kernel supported on device");
+  require_device(device);
+  auto* M = new gpmppi_model();
+  try {
+    M->device = device;
+    M->n = n;
+    M->m = m;
+    M->inputs.assign(X, X + (size_t)n * 4);
+    M->outputs.assign(Y, Y + (size_t)n * m);
+    M->kernels.assign(kernels, kernels + (size_t)m * 6);
+    M->lml.assign(m, 0.0);
+    M->groups = std::move(groups);
+    for (auto& G : M->groups) factor_group(G, X, Y, n, m, M->lml);
+    // device upload
+    M->dev.n = n;
+    M->dev.m = m;
+    M->dev.G = (int)M->groups.size();
+    for (int gi = 0; gi < M->dev.G; ++gi) {
+      const HostGroup& G = M->groups[gi];
+      gpm::GroupDev& D = M->dev.g[gi];
+      const int no = (int)G.outputs.size();
+      std::vector<double> pts((size_t)(5 + no) * n);
+      for (int j = 0; j < n; ++j) {
+        for (int d = 0; d < 4; ++d) pts[(size_t)d * n + j] = G.aug[(size_t)j * 6 + d];
+        pts[(size_t)4 * n + j] = G.aug[(size_t)j * 6 + 5];
+        for (int c = 0; c < no; ++c) pts[(size_t)(5 + c) * n + j] = G.alphas[(size_t)j * no + c];
+      }
+      std::vector<float> ilt32(G.ilt.size()), zs32((size_t)4 * n);
+      for (size_t i = 0; i < G.ilt.size(); ++i) ilt32[i] = (float)G.ilt[i];
+      for (int j = 0; j < n; ++j)
+        for (int d = 0; d < 4; ++d) zs32[(size_t)d * n + j] = (float)G.aug[(size_t)j * 6 + d];
+      D.pts = M->upload(pts);
+      D.ilt64 = M->upload(G.ilt);
+      D.ilt32 = M->upload(ilt32);
+      D.zs32 = M->upload(zs32);
+      D.tc_b = nullptr;
+      for (int d = 0; d < 4; ++d) D.ls[d] = G.kernel[1 + d];
+      D.sv = G.kernel[0];
+      D.log_sv = std::log(G.kernel[0]);
+      D.n_out = no;
+      for (int c = 0; c < gpm::kMaxOutPerGroup; ++c) D.out_idx[c] = c < no ? G.outputs[c] : 0;
+    }
+  } catch (...) {
+    delete M;
+    throw;
+  }
+  return M;
+}
+
+const char kGpMagic[8] = {'G', 'P', 'M', 'P', 'P', 'I', 'G', '1'};  // gp.cpp:19
+
+}  // namespace
+
+extern "C" {
+
+const char* gpmppi_last_error(void) { return g_err.c_str(); }
+int gpmppi_abi_version(void) { return GPMPPI_ABI_VERSION; }
+uint64_t gpmppi_kernel_launches(void) { return gpm::launches_total(); }
+
+int gpmppi_model_fit(const double* inputs, const double* outputs, int64_t n, int64_t m,
+                     const double* kernels, int device, gpmppi_model** out) {
+  if (!out) return fail(GPMPPI_INVALID_ARGUMENT, "null output handle");
+  *out = nullptr;
+  return guarded([&] { *out = build_model(inputs, outputs, n, m, kernels, device); });
+}
+
+int gpmppi_model_load(const char* path, int device, gpmppi_model** out) {  // gp.cpp:244-272
+  if (!out) return fail(GPMPPI_INVALID_ARGUMENT, "null output handle");
+  *out = nullptr;
+  return guarded([&] {
+    std::ifstream is(path ? path : "", std::ios::binary);
+    if (!is) runtime(std::string("GpModel::load: cannot open ") + (path ? path : ""));
+    auto read_raw = [&](void* p, size_t bytes) {
+      is.read(static_cast<char*>(p), (std::streamsize)bytes);
+      if (!is) runtime("GpModel::load: truncated record");
+    };
+    char magic[8];
+    read_raw(magic, 8);
+    if (std::memcmp(magic, kGpMagic, 8) != 0) runtime("GpModel::load: bad magic");
+    int64_t n = 0, m = 0;
+    read_raw(&n, 8);
+    read_raw(&m, 8);
+    if (n < 1 || m < 1 || n > (1 << 24) || m > (1 << 16)) runtime("GpModel::load: implausible dimensions");
+    std::vector<double> cin((size_t)n * 4), cout((size_t)n * m), kern((size_t)m * 6);
+    read_raw(cin.data(), sizeof(double) * cin.size());
+    read_raw(cout.data(), sizeof(double) * cout.size());
+    read_raw(kern.data(), sizeof(double) * kern.size());  // per output: sv, l0..l3, nv
+    std::vector<double> X((size_t)n * 4), Y((size_t)n * m);  // column-major → row-major
+    for (int64_t i = 0; i < n; ++i) {
+      for (int d = 0; d < 4; ++d) X[(size_t)i * 4 + d] = cin[(size_t)d * n + i];
+      for (int64_t j = 0; j < m; ++j) Y[(size_t)i * m + j] = cout[(size_t)j * n + i];
+    }
+    *out = build_model(X.data(), Y.data(), n, m, kern.data(), device);
+  });
+}
+
+int gpmppi_model_save(const gpmppi_model* M, const char* path) {  // gp.cpp:223-242
+  if (!M) return fail(GPMPPI_INVALID_ARGUMENT, "null model");
+  return guarded([&] {
+    std::ofstream os(path ? path : "", std::ios::binary);
+    if (!os) runtime(std::string("GpModel::save: cannot open ") + (path ? path : ""));
+    const int64_t n = M->n, m = M->m;
+    os.write(kGpMagic, 8);
+    os.write(reinterpret_cast<const char*>(&n), 8);
+    os.write(reinterpret_cast<const char*>(&m), 8);
+    std::vector<double> cin((size_t)n * 4), cout((size_t)n * m);
+    for (int64_t i = 0; i < n; ++i) {
+      for (int d = 0; d < 4; ++d) cin[(size_t)d * n + i] = M->inputs[(size_t)i * 4 + d];
+      for (int64_t j = 0; j < m; ++j) cout[(size_t)j * n + i] = M->outputs[(size_t)i * m + j];
+    }
+    os.write(reinterpret_cast<const char*>(cin.data()), sizeof(double) * cin.size());
+    os.write(reinterpret_cast<const char*>(cout.data()), sizeof(double) * cout.size());
+    os.write(reinterpret_cast<const char*>(M->kernels.data()), sizeof(double) * M->kernels.size());
+    if (!os) runtime(std::string("GpModel::save: write failed for ") + path);
+  });
+}
+
+void gpmppi_model_free(gpmppi_model* M) { delete M; }
+int gpmppi_model_n_points(const gpmppi_model* M) { return M ? M->n : 0; }
+int gpmppi_model_n_outputs(const gpmppi_model* M) { return M ? M->m : 0; }
+int gpmppi_model_n_groups(const gpmppi_model* M) { return M ? (int)M->groups.size() : 0; }
+double gpmppi_model_group_jitter(const gpmppi_model* M, int g) {
+  return (M && g >= 0 && g < (int)M->groups.size()) ? M->groups[g].jitter : NAN;
+}
+double gpmppi_model_log_marginal_likelihood(const gpmppi_model* M, int o) {
+  return (M && o >= 0 && o < M->m) ? M->lml[o] : NAN;
+}
+int gpmppi_model_training_data(const gpmppi_model* M, double* inputs, double* outputs) {
+  if (!M) return fail(GPMPPI_INVALID_ARGUMENT, "null model");
+  if (inputs) std::memcpy(inputs, M->inputs.data(), sizeof(double) * M->inputs.size());
+  if (outputs) std::memcpy(outputs, M->outputs.data(), sizeof(double) * M->outputs.size());
+  return GPMPPI_OK;
+}
+
+int gpmppi_model_predict_batch(const gpmppi_model* M, const double* q, int64_t S, double* mean,
+                               double* var) {  // gp.cpp:152-207
+  if (!M) return fail(GPMPPI_LOGIC_ERROR, "GpModel::predict_batch: model not fitted");
+  if (S < 0) return fail(GPMPPI_INVALID_ARGUMENT, "GpModel::predict_batch: queries must be S x 4");
+  if (S == 0) return GPMPPI_OK;
+  for (int64_t i = 0; i < S * 4; ++i)
+    if (!std::isfinite(q[i])) return fail(GPMPPI_INVALID_ARGUMENT, "GpModel::predict: non-finite query");
+  return guarded([&] {
+    CK(cudaSetDevice(M->device));
+    double *dq = nullptr, *dm = nullptr, *dv = nullptr;
+    CK(cudaMalloc(&dq, sizeof(double) * S * 4));
+    CK(cudaMalloc(&dm, sizeof(double) * S * M->m));
+    CK(cudaMalloc(&dv, sizeof(double) * S * M->m));
+    CK(cudaMemcpy(dq, q, sizeof(double) * S * 4, cudaMemcpyHostToDevice));
+    cudaError_t e = gpm::launch_predict(M->dev, dq, S, dm, dv, 0);
+    if (e == cudaSuccess) e = cudaMemcpy(mean, dm, sizeof(double) * S * M->m, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(var, dv, sizeof(double) * S * M->m, cudaMemcpyDeviceToHost);
+    cudaFree(dq);
+    cudaFree(dm);
+    cudaFree(dv);
+    if (e != cudaSuccess) throw CudaError{e, "predict_kernel"};
+  });
+}
+
+}  // extern "C"
+
+// ===========================================================================
+struct gpmppi_planner {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  gpmppi_mppi_config cfg{};
+  int model_kind = 0;
+  const gpmppi_model* model = nullptr;
+  int R = 1;
+  gpm::Edd5Dev edd5{};
+  gpm::NominalDev nom{};
+  double p_x = 0.95, chi2 = 0.0, z = 0.0;
+  std::vector<double> tw;
+  uint64_t tick = 0;
+  int noise_mode = gpm::NOISE_PHILOX;
+  bool injected_set = false;
+  int var_path = GPMPPI_VAR_FFMA;
+  long long s_begin = 0, K_local = 0, K_total = 0;
+  bool rbar_init = false;
+  int margins_O = -1;
+  int reduce_blocks = 1;
+  int last_task_kind = -1;
+  int T = 0, words = 1;
+  // device buffers
+  std::vector<void*> allocs;
+  double *d_nom = nullptr, *d_tw = nullptr, *d_x0 = nullptr, *d_rbar = nullptr, *d_margins = nullptr;
+  double* d_eps = nullptr;
+  gpm::TaskDev* d_task = nullptr;
+  double *d_cost_mean = nullptr, *d_trace = nullptr, *d_costs = nullptr, *d_e = nullptr;
+  float4* d_queries = nullptr;
+  uint32_t *d_viol = nullptr, *d_coll = nullptr;
+  uint8_t *d_term = nullptr, *d_alive = nullptr;
+  double *d_partials = nullptr, *d_rank_tuple = nullptr, *d_out = nullptr, *d_hcov = nullptr,
+         *d_combined = nullptr;
+  unsigned int* d_ticket = nullptr;
+  int* d_infeasible = nullptr;
+  // pinned staging
+  gpm::TaskDev* h_task = nullptr;
+  double* h_x0 = nullptr;
+  double* h_out = nullptr;
+  int* h_infeasible = nullptr;
+  cudaEvent_t ev[8] = {};
+
+  template <class T>
+  T* dalloc(size_t count) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, sizeof(T) * std::max<size_t>(count, 1)));
+    allocs.push_back(p);
+    CK(cudaMemsetAsync(p, 0, sizeof(T) * std::max<size_t>(count, 1), stream));
+    return static_cast<T*>(p);
+  }
+  ~gpmppi_planner() {
+    cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    for (void* p : allocs) cudaFree(p);
+    if (h_task) cudaFreeHost(h_task);
+    if (h_x0) cudaFreeHost(h_x0);
+    if (h_out) cudaFreeHost(h_out);
+    if (h_infeasible) cudaFreeHost(h_infeasible);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+  }
+  void alloc_sample_buffers() {
+    const long long K = K_local;
+    d_cost_mean = dalloc<double>(K);
+    d_costs = dalloc<double>(K);
+    d_e = dalloc<double>(K);
+    d_viol = dalloc<uint32_t>((size_t)K * words);
+    d_coll = dalloc<uint32_t>((size_t)K * words);
+    d_term = dalloc<uint8_t>(K);
+    d_alive = dalloc<uint8_t>(K);
+    if (model_kind == GPMPPI_MODEL_GP_ENSEMBLE) {
+      d_queries = dalloc<float4>((size_t)K * T);
+      d_trace = dalloc<double>((size_t)K * T);
+    }
+    reduce_blocks = gpm::reduce_blocks_for((int)K, num_sms);
+    d_partials = dalloc<double>((size_t)reduce_blocks * gpm::tuple_doubles(T));
+  }
+};
+
+namespace {
+
+double normal_quantile(double p) {  // uncertainty.cpp:19-60 (Acklam + one Newton step)
+  static const double a[] = {-3.969683028665376e+01, 2.209460984245205e+02, -2.759285104469687e+02,
+                             1.383577518672690e+02,  -3.066479806614716e+01, 2.506628277459239e+00};
+  static const double b[] = {-5.447609879822406e+01, 1.615858368580409e+02, -1.556989798598866e+02,
+                             6.680131188771972e+01,  -1.328068155288572e+01};
+  static const double c[] = {-7.784894002430293e-03, -3.223964580411365e-01, -2.400758277161838e+00,
+                             -2.549732539343734e+00, 4.374664141464968e+00,  2.938163982698783e+00};
+  static const double d[] = {7.784695709041462e-03, 3.224671290700398e-01, 2.445134137142996e+00,
+                             3.754408661907416e+00};
+  const double plow = 0.02425;
+  double x;
+  if (p < plow) {
+    const double q = std::sqrt(-2.0 * std::log(p));
+    x = (((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) /
+        ((((d[0] * q + d[1]) * q + d[2]) * q + d[3]) * q + 1.0);
+  } else if (p > 1.0 - plow) {
+    const double q = std::sqrt(-2.0 * std::log(1.0 - p));
+    x = -(((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) /
+        ((((d[0] * q + d[1]) * q + d[2]) * q + d[3]) * q + 1.0);
+  } else {
+    const double q = p - 0.5, r = q * q;
+    x = (((((a[0] * r + a[1]) * r + a[2]) * r + a[3]) * r + a[4]) * r + a[5]) * q /
+        (((((b[0] * r + b[1]) * r + b[2]) * r + b[3]) * r + b[4]) * r + 1.0);
+  }
+  const double pdf = std::exp(-0.5 * x * x) / std::sqrt(2.0 * gpm::kPi);
+  if (pdf > 1e-300) x -= (0.5 * std::erfc(-x * 0.70710678118654752440) - p) / pdf;
+  return x;
+}
+
+bool on_simplex(const double* w, int R, double tol) {  // core.hpp:107-111
+  if (R <= 0) return false;
+  double s = 0.0;
+  for (int i = 0; i < R; ++i) s += w[i];
+  if (std::fabs(s - 1.0) > tol) return false;
+  for (int i = 0; i < R; ++i)
+    if (!(w[i] >= -tol) || !(w[i] <= 1.0 + tol)) return false;
+  return true;
+}
+
+void validate_task(const gpmppi_task* t) {
+  if (!t) invalid("plan_step: null task");
+  if (t->kind < 0 || t->kind > 2) invalid("plan_step: unknown task kind");
+  if (t->kind != GPMPPI_TASK_AVOIDANCE) {
+    if (!t->track) invalid("plan_step: tracking task needs a track");
+    const gpmppi_track& k = *t->track;  // costs.cpp:44-60
+    if (!(k.half_width > 0.0)) invalid("Track: half_width must be positive");
+    if (k.is_circle) {
+      if (!(k.radius > 0.0)) invalid("Track: circle radius must be positive");
+    } else {
+      if (k.n_waypoints < 2) invalid("Track: polyline needs at least 2 waypoints");
+      if (k.n_waypoints > GPMPPI_MAX_WAYPOINTS) invalid("Track: too many waypoints for the device task");
+      for (int i = 1; i < k.n_waypoints; ++i) {
+        const double dx = k.waypoints[2 * i] - k.waypoints[2 * i - 2];
+        const double dy = k.waypoints[2 * i + 1] - k.waypoints[2 * i - 1];
+        if (std::sqrt(dx * dx + dy * dy) < 1e-12) invalid("Track: consecutive waypoints must be distinct");
+      }
+    }
+  }
+  if (t->kind != GPMPPI_TASK_TRACKING) {
+    if (t->n_obstacles < 0) invalid("plan_step: avoidance task needs an obstacle list");
+    if (t->n_obstacles > 0 && !t->obstacles) invalid("plan_step: avoidance task needs an obstacle list");
+    if (t->n_obstacles > GPMPPI_MAX_OBSTACLES) invalid("plan_step: too many obstacles for the device task");
+  }
+  if (t->kind == GPMPPI_TASK_AVOIDANCE && !(t->high_cost > 0.0))
+    invalid("terminal_cost: high_cost must be positive");
+}
+
+void fill_task(gpm::TaskDev& d, const gpmppi_task* t) {
+  std::memset(&d, 0, sizeof d);
+  d.kind = t->kind;
+  if (t->kind != GPMPPI_TASK_AVOIDANCE) {
+    const gpmppi_track& k = *t->track;
+    d.is_circle = k.is_circle;
+    d.cx = k.cx;
+    d.cy = k.cy;
+    d.radius = k.radius;
+    d.half_width = k.half_width;
+    d.closed = k.closed;
+    d.n_wp = k.is_circle ? 0 : k.n_waypoints;
+    for (int i = 0; i < d.n_wp; ++i) {
+      d.wp[i][0] = k.waypoints[2 * i];
+      d.wp[i][1] = k.waypoints[2 * i + 1];
+    }
+  }
+  d.v_desired = t->v_desired;
+  d.tw[0] = t->tracking.variance;
+  d.tw[1] = t->tracking.deviation;
+  d.tw[2] = t->tracking.slip;
+  d.tw[3] = t->tracking.safety;
+  d.tw[4] = t->tracking.speed;
+  d.aw[0] = t->avoidance.variance;
+  d.aw[1] = t->avoidance.obstacle;
+  d.aw[2] = t->avoidance.stage;
+  d.aw[3] = t->avoidance.terminal;
+  d.goal[0] = t->goal[0];
+  d.goal[1] = t->goal[1];
+  d.goal[2] = t->goal[2];
+  d.high_cost = t->high_cost;
+  d.n_obs = t->kind == GPMPPI_TASK_TRACKING ? 0 : t->n_obstacles;
+  for (int i = 0; i < d.n_obs; ++i)
+    for (int c = 0; c < 3; ++c) d.obs[i][c] = t->obstacles[3 * i + c];
+}
+
+void check(cudaError_t e, const char* where) {
+  if (e != cudaSuccess) throw CudaError{e, where};
+}
+
+// mppi.cpp:235-248 ensure_thresholds + per-tick upload of x0 and the task.
+void stage_tick(gpmppi_planner* p, const double x0[5], const gpmppi_task* task) {
+  for (int i = 0; i < 5; ++i)
+    if (!std::isfinite(x0[i])) invalid("plan_step: non-finite state estimate");
+  validate_task(task);
+  const int T = p->T;
+  if (task->kind != GPMPPI_TASK_AVOIDANCE && !p->rbar_init) {
+    std::vector<double> r(T, task->track->half_width);
+    CK(cudaMemcpyAsync(p->d_rbar, r.data(), sizeof(double) * T, cudaMemcpyHostToDevice, p->stream));
+    CK(cudaStreamSynchronize(p->stream));
+    p->rbar_init = true;
+  }
+  if (task->kind != GPMPPI_TASK_TRACKING && p->margins_O != task->n_obstacles) {
+    CK(cudaMemsetAsync(p->d_margins, 0, sizeof(double) * T * gpm::kMaxObstacles, p->stream));
+    p->margins_O = task->n_obstacles;
+  }
+  fill_task(*p->h_task, task);
+  std::memcpy(p->h_x0, x0, sizeof(double) * 5);
+  CK(cudaMemcpyAsync(p->d_task, p->h_task, sizeof(gpm::TaskDev), cudaMemcpyHostToDevice, p->stream));
+  CK(cudaMemcpyAsync(p->d_x0, p->h_x0, sizeof(double) * 5, cudaMemcpyHostToDevice, p->stream));
+  p->last_task_kind = task->kind;
+}
+
+double trace_coef(const gpmppi_planner* p, const gpm::GroupDev& g) {
+  double c = 0.0;
+  for (int o = 0; o < g.n_out; ++o) {
+    const double w = p->tw[g.out_idx[o] >> 1];
+    c += w * w;
+  }
+  return c;
+}
+
+// Rollout + variance + reduce for this planner's sample range. finish=1 also
+// applies the update (single-rank solve).
+void enqueue_samples(gpmppi_planner* p, int n_obs, double var_w, int finish, cudaEvent_t* evs) {
+  const int T = p->T;
+  const uint64_t key = gpm::philox_key(p->cfg.seed, p->tick);
+  gpm::RolloutArgs a{};
+  if (p->model) a.model = p->model->dev;
+  a.model_kind = p->model_kind;
+  a.nom = p->nom;
+  a.edd5 = p->edd5;
+  a.K_local = (int)p->K_local;
+  a.s_begin = p->s_begin;
+  a.T = T;
+  a.n_obs = n_obs;
+  a.lo[0] = p->cfg.lo[0];
+  a.lo[1] = p->cfg.lo[1];
+  a.hi[0] = p->cfg.hi[0];
+  a.hi[1] = p->cfg.hi[1];
+  a.sv = std::sqrt(p->cfg.sigma_v2);
+  a.sw = std::sqrt(p->cfg.sigma_w2);
+  a.noise_mode = p->noise_mode;
+  a.eps = p->d_eps;
+  a.key = key;
+  a.nominal_seq = p->d_nom;
+  a.tw = p->d_tw;
+  a.R = p->R;
+  a.task = p->d_task;
+  a.r_bar = p->d_rbar;
+  a.margins = p->d_margins;
+  a.x0 = p->d_x0;
+  a.cost_mean = p->d_cost_mean;
+  a.queries = p->d_queries;
+  a.viol_bits = p->d_viol;
+  a.coll_bits = p->d_coll;
+  a.term = p->d_term;
+  a.alive = p->d_alive;
+  a.words = p->words;
+  if (evs) CK(cudaEventRecord(evs[0], p->stream));
+  check(gpm::launch_rollout(a, p->num_sms, p->stream), "rollout kernel");
+  if (evs) CK(cudaEventRecord(evs[1], p->stream));
+  const bool gp = p->model_kind == GPMPPI_MODEL_GP_ENSEMBLE;
+  if (gp) {
+    for (int g = 0; g < p->model->dev.G; ++g) {
+      gpm::VarianceArgs v{};
+      v.queries = p->d_queries;
+      v.KT = (long long)p->K_local * T;
+      v.n = p->model->n;
+      v.g = p->model->dev.g[g];
+      v.coef = trace_coef(p, v.g);
+      v.accumulate = g > 0;
+      v.trace = p->d_trace;
+      check(gpm::launch_variance(v, p->var_path, p->stream), "variance kernel");
+    }
+  }
+  if (evs) CK(cudaEventRecord(evs[2], p->stream));
+  gpm::ReduceArgs r{};
+  r.K_local = (int)p->K_local;
+  r.s_begin = p->s_begin;
+  r.T = T;
+  r.lambda = p->cfg.lambda;
+  r.cost_mean = p->d_cost_mean;
+  r.trace = gp ? p->d_trace : nullptr;
+  r.var_w = var_w;
+  r.noise_mode = p->noise_mode;
+  r.eps = p->d_eps;
+  r.key = key;
+  r.sv = a.sv;
+  r.sw = a.sw;
+  r.costs_out = p->d_costs;
+  r.e_out = p->d_e;
+  r.partials = p->d_partials;
+  r.ticket = p->d_ticket;
+  r.rank_tuple = p->d_rank_tuple;
+  r.finish = finish;
+  r.nominal_seq = p->d_nom;
+  r.lo[0] = p->cfg.lo[0];
+  r.lo[1] = p->cfg.lo[1];
+  r.hi[0] = p->cfg.hi[0];
+  r.hi[1] = p->cfg.hi[1];
+  r.out = p->d_out;
+  r.K_total = p->K_total;
+  check(gpm::launch_reduce(r, p->reduce_blocks, p->stream), "reduce kernel");
+  if (evs) CK(cudaEventRecord(evs[3], p->stream));
+}
+
+void enqueue_tighten(gpmppi_planner* p) {
+  gpm::TightenArgs t{};
+  if (p->model) t.model = p->model->dev;
+  t.model_kind = p->model_kind;
+  t.nom = p->nom;
+  t.T = p->T;
+  t.tw = p->d_tw;
+  t.R = p->R;
+  t.x0 = p->d_x0;
+  t.nominal_seq = p->d_nom;
+  t.task = p->d_task;
+  t.chi2 = p->chi2;
+  t.z = p->z;
+  t.horizon_cov = p->d_hcov;
+  t.r_bar = p->d_rbar;
+  t.margins = p->d_margins;
+  t.infeasible = p->d_infeasible;
+  check(gpm::launch_tighten(t, p->stream), "tighten kernel");
+}
+
+double task_var_weight(const gpmppi_task* t) {
+  return t->kind == GPMPPI_TASK_AVOIDANCE ? t->avoidance.variance : t->tracking.variance;
+}
+
+void fill_diag(gpmppi_planner* p, double command[2], gpmppi_diag* diag, double t_cmd, double t_all) {
+  command[0] = p->h_out[0];
+  command[1] = p->h_out[1];
+  if (diag) {
+    diag->best_cost = p->h_out[2];
+    diag->mean_cost = p->h_out[3];
+    diag->ess = p->h_out[4];
+    diag->weight_entropy = p->h_out[5];
+    diag->nonfinite_samples = (int)p->h_out[6];
+    diag->tightening_infeasible = *p->h_infeasible;
+    diag->plan_ms = t_all;
+    diag->command_ms = t_cmd;
+  }
+}
+
+using Clock = std::chrono::steady_clock;
+double ms_since(Clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+}
+
+}  // namespace
+
+extern "C" {
+
+int gpmppi_planner_create(const gpmppi_mppi_config* cfg, const gpmppi_prediction_model* pm,
+                          const gpmppi_nominal* nominal, double p_x, int device,
+                          gpmppi_planner** out) {
+  if (!out) return fail(GPMPPI_INVALID_ARGUMENT, "null output handle");
+  *out = nullptr;
+  return guarded([&] {
+    if (!cfg || !pm || !nominal) invalid("Planner: null argument");
+    if (!(p_x > 0.5) || !(p_x < 1.0)) invalid("QuantileTables: p_x must lie in (0.5, 1)");
+    if (cfg->samples < 1 || cfg->horizon < 1) invalid("MppiConfig: samples and horizon must be >= 1");
+    if (!(cfg->lambda > 0.0)) invalid("MppiConfig: lambda must be positive");
+    if (!(cfg->sigma_v2 > 0.0) || !(cfg->sigma_w2 > 0.0))
+      invalid("MppiConfig: sampling variances must be positive");
+    if (cfg->lo[0] >= cfg->hi[0] || cfg->lo[1] >= cfg->hi[1])
+      invalid("MppiConfig: control bounds must be a nonempty box");
+    if (!(nominal->tau_v > 0.0) || !(nominal->tau_omega > 0.0))
+      invalid("NominalParams: time constants must be positive");
+    if (!(nominal->dt > 0.0) || nominal->dt >= std::min(nominal->tau_v, nominal->tau_omega))
+      invalid("NominalParams: require 0 < dt < min(tau_v, tau_omega)");
+    if (pm->kind < 0 || pm->kind > 3) invalid("Planner: unknown prediction model");
+    if (pm->kind == GPMPPI_MODEL_GP_ENSEMBLE &&
+        (pm->gp == nullptr || pm->n_terrains < 1 || pm->gp->m != 2 * pm->n_terrains))
+      invalid("Planner: GP ensemble needs a model with 2M outputs");
+    if (pm->kind == GPMPPI_MODEL_GP_ENSEMBLE && pm->n_terrains > gpm::kMaxTerrains)
+      invalid("Planner: too many terrains for the device planner");
+    if (pm->kind == GPMPPI_MODEL_EDD5) {
+      if (!(pm->track_width > 0.0)) invalid("step_edd5: track_width must be positive");
+      if (pm->edd5.y_icr_r - pm->edd5.y_icr_l <= 1e-6)
+        invalid("step_edd5: degenerate ICR span (y_icr_r - y_icr_l <= 1e-6)");
+    }
+    require_device(device);
+    auto* p = new gpmppi_planner();
+    try {
+      p->device = device;
+      CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+      CK(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device));
+      p->cfg = *cfg;
+      p->model_kind = pm->kind;
+      p->model = pm->kind == GPMPPI_MODEL_GP_ENSEMBLE ? pm->gp : nullptr;
+      if (p->model && p->model->device != device) invalid("Planner: GP model lives on another device");
+      p->R = pm->kind == GPMPPI_MODEL_GP_ENSEMBLE ? pm->n_terrains : 1;
+      p->edd5 = {pm->edd5.alpha_l, pm->edd5.alpha_r, pm->edd5.x_icr, pm->edd5.y_icr_l,
+                 pm->edd5.y_icr_r, pm->track_width};
+      p->nom = {nominal->tau_v, nominal->tau_omega, nominal->dt};
+      p->p_x = p_x;
+      p->chi2 = -2.0 * std::log1p(-p_x);  // uncertainty.cpp:8-13
+      p->z = normal_quantile(p_x);
+      p->tw.assign(p->R, 1.0 / p->R);
+      p->T = cfg->horizon;
+      p->words = (p->T + 31) / 32;
+      p->K_total = cfg->samples;
+      p->K_local = cfg->samples;
+      p->s_begin = 0;
+      const int T = p->T;
+      p->d_nom = p->dalloc<double>(2 * T);
+      std::vector<double> nom0(2 * T);  // bounds.clamp(Control{}) (mppi.cpp:200)
+      for (int k = 0; k < T; ++k) {
+        nom0[2 * k] = gpm::clampd(0.0, cfg->lo[0], cfg->hi[0]);
+        nom0[2 * k + 1] = gpm::clampd(0.0, cfg->lo[1], cfg->hi[1]);
+      }
+      CK(cudaMemcpyAsync(p->d_nom, nom0.data(), sizeof(double) * 2 * T, cudaMemcpyHostToDevice, p->stream));
+      p->d_tw = p->dalloc<double>(gpm::kMaxTerrains);
+      CK(cudaMemcpyAsync(p->d_tw, p->tw.data(), sizeof(double) * p->R, cudaMemcpyHostToDevice, p->stream));
+      p->d_x0 = p->dalloc<double>(8);
+      p->d_rbar = p->dalloc<double>(T);
+      p->d_margins = p->dalloc<double>((size_t)T * gpm::kMaxObstacles);
+      p->d_task = p->dalloc<gpm::TaskDev>(1);
+      p->d_rank_tuple = p->dalloc<double>(gpm::tuple_doubles(T));
+      p->d_combined = p->dalloc<double>(gpm::tuple_doubles(T));
+      p->d_out = p->dalloc<double>(16);
+      p->d_hcov = p->dalloc<double>((size_t)T * 25);
+      p->d_ticket = p->dalloc<unsigned int>(1);
+      p->d_infeasible = p->dalloc<int>(1);
+      p->alloc_sample_buffers();
+      CK(cudaMallocHost(&p->h_task, sizeof(gpm::TaskDev)));
+      CK(cudaMallocHost(&p->h_x0, sizeof(double) * 8));
+      CK(cudaMallocHost(&p->h_out, sizeof(double) * 16));
+      CK(cudaMallocHost(&p->h_infeasible, sizeof(int)));
+      for (auto& e : p->ev) CK(cudaEventCreate(&e));
+      CK(cudaStreamSynchronize(p->stream));
+    } catch (...) {
+      delete p;
+      throw;
+    }
+    *out = p;
+  });
+}
+
+void gpmppi_planner_free(gpmppi_planner* p) { delete p; }
+
+int gpmppi_planner_plan_step(gpmppi_planner* p, const double x0[5], const gpmppi_task* task,
+                             double command[2], gpmppi_diag* diag) {
+  if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
+  return guarded([&] {
+    const auto t0 = Clock::now();  // mppi.cpp:391
+    CK(cudaSetDevice(p->device));
+    if (p->K_local != p->K_total) invalid("plan_step: sharded planner; use plan_partial/plan_finish");
+    if (p->noise_mode == gpm::NOISE_INJECTED && !p->injected_set) invalid("plan_step: injected noise mode without noise");
+    stage_tick(p, x0, task);
+    enqueue_samples(p, task->kind == GPMPPI_TASK_TRACKING ? 0 : task->n_obstacles,
+                    task_var_weight(task), 1, nullptr);
+    CK(cudaMemcpyAsync(p->h_out, p->d_out, sizeof(double) * 8, cudaMemcpyDeviceToHost, p->stream));
+    CK(cudaEventRecord(p->ev[0], p->stream));
+    enqueue_tighten(p);  // mppi.cpp:433
+    CK(cudaMemcpyAsync(p->h_infeasible, p->d_infeasible, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+    CK(cudaEventSynchronize(p->ev[0]));
+    const double t_cmd = ms_since(t0);
+    CK(cudaStreamSynchronize(p->stream));
+    fill_diag(p, command, diag, t_cmd, ms_since(t0));
+    ++p->tick;  // mppi.cpp:460
+  });
+}
+
+int gpmppi_planner_set_terrain_weights(gpmppi_planner* p, const double* w, int R) {
+  if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
+  return guarded([&] {  // mppi.cpp:208-218
+    if (p->model_kind == GPMPPI_MODEL_GP_ENSEMBLE && R != p->R)
+      invalid("set_terrain_weights: size mismatch with terrain count");
+    if (!on_simplex(w, R, 1e-6)) invalid("set_terrain_weights: weights must lie on the simplex");
+    if (R > gpm::kMaxTerrains) invalid("set_terrain_weights: too many terrains");
+    p->tw.assign(w, w + R);
+    p->R = R;
+    CK(cudaMemcpyAsync(p->d_tw, p->tw.data(), sizeof(double) * R, cudaMemcpyHostToDevice, p->stream));
+    CK(cudaStreamSynchronize(p->stream));
+  });
+}
+
+int gpmppi_planner_terrain_weights(const gpmppi_planner* p, double* w) {
+  if (!p) return 0;
+  if (w) std::memcpy(w, p->tw.data(), sizeof(double) * p->tw.size());
+  return (int)p->tw.size();
+}
+
+static int copy_back(const gpmppi_planner* p, void* dst, const void* src, size_t bytes) {
+  return guarded([&] {
+    CK(cudaSetDevice(p->device));
+    CK(cudaStreamSynchronize(p->stream));
+    CK(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+  });
+}
+
+int gpmppi_planner_nominal_sequence(const gpmppi_planner* p, double* seq) {
+  if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
+  return copy_back(p, seq, p->d_nom, sizeof(double) * 2 * p->T);
+}
+int gpmppi_planner_set_nominal_sequence(gpmppi_planner* p, const double* seq) {
+  if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
+  return guarded([&] {
+    CK(cudaMemcpyAsync(p->d_nom, seq, sizeof(double) * 2 * p->T, cudaMemcpyHostToDevice, p->stream));
+    CK(cudaStreamSynchronize(p->stream));
+  });
+}
+int gpmppi_planner_horizon_covariances(const gpmppi_planner* p, double* cov) {
+  if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
+  return copy_back(p, cov, p->d_hcov, sizeof(double) * 25 * p->T);
+}
+int gpmppi_planner_lane_radii(const gpmppi_planner* p, double* r) {
+  if (!p || !p->rbar_init) return 0;
+  if (r && copy_back(p, r, p->d_rbar, sizeof(double) * p->T) != GPMPPI_OK) return -1;
+  return p->T;
+}
+int gpmppi_planner_obstacle_margins(const gpmppi_planner* p, double* m) {
+  if (!p || p->margins_O <= 0) return 0;
+  if (m) {
+    std::vector<double> tmp((size_t)p->T * gpm::kMaxObstacles);
+    if (copy_back(p, tmp.data(), p->d_margins, sizeof(double) * p->T * p->margins_O) != GPMPPI_OK) return -1;
+    std::memcpy(m, tmp.data(), sizeof(double) * p->T * p->margins_O);
+  }
+  return p->margins_O;
+}
+int gpmppi_planner_set_thresholds(gpmppi_planner* p, const double* r_bar, const double* margins,
+                                  int n_obstacles) {
+  if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
+  return guarded([&] {
+    if (n_obstacles < 0 || n_obstacles > gpm::kMaxObstacles) invalid("set_thresholds: bad obstacle count");
+    if (r_bar) {
+      CK(cudaMemcpyAsync(p->d_rbar, r_bar, sizeof(double) * p->T, cudaMemcpyHostToDevice, p->stream));
+      p->rbar_init = true;
+    }
+    if (margins) {
+      CK(cudaMemcpyAsync(p->d_margins, margins, sizeof(double) * p->T * n_obstacles, cudaMemcpyHostToDevice, p->stream));
+      p->margins_O = n_obstacles;
+    }
+    CK(cudaStreamSynchronize(p->stream));
+  });
+}
+uint64_t gpmppi_planner_tick(const gpmppi_planner* p) { return p ? p->tick : 0; }
+int gpmppi_planner_horizon(const gpmppi_planner* p) { return p ? p->T : 0; }
+int gpmppi_planner_samples(const gpmppi_planner* p) { return p ? (int)p->K_local : 0; }
+
+int gpmppi_planner_set_noise_mode(gpmppi_planner* p, int mode) {
+  if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
+  if (mode != GPMPPI_NOISE_PHILOX && mode != GPMPPI_NOISE_INJECTED) return fail(GPMPPI_INVALID_ARGUMENT, "unknown noise mode");
+  p->noise_mode = mode;
+  return GPMPPI_OK;
+}
+int gpmppi_planner_inject_noise(gpmppi_planner* p, const double* eps) {
+  if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
+  return guarded([&] {
+    if (!p->d_eps) p->d_eps = p->dalloc<double>((size_t)p->K_local * p->T * 2);
+    CK(cudaMemcpyAsync(p->d_eps, eps, sizeof(double) * p->K_local * p->T * 2, cudaMemcpyHostToDevice, p->stream));
+    CK(cudaStreamSynchronize(p->stream));
+    p->injected_set = true;
+    p->noise_mode = gpm::NOISE_INJECTED;
+  });
+}
+int gpmppi_planner_philox_noise(const gpmppi_planner* p, uint64_t tick, double* eps) {
+  if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
+  return guarded([&] {
+    CK(cudaSetDevice(p->device));
+    double* d = nullptr;
+    const size_t cnt = (size_t)p->K_local * p->T * 2;
+    CK(cudaMalloc(&d, sizeof(double) * cnt));
+    cudaError_t e = gpm::launch_philox_noise(gpm::philox_key(p->cfg.seed, tick), p->s_begin,
+                                             (int)p->K_local, p->T, std::sqrt(p->cfg.sigma_v2),
+                                             std::sqrt(p->cfg.sigma_w2), d, p->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+    if (e == cudaSuccess) e = cudaMemcpy(eps, d, sizeof(double) * cnt, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) throw CudaError{e, "philox_noise_kernel"};
+  });
+}
+
+int gpmppi_planner_sample_costs(const gpmppi_planner* p, double* costs) {
+  if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
+  return copy_back(p, costs, p->d_costs, sizeof(double) * p->K_local);
+}
+int gpmppi_planner_sample_weights(const gpmppi_planner* p, double* w) {
+  if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
+  return guarded([&] {
+    CK(cudaSetDevice(p->device));
+    CK(cudaStreamSynchronize(p->stream));
+    const int W = gpm::tuple_doubles(p->T);
+    std::vector<double> e(p->K_local), parts((size_t)p->reduce_blocks * W), tup(W);
+    CK(cudaMemcpy(e.data(), p->d_e, sizeof(double) * p->K_local, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(parts.data(), p->d_partials, sizeof(double) * parts.size(), cudaMemcpyDeviceToHost));
+    const double* src = p->K_local == p->K_total ? p->d_rank_tuple : p->d_combined;
+    CK(cudaMemcpy(tup.data(), src, sizeof(double) * W, cudaMemcpyDeviceToHost));
+    const int per = (int)((p->K_local + p->reduce_blocks - 1) / p->reduce_blocks);
+    for (long long s = 0; s < p->K_local; ++s) {
+      const int b = (int)(s / per);
+      const double mb = parts[(size_t)b * W];
+      w[s] = (e[s] == 0.0 || !(tup[1] > 0.0)) ? 0.0 : e[s] * std::exp(-(mb - tup[0]) / p->cfg.lambda) / tup[1];
+    }
+  });
+}
+int gpmppi_planner_flags(const gpmppi_planner* p, uint8_t* viol, uint8_t* coll, uint8_t* terminal,
+                         uint8_t* alive) {
+  if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
+  return guarded([&] {
+    CK(cudaSetDevice(p->device));
+    CK(cudaStreamSynchronize(p->stream));
+    const size_t nw = (size_t)p->K_local * p->words;
+    std::vector<uint32_t> vb(nw), cb(nw);
+    CK(cudaMemcpy(vb.data(), p->d_viol, sizeof(uint32_t) * nw, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(cb.data(), p->d_coll, sizeof(uint32_t) * nw, cudaMemcpyDeviceToHost));
+    for (long long s = 0; s < p->K_local; ++s)
+      for (int k = 0; k < p->T; ++k) {
+        const uint32_t word = (uint32_t)(s * p->words + (k >> 5));
+        if (viol) viol[s * p->T + k] = (vb[word] >> (k & 31)) & 1u;
+        if (coll) coll[s * p->T + k] = (cb[word] >> (k & 31)) & 1u;
+      }
+    if (terminal) CK(cudaMemcpy(terminal, p->d_term, p->K_local, cudaMemcpyDeviceToHost));
+    if (alive) CK(cudaMemcpy(alive, p->d_alive, p->K_local, cudaMemcpyDeviceToHost));
+  });
+}
+
+int gpmppi_planner_set_variance_path(gpmppi_planner* p, int path) {
+  if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
+  if (path < 0 || path > 2) return fail(GPMPPI_INVALID_ARGUMENT, "unknown variance path");
+  p->var_path = path;
+  return GPMPPI_OK;
+}
+int gpmppi_planner_variance_path(const gpmppi_planner* p) { return p ? p->var_path : -1; }
+
+int gpmppi_planner_bench_device(gpmppi_planner* p, const double x0[5], const gpmppi_task* task,
+                                int ticks, int flush_l2, double* tick_ms, double* phase_ms) {
+  if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
+  return guarded([&] {
+    CK(cudaSetDevice(p->device));
+    if (ticks < 1) invalid("bench_device: ticks must be >= 1");
+    stage_tick(p, x0, task);
+    const int n_obs = task->kind == GPMPPI_TASK_TRACKING ? 0 : task->n_obstacles;
+    const double vw = task_var_weight(task);
+    void* flush = nullptr;
+    size_t flush_bytes = 0;
+    if (flush_l2) {
+      int l2 = 0;
+      CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, p->device));
+      flush_bytes = (size_t)std::max(l2, 1 << 20) * 2;
+      CK(cudaMalloc(&flush, flush_bytes));
+    }
+    std::vector<cudaEvent_t> evs((size_t)ticks * 5);
+    for (auto& e : evs) CK(cudaEventCreate(&e));
+    for (int t = 0; t < ticks; ++t) {
+      cudaEvent_t* E = &evs[(size_t)t * 5];
+      if (flush) CK(cudaMemsetAsync(flush, t & 0xff, flush_bytes, p->stream));  // outside the timed span
+      enqueue_samples(p, n_obs, vw, 1, E);
+      enqueue_tighten(p);
+      CK(cudaEventRecord(E[4], p->stream));
+      ++p->tick;
+    }
+    cudaError_t se = cudaStreamSynchronize(p->stream);
+    if (flush) cudaFree(flush);
+    CK(se);
+    double ph[4] = {0, 0, 0, 0};
+    for (int t = 0; t < ticks; ++t) {
+      cudaEvent_t* E = &evs[(size_t)t * 5];
+      for (int i = 0; i < 4; ++i) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, E[i], E[i + 1]));
+        ph[i] += ms;
+      }
+      float tot = 0.f;
+      CK(cudaEventElapsedTime(&tot, E[0], E[4]));
+      if (tick_ms) tick_ms[t] = tot;
+    }
+    for (auto& e : evs) cudaEventDestroy(e);
+    if (phase_ms)
+      for (int i = 0; i < 4; ++i) phase_ms[i] = ph[i];  // rollout, variance, reduce+update, tightening
+  });
+}
+
+int gpmppi_flush_l2(int device) {
+  return guarded([&] {
+    require_device(device);
+    int l2 = 0;
+    CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device));
+    const size_t bytes = (size_t)std::max(l2, 1 << 20) * 2;
+    void* buf = nullptr;
+    CK(cudaMalloc(&buf, bytes));
+    cudaError_t e = cudaMemset(buf, 0x5a, bytes);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    cudaFree(buf);
+    CK(e);
+  });
+}
+
+int gpmppi_planner_io_bytes(const gpmppi_planner* p, int64_t* h2d, int64_t* d2h) {
+  if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
+  if (h2d) *h2d = (int64_t)(sizeof(gpm::TaskDev) + 5 * sizeof(double));
+  if (d2h) *d2h = (int64_t)(8 * sizeof(double) + sizeof(int));
+  return GPMPPI_OK;
+}
+
+int gpmppi_tuple_doubles(int horizon) { return gpm::tuple_doubles(horizon); }
+
+int gpmppi_planner_set_shard(gpmppi_planner* p, int64_t begin, int64_t count) {
+  if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
+  return guarded([&] {
+    if (begin < 0 || count < 1 || begin + count > p->K_total) invalid("set_shard: range outside [0, samples)");
+    CK(cudaSetDevice(p->device));
+    CK(cudaStreamSynchronize(p->stream));
+    p->s_begin = begin;
+    p->K_local = count;
+    p->d_eps = nullptr;
+    p->injected_set = false;
+    p->alloc_sample_buffers();
+    CK(cudaStreamSynchronize(p->stream));
+  });
+}
+
+int gpmppi_planner_plan_partial(gpmppi_planner* p, const double x0[5], const gpmppi_task* task,
+                                void* device_tuple_out) {
+  if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
+  return guarded([&] {
+    CK(cudaSetDevice(p->device));
+    if (p->noise_mode == gpm::NOISE_INJECTED && !p->injected_set) invalid("plan_partial: injected noise mode without noise");
+    stage_tick(p, x0, task);
+    enqueue_samples(p, task->kind == GPMPPI_TASK_TRACKING ? 0 : task->n_obstacles,
+                    task_var_weight(task), 0, nullptr);
+    CK(cudaMemcpyAsync(device_tuple_out, p->d_rank_tuple, sizeof(double) * gpm::tuple_doubles(p->T),
+                       cudaMemcpyDeviceToDevice, p->stream));
+    CK(cudaStreamSynchronize(p->stream));
+  });
+}
+
+int gpmppi_planner_plan_finish(gpmppi_planner* p, const void* device_tuples, int n_ranks,
+                               double command[2], gpmppi_diag* diag) {
+  if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
+  return guarded([&] {
+    const auto t0 = Clock::now();
+    CK(cudaSetDevice(p->device));
+    if (n_ranks < 1) invalid("plan_finish: n_ranks must be >= 1");
+    check(gpm::launch_finish(static_cast<const double*>(device_tuples), n_ranks, p->T,
+                             p->cfg.lambda, p->d_nom, p->cfg.lo, p->cfg.hi, p->d_out, p->K_total,
+                             p->d_combined, p->stream),
+          "finish kernel");
+    CK(cudaMemcpyAsync(p->h_out, p->d_out, sizeof(double) * 8, cudaMemcpyDeviceToHost, p->stream));
+    CK(cudaEventRecord(p->ev[0], p->stream));
+    enqueue_tighten(p);
+    CK(cudaMemcpyAsync(p->h_infeasible, p->d_infeasible, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+    CK(cudaEventSynchronize(p->ev[0]));
+    const double t_cmd = ms_since(t0);
+    CK(cudaStreamSynchronize(p->stream));
+    fill_diag(p, command, diag, t_cmd, ms_since(t0));
+    ++p->tick;
+  });
+}
+
+int gpmppi_combine_tuples_host(const double* tuples, int n_ranks, int horizon, double lambda,
+                               double* out) {
+  if (!tuples || !out || n_ranks < 1 || horizon < 1 || !(lambda > 0.0))
+    return fail(GPMPPI_INVALID_ARGUMENT, "combine_tuples: bad arguments");
+  gpm::combine_tuples(tuples, n_ranks, horizon, lambda, out);
+  return GPMPPI_OK;
+}
+
+}  // extern "C"

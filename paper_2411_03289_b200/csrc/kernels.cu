@@ -1,0 +1,925 @@
+// kernels.cu — sm_100a kernels of the GP-MPPI solve (mppi.cpp:389-462).
+//
+//   rollout_gp_kernel     one warp per sample: Philox/injected noise, clamp,
+//                         FP64 GP-mean (k*·alpha, gp.cpp:172-182) + dynamic
+//                         unicycle (dynamics.cpp:39-66) + per-step costs and
+//                         flags (costs.cpp:127-171); writes the step queries.
+//   rollout_base_kernel   one thread per sample for the GP-free models.
+//   variance_ffma_kernel  flash-style var = sf2 - ||k* L^{-T}||^2 (gp.cpp:184-191)
+//                         with k* recomputed on the fly, FP32 FFMA, FP64 sum.
+//   reduce_kernel         costs, min-baselined softmax, Σw·eps, ESS/entropy
+//                         as one tuple per block; the last block combines the
+//                         tuples, updates/clamps/shifts (mppi.cpp:125-173).
+//   tighten_kernel        tightening pass (mppi.cpp:250-282), FP64.
+//   predict_kernel        GpModel::predict_batch in FP64 (gp.cpp:152-198).
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cfloat>
+#include <cstdio>
+#include <cstdlib>
+
+#include "internal.hpp"
+
+namespace gpm {
+
+static std::atomic<unsigned long long> g_launches{0};
+void count_launch(int n) { g_launches += n; }
+unsigned long long launches_total() { return g_launches.load(); }
+
+// -------------------------------------------------------------------------
+// warp helpers (xor butterfly: every lane ends with bit-identical sums)
+GPM_D double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+GPM_D double warp_min(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// -------------------------------------------------------------------------
+// Rollout, GP ensemble model. NO = max outputs per kernel group (compile time).
+size_t rollout_smem_bytes(const RolloutArgs& a) {
+  size_t b = sizeof(TaskDev);
+  b += sizeof(double) * (size_t)(2 * a.T + a.T + a.T * (a.n_obs > 0 ? a.n_obs : 1) + a.R + 2);
+  b = (b + 15) & ~(size_t)15;
+  if (a.model_kind == MODEL_GP)
+    for (int g = 0; g < a.model.G; ++g) b += sizeof(double) * (size_t)(5 + a.model.g[g].n_out) * a.model.n;
+  return b;
+}
+
+struct SmemView {
+  TaskDev* task;
+  double* nom;
+  double* rbar;
+  double* marg;
+  double* tw;
+  double* pts;  // groups back to back
+};
+
+GPM_D SmemView load_common_smem(const RolloutArgs& a, unsigned char* smem) {
+  SmemView v;
+  v.task = reinterpret_cast<TaskDev*>(smem);
+  double* p = reinterpret_cast<double*>(smem + sizeof(TaskDev));
+  v.nom = p;
+  p += 2 * a.T;
+  v.rbar = p;
+  p += a.T;
+  v.marg = p;
+  p += a.T * (a.n_obs > 0 ? a.n_obs : 1);
+  v.tw = p;
+  p += a.R + 2;
+  size_t off = (reinterpret_cast<size_t>(p) + 15) & ~(size_t)15;
+  v.pts = reinterpret_cast<double*>(off);
+  {  // task (plain words)
+    const int nw = sizeof(TaskDev) / 8;
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(a.task);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(v.task);
+    for (int i = threadIdx.x; i < nw; i += blockDim.x) dst[i] = src[i];
+  }
+  for (int i = threadIdx.x; i < 2 * a.T; i += blockDim.x) v.nom[i] = a.nominal_seq[i];
+  if (a.r_bar)
+    for (int i = threadIdx.x; i < a.T; i += blockDim.x) v.rbar[i] = a.r_bar[i];
+  if (a.margins)
+    for (int i = threadIdx.x; i < a.T * a.n_obs; i += blockDim.x) v.marg[i] = a.margins[i];
+  for (int i = threadIdx.x; i < a.R; i += blockDim.x) v.tw[i] = a.tw[i];
+  return v;
+}
+
+GPM_D void sample_noise(const RolloutArgs& a, int sl, long long s, int k, double* e0, double* e1) {
+  if (a.noise_mode == NOISE_INJECTED) {
+    const double2 e = reinterpret_cast<const double2*>(a.eps)[(size_t)sl * a.T + k];
+    *e0 = e.x;
+    *e1 = e.y;
+  } else {
+    double z1, z2;
+    philox_gaussian_pair(a.key, (uint64_t)s, (uint32_t)k, &z1, &z2);
+    *e0 = a.sv * z1;
+    *e1 = a.sw * z2;
+  }
+}
+
+template <int LPS>
+GPM_D double group_sum(double v) {  // xor butterfly inside an LPS-lane group
+#pragma unroll
+  for (int o = LPS / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// One LPS-lane group per sample (32/LPS samples per warp share every Z/alpha
+// shared-memory read); lanes split the n GP points, the dynamics and cost are
+// evaluated redundantly (bit-identically) by the group's lanes.
+template <int NO, int LPS>
+__global__ void __launch_bounds__(256, 1) rollout_gp_kernel(const RolloutArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  SmemView sv = load_common_smem(a, smem);
+  const int n = a.model.n;
+  {  // stage Z / alpha of every group (SoA) into shared memory
+    double* dst = sv.pts;
+    for (int g = 0; g < a.model.G; ++g) {
+      const int cnt = (5 + a.model.g[g].n_out) * n;
+      const double2* src = reinterpret_cast<const double2*>(a.model.g[g].pts);
+      double2* d2 = reinterpret_cast<double2*>(dst);
+      for (int i = threadIdx.x; i < cnt / 2; i += blockDim.x) d2[i] = src[i];
+      if ((cnt & 1) && threadIdx.x == 0) dst[cnt - 1] = a.model.g[g].pts[cnt - 1];
+      dst += cnt;
+    }
+  }
+  __syncthreads();
+  const TaskDev& task = *sv.task;
+  const int gl = threadIdx.x % LPS;  // lane inside the sample group
+  const int groups_per_block = blockDim.x / LPS;
+  const int gid = blockIdx.x * groups_per_block + threadIdx.x / LPS;
+  const int ngroups = gridDim.x * groups_per_block;
+  const int T = a.T;
+  const int O = a.n_obs;
+  // every lane of the warp runs the same trip count (samples beyond K are masked)
+  const int rounds = (a.K_local + ngroups - 1) / ngroups;
+
+  for (int r = 0; r < rounds; ++r) {
+    const int sl = gid + r * ngroups;
+    const bool valid = sl < a.K_local;
+    const long long s = a.s_begin + (valid ? sl : 0);
+    double st[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) st[i] = a.x0[i];
+    bool alive = valid;
+    double cost = 0.0, decay = 1.0;
+    uint32_t vb = 0, cb = 0;
+    for (int k = 0; k < T; ++k) {
+      double e0 = 0.0, e1 = 0.0;
+      if (valid) sample_noise(a, sl, s, k, &e0, &e1);
+      const double u[2] = {clampd(sv.nom[2 * k] + e0, a.lo[0], a.hi[0]),
+                           clampd(sv.nom[2 * k + 1] + e1, a.lo[1], a.hi[1])};  // mppi.cpp:298-308
+      if (valid && gl == 0)
+        a.queries[(size_t)sl * T + k] =
+            make_float4((float)st[3], (float)st[4], (float)u[0], (float)u[1]);
+      double sp, cp;
+      sincos(st[2], &sp, &cp);
+      double nx[5];
+      // the shuffles below need every lane of the warp: no divergent exit here
+      double cm0 = 0.0, cm1 = 0.0;
+      {
+        const double* gp = sv.pts;
+        for (int g = 0; g < a.model.G; ++g) {
+          const GroupDev& G = a.model.g[g];
+          const int nout = G.n_out;
+          // gp.cpp:172-176 augmented query [q/l | -1/2|q/l|^2 | 1]
+          const double q0 = st[3] / G.ls[0], q1 = st[4] / G.ls[1];
+          const double q2 = u[0] / G.ls[2], q3 = u[1] / G.ls[3];
+          const double qn = -0.5 * (q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
+          double acc[NO];
+#pragma unroll
+          for (int o = 0; o < NO; ++o) acc[o] = 0.0;
+          if (alive) {
+            const double* z0 = gp;
+            const double* z1 = gp + n;
+            const double* z2 = gp + 2 * n;
+            const double* z3 = gp + 3 * n;
+            const double* zn = gp + 4 * n;
+            const double* al = gp + 5 * n;
+#pragma unroll 4
+            for (int j = gl; j < n; j += LPS) {
+              // gp.cpp:177-179: k*_j = exp(q_aug · inputs_aug_j)
+              const double d = q0 * z0[j] + q1 * z1[j] + q2 * z2[j] + q3 * z3[j] + qn + zn[j];
+              const double kj = exp(d);
+#pragma unroll
+              for (int o = 0; o < NO; ++o)
+                if (o < nout) acc[o] = fma(kj, al[o * n + j], acc[o]);  // gp.cpp:181-182
+            }
+          }
+#pragma unroll
+          for (int o = 0; o < NO; ++o) {
+            if (o < nout) {
+              const double mo = group_sum<LPS>(acc[o]);
+              const int gi = G.out_idx[o];
+              const double w = sv.tw[gi >> 1];  // combine_terrains (mppi.cpp:34-49)
+              if (gi & 1)
+                cm1 += w * mo;
+              else
+                cm0 += w * mo;
+            }
+          }
+          gp += (size_t)(5 + nout) * n;
+        }
+      }
+      if (alive) {  // mppi.cpp:329-349
+        step_nominal(st, u, a.nom, nx, sp, cp);
+        nx[3] += cm0;  // mppi.cpp:341-342
+        nx[4] += cm1;
+        if (!finite5(nx)) {  // mppi.cpp:343-346
+          alive = false;
+#pragma unroll
+          for (int i = 0; i < 5; ++i) nx[i] = st[i];
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 5; ++i) nx[i] = st[i];
+      }
+      const StepCost c = step_cost(task, st, nx, sp, cp, sv.rbar[k], sv.marg + (size_t)k * O, u[0], decay);
+      cost += c.cost;
+      decay *= 0.9;
+      vb |= (uint32_t)c.viol << (k & 31);
+      cb |= (uint32_t)c.coll << (k & 31);
+      if ((k & 31) == 31 || k == T - 1) {
+        if (valid && gl == 0) {
+          a.viol_bits[(size_t)sl * a.words + (k >> 5)] = vb;
+          a.coll_bits[(size_t)sl * a.words + (k >> 5)] = cb;
+        }
+        vb = cb = 0;
+      }
+#pragma unroll
+      for (int i = 0; i < 5; ++i) st[i] = nx[i];
+    }
+    bool term = false;
+    if (task.kind == TASK_AVOIDANCE) {  // costs.cpp:169 terminal_cost
+      const double gx = st[0] - task.goal[0], gy = st[1] - task.goal[1];
+      term = sqrt(gx * gx + gy * gy) <= task.goal[2];
+      cost += task.aw[3] * (term ? 0.0 : task.high_cost);
+    }
+    if (valid && gl == 0) {
+      a.cost_mean[sl] = alive ? cost : __longlong_as_double(0x7ff8000000000000LL);
+      a.term[sl] = term;
+      a.alive[sl] = alive;
+    }
+  }
+}
+
+// GP-free models (mppi.cpp:351-368): one thread per sample.
+__global__ void __launch_bounds__(256) rollout_base_kernel(const RolloutArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  SmemView sv = load_common_smem(a, smem);
+  __syncthreads();
+  const TaskDev& task = *sv.task;
+  const int T = a.T, O = a.n_obs;
+  for (int sl = blockIdx.x * blockDim.x + threadIdx.x; sl < a.K_local; sl += gridDim.x * blockDim.x) {
+    const long long s = a.s_begin + sl;
+    double st[5];
+    for (int i = 0; i < 5; ++i) st[i] = a.x0[i];
+    bool alive = true;
+    double cost = 0.0, decay = 1.0;
+    uint32_t vb = 0, cb = 0;
+    for (int k = 0; k < T; ++k) {
+      double e0, e1;
+      sample_noise(a, sl, s, k, &e0, &e1);
+      const double u[2] = {clampd(sv.nom[2 * k] + e0, a.lo[0], a.hi[0]),
+                           clampd(sv.nom[2 * k + 1] + e1, a.lo[1], a.hi[1])};
+      double nx[5];
+      if (alive) {
+        if (a.model_kind == MODEL_EDD5) {
+          step_edd5(st, u, a.edd5, a.nom.dt, nx);
+        } else if (a.model_kind == MODEL_UNICYCLE) {
+          step_kinematic(st, u, a.nom.dt, nx);
+        } else {
+          double sp0, cp0;
+          sincos(st[2], &sp0, &cp0);
+          step_nominal(st, u, a.nom, nx, sp0, cp0);
+        }
+        if (!finite5(nx)) {
+          alive = false;
+          for (int i = 0; i < 5; ++i) nx[i] = st[i];
+        }
+      } else {
+        for (int i = 0; i < 5; ++i) nx[i] = st[i];
+      }
+      double sp, cp;
+      sincos(st[2], &sp, &cp);
+      const StepCost c = step_cost(task, st, nx, sp, cp, sv.rbar[k], sv.marg + (size_t)k * O, u[0], decay);
+      cost += c.cost;
+      decay *= 0.9;
+      vb |= (uint32_t)c.viol << (k & 31);
+      cb |= (uint32_t)c.coll << (k & 31);
+      if ((k & 31) == 31 || k == T - 1) {
+        a.viol_bits[(size_t)sl * a.words + (k >> 5)] = vb;
+        a.coll_bits[(size_t)sl * a.words + (k >> 5)] = cb;
+        vb = cb = 0;
+      }
+      for (int i = 0; i < 5; ++i) st[i] = nx[i];
+    }
+    bool term = false;
+    if (task.kind == TASK_AVOIDANCE) {
+      const double gx = st[0] - task.goal[0], gy = st[1] - task.goal[1];
+      term = sqrt(gx * gx + gy * gy) <= task.goal[2];
+      cost += task.aw[3] * (term ? 0.0 : task.high_cost);
+    }
+    a.cost_mean[sl] = alive ? cost : __longlong_as_double(0x7ff8000000000000LL);
+    a.term[sl] = term;
+    a.alive[sl] = alive;
+  }
+}
+
+int rollout_lanes_per_sample(int K, int num_sms) {
+  static int forced = -1;
+  if (forced < 0) {
+    const char* e = getenv("GPMPPI_LPS");
+    forced = e ? atoi(e) : 0;
+  }
+  if (forced == 8 || forced == 16 || forced == 32) return forced;
+  // aim for >= ~7 warps per SM before widening the lane groups
+  const long long per_sm = ((long long)K + num_sms - 1) / num_sms;
+  if (per_sm >= 28) return 8;
+  if (per_sm >= 14) return 16;
+  return 32;
+}
+
+cudaError_t launch_rollout(const RolloutArgs& a, int num_sms, cudaStream_t st) {
+  const size_t smem = rollout_smem_bytes(a);
+  if (a.K_local <= 0) return cudaSuccess;
+  if (a.model_kind == MODEL_GP) {
+    int no = 0;
+    for (int g = 0; g < a.model.G; ++g) no = a.model.g[g].n_out > no ? a.model.g[g].n_out : no;
+    int lps = rollout_lanes_per_sample(a.K_local, num_sms);
+    // groups per block: spread the samples evenly over the SMs (one block per SM)
+    const int spw = 32 / lps;
+    long long warps = ((long long)a.K_local + spw - 1) / spw;
+    int wpb = (int)((warps + num_sms - 1) / num_sms);
+    wpb = wpb < 1 ? 1 : (wpb > 8 ? 8 : wpb);
+    long long blocks = (warps + wpb - 1) / wpb;
+    if (blocks > num_sms) blocks = num_sms;
+    const int threads = wpb * 32;
+    using KF = void (*)(const RolloutArgs);
+    KF table[4][3] = {
+        {rollout_gp_kernel<2, 8>, rollout_gp_kernel<2, 16>, rollout_gp_kernel<2, 32>},
+        {rollout_gp_kernel<4, 8>, rollout_gp_kernel<4, 16>, rollout_gp_kernel<4, 32>},
+        {rollout_gp_kernel<6, 8>, rollout_gp_kernel<6, 16>, rollout_gp_kernel<6, 32>},
+        {rollout_gp_kernel<8, 8>, rollout_gp_kernel<8, 16>, rollout_gp_kernel<8, 32>}};
+    const int ni = no <= 2 ? 0 : no <= 4 ? 1 : no <= 6 ? 2 : 3;
+    const int li = lps == 8 ? 0 : lps == 16 ? 1 : 2;
+    KF kern = table[ni][li];
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)blocks, threads, smem, st>>>(a);
+  } else {
+    const int threads = 128;
+    int blocks = (a.K_local + threads - 1) / threads;
+    cudaError_t e = cudaFuncSetAttribute(rollout_base_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    rollout_base_kernel<<<blocks, threads, smem, st>>>(a);
+  }
+  count_launch();
+  return cudaGetLastError();
+}
+
+// -------------------------------------------------------------------------
+// Variance (FP32 FFMA): per 64-query tile, column blocks of 128, row chunks of
+// 32. k* recomputed per (column block, row chunk) in the exact-difference form
+// exp(ln sf2 - 1/2 |q/l - z/l|^2) (no augmented-form cancellation in FP32).
+constexpr int VQ = 64, VJ = 128, VI = 32;
+
+__global__ void __launch_bounds__(256) variance_ffma_kernel(const VarianceArgs a) {
+  __shared__ float qs[VQ][4];
+  __shared__ __align__(16) float kT[VI][VQ];
+  __shared__ __align__(16) float Ls[VI][VJ];
+  const int n = a.n;
+  const long long q0 = (long long)blockIdx.x * VQ;
+  const int t = threadIdx.x, lane = t & 31, ty = t >> 5;
+  if (t < VQ) {
+    const long long qi = q0 + t;
+    float4 q = qi < a.KT ? a.queries[qi] : make_float4(0.f, 0.f, 0.f, 0.f);
+    qs[t][0] = q.x / (float)a.g.ls[0];
+    qs[t][1] = q.y / (float)a.g.ls[1];
+    qs[t][2] = q.z / (float)a.g.ls[2];
+    qs[t][3] = q.w / (float)a.g.ls[3];
+  }
+  const float lsv = (float)a.g.log_sv;
+  double part[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) part[i] = 0.0;
+  for (int j0 = 0; j0 < n; j0 += VJ) {
+    float acc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int d = 0; d < 4; ++d) acc[i][d] = 0.f;
+    const int iend = min(n, j0 + VJ);
+    for (int i0 = 0; i0 < iend; i0 += VI) {
+      __syncthreads();
+      // k* chunk: VI points × VQ queries (8 per thread)
+      for (int e = t; e < VI * VQ; e += 256) {
+        const int ii = e / VQ, qq = e % VQ;
+        const int gi = i0 + ii;
+        float v = 0.f;
+        if (gi < n) {
+          const float d0 = qs[qq][0] - a.g.zs32[gi];
+          const float d1 = qs[qq][1] - a.g.zs32[n + gi];
+          const float d2 = qs[qq][2] - a.g.zs32[2 * n + gi];
+          const float d3 = qs[qq][3] - a.g.zs32[3 * n + gi];
+          v = expf(lsv - 0.5f * (d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3));
+        }
+        kT[ii][qq] = v;
+      }
+      // L^{-T}[i0:i0+VI, j0:j0+VJ]
+      for (int e = t; e < VI * VJ / 4; e += 256) {
+        const int ii = e / (VJ / 4), jj = (e % (VJ / 4)) * 4;
+        const int gi = i0 + ii, gj = j0 + jj;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (gi < n) {
+          const float* row = a.g.ilt32 + (size_t)gi * n;
+          if (gj + 3 < n && ((n & 3) == 0)) {
+            v = *reinterpret_cast<const float4*>(row + gj);
+          } else {
+            v.x = gj < n ? row[gj] : 0.f;
+            v.y = gj + 1 < n ? row[gj + 1] : 0.f;
+            v.z = gj + 2 < n ? row[gj + 2] : 0.f;
+            v.w = gj + 3 < n ? row[gj + 3] : 0.f;
+          }
+        }
+        *reinterpret_cast<float4*>(&Ls[ii][jj]) = v;
+      }
+      __syncthreads();
+#pragma unroll 8
+      for (int ii = 0; ii < VI; ++ii) {
+        const float4 ka = *reinterpret_cast<const float4*>(&kT[ii][ty * 8]);
+        const float4 kb = *reinterpret_cast<const float4*>(&kT[ii][ty * 8 + 4]);
+        const float kk[8] = {ka.x, ka.y, ka.z, ka.w, kb.x, kb.y, kb.z, kb.w};
+        float l[4];
+#pragma unroll
+        for (int d = 0; d < 4; ++d) l[d] = Ls[ii][lane + 32 * d];
+#pragma unroll
+        for (int qq = 0; qq < 8; ++qq)
+#pragma unroll
+          for (int d = 0; d < 4; ++d) acc[qq][d] = fmaf(kk[qq], l[d], acc[qq][d]);
+      }
+    }
+#pragma unroll
+    for (int qq = 0; qq < 8; ++qq) {
+      double p = 0.0;
+#pragma unroll
+      for (int d = 0; d < 4; ++d) p += (double)acc[qq][d] * (double)acc[qq][d];
+      part[qq] += warp_sum(p);
+    }
+  }
+  if (lane < 8) {
+    double mine = 0.0;
+#pragma unroll
+    for (int qq = 0; qq < 8; ++qq)
+      if (qq == lane) mine = part[qq];
+    const long long qi = q0 + ty * 8 + lane;
+    if (qi < a.KT) {
+      double v = a.g.sv - mine;  // gp.cpp:187-191
+      v = v > 0.0 ? v : 0.0;
+      const double c = a.coef * v;
+      a.trace[qi] = a.accumulate ? a.trace[qi] + c : c;
+    }
+  }
+}
+
+cudaError_t launch_tc_variance(const VarianceArgs& a, int one_pass, cudaStream_t st);  // kernels_tc.cu
+
+cudaError_t launch_variance(const VarianceArgs& a, int path, cudaStream_t st) {
+  if (a.KT <= 0) return cudaSuccess;
+  if (path != 0) return launch_tc_variance(a, path == 2, st);
+  const long long blocks = (a.KT + VQ - 1) / VQ;
+  variance_ffma_kernel<<<(unsigned)blocks, 256, 0, st>>>(a);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// -------------------------------------------------------------------------
+// Reduction: tuple per block, last block combines (+ update/shift/diag).
+int reduce_blocks_for(int K_local, int num_sms) {
+  int b = (K_local + 63) / 64;
+  if (b > num_sms) b = num_sms;
+  return b < 1 ? 1 : b;
+}
+
+GPM_D void block_reduce_5(double v[5], double* red /*[32*5]*/) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int i = 0; i < 5; ++i) v[i] = warp_sum(v[i]);
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < 5; ++i) red[w * 5 + i] = v[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 5; ++i) {
+      double s = 0.0;
+      for (int q = 0; q < nw; ++q) s += red[q * 5 + i];
+      red[i] = s;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 5; ++i) v[i] = red[i];
+  __syncthreads();
+}
+
+// Apply a combined tuple: update + clamp (mppi.cpp:147-164), command (:430),
+// shift (:166-173), diagnostics (:435-455). Executed by one block.
+GPM_D void apply_tuple(const double* tup, int T, double lambda, double* nominal_seq,
+                       const double lo[2], const double hi[2], double* out, long long K_total,
+                       double* tmp /*2T*/) {
+  const double Z = tup[1];
+  for (int r = threadIdx.x; r < 2 * T; r += blockDim.x) {
+    const double dv = Z > 0.0 ? tup[kTupleHead + r] / Z : 0.0;
+    tmp[r] = clampd(nominal_seq[r] + dv, lo[r & 1], hi[r & 1]);
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < 2 * T; r += blockDim.x) {
+    const int k = r >> 1;
+    nominal_seq[r] = k + 1 < T ? tmp[r + 2] : tmp[r];
+  }
+  if (threadIdx.x == 0) {
+    const double m = tup[0], E2 = tup[2], H = tup[3], N = tup[4], C = tup[5];
+    out[0] = tmp[0];
+    out[1] = tmp[1];
+    out[2] = N > 0.0 ? m : INFINITY;                                      // best_cost
+    out[3] = N > 0.0 ? C / N : __longlong_as_double(0x7ff8000000000000LL);  // mean_cost
+    out[4] = (Z > 0.0 && E2 > 0.0) ? (Z * Z) / E2 : 0.0;                   // ess = 1/Σw²
+    out[5] = Z > 0.0 ? log(Z) + H / (lambda * Z) : 0.0;                    // -Σ w ln w
+    out[6] = (double)K_total - N;                                           // nonfinite
+    out[7] = N;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) reduce_kernel(const ReduceArgs a) {
+  extern __shared__ __align__(16) double dsm[];
+  __shared__ double red[32 * 5];
+  __shared__ unsigned int s_last;
+  const int T = a.T;
+  const int per = (a.K_local + gridDim.x - 1) / gridDim.x;
+  const int b0 = blockIdx.x * per;
+  const int b1 = min(a.K_local, b0 + per);
+  const int W = tuple_doubles(T);
+  // pass 1: costs (cost_mean + var_w * Σ_k trace), block min over finite
+  double lmin = INFINITY;
+  for (int s = b0 + threadIdx.x; s < b1; s += blockDim.x) {
+    double c = a.cost_mean[s];
+    if (a.trace) {
+      double vsum = 0.0;
+      const double* tr = a.trace + (size_t)s * T;
+      for (int k = 0; k < T; ++k) vsum += tr[k];
+      c += a.var_w * vsum;
+    }
+    a.costs_out[s] = c;
+    if (isfinite(c)) lmin = fmin(lmin, c);
+  }
+  lmin = warp_min(lmin);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = lmin;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = INFINITY;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmin(m, red[w]);
+    red[31 * 5] = m;
+  }
+  __syncthreads();
+  const double mb = red[31 * 5];
+  __syncthreads();
+  // pass 2: e_s = exp(-(c - m_b)/lambda) (mppi.cpp:137-142) and scalar sums
+  double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // Z, E2, H, N, C
+  for (int s = b0 + threadIdx.x; s < b1; s += blockDim.x) {
+    const double c = a.costs_out[s];
+    double e = 0.0;
+    if (isfinite(c)) {
+      e = exp(-(c - mb) / a.lambda);
+      v[0] += e;
+      v[1] += e * e;
+      v[2] += e * (c - mb);
+      v[3] += 1.0;
+      v[4] += c;
+    }
+    a.e_out[s] = e;
+  }
+  block_reduce_5(v, red);
+  // pass 3: S[k][c] = Σ_s e_s eps[s][k][c]; thread = (k, slice)
+  const int nsl = max(1, (int)blockDim.x / T);
+  double* Ssl = dsm;  // [nsl][T][2]
+  for (int idx = threadIdx.x; idx < T * nsl; idx += blockDim.x) {
+    const int k = idx % T, sl = idx / T;
+    double s0 = 0.0, s1 = 0.0;
+    for (int s = b0 + sl; s < b1; s += nsl) {
+      const double e = a.e_out[s];
+      if (e == 0.0) continue;
+      double e0, e1;
+      if (a.noise_mode == NOISE_INJECTED) {
+        const double2 ep = reinterpret_cast<const double2*>(a.eps)[(size_t)s * T + k];
+        e0 = ep.x;
+        e1 = ep.y;
+      } else {
+        double z1, z2;
+        philox_gaussian_pair(a.key, (uint64_t)(a.s_begin + s), (uint32_t)k, &z1, &z2);
+        e0 = a.sv * z1;
+        e1 = a.sw * z2;
+      }
+      s0 += e * e0;
+      s1 += e * e1;
+    }
+    Ssl[(sl * T + k) * 2] = s0;
+    Ssl[(sl * T + k) * 2 + 1] = s1;
+  }
+  __syncthreads();
+  double* mine = a.partials + (size_t)blockIdx.x * W;
+  for (int r = threadIdx.x; r < 2 * T; r += blockDim.x) {
+    double acc = 0.0;
+    for (int sl = 0; sl < nsl; ++sl) acc += Ssl[sl * 2 * T + r];
+    mine[kTupleHead + r] = acc;
+  }
+  if (threadIdx.x == 0) {
+    mine[0] = v[3] > 0.0 ? mb : INFINITY;
+    mine[1] = v[0];
+    mine[2] = v[1];
+    mine[3] = v[2];
+    mine[4] = v[3];
+    mine[5] = v[4];
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // last block: combine the block tuples in block order
+  double* tup = a.rank_tuple;
+  if (threadIdx.x == 0) {
+    double m = INFINITY;
+    for (int b = 0; b < (int)gridDim.x; ++b) {
+      const volatile double* p = a.partials + (size_t)b * W;
+      if (p[0] < m) m = p[0];
+    }
+    double Z = 0.0, E2 = 0.0, H = 0.0, N = 0.0, C = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) {
+      const volatile double* p = a.partials + (size_t)b * W;
+      N += p[4];
+      C += p[5];
+      if (!(p[4] > 0.0)) continue;
+      const double sc = exp(-(p[0] - m) / a.lambda);
+      Z += sc * p[1];
+      E2 += sc * sc * p[2];
+      H += sc * (p[3] + (p[0] - m) * p[1]);
+    }
+    tup[0] = m;
+    tup[1] = Z;
+    tup[2] = E2;
+    tup[3] = H;
+    tup[4] = N;
+    tup[5] = C;
+    red[0] = m;
+    *a.ticket = 0u;  // re-arm for the next launch
+  }
+  __syncthreads();
+  const double m = red[0];
+  for (int r = threadIdx.x; r < 2 * T; r += blockDim.x) {
+    double acc = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) {
+      const volatile double* p = a.partials + (size_t)b * W;
+      if (!(p[4] > 0.0)) continue;
+      acc += exp(-(p[0] - m) / a.lambda) * p[kTupleHead + r];
+    }
+    tup[kTupleHead + r] = acc;
+  }
+  __syncthreads();
+  if (a.finish) apply_tuple(tup, T, a.lambda, a.nominal_seq, a.lo, a.hi, a.out, a.K_total, dsm);
+}
+
+cudaError_t launch_reduce(const ReduceArgs& a, int blocks, cudaStream_t st) {
+  const int threads = 256;
+  const int nsl = threads / a.T > 1 ? threads / a.T : 1;
+  size_t smem = sizeof(double) * (size_t)nsl * a.T * 2;
+  if (smem < sizeof(double) * 2 * a.T) smem = sizeof(double) * 2 * a.T;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  reduce_kernel<<<blocks, threads, smem, st>>>(a);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// Combine rank tuples (multi-GPU) and apply: one block.
+__global__ void finish_kernel(const double* tuples, int n, int T, double lambda,
+                              double* nominal_seq, double lo0, double lo1, double hi0, double hi1,
+                              double* out, long long K_total, double* combined) {
+  extern __shared__ __align__(16) double tmp[];
+  if (threadIdx.x == 0) combine_tuples(tuples, n, T, lambda, combined);
+  __syncthreads();
+  __threadfence_block();
+  const double lo[2] = {lo0, lo1}, hi[2] = {hi0, hi1};
+  apply_tuple(combined, T, lambda, nominal_seq, lo, hi, out, K_total, tmp);
+}
+
+cudaError_t launch_finish(const double* tuples, int n, int T, double lambda, double* nominal_seq,
+                          const double lo[2], const double hi[2], double* out, long long K_total,
+                          double* combined, cudaStream_t st) {
+  finish_kernel<<<1, 128, sizeof(double) * 2 * T, st>>>(tuples, n, T, lambda, nominal_seq, lo[0],
+                                                          lo[1], hi[0], hi[1], out, K_total,
+                                                          combined);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// -------------------------------------------------------------------------
+// FP64 single-query GP predict by one block (used by tightening and predict).
+// Returns per-output mean (into mean[m]) and per-group variance (var_g[G]).
+GPM_D void block_gp_predict(const ModelDev& M, const double q[4], double* kst /*n*/,
+                            double* red /*>= 32*8*/, double* mean /*m*/, double* var_g) {
+  const int n = M.n;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int g = 0; g < M.G; ++g) {
+    const GroupDev& G = M.g[g];
+    const double q0 = q[0] / G.ls[0], q1 = q[1] / G.ls[1], q2 = q[2] / G.ls[2], q3 = q[3] / G.ls[3];
+    const double qn = -0.5 * (q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
+    const double* p = G.pts;
+    double acc[kMaxOutPerGroup];
+    for (int o = 0; o < kMaxOutPerGroup; ++o) acc[o] = 0.0;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      const double d = q0 * p[j] + q1 * p[n + j] + q2 * p[2 * n + j] + q3 * p[3 * n + j] + qn + p[4 * n + j];
+      const double kj = exp(d);
+      kst[j] = kj;
+      for (int o = 0; o < G.n_out; ++o) acc[o] = fma(kj, p[(5 + o) * n + j], acc[o]);
+    }
+    for (int o = 0; o < G.n_out; ++o) {
+      const double s = warp_sum(acc[o]);
+      if (lane == 0) red[w * 8 + o] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int o = 0; o < G.n_out; ++o) {
+        double s = 0.0;
+        for (int q2i = 0; q2i < nw; ++q2i) s += red[q2i * 8 + o];
+        mean[G.out_idx[o]] = s;
+      }
+    __syncthreads();
+    // a_j = Σ_{i<=j} k_i L^{-T}[i][j]; ssq = Σ a_j^2
+    double ssq = 0.0;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      double aj = 0.0;
+      for (int i = 0; i <= j; ++i) aj = fma(kst[i], G.ilt64[(size_t)i * n + j], aj);
+      ssq = fma(aj, aj, ssq);
+    }
+    ssq = warp_sum(ssq);
+    if (lane == 0) red[w * 8] = ssq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int q2i = 0; q2i < nw; ++q2i) s += red[q2i * 8];
+      double v = G.sv - s;
+      var_g[g] = v > 0.0 ? v : 0.0;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(512) predict_kernel(const ModelDev M, const double* q, long long S,
+                                                      double* mean, double* var) {
+  extern __shared__ __align__(16) double kst[];
+  __shared__ double red[32 * 8];
+  __shared__ double smean[kMaxGroups * kMaxOutPerGroup];
+  __shared__ double svar[kMaxGroups];
+  for (long long s = blockIdx.x; s < S; s += gridDim.x) {
+    const double qq[4] = {q[s * 4], q[s * 4 + 1], q[s * 4 + 2], q[s * 4 + 3]};
+    block_gp_predict(M, qq, kst, red, smean, svar);
+    if (threadIdx.x == 0)
+      for (int g = 0; g < M.G; ++g)
+        for (int o = 0; o < M.g[g].n_out; ++o) {
+          const int oi = M.g[g].out_idx[o];
+          mean[s * M.m + oi] = smean[oi];
+          var[s * M.m + oi] = svar[g];
+        }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_predict(const ModelDev& m, const double* q, long long S, double* mean,
+                           double* var, cudaStream_t st) {
+  if (S <= 0) return cudaSuccess;
+  const size_t smem = sizeof(double) * (size_t)m.n;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(predict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int blocks = S < 1184 ? (int)S : 1184;
+  predict_kernel<<<blocks, 512, smem, st>>>(m, q, S, mean, var);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// -------------------------------------------------------------------------
+// Tightening pass (mppi.cpp:250-282 + uncertainty.cpp:75-116), one block, FP64.
+__global__ void __launch_bounds__(512) tighten_kernel(const TightenArgs a) {
+  extern __shared__ __align__(16) double kst[];
+  __shared__ double red[32 * 8];
+  __shared__ double smean[kMaxGroups * kMaxOutPerGroup];
+  __shared__ double svar[kMaxGroups];
+  __shared__ double mu[5], cov[25];
+  __shared__ int infeasible;
+  const TaskDev& t = *a.task;
+  if (threadIdx.x < 5) mu[threadIdx.x] = a.x0[threadIdx.x];
+  if (threadIdx.x < 25) cov[threadIdx.x] = 0.0;
+  if (threadIdx.x == 0) infeasible = 0;
+  __syncthreads();
+  for (int k = 0; k < a.T; ++k) {
+    const double u[2] = {a.nominal_seq[2 * k], a.nominal_seq[2 * k + 1]};
+    double cm0 = 0.0, cm1 = 0.0, cv0 = 0.0, cv1 = 0.0;
+    if (a.model_kind == MODEL_GP) {  // correction_at (mppi.cpp:220-233)
+      const double q[4] = {mu[3], mu[4], u[0], u[1]};
+      block_gp_predict(a.model, q, kst, red, smean, svar);
+      if (threadIdx.x == 0) {
+        // ensemble_combine (gp.cpp:368-389): ascending terrain order
+        for (int i = 0; i < a.R; ++i) {
+          const double wi = a.tw[i];
+          int g0 = 0, g1 = 0;
+          for (int g = 0; g < a.model.G; ++g)
+            for (int o = 0; o < a.model.g[g].n_out; ++o) {
+              if (a.model.g[g].out_idx[o] == 2 * i) g0 = g;
+              if (a.model.g[g].out_idx[o] == 2 * i + 1) g1 = g;
+            }
+          cm0 += wi * smean[2 * i];
+          cm1 += wi * smean[2 * i + 1];
+          cv0 += wi * wi * svar[g0];
+          cv1 += wi * wi * svar[g1];
+        }
+      }
+    }
+    if (threadIdx.x == 0) {  // propagate_belief (uncertainty.cpp:75-88)
+      double nm[5], J[25], JS[25], C[25];
+      double sp, cp;
+      sincos(mu[2], &sp, &cp);
+      double m0[5] = {mu[0], mu[1], mu[2], mu[3], mu[4]};
+      step_nominal(m0, u, a.nom, nm, sp, cp);
+      nm[3] += cm0;
+      nm[4] += cm1;
+      jacobian_nominal(m0, a.nom, J);
+      for (int i = 0; i < 5; ++i)
+        for (int j = 0; j < 5; ++j) {
+          double s = 0.0;
+          for (int q = 0; q < 5; ++q) s += J[i * 5 + q] * cov[q * 5 + j];
+          JS[i * 5 + j] = s;
+        }
+      for (int i = 0; i < 5; ++i)
+        for (int j = 0; j < 5; ++j) {
+          double s = 0.0;
+          for (int q = 0; q < 5; ++q) s += JS[i * 5 + q] * J[j * 5 + q];
+          C[i * 5 + j] = s;
+        }
+      C[3 * 5 + 3] += cv0;
+      C[4 * 5 + 4] += cv1;
+      for (int i = 0; i < 5; ++i)
+        for (int j = 0; j < 5; ++j) cov[i * 5 + j] = 0.5 * (C[i * 5 + j] + C[j * 5 + i]);
+      for (int i = 0; i < 5; ++i) mu[i] = nm[i];
+      for (int i = 0; i < 25; ++i) a.horizon_cov[(size_t)k * 25 + i] = cov[i];
+      const double c00 = cov[0], c01 = cov[1], c10 = cov[5], c11 = cov[6];
+      if (t.kind != TASK_AVOIDANCE) {  // tighten_lane_radius (uncertainty.cpp:90-96)
+        const double half_tr = 0.5 * (c00 + c11);
+        const double disc = 0.25 * (c00 - c11) * (c00 - c11) + c01 * c10;
+        double l = half_tr + sqrt(disc > 0.0 ? disc : 0.0);
+        l = l > 0.0 ? l : 0.0;
+        const double r = t.half_width - sqrt(a.chi2 * l);
+        a.r_bar[k] = r;
+        if (r <= 0.0) infeasible = 1;
+      }
+      if (t.kind != TASK_TRACKING) {  // tighten_obstacle_distance (uncertainty.cpp:98-116)
+        for (int o = 0; o < t.n_obs; ++o) {
+          const double dx = mu[0] - t.obs[o][0], dy = mu[1] - t.obs[o][1];
+          const double dist = sqrt(dx * dx + dy * dy);
+          double d, n0, n1;
+          if (dist < 1e-12) {
+            n0 = 1.0;
+            n1 = 0.0;
+            d = -t.obs[o][2];
+          } else {
+            n0 = dx / dist;
+            n1 = dy / dist;
+            d = dist - t.obs[o][2];
+          }
+          const double cn0 = c00 * n0 + c01 * n1, cn1 = c10 * n0 + c11 * n1;
+          double dv = n0 * cn0 + n1 * cn1;
+          dv = dv > 0.0 ? dv : 0.0;
+          const double dbar = d - a.z * sqrt(dv);
+          a.margins[(size_t)k * t.n_obs + o] = d - dbar;
+          if (dbar <= 0.0) infeasible = 1;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *a.infeasible = infeasible;
+}
+
+cudaError_t launch_tighten(const TightenArgs& a, cudaStream_t st) {
+  const size_t smem = sizeof(double) * (size_t)(a.model.n > 0 ? a.model.n : 1);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(tighten_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  tighten_kernel<<<1, 512, smem, st>>>(a);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// -------------------------------------------------------------------------
+__global__ void philox_noise_kernel(uint64_t key, long long s_begin, int K, int T, double sv,
+                                    double sw, double* eps) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)K * T) return;
+  const long long s = i / T;
+  const int k = (int)(i % T);
+  double z1, z2;
+  philox_gaussian_pair(key, (uint64_t)(s_begin + s), (uint32_t)k, &z1, &z2);
+  eps[2 * i] = sv * z1;
+  eps[2 * i + 1] = sw * z2;
+}
+
+cudaError_t launch_philox_noise(uint64_t key, long long s_begin, int K, int T, double sv,
+                                double sw, double* eps, cudaStream_t st) {
+  const long long n = (long long)K * T;
+  philox_noise_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(key, s_begin, K, T, sv, sw, eps);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace gpm

@@ -1,0 +1,540 @@
+"""Host-side mirror of the reference planner API over the C ABI.
+
+Same names, argument meaning and error behaviour as the reference's C++ API
+(/root/reference/proj/include/gpmppi/{mppi,gp,costs,dynamics}.hpp) and its
+pybind11 module (bindings/module.cpp): invalid arguments raise ValueError
+(std::invalid_argument), factorisation / IO failures raise RuntimeError
+(std::runtime_error). All compute runs on the GPU through libgpmppi_b200.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _capi as A
+
+
+def _f64(a, shape=None):
+    out = np.ascontiguousarray(a, dtype=np.float64)
+    if shape is not None:
+        out = out.reshape(shape)
+    return out
+
+
+# ----------------------------------------------------------------- value types
+@dataclass
+class KernelParams:  # gp.hpp:12-22
+    signal_var: float = 1.0
+    lengthscales: Sequence[float] = (1.0, 1.0, 1.0, 1.0)
+    noise_var: float = 1e-4
+
+    def as_row(self):
+        return [self.signal_var, *list(self.lengthscales), self.noise_var]
+
+
+@dataclass
+class NominalParams:  # dynamics.hpp:12-18
+    tau_v: float = 0.5
+    tau_omega: float = 0.35
+    dt: float = 0.05
+
+
+@dataclass
+class ControlBounds:  # core.hpp:61-74
+    lo: tuple = (-0.5, -2.0)
+    hi: tuple = (2.0, 2.0)
+
+
+@dataclass
+class MppiConfig:  # mppi.hpp:16-26
+    samples: int = 1024
+    horizon: int = 30
+    lam: float = 0.1
+    sigma_sim: tuple = (0.09, 0.25)
+    bounds: ControlBounds = field(default_factory=ControlBounds)
+    seed: int = 0
+    threads: int = 0
+
+    def to_c(self):
+        return A.MppiConfigC(self.samples, self.horizon, self.lam, self.sigma_sim[0],
+                             self.sigma_sim[1], (C.c_double * 2)(*self.bounds.lo),
+                             (C.c_double * 2)(*self.bounds.hi), self.seed, self.threads)
+
+
+@dataclass
+class Edd5Params:  # dynamics.hpp:36-45
+    alpha_l: float = 1.0
+    alpha_r: float = 1.0
+    x_icr: float = 0.0
+    y_icr_l: float = 0.0
+    y_icr_r: float = 0.0
+
+    @staticmethod
+    def ideal(track_width):
+        return Edd5Params(1.0, 1.0, 0.0, -0.5 * track_width, 0.5 * track_width)
+
+
+@dataclass
+class TrackingWeights:  # costs.hpp:34-40
+    variance: float = 0.1
+    deviation: float = 1.0
+    slip: float = 0.3
+    safety: float = 1.0
+    speed: float = 0.2
+
+
+@dataclass
+class AvoidanceWeights:  # costs.hpp:44-50
+    variance: float = 0.1
+    obstacle: float = 1.0
+    stage: float = 0.5
+    terminal: float = 1.0
+
+
+@dataclass
+class GoalSpec:  # costs.hpp:52-55
+    position: tuple = (0.0, 0.0)
+    capture_radius: float = 0.5
+
+
+@dataclass
+class CircleObstacle:  # costs.hpp:29-32
+    center: tuple
+    radius: float
+
+
+class Track:  # costs.hpp:13-27
+    def __init__(self, is_circle, center=(0.0, 0.0), radius=0.0, waypoints=None, closed=True,
+                 half_width=0.5):
+        self.is_circle = bool(is_circle)
+        self.center = tuple(center)
+        self.radius = float(radius)
+        self.waypoints = None if waypoints is None else _f64(waypoints, (-1, 2))
+        self.closed = bool(closed)
+        self.half_width = float(half_width)
+
+    @staticmethod
+    def circle_track(center, radius, half_width):
+        return Track(True, center=center, radius=radius, half_width=half_width)
+
+    @staticmethod
+    def polyline_track(points, half_width, closed):
+        return Track(False, waypoints=points, closed=closed, half_width=half_width)
+
+    def to_c(self):
+        t = A.TrackC()
+        t.is_circle = int(self.is_circle)
+        t.cx, t.cy = self.center
+        t.radius = self.radius
+        if self.waypoints is not None:
+            t.n_waypoints = self.waypoints.shape[0]
+            t.waypoints = A.dptr(self.waypoints)
+        t.closed = int(self.closed)
+        t.half_width = self.half_width
+        return t
+
+
+def _obstacle_array(obstacles):
+    if obstacles is None:
+        return np.zeros((0, 3))
+    rows = []
+    for o in obstacles:
+        if isinstance(o, CircleObstacle):
+            rows.append([o.center[0], o.center[1], o.radius])
+        else:
+            rows.append(list(o))
+    return _f64(rows, (-1, 3)) if rows else np.zeros((0, 3))
+
+
+class TrackingTask:  # mppi.hpp:42-46
+    kind = A.TASK_TRACKING
+
+    def __init__(self, track: Track, v_desired: float, weights: TrackingWeights = None):
+        self.track = track
+        self.v_desired = v_desired
+        self.weights = weights or TrackingWeights()
+        self.obstacles = np.zeros((0, 3))
+        self.goal = GoalSpec()
+        self.avoidance = AvoidanceWeights()
+        self.high_cost = 1e4
+
+    def to_c(self):
+        t = A.TaskC()
+        t.kind = self.kind
+        self._track_c = self.track.to_c() if self.track is not None else None
+        if self._track_c is not None:
+            t.track = C.pointer(self._track_c)
+        t.v_desired = self.v_desired
+        w = self.weights
+        t.tracking = A.TrackingWeightsC(w.variance, w.deviation, w.slip, w.safety, w.speed)
+        self._obs = _obstacle_array(self.obstacles)
+        t.obstacles = A.dptr(self._obs) if self._obs.shape[0] else None
+        t.n_obstacles = self._obs.shape[0]
+        t.goal = (C.c_double * 3)(self.goal.position[0], self.goal.position[1],
+                                  self.goal.capture_radius)
+        a = self.avoidance
+        t.avoidance = A.AvoidanceWeightsC(a.variance, a.obstacle, a.stage, a.terminal)
+        t.high_cost = self.high_cost
+        self._c = t
+        return t
+
+
+class AvoidanceTask(TrackingTask):  # mppi.hpp:47-52
+    kind = A.TASK_AVOIDANCE
+
+    def __init__(self, obstacles, goal: GoalSpec, weights: AvoidanceWeights = None,
+                 high_cost: float = 1e4):
+        super().__init__(None, 0.0)
+        self.obstacles = obstacles
+        self.goal = goal
+        self.avoidance = weights or AvoidanceWeights()
+        self.high_cost = high_cost
+
+
+class CombinedTask(TrackingTask):
+    """Path tracking + tightened obstacle chance constraints (BASELINE config 2).
+
+    cost = tracking_cost (costs.cpp:127-149) + obstacle weight · Σ_k
+    collision_indicator(x_{k+1}, obstacles, margins[k]) (costs.cpp:104-114),
+    composed from unmodified reference terms."""
+    kind = A.TASK_COMBINED
+
+    def __init__(self, track: Track, v_desired: float, obstacles,
+                 weights: TrackingWeights = None, obstacle_weight: float = 1.0):
+        super().__init__(track, v_desired, weights)
+        self.obstacles = obstacles
+        self.avoidance = AvoidanceWeights(obstacle=obstacle_weight)
+
+
+@dataclass
+class StepDiagnostics:  # mppi.hpp:81-89
+    best_cost: float = 0.0
+    mean_cost: float = 0.0
+    ess: float = 0.0
+    weight_entropy: float = 0.0
+    nonfinite_samples: int = 0
+    tightening_infeasible: bool = False
+    plan_ms: float = 0.0
+    command_ms: float = 0.0
+
+
+# ----------------------------------------------------------------- GP model
+class GpModel:
+    """Exact GP with device-resident factors (gp.hpp:30-98)."""
+
+    def __init__(self, handle, device=0):
+        self._h = handle
+        self.device = device
+
+    @staticmethod
+    def fit(inputs, outputs, kernels, device: int = 0) -> "GpModel":
+        X = _f64(inputs)
+        if X.ndim != 2 or X.shape[1] != 4:
+            raise ValueError("GpModel::fit: inputs must be n x 4 with n >= 1")
+        Y = _f64(outputs)
+        if Y.ndim == 1:
+            Y = Y[:, None]
+        if Y.shape[0] != X.shape[0]:
+            raise ValueError("GpModel::fit: outputs must be n x m with m >= 1")
+        rows = [k.as_row() if isinstance(k, KernelParams) else list(k) for k in kernels]
+        if len(rows) != Y.shape[1]:
+            raise ValueError("GpModel::fit: one KernelParams per output column required")
+        K = _f64(rows, (-1, 6))
+        h = C.c_void_p()
+        A.check(A.lib().gpmppi_model_fit(A.dptr(X), A.dptr(Y), X.shape[0], Y.shape[1], A.dptr(K),
+                                         device, C.byref(h)))
+        return GpModel(h, device)
+
+    @staticmethod
+    def load(path: str, device: int = 0) -> "GpModel":
+        h = C.c_void_p()
+        A.check(A.lib().gpmppi_model_load(path.encode(), device, C.byref(h)))
+        return GpModel(h, device)
+
+    def save(self, path: str) -> None:
+        A.check(A.lib().gpmppi_model_save(self._h, path.encode()))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and A._LIB is not None:
+            A._LIB.gpmppi_model_free(self._h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def n_points(self) -> int:
+        return A.lib().gpmppi_model_n_points(self._h)
+
+    @property
+    def n_outputs(self) -> int:
+        return A.lib().gpmppi_model_n_outputs(self._h)
+
+    def n_groups(self) -> int:
+        return A.lib().gpmppi_model_n_groups(self._h)
+
+    def group_jitter(self, g: int) -> float:
+        return A.lib().gpmppi_model_group_jitter(self._h, g)
+
+    def log_marginal_likelihood(self, output: int) -> float:
+        return A.lib().gpmppi_model_log_marginal_likelihood(self._h, output)
+
+    def training_data(self):
+        X = np.empty((self.n_points, 4))
+        Y = np.empty((self.n_points, self.n_outputs))
+        A.check(A.lib().gpmppi_model_training_data(self._h, A.dptr(X), A.dptr(Y)))
+        return X, Y
+
+    def predict_batch(self, queries):
+        Q = _f64(queries)
+        if Q.ndim != 2 or Q.shape[1] != 4:
+            raise ValueError("GpModel::predict_batch: queries must be S x 4")
+        S, m = Q.shape[0], self.n_outputs
+        mean = np.empty((S, m))
+        var = np.empty((S, m))
+        A.check(A.lib().gpmppi_model_predict_batch(self._h, A.dptr(Q), S, A.dptr(mean), A.dptr(var)))
+        return mean, var
+
+    def predict(self, query):
+        q = _f64(query, (1, 4))
+        if not np.isfinite(q).all():
+            raise ValueError("GpModel::predict: non-finite query")
+        mean, var = self.predict_batch(q)
+        return mean[0], var[0]
+
+
+# ----------------------------------------------------------------- planner
+class GpEnsemble:  # mppi.hpp:30-33
+    def __init__(self, model: GpModel, n_terrains: int):
+        self.model = model
+        self.n_terrains = n_terrains
+
+
+class Edd5Baseline:  # mppi.hpp:34-37
+    def __init__(self, params: Edd5Params, track_width: float = 0.4):
+        self.params = params
+        self.track_width = track_width
+
+
+class UnicycleBaseline:  # mppi.hpp:38
+    pass
+
+
+class NominalDynamic:
+    """Dynamic unicycle with zero GP residual (BASELINE config 1 extension)."""
+
+
+def _model_c(model):
+    pm = A.PredictionModelC()
+    if isinstance(model, GpEnsemble):
+        pm.kind = A.MODEL_GP_ENSEMBLE
+        pm.gp = model.model.handle
+        pm.n_terrains = model.n_terrains
+    elif isinstance(model, Edd5Baseline):
+        pm.kind = A.MODEL_EDD5
+        p = model.params
+        pm.edd5 = A.Edd5C(p.alpha_l, p.alpha_r, p.x_icr, p.y_icr_l, p.y_icr_r)
+        pm.track_width = model.track_width
+    elif isinstance(model, UnicycleBaseline):
+        pm.kind = A.MODEL_UNICYCLE
+    elif isinstance(model, NominalDynamic):
+        pm.kind = A.MODEL_NOMINAL
+    else:
+        raise ValueError("Planner: unknown prediction model")
+    return pm
+
+
+class Planner:
+    """B200 GP-MPPI planner (mppi.hpp:96-143)."""
+
+    def __init__(self, cfg: MppiConfig, model, nominal: NominalParams = None, p_x: float = 0.95,
+                 device: int = 0):
+        nominal = nominal or NominalParams()
+        self.cfg = cfg
+        self._model_ref = model  # keep the non-owning GP model alive
+        self._cfg_c = cfg.to_c()
+        self._pm_c = _model_c(model)
+        self._nom_c = A.NominalC(nominal.tau_v, nominal.tau_omega, nominal.dt)
+        h = C.c_void_p()
+        A.check(A.lib().gpmppi_planner_create(C.byref(self._cfg_c), C.byref(self._pm_c),
+                                              C.byref(self._nom_c), p_x, device, C.byref(h)))
+        self._h = h
+        self.T = cfg.horizon
+        self.K = cfg.samples
+
+    def __del__(self):
+        if getattr(self, "_h", None) and A._LIB is not None:
+            A._LIB.gpmppi_planner_free(self._h)
+            self._h = None
+
+    # -- Planner::plan_step (mppi.cpp:464-475)
+    def plan_step(self, x0, task, diag: Optional[StepDiagnostics] = None):
+        x = _f64(x0, (5,))
+        tc = task.to_c()
+        cmd = np.empty(2)
+        d = A.DiagC()
+        A.check(A.lib().gpmppi_planner_plan_step(self._h, A.dptr(x), C.byref(tc), A.dptr(cmd),
+                                                 C.byref(d)))
+        if diag is not None:
+            for k, _ in A.DiagC._fields_:
+                setattr(diag, k, getattr(d, k))
+            diag.tightening_infeasible = bool(d.tightening_infeasible)
+        return cmd
+
+    def set_terrain_weights(self, w):
+        w = _f64(w, (-1,))
+        A.check(A.lib().gpmppi_planner_set_terrain_weights(self._h, A.dptr(w), w.shape[0]))
+
+    def terrain_weights(self):
+        buf = np.empty(64)
+        R = A.lib().gpmppi_planner_terrain_weights(self._h, A.dptr(buf))
+        return buf[:R].copy()
+
+    def nominal_sequence(self):
+        s = np.empty((self.T, 2))
+        A.check(A.lib().gpmppi_planner_nominal_sequence(self._h, A.dptr(s)))
+        return s
+
+    def set_nominal_sequence(self, seq):
+        s = _f64(seq, (self.T, 2))
+        A.check(A.lib().gpmppi_planner_set_nominal_sequence(self._h, A.dptr(s)))
+
+    def horizon_covariances(self):
+        c = np.empty((self.T, 5, 5))
+        A.check(A.lib().gpmppi_planner_horizon_covariances(self._h, A.dptr(c)))
+        return c
+
+    def lane_radii(self):
+        r = np.empty(self.T)
+        n = A.lib().gpmppi_planner_lane_radii(self._h, A.dptr(r))
+        if n < 0:
+            A.check(A.CUDA_ERROR)
+        return r[:n].copy()
+
+    def obstacle_margins(self):
+        m = np.empty(self.T * A.MAX_OBSTACLES)
+        O = A.lib().gpmppi_planner_obstacle_margins(self._h, A.dptr(m))
+        if O < 0:
+            A.check(A.CUDA_ERROR)
+        return m[: self.T * O].reshape(self.T, O).copy()
+
+    def set_thresholds(self, r_bar=None, margins=None):
+        r = None if r_bar is None else _f64(r_bar, (self.T,))
+        m = None if margins is None else _f64(margins, (self.T, -1))
+        O = 0 if m is None else m.shape[1]
+        A.check(A.lib().gpmppi_planner_set_thresholds(self._h, A.dptr(r), A.dptr(m), O))
+
+    def tick(self) -> int:
+        return A.lib().gpmppi_planner_tick(self._h)
+
+    def config(self) -> MppiConfig:
+        return self.cfg
+
+    # -- noise / parity hooks
+    def set_noise_mode(self, mode: int):
+        A.check(A.lib().gpmppi_planner_set_noise_mode(self._h, mode))
+
+    def inject_noise(self, eps):
+        e = _f64(eps, (self.samples_local(), self.T, 2))
+        A.check(A.lib().gpmppi_planner_inject_noise(self._h, A.dptr(e)))
+
+    def philox_noise(self, tick: int):
+        e = np.empty((self.samples_local(), self.T, 2))
+        A.check(A.lib().gpmppi_planner_philox_noise(self._h, tick, A.dptr(e)))
+        return e
+
+    def samples_local(self) -> int:
+        return A.lib().gpmppi_planner_samples(self._h)
+
+    def sample_costs(self):
+        c = np.empty(self.samples_local())
+        A.check(A.lib().gpmppi_planner_sample_costs(self._h, A.dptr(c)))
+        return c
+
+    def sample_weights(self):
+        w = np.empty(self.samples_local())
+        A.check(A.lib().gpmppi_planner_sample_weights(self._h, A.dptr(w)))
+        return w
+
+    def flags(self):
+        K, T = self.samples_local(), self.T
+        v = np.empty((K, T), np.uint8)
+        c = np.empty((K, T), np.uint8)
+        t = np.empty(K, np.uint8)
+        a = np.empty(K, np.uint8)
+        A.check(A.lib().gpmppi_planner_flags(self._h, A.u8ptr(v), A.u8ptr(c), A.u8ptr(t),
+                                             A.u8ptr(a)))
+        return dict(viol=v, coll=c, terminal=t, alive=a)
+
+    def set_variance_path(self, path: int):
+        A.check(A.lib().gpmppi_planner_set_variance_path(self._h, path))
+
+    def variance_path(self) -> int:
+        return A.lib().gpmppi_planner_variance_path(self._h)
+
+    def bench_device(self, x0, task, ticks: int, flush_l2: bool = True):
+        """Device-resident timing: per-tick CUDA-event ms and per-phase sums."""
+        x = _f64(x0, (5,))
+        tc = task.to_c()
+        tick_ms = np.zeros(ticks)
+        ph = np.zeros(4)
+        A.check(A.lib().gpmppi_planner_bench_device(self._h, A.dptr(x), C.byref(tc), ticks,
+                                                    int(flush_l2), A.dptr(tick_ms), A.dptr(ph)))
+        return tick_ms, ph
+
+    def io_bytes(self):
+        h, d = C.c_int64(), C.c_int64()
+        A.check(A.lib().gpmppi_planner_io_bytes(self._h, C.byref(h), C.byref(d)))
+        return h.value, d.value
+
+    # -- sharded solve
+    def set_shard(self, begin: int, count: int):
+        A.check(A.lib().gpmppi_planner_set_shard(self._h, begin, count))
+
+    def plan_partial(self, x0, task, device_tuple_ptr: int):
+        x = _f64(x0, (5,))
+        tc = task.to_c()
+        A.check(A.lib().gpmppi_planner_plan_partial(self._h, A.dptr(x), C.byref(tc),
+                                                    C.c_void_p(device_tuple_ptr)))
+
+    def plan_finish(self, device_tuples_ptr: int, n_ranks: int, diag=None):
+        cmd = np.empty(2)
+        d = A.DiagC()
+        A.check(A.lib().gpmppi_planner_plan_finish(self._h, C.c_void_p(device_tuples_ptr), n_ranks,
+                                                   A.dptr(cmd), C.byref(d)))
+        if diag is not None:
+            for k, _ in A.DiagC._fields_:
+                setattr(diag, k, getattr(d, k))
+        return cmd
+
+
+def tuple_doubles(horizon: int) -> int:
+    return A.lib().gpmppi_tuple_doubles(horizon)
+
+
+def combine_tuples(tuples, horizon: int, lam: float):
+    """Host restatement of the device tuple combine (for CPU multi-rank tests)."""
+    t = _f64(tuples, (-1, tuple_doubles(horizon)))
+    out = np.empty(t.shape[1])
+    A.check(A.lib().gpmppi_combine_tuples_host(A.dptr(t), t.shape[0], horizon, lam, A.dptr(out)))
+    return out
+
+
+def flush_l2(device: int = 0) -> None:
+    A.check(A.lib().gpmppi_flush_l2(device))
+
+
+def kernel_launches() -> int:
+    return A.lib().gpmppi_kernel_launches()
+
+
+# ----------------------------------------------------------------- small host math
+def chi2_quantile_2dof(p: float) -> float:  # uncertainty.cpp:8-13
+    if not (p >= 0.0) or p >= 1.0:
+        raise ValueError("chi2_quantile_2dof: p must lie in [0, 1)")
+    return -2.0 * math.log1p(-p)
