@@ -69,6 +69,10 @@ int gpmppi_model_training_data(const gpmppi_model* model, double* inputs, double
 /* GpModel::predict_batch (gp.cpp:152-207) on the device, FP64: S×4 → mean, var S×m. */
 int gpmppi_model_predict_batch(const gpmppi_model* model, const double* queries, int64_t S,
                                double* mean, double* var);
+/* Per-kernel-group variance of S queries through one of the rollout variance
+ * paths (GPMPPI_VAR_*; queries rounded to FP32 as in the solve): var S×G. */
+int gpmppi_model_variance_batch(const gpmppi_model* model, const double* queries, int64_t S,
+                                int path, double* var);
 
 /* =============================== planner ===============================
  * Replaces gpmppi::Planner (mppi.hpp:96-143) and MppiConfig (mppi.hpp:16-26). */

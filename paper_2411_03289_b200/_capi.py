@@ -94,6 +94,7 @@ SIGNATURES = [
     ("gpmppi_model_log_marginal_likelihood", C.c_double, [_vp, C.c_int]),
     ("gpmppi_model_training_data", C.c_int, [_vp, _dp, _dp]),
     ("gpmppi_model_predict_batch", C.c_int, [_vp, _dp, C.c_int64, _dp, _dp]),
+    ("gpmppi_model_variance_batch", C.c_int, [_vp, _dp, C.c_int64, C.c_int, _dp]),
     ("gpmppi_planner_create", C.c_int, [C.POINTER(MppiConfigC), C.POINTER(PredictionModelC),
                                         C.POINTER(NominalC), C.c_double, C.c_int, C.POINTER(_vp)]),
     ("gpmppi_planner_free", None, [_vp]),

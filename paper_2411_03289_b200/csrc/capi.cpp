@@ -281,7 +281,13 @@ gpmppi_model* build_model(const double* X, const double* Y, int64_t n64, int64_t
       D.ilt64 = M->upload(G.ilt);
       D.ilt32 = M->upload(ilt32);
       D.zs32 = M->upload(zs32);
-      D.tc_b = nullptr;
+      {  // tensor-core operand (pre-tiled TF32 hi/lo L^{-T}, kernels_tc.cu)
+        std::vector<float> tcd;
+        std::vector<int4> tcm;
+        gpm::build_tc_operand(G.ilt.data(), n, tcd, tcm, D.tc_npad, D.tc_np, D.tc_npass);
+        D.tc_b = M->upload(tcd);
+        D.tc_meta = M->upload(tcm);
+      }
       for (int d = 0; d < 4; ++d) D.ls[d] = G.kernel[1 + d];
       D.sv = G.kernel[0];
       D.log_sv = std::log(G.kernel[0]);
@@ -404,6 +410,42 @@ int gpmppi_model_predict_batch(const gpmppi_model* M, const double* q, int64_t S
   });
 }
 
+int gpmppi_model_variance_batch(const gpmppi_model* M, const double* q, int64_t S, int path,
+                                double* var) {
+  if (!M) return fail(GPMPPI_LOGIC_ERROR, "GpModel::predict_batch: model not fitted");
+  if (S < 0 || path < 0 || path > 2) return fail(GPMPPI_INVALID_ARGUMENT, "variance_batch: bad arguments");
+  if (S == 0) return GPMPPI_OK;
+  return guarded([&] {
+    CK(cudaSetDevice(M->device));
+    std::vector<float4> qf(S);
+    for (int64_t i = 0; i < S; ++i)
+      qf[i] = make_float4((float)q[i * 4], (float)q[i * 4 + 1], (float)q[i * 4 + 2], (float)q[i * 4 + 3]);
+    float4* dq = nullptr;
+    double* dv = nullptr;
+    CK(cudaMalloc(&dq, sizeof(float4) * S));
+    CK(cudaMalloc(&dv, sizeof(double) * S));
+    cudaError_t e = cudaMemcpy(dq, qf.data(), sizeof(float4) * S, cudaMemcpyHostToDevice);
+    std::vector<double> hv(S);
+    for (int g = 0; g < M->dev.G && e == cudaSuccess; ++g) {
+      gpm::VarianceArgs v{};
+      v.queries = dq;
+      v.KT = S;
+      v.n = M->n;
+      v.g = M->dev.g[g];
+      v.coef = 1.0;
+      v.accumulate = 0;
+      v.trace = dv;
+      e = gpm::launch_variance(v, path, 0);
+      if (e == cudaSuccess) e = cudaDeviceSynchronize();
+      if (e == cudaSuccess) e = cudaMemcpy(hv.data(), dv, sizeof(double) * S, cudaMemcpyDeviceToHost);
+      for (int64_t i = 0; i < S && e == cudaSuccess; ++i) var[i * M->dev.G + g] = hv[i];
+    }
+    cudaFree(dq);
+    cudaFree(dv);
+    if (e != cudaSuccess) throw CudaError{e, "variance kernel"};
+  });
+}
+
 }  // extern "C"
 
 // ===========================================================================
@@ -422,7 +464,7 @@ struct gpmppi_planner {
   uint64_t tick = 0;
   int noise_mode = gpm::NOISE_PHILOX;
   bool injected_set = false;
-  int var_path = GPMPPI_VAR_FFMA;
+  int var_path = GPMPPI_VAR_TC_3XTF32;  // tensor cores within the stated tolerance
   long long s_begin = 0, K_local = 0, K_total = 0;
   bool rbar_init = false;
   int margins_O = -1;
@@ -442,6 +484,7 @@ struct gpmppi_planner {
          *d_combined = nullptr;
   unsigned int* d_ticket = nullptr;
   int* d_infeasible = nullptr;
+  double *d_tq = nullptr, *d_tmu = nullptr, *d_tJ = nullptr, *d_tvar = nullptr;
   // pinned staging
   gpm::TaskDev* h_task = nullptr;
   double* h_x0 = nullptr;
@@ -730,6 +773,10 @@ void enqueue_tighten(gpmppi_planner* p) {
   t.r_bar = p->d_rbar;
   t.margins = p->d_margins;
   t.infeasible = p->d_infeasible;
+  t.tq = p->d_tq;
+  t.tmu = p->d_tmu;
+  t.tJ = p->d_tJ;
+  t.tvar_part = p->d_tvar;
   check(gpm::launch_tighten(t, p->stream), "tighten kernel");
 }
 
@@ -833,6 +880,14 @@ int gpmppi_planner_create(const gpmppi_mppi_config* cfg, const gpmppi_prediction
       p->d_hcov = p->dalloc<double>((size_t)T * 25);
       p->d_ticket = p->dalloc<unsigned int>(1);
       p->d_infeasible = p->dalloc<int>(1);
+      p->d_tq = p->dalloc<double>((size_t)T * 4);
+      p->d_tmu = p->dalloc<double>((size_t)(T + 1) * 5);
+      p->d_tJ = p->dalloc<double>((size_t)T * 25);
+      {
+        const int G = p->model ? p->model->dev.G : 1;
+        const int ns = p->model ? gpm::tighten_splits(p->model->n) : 1;
+        p->d_tvar = p->dalloc<double>((size_t)T * G * ns);
+      }
       p->alloc_sample_buffers();
       CK(cudaMallocHost(&p->h_task, sizeof(gpm::TaskDev)));
       CK(cudaMallocHost(&p->h_x0, sizeof(double) * 8));

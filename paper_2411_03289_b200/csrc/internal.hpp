@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 #include "common.cuh"
 
@@ -17,6 +18,8 @@ struct GroupDev {
   const float* ilt32;  // FP32 copy of L^{-T}
   const float* zs32;   // FP32 scaled inputs [4][n]
   const float* tc_b;   // tensor-core operand: L^{-T} hi/lo TF32 tiles (see kernels_tc.cu)
+  const int4* tc_meta; // per (pass, chunk): float offset, ncols, col0
+  int tc_npad, tc_np, tc_npass;
   double ls[4];
   double sv, log_sv;
   int n_out;
@@ -108,6 +111,11 @@ struct TightenArgs {
   double* r_bar;
   double* margins;
   int* infeasible;
+  // scratch of the three-phase pass
+  double* tq;         // [T][4] GP queries at the belief means
+  double* tmu;        // [T+1][5] belief means
+  double* tJ;         // [T][25] Jacobians
+  double* tvar_part;  // [T][G][splits] partial ||L^{-1}k*||^2
 };
 
 // launchers (kernels.cu); all enqueue on `st` and return cudaGetLastError()
@@ -124,6 +132,9 @@ cudaError_t launch_philox_noise(uint64_t key, long long s_begin, int K, int T, d
                                 double sw, double* eps, cudaStream_t st);
 size_t rollout_smem_bytes(const RolloutArgs& a);
 int reduce_blocks_for(int K_local, int num_sms);
+int tighten_splits(int n);
+void build_tc_operand(const double* ilt, int n, std::vector<float>& data, std::vector<int4>& meta,
+                      int& n_pad, int& np, int& n_pass);
 void count_launch(int n = 1);
 unsigned long long launches_total();
 

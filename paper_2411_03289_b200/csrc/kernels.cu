@@ -481,7 +481,7 @@ cudaError_t launch_variance(const VarianceArgs& a, int path, cudaStream_t st) {
 // -------------------------------------------------------------------------
 // Reduction: tuple per block, last block combines (+ update/shift/diag).
 int reduce_blocks_for(int K_local, int num_sms) {
-  int b = (K_local + 63) / 64;
+  int b = (K_local + 15) / 16;
   if (b > num_sms) b = num_sms;
   return b < 1 ? 1 : b;
 }
@@ -552,7 +552,8 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceArgs a) {
     if (a.trace) {
       double vsum = 0.0;
       const double* tr = a.trace + (size_t)s * T;
-      for (int k = 0; k < T; ++k) vsum += tr[k];
+#pragma unroll 8
+      for (int k = 0; k < T; ++k) vsum += __ldcg(tr + k);
       c += a.var_w * vsum;
     }
     a.costs_out[s] = c;
@@ -632,24 +633,34 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceArgs a) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  // last block: combine the block tuples in block order
+  // last block: combine the block tuples in block order (heads staged in smem)
   double* tup = a.rank_tuple;
+  const int B = gridDim.x;
+  double* heads = dsm;          // [B][6]   (dsm holds >= 7*B + 2T doubles, see launch_reduce)
+  double* sc = dsm + 6 * B;     // [B] rescale factors
+  for (int i = threadIdx.x; i < 6 * B; i += blockDim.x)
+    heads[i] = __ldcg(a.partials + (size_t)(i / 6) * W + (i % 6));
+  __syncthreads();
   if (threadIdx.x == 0) {
     double m = INFINITY;
-    for (int b = 0; b < (int)gridDim.x; ++b) {
-      const volatile double* p = a.partials + (size_t)b * W;
-      if (p[0] < m) m = p[0];
-    }
+    for (int b = 0; b < B; ++b) m = fmin(m, heads[b * 6]);
+    red[0] = m;
+  }
+  __syncthreads();
+  const double m = red[0];
+  for (int b = threadIdx.x; b < B; b += blockDim.x)
+    sc[b] = heads[b * 6 + 4] > 0.0 ? exp(-(heads[b * 6] - m) / a.lambda) : 0.0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
     double Z = 0.0, E2 = 0.0, H = 0.0, N = 0.0, C = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) {
-      const volatile double* p = a.partials + (size_t)b * W;
+    for (int b = 0; b < B; ++b) {
+      const double* p = heads + b * 6;
       N += p[4];
       C += p[5];
       if (!(p[4] > 0.0)) continue;
-      const double sc = exp(-(p[0] - m) / a.lambda);
-      Z += sc * p[1];
-      E2 += sc * sc * p[2];
-      H += sc * (p[3] + (p[0] - m) * p[1]);
+      Z += sc[b] * p[1];
+      E2 += sc[b] * sc[b] * p[2];
+      H += sc[b] * (p[3] + (p[0] - m) * p[1]);
     }
     tup[0] = m;
     tup[1] = Z;
@@ -657,29 +668,24 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceArgs a) {
     tup[3] = H;
     tup[4] = N;
     tup[5] = C;
-    red[0] = m;
     *a.ticket = 0u;  // re-arm for the next launch
   }
-  __syncthreads();
-  const double m = red[0];
   for (int r = threadIdx.x; r < 2 * T; r += blockDim.x) {
     double acc = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) {
-      const volatile double* p = a.partials + (size_t)b * W;
-      if (!(p[4] > 0.0)) continue;
-      acc += exp(-(p[0] - m) / a.lambda) * p[kTupleHead + r];
-    }
+    for (int b = 0; b < B; ++b) acc = fma(sc[b], __ldcg(a.partials + (size_t)b * W + kTupleHead + r), acc);
     tup[kTupleHead + r] = acc;
   }
   __syncthreads();
-  if (a.finish) apply_tuple(tup, T, a.lambda, a.nominal_seq, a.lo, a.hi, a.out, a.K_total, dsm);
+  double* tmp = dsm + 7 * B;  // 2T doubles
+  if (a.finish) apply_tuple(tup, T, a.lambda, a.nominal_seq, a.lo, a.hi, a.out, a.K_total, tmp);
 }
 
 cudaError_t launch_reduce(const ReduceArgs& a, int blocks, cudaStream_t st) {
   const int threads = 256;
   const int nsl = threads / a.T > 1 ? threads / a.T : 1;
   size_t smem = sizeof(double) * (size_t)nsl * a.T * 2;
-  if (smem < sizeof(double) * 2 * a.T) smem = sizeof(double) * 2 * a.T;
+  const size_t need = sizeof(double) * ((size_t)7 * blocks + 2 * a.T);
+  if (smem < need) smem = need;
   if (smem > 48 * 1024) cudaFuncSetAttribute(reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   reduce_kernel<<<blocks, threads, smem, st>>>(a);
   count_launch();
@@ -792,112 +798,294 @@ cudaError_t launch_predict(const ModelDev& m, const double* q, long long S, doub
 }
 
 // -------------------------------------------------------------------------
-// Tightening pass (mppi.cpp:250-282 + uncertainty.cpp:75-116), one block, FP64.
-__global__ void __launch_bounds__(512) tighten_kernel(const TightenArgs a) {
-  extern __shared__ __align__(16) double kst[];
-  __shared__ double red[32 * 8];
-  __shared__ double smean[kMaxGroups * kMaxOutPerGroup];
-  __shared__ double svar[kMaxGroups];
-  __shared__ double mu[5], cov[25];
-  __shared__ int infeasible;
-  const TaskDev& t = *a.task;
-  if (threadIdx.x < 5) mu[threadIdx.x] = a.x0[threadIdx.x];
-  if (threadIdx.x < 25) cov[threadIdx.x] = 0.0;
-  if (threadIdx.x == 0) infeasible = 0;
-  __syncthreads();
-  for (int k = 0; k < a.T; ++k) {
-    const double u[2] = {a.nominal_seq[2 * k], a.nominal_seq[2 * k + 1]};
-    double cm0 = 0.0, cm1 = 0.0, cv0 = 0.0, cv1 = 0.0;
-    if (a.model_kind == MODEL_GP) {  // correction_at (mppi.cpp:220-233)
-      const double q[4] = {mu[3], mu[4], u[0], u[1]};
-      block_gp_predict(a.model, q, kst, red, smean, svar);
-      if (threadIdx.x == 0) {
-        // ensemble_combine (gp.cpp:368-389): ascending terrain order
-        for (int i = 0; i < a.R; ++i) {
-          const double wi = a.tw[i];
-          int g0 = 0, g1 = 0;
-          for (int g = 0; g < a.model.G; ++g)
-            for (int o = 0; o < a.model.g[g].n_out; ++o) {
-              if (a.model.g[g].out_idx[o] == 2 * i) g0 = g;
-              if (a.model.g[g].out_idx[o] == 2 * i + 1) g1 = g;
-            }
-          cm0 += wi * smean[2 * i];
-          cm1 += wi * smean[2 * i + 1];
-          cv0 += wi * wi * svar[g0];
-          cv1 += wi * wi * svar[g1];
-        }
-      }
-    }
-    if (threadIdx.x == 0) {  // propagate_belief (uncertainty.cpp:75-88)
-      double nm[5], J[25], JS[25], C[25];
-      double sp, cp;
-      sincos(mu[2], &sp, &cp);
-      double m0[5] = {mu[0], mu[1], mu[2], mu[3], mu[4]};
-      step_nominal(m0, u, a.nom, nm, sp, cp);
-      nm[3] += cm0;
-      nm[4] += cm1;
-      jacobian_nominal(m0, a.nom, J);
-      for (int i = 0; i < 5; ++i)
-        for (int j = 0; j < 5; ++j) {
-          double s = 0.0;
-          for (int q = 0; q < 5; ++q) s += J[i * 5 + q] * cov[q * 5 + j];
-          JS[i * 5 + j] = s;
-        }
-      for (int i = 0; i < 5; ++i)
-        for (int j = 0; j < 5; ++j) {
-          double s = 0.0;
-          for (int q = 0; q < 5; ++q) s += JS[i * 5 + q] * J[j * 5 + q];
-          C[i * 5 + j] = s;
-        }
-      C[3 * 5 + 3] += cv0;
-      C[4 * 5 + 4] += cv1;
-      for (int i = 0; i < 5; ++i)
-        for (int j = 0; j < 5; ++j) cov[i * 5 + j] = 0.5 * (C[i * 5 + j] + C[j * 5 + i]);
-      for (int i = 0; i < 5; ++i) mu[i] = nm[i];
-      for (int i = 0; i < 25; ++i) a.horizon_cov[(size_t)k * 25 + i] = cov[i];
-      const double c00 = cov[0], c01 = cov[1], c10 = cov[5], c11 = cov[6];
-      if (t.kind != TASK_AVOIDANCE) {  // tighten_lane_radius (uncertainty.cpp:90-96)
-        const double half_tr = 0.5 * (c00 + c11);
-        const double disc = 0.25 * (c00 - c11) * (c00 - c11) + c01 * c10;
-        double l = half_tr + sqrt(disc > 0.0 ? disc : 0.0);
-        l = l > 0.0 ? l : 0.0;
-        const double r = t.half_width - sqrt(a.chi2 * l);
-        a.r_bar[k] = r;
-        if (r <= 0.0) infeasible = 1;
-      }
-      if (t.kind != TASK_TRACKING) {  // tighten_obstacle_distance (uncertainty.cpp:98-116)
-        for (int o = 0; o < t.n_obs; ++o) {
-          const double dx = mu[0] - t.obs[o][0], dy = mu[1] - t.obs[o][1];
-          const double dist = sqrt(dx * dx + dy * dy);
-          double d, n0, n1;
-          if (dist < 1e-12) {
-            n0 = 1.0;
-            n1 = 0.0;
-            d = -t.obs[o][2];
-          } else {
-            n0 = dx / dist;
-            n1 = dy / dist;
-            d = dist - t.obs[o][2];
-          }
-          const double cn0 = c00 * n0 + c01 * n1, cn1 = c10 * n0 + c11 * n1;
-          double dv = n0 * cn0 + n1 * cn1;
-          dv = dv > 0.0 ? dv : 0.0;
-          const double dbar = d - a.z * sqrt(dv);
-          a.margins[(size_t)k * t.n_obs + o] = d - dbar;
-          if (dbar <= 0.0) infeasible = 1;
-        }
-      }
-    }
-    __syncthreads();
+// Tightening pass (mppi.cpp:250-282 + uncertainty.cpp:75-116), FP64, in three
+// launches. propagate_belief's mean update uses only the GP mean, never the
+// covariance, so the belief-mean chain mu_0..mu_T is computed first (serial,
+// one block), then every step's GP variance and Jacobian in parallel (one block
+// per (step, group, column slice)), then the 5×5 covariance recursion and the
+// thresholds (one warp).
+constexpr int TIGHT_COLS = 256;  // columns of L^{-T} per variance block
+
+// Belief-mean chain. The GP query of step k needs only (v_k, omega_k, u_k) and
+// the lag update of (v, omega) is cheap, so the serial part carries (v, omega)
+// only; theta is a cheap wrap recursion; the FP64 sincos / arc increments /
+// Jacobians are then evaluated for all k in parallel and x, y accumulated in
+// step order exactly as arc_advance does (dynamics.cpp:39-66).
+constexpr int TMEAN_THREADS = 128;
+__global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const TightenArgs a) {
+  extern __shared__ __align__(16) double tsm[];  // [2T nominal][T+1 v][T+1 w][T+1 th][T dx][T dy][pts]
+  __shared__ double tw[kMaxTerrains];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int T = a.T, n = a.model.n;
+  double* nom = tsm;
+  double* vv = nom + 2 * T;
+  double* ww = vv + (T + 1);
+  double* th = ww + (T + 1);
+  double* dx = th + (T + 1);
+  double* dy = dx + T;
+  double* pts = dy + T;
+  if (threadIdx.x < a.R) tw[threadIdx.x] = a.tw[threadIdx.x];
+  for (int i = threadIdx.x; i < 2 * T; i += blockDim.x) nom[i] = a.nominal_seq[i];
+  if (threadIdx.x == 0) {
+    vv[0] = a.x0[3];
+    ww[0] = a.x0[4];
+    th[0] = a.x0[2];
   }
-  if (threadIdx.x == 0) *a.infeasible = infeasible;
+  if (a.model_kind == MODEL_GP) {
+    double* dst = pts;
+    for (int g = 0; g < a.model.G; ++g) {
+      const int cnt = (5 + a.model.g[g].n_out) * n;
+      for (int i = threadIdx.x; i < cnt; i += blockDim.x) dst[i] = a.model.g[g].pts[i];
+      dst += cnt;
+    }
+  }
+  __syncthreads();
+  const double av = a.nom.dt / a.nom.tau_v, aw = a.nom.dt / a.nom.tau_omega;
+  // serial (v, omega) chain with the GP mean (mppi.cpp:220-233), one warp: no
+  // block barriers on the critical path, the butterfly leaves the sums in every lane.
+  if (w == 0) {
+    double v = vv[0], om = ww[0];
+    for (int k = 0; k < T; ++k) {
+      const double u0 = nom[2 * k], u1 = nom[2 * k + 1];
+      double c0 = 0.0, c1 = 0.0;
+      if (a.model_kind == MODEL_GP) {
+        const double* p = pts;
+        for (int g = 0; g < a.model.G; ++g) {
+          const GroupDev& G = a.model.g[g];
+          const double q0 = v / G.ls[0], q1 = om / G.ls[1], q2 = u0 / G.ls[2], q3 = u1 / G.ls[3];
+          const double qn = -0.5 * (q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
+          double acc[kMaxOutPerGroup];
+#pragma unroll
+          for (int o = 0; o < kMaxOutPerGroup; ++o) acc[o] = 0.0;
+#pragma unroll 4
+          for (int j = lane; j < n; j += 32) {
+            const double kj = exp(q0 * p[j] + q1 * p[n + j] + q2 * p[2 * n + j] + q3 * p[3 * n + j] + qn + p[4 * n + j]);
+#pragma unroll
+            for (int o = 0; o < kMaxOutPerGroup; ++o)
+              if (o < G.n_out) acc[o] = fma(kj, p[(5 + o) * n + j], acc[o]);
+          }
+#pragma unroll
+          for (int o = 0; o < kMaxOutPerGroup; ++o)
+            if (o < G.n_out) {
+              const double sm = warp_sum(acc[o]);
+              const int gi = G.out_idx[o];
+              if (gi & 1)
+                c1 += tw[gi >> 1] * sm;  // ensemble_combine, ascending terrains
+              else
+                c0 += tw[gi >> 1] * sm;
+            }
+          p += (size_t)(5 + G.n_out) * n;
+        }
+      }
+      if (lane == 0) {
+        a.tq[k * 4 + 0] = v;
+        a.tq[k * 4 + 1] = om;
+        a.tq[k * 4 + 2] = u0;
+        a.tq[k * 4 + 3] = u1;
+      }
+      v = v + av * (u0 - v) + c0;  // step_nominal lag (dynamics.cpp:63-64) + correction mean
+      om = om + aw * (u1 - om) + c1;
+      if (lane == 0) {
+        vv[k + 1] = v;
+        ww[k + 1] = om;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)  // heading recursion (arc_advance: theta = wrap(theta + omega dt))
+    for (int k = 0; k < T; ++k) th[k + 1] = wrap_angle(th[k] + ww[k] * a.nom.dt);
+  __syncthreads();
+  for (int k = threadIdx.x; k < T; k += blockDim.x) {  // arc increments + Jacobians, parallel in k
+    const double m0[5] = {0.0, 0.0, th[k], vv[k], ww[k]};
+    double s0, c0;
+    sincos(th[k], &s0, &c0);
+    double x = 0.0, y = 0.0, t2 = th[k];
+    arc_advance(x, y, t2, vv[k], 0.0, ww[k], a.nom.dt, s0, c0);
+    dx[k] = x;
+    dy[k] = y;
+    double J[25];
+    jacobian_nominal(m0, a.nom, J);
+    for (int i = 0; i < 25; ++i) a.tJ[k * 25 + i] = J[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = a.x0[0], y = a.x0[1];
+    for (int k = 0; k <= T; ++k) {
+      a.tmu[k * 5 + 0] = x;
+      a.tmu[k * 5 + 1] = y;
+      a.tmu[k * 5 + 2] = th[k];
+      a.tmu[k * 5 + 3] = vv[k];
+      a.tmu[k * 5 + 4] = ww[k];
+      if (k < T) {
+        x += dx[k];
+        y += dy[k];
+      }
+    }
+  }
 }
 
+// grid (T, G, ceil(n / TIGHT_COLS)): partial ||L^{-1} k*||^2 over a column slice.
+__global__ void __launch_bounds__(TIGHT_COLS) tighten_var_kernel(const TightenArgs a) {
+  extern __shared__ __align__(16) double kst[];
+  __shared__ double red[TIGHT_COLS / 32];
+  const int k = blockIdx.x, g = blockIdx.y, c = blockIdx.z;
+  const int n = a.model.n;
+  if (a.model_kind != MODEL_GP) return;
+  const GroupDev& G = a.model.g[g];
+  const double* q = a.tq + k * 4;
+  const double q0 = q[0] / G.ls[0], q1 = q[1] / G.ls[1], q2 = q[2] / G.ls[2], q3 = q[3] / G.ls[3];
+  const double qn = -0.5 * (q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
+  const int j0 = c * TIGHT_COLS;
+  const int jend = min(n, j0 + TIGHT_COLS);
+  const double* p = G.pts;
+  for (int i = threadIdx.x; i < jend; i += blockDim.x)  // rows i <= j only
+    kst[i] = exp(q0 * p[i] + q1 * p[n + i] + q2 * p[2 * n + i] + q3 * p[3 * n + i] + qn + p[4 * n + i]);
+  __syncthreads();
+  double ssq = 0.0;
+  const int j = j0 + threadIdx.x;
+  if (j < n) {
+    double a0 = 0.0, a1 = 0.0;  // a_j = Σ_{i<=j} k_i L^{-T}[i][j]  (gp.cpp:184-185)
+    int i = 0;
+    for (; i + 1 <= j; i += 2) {
+      a0 = fma(kst[i], G.ilt64[(size_t)i * n + j], a0);
+      a1 = fma(kst[i + 1], G.ilt64[(size_t)(i + 1) * n + j], a1);
+    }
+    if (i <= j) a0 = fma(kst[i], G.ilt64[(size_t)i * n + j], a0);
+    const double aj = a0 + a1;
+    ssq = aj * aj;
+  }
+  ssq = warp_sum(ssq);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ssq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    a.tvar_part[((size_t)k * a.model.G + g) * gridDim.z + c] = s;
+  }
+}
+
+// one warp: Σ_{k+1} = J Σ Jᵀ + diag(0,0,0,cv0,cv1), symmetrised; r̄_k and margins.
+__global__ void __launch_bounds__(32) tighten_cov_kernel(const TightenArgs a, int nsplit) {
+  extern __shared__ __align__(16) double csm[];  // [T][25] J, [T][2] cv, [T+1][5] mu
+  __shared__ double S[25], JS[25], C[25];
+  __shared__ int infeasible;
+  const int l = threadIdx.x;
+  const TaskDev& t = *a.task;
+  const int T = a.T;
+  double* Js = csm;
+  double* cvs = csm + 25 * T;
+  double* mus = cvs + 2 * T;
+  for (int i = l; i < 25 * T; i += 32) Js[i] = a.tJ[i];
+  for (int i = l; i < 5 * (T + 1); i += 32) mus[i] = a.tmu[i];
+  // per-step combined correction variance (gp.cpp:187-191 + ensemble_combine gp.cpp:380-386)
+  for (int k = l; k < T; k += 32) {
+    double c0 = 0.0, c1 = 0.0;
+    if (a.model_kind == MODEL_GP) {
+      double vg[kMaxGroups];
+      for (int g = 0; g < a.model.G; ++g) {
+        double s = 0.0;
+        for (int c = 0; c < nsplit; ++c) s += a.tvar_part[((size_t)k * a.model.G + g) * nsplit + c];
+        const double v = a.model.g[g].sv - s;
+        vg[g] = v > 0.0 ? v : 0.0;
+      }
+      for (int i = 0; i < a.R; ++i) {
+        const double wi = a.tw[i];
+        int g0 = 0, g1 = 0;
+        for (int g = 0; g < a.model.G; ++g)
+          for (int o = 0; o < a.model.g[g].n_out; ++o) {
+            if (a.model.g[g].out_idx[o] == 2 * i) g0 = g;
+            if (a.model.g[g].out_idx[o] == 2 * i + 1) g1 = g;
+          }
+        c0 += wi * wi * vg[g0];
+        c1 += wi * wi * vg[g1];
+      }
+    }
+    cvs[2 * k] = c0;
+    cvs[2 * k + 1] = c1;
+  }
+  if (l < 25) S[l] = 0.0;
+  if (l == 0) infeasible = 0;
+  __syncwarp();
+  for (int k = 0; k < a.T; ++k) {
+    const double* J = Js + 25 * k;
+    const double* cv = cvs + 2 * k;
+    if (l < 25) {
+      const int i = l / 5, j = l % 5;
+      double s = 0.0;
+      for (int q = 0; q < 5; ++q) s += J[i * 5 + q] * S[q * 5 + j];
+      JS[l] = s;
+    }
+    __syncwarp();
+    if (l < 25) {
+      const int i = l / 5, j = l % 5;
+      double s = 0.0;
+      for (int q = 0; q < 5; ++q) s += JS[i * 5 + q] * J[j * 5 + q];
+      if (l == 18) s += cv[0];
+      if (l == 24) s += cv[1];
+      C[l] = s;
+    }
+    __syncwarp();
+    if (l < 25) {
+      const int i = l / 5, j = l % 5;
+      const double v = 0.5 * (C[i * 5 + j] + C[j * 5 + i]);
+      S[l] = v;
+      a.horizon_cov[(size_t)k * 25 + l] = v;
+    }
+    __syncwarp();
+    const double* mu = mus + (k + 1) * 5;  // belief mean after step k
+    const double c00 = S[0], c01 = S[1], c10 = S[5], c11 = S[6];
+    if (l == 0 && t.kind != TASK_AVOIDANCE) {  // tighten_lane_radius (uncertainty.cpp:90-96)
+      const double half_tr = 0.5 * (c00 + c11);
+      const double disc = 0.25 * (c00 - c11) * (c00 - c11) + c01 * c10;
+      double lm = half_tr + sqrt(disc > 0.0 ? disc : 0.0);
+      lm = lm > 0.0 ? lm : 0.0;
+      const double r = t.half_width - sqrt(a.chi2 * lm);
+      a.r_bar[k] = r;
+      if (r <= 0.0) infeasible = 1;
+    }
+    if (t.kind != TASK_TRACKING)  // tighten_obstacle_distance (uncertainty.cpp:98-116)
+      for (int o = l; o < t.n_obs; o += 32) {
+        const double dx = mu[0] - t.obs[o][0], dy = mu[1] - t.obs[o][1];
+        const double dist = sqrt(dx * dx + dy * dy);
+        double d, n0, n1;
+        if (dist < 1e-12) {
+          n0 = 1.0;
+          n1 = 0.0;
+          d = -t.obs[o][2];
+        } else {
+          n0 = dx / dist;
+          n1 = dy / dist;
+          d = dist - t.obs[o][2];
+        }
+        const double cn0 = c00 * n0 + c01 * n1, cn1 = c10 * n0 + c11 * n1;
+        double dv = n0 * cn0 + n1 * cn1;
+        dv = dv > 0.0 ? dv : 0.0;
+        const double dbar = d - a.z * sqrt(dv);
+        a.margins[(size_t)k * t.n_obs + o] = d - dbar;
+        if (dbar <= 0.0) atomicOr(&infeasible, 1);
+      }
+    __syncwarp();
+  }
+  if (l == 0) *a.infeasible = infeasible;
+}
+
+int tighten_splits(int n) { return n > 0 ? (n + TIGHT_COLS - 1) / TIGHT_COLS : 1; }
+
 cudaError_t launch_tighten(const TightenArgs& a, cudaStream_t st) {
+  size_t msm = sizeof(double) * (size_t)(2 * a.T + 3 * (a.T + 1) + 2 * a.T);
+  if (a.model_kind == MODEL_GP)
+    for (int g = 0; g < a.model.G; ++g) msm += sizeof(double) * (size_t)(5 + a.model.g[g].n_out) * a.model.n;
+  if (msm > 48 * 1024) cudaFuncSetAttribute(tighten_mean_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm);
+  tighten_mean_kernel<<<1, TMEAN_THREADS, msm, st>>>(a);
+  const int G = a.model_kind == MODEL_GP ? a.model.G : 1;
+  const int ns = a.model_kind == MODEL_GP ? tighten_splits(a.model.n) : 1;
   const size_t smem = sizeof(double) * (size_t)(a.model.n > 0 ? a.model.n : 1);
-  if (smem > 48 * 1024) cudaFuncSetAttribute(tighten_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  tighten_kernel<<<1, 512, smem, st>>>(a);
-  count_launch();
+  if (smem > 48 * 1024) cudaFuncSetAttribute(tighten_var_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (a.model_kind == MODEL_GP) tighten_var_kernel<<<dim3(a.T, G, ns), TIGHT_COLS, smem, st>>>(a);
+  const size_t csmem = sizeof(double) * (size_t)(25 * a.T + 2 * a.T + 5 * (a.T + 1));
+  if (csmem > 48 * 1024) cudaFuncSetAttribute(tighten_cov_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem);
+  tighten_cov_kernel<<<1, 32, csmem, st>>>(a, ns);
+  count_launch(3);
   return cudaGetLastError();
 }
 

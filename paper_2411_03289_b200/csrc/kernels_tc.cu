@@ -1,7 +1,396 @@
-// kernels_tc.cu — tensor-core (tcgen05, TF32) variance path. Placeholder until
-// the sm_100a UMMA kernel lands; the FFMA path is the default.
+// kernels_tc.cu — tensor-core GP variance on sm_100a (tcgen05 + TMEM + bulk copy).
+//
+// var(q) = sf2 - || k*(q) L^{-T} ||^2   (gp.cpp:184-191, upper-triangular L^{-T})
+//
+// Per CTA (persistent, one per SM) and per 128-query tile:
+//   D[128 x NP] (fp32, TMEM) = A[128 x n] · B[n x NP],  A = k* (recomputed on the
+//   fly, never in HBM), B = L^{-T} columns of this pass, accumulated over 16-point
+//   K chunks; chunks below the diagonal are skipped (triangular factor).
+// 3xTF32: A = A_hi + A_lo, B = B_hi + B_lo (TF32 each), D = A_hi B_hi + A_hi B_lo +
+// A_lo B_hi — FP32-level accuracy on tensor cores (single-pass TF32
+// loses 2-8% relative variance to cancellation). 1xTF32 (hi·hi only) is the
+// optional fast path, gated by the tolerance harness.
+//
+// Warp roles (12 warps): w0 bulk-copies the pre-tiled B chunk (host-arranged in
+// the UMMA K-major no-swizzle canonical layout), w1 issues tcgen05.mma from one
+// thread and owns the TMEM allocation, w4-7 drain TMEM (tcgen05.ld) into
+// Σ a_j^2, w8-11 produce A (exp, hi/lo split) into shared memory.
+// Pipelines: smem ring (full_a/full_b -> MMA -> empty), TMEM (full -> epilogue -> empty).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
 #include "internal.hpp"
 
 namespace gpm {
-cudaError_t launch_tc_variance(const VarianceArgs&, int, cudaStream_t) { return cudaErrorNotSupported; }
+
+namespace tc {
+
+constexpr int M = 128;      // queries per tile (UMMA M, TMEM lanes)
+constexpr int KC = 16;      // points per K chunk (two K=8 TF32 MMAs)
+constexpr int STAGES = 2;
+constexpr int THREADS = 384;
+constexpr int A_STAGE_FLOATS = M * KC;       // per hi or lo
+constexpr int SBO = (KC / 4) * 128;          // bytes between 8-row groups
+constexpr int LBO = 128;                     // bytes between 16-byte K chunks
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+  // UMMA shared-memory descriptor, K-major, SWIZZLE_NONE (cute::UMMA::SmemDescriptor):
+  // [0,14) addr>>4, [16,30) LBO>>4, [32,46) SBO>>4, [46,48) version=1, [61,64) layout=0
+  return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)((LBO >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((SBO >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+__device__ __forceinline__ uint32_t instr_desc(int n) {
+  // kind::tf32, D f32 ([4,6)=1), A/B TF32 ([7,10)=2, [10,13)=2), K-major A/B,
+  // N>>3 at [17,23), M>>4 at [24,29)
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// chunks of pass p: every 16-point chunk whose rows can reach a column of the pass
+__device__ __forceinline__ int pass_chunks(int p, int np, int n_pad) {
+  const int end = min(n_pad, (p + 1) * np);
+  return end / KC;
+}
+
+}  // namespace tc
+
+__global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const VarianceArgs a, int one_pass) {
+  using namespace tc;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const GroupDev& G = a.g;
+  const int n = a.n, n_pad = G.tc_npad, NP = G.tc_np, n_pass = G.tc_npass;
+  // ---- shared memory carve-up (1024-aligned operand stages)
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<size_t>(smem_raw) + 1023) & ~(size_t)1023);
+  float* sA = reinterpret_cast<float*>(base);                                   // [S][2][M*KC]
+  float* sB = sA + STAGES * 2 * A_STAGE_FLOATS;                                 // [S][2][NP*KC]
+  float* zs = sB + (size_t)STAGES * 2 * NP * KC;                                 // [4][n_pad]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(zs + 4 * n_pad);                  // 8-aligned
+  uint64_t* full_a = bars;
+  uint64_t* full_b = bars + STAGES;
+  uint64_t* empty = bars + 2 * STAGES;
+  uint64_t* tfull = bars + 3 * STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_tiles = (int)((a.KT + M - 1) / M);
+  const uint32_t tmem_cols = NP <= 32 ? 32 : NP <= 64 ? 64 : NP <= 128 ? 128 : NP <= 256 ? 256 : 512;
+
+  for (int i = threadIdx.x; i < 4 * n_pad; i += blockDim.x) {
+    const int d = i / n_pad, j = i % n_pad;
+    zs[i] = j < n ? G.zs32[(size_t)d * n + j] : 0.f;
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(smem_u32(&full_a[s]), 4);  // one arrival per producer warp
+      mbar_init(smem_u32(&full_b[s]), 1);  // expect_tx arrival + bytes
+      mbar_init(smem_u32(&empty[s]), 1);   // tcgen05.commit
+    }
+    mbar_init(smem_u32(tfull), 1);
+    mbar_init(smem_u32(tempty), 4);        // one arrival per epilogue warp
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- B producer: one bulk copy (hi + lo) per chunk
+    uint32_t it = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      int chunk0 = 0;
+      for (int p = 0; p < n_pass; ++p) {
+        const int nk = pass_chunks(p, NP, n_pad);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(smem_u32(&empty[s]), ph ^ 1);
+          const int4 meta = G.tc_meta[chunk0 + kb];
+          const uint32_t bytes = (uint32_t)meta.y * KC * 4 * 2;
+          mbar_arrive_tx(smem_u32(&full_b[s]), bytes);
+          bulk_g2s(smem_u32(sB + (size_t)s * 2 * NP * KC), G.tc_b + meta.x, bytes, smem_u32(&full_b[s]));
+        }
+        chunk0 += nk;
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer (single thread)
+    uint32_t it = 0, uc = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      int chunk0 = 0;
+      for (int p = 0; p < n_pass; ++p, ++uc) {
+        mbar_wait(smem_u32(tempty), (uc & 1) ^ 1);  // epilogue drained the accumulator
+        tc_after();
+        const int nk = pass_chunks(p, NP, n_pad);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(smem_u32(&full_a[s]), ph);
+          mbar_wait(smem_u32(&full_b[s]), ph);
+          tc_after();
+          const int4 meta = G.tc_meta[chunk0 + kb];
+          const int ncols = meta.y, col0 = meta.z;
+          const uint32_t a_hi = smem_u32(sA + (size_t)s * 2 * A_STAGE_FLOATS);
+          const uint32_t a_lo = a_hi + A_STAGE_FLOATS * 4;
+          const uint32_t b_hi = smem_u32(sB + (size_t)s * 2 * NP * KC);
+          const uint32_t b_lo = b_hi + (uint32_t)ncols * KC * 4;
+#pragma unroll
+          for (int kk = 0; kk < KC / 8; ++kk) {
+            for (int c = 0; c < ncols; c += 256) {
+              const int nn = min(256, ncols - c);
+              const uint32_t idesc = instr_desc(nn);
+              const uint32_t d = tmem_base + (uint32_t)(col0 + c);
+              const uint32_t aoff = kk * 256;                        // two 16-byte K chunks per K=8 step
+              const uint32_t boff = (uint32_t)(c / 8) * SBO + kk * 256;
+              const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
+              mma_tf32(d, smem_desc(a_hi + aoff), smem_desc(b_hi + boff), idesc, acc0);
+              if (!one_pass) {
+                mma_tf32(d, smem_desc(a_hi + aoff), smem_desc(b_lo + boff), idesc, 1u);
+                mma_tf32(d, smem_desc(a_lo + aoff), smem_desc(b_hi + boff), idesc, 1u);
+              }
+            }
+          }
+          mma_commit(smem_u32(&empty[s]));  // frees the stage once these MMAs complete
+        }
+        mma_commit(smem_u32(tfull));  // accumulator of this pass ready
+        chunk0 += nk;
+      }
+    }
+  } else if (warp >= 8) {
+    // ---------------- A producers: k* rows, hi/lo TF32 split, canonical layout
+    const int m = threadIdx.x - 256;  // tile row == TMEM lane
+    uint32_t it = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      const long long q = (long long)tile * M + m;
+      const bool valid = q < a.KT;
+      float4 qv = valid ? a.queries[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float q0 = qv.x / (float)G.ls[0], q1 = qv.y / (float)G.ls[1];
+      const float q2 = qv.z / (float)G.ls[2], q3 = qv.w / (float)G.ls[3];
+      const float lsv = (float)G.log_sv;
+      for (int p = 0; p < n_pass; ++p) {
+        const int nk = pass_chunks(p, NP, n_pad);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(smem_u32(&empty[s]), ph ^ 1);
+          float* ahi = sA + (size_t)s * 2 * A_STAGE_FLOATS;
+          float* alo = ahi + A_STAGE_FLOATS;
+          const int row_off = (m >> 3) * (SBO / 4) + (m & 7) * 4;
+#pragma unroll
+          for (int c = 0; c < KC / 4; ++c) {
+            float hi[4], lo[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int i = kb * KC + c * 4 + e;
+              float kv = 0.f;
+              if (valid && i < n) {
+                const float d0 = q0 - zs[i], d1 = q1 - zs[n_pad + i];
+                const float d2 = q2 - zs[2 * n_pad + i], d3 = q3 - zs[3 * n_pad + i];
+                kv = expf(lsv - 0.5f * (d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3));
+              }
+              hi[e] = tf32_rna(kv);
+              lo[e] = tf32_rna(kv - hi[e]);
+            }
+            *reinterpret_cast<float4*>(ahi + row_off + c * 32) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+            *reinterpret_cast<float4*>(alo + row_off + c * 32) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+          }
+          fence_proxy_async();  // generic-proxy smem writes -> visible to tcgen05 (async proxy)
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&full_a[s]));
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: TMEM -> Σ a_j^2 -> var
+    const int e = warp - 4;  // TMEM lanes 32e..32e+31 (warp % 4 == e)
+    const int m = e * 32 + lane;
+    uint32_t uc = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      double ssq = 0.0;
+      for (int p = 0; p < n_pass; ++p, ++uc) {
+        const int npw = min(NP, n_pad - p * NP);
+        mbar_wait(smem_u32(tfull), uc & 1);
+        tc_after();
+        for (int c = 0; c < npw; c += 16) {
+          float v[16];
+          tmem_ld16(tmem_base + ((uint32_t)(e * 32) << 16) + (uint32_t)c, v);
+          float part = 0.f;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) part = fmaf(v[i], v[i], part);
+          ssq += (double)part;
+        }
+        tc_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(tempty));
+      }
+      const long long q = (long long)tile * M + m;
+      if (q < a.KT) {
+        double var = G.sv - ssq;  // gp.cpp:187-191
+        var = var > 0.0 ? var : 0.0;
+        const double c = a.coef * var;
+        a.trace[q] = a.accumulate ? a.trace[q] + c : c;
+      }
+    }
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols)
+                 : "memory");
+}
+
+size_t tc_smem_bytes(const GroupDev& g) {
+  size_t b = 1024;  // alignment slack
+  b += sizeof(float) * (size_t)tc::STAGES * 2 * tc::A_STAGE_FLOATS;
+  b += sizeof(float) * (size_t)tc::STAGES * 2 * g.tc_np * tc::KC;
+  b += sizeof(float) * (size_t)4 * g.tc_npad;
+  b += sizeof(uint64_t) * (3 * tc::STAGES + 2) + 16;
+  return b;
+}
+
+cudaError_t launch_tc_variance(const VarianceArgs& a, int one_pass, cudaStream_t st) {
+  if (!a.g.tc_b || !a.g.tc_meta) return cudaErrorNotSupported;
+  const size_t smem = tc_smem_bytes(a.g);
+  cudaError_t e = cudaFuncSetAttribute(variance_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long tiles = (a.KT + tc::M - 1) / tc::M;
+  const int grid = (int)(tiles < sms ? tiles : sms);
+  variance_tc_kernel<<<grid, tc::THREADS, smem, st>>>(a, one_pass);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// Host: L^{-T} (n×n FP64, row-major, upper) → per-(pass, chunk) TF32 hi/lo blocks
+// in the UMMA K-major canonical layout ((8,n),(4,KC/4)) with SBO=(KC/4)·128 B, LBO=128 B.
+void build_tc_operand(const double* ilt, int n, std::vector<float>& data, std::vector<int4>& meta,
+                      int& n_pad, int& np, int& n_pass) {
+  const int KC = tc::KC;
+  n_pad = (n + 15) / 16 * 16;
+  np = n_pad < 512 ? n_pad : 512;
+  n_pass = (n_pad + np - 1) / np;
+  auto tf32 = [](float x) {
+    uint32_t u;
+    std::memcpy(&u, &x, 4);
+    if ((u & 0x7f800000u) != 0x7f800000u) {
+      u += 0xFFFu + ((u >> 13) & 1u);
+      u &= 0xFFFFE000u;
+    }
+    float r;
+    std::memcpy(&r, &u, 4);
+    return r;
+  };
+  data.clear();
+  meta.clear();
+  for (int p = 0; p < n_pass; ++p) {
+    const int npw = std::min(np, n_pad - p * np);
+    const int nk = std::min(n_pad, (p + 1) * np) / KC;
+    for (int kb = 0; kb < nk; ++kb) {
+      const int col0 = std::max(0, kb * KC - p * np);
+      const int ncols = npw - col0;
+      const size_t off = data.size();
+      data.resize(off + (size_t)2 * ncols * KC, 0.f);
+      float* hi = data.data() + off;
+      float* lo = hi + (size_t)ncols * KC;
+      for (int r = 0; r < ncols; ++r) {
+        const int j = p * np + col0 + r;
+        for (int k = 0; k < KC; ++k) {
+          const int i = kb * KC + k;
+          const double v = (i < n && j < n) ? ilt[(size_t)i * n + j] : 0.0;
+          const float h = tf32((float)v);
+          const float l = tf32((float)(v - (double)h));
+          const size_t o = (size_t)(r >> 3) * (KC / 4) * 32 + (size_t)(k >> 2) * 32 + (r & 7) * 4 + (k & 3);
+          hi[o] = h;
+          lo[o] = l;
+        }
+      }
+      meta.push_back(make_int4((int)off, ncols, col0, 0));
+    }
+  }
+}
+
 }  // namespace gpm

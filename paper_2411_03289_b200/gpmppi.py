@@ -300,6 +300,14 @@ class GpModel:
         A.check(A.lib().gpmppi_model_predict_batch(self._h, A.dptr(Q), S, A.dptr(mean), A.dptr(var)))
         return mean, var
 
+    def variance_batch(self, queries, path: int):
+        """Per-group variance through a solve variance path (VAR_FFMA / VAR_TC_*)."""
+        Q = _f64(queries, (-1, 4))
+        out = np.empty((Q.shape[0], self.n_groups()))
+        A.check(A.lib().gpmppi_model_variance_batch(self._h, A.dptr(Q), Q.shape[0], path,
+                                                    A.dptr(out)))
+        return out
+
     def predict(self, query):
         q = _f64(query, (1, 4))
         if not np.isfinite(q).all():

@@ -28,7 +28,7 @@ def oracle_task(w, obstacles):
                        obstacles=obstacles if len(obstacles) else None, goal=(8.0, 0.0, 0.5))
 
 
-def build_pair(w, gp_seed=0, samples=None, threads=0):
+def build_pair(w, gp_seed=0, samples=None, threads=0, var_path=None):
     """Returns (oracle_planner, device_planner, oracle_task, device_task, gp_data)."""
     import paper_2411_03289_b200 as G
     K = samples or w.samples
@@ -45,6 +45,8 @@ def build_pair(w, gp_seed=0, samples=None, threads=0):
         po = O.Planner(K, w.horizon, O.ORC_MODEL_GP, gp_o, w.terrains, lam=w.lam,
                        sigma_sim=w.sigma_sim, seed=w.seed, threads=threads, p_x=w.p_x)
         pd = G.Planner(cfg, G.GpEnsemble(gp_d, w.terrains), p_x=w.p_x)
+        if var_path is not None:
+            pd.set_variance_path(var_path)
     else:
         kind_o = {"nominal": O.ORC_MODEL_NOMINAL, "unicycle": O.ORC_MODEL_UNICYCLE,
                   "edd5": O.ORC_MODEL_EDD5}[w.model]

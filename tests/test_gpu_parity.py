@@ -17,8 +17,8 @@ from tests.helpers import (COST_ATOL, SEQ_ATOL, TIGHT_RTOL, assert_tick_parity, 
 pytestmark = pytest.mark.gpu
 
 
-def _run_ticks(w, ticks=3, samples=None, philox=False, gp_seed=0, flags_exact=True):
-    po, pd, to, td, _ = build_pair(w, gp_seed=gp_seed, samples=samples)
+def _run_ticks(w, ticks=3, samples=None, philox=False, gp_seed=0, flags_exact=True, var_path=None):
+    po, pd, to, td, _ = build_pair(w, gp_seed=gp_seed, samples=samples, var_path=var_path)
     K, T = po.K, po.T
     x = np.array(w.x0, dtype=np.float64)
     for t in range(ticks):
@@ -110,6 +110,17 @@ def test_config2_shape_reduced_K_injected_reference_noise(task):
     w = dataclasses.replace(W.CONFIGS["config2"], task=task, track="lane" if task != "tracking" else "circle",
                             x0=(0.0, 0.0, 0.0, 0.0, 0.0) if task != "tracking" else (2.0, 0.0, np.pi / 2, 0.0, 0.0))
     _run_ticks(w, ticks=3, samples=512)
+
+
+@pytest.mark.parametrize("var_path", [0, 1])
+def test_config2_variance_paths_parity(var_path):
+    """FFMA and tcgen05 3xTF32 variance paths both meet the stated cost tolerance."""
+    _run_ticks(W.CONFIGS["config2"], ticks=2, samples=2048, var_path=var_path)
+
+
+def test_config3_shape_parity_tc():
+    """n=2048, T=60 multi-terrain (BASELINE config 3 shape) at reduced K, 3xTF32 variance."""
+    _run_ticks(W.CONFIGS["config3"], ticks=1, samples=512, var_path=1)
 
 
 def test_config2_philox_noise_parity():

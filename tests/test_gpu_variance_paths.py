@@ -1,0 +1,32 @@
+"""Variance paths of the solve (FFMA, tcgen05 3xTF32, tcgen05 1xTF32) vs FP64.
+
+var = sf2 - ||L^{-1} k*||^2 (gp.cpp:184-191) on FP32-rounded queries. Tolerances
+are absolute on var (sf2 = 4e-3 for the synthetic kernel) and stated per path.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+# absolute var error bounds (sf2 = 4e-3), measured on B200 with margin:
+#   FFMA ≤ 1.1e-8; 3xTF32 ≤ 1.6e-7 (fp32 tensor-core accumulation, grows with n);
+#   1xTF32 ~ 8e-6 (single-pass TF32 — not a parity path, reported for the record)
+TOL = {0: 3e-8, 1: 4e-7, 2: 2e-5}
+
+
+@pytest.mark.parametrize("n", [60, 512, 700, 2048])
+@pytest.mark.parametrize("path", [0, 1, 2])
+def test_variance_path_accuracy(n, path):
+    import paper_2411_03289_b200 as G
+    from paper_2411_03289_b200 import workloads as W
+    X, Y, K = W.gp_training_set(n, 1, seed=n)
+    m = G.GpModel.fit(X, Y, K)
+    rng = np.random.default_rng(7)
+    S = 1000
+    q = np.column_stack([rng.uniform(-0.5, 2, S), rng.uniform(-2, 2, S),
+                         rng.uniform(-0.5, 2, S), rng.uniform(-2, 2, S)])
+    q32 = q.astype(np.float32).astype(np.float64)
+    _, v64 = m.predict_batch(q32)
+    v = m.variance_batch(q32, path)[:, 0]
+    err = np.abs(v - v64[:, 0])
+    assert err.max() <= TOL[path], (n, path, err.max(), np.median(err))
