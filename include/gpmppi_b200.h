@@ -217,6 +217,9 @@ int gpmppi_planner_io_bytes(const gpmppi_planner* p, int64_t* h2d, int64_t* d2h)
  * doubles) to a DEVICE buffer; the caller all-gathers the tuples (NCCL) and
  * plan_finish combines them in rank order, updates/shifts the sequence, runs
  * the tightening pass and returns the command. */
+/* diagnostics: per-role cycle counters of the tensor-core variance kernel,
+ * filled when GPMPPI_TC_DEBUG has bit 512 set; read-and-reset */
+int gpmppi_debug_tc_profile(double* out16);
 int gpmppi_tuple_doubles(int horizon);
 int gpmppi_planner_set_shard(gpmppi_planner* p, int64_t begin, int64_t count);
 int gpmppi_planner_plan_partial(gpmppi_planner* p, const double x0[5], const gpmppi_task* task,

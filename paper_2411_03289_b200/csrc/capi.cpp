@@ -1160,6 +1160,10 @@ int gpmppi_planner_io_bytes(const gpmppi_planner* p, int64_t* h2d, int64_t* d2h)
   return GPMPPI_OK;
 }
 
+int gpmppi_debug_tc_profile(double* out16) {
+  return guarded([&] { gpm::tc_profile_read(out16); });
+}
+
 int gpmppi_tuple_doubles(int horizon) { return gpm::tuple_doubles(horizon); }
 
 int gpmppi_planner_set_shard(gpmppi_planner* p, int64_t begin, int64_t count) {

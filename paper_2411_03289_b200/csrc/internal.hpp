@@ -135,6 +135,7 @@ int reduce_blocks_for(int K_local, int num_sms);
 int tighten_splits(int n);
 void build_tc_operand(const double* ilt, int n, std::vector<float>& data, std::vector<int4>& meta,
                       int& n_pad, int& np, int& n_pass);
+void tc_profile_read(double* out);
 void count_launch(int n = 1);
 unsigned long long launches_total();
 

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -31,8 +32,10 @@ namespace tc {
 
 constexpr int M = 128;      // queries per tile (UMMA M, TMEM lanes)
 constexpr int KC = 16;      // points per K chunk (two K=8 TF32 MMAs)
-constexpr int STAGES = 2;
-constexpr int THREADS = 384;
+constexpr int STAGES_A = 4; // k* ring, max (16 KB per stage: hi + lo); 3 when n is large
+constexpr int STAGES_B = 2; // L^{-T} ring (<= 64 KB per stage)
+constexpr int PRODUCER_WARPS = 8;
+constexpr int THREADS = 256 + 32 * PRODUCER_WARPS;
 constexpr int A_STAGE_FLOATS = M * KC;       // per hi or lo
 constexpr int SBO = (KC / 4) * 128;          // bytes between 8-row groups
 constexpr int LBO = 128;                     // bytes between 16-byte K chunks
@@ -103,10 +106,15 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                : "memory");
 }
+__device__ __forceinline__ float exp2f_approx(float x) {  // MUFU.EX2, ~2 ulp
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 __device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+  // round-to-nearest (ties away) to 10 mantissa bits on the ALU pipe (cvt.rna.tf32
+  // would occupy the XU pipe that the exponentials need); finite inputs only
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   uint32_t r[16];
@@ -120,6 +128,26 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+
+// per-role cycle counters (diagnostics, env GPMPPI_TC_DEBUG bit 512)
+__device__ unsigned long long g_prof[16];
+__device__ __forceinline__ void prof_add(int slot, unsigned long long v, int dbg) {
+  if (dbg & 512) atomicAdd(&g_prof[slot], v);
+}
+__device__ __forceinline__ void mbar_wait_prof(uint32_t bar, uint32_t parity, int slot, int dbg) {
+  const unsigned long long t0 = clock64();
+  while (!mbar_try_wait(bar, parity)) {
+  }
+  prof_add(slot, clock64() - t0, dbg);
+}
+
 // chunks of pass p: every 16-point chunk whose rows can reach a column of the pass
 __device__ __forceinline__ int pass_chunks(int p, int np, int n_pad) {
   const int end = min(n_pad, (p + 1) * np);
@@ -128,21 +156,26 @@ __device__ __forceinline__ int pass_chunks(int p, int np, int n_pad) {
 
 }  // namespace tc
 
-__global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const VarianceArgs a, int one_pass) {
+// dbg (diagnostics only, env GPMPPI_TC_DEBUG): 1 = skip B copies, 2 = skip k* math,
+// 4 = skip MMAs, 8 = skip TMEM reads. Results are garbage when set.
+__global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const VarianceArgs a, int one_pass, int dbg,
+                                                                  int SA) {
   using namespace tc;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const GroupDev& G = a.g;
   const int n = a.n, n_pad = G.tc_npad, NP = G.tc_np, n_pass = G.tc_npass;
-  // ---- shared memory carve-up (1024-aligned operand stages)
-  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<size_t>(smem_raw) + 1023) & ~(size_t)1023);
-  float* sA = reinterpret_cast<float*>(base);                                   // [S][2][M*KC]
-  float* sB = sA + STAGES * 2 * A_STAGE_FLOATS;                                 // [S][2][NP*KC]
-  float* zs = sB + (size_t)STAGES * 2 * NP * KC;                                 // [4][n_pad]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(zs + 4 * n_pad);                  // 8-aligned
+  // ---- shared memory carve-up. Align with pointer arithmetic on the shared array
+  // (a size_t round trip turns every access into a generic LD/ST).
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  float* sA = reinterpret_cast<float*>(base);                  // [SA][2][M*KC]
+  float* sB = sA + SA * 2 * A_STAGE_FLOATS;              // [SB][2][NP*KC]
+  float* zs = sB + (size_t)STAGES_B * 2 * NP * KC;             // [5][n_pad] log2e-scaled aug. inputs
+  uint64_t* bars = reinterpret_cast<uint64_t*>(zs + 5 * n_pad);
   uint64_t* full_a = bars;
-  uint64_t* full_b = bars + STAGES;
-  uint64_t* empty = bars + 2 * STAGES;
-  uint64_t* tfull = bars + 3 * STAGES;
+  uint64_t* empty_a = full_a + SA;
+  uint64_t* full_b = empty_a + SA;
+  uint64_t* empty_b = full_b + STAGES_B;
+  uint64_t* tfull = empty_b + STAGES_B;
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
 
@@ -150,18 +183,30 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
   const int n_tiles = (int)((a.KT + M - 1) / M);
   const uint32_t tmem_cols = NP <= 32 ? 32 : NP <= 64 ? 64 : NP <= 128 ? 128 : NP <= 256 ? 256 : 512;
 
-  for (int i = threadIdx.x; i < 4 * n_pad; i += blockDim.x) {
-    const int d = i / n_pad, j = i % n_pad;
-    zs[i] = j < n ? G.zs32[(size_t)d * n + j] : 0.f;
+  // exponent in base 2: log2(k*) = q'·z' + qn' + zn'  with z' = log2e·z/l, zn' = log2e·(-|z/l|²/2 + ln sf2)
+  const float L2E = 1.4426950408889634f;
+  for (int i = threadIdx.x; i < n_pad; i += blockDim.x) {
+    float z[4], sq = 0.f;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      z[d] = i < n ? G.zs32[(size_t)d * n + i] : 0.f;
+      sq += z[d] * z[d];
+    }
+#pragma unroll
+    for (int d = 0; d < 4; ++d) zs[d * n_pad + i] = L2E * z[d];
+    zs[4 * n_pad + i] = i < n ? L2E * (-0.5f * sq + (float)G.log_sv) : -1e30f;  // padded points: k* = 0
   }
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(smem_u32(&full_a[s]), 4);  // one arrival per producer warp
-      mbar_init(smem_u32(&full_b[s]), 1);  // expect_tx arrival + bytes
-      mbar_init(smem_u32(&empty[s]), 1);   // tcgen05.commit
+    for (int s = 0; s < SA; ++s) {
+      mbar_init(smem_u32(&full_a[s]), PRODUCER_WARPS);
+      mbar_init(smem_u32(&empty_a[s]), 1);
+    }
+    for (int s = 0; s < STAGES_B; ++s) {
+      mbar_init(smem_u32(&full_b[s]), 1);
+      mbar_init(smem_u32(&empty_b[s]), 1);
     }
     mbar_init(smem_u32(tfull), 1);
-    mbar_init(smem_u32(tempty), 4);        // one arrival per epilogue warp
+    mbar_init(smem_u32(tempty), 4);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -174,6 +219,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
   __syncthreads();
   tc_after();
   const uint32_t tmem_base = *tmem_slot;
+  const unsigned long long t_start = clock64();
 
   if (warp == 0 && lane == 0) {
     // ---------------- B producer: one bulk copy (hi + lo) per chunk
@@ -183,37 +229,40 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
       for (int p = 0; p < n_pass; ++p) {
         const int nk = pass_chunks(p, NP, n_pad);
         for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = it % STAGES;
-          const uint32_t ph = (it / STAGES) & 1;
-          mbar_wait(smem_u32(&empty[s]), ph ^ 1);
+          const int s = it % STAGES_B;
+          const uint32_t ph = (it / STAGES_B) & 1;
+          if (!(dbg & 64)) mbar_wait_prof(smem_u32(&empty_b[s]), ph ^ 1, 0, dbg);
           const int4 meta = G.tc_meta[chunk0 + kb];
           const uint32_t bytes = (uint32_t)meta.y * KC * 4 * 2;
-          mbar_arrive_tx(smem_u32(&full_b[s]), bytes);
-          bulk_g2s(smem_u32(sB + (size_t)s * 2 * NP * KC), G.tc_b + meta.x, bytes, smem_u32(&full_b[s]));
+          if (dbg & 1) {
+            mbar_arrive(smem_u32(&full_b[s]));
+          } else {
+            mbar_arrive_tx(smem_u32(&full_b[s]), bytes);
+            bulk_g2s(smem_u32(sB + (size_t)s * 2 * NP * KC), G.tc_b + meta.x, bytes, smem_u32(&full_b[s]));
+          }
         }
         chunk0 += nk;
       }
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer (single thread)
-    uint32_t it = 0, uc = 0;
+    uint32_t ia = 0, ib = 0, uc = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       int chunk0 = 0;
       for (int p = 0; p < n_pass; ++p, ++uc) {
-        mbar_wait(smem_u32(tempty), (uc & 1) ^ 1);  // epilogue drained the accumulator
+        mbar_wait_prof(smem_u32(tempty), (uc & 1) ^ 1, 1, dbg);  // epilogue drained the accumulator
         tc_after();
         const int nk = pass_chunks(p, NP, n_pad);
-        for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = it % STAGES;
-          const uint32_t ph = (it / STAGES) & 1;
-          mbar_wait(smem_u32(&full_a[s]), ph);
-          mbar_wait(smem_u32(&full_b[s]), ph);
+        for (int kb = 0; kb < nk; ++kb, ++ia, ++ib) {
+          const int sa = ia % SA, sb = ib % STAGES_B;
+          if (!(dbg & 16)) mbar_wait_prof(smem_u32(&full_a[sa]), (ia / SA) & 1, 2, dbg);
+          if (!(dbg & 32)) mbar_wait_prof(smem_u32(&full_b[sb]), (ib / STAGES_B) & 1, 3, dbg);
           tc_after();
           const int4 meta = G.tc_meta[chunk0 + kb];
           const int ncols = meta.y, col0 = meta.z;
-          const uint32_t a_hi = smem_u32(sA + (size_t)s * 2 * A_STAGE_FLOATS);
+          const uint32_t a_hi = smem_u32(sA + (size_t)sa * 2 * A_STAGE_FLOATS);
           const uint32_t a_lo = a_hi + A_STAGE_FLOATS * 4;
-          const uint32_t b_hi = smem_u32(sB + (size_t)s * 2 * NP * KC);
+          const uint32_t b_hi = smem_u32(sB + (size_t)sb * 2 * NP * KC);
           const uint32_t b_lo = b_hi + (uint32_t)ncols * KC * 4;
 #pragma unroll
           for (int kk = 0; kk < KC / 8; ++kk) {
@@ -224,6 +273,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
               const uint32_t aoff = kk * 256;                        // two 16-byte K chunks per K=8 step
               const uint32_t boff = (uint32_t)(c / 8) * SBO + kk * 256;
               const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
+              if (dbg & 4) continue;
               mma_tf32(d, smem_desc(a_hi + aoff), smem_desc(b_hi + boff), idesc, acc0);
               if (!one_pass) {
                 mma_tf32(d, smem_desc(a_hi + aoff), smem_desc(b_lo + boff), idesc, 1u);
@@ -231,15 +281,19 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
               }
             }
           }
-          mma_commit(smem_u32(&empty[s]));  // frees the stage once these MMAs complete
+          mma_commit(smem_u32(&empty_a[sa]));  // stages free once these MMAs complete
+          mma_commit(smem_u32(&empty_b[sb]));
         }
         mma_commit(smem_u32(tfull));  // accumulator of this pass ready
         chunk0 += nk;
       }
     }
   } else if (warp >= 8) {
-    // ---------------- A producers: k* rows, hi/lo TF32 split, canonical layout
-    const int m = threadIdx.x - 256;  // tile row == TMEM lane
+    // ---------------- A producers: k* rows, hi/lo TF32 split, canonical layout.
+    // Two warps per 32 rows: warp half h produces K sub-chunks 2h and 2h+1.
+    const int pw = warp - 8;
+    const int m = (pw & 3) * 32 + lane;  // tile row == TMEM lane
+    const int h = pw >> 2;
     uint32_t it = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       const long long q = (long long)tile * M + m;
@@ -247,35 +301,37 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
       float4 qv = valid ? a.queries[q] : make_float4(0.f, 0.f, 0.f, 0.f);
       const float q0 = qv.x / (float)G.ls[0], q1 = qv.y / (float)G.ls[1];
       const float q2 = qv.z / (float)G.ls[2], q3 = qv.w / (float)G.ls[3];
-      const float lsv = (float)G.log_sv;
+      const float qn = valid ? -0.5f * L2E * (q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3) : -1e30f;
       for (int p = 0; p < n_pass; ++p) {
         const int nk = pass_chunks(p, NP, n_pad);
         for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = it % STAGES;
-          const uint32_t ph = (it / STAGES) & 1;
-          mbar_wait(smem_u32(&empty[s]), ph ^ 1);
+          const int s = it % SA;
+          const uint32_t ph = (it / SA) & 1;
+          if (lane == 0 && !(dbg & 64)) mbar_wait_prof(smem_u32(&empty_a[s]), ph ^ 1, 4, dbg);
+          __syncwarp();
           float* ahi = sA + (size_t)s * 2 * A_STAGE_FLOATS;
           float* alo = ahi + A_STAGE_FLOATS;
           const int row_off = (m >> 3) * (SBO / 4) + (m & 7) * 4;
 #pragma unroll
-          for (int c = 0; c < KC / 4; ++c) {
+          for (int cc = 0; cc < 2; ++cc) {
+            const int c = 2 * h + cc;
             float hi[4], lo[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int i = kb * KC + c * 4 + e;
-              float kv = 0.f;
-              if (valid && i < n) {
-                const float d0 = q0 - zs[i], d1 = q1 - zs[n_pad + i];
-                const float d2 = q2 - zs[2 * n_pad + i], d3 = q3 - zs[3 * n_pad + i];
-                kv = expf(lsv - 0.5f * (d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3));
-              }
+              float x = fmaf(q0, zs[i], fmaf(q1, zs[n_pad + i], fmaf(q2, zs[2 * n_pad + i],
+                             fmaf(q3, zs[3 * n_pad + i], qn + zs[4 * n_pad + i]))));
+              if (dbg & 2) x = -1e30f;
+              const float kv = exp2f_approx(x);
               hi[e] = tf32_rna(kv);
-              lo[e] = tf32_rna(kv - hi[e]);
+              lo[e] = kv - hi[e];  // low 13 bits are truncated by the tensor core
             }
-            *reinterpret_cast<float4*>(ahi + row_off + c * 32) = make_float4(hi[0], hi[1], hi[2], hi[3]);
-            *reinterpret_cast<float4*>(alo + row_off + c * 32) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+            if (!(dbg & 256)) {
+              *reinterpret_cast<float4*>(ahi + row_off + c * 32) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+              *reinterpret_cast<float4*>(alo + row_off + c * 32) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+            }
           }
-          fence_proxy_async();  // generic-proxy smem writes -> visible to tcgen05 (async proxy)
+          if (!(dbg & 128)) fence_proxy_async();  // generic-proxy smem writes -> visible to tcgen05
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(&full_a[s]));
         }
@@ -290,11 +346,26 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
       double ssq = 0.0;
       for (int p = 0; p < n_pass; ++p, ++uc) {
         const int npw = min(NP, n_pad - p * NP);
-        mbar_wait(smem_u32(tfull), uc & 1);
+        if (lane == 0) mbar_wait_prof(smem_u32(tfull), uc & 1, 5, dbg);
+        __syncwarp();
         tc_after();
-        for (int c = 0; c < npw; c += 16) {
+        const uint32_t trow = tmem_base + ((uint32_t)(e * 32) << 16);
+        int c = (dbg & 8) ? npw : 0;
+        for (; c + 64 <= npw; c += 64) {  // four loads in flight per wait
+          uint32_t r[64];
+          tmem_ld16_nowait(trow + c, r);
+          tmem_ld16_nowait(trow + c + 16, r + 16);
+          tmem_ld16_nowait(trow + c + 32, r + 32);
+          tmem_ld16_nowait(trow + c + 48, r + 48);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          float part = 0.f;
+#pragma unroll
+          for (int i = 0; i < 64; ++i) part = fmaf(__uint_as_float(r[i]), __uint_as_float(r[i]), part);
+          ssq += (double)part;
+        }
+        for (; c < npw; c += 16) {
           float v[16];
-          tmem_ld16(tmem_base + ((uint32_t)(e * 32) << 16) + (uint32_t)c, v);
+          tmem_ld16(trow + c, v);
           float part = 0.f;
 #pragma unroll
           for (int i = 0; i < 16; ++i) part = fmaf(v[i], v[i], part);
@@ -313,6 +384,11 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
       }
     }
   }
+  if (lane == 0) {
+    const int slot = warp == 0 ? 6 : warp == 1 ? 7 : warp >= 8 ? 8 : warp >= 4 ? 9 : 10;
+    prof_add(slot, clock64() - t_start, dbg);
+    if (warp == 1) prof_add(11, 1, dbg);
+  }
   tc_before();
   __syncthreads();
   tc_after();
@@ -321,18 +397,28 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
                  : "memory");
 }
 
-size_t tc_smem_bytes(const GroupDev& g) {
+size_t tc_smem_bytes(const GroupDev& g, int stages_a) {
   size_t b = 1024;  // alignment slack
-  b += sizeof(float) * (size_t)tc::STAGES * 2 * tc::A_STAGE_FLOATS;
-  b += sizeof(float) * (size_t)tc::STAGES * 2 * g.tc_np * tc::KC;
-  b += sizeof(float) * (size_t)4 * g.tc_npad;
-  b += sizeof(uint64_t) * (3 * tc::STAGES + 2) + 16;
+  b += sizeof(float) * (size_t)stages_a * 2 * tc::A_STAGE_FLOATS;
+  b += sizeof(float) * (size_t)tc::STAGES_B * 2 * g.tc_np * tc::KC;
+  b += sizeof(float) * (size_t)5 * g.tc_npad;
+  b += sizeof(uint64_t) * (2 * stages_a + 2 * tc::STAGES_B + 2) + 16;
   return b;
+}
+
+void tc_profile_read(double* out) {
+  unsigned long long h[16];
+  cudaMemcpyFromSymbol(h, tc::g_prof, sizeof h);
+  for (int i = 0; i < 16; ++i) out[i] = (double)h[i];
+  unsigned long long z[16] = {};
+  cudaMemcpyToSymbol(tc::g_prof, z, sizeof z);
 }
 
 cudaError_t launch_tc_variance(const VarianceArgs& a, int one_pass, cudaStream_t st) {
   if (!a.g.tc_b || !a.g.tc_meta) return cudaErrorNotSupported;
-  const size_t smem = tc_smem_bytes(a.g);
+  int SA = tc::STAGES_A;
+  while (SA > 2 && tc_smem_bytes(a.g, SA) > 227 * 1024) --SA;
+  const size_t smem = tc_smem_bytes(a.g, SA);
   cudaError_t e = cudaFuncSetAttribute(variance_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
@@ -340,7 +426,12 @@ cudaError_t launch_tc_variance(const VarianceArgs& a, int one_pass, cudaStream_t
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long tiles = (a.KT + tc::M - 1) / tc::M;
   const int grid = (int)(tiles < sms ? tiles : sms);
-  variance_tc_kernel<<<grid, tc::THREADS, smem, st>>>(a, one_pass);
+  static int dbg = -1;
+  if (dbg < 0) {
+    const char* e = getenv("GPMPPI_TC_DEBUG");
+    dbg = e ? atoi(e) : 0;
+  }
+  variance_tc_kernel<<<grid, tc::THREADS, smem, st>>>(a, one_pass, dbg, SA);
   count_launch();
   return cudaGetLastError();
 }
