@@ -485,6 +485,7 @@ struct gpmppi_planner {
   unsigned int* d_ticket = nullptr;
   int* d_infeasible = nullptr;
   double *d_tq = nullptr, *d_tmu = nullptr, *d_tJ = nullptr, *d_tvar = nullptr;
+  double* d_scratch = nullptr;
   // pinned staging
   gpm::TaskDev* h_task = nullptr;
   double* h_x0 = nullptr;
@@ -524,6 +525,7 @@ struct gpmppi_planner {
     if (model_kind == GPMPPI_MODEL_GP_ENSEMBLE) {
       d_queries = dalloc<float4>((size_t)K * T);
       d_trace = dalloc<double>((size_t)K * T);
+      if (!d_scratch) d_scratch = dalloc<double>(gpm::rollout_scratch_doubles(T, num_sms));
     }
     reduce_blocks = gpm::reduce_blocks_for((int)K, num_sms);
     d_partials = dalloc<double>((size_t)reduce_blocks * gpm::tuple_doubles(T));
@@ -708,6 +710,7 @@ void enqueue_samples(gpmppi_planner* p, int n_obs, double var_w, int finish, cud
   a.term = p->d_term;
   a.alive = p->d_alive;
   a.words = p->words;
+  a.scratch = p->d_scratch;
   if (evs) CK(cudaEventRecord(evs[0], p->stream));
   check(gpm::launch_rollout(a, p->num_sms, p->stream), "rollout kernel");
   if (evs) CK(cudaEventRecord(evs[1], p->stream));

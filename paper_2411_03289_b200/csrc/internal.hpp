@@ -60,6 +60,7 @@ struct RolloutArgs {
   uint8_t* term;
   uint8_t* alive;
   int words;  // ceil(T/32)
+  double* scratch;  // per lane-group trajectory scratch (rollout_scratch_doubles)
 };
 
 struct VarianceArgs {
@@ -131,6 +132,7 @@ cudaError_t launch_predict(const ModelDev& m, const double* q, long long S, doub
 cudaError_t launch_philox_noise(uint64_t key, long long s_begin, int K, int T, double sv,
                                 double sw, double* eps, cudaStream_t st);
 size_t rollout_smem_bytes(const RolloutArgs& a);
+size_t rollout_scratch_doubles(int T, int num_sms);
 int reduce_blocks_for(int K_local, int num_sms);
 int tighten_splits(int n);
 void build_tc_operand(const double* ilt, int n, std::vector<float>& data, std::vector<int4>& meta,

@@ -41,10 +41,46 @@ GPM_D double warp_min(double v) {
 }
 
 // -------------------------------------------------------------------------
+// FP64 exp for the GP kernel row: exp(x) = 2^(n/32)·e^r, n = rint(32x/ln2),
+// |r| <= ln2/64, degree-6 Taylor (truncation < 4e-18) and a 32-entry 2^(j/32)
+// table in shared memory. ~12 FP64 ops instead of ~22 for libm's exp, within
+// ~2 ulp of it; arguments below -700 flush to 0 (k* < 1e-304).
+__constant__ double kExp2Frac[32] = {
+    0x1.0000000000000p+0, 0x1.059b0d3158574p+0, 0x1.0b5586cf9890fp+0, 0x1.11301d0125b51p+0,
+    0x1.172b83c7d517bp+0, 0x1.1d4873168b9aap+0, 0x1.2387a6e756238p+0, 0x1.29e9df51fdee1p+0,
+    0x1.306fe0a31b715p+0, 0x1.371a7373aa9cbp+0, 0x1.3dea64c123422p+0, 0x1.44e086061892dp+0,
+    0x1.4bfdad5362a27p+0, 0x1.5342b569d4f82p+0, 0x1.5ab07dd485429p+0, 0x1.6247eb03a5585p+0,
+    0x1.6a09e667f3bcdp+0, 0x1.71f75e8ec5f74p+0, 0x1.7a11473eb0187p+0, 0x1.82589994cce13p+0,
+    0x1.8ace5422aa0dbp+0, 0x1.93737b0cdc5e5p+0, 0x1.9c49182a3f090p+0, 0x1.a5503b23e255dp+0,
+    0x1.ae89f995ad3adp+0, 0x1.b7f76f2fb5e47p+0, 0x1.c199bdd85529cp+0, 0x1.cb720dcef9069p+0,
+    0x1.d5818dcfba487p+0, 0x1.dfc97337b9b5fp+0, 0x1.ea4afa2a490dap+0, 0x1.f50765b6e4540p+0};
+constexpr double kInvLn2x32 = 0x1.71547652b82fep+5;
+constexpr double kLn2d32Hi = 0x1.62e42fee00000p-6;  // 32 significant bits: n·hi exact for |n| < 2^21
+constexpr double kLn2d32Lo = 0x1.a39ef35793c76p-38;
+GPM_D double exp_tab(double x, const double* tab) {
+  const double magic = 6755399441055744.0;  // 1.5·2^52: round-to-nearest integer trick
+  const double t = fma(x, kInvLn2x32, magic);
+  const int n = __double2loint(t);
+  const double nd = t - magic;
+  double r = fma(nd, -kLn2d32Hi, x);
+  r = fma(nd, -kLn2d32Lo, r);
+  double p = fma(r, 1.0 / 720.0, 1.0 / 120.0);
+  p = fma(r, p, 1.0 / 24.0);
+  p = fma(r, p, 1.0 / 6.0);
+  p = fma(r, p, 0.5);
+  p = fma(r, p, 1.0);
+  p *= r;  // e^r - 1
+  const double tj = tab[n & 31];
+  const double res = fma(tj, p, tj);
+  const double scaled = __hiloint2double(__double2hiint(res) + ((n >> 5) << 20), __double2loint(res));
+  return x < -700.0 ? 0.0 : scaled;
+}
+
+// -------------------------------------------------------------------------
 // Rollout, GP ensemble model. NO = max outputs per kernel group (compile time).
 size_t rollout_smem_bytes(const RolloutArgs& a) {
   size_t b = sizeof(TaskDev);
-  b += sizeof(double) * (size_t)(2 * a.T + a.T + a.T * (a.n_obs > 0 ? a.n_obs : 1) + a.R + 2);
+  b += sizeof(double) * (size_t)(2 * a.T + a.T + a.T * (a.n_obs > 0 ? a.n_obs : 1) + a.R + 2 + 32);
   b = (b + 15) & ~(size_t)15;
   if (a.model_kind == MODEL_GP)
     for (int g = 0; g < a.model.G; ++g) b += sizeof(double) * (size_t)(5 + a.model.g[g].n_out) * a.model.n;
@@ -57,7 +93,8 @@ struct SmemView {
   double* rbar;
   double* marg;
   double* tw;
-  double* pts;  // groups back to back
+  double* etab;  // 2^(j/32), j < 32
+  double* pts;   // groups back to back
 };
 
 GPM_D SmemView load_common_smem(const RolloutArgs& a, unsigned char* smem) {
@@ -72,8 +109,13 @@ GPM_D SmemView load_common_smem(const RolloutArgs& a, unsigned char* smem) {
   p += a.T * (a.n_obs > 0 ? a.n_obs : 1);
   v.tw = p;
   p += a.R + 2;
-  size_t off = (reinterpret_cast<size_t>(p) + 15) & ~(size_t)15;
-  v.pts = reinterpret_cast<double*>(off);
+  v.etab = p;
+  p += 32;
+  // 16-byte align by pointer arithmetic on the shared array (an integer round trip
+  // would turn every access into a generic LD instead of LDS)
+  size_t off = (size_t)(reinterpret_cast<unsigned char*>(p) - smem);
+  off = (off + 15) & ~(size_t)15;
+  v.pts = reinterpret_cast<double*>(smem + off);
   {  // task (plain words)
     const int nw = sizeof(TaskDev) / 8;
     const unsigned long long* src = reinterpret_cast<const unsigned long long*>(a.task);
@@ -86,6 +128,7 @@ GPM_D SmemView load_common_smem(const RolloutArgs& a, unsigned char* smem) {
   if (a.margins)
     for (int i = threadIdx.x; i < a.T * a.n_obs; i += blockDim.x) v.marg[i] = a.margins[i];
   for (int i = threadIdx.x; i < a.R; i += blockDim.x) v.tw[i] = a.tw[i];
+  for (int i = threadIdx.x; i < 32; i += blockDim.x) v.etab[i] = kExp2Frac[i];
   return v;
 }
 
@@ -110,8 +153,14 @@ GPM_D double group_sum(double v) {  // xor butterfly inside an LPS-lane group
 }
 
 // One LPS-lane group per sample (32/LPS samples per warp share every Z/alpha
-// shared-memory read); lanes split the n GP points, the dynamics and cost are
-// evaluated redundantly (bit-identically) by the group's lanes.
+// shared-memory read). The GP query of step k needs only (v_k, omega_k, u_k), so:
+//  phase 1 (serial in k): noise, clamp, GP mean k*·alpha (lanes split the n
+//          points, butterfly sum), first-order lag update of (v, omega);
+//  phase 2 (lanes split the steps k): heading recursion, FP64 sincos / exact-arc
+//          increments, x/y in step order, non-finite freeze (mppi.cpp:343-346),
+//          per-step costs and flags (costs.cpp:127-171) and their group sums.
+// Per-group trajectory scratch lives in L2 (scr, 9 arrays of T+1 doubles).
+constexpr int SCR_ARRAYS = 9;
 template <int NO, int LPS>
 __global__ void __launch_bounds__(256, 1) rollout_gp_kernel(const RolloutArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -136,6 +185,18 @@ __global__ void __launch_bounds__(256, 1) rollout_gp_kernel(const RolloutArgs a)
   const int ngroups = gridDim.x * groups_per_block;
   const int T = a.T;
   const int O = a.n_obs;
+  const int stride = T + 1;
+  double* scr = a.scratch + (size_t)gid * SCR_ARRAYS * stride;
+  double* su0 = scr;
+  double* su1 = scr + stride;
+  double* sv_ = scr + 2 * stride;
+  double* sw = scr + 3 * stride;
+  double* sth = scr + 4 * stride;
+  double* ssin = scr + 5 * stride;
+  double* scos = scr + 6 * stride;
+  double* sx = scr + 7 * stride;
+  double* sy = scr + 8 * stride;
+  const double av = a.nom.dt / a.nom.tau_v, aw = a.nom.dt / a.nom.tau_omega;
   // every lane of the warp runs the same trip count (samples beyond K are masked)
   const int rounds = (a.K_local + ngroups - 1) / ngroups;
 
@@ -143,100 +204,144 @@ __global__ void __launch_bounds__(256, 1) rollout_gp_kernel(const RolloutArgs a)
     const int sl = gid + r * ngroups;
     const bool valid = sl < a.K_local;
     const long long s = a.s_begin + (valid ? sl : 0);
-    double st[5];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) st[i] = a.x0[i];
-    bool alive = valid;
-    double cost = 0.0, decay = 1.0;
-    uint32_t vb = 0, cb = 0;
+    // ---------------- phase 1: serial (v, omega) chain with the GP mean
+    double v = a.x0[3], w = a.x0[4];
+    if (gl == 0) {
+      sv_[0] = v;
+      sw[0] = w;
+    }
     for (int k = 0; k < T; ++k) {
       double e0 = 0.0, e1 = 0.0;
       if (valid) sample_noise(a, sl, s, k, &e0, &e1);
-      const double u[2] = {clampd(sv.nom[2 * k] + e0, a.lo[0], a.hi[0]),
-                           clampd(sv.nom[2 * k + 1] + e1, a.lo[1], a.hi[1])};  // mppi.cpp:298-308
-      if (valid && gl == 0)
-        a.queries[(size_t)sl * T + k] =
-            make_float4((float)st[3], (float)st[4], (float)u[0], (float)u[1]);
-      double sp, cp;
-      sincos(st[2], &sp, &cp);
-      double nx[5];
-      // the shuffles below need every lane of the warp: no divergent exit here
-      double cm0 = 0.0, cm1 = 0.0;
-      {
-        const double* gp = sv.pts;
-        for (int g = 0; g < a.model.G; ++g) {
-          const GroupDev& G = a.model.g[g];
-          const int nout = G.n_out;
-          // gp.cpp:172-176 augmented query [q/l | -1/2|q/l|^2 | 1]
-          const double q0 = st[3] / G.ls[0], q1 = st[4] / G.ls[1];
-          const double q2 = u[0] / G.ls[2], q3 = u[1] / G.ls[3];
-          const double qn = -0.5 * (q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
-          double acc[NO];
+      const double u0 = clampd(sv.nom[2 * k] + e0, a.lo[0], a.hi[0]);  // mppi.cpp:298-308
+      const double u1 = clampd(sv.nom[2 * k + 1] + e1, a.lo[1], a.hi[1]);
+      if (valid && gl == 0) {
+        a.queries[(size_t)sl * T + k] = make_float4((float)v, (float)w, (float)u0, (float)u1);
+        su0[k] = u0;
+        su1[k] = u1;
+      }
+      double cm0 = 0.0, cm1 = 0.0;  // combine_terrains (mppi.cpp:34-49)
+      const double* gp = sv.pts;
+      for (int g = 0; g < a.model.G; ++g) {
+        const GroupDev& G = a.model.g[g];
+        const int nout = G.n_out;
+        // gp.cpp:172-176 augmented query [q/l | -1/2|q/l|^2 | 1]
+        const double q0 = v / G.ls[0], q1 = w / G.ls[1], q2 = u0 / G.ls[2], q3 = u1 / G.ls[3];
+        const double qn = -0.5 * (q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
+        double acc[NO];
 #pragma unroll
-          for (int o = 0; o < NO; ++o) acc[o] = 0.0;
-          if (alive) {
-            const double* z0 = gp;
-            const double* z1 = gp + n;
-            const double* z2 = gp + 2 * n;
-            const double* z3 = gp + 3 * n;
-            const double* zn = gp + 4 * n;
-            const double* al = gp + 5 * n;
+        for (int o = 0; o < NO; ++o) acc[o] = 0.0;
+        const double* z0 = gp;
+        const double* z1 = gp + n;
+        const double* z2 = gp + 2 * n;
+        const double* z3 = gp + 3 * n;
+        const double* zn = gp + 4 * n;
+        const double* al = gp + 5 * n;
 #pragma unroll 4
-            for (int j = gl; j < n; j += LPS) {
-              // gp.cpp:177-179: k*_j = exp(q_aug · inputs_aug_j)
-              const double d = q0 * z0[j] + q1 * z1[j] + q2 * z2[j] + q3 * z3[j] + qn + zn[j];
-              const double kj = exp(d);
+        for (int j = gl; j < n; j += LPS) {
+          // gp.cpp:177-179: k*_j = exp(q_aug · inputs_aug_j)
+          const double d = q0 * z0[j] + q1 * z1[j] + q2 * z2[j] + q3 * z3[j] + qn + zn[j];
+          const double kj = exp_tab(d, sv.etab);
 #pragma unroll
-              for (int o = 0; o < NO; ++o)
-                if (o < nout) acc[o] = fma(kj, al[o * n + j], acc[o]);  // gp.cpp:181-182
-            }
+          for (int o = 0; o < NO; ++o)
+            if (o < nout) acc[o] = fma(kj, al[o * n + j], acc[o]);  // gp.cpp:181-182
+        }
+#pragma unroll
+        for (int o = 0; o < NO; ++o) {
+          if (o < nout) {
+            const double mo = group_sum<LPS>(acc[o]);
+            const int gi = G.out_idx[o];
+            const double wt = sv.tw[gi >> 1];
+            if (gi & 1)
+              cm1 += wt * mo;
+            else
+              cm0 += wt * mo;
           }
-#pragma unroll
-          for (int o = 0; o < NO; ++o) {
-            if (o < nout) {
-              const double mo = group_sum<LPS>(acc[o]);
-              const int gi = G.out_idx[o];
-              const double w = sv.tw[gi >> 1];  // combine_terrains (mppi.cpp:34-49)
-              if (gi & 1)
-                cm1 += w * mo;
-              else
-                cm0 += w * mo;
-            }
-          }
-          gp += (size_t)(5 + nout) * n;
         }
+        gp += (size_t)(5 + nout) * n;
       }
-      if (alive) {  // mppi.cpp:329-349
-        step_nominal(st, u, a.nom, nx, sp, cp);
-        nx[3] += cm0;  // mppi.cpp:341-342
-        nx[4] += cm1;
-        if (!finite5(nx)) {  // mppi.cpp:343-346
-          alive = false;
-#pragma unroll
-          for (int i = 0; i < 5; ++i) nx[i] = st[i];
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 5; ++i) nx[i] = st[i];
+      v = v + av * (u0 - v) + cm0;  // step_nominal lag (dynamics.cpp:63-64) + mppi.cpp:341-342
+      w = w + aw * (u1 - w) + cm1;
+      if (gl == 0) {
+        sv_[k + 1] = v;
+        sw[k + 1] = w;
       }
-      const StepCost c = step_cost(task, st, nx, sp, cp, sv.rbar[k], sv.marg + (size_t)k * O, u[0], decay);
-      cost += c.cost;
-      decay *= 0.9;
-      vb |= (uint32_t)c.viol << (k & 31);
-      cb |= (uint32_t)c.coll << (k & 31);
-      if ((k & 31) == 31 || k == T - 1) {
-        if (valid && gl == 0) {
-          a.viol_bits[(size_t)sl * a.words + (k >> 5)] = vb;
-          a.coll_bits[(size_t)sl * a.words + (k >> 5)] = cb;
-        }
-        vb = cb = 0;
-      }
-#pragma unroll
-      for (int i = 0; i < 5; ++i) st[i] = nx[i];
     }
+    __syncwarp();
+    // ---------------- phase 2a: heading recursion (arc_advance: theta = wrap(theta + omega dt))
+    if (gl == 0) {
+      double th = a.x0[2];
+      sth[0] = th;
+      for (int k = 0; k < T; ++k) {
+        th = wrap_angle(th + sw[k] * a.nom.dt);
+        sth[k + 1] = th;
+      }
+    }
+    __syncwarp();
+    // ---------------- phase 2b: sincos and exact-arc increments, lanes split the steps
+    for (int k = gl; k < T; k += LPS) {
+      const double th = sth[k], vk = sv_[k], wk = sw[k];
+      double sp, cp;
+      sincos(th, &sp, &cp);
+      ssin[k] = sp;
+      scos[k] = cp;
+      double dx = 0.0, dy = 0.0, t2 = th;
+      arc_advance(dx, dy, t2, vk, 0.0, wk, a.nom.dt, sp, cp);
+      sx[k + 1] = dx;
+      sy[k + 1] = dy;
+    }
+    __syncwarp();
+    // ---------------- phase 2c: positions in step order + first non-finite state
+    int kd = T;  // states k > kd are frozen at state kd (mppi.cpp:343-346)
+    if (gl == 0) {
+      double x = a.x0[0], y = a.x0[1];
+      sx[0] = x;
+      sy[0] = y;
+      for (int k = 0; k < T; ++k) {
+        x += sx[k + 1];
+        y += sy[k + 1];
+        sx[k + 1] = x;
+        sy[k + 1] = y;
+        if (kd == T && !(isfinite(x) && isfinite(y) && isfinite(sth[k + 1]) && isfinite(sv_[k + 1]) &&
+                         isfinite(sw[k + 1])))
+          kd = k;
+      }
+    }
+    kd = __shfl_sync(0xffffffffu, kd, (threadIdx.x & 31) & ~(LPS - 1));
+    __syncwarp();
+    // ---------------- phase 2d: per-step costs and flags (costs.cpp:127-171), lanes split the steps
+    double cost = 0.0;
+    for (int wd = 0; wd < a.words; ++wd) {
+      uint32_t vb = 0, cb = 0;
+      const int kend = min(T, 32 * wd + 32);
+      for (int k = 32 * wd + gl; k < kend; k += LPS) {
+        const int ip = min(k, kd), in = min(k + 1, kd);
+        const double prev[5] = {sx[ip], sy[ip], sth[ip], sv_[ip], sw[ip]};
+        const double next[5] = {sx[in], sy[in], sth[in], sv_[in], sw[in]};
+        double decay = 1.0;  // 0.9^k by repeated multiplication, as costs.cpp:146
+        for (int i = 0; i < k; ++i) decay *= 0.9;
+        const StepCost c = step_cost(task, prev, next, ssin[ip], scos[ip], sv.rbar[k],
+                                     sv.marg + (size_t)k * O, su0[k], decay);
+        cost += c.cost;
+        vb |= (uint32_t)c.viol << (k & 31);
+        cb |= (uint32_t)c.coll << (k & 31);
+      }
+#pragma unroll
+      for (int o = LPS / 2; o > 0; o >>= 1) {
+        vb |= __shfl_xor_sync(0xffffffffu, vb, o);
+        cb |= __shfl_xor_sync(0xffffffffu, cb, o);
+      }
+      if (valid && gl == 0) {
+        a.viol_bits[(size_t)sl * a.words + wd] = vb;
+        a.coll_bits[(size_t)sl * a.words + wd] = cb;
+      }
+    }
+    cost = group_sum<LPS>(cost);
+    const bool alive = valid && kd == T;
     bool term = false;
     if (task.kind == TASK_AVOIDANCE) {  // costs.cpp:169 terminal_cost
-      const double gx = st[0] - task.goal[0], gy = st[1] - task.goal[1];
+      const int il = min(T, kd);
+      const double gx = sx[il] - task.goal[0], gy = sy[il] - task.goal[1];
       term = sqrt(gx * gx + gy * gy) <= task.goal[2];
       cost += task.aw[3] * (term ? 0.0 : task.high_cost);
     }
@@ -245,6 +350,7 @@ __global__ void __launch_bounds__(256, 1) rollout_gp_kernel(const RolloutArgs a)
       a.term[sl] = term;
       a.alive[sl] = alive;
     }
+    __syncwarp();
   }
 }
 
@@ -317,12 +423,17 @@ int rollout_lanes_per_sample(int K, int num_sms) {
     const char* e = getenv("GPMPPI_LPS");
     forced = e ? atoi(e) : 0;
   }
-  if (forced == 8 || forced == 16 || forced == 32) return forced;
+  if (forced == 4 || forced == 8 || forced == 16 || forced == 32) return forced;
   // aim for >= ~7 warps per SM before widening the lane groups
   const long long per_sm = ((long long)K + num_sms - 1) / num_sms;
   if (per_sm >= 28) return 8;
   if (per_sm >= 14) return 16;
   return 32;
+}
+
+// trajectory scratch for every lane group the launcher can create (<= 64 per block)
+size_t rollout_scratch_doubles(int T, int num_sms) {
+  return (size_t)num_sms * 64 * SCR_ARRAYS * (size_t)(T + 1);
 }
 
 cudaError_t launch_rollout(const RolloutArgs& a, int num_sms, cudaStream_t st) {
@@ -341,13 +452,13 @@ cudaError_t launch_rollout(const RolloutArgs& a, int num_sms, cudaStream_t st) {
     if (blocks > num_sms) blocks = num_sms;
     const int threads = wpb * 32;
     using KF = void (*)(const RolloutArgs);
-    KF table[4][3] = {
-        {rollout_gp_kernel<2, 8>, rollout_gp_kernel<2, 16>, rollout_gp_kernel<2, 32>},
-        {rollout_gp_kernel<4, 8>, rollout_gp_kernel<4, 16>, rollout_gp_kernel<4, 32>},
-        {rollout_gp_kernel<6, 8>, rollout_gp_kernel<6, 16>, rollout_gp_kernel<6, 32>},
-        {rollout_gp_kernel<8, 8>, rollout_gp_kernel<8, 16>, rollout_gp_kernel<8, 32>}};
+    KF table[4][4] = {
+        {rollout_gp_kernel<2, 4>, rollout_gp_kernel<2, 8>, rollout_gp_kernel<2, 16>, rollout_gp_kernel<2, 32>},
+        {rollout_gp_kernel<4, 4>, rollout_gp_kernel<4, 8>, rollout_gp_kernel<4, 16>, rollout_gp_kernel<4, 32>},
+        {rollout_gp_kernel<6, 4>, rollout_gp_kernel<6, 8>, rollout_gp_kernel<6, 16>, rollout_gp_kernel<6, 32>},
+        {rollout_gp_kernel<8, 4>, rollout_gp_kernel<8, 8>, rollout_gp_kernel<8, 16>, rollout_gp_kernel<8, 32>}};
     const int ni = no <= 2 ? 0 : no <= 4 ? 1 : no <= 6 ? 2 : 3;
-    const int li = lps == 8 ? 0 : lps == 16 ? 1 : 2;
+    const int li = lps == 4 ? 0 : lps == 8 ? 1 : lps == 16 ? 2 : 3;
     KF kern = table[ni][li];
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
