@@ -797,7 +797,7 @@ cudaError_t launch_reduce(const ReduceArgs& a, int blocks, cudaStream_t st) {
   size_t smem = sizeof(double) * (size_t)nsl * a.T * 2;
   const size_t need = sizeof(double) * ((size_t)7 * blocks + 2 * a.T);
   if (smem < need) smem = need;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   reduce_kernel<<<blocks, threads, smem, st>>>(a);
   count_launch();
   return cudaGetLastError();
@@ -901,7 +901,7 @@ cudaError_t launch_predict(const ModelDev& m, const double* q, long long S, doub
                            double* var, cudaStream_t st) {
   if (S <= 0) return cudaSuccess;
   const size_t smem = sizeof(double) * (size_t)m.n;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(predict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(predict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int blocks = S < 1184 ? (int)S : 1184;
   predict_kernel<<<blocks, 512, smem, st>>>(m, q, S, mean, var);
   count_launch();
@@ -923,9 +923,12 @@ constexpr int TIGHT_COLS = 256;  // columns of L^{-T} per variance block
 // Jacobians are then evaluated for all k in parallel and x, y accumulated in
 // step order exactly as arc_advance does (dynamics.cpp:39-66).
 constexpr int TMEAN_THREADS = 128;
+template <int NO>
 __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const TightenArgs a) {
   extern __shared__ __align__(16) double tsm[];  // [2T nominal][T+1 v][T+1 w][T+1 th][T dx][T dy][pts]
   __shared__ double tw[kMaxTerrains];
+  __shared__ double etab[32];
+  if (threadIdx.x < 32) etab[threadIdx.x] = kExp2Frac[threadIdx.x];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int T = a.T, n = a.model.n;
   double* nom = tsm;
@@ -934,7 +937,7 @@ __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const Tight
   double* th = ww + (T + 1);
   double* dx = th + (T + 1);
   double* dy = dx + T;
-  double* pts = dy + T;
+  double* pts = dy + T + ((7 * T + 3) & 1);  // 16-byte aligned for the vectorised staging
   if (threadIdx.x < a.R) tw[threadIdx.x] = a.tw[threadIdx.x];
   for (int i = threadIdx.x; i < 2 * T; i += blockDim.x) nom[i] = a.nominal_seq[i];
   if (threadIdx.x == 0) {
@@ -942,64 +945,97 @@ __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const Tight
     ww[0] = a.x0[4];
     th[0] = a.x0[2];
   }
-  if (a.model_kind == MODEL_GP) {
+  if (a.model_kind == MODEL_GP) {  // vectorised staging of Z / alpha
     double* dst = pts;
     for (int g = 0; g < a.model.G; ++g) {
       const int cnt = (5 + a.model.g[g].n_out) * n;
-      for (int i = threadIdx.x; i < cnt; i += blockDim.x) dst[i] = a.model.g[g].pts[i];
+      const double2* src = reinterpret_cast<const double2*>(a.model.g[g].pts);
+      double2* d2 = reinterpret_cast<double2*>(dst);
+#pragma unroll 4
+      for (int i = threadIdx.x; i < cnt / 2; i += blockDim.x) d2[i] = __ldg(src + i);
+      if ((cnt & 1) && threadIdx.x == 0) dst[cnt - 1] = a.model.g[g].pts[cnt - 1];
       dst += cnt;
     }
   }
   __syncthreads();
   const double av = a.nom.dt / a.nom.tau_v, aw = a.nom.dt / a.nom.tau_omega;
-  // serial (v, omega) chain with the GP mean (mppi.cpp:220-233), one warp: no
-  // block barriers on the critical path, the butterfly leaves the sums in every lane.
-  if (w == 0) {
-    double v = vv[0], om = ww[0];
-    for (int k = 0; k < T; ++k) {
-      const double u0 = nom[2 * k], u1 = nom[2 * k + 1];
-      double c0 = 0.0, c1 = 0.0;
-      if (a.model_kind == MODEL_GP) {
-        const double* p = pts;
-        for (int g = 0; g < a.model.G; ++g) {
-          const GroupDev& G = a.model.g[g];
-          const double q0 = v / G.ls[0], q1 = om / G.ls[1], q2 = u0 / G.ls[2], q3 = u1 / G.ls[3];
-          const double qn = -0.5 * (q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
-          double acc[kMaxOutPerGroup];
+  // serial (v, omega) chain with the GP mean (mppi.cpp:220-233). The warps split the
+  // n points; every warp reduces the per-warp partials itself (double-buffered), so a
+  // step costs one block barrier. q/l uses reciprocal lengthscales (<= 1 ulp from the
+  // reference's division) to keep FP64 divides off the serial path.
+  __shared__ double red[2][TMEAN_THREADS / 32][kMaxGroups * NO];
+  __shared__ double gil[kMaxGroups][4];       // reciprocal lengthscales
+  __shared__ double gwt[kMaxGroups][NO];      // terrain weight of each output
+  __shared__ int gch[kMaxGroups][NO];         // 0: v channel, 1: omega channel, -1: unused
+  __shared__ int gno[kMaxGroups];
+  const int nwarps = blockDim.x >> 5;
+  const int G = a.model_kind == MODEL_GP ? a.model.G : 0;
+  if (threadIdx.x == 0) {  // group constants out of the (register-indexed) parameter space
+    for (int g = 0; g < G; ++g) {
+      gno[g] = a.model.g[g].n_out;
+      for (int d = 0; d < 4; ++d) gil[g][d] = 1.0 / a.model.g[g].ls[d];
+      for (int o = 0; o < NO; ++o) {
+        const bool used = o < a.model.g[g].n_out;
+        const int gi = used ? a.model.g[g].out_idx[o] : 0;
+        gwt[g][o] = used ? tw[gi >> 1] : 0.0;
+        gch[g][o] = used ? (gi & 1) : -1;
+      }
+    }
+  }
+  __syncthreads();
+  double v = vv[0], om = ww[0];
+  for (int k = 0; k < T; ++k) {
+    const double u0 = nom[2 * k], u1 = nom[2 * k + 1];
+    double c0 = 0.0, c1 = 0.0;
+    if (G > 0) {
+      const double* p = pts;
+      for (int g = 0; g < G; ++g) {
+        const double q0 = v * gil[g][0], q1 = om * gil[g][1];
+        const double q2 = u0 * gil[g][2], q3 = u1 * gil[g][3];
+        const double qn = -0.5 * (q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
+        const int no = gno[g];
+        double acc[NO];
 #pragma unroll
-          for (int o = 0; o < kMaxOutPerGroup; ++o) acc[o] = 0.0;
+        for (int o = 0; o < NO; ++o) acc[o] = 0.0;
 #pragma unroll 4
-          for (int j = lane; j < n; j += 32) {
-            const double kj = exp(q0 * p[j] + q1 * p[n + j] + q2 * p[2 * n + j] + q3 * p[3 * n + j] + qn + p[4 * n + j]);
+        for (int j = threadIdx.x; j < n; j += TMEAN_THREADS) {
+          const double kj = exp_tab(q0 * p[j] + q1 * p[n + j] + q2 * p[2 * n + j] + q3 * p[3 * n + j] + qn + p[4 * n + j], etab);
 #pragma unroll
-            for (int o = 0; o < kMaxOutPerGroup; ++o)
-              if (o < G.n_out) acc[o] = fma(kj, p[(5 + o) * n + j], acc[o]);
-          }
+          for (int o = 0; o < NO; ++o)
+            if (o < no) acc[o] = fma(kj, p[(5 + o) * n + j], acc[o]);
+        }
 #pragma unroll
-          for (int o = 0; o < kMaxOutPerGroup; ++o)
-            if (o < G.n_out) {
-              const double sm = warp_sum(acc[o]);
-              const int gi = G.out_idx[o];
-              if (gi & 1)
-                c1 += tw[gi >> 1] * sm;  // ensemble_combine, ascending terrains
-              else
-                c0 += tw[gi >> 1] * sm;
-            }
-          p += (size_t)(5 + G.n_out) * n;
+        for (int o = 0; o < NO; ++o) {
+          const double sm = warp_sum(acc[o]);
+          if (lane == 0) red[k & 1][w][g * NO + o] = sm;
+        }
+        p += (size_t)(5 + no) * n;
+      }
+      __syncthreads();
+      for (int g = 0; g < G; ++g) {
+#pragma unroll
+        for (int o = 0; o < NO; ++o) {
+          // full 32-lane butterfly: every lane of every warp ends with the same bits
+          const double x = warp_sum(lane < nwarps ? red[k & 1][lane][g * NO + o] : 0.0);
+          const int ch = gch[g][o];
+          if (ch == 1)
+            c1 += gwt[g][o] * x;  // ensemble_combine, ascending terrains
+          else if (ch == 0)
+            c0 += gwt[g][o] * x;
         }
       }
-      if (lane == 0) {
-        a.tq[k * 4 + 0] = v;
-        a.tq[k * 4 + 1] = om;
-        a.tq[k * 4 + 2] = u0;
-        a.tq[k * 4 + 3] = u1;
-      }
-      v = v + av * (u0 - v) + c0;  // step_nominal lag (dynamics.cpp:63-64) + correction mean
-      om = om + aw * (u1 - om) + c1;
-      if (lane == 0) {
-        vv[k + 1] = v;
-        ww[k + 1] = om;
-      }
+    }
+    if (threadIdx.x == 0) {
+      a.tq[k * 4 + 0] = v;
+      a.tq[k * 4 + 1] = om;
+      a.tq[k * 4 + 2] = u0;
+      a.tq[k * 4 + 3] = u1;
+    }
+    v = v + av * (u0 - v) + c0;  // step_nominal lag (dynamics.cpp:63-64) + correction mean
+    om = om + aw * (u1 - om) + c1;
+    if (threadIdx.x == 0) {
+      vv[k + 1] = v;
+      ww[k + 1] = om;
     }
   }
   __syncthreads();
@@ -1116,85 +1152,95 @@ __global__ void __launch_bounds__(32) tighten_cov_kernel(const TightenArgs a, in
   }
   if (l < 25) S[l] = 0.0;
   if (l == 0) infeasible = 0;
+  double* Ss = mus + 5 * (T + 1);  // [T][25] propagated covariances
   __syncwarp();
-  for (int k = 0; k < a.T; ++k) {
+  const int i5 = l / 5, j5 = l % 5;
+  for (int k = 0; k < a.T; ++k) {  // Σ' = J Σ Jᵀ + diag(0,0,0,cv0,cv1), symmetrised (uncertainty.cpp:83-87)
     const double* J = Js + 25 * k;
     const double* cv = cvs + 2 * k;
     if (l < 25) {
-      const int i = l / 5, j = l % 5;
       double s = 0.0;
-      for (int q = 0; q < 5; ++q) s += J[i * 5 + q] * S[q * 5 + j];
+      for (int q = 0; q < 5; ++q) s += J[i5 * 5 + q] * S[q * 5 + j5];
       JS[l] = s;
     }
     __syncwarp();
     if (l < 25) {
-      const int i = l / 5, j = l % 5;
       double s = 0.0;
-      for (int q = 0; q < 5; ++q) s += JS[i * 5 + q] * J[j * 5 + q];
+      for (int q = 0; q < 5; ++q) s += JS[i5 * 5 + q] * J[j5 * 5 + q];
       if (l == 18) s += cv[0];
       if (l == 24) s += cv[1];
       C[l] = s;
     }
     __syncwarp();
     if (l < 25) {
-      const int i = l / 5, j = l % 5;
-      const double v = 0.5 * (C[i * 5 + j] + C[j * 5 + i]);
+      const double v = 0.5 * (C[i5 * 5 + j5] + C[j5 * 5 + i5]);
       S[l] = v;
-      a.horizon_cov[(size_t)k * 25 + l] = v;
+      Ss[k * 25 + l] = v;
     }
-    __syncwarp();
-    const double* mu = mus + (k + 1) * 5;  // belief mean after step k
-    const double c00 = S[0], c01 = S[1], c10 = S[5], c11 = S[6];
-    if (l == 0 && t.kind != TASK_AVOIDANCE) {  // tighten_lane_radius (uncertainty.cpp:90-96)
-      const double half_tr = 0.5 * (c00 + c11);
-      const double disc = 0.25 * (c00 - c11) * (c00 - c11) + c01 * c10;
-      double lm = half_tr + sqrt(disc > 0.0 ? disc : 0.0);
-      lm = lm > 0.0 ? lm : 0.0;
-      const double r = t.half_width - sqrt(a.chi2 * lm);
-      a.r_bar[k] = r;
-      if (r <= 0.0) infeasible = 1;
-    }
-    if (t.kind != TASK_TRACKING)  // tighten_obstacle_distance (uncertainty.cpp:98-116)
-      for (int o = l; o < t.n_obs; o += 32) {
-        const double dx = mu[0] - t.obs[o][0], dy = mu[1] - t.obs[o][1];
-        const double dist = sqrt(dx * dx + dy * dy);
-        double d, n0, n1;
-        if (dist < 1e-12) {
-          n0 = 1.0;
-          n1 = 0.0;
-          d = -t.obs[o][2];
-        } else {
-          n0 = dx / dist;
-          n1 = dy / dist;
-          d = dist - t.obs[o][2];
-        }
-        const double cn0 = c00 * n0 + c01 * n1, cn1 = c10 * n0 + c11 * n1;
-        double dv = n0 * cn0 + n1 * cn1;
-        dv = dv > 0.0 ? dv : 0.0;
-        const double dbar = d - a.z * sqrt(dv);
-        a.margins[(size_t)k * t.n_obs + o] = d - dbar;
-        if (dbar <= 0.0) atomicOr(&infeasible, 1);
-      }
     __syncwarp();
   }
+  for (int i = l; i < 25 * T; i += 32) a.horizon_cov[i] = Ss[i];
+  for (int k = l; k < T; k += 32) {  // tighten_lane_radius (uncertainty.cpp:90-96), parallel in k
+    if (t.kind == TASK_AVOIDANCE) break;
+    const double* Sk = Ss + 25 * k;
+    const double c00 = Sk[0], c01 = Sk[1], c10 = Sk[5], c11 = Sk[6];
+    const double half_tr = 0.5 * (c00 + c11);
+    const double disc = 0.25 * (c00 - c11) * (c00 - c11) + c01 * c10;
+    double lm = half_tr + sqrt(disc > 0.0 ? disc : 0.0);
+    lm = lm > 0.0 ? lm : 0.0;
+    const double r = t.half_width - sqrt(a.chi2 * lm);
+    a.r_bar[k] = r;
+    if (r <= 0.0) atomicOr(&infeasible, 1);
+  }
+  if (t.kind != TASK_TRACKING)  // tighten_obstacle_distance (uncertainty.cpp:98-116), parallel in (k, o)
+    for (int idx = l; idx < T * t.n_obs; idx += 32) {
+      const int k = idx / t.n_obs, o = idx % t.n_obs;
+      const double* Sk = Ss + 25 * k;
+      const double c00 = Sk[0], c01 = Sk[1], c10 = Sk[5], c11 = Sk[6];
+      const double* mu = mus + (k + 1) * 5;  // belief mean after step k
+      const double dx = mu[0] - t.obs[o][0], dy = mu[1] - t.obs[o][1];
+      const double dist = sqrt(dx * dx + dy * dy);
+      double d, n0, n1;
+      if (dist < 1e-12) {
+        n0 = 1.0;
+        n1 = 0.0;
+        d = -t.obs[o][2];
+      } else {
+        n0 = dx / dist;
+        n1 = dy / dist;
+        d = dist - t.obs[o][2];
+      }
+      const double cn0 = c00 * n0 + c01 * n1, cn1 = c10 * n0 + c11 * n1;
+      double dv = n0 * cn0 + n1 * cn1;
+      dv = dv > 0.0 ? dv : 0.0;
+      const double dbar = d - a.z * sqrt(dv);
+      a.margins[(size_t)k * t.n_obs + o] = d - dbar;
+      if (dbar <= 0.0) atomicOr(&infeasible, 1);
+    }
+  __syncwarp();
   if (l == 0) *a.infeasible = infeasible;
 }
 
 int tighten_splits(int n) { return n > 0 ? (n + TIGHT_COLS - 1) / TIGHT_COLS : 1; }
 
 cudaError_t launch_tighten(const TightenArgs& a, cudaStream_t st) {
-  size_t msm = sizeof(double) * (size_t)(2 * a.T + 3 * (a.T + 1) + 2 * a.T);
+  size_t msm = sizeof(double) * (size_t)(2 * a.T + 3 * (a.T + 1) + 2 * a.T + 1);
   if (a.model_kind == MODEL_GP)
     for (int g = 0; g < a.model.G; ++g) msm += sizeof(double) * (size_t)(5 + a.model.g[g].n_out) * a.model.n;
-  if (msm > 48 * 1024) cudaFuncSetAttribute(tighten_mean_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm);
-  tighten_mean_kernel<<<1, TMEAN_THREADS, msm, st>>>(a);
+  int no = 1;
+  if (a.model_kind == MODEL_GP)
+    for (int g = 0; g < a.model.G; ++g) no = a.model.g[g].n_out > no ? a.model.g[g].n_out : no;
+  void (*mk)(const TightenArgs) = no <= 2 ? tighten_mean_kernel<2> : no <= 4 ? tighten_mean_kernel<4>
+                                  : no <= 6 ? tighten_mean_kernel<6> : tighten_mean_kernel<8>;
+  cudaFuncSetAttribute(mk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm);  // static + dynamic may exceed 48 KB
+  mk<<<1, TMEAN_THREADS, msm, st>>>(a);
   const int G = a.model_kind == MODEL_GP ? a.model.G : 1;
   const int ns = a.model_kind == MODEL_GP ? tighten_splits(a.model.n) : 1;
   const size_t smem = sizeof(double) * (size_t)(a.model.n > 0 ? a.model.n : 1);
-  if (smem > 48 * 1024) cudaFuncSetAttribute(tighten_var_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(tighten_var_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (a.model_kind == MODEL_GP) tighten_var_kernel<<<dim3(a.T, G, ns), TIGHT_COLS, smem, st>>>(a);
-  const size_t csmem = sizeof(double) * (size_t)(25 * a.T + 2 * a.T + 5 * (a.T + 1));
-  if (csmem > 48 * 1024) cudaFuncSetAttribute(tighten_cov_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem);
+  const size_t csmem = sizeof(double) * (size_t)(25 * a.T + 2 * a.T + 5 * (a.T + 1) + 25 * a.T);
+  cudaFuncSetAttribute(tighten_cov_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem);
   tighten_cov_kernel<<<1, 32, csmem, st>>>(a, ns);
   count_launch(3);
   return cudaGetLastError();
