@@ -1,0 +1,353 @@
+// gpmppi/planner.hpp — header-only C++ drop-in for the reference planner API
+// (/root/reference/proj/include/gpmppi/{mppi,gp,costs,dynamics,core}.hpp) on top
+// of the C ABI in gpmppi_b200.h. Same class / member names, argument meaning and
+// exception types (std::invalid_argument, std::runtime_error, std::logic_error);
+// value types use std::array instead of Eigen (Eigen is not a dependency here).
+// Link with -lgpmppi_b200 (paper_2411_03289_b200/lib/libgpmppi_b200.so).
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <variant>
+#include <vector>
+
+#include "gpmppi_b200.h"
+
+namespace gpmppi {
+
+namespace detail {
+inline void check(int rc) {
+  if (rc == GPMPPI_OK) return;
+  const std::string msg = gpmppi_last_error();
+  switch (rc) {
+    case GPMPPI_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    case GPMPPI_LOGIC_ERROR: throw std::logic_error(msg);
+    default: throw std::runtime_error(msg);  // runtime errors and CUDA failures
+  }
+}
+}  // namespace detail
+
+using Vec2 = std::array<double, 2>;
+
+struct RobotState {  // core.hpp:30-51
+  double x{0.0}, y{0.0}, theta{0.0}, v{0.0}, omega{0.0};
+  std::array<double, 5> vec() const { return {x, y, theta, v, omega}; }
+};
+struct Control {  // core.hpp:54-59
+  double v_ref{0.0}, omega_ref{0.0};
+};
+struct ControlBounds {  // core.hpp:61-74
+  Control lo{-0.5, -2.0};
+  Control hi{2.0, 2.0};
+};
+using ControlSequence = std::vector<Control>;
+
+struct MppiConfig {  // mppi.hpp:16-26
+  int samples{1024};
+  int horizon{30};
+  double lambda{0.1};
+  Vec2 sigma_sim{0.09, 0.25};
+  ControlBounds bounds;
+  std::uint64_t seed{0};
+  int threads{0};
+  gpmppi_mppi_config c() const {
+    return {samples, horizon, lambda, sigma_sim[0], sigma_sim[1], {bounds.lo.v_ref, bounds.lo.omega_ref},
+            {bounds.hi.v_ref, bounds.hi.omega_ref}, seed, threads};
+  }
+};
+struct NominalParams {  // dynamics.hpp:12-18
+  double tau_v{0.5}, tau_omega{0.35}, dt{0.05};
+};
+struct Edd5Params {  // dynamics.hpp:36-45
+  double alpha_l{1.0}, alpha_r{1.0}, x_icr{0.0}, y_icr_l{0.0}, y_icr_r{0.0};
+  static Edd5Params ideal(double w) { return {1.0, 1.0, 0.0, -0.5 * w, 0.5 * w}; }
+};
+struct KernelParams {  // gp.hpp:12-22
+  double signal_var{1.0};
+  std::array<double, 4> lengthscales{1.0, 1.0, 1.0, 1.0};
+  double noise_var{1e-4};
+};
+
+// GpModel (gp.hpp:30-98): device-resident exact GP.
+class GpModel {
+ public:
+  GpModel() = default;
+  GpModel(GpModel&& o) noexcept : h_(std::exchange(o.h_, nullptr)) {}
+  GpModel& operator=(GpModel&& o) noexcept {
+    std::swap(h_, o.h_);
+    return *this;
+  }
+  GpModel(const GpModel&) = delete;
+  ~GpModel() { gpmppi_model_free(h_); }
+
+  // inputs n×4 and outputs n×m, row-major
+  static GpModel fit(const std::vector<double>& inputs, const std::vector<double>& outputs, int64_t m,
+                     const std::vector<KernelParams>& kernels, int device = 0) {
+    if (inputs.size() % 4 != 0 || inputs.empty())
+      throw std::invalid_argument("GpModel::fit: inputs must be n x 4 with n >= 1");
+    const int64_t n = static_cast<int64_t>(inputs.size() / 4);
+    if (m < 1 || static_cast<int64_t>(outputs.size()) != n * m)
+      throw std::invalid_argument("GpModel::fit: outputs must be n x m with m >= 1");
+    if (static_cast<int64_t>(kernels.size()) != m)
+      throw std::invalid_argument("GpModel::fit: one KernelParams per output column required");
+    std::vector<double> k;
+    for (const auto& p : kernels) {
+      k.push_back(p.signal_var);
+      for (double l : p.lengthscales) k.push_back(l);
+      k.push_back(p.noise_var);
+    }
+    GpModel g;
+    detail::check(gpmppi_model_fit(inputs.data(), outputs.data(), n, m, k.data(), device, &g.h_));
+    return g;
+  }
+  static GpModel load(const std::string& path, int device = 0) {
+    GpModel g;
+    detail::check(gpmppi_model_load(path.c_str(), device, &g.h_));
+    return g;
+  }
+  void save(const std::string& path) const { detail::check(gpmppi_model_save(h_, path.c_str())); }
+  int n_points() const { return gpmppi_model_n_points(h_); }
+  int n_outputs() const { return gpmppi_model_n_outputs(h_); }
+  int n_groups() const { return gpmppi_model_n_groups(h_); }
+  double group_jitter(int g) const { return gpmppi_model_group_jitter(h_, g); }
+  double log_marginal_likelihood(int o) const { return gpmppi_model_log_marginal_likelihood(h_, o); }
+  struct BatchPrediction {
+    std::vector<double> mean, var;  // S × n_outputs, row-major
+  };
+  BatchPrediction predict_batch(const std::vector<double>& queries) const {
+    if (!h_) throw std::logic_error("GpModel::predict_batch: model not fitted");
+    const int64_t S = static_cast<int64_t>(queries.size() / 4);
+    BatchPrediction p{std::vector<double>(S * n_outputs()), std::vector<double>(S * n_outputs())};
+    detail::check(gpmppi_model_predict_batch(h_, queries.data(), S, p.mean.data(), p.var.data()));
+    return p;
+  }
+  const gpmppi_model* handle() const { return h_; }
+
+ private:
+  gpmppi_model* h_ = nullptr;
+};
+
+// Prediction models (mppi.hpp:30-39)
+struct GpEnsemble {
+  const GpModel* model{nullptr};
+  int n_terrains{0};
+};
+struct Edd5Baseline {
+  Edd5Params params;
+  double track_width{0.4};
+};
+struct UnicycleBaseline {};
+struct NominalDynamic {};  // extension: zero-residual dynamic unicycle (BASELINE config 1)
+using PredictionModel = std::variant<GpEnsemble, Edd5Baseline, UnicycleBaseline, NominalDynamic>;
+
+// Tasks (costs.hpp:13-56, mppi.hpp:42-52)
+struct Track {
+  bool is_circle{false};
+  Vec2 center{0.0, 0.0};
+  double radius{0.0};
+  std::vector<Vec2> waypoints;
+  bool closed{true};
+  double half_width{0.5};
+  static Track circle_track(Vec2 c, double r, double hw) { return {true, c, r, {}, true, hw}; }
+  static Track polyline_track(std::vector<Vec2> pts, double hw, bool closed) {
+    return {false, {0.0, 0.0}, 0.0, std::move(pts), closed, hw};
+  }
+};
+struct CircleObstacle {
+  Vec2 center{0.0, 0.0};
+  double radius{0.0};
+};
+struct TrackingWeights {
+  double variance{0.1}, deviation{1.0}, slip{0.3}, safety{1.0}, speed{0.2};
+};
+struct AvoidanceWeights {
+  double variance{0.1}, obstacle{1.0}, stage{0.5}, terminal{1.0};
+};
+struct GoalSpec {
+  Vec2 position{0.0, 0.0};
+  double capture_radius{0.5};
+};
+struct TrackingTask {
+  const Track* track{nullptr};
+  double v_desired{0.0};
+  TrackingWeights weights;
+};
+struct AvoidanceTask {
+  const std::vector<CircleObstacle>* obstacles{nullptr};
+  GoalSpec goal;
+  AvoidanceWeights weights;
+  double high_cost{1e4};
+};
+// path tracking + tightened obstacle chance constraints (BASELINE config 2)
+struct CombinedTask {
+  const Track* track{nullptr};
+  double v_desired{0.0};
+  TrackingWeights weights;
+  const std::vector<CircleObstacle>* obstacles{nullptr};
+  double obstacle_weight{1.0};
+};
+
+struct StepDiagnostics {  // mppi.hpp:81-89
+  double best_cost{0.0}, mean_cost{0.0}, ess{0.0}, weight_entropy{0.0};
+  int nonfinite_samples{0};
+  bool tightening_infeasible{false};
+  double plan_ms{0.0};
+  double command_ms{0.0};
+};
+
+// Planner (mppi.hpp:96-143)
+class Planner {
+ public:
+  Planner(const MppiConfig& cfg, PredictionModel model, NominalParams nominal, double p_x,
+          int device = 0)
+      : cfg_(cfg) {
+    gpmppi_prediction_model pm{};
+    if (auto* g = std::get_if<GpEnsemble>(&model)) {
+      pm.kind = GPMPPI_MODEL_GP_ENSEMBLE;
+      pm.gp = g->model ? g->model->handle() : nullptr;
+      pm.n_terrains = g->n_terrains;
+    } else if (auto* e = std::get_if<Edd5Baseline>(&model)) {
+      pm.kind = GPMPPI_MODEL_EDD5;
+      pm.edd5 = {e->params.alpha_l, e->params.alpha_r, e->params.x_icr, e->params.y_icr_l, e->params.y_icr_r};
+      pm.track_width = e->track_width;
+    } else if (std::holds_alternative<UnicycleBaseline>(model)) {
+      pm.kind = GPMPPI_MODEL_UNICYCLE;
+    } else {
+      pm.kind = GPMPPI_MODEL_NOMINAL;
+    }
+    const gpmppi_mppi_config c = cfg.c();
+    const gpmppi_nominal nom{nominal.tau_v, nominal.tau_omega, nominal.dt};
+    detail::check(gpmppi_planner_create(&c, &pm, &nom, p_x, device, &h_));
+  }
+  Planner(Planner&& o) noexcept : cfg_(o.cfg_), h_(std::exchange(o.h_, nullptr)) {}
+  Planner& operator=(Planner&& o) noexcept {
+    std::swap(h_, o.h_);
+    cfg_ = o.cfg_;
+    return *this;
+  }
+  Planner(const Planner&) = delete;
+  ~Planner() { gpmppi_planner_free(h_); }
+
+  Control plan_step(const RobotState& x0, const TrackingTask& task, StepDiagnostics* diag = nullptr) {
+    if (task.track == nullptr) throw std::invalid_argument("plan_step: tracking task needs a track");
+    gpmppi_task t = base_task(GPMPPI_TASK_TRACKING, task.track, task.v_desired, task.weights);
+    return run(x0, t, diag);
+  }
+  Control plan_step(const RobotState& x0, const AvoidanceTask& task, StepDiagnostics* diag = nullptr) {
+    if (task.obstacles == nullptr) throw std::invalid_argument("plan_step: avoidance task needs an obstacle list");
+    gpmppi_task t{};
+    t.kind = GPMPPI_TASK_AVOIDANCE;
+    set_obstacles(t, *task.obstacles);
+    t.goal[0] = task.goal.position[0];
+    t.goal[1] = task.goal.position[1];
+    t.goal[2] = task.goal.capture_radius;
+    t.avoidance = {task.weights.variance, task.weights.obstacle, task.weights.stage, task.weights.terminal};
+    t.high_cost = task.high_cost;
+    return run(x0, t, diag);
+  }
+  Control plan_step(const RobotState& x0, const CombinedTask& task, StepDiagnostics* diag = nullptr) {
+    if (task.track == nullptr) throw std::invalid_argument("plan_step: tracking task needs a track");
+    if (task.obstacles == nullptr) throw std::invalid_argument("plan_step: avoidance task needs an obstacle list");
+    gpmppi_task t = base_task(GPMPPI_TASK_COMBINED, task.track, task.v_desired, task.weights);
+    set_obstacles(t, *task.obstacles);
+    t.avoidance.obstacle = task.obstacle_weight;
+    t.high_cost = 1e4;
+    return run(x0, t, diag);
+  }
+
+  void set_terrain_weights(const std::vector<double>& w) {
+    detail::check(gpmppi_planner_set_terrain_weights(h_, w.data(), static_cast<int>(w.size())));
+  }
+  std::vector<double> terrain_weights() const {
+    std::vector<double> w(64);
+    w.resize(gpmppi_planner_terrain_weights(h_, w.data()));
+    return w;
+  }
+  ControlSequence nominal_sequence() const {
+    std::vector<double> s(2 * cfg_.horizon);
+    detail::check(gpmppi_planner_nominal_sequence(h_, s.data()));
+    ControlSequence out(cfg_.horizon);
+    for (int k = 0; k < cfg_.horizon; ++k) out[k] = {s[2 * k], s[2 * k + 1]};
+    return out;
+  }
+  std::vector<std::array<double, 25>> horizon_covariances() const {
+    std::vector<std::array<double, 25>> c(cfg_.horizon);
+    detail::check(gpmppi_planner_horizon_covariances(h_, c[0].data()));
+    return c;
+  }
+  std::vector<double> lane_radii() const {
+    std::vector<double> r(cfg_.horizon);
+    r.resize(gpmppi_planner_lane_radii(h_, r.data()));
+    return r;
+  }
+  std::vector<double> obstacle_margins() const {  // T × O row-major
+    std::vector<double> m(static_cast<size_t>(cfg_.horizon) * GPMPPI_MAX_OBSTACLES);
+    const int O = gpmppi_planner_obstacle_margins(h_, m.data());
+    m.resize(static_cast<size_t>(cfg_.horizon) * O);
+    return m;
+  }
+  const MppiConfig& config() const { return cfg_; }
+  std::uint64_t tick() const { return gpmppi_planner_tick(h_); }
+  gpmppi_planner* handle() { return h_; }
+
+ private:
+  static gpmppi_task base_task(int kind, const Track* tr, double v_des, const TrackingWeights& w) {
+    gpmppi_task t{};
+    t.kind = kind;
+    track_c_.is_circle = tr->is_circle;
+    track_c_.cx = tr->center[0];
+    track_c_.cy = tr->center[1];
+    track_c_.radius = tr->radius;
+    wp_.clear();
+    for (const auto& p : tr->waypoints) {
+      wp_.push_back(p[0]);
+      wp_.push_back(p[1]);
+    }
+    track_c_.n_waypoints = static_cast<int>(tr->waypoints.size());
+    track_c_.waypoints = wp_.data();
+    track_c_.closed = tr->closed;
+    track_c_.half_width = tr->half_width;
+    t.track = &track_c_;
+    t.v_desired = v_des;
+    t.tracking = {w.variance, w.deviation, w.slip, w.safety, w.speed};
+    return t;
+  }
+  static void set_obstacles(gpmppi_task& t, const std::vector<CircleObstacle>& obs) {
+    obs_.clear();
+    for (const auto& o : obs) {
+      obs_.push_back(o.center[0]);
+      obs_.push_back(o.center[1]);
+      obs_.push_back(o.radius);
+    }
+    t.obstacles = obs_.data();
+    t.n_obstacles = static_cast<int>(obs.size());
+  }
+  Control run(const RobotState& x0, const gpmppi_task& t, StepDiagnostics* diag) {
+    const auto s = x0.vec();
+    double cmd[2];
+    gpmppi_diag d{};
+    detail::check(gpmppi_planner_plan_step(h_, s.data(), &t, cmd, &d));
+    if (diag) {
+      diag->best_cost = d.best_cost;
+      diag->mean_cost = d.mean_cost;
+      diag->ess = d.ess;
+      diag->weight_entropy = d.weight_entropy;
+      diag->nonfinite_samples = d.nonfinite_samples;
+      diag->tightening_infeasible = d.tightening_infeasible != 0;
+      diag->plan_ms = d.plan_ms;
+      diag->command_ms = d.command_ms;
+    }
+    return {cmd[0], cmd[1]};
+  }
+
+  MppiConfig cfg_;
+  gpmppi_planner* h_ = nullptr;
+  static inline thread_local gpmppi_track track_c_{};
+  static inline thread_local std::vector<double> wp_;
+  static inline thread_local std::vector<double> obs_;
+};
+
+}  // namespace gpmppi

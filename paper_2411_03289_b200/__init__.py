@@ -5,8 +5,8 @@ from .gpmppi import (  # noqa: F401
     AvoidanceTask, AvoidanceWeights, CircleObstacle, CombinedTask, ControlBounds, Edd5Baseline,
     Edd5Params, GoalSpec, GpEnsemble, GpModel, KernelParams, MppiConfig, NominalDynamic,
     NominalParams, Planner, StepDiagnostics, Track, TrackingTask, TrackingWeights,
-    UnicycleBaseline, chi2_quantile_2dof, combine_tuples, flush_l2, kernel_launches,
-    tuple_doubles)
+    UnicycleBaseline, apply_tuple, chi2_quantile_2dof, combine_tuples, flush_l2,
+    kernel_launches, shard_range, tuple_doubles)
 from ._capi import (  # noqa: F401
     NOISE_INJECTED, NOISE_PHILOX, VAR_FFMA, VAR_TC_1XTF32, VAR_TC_3XTF32, CudaError)
 

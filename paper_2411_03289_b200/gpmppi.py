@@ -521,6 +521,23 @@ class Planner:
         return cmd
 
 
+def shard_range(total: int, world: int, rank: int):
+    """Contiguous global sample range of `rank`: [begin, begin+count)."""
+    base, extra = divmod(total, world)
+    begin = rank * base + min(rank, extra)
+    return begin, base + (1 if rank < extra else 0)
+
+
+def apply_tuple(tup, nominal, lo=(-0.5, -2.0), hi=(2.0, 2.0)):
+    """Update + clamp + shift from a combined tuple (mppi.cpp:147-173), host arithmetic
+    for the CPU multi-rank tests (the device runs the same in finish_kernel)."""
+    T = len(nominal)
+    Z = tup[1]
+    dv = tup[6:].reshape(T, 2) / Z if Z > 0 else np.zeros((T, 2))
+    upd = np.clip(np.asarray(nominal) + dv, lo, hi)
+    return upd[0].copy(), np.vstack([upd[1:], upd[-1:]])
+
+
 def tuple_doubles(horizon: int) -> int:
     return A.lib().gpmppi_tuple_doubles(horizon)
 
