@@ -96,6 +96,41 @@ def load_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
+def roofline_block(w, phase, steps, peaks, peaks_kind):
+    """Roofline of the dominant kernel (SURVEY §8(d) algorithmic work per unit).
+
+    unit = one sample-rollout-step; F = n² + 24n FLOP split as
+      variance kernel: n(n+1) (triangular ||L^-1 k*||²) + 2n (squares, sum)
+      rollout kernel:  22n (kernel-row dot 4n FMA + exponent offsets, mean 6n FMA) + n exp
+    The contract's denominator is the measured bf16 dense peak; the path's own
+    ceilings (TF32 dense = bf16/2, FP64 = 148·64 DFMA·2·clock) are reported beside it.
+    """
+    n = w.n_points
+    units = w.samples * w.horizon
+    roll_ms, var_ms = phase[0] / steps, phase[1] / steps
+    if var_ms >= roll_ms:
+        kern, ms, flop = "variance_tc_kernel", var_ms, units * (n * n + 3 * n)
+        own_peak, own_name = peaks.get("bf16_tflops", 1590.0) / 2, "tf32_dense_tflops (bf16/2)"
+    else:
+        kern, ms, flop = "rollout_gp_kernel", roll_ms, units * 22 * n
+        own_peak = 148 * 64 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        own_name = "fp64_tflops (148 SM x 64 DFMA x 2 x max clock)"
+    achieved = flop / (ms / 1e3) / 1e12
+    peak = peaks.get("bf16_tflops", 1590.0)
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(kern)
+    except Exception:
+        pass
+    return {"bound": "tensor", "kernel": kern, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak, "traffic": traffic,
+            "peak_kind": f"{peaks_kind} bf16 dense burst (MEASURED_PEAKS.json)",
+            "flop_per_launch": flop, "launch_ms": ms, "own_peak": own_peak, "own_peak_kind": own_name,
+            "frac_of_own_peak": achieved / own_peak,
+            "phase_share": ms / (sum(phase) / steps)}
+
+
 def build_planner(w, api, samples=None, var_path=None):
     from paper_2411_03289_b200 import workloads as W
     task, track, obstacles = W.make_task_objects(w, api)
@@ -164,6 +199,16 @@ def run_reference_arm(args, w):
     print(json.dumps(line), flush=True)
 
 
+class _DryPlanner:
+    def variance_path(self):
+        return 1
+
+
+class _DryClock:
+    def summary(self):
+        return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["dry run"]}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -174,6 +219,8 @@ def main():
     ap.add_argument("--variance-path", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU contract check only: fake timings, no GPU, never a result")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -189,39 +236,36 @@ def main():
         run_sharded(args, w, world, rank)
         return
 
-    import paper_2411_03289_b200 as G
-    planner, task = build_planner(w, G, var_path=args.variance_path)
-    x0 = np.array(w.x0, dtype=np.float64)
-    for _ in range(args.warmup):
-        planner.plan_step(x0, task)
-    launches0 = G.kernel_launches()
-    with ClockSampler(0) as clk:
-        tick_ms, phase = planner.bench_device(x0, task, args.steps, flush_l2=True)
-    launches = G.kernel_launches() - launches0
-    # e2e through the public plan_step (host buffers), L2 flushed between ticks
-    e2e_ms = []
-    for _ in range(args.steps):
-        G.flush_l2(0)
-        t0 = time.perf_counter()
-        planner.plan_step(x0, task)
-        e2e_ms.append((time.perf_counter() - t0) * 1e3)
-    h2d, d2h = planner.io_bytes()
+    if args.dry_run:
+        planner, clk = _DryPlanner(), _DryClock()
+        tick_ms, phase = np.full(args.steps, 1.0), np.array([0.4, 0.35, 0.05, 0.2]) * args.steps
+        launches, e2e_ms, (h2d, d2h) = 7 * args.steps, [1.1] * args.steps, (2768, 68)
+    else:
+        import paper_2411_03289_b200 as G
+        planner, task = build_planner(w, G, var_path=args.variance_path)
+        x0 = np.array(w.x0, dtype=np.float64)
+        for _ in range(args.warmup):
+            planner.plan_step(x0, task)
+        launches0 = G.kernel_launches()
+        with ClockSampler(0) as clk:
+            tick_ms, phase = planner.bench_device(x0, task, args.steps, flush_l2=True)
+        launches = G.kernel_launches() - launches0
+        # e2e through the public plan_step (host buffers), L2 flushed between ticks
+        e2e_ms = []
+        for _ in range(args.steps):
+            G.flush_l2(0)
+            t0 = time.perf_counter()
+            planner.plan_step(x0, task)
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        h2d, d2h = planner.io_bytes()
     steps_per_tick = w.samples * w.horizon
     mean_ms = float(np.mean(tick_ms))
     value = steps_per_tick / (mean_ms / 1e3)
     e2e_value = steps_per_tick / (float(np.mean(e2e_ms)) / 1e3)
     peaks, peaks_kind = load_peaks()
-    # roofline of the dominant kernel phase (algorithmic FLOP)
+    roofline = roofline_block(w, phase, args.steps, peaks, peaks_kind)
     n = w.n_points
     rollout_ms, var_ms = phase[0] / args.steps, phase[1] / args.steps
-    var_flop = steps_per_tick * (n * n + 2 * n)
-    roll_flop = steps_per_tick * 22 * n
-    if var_ms >= rollout_ms:
-        dom, dom_ms, dom_flop = "variance", var_ms, var_flop
-    else:
-        dom, dom_ms, dom_flop = "rollout", rollout_ms, roll_flop
-    achieved = dom_flop / (dom_ms / 1e3) / 1e12
-    peak = peaks.get("bf16_tflops", 1590.0)
     line = {
         "metric": "sample-rollout-steps/s (GP-MPPI solve; p50/p99 latency in p50_ms/p99_ms)",
         "value": value, "unit": "sample-rollout-steps/s", "n_gpus": 1, "steps": args.steps,
@@ -238,13 +282,12 @@ def main():
         "e2e": {"value": e2e_value, "unit": "sample-rollout-steps/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "p50_ms": _percentile(e2e_ms, 50),
                 "p99_ms": _percentile(e2e_ms, 99)},
-        "roofline": {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak,
-                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
-                     "peak_kind": f"{peaks_kind} bf16 dense (MEASURED_PEAKS.json)",
-                     "flop_per_launch": dom_flop},
+        "roofline": roofline,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    if args.dry_run:
+        line["dry_run"] = True
     if not args.no_cpu_baseline:
         ms, threads, K = cpu_reference(w, args.cpu_steps, 1, 0)
         cpu_val = K * w.horizon / (statistics.mean(ms) / 1e3)
