@@ -263,15 +263,21 @@ gpmppi_model* build_model(const double* X, const double* Y, int64_t n64, int64_t
     M->dev.n = n;
     M->dev.m = m;
     M->dev.G = (int)M->groups.size();
+    M->dev.ns = (n + 1) & ~1;
     for (int gi = 0; gi < M->dev.G; ++gi) {
       const HostGroup& G = M->groups[gi];
       gpm::GroupDev& D = M->dev.g[gi];
       const int no = (int)G.outputs.size();
-      std::vector<double> pts((size_t)(5 + no) * n);
-      for (int j = 0; j < n; ++j) {
-        for (int d = 0; d < 4; ++d) pts[(size_t)d * n + j] = G.aug[(size_t)j * 6 + d];
-        pts[(size_t)4 * n + j] = G.aug[(size_t)j * 6 + 5];
-        for (int c = 0; c < no; ++c) pts[(size_t)(5 + c) * n + j] = G.alphas[(size_t)j * no + c];
+      const int ns = M->dev.ns;
+      std::vector<double> pts((size_t)(5 + no) * ns, 0.0);
+      for (int j = 0; j < ns; ++j) {
+        if (j >= n) {  // padding point: k* = exp(-1e300) = 0, alpha = 0
+          pts[(size_t)4 * ns + j] = -1e300;
+          continue;
+        }
+        for (int d = 0; d < 4; ++d) pts[(size_t)d * ns + j] = G.aug[(size_t)j * 6 + d];
+        pts[(size_t)4 * ns + j] = G.aug[(size_t)j * 6 + 5];
+        for (int c = 0; c < no; ++c) pts[(size_t)(5 + c) * ns + j] = G.alphas[(size_t)j * no + c];
       }
       std::vector<float> ilt32(G.ilt.size()), zs32((size_t)4 * n);
       for (size_t i = 0; i < G.ilt.size(); ++i) ilt32[i] = (float)G.ilt[i];

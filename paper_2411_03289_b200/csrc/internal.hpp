@@ -13,7 +13,7 @@ namespace gpm {
 
 // One kernel group of the exact GP (gp.hpp:81-92) as uploaded to the device.
 struct GroupDev {
-  const double* pts;   // FP64 SoA [(5 + n_out)][n]: zs0..zs3, zn(+ln sv), alpha_0..alpha_{n_out-1}
+  const double* pts;   // FP64 SoA [(5 + n_out)][ns]: zs0..zs3, zn(+ln sv), alpha_0..alpha_{n_out-1}
   const double* ilt64; // FP64 L^{-T} [n][n] row-major (upper triangular, zeros below)
   const float* ilt32;  // FP32 copy of L^{-T}
   const float* zs32;   // FP32 scaled inputs [4][n]
@@ -27,6 +27,7 @@ struct GroupDev {
 };
 struct ModelDev {
   int n, m, G;
+  int ns;  // stride of the pts SoA arrays: n rounded up to even (padded points contribute 0)
   GroupDev g[kMaxGroups];
 };
 

@@ -83,7 +83,7 @@ size_t rollout_smem_bytes(const RolloutArgs& a) {
   b += sizeof(double) * (size_t)(2 * a.T + a.T + a.T * (a.n_obs > 0 ? a.n_obs : 1) + a.R + 2 + 32);
   b = (b + 15) & ~(size_t)15;
   if (a.model_kind == MODEL_GP)
-    for (int g = 0; g < a.model.G; ++g) b += sizeof(double) * (size_t)(5 + a.model.g[g].n_out) * a.model.n;
+    for (int g = 0; g < a.model.G; ++g) b += sizeof(double) * (size_t)(5 + a.model.g[g].n_out) * a.model.ns;
   return b;
 }
 
@@ -165,15 +165,15 @@ template <int NO, int LPS>
 __global__ void __launch_bounds__(256, 1) rollout_gp_kernel(const RolloutArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   SmemView sv = load_common_smem(a, smem);
-  const int n = a.model.n;
+  const int ns = a.model.ns;  // even SoA stride (padding points contribute exactly 0)
   {  // stage Z / alpha of every group (SoA) into shared memory
     double* dst = sv.pts;
     for (int g = 0; g < a.model.G; ++g) {
-      const int cnt = (5 + a.model.g[g].n_out) * n;
+      const int cnt = (5 + a.model.g[g].n_out) * ns;
       const double2* src = reinterpret_cast<const double2*>(a.model.g[g].pts);
       double2* d2 = reinterpret_cast<double2*>(dst);
-      for (int i = threadIdx.x; i < cnt / 2; i += blockDim.x) d2[i] = src[i];
-      if ((cnt & 1) && threadIdx.x == 0) dst[cnt - 1] = a.model.g[g].pts[cnt - 1];
+#pragma unroll 4
+      for (int i = threadIdx.x; i < cnt / 2; i += blockDim.x) d2[i] = __ldg(src + i);
       dst += cnt;
     }
   }
@@ -231,20 +231,28 @@ __global__ void __launch_bounds__(256, 1) rollout_gp_kernel(const RolloutArgs a)
         double acc[NO];
 #pragma unroll
         for (int o = 0; o < NO; ++o) acc[o] = 0.0;
-        const double* z0 = gp;
-        const double* z1 = gp + n;
-        const double* z2 = gp + 2 * n;
-        const double* z3 = gp + 3 * n;
-        const double* zn = gp + 4 * n;
-        const double* al = gp + 5 * n;
-#pragma unroll 4
-        for (int j = gl; j < n; j += LPS) {
+        // two adjacent points per lane and load (LDS.128): the 32/LPS sample groups of a
+        // warp read the same addresses, so a 16-byte access doubles the bytes per wavefront
+        const double2* z0 = reinterpret_cast<const double2*>(gp);
+        const double2* z1 = reinterpret_cast<const double2*>(gp + ns);
+        const double2* z2 = reinterpret_cast<const double2*>(gp + 2 * ns);
+        const double2* z3 = reinterpret_cast<const double2*>(gp + 3 * ns);
+        const double2* zn = reinterpret_cast<const double2*>(gp + 4 * ns);
+        const double2* al = reinterpret_cast<const double2*>(gp + 5 * ns);
+        const int half = ns >> 1;
+#pragma unroll 2
+        for (int jp = gl; jp < half; jp += LPS) {
           // gp.cpp:177-179: k*_j = exp(q_aug · inputs_aug_j)
-          const double d = q0 * z0[j] + q1 * z1[j] + q2 * z2[j] + q3 * z3[j] + qn + zn[j];
-          const double kj = exp_tab(d, sv.etab);
+          const double2 a0 = z0[jp], a1 = z1[jp], a2 = z2[jp], a3 = z3[jp], an = zn[jp];
+          const double d0 = q0 * a0.x + q1 * a1.x + q2 * a2.x + q3 * a3.x + qn + an.x;
+          const double d1 = q0 * a0.y + q1 * a1.y + q2 * a2.y + q3 * a3.y + qn + an.y;
+          const double k0 = exp_tab(d0, sv.etab), k1 = exp_tab(d1, sv.etab);
 #pragma unroll
           for (int o = 0; o < NO; ++o)
-            if (o < nout) acc[o] = fma(kj, al[o * n + j], acc[o]);  // gp.cpp:181-182
+            if (o < nout) {
+              const double2 ao = al[o * half + jp];
+              acc[o] = fma(k1, ao.y, fma(k0, ao.x, acc[o]));  // gp.cpp:181-182
+            }
         }
 #pragma unroll
         for (int o = 0; o < NO; ++o) {
@@ -258,7 +266,7 @@ __global__ void __launch_bounds__(256, 1) rollout_gp_kernel(const RolloutArgs a)
               cm0 += wt * mo;
           }
         }
-        gp += (size_t)(5 + nout) * n;
+        gp += (size_t)(5 + nout) * ns;
       }
       v = v + av * (u0 - v) + cm0;  // step_nominal lag (dynamics.cpp:63-64) + mppi.cpp:341-342
       w = w + aw * (u1 - w) + cm1;
@@ -830,7 +838,7 @@ cudaError_t launch_finish(const double* tuples, int n, int T, double lambda, dou
 // Returns per-output mean (into mean[m]) and per-group variance (var_g[G]).
 GPM_D void block_gp_predict(const ModelDev& M, const double q[4], double* kst /*n*/,
                             double* red /*>= 32*8*/, double* mean /*m*/, double* var_g) {
-  const int n = M.n;
+  const int n = M.n, ns = M.ns;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int g = 0; g < M.G; ++g) {
     const GroupDev& G = M.g[g];
@@ -840,10 +848,10 @@ GPM_D void block_gp_predict(const ModelDev& M, const double q[4], double* kst /*
     double acc[kMaxOutPerGroup];
     for (int o = 0; o < kMaxOutPerGroup; ++o) acc[o] = 0.0;
     for (int j = threadIdx.x; j < n; j += blockDim.x) {
-      const double d = q0 * p[j] + q1 * p[n + j] + q2 * p[2 * n + j] + q3 * p[3 * n + j] + qn + p[4 * n + j];
+      const double d = q0 * p[j] + q1 * p[ns + j] + q2 * p[2 * ns + j] + q3 * p[3 * ns + j] + qn + p[4 * ns + j];
       const double kj = exp(d);
       kst[j] = kj;
-      for (int o = 0; o < G.n_out; ++o) acc[o] = fma(kj, p[(5 + o) * n + j], acc[o]);
+      for (int o = 0; o < G.n_out; ++o) acc[o] = fma(kj, p[(5 + o) * ns + j], acc[o]);
     }
     for (int o = 0; o < G.n_out; ++o) {
       const double s = warp_sum(acc[o]);
@@ -948,12 +956,11 @@ __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const Tight
   if (a.model_kind == MODEL_GP) {  // vectorised staging of Z / alpha
     double* dst = pts;
     for (int g = 0; g < a.model.G; ++g) {
-      const int cnt = (5 + a.model.g[g].n_out) * n;
+      const int cnt = (5 + a.model.g[g].n_out) * a.model.ns;
       const double2* src = reinterpret_cast<const double2*>(a.model.g[g].pts);
       double2* d2 = reinterpret_cast<double2*>(dst);
 #pragma unroll 4
       for (int i = threadIdx.x; i < cnt / 2; i += blockDim.x) d2[i] = __ldg(src + i);
-      if ((cnt & 1) && threadIdx.x == 0) dst[cnt - 1] = a.model.g[g].pts[cnt - 1];
       dst += cnt;
     }
   }
@@ -969,6 +976,7 @@ __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const Tight
   __shared__ int gch[kMaxGroups][NO];         // 0: v channel, 1: omega channel, -1: unused
   __shared__ int gno[kMaxGroups];
   const int nwarps = blockDim.x >> 5;
+  const int ns = a.model.ns;
   const int G = a.model_kind == MODEL_GP ? a.model.G : 0;
   if (threadIdx.x == 0) {  // group constants out of the (register-indexed) parameter space
     for (int g = 0; g < G; ++g) {
@@ -999,17 +1007,17 @@ __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const Tight
         for (int o = 0; o < NO; ++o) acc[o] = 0.0;
 #pragma unroll 4
         for (int j = threadIdx.x; j < n; j += TMEAN_THREADS) {
-          const double kj = exp_tab(q0 * p[j] + q1 * p[n + j] + q2 * p[2 * n + j] + q3 * p[3 * n + j] + qn + p[4 * n + j], etab);
+          const double kj = exp_tab(q0 * p[j] + q1 * p[ns + j] + q2 * p[2 * ns + j] + q3 * p[3 * ns + j] + qn + p[4 * ns + j], etab);
 #pragma unroll
           for (int o = 0; o < NO; ++o)
-            if (o < no) acc[o] = fma(kj, p[(5 + o) * n + j], acc[o]);
+            if (o < no) acc[o] = fma(kj, p[(5 + o) * ns + j], acc[o]);
         }
 #pragma unroll
         for (int o = 0; o < NO; ++o) {
           const double sm = warp_sum(acc[o]);
           if (lane == 0) red[k & 1][w][g * NO + o] = sm;
         }
-        p += (size_t)(5 + no) * n;
+        p += (size_t)(5 + no) * ns;
       }
       __syncthreads();
       for (int g = 0; g < G; ++g) {
@@ -1085,8 +1093,9 @@ __global__ void __launch_bounds__(TIGHT_COLS) tighten_var_kernel(const TightenAr
   const int j0 = c * TIGHT_COLS;
   const int jend = min(n, j0 + TIGHT_COLS);
   const double* p = G.pts;
+  const int ns = a.model.ns;
   for (int i = threadIdx.x; i < jend; i += blockDim.x)  // rows i <= j only
-    kst[i] = exp(q0 * p[i] + q1 * p[n + i] + q2 * p[2 * n + i] + q3 * p[3 * n + i] + qn + p[4 * n + i]);
+    kst[i] = exp(q0 * p[i] + q1 * p[ns + i] + q2 * p[2 * ns + i] + q3 * p[3 * ns + i] + qn + p[4 * ns + i]);
   __syncthreads();
   double ssq = 0.0;
   const int j = j0 + threadIdx.x;
@@ -1226,7 +1235,7 @@ int tighten_splits(int n) { return n > 0 ? (n + TIGHT_COLS - 1) / TIGHT_COLS : 1
 cudaError_t launch_tighten(const TightenArgs& a, cudaStream_t st) {
   size_t msm = sizeof(double) * (size_t)(2 * a.T + 3 * (a.T + 1) + 2 * a.T + 1);
   if (a.model_kind == MODEL_GP)
-    for (int g = 0; g < a.model.G; ++g) msm += sizeof(double) * (size_t)(5 + a.model.g[g].n_out) * a.model.n;
+    for (int g = 0; g < a.model.G; ++g) msm += sizeof(double) * (size_t)(5 + a.model.g[g].n_out) * a.model.ns;
   int no = 1;
   if (a.model_kind == MODEL_GP)
     for (int g = 0; g < a.model.G; ++g) no = a.model.g[g].n_out > no ? a.model.g[g].n_out : no;
