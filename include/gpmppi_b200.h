@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define GPMPPI_ABI_VERSION 1
+#define GPMPPI_ABI_VERSION 2
 
 typedef enum {
   GPMPPI_OK = 0,
@@ -161,19 +161,33 @@ int gpmppi_planner_create(const gpmppi_mppi_config* cfg, const gpmppi_prediction
                           const gpmppi_nominal* nominal, double p_x, int device,
                           gpmppi_planner** out);
 void gpmppi_planner_free(gpmppi_planner* p);
+/* B independent planners sharing one model (BASELINE config 4):
+ * robot b behaves exactly like gpmppi_planner_create with cfg.seed = seeds[b]
+ * (seeds may be NULL: cfg.seed + b). Every per-robot array of the getters/setters
+ * below is robot-major ([B][...]); B = 1 gives the single-planner layout. */
+int gpmppi_planner_create_batch(const gpmppi_mppi_config* cfg, const gpmppi_prediction_model* model,
+                                const gpmppi_nominal* nominal, double p_x, int n_robots,
+                                const uint64_t* seeds, int device, gpmppi_planner** out);
+int gpmppi_planner_robots(const gpmppi_planner* p);
 /* Planner::plan_step (mppi.cpp:389-475), both overloads + the combined task. Host
  * buffers in, host command out; the GPU work runs on the planner's stream. */
 int gpmppi_planner_plan_step(gpmppi_planner* p, const double x0[5], const gpmppi_task* task,
                              double command[2], gpmppi_diag* diag);
-int gpmppi_planner_set_terrain_weights(gpmppi_planner* p, const double* w, int R); /* :208-218 */
-int gpmppi_planner_terrain_weights(const gpmppi_planner* p, double* w);      /* returns R */
-int gpmppi_planner_nominal_sequence(const gpmppi_planner* p, double* seq);   /* T×2 */
+/* one tick of every robot: x0 [B][5], tasks [B], commands [B][2], diags [B] or NULL */
+int gpmppi_planner_plan_step_batch(gpmppi_planner* p, const double* x0, const gpmppi_task* tasks,
+                                   double* commands, gpmppi_diag* diags);
+/* Planner::set_terrain_weights (mppi.cpp:208-218): every robot / one robot */
+int gpmppi_planner_set_terrain_weights(gpmppi_planner* p, const double* w, int R);
+int gpmppi_planner_set_robot_terrain_weights(gpmppi_planner* p, int robot, const double* w, int R);
+int gpmppi_planner_terrain_weights(const gpmppi_planner* p, double* w);      /* [B][R], returns R */
+int gpmppi_planner_nominal_sequence(const gpmppi_planner* p, double* seq);   /* [B][T][2] */
 int gpmppi_planner_set_nominal_sequence(gpmppi_planner* p, const double* seq);
-int gpmppi_planner_horizon_covariances(const gpmppi_planner* p, double* cov); /* T×5×5 */
-int gpmppi_planner_lane_radii(const gpmppi_planner* p, double* r);    /* returns T, 0 if unset */
-int gpmppi_planner_obstacle_margins(const gpmppi_planner* p, double* m); /* T×O, returns O */
+int gpmppi_planner_horizon_covariances(const gpmppi_planner* p, double* cov); /* [B][T][5][5] */
+int gpmppi_planner_lane_radii(const gpmppi_planner* p, double* r);    /* [B][T]; returns T, 0 if no robot has radii yet */
+/* [B][T][O] with O = max obstacle count over robots (zero-padded); returns O */
+int gpmppi_planner_obstacle_margins(const gpmppi_planner* p, double* m);
 int gpmppi_planner_set_thresholds(gpmppi_planner* p, const double* r_bar, const double* margins,
-                                  int n_obstacles);
+                                  int n_obstacles); /* [B][T], [B][T][n_obstacles] */
 uint64_t gpmppi_planner_tick(const gpmppi_planner* p);
 int gpmppi_planner_horizon(const gpmppi_planner* p);
 int gpmppi_planner_samples(const gpmppi_planner* p);
@@ -181,15 +195,15 @@ int gpmppi_planner_samples(const gpmppi_planner* p);
 /* ---- noise (north star: Philox production sampler + injection hook) ---- */
 enum { GPMPPI_NOISE_PHILOX = 0, GPMPPI_NOISE_INJECTED = 1 };
 int gpmppi_planner_set_noise_mode(gpmppi_planner* p, int mode);
-/* eps K×T×2 (this rank's samples), used by every following tick until replaced */
+/* eps [B][K][T][2] (this rank's samples), used by every following tick until replaced */
 int gpmppi_planner_inject_noise(gpmppi_planner* p, const double* eps);
-/* materialise the Philox noise the planner uses at tick t (K×T×2) */
+/* materialise the Philox noise the planner uses at tick t ([B][K][T][2]) */
 int gpmppi_planner_philox_noise(const gpmppi_planner* p, uint64_t tick, double* eps);
 
 /* ---- parity outputs of the last plan_step ---- */
-int gpmppi_planner_sample_costs(const gpmppi_planner* p, double* costs);   /* K */
-int gpmppi_planner_sample_weights(const gpmppi_planner* p, double* w);     /* K */
-/* per-step lane-violation and collision flags, terminal-capture and alive per sample */
+int gpmppi_planner_sample_costs(const gpmppi_planner* p, double* costs);   /* [B][K] */
+int gpmppi_planner_sample_weights(const gpmppi_planner* p, double* w);     /* [B][K] */
+/* per-step lane-violation and collision flags [B][K][T], terminal-capture and alive [B][K] */
 int gpmppi_planner_flags(const gpmppi_planner* p, uint8_t* viol, uint8_t* coll,
                          uint8_t* terminal, uint8_t* alive);
 
@@ -203,11 +217,12 @@ int gpmppi_planner_variance_path(const gpmppi_planner* p);
  * on the planner's stream; with flush_l2 a >L2-sized memset runs between ticks
  * outside the timed spans. phase_ms[0..3] = summed event time of rollout,
  * variance, reduce+update, tightening. */
-int gpmppi_planner_bench_device(gpmppi_planner* p, const double x0[5], const gpmppi_task* task,
+int gpmppi_planner_bench_device(gpmppi_planner* p, const double* x0, const gpmppi_task* tasks,
                                 int ticks, int flush_l2, double* tick_ms, double* phase_ms);
 /* write a buffer twice the L2 size on `device` and synchronise */
 int gpmppi_flush_l2(int device);
-/* bytes one plan_step copies host->device (x0 + task) and device->host (command + diag) */
+/* bytes one plan_step copies host->device (robot tick blocks + tasks) and device->host
+ * (command + diag), all robots */
 int gpmppi_planner_io_bytes(const gpmppi_planner* p, int64_t* h2d, int64_t* d2h);
 
 /* ---- sharded solve (multi-GPU) ----

@@ -4,7 +4,7 @@ compute runs in lib/libgpmppi_b200.so (sm_100a CUDA) through a C ABI."""
 from .gpmppi import (  # noqa: F401
     AvoidanceTask, AvoidanceWeights, CircleObstacle, CombinedTask, ControlBounds, Edd5Baseline,
     Edd5Params, GoalSpec, GpEnsemble, GpModel, KernelParams, MppiConfig, NominalDynamic,
-    NominalParams, Planner, StepDiagnostics, Track, TrackingTask, TrackingWeights,
+    NominalParams, Planner, BatchPlanner, StepDiagnostics, Track, TrackingTask, TrackingWeights,
     UnicycleBaseline, apply_tuple, chi2_quantile_2dof, combine_tuples, flush_l2,
     kernel_launches, shard_range, tuple_doubles)
 from ._capi import (  # noqa: F401

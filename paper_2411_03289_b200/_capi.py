@@ -23,6 +23,7 @@ NOISE_PHILOX, NOISE_INJECTED = 0, 1
 VAR_FFMA, VAR_TC_3XTF32, VAR_TC_1XTF32 = 0, 1, 2
 MAX_WAYPOINTS = 64
 MAX_OBSTACLES = 64
+MAX_TERRAINS = 16
 
 
 class CudaError(RuntimeError):
@@ -97,7 +98,13 @@ SIGNATURES = [
     ("gpmppi_model_variance_batch", C.c_int, [_vp, _dp, C.c_int64, C.c_int, _dp]),
     ("gpmppi_planner_create", C.c_int, [C.POINTER(MppiConfigC), C.POINTER(PredictionModelC),
                                         C.POINTER(NominalC), C.c_double, C.c_int, C.POINTER(_vp)]),
+    ("gpmppi_planner_create_batch", C.c_int, [C.POINTER(MppiConfigC), C.POINTER(PredictionModelC),
+                                              C.POINTER(NominalC), C.c_double, C.c_int,
+                                              C.POINTER(C.c_uint64), C.c_int, C.POINTER(_vp)]),
     ("gpmppi_planner_free", None, [_vp]),
+    ("gpmppi_planner_robots", C.c_int, [_vp]),
+    ("gpmppi_planner_plan_step_batch", C.c_int, [_vp, _dp, C.POINTER(TaskC), _dp, C.POINTER(DiagC)]),
+    ("gpmppi_planner_set_robot_terrain_weights", C.c_int, [_vp, C.c_int, _dp, C.c_int]),
     ("gpmppi_planner_plan_step", C.c_int, [_vp, _dp, C.POINTER(TaskC), _dp, C.POINTER(DiagC)]),
     ("gpmppi_planner_set_terrain_weights", C.c_int, [_vp, _dp, C.c_int]),
     ("gpmppi_planner_terrain_weights", C.c_int, [_vp, _dp]),

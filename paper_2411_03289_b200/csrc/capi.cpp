@@ -463,26 +463,29 @@ struct gpmppi_planner {
   int model_kind = 0;
   const gpmppi_model* model = nullptr;
   int R = 1;
+  int B = 1;                    // robots (independent planners sharing the model)
+  std::vector<uint64_t> seeds;  // [B] noise seed of each robot
   gpm::Edd5Dev edd5{};
   gpm::NominalDev nom{};
   double p_x = 0.95, chi2 = 0.0, z = 0.0;
-  std::vector<double> tw;
+  std::vector<double> tw;  // [B][R]
   uint64_t tick = 0;
   int noise_mode = gpm::NOISE_PHILOX;
   bool injected_set = false;
   int var_path = GPMPPI_VAR_TC_3XTF32;  // tensor cores within the stated tolerance
   long long s_begin = 0, K_local = 0, K_total = 0;
-  bool rbar_init = false;
-  int margins_O = -1;
-  int reduce_blocks = 1;
-  int last_task_kind = -1;
+  std::vector<uint8_t> rbar_init;  // [B]
+  std::vector<int> margins_O;      // [B] obstacle count the margins were sized for
+  int n_obs_max = 0;
+  int reduce_blocks = 1;  // per robot
   int T = 0, words = 1;
-  // device buffers
+  signed char coef_terrain[gpm::kMaxGroups][8];
+  // device buffers (robot-major, strides in gpm::BatchStrides)
   std::vector<void*> allocs;
   double *d_nom = nullptr, *d_tw = nullptr, *d_x0 = nullptr, *d_rbar = nullptr, *d_margins = nullptr;
   double* d_eps = nullptr;
   gpm::TaskDev* d_task = nullptr;
-  double *d_cost_mean = nullptr, *d_trace = nullptr, *d_costs = nullptr, *d_e = nullptr;
+  double *d_cost_mean = nullptr, *d_var = nullptr, *d_costs = nullptr, *d_e = nullptr;
   float4* d_queries = nullptr;
   uint32_t *d_viol = nullptr, *d_coll = nullptr;
   uint8_t *d_term = nullptr, *d_alive = nullptr;
@@ -493,10 +496,10 @@ struct gpmppi_planner {
   double *d_tq = nullptr, *d_tmu = nullptr, *d_tJ = nullptr, *d_tvar = nullptr;
   double* d_scratch = nullptr;
   // pinned staging
-  gpm::TaskDev* h_task = nullptr;
-  double* h_x0 = nullptr;
-  double* h_out = nullptr;
-  int* h_infeasible = nullptr;
+  gpm::TaskDev* h_task = nullptr;  // [B]
+  double* h_x0 = nullptr;          // [B][8] robot tick blocks
+  double* h_out = nullptr;         // [B][16]
+  int* h_infeasible = nullptr;     // [B]
   cudaEvent_t ev[8] = {};
 
   template <class T>
@@ -519,22 +522,24 @@ struct gpmppi_planner {
       if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
   }
+  long long slots() const { return (long long)B * K_local; }
+  int groups() const { return model ? model->dev.G : 0; }
   void alloc_sample_buffers() {
-    const long long K = K_local;
-    d_cost_mean = dalloc<double>(K);
-    d_costs = dalloc<double>(K);
-    d_e = dalloc<double>(K);
-    d_viol = dalloc<uint32_t>((size_t)K * words);
-    d_coll = dalloc<uint32_t>((size_t)K * words);
-    d_term = dalloc<uint8_t>(K);
-    d_alive = dalloc<uint8_t>(K);
+    const long long S = slots();
+    d_cost_mean = dalloc<double>(S);
+    d_costs = dalloc<double>(S);
+    d_e = dalloc<double>(S);
+    d_viol = dalloc<uint32_t>((size_t)S * words);
+    d_coll = dalloc<uint32_t>((size_t)S * words);
+    d_term = dalloc<uint8_t>(S);
+    d_alive = dalloc<uint8_t>(S);
     if (model_kind == GPMPPI_MODEL_GP_ENSEMBLE) {
-      d_queries = dalloc<float4>((size_t)K * T);
-      d_trace = dalloc<double>((size_t)K * T);
+      d_queries = dalloc<float4>((size_t)S * T);
+      d_var = dalloc<double>((size_t)groups() * S * T);
       if (!d_scratch) d_scratch = dalloc<double>(gpm::rollout_scratch_doubles(T, num_sms));
     }
-    reduce_blocks = gpm::reduce_blocks_for((int)K, num_sms);
-    d_partials = dalloc<double>((size_t)reduce_blocks * gpm::tuple_doubles(T));
+    reduce_blocks = gpm::reduce_blocks_for((int)K_local, B, num_sms);
+    d_partials = dalloc<double>((size_t)B * reduce_blocks * gpm::tuple_doubles(T));
   }
 };
 
@@ -647,52 +652,73 @@ void check(cudaError_t e, const char* where) {
   if (e != cudaSuccess) throw CudaError{e, where};
 }
 
-// mppi.cpp:235-248 ensure_thresholds + per-tick upload of x0 and the task.
-void stage_tick(gpmppi_planner* p, const double x0[5], const gpmppi_task* task) {
-  for (int i = 0; i < 5; ++i)
-    if (!std::isfinite(x0[i])) invalid("plan_step: non-finite state estimate");
-  validate_task(task);
+double task_var_weight(const gpmppi_task* t) {
+  return t->kind == GPMPPI_TASK_AVOIDANCE ? t->avoidance.variance : t->tracking.variance;
+}
+
+// mppi.cpp:235-248 ensure_thresholds + the per-tick upload of every robot's state,
+// task, variance weight and Philox key (two H2D copies for all B robots).
+void stage_tick(gpmppi_planner* p, const double* x0, const gpmppi_task* tasks) {
+  if (!x0 || !tasks) invalid("plan_step: null state or task");
   const int T = p->T;
-  if (task->kind != GPMPPI_TASK_AVOIDANCE && !p->rbar_init) {
-    std::vector<double> r(T, task->track->half_width);
-    CK(cudaMemcpyAsync(p->d_rbar, r.data(), sizeof(double) * T, cudaMemcpyHostToDevice, p->stream));
-    CK(cudaStreamSynchronize(p->stream));
-    p->rbar_init = true;
+  for (int b = 0; b < p->B; ++b) {
+    for (int i = 0; i < 5; ++i)
+      if (!std::isfinite(x0[5 * b + i])) invalid("plan_step: non-finite state estimate");
+    validate_task(&tasks[b]);
   }
-  if (task->kind != GPMPPI_TASK_TRACKING && p->margins_O != task->n_obstacles) {
-    CK(cudaMemsetAsync(p->d_margins, 0, sizeof(double) * T * gpm::kMaxObstacles, p->stream));
-    p->margins_O = task->n_obstacles;
+  int omax = 0;
+  bool synced = false;
+  for (int b = 0; b < p->B; ++b) {
+    const gpmppi_task* task = &tasks[b];
+    if (task->kind != GPMPPI_TASK_AVOIDANCE && !p->rbar_init[b]) {
+      if (!synced) {  // the pinned staging buffers may still feed the previous tick's copies
+        CK(cudaStreamSynchronize(p->stream));
+        synced = true;
+      }
+      std::vector<double> r(T, task->track->half_width);
+      CK(cudaMemcpy(p->d_rbar + (size_t)b * gpm::BatchStrides::rbar(T), r.data(), sizeof(double) * T,
+                    cudaMemcpyHostToDevice));
+      p->rbar_init[b] = 1;
+    }
+    const int O = task->kind == GPMPPI_TASK_TRACKING ? 0 : task->n_obstacles;
+    if (task->kind != GPMPPI_TASK_TRACKING && p->margins_O[b] != O) {
+      CK(cudaMemsetAsync(p->d_margins + (size_t)b * gpm::BatchStrides::marg(T), 0,
+                         sizeof(double) * gpm::BatchStrides::marg(T), p->stream));
+      p->margins_O[b] = O;
+    }
+    omax = std::max(omax, O);
   }
-  fill_task(*p->h_task, task);
-  std::memcpy(p->h_x0, x0, sizeof(double) * 5);
-  CK(cudaMemcpyAsync(p->d_task, p->h_task, sizeof(gpm::TaskDev), cudaMemcpyHostToDevice, p->stream));
-  CK(cudaMemcpyAsync(p->d_x0, p->h_x0, sizeof(double) * 5, cudaMemcpyHostToDevice, p->stream));
-  p->last_task_kind = task->kind;
+  CK(cudaStreamSynchronize(p->stream));  // previous tick's staging copies are done
+  for (int b = 0; b < p->B; ++b) {
+    fill_task(p->h_task[b], &tasks[b]);
+    double* blk = p->h_x0 + (size_t)b * gpm::BatchStrides::X0;
+    for (int i = 0; i < 5; ++i) blk[i] = x0[5 * b + i];
+    blk[5] = task_var_weight(&tasks[b]);
+    const uint64_t key = gpm::philox_key(p->seeds[b], p->tick);
+    std::memcpy(&blk[6], &key, sizeof key);
+    blk[7] = 0.0;
+  }
+  p->n_obs_max = omax;
+  CK(cudaMemcpyAsync(p->d_task, p->h_task, sizeof(gpm::TaskDev) * p->B, cudaMemcpyHostToDevice, p->stream));
+  CK(cudaMemcpyAsync(p->d_x0, p->h_x0, sizeof(double) * gpm::BatchStrides::X0 * p->B,
+                     cudaMemcpyHostToDevice, p->stream));
 }
 
-double trace_coef(const gpmppi_planner* p, const gpm::GroupDev& g) {
-  double c = 0.0;
-  for (int o = 0; o < g.n_out; ++o) {
-    const double w = p->tw[g.out_idx[o] >> 1];
-    c += w * w;
-  }
-  return c;
-}
-
-// Rollout + variance + reduce for this planner's sample range. finish=1 also
+// Rollout + variance + reduce for every robot's sample range. finish=1 also
 // applies the update (single-rank solve).
-void enqueue_samples(gpmppi_planner* p, int n_obs, double var_w, int finish, cudaEvent_t* evs) {
+void enqueue_samples(gpmppi_planner* p, int finish, cudaEvent_t* evs) {
   const int T = p->T;
-  const uint64_t key = gpm::philox_key(p->cfg.seed, p->tick);
   gpm::RolloutArgs a{};
   if (p->model) a.model = p->model->dev;
   a.model_kind = p->model_kind;
   a.nom = p->nom;
   a.edd5 = p->edd5;
+  a.B = p->B;
   a.K_local = (int)p->K_local;
+  a.K_total = p->K_total;
   a.s_begin = p->s_begin;
   a.T = T;
-  a.n_obs = n_obs;
+  a.n_obs_max = p->n_obs_max;
   a.lo[0] = p->cfg.lo[0];
   a.lo[1] = p->cfg.lo[1];
   a.hi[0] = p->cfg.hi[0];
@@ -701,7 +727,6 @@ void enqueue_samples(gpmppi_planner* p, int n_obs, double var_w, int finish, cud
   a.sw = std::sqrt(p->cfg.sigma_w2);
   a.noise_mode = p->noise_mode;
   a.eps = p->d_eps;
-  a.key = key;
   a.nominal_seq = p->d_nom;
   a.tw = p->d_tw;
   a.R = p->R;
@@ -721,31 +746,37 @@ void enqueue_samples(gpmppi_planner* p, int n_obs, double var_w, int finish, cud
   check(gpm::launch_rollout(a, p->num_sms, p->stream), "rollout kernel");
   if (evs) CK(cudaEventRecord(evs[1], p->stream));
   const bool gp = p->model_kind == GPMPPI_MODEL_GP_ENSEMBLE;
+  const long long KT = p->slots() * T;
   if (gp) {
-    for (int g = 0; g < p->model->dev.G; ++g) {
+    for (int g = 0; g < p->groups(); ++g) {  // raw variances; the reduce applies Σ w² per robot
       gpm::VarianceArgs v{};
       v.queries = p->d_queries;
-      v.KT = (long long)p->K_local * T;
+      v.KT = KT;
       v.n = p->model->n;
       v.g = p->model->dev.g[g];
-      v.coef = trace_coef(p, v.g);
-      v.accumulate = g > 0;
-      v.trace = p->d_trace;
+      v.coef = 1.0;
+      v.accumulate = 0;
+      v.trace = p->d_var + (size_t)g * KT;
       check(gpm::launch_variance(v, p->var_path, p->stream), "variance kernel");
     }
   }
   if (evs) CK(cudaEventRecord(evs[2], p->stream));
   gpm::ReduceArgs r{};
+  r.B = p->B;
   r.K_local = (int)p->K_local;
+  r.K_total = p->K_total;
   r.s_begin = p->s_begin;
   r.T = T;
+  r.bpr = p->reduce_blocks;
   r.lambda = p->cfg.lambda;
   r.cost_mean = p->d_cost_mean;
-  r.trace = gp ? p->d_trace : nullptr;
-  r.var_w = var_w;
+  r.var = gp ? p->d_var : nullptr;
+  r.G = gp ? p->groups() : 0;
+  r.tw = p->d_tw;
+  std::memcpy(r.coef_terrain, p->coef_terrain, sizeof r.coef_terrain);
+  r.x0 = p->d_x0;
   r.noise_mode = p->noise_mode;
   r.eps = p->d_eps;
-  r.key = key;
   r.sv = a.sv;
   r.sw = a.sw;
   r.costs_out = p->d_costs;
@@ -760,8 +791,7 @@ void enqueue_samples(gpmppi_planner* p, int n_obs, double var_w, int finish, cud
   r.hi[0] = p->cfg.hi[0];
   r.hi[1] = p->cfg.hi[1];
   r.out = p->d_out;
-  r.K_total = p->K_total;
-  check(gpm::launch_reduce(r, p->reduce_blocks, p->stream), "reduce kernel");
+  check(gpm::launch_reduce(r, p->B * p->reduce_blocks, p->stream), "reduce kernel");
   if (evs) CK(cudaEventRecord(evs[3], p->stream));
 }
 
@@ -770,6 +800,7 @@ void enqueue_tighten(gpmppi_planner* p) {
   if (p->model) t.model = p->model->dev;
   t.model_kind = p->model_kind;
   t.nom = p->nom;
+  t.B = p->B;
   t.T = p->T;
   t.tw = p->d_tw;
   t.R = p->R;
@@ -789,28 +820,181 @@ void enqueue_tighten(gpmppi_planner* p) {
   check(gpm::launch_tighten(t, p->stream), "tighten kernel");
 }
 
-double task_var_weight(const gpmppi_task* t) {
-  return t->kind == GPMPPI_TASK_AVOIDANCE ? t->avoidance.variance : t->tracking.variance;
+void copy_out_async(gpmppi_planner* p) {  // command + diagnostics of every robot
+  CK(cudaMemcpyAsync(p->h_out, p->d_out, sizeof(double) * gpm::BatchStrides::OUT * p->B,
+                     cudaMemcpyDeviceToHost, p->stream));
 }
 
-void fill_diag(gpmppi_planner* p, double command[2], gpmppi_diag* diag, double t_cmd, double t_all) {
-  command[0] = p->h_out[0];
-  command[1] = p->h_out[1];
-  if (diag) {
-    diag->best_cost = p->h_out[2];
-    diag->mean_cost = p->h_out[3];
-    diag->ess = p->h_out[4];
-    diag->weight_entropy = p->h_out[5];
-    diag->nonfinite_samples = (int)p->h_out[6];
-    diag->tightening_infeasible = *p->h_infeasible;
-    diag->plan_ms = t_all;
-    diag->command_ms = t_cmd;
+void fill_diag(gpmppi_planner* p, double* command, gpmppi_diag* diag, double t_cmd, double t_all) {
+  for (int b = 0; b < p->B; ++b) {
+    const double* o = p->h_out + (size_t)b * gpm::BatchStrides::OUT;
+    command[2 * b] = o[0];
+    command[2 * b + 1] = o[1];
+    if (diag) {
+      gpmppi_diag& d = diag[b];
+      d.best_cost = o[2];
+      d.mean_cost = o[3];
+      d.ess = o[4];
+      d.weight_entropy = o[5];
+      d.nonfinite_samples = (int)o[6];
+      d.tightening_infeasible = p->h_infeasible[b];
+      d.plan_ms = t_all;
+      d.command_ms = t_cmd;
+    }
   }
 }
 
 using Clock = std::chrono::steady_clock;
 double ms_since(Clock::time_point t0) {
   return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+}
+
+void upload_terrain_weights(gpmppi_planner* p) {
+  std::vector<double> w((size_t)p->B * gpm::BatchStrides::TW, 0.0);
+  for (int b = 0; b < p->B; ++b)
+    for (int i = 0; i < p->R; ++i) w[(size_t)b * gpm::BatchStrides::TW + i] = p->tw[(size_t)b * p->R + i];
+  CK(cudaStreamSynchronize(p->stream));
+  CK(cudaMemcpy(p->d_tw, w.data(), sizeof(double) * w.size(), cudaMemcpyHostToDevice));
+}
+
+gpmppi_planner* create_planner(const gpmppi_mppi_config* cfg, const gpmppi_prediction_model* pm,
+                               const gpmppi_nominal* nominal, double p_x, int n_robots,
+                               const uint64_t* seeds, int device) {
+  if (!cfg || !pm || !nominal) invalid("Planner: null argument");
+  if (!(p_x > 0.5) || !(p_x < 1.0)) invalid("QuantileTables: p_x must lie in (0.5, 1)");
+  if (cfg->samples < 1 || cfg->horizon < 1) invalid("MppiConfig: samples and horizon must be >= 1");
+  if (!(cfg->lambda > 0.0)) invalid("MppiConfig: lambda must be positive");
+  if (!(cfg->sigma_v2 > 0.0) || !(cfg->sigma_w2 > 0.0))
+    invalid("MppiConfig: sampling variances must be positive");
+  if (cfg->lo[0] >= cfg->hi[0] || cfg->lo[1] >= cfg->hi[1])
+    invalid("MppiConfig: control bounds must be a nonempty box");
+  if (!(nominal->tau_v > 0.0) || !(nominal->tau_omega > 0.0))
+    invalid("NominalParams: time constants must be positive");
+  if (!(nominal->dt > 0.0) || nominal->dt >= std::min(nominal->tau_v, nominal->tau_omega))
+    invalid("NominalParams: require 0 < dt < min(tau_v, tau_omega)");
+  if (pm->kind < 0 || pm->kind > 3) invalid("Planner: unknown prediction model");
+  if (pm->kind == GPMPPI_MODEL_GP_ENSEMBLE &&
+      (pm->gp == nullptr || pm->n_terrains < 1 || pm->gp->m != 2 * pm->n_terrains))
+    invalid("Planner: GP ensemble needs a model with 2M outputs");
+  if (pm->kind == GPMPPI_MODEL_GP_ENSEMBLE && pm->n_terrains > gpm::kMaxTerrains)
+    invalid("Planner: too many terrains for the device planner");
+  if (pm->kind == GPMPPI_MODEL_EDD5) {
+    if (!(pm->track_width > 0.0)) invalid("step_edd5: track_width must be positive");
+    if (pm->edd5.y_icr_r - pm->edd5.y_icr_l <= 1e-6)
+      invalid("step_edd5: degenerate ICR span (y_icr_r - y_icr_l <= 1e-6)");
+  }
+  if (n_robots < 1) invalid("Planner: robot count must be >= 1");
+  if ((long long)n_robots * cfg->samples * cfg->horizon > (1LL << 31) - 1)
+    invalid("Planner: robots x samples x horizon exceeds 2^31 sample-steps");
+  require_device(device);
+  auto* p = new gpmppi_planner();
+  try {
+    p->device = device;
+    CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    CK(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device));
+    p->cfg = *cfg;
+    p->B = n_robots;
+    p->seeds.resize(n_robots);
+    for (int b = 0; b < n_robots; ++b) p->seeds[b] = seeds ? seeds[b] : cfg->seed + (uint64_t)b;
+    p->model_kind = pm->kind;
+    p->model = pm->kind == GPMPPI_MODEL_GP_ENSEMBLE ? pm->gp : nullptr;
+    if (p->model && p->model->device != device) invalid("Planner: GP model lives on another device");
+    p->R = pm->kind == GPMPPI_MODEL_GP_ENSEMBLE ? pm->n_terrains : 1;
+    std::memset(p->coef_terrain, -1, sizeof p->coef_terrain);
+    for (int g = 0; g < p->groups(); ++g)
+      for (int o = 0; o < p->model->dev.g[g].n_out && o < 8; ++o)
+        p->coef_terrain[g][o] = (signed char)(p->model->dev.g[g].out_idx[o] >> 1);
+    p->edd5 = {pm->edd5.alpha_l, pm->edd5.alpha_r, pm->edd5.x_icr, pm->edd5.y_icr_l,
+               pm->edd5.y_icr_r, pm->track_width};
+    p->nom = {nominal->tau_v, nominal->tau_omega, nominal->dt};
+    p->p_x = p_x;
+    p->chi2 = -2.0 * std::log1p(-p_x);  // uncertainty.cpp:8-13
+    p->z = normal_quantile(p_x);
+    p->tw.assign((size_t)n_robots * p->R, 1.0 / p->R);
+    p->T = cfg->horizon;
+    p->words = (p->T + 31) / 32;
+    p->K_total = cfg->samples;
+    p->K_local = cfg->samples;
+    p->s_begin = 0;
+    p->rbar_init.assign(n_robots, 0);
+    p->margins_O.assign(n_robots, -1);
+    const int T = p->T, B = n_robots;
+    p->d_nom = p->dalloc<double>((size_t)B * 2 * T);
+    std::vector<double> nom0((size_t)B * 2 * T);  // bounds.clamp(Control{}) (mppi.cpp:200)
+    for (size_t k = 0; k < (size_t)B * T; ++k) {
+      nom0[2 * k] = gpm::clampd(0.0, cfg->lo[0], cfg->hi[0]);
+      nom0[2 * k + 1] = gpm::clampd(0.0, cfg->lo[1], cfg->hi[1]);
+    }
+    CK(cudaMemcpyAsync(p->d_nom, nom0.data(), sizeof(double) * nom0.size(), cudaMemcpyHostToDevice, p->stream));
+    p->d_tw = p->dalloc<double>((size_t)B * gpm::BatchStrides::TW);
+    upload_terrain_weights(p);
+    p->d_x0 = p->dalloc<double>((size_t)B * gpm::BatchStrides::X0);
+    p->d_rbar = p->dalloc<double>((size_t)B * gpm::BatchStrides::rbar(T));
+    p->d_margins = p->dalloc<double>((size_t)B * gpm::BatchStrides::marg(T));
+    p->d_task = p->dalloc<gpm::TaskDev>(B);
+    p->d_rank_tuple = p->dalloc<double>((size_t)B * gpm::tuple_doubles(T));
+    p->d_combined = p->dalloc<double>(gpm::tuple_doubles(T));
+    p->d_out = p->dalloc<double>((size_t)B * gpm::BatchStrides::OUT);
+    p->d_hcov = p->dalloc<double>((size_t)B * T * 25);
+    p->d_ticket = p->dalloc<unsigned int>(B);
+    p->d_infeasible = p->dalloc<int>(B);
+    p->d_tq = p->dalloc<double>((size_t)B * T * 4);
+    p->d_tmu = p->dalloc<double>((size_t)B * (T + 1) * 5);
+    p->d_tJ = p->dalloc<double>((size_t)B * T * 25);
+    {
+      const int G = p->model ? p->groups() : 1;
+      const int ns = p->model ? gpm::tighten_splits(p->model->n) : 1;
+      p->d_tvar = p->dalloc<double>((size_t)B * T * G * ns);
+    }
+    p->alloc_sample_buffers();
+    CK(cudaMallocHost(&p->h_task, sizeof(gpm::TaskDev) * B));
+    CK(cudaMallocHost(&p->h_x0, sizeof(double) * gpm::BatchStrides::X0 * B));
+    CK(cudaMallocHost(&p->h_out, sizeof(double) * gpm::BatchStrides::OUT * B));
+    CK(cudaMallocHost(&p->h_infeasible, sizeof(int) * B));
+    for (auto& e : p->ev) CK(cudaEventCreate(&e));
+    CK(cudaStreamSynchronize(p->stream));
+  } catch (...) {
+    delete p;
+    throw;
+  }
+  return p;
+}
+
+// One tick of every robot: mppi.cpp:389-462 (plan_step_impl) for B planners at once.
+void plan_tick(gpmppi_planner* p, const double* x0, const gpmppi_task* tasks, double* command,
+               gpmppi_diag* diag) {
+  const auto t0 = Clock::now();  // mppi.cpp:391
+  CK(cudaSetDevice(p->device));
+  if (!command) invalid("plan_step: null command output");
+  if (p->K_local != p->K_total) invalid("plan_step: sharded planner; use plan_partial/plan_finish");
+  if (p->noise_mode == gpm::NOISE_INJECTED && !p->injected_set) invalid("plan_step: injected noise mode without noise");
+  stage_tick(p, x0, tasks);
+  enqueue_samples(p, 1, nullptr);
+  copy_out_async(p);
+  CK(cudaEventRecord(p->ev[0], p->stream));
+  enqueue_tighten(p);  // mppi.cpp:433
+  CK(cudaMemcpyAsync(p->h_infeasible, p->d_infeasible, sizeof(int) * p->B, cudaMemcpyDeviceToHost, p->stream));
+  CK(cudaEventSynchronize(p->ev[0]));
+  const double t_cmd = ms_since(t0);
+  CK(cudaStreamSynchronize(p->stream));
+  fill_diag(p, command, diag, t_cmd, ms_since(t0));
+  ++p->tick;  // mppi.cpp:460
+}
+
+void set_weights(gpmppi_planner* p, int robot, const double* w, int R) {  // mppi.cpp:208-218
+  if (!w) invalid("set_terrain_weights: null weights");
+  if (p->model_kind == GPMPPI_MODEL_GP_ENSEMBLE && R != p->R)
+    invalid("set_terrain_weights: size mismatch with terrain count");
+  if (!on_simplex(w, R, 1e-6)) invalid("set_terrain_weights: weights must lie on the simplex");
+  if (R > gpm::kMaxTerrains) invalid("set_terrain_weights: too many terrains");
+  if (R != p->R) {  // GP-free models carry weights they never use; keep every robot's row
+    std::vector<double> nw((size_t)p->B * R, 1.0 / R);
+    p->tw.swap(nw);
+    p->R = R;
+  }
+  for (int b = 0; b < p->B; ++b)
+    if (robot < 0 || robot == b) std::copy(w, w + R, p->tw.begin() + (size_t)b * R);
+  upload_terrain_weights(p);
 }
 
 }  // namespace
@@ -822,139 +1006,53 @@ int gpmppi_planner_create(const gpmppi_mppi_config* cfg, const gpmppi_prediction
                           gpmppi_planner** out) {
   if (!out) return fail(GPMPPI_INVALID_ARGUMENT, "null output handle");
   *out = nullptr;
-  return guarded([&] {
-    if (!cfg || !pm || !nominal) invalid("Planner: null argument");
-    if (!(p_x > 0.5) || !(p_x < 1.0)) invalid("QuantileTables: p_x must lie in (0.5, 1)");
-    if (cfg->samples < 1 || cfg->horizon < 1) invalid("MppiConfig: samples and horizon must be >= 1");
-    if (!(cfg->lambda > 0.0)) invalid("MppiConfig: lambda must be positive");
-    if (!(cfg->sigma_v2 > 0.0) || !(cfg->sigma_w2 > 0.0))
-      invalid("MppiConfig: sampling variances must be positive");
-    if (cfg->lo[0] >= cfg->hi[0] || cfg->lo[1] >= cfg->hi[1])
-      invalid("MppiConfig: control bounds must be a nonempty box");
-    if (!(nominal->tau_v > 0.0) || !(nominal->tau_omega > 0.0))
-      invalid("NominalParams: time constants must be positive");
-    if (!(nominal->dt > 0.0) || nominal->dt >= std::min(nominal->tau_v, nominal->tau_omega))
-      invalid("NominalParams: require 0 < dt < min(tau_v, tau_omega)");
-    if (pm->kind < 0 || pm->kind > 3) invalid("Planner: unknown prediction model");
-    if (pm->kind == GPMPPI_MODEL_GP_ENSEMBLE &&
-        (pm->gp == nullptr || pm->n_terrains < 1 || pm->gp->m != 2 * pm->n_terrains))
-      invalid("Planner: GP ensemble needs a model with 2M outputs");
-    if (pm->kind == GPMPPI_MODEL_GP_ENSEMBLE && pm->n_terrains > gpm::kMaxTerrains)
-      invalid("Planner: too many terrains for the device planner");
-    if (pm->kind == GPMPPI_MODEL_EDD5) {
-      if (!(pm->track_width > 0.0)) invalid("step_edd5: track_width must be positive");
-      if (pm->edd5.y_icr_r - pm->edd5.y_icr_l <= 1e-6)
-        invalid("step_edd5: degenerate ICR span (y_icr_r - y_icr_l <= 1e-6)");
-    }
-    require_device(device);
-    auto* p = new gpmppi_planner();
-    try {
-      p->device = device;
-      CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
-      CK(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device));
-      p->cfg = *cfg;
-      p->model_kind = pm->kind;
-      p->model = pm->kind == GPMPPI_MODEL_GP_ENSEMBLE ? pm->gp : nullptr;
-      if (p->model && p->model->device != device) invalid("Planner: GP model lives on another device");
-      p->R = pm->kind == GPMPPI_MODEL_GP_ENSEMBLE ? pm->n_terrains : 1;
-      p->edd5 = {pm->edd5.alpha_l, pm->edd5.alpha_r, pm->edd5.x_icr, pm->edd5.y_icr_l,
-                 pm->edd5.y_icr_r, pm->track_width};
-      p->nom = {nominal->tau_v, nominal->tau_omega, nominal->dt};
-      p->p_x = p_x;
-      p->chi2 = -2.0 * std::log1p(-p_x);  // uncertainty.cpp:8-13
-      p->z = normal_quantile(p_x);
-      p->tw.assign(p->R, 1.0 / p->R);
-      p->T = cfg->horizon;
-      p->words = (p->T + 31) / 32;
-      p->K_total = cfg->samples;
-      p->K_local = cfg->samples;
-      p->s_begin = 0;
-      const int T = p->T;
-      p->d_nom = p->dalloc<double>(2 * T);
-      std::vector<double> nom0(2 * T);  // bounds.clamp(Control{}) (mppi.cpp:200)
-      for (int k = 0; k < T; ++k) {
-        nom0[2 * k] = gpm::clampd(0.0, cfg->lo[0], cfg->hi[0]);
-        nom0[2 * k + 1] = gpm::clampd(0.0, cfg->lo[1], cfg->hi[1]);
-      }
-      CK(cudaMemcpyAsync(p->d_nom, nom0.data(), sizeof(double) * 2 * T, cudaMemcpyHostToDevice, p->stream));
-      p->d_tw = p->dalloc<double>(gpm::kMaxTerrains);
-      CK(cudaMemcpyAsync(p->d_tw, p->tw.data(), sizeof(double) * p->R, cudaMemcpyHostToDevice, p->stream));
-      p->d_x0 = p->dalloc<double>(8);
-      p->d_rbar = p->dalloc<double>(T);
-      p->d_margins = p->dalloc<double>((size_t)T * gpm::kMaxObstacles);
-      p->d_task = p->dalloc<gpm::TaskDev>(1);
-      p->d_rank_tuple = p->dalloc<double>(gpm::tuple_doubles(T));
-      p->d_combined = p->dalloc<double>(gpm::tuple_doubles(T));
-      p->d_out = p->dalloc<double>(16);
-      p->d_hcov = p->dalloc<double>((size_t)T * 25);
-      p->d_ticket = p->dalloc<unsigned int>(1);
-      p->d_infeasible = p->dalloc<int>(1);
-      p->d_tq = p->dalloc<double>((size_t)T * 4);
-      p->d_tmu = p->dalloc<double>((size_t)(T + 1) * 5);
-      p->d_tJ = p->dalloc<double>((size_t)T * 25);
-      {
-        const int G = p->model ? p->model->dev.G : 1;
-        const int ns = p->model ? gpm::tighten_splits(p->model->n) : 1;
-        p->d_tvar = p->dalloc<double>((size_t)T * G * ns);
-      }
-      p->alloc_sample_buffers();
-      CK(cudaMallocHost(&p->h_task, sizeof(gpm::TaskDev)));
-      CK(cudaMallocHost(&p->h_x0, sizeof(double) * 8));
-      CK(cudaMallocHost(&p->h_out, sizeof(double) * 16));
-      CK(cudaMallocHost(&p->h_infeasible, sizeof(int)));
-      for (auto& e : p->ev) CK(cudaEventCreate(&e));
-      CK(cudaStreamSynchronize(p->stream));
-    } catch (...) {
-      delete p;
-      throw;
-    }
-    *out = p;
-  });
+  return guarded([&] { *out = create_planner(cfg, pm, nominal, p_x, 1, nullptr, device); });
+}
+
+int gpmppi_planner_create_batch(const gpmppi_mppi_config* cfg, const gpmppi_prediction_model* pm,
+                                const gpmppi_nominal* nominal, double p_x, int n_robots,
+                                const uint64_t* seeds, int device, gpmppi_planner** out) {
+  if (!out) return fail(GPMPPI_INVALID_ARGUMENT, "null output handle");
+  *out = nullptr;
+  return guarded([&] { *out = create_planner(cfg, pm, nominal, p_x, n_robots, seeds, device); });
 }
 
 void gpmppi_planner_free(gpmppi_planner* p) { delete p; }
+
+int gpmppi_planner_robots(const gpmppi_planner* p) { return p ? p->B : 0; }
 
 int gpmppi_planner_plan_step(gpmppi_planner* p, const double x0[5], const gpmppi_task* task,
                              double command[2], gpmppi_diag* diag) {
   if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
   return guarded([&] {
-    const auto t0 = Clock::now();  // mppi.cpp:391
-    CK(cudaSetDevice(p->device));
-    if (p->K_local != p->K_total) invalid("plan_step: sharded planner; use plan_partial/plan_finish");
-    if (p->noise_mode == gpm::NOISE_INJECTED && !p->injected_set) invalid("plan_step: injected noise mode without noise");
-    stage_tick(p, x0, task);
-    enqueue_samples(p, task->kind == GPMPPI_TASK_TRACKING ? 0 : task->n_obstacles,
-                    task_var_weight(task), 1, nullptr);
-    CK(cudaMemcpyAsync(p->h_out, p->d_out, sizeof(double) * 8, cudaMemcpyDeviceToHost, p->stream));
-    CK(cudaEventRecord(p->ev[0], p->stream));
-    enqueue_tighten(p);  // mppi.cpp:433
-    CK(cudaMemcpyAsync(p->h_infeasible, p->d_infeasible, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
-    CK(cudaEventSynchronize(p->ev[0]));
-    const double t_cmd = ms_since(t0);
-    CK(cudaStreamSynchronize(p->stream));
-    fill_diag(p, command, diag, t_cmd, ms_since(t0));
-    ++p->tick;  // mppi.cpp:460
+    if (p->B != 1) invalid("plan_step: batched planner; use plan_step_batch");
+    plan_tick(p, x0, task, command, diag);
   });
+}
+
+int gpmppi_planner_plan_step_batch(gpmppi_planner* p, const double* x0, const gpmppi_task* tasks,
+                                   double* commands, gpmppi_diag* diags) {
+  if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
+  return guarded([&] { plan_tick(p, x0, tasks, commands, diags); });
 }
 
 int gpmppi_planner_set_terrain_weights(gpmppi_planner* p, const double* w, int R) {
   if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
-  return guarded([&] {  // mppi.cpp:208-218
-    if (p->model_kind == GPMPPI_MODEL_GP_ENSEMBLE && R != p->R)
-      invalid("set_terrain_weights: size mismatch with terrain count");
-    if (!on_simplex(w, R, 1e-6)) invalid("set_terrain_weights: weights must lie on the simplex");
-    if (R > gpm::kMaxTerrains) invalid("set_terrain_weights: too many terrains");
-    p->tw.assign(w, w + R);
-    p->R = R;
-    CK(cudaMemcpyAsync(p->d_tw, p->tw.data(), sizeof(double) * R, cudaMemcpyHostToDevice, p->stream));
-    CK(cudaStreamSynchronize(p->stream));
+  return guarded([&] { set_weights(p, -1, w, R); });
+}
+
+int gpmppi_planner_set_robot_terrain_weights(gpmppi_planner* p, int robot, const double* w, int R) {
+  if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
+  return guarded([&] {
+    if (robot < 0 || robot >= p->B) invalid("set_robot_terrain_weights: robot index out of range");
+    set_weights(p, robot, w, R);
   });
 }
 
 int gpmppi_planner_terrain_weights(const gpmppi_planner* p, double* w) {
   if (!p) return 0;
   if (w) std::memcpy(w, p->tw.data(), sizeof(double) * p->tw.size());
-  return (int)p->tw.size();
+  return p->R;
 }
 
 static int copy_back(const gpmppi_planner* p, void* dst, const void* src, size_t bytes) {
@@ -967,47 +1065,64 @@ static int copy_back(const gpmppi_planner* p, void* dst, const void* src, size_t
 
 int gpmppi_planner_nominal_sequence(const gpmppi_planner* p, double* seq) {
   if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
-  return copy_back(p, seq, p->d_nom, sizeof(double) * 2 * p->T);
+  return copy_back(p, seq, p->d_nom, sizeof(double) * 2 * p->T * p->B);
 }
 int gpmppi_planner_set_nominal_sequence(gpmppi_planner* p, const double* seq) {
   if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
   return guarded([&] {
-    CK(cudaMemcpyAsync(p->d_nom, seq, sizeof(double) * 2 * p->T, cudaMemcpyHostToDevice, p->stream));
     CK(cudaStreamSynchronize(p->stream));
+    CK(cudaMemcpy(p->d_nom, seq, sizeof(double) * 2 * p->T * p->B, cudaMemcpyHostToDevice));
   });
 }
 int gpmppi_planner_horizon_covariances(const gpmppi_planner* p, double* cov) {
   if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
-  return copy_back(p, cov, p->d_hcov, sizeof(double) * 25 * p->T);
+  return copy_back(p, cov, p->d_hcov, sizeof(double) * 25 * p->T * p->B);
 }
 int gpmppi_planner_lane_radii(const gpmppi_planner* p, double* r) {
-  if (!p || !p->rbar_init) return 0;
-  if (r && copy_back(p, r, p->d_rbar, sizeof(double) * p->T) != GPMPPI_OK) return -1;
+  if (!p) return 0;
+  bool any = false;  // robots without a track keep zero rows
+  for (int b = 0; b < p->B; ++b) any = any || p->rbar_init[b];
+  if (!any) return 0;
+  if (r && copy_back(p, r, p->d_rbar, sizeof(double) * p->T * p->B) != GPMPPI_OK) return -1;
   return p->T;
 }
 int gpmppi_planner_obstacle_margins(const gpmppi_planner* p, double* m) {
-  if (!p || p->margins_O <= 0) return 0;
+  if (!p) return 0;
+  int O = 0;
+  for (int b = 0; b < p->B; ++b) O = std::max(O, p->margins_O[b]);
+  if (O <= 0) return 0;
   if (m) {
-    std::vector<double> tmp((size_t)p->T * gpm::kMaxObstacles);
-    if (copy_back(p, tmp.data(), p->d_margins, sizeof(double) * p->T * p->margins_O) != GPMPPI_OK) return -1;
-    std::memcpy(m, tmp.data(), sizeof(double) * p->T * p->margins_O);
+    const size_t stride = gpm::BatchStrides::marg(p->T);
+    std::vector<double> tmp((size_t)p->B * stride);
+    if (copy_back(p, tmp.data(), p->d_margins, sizeof(double) * tmp.size()) != GPMPPI_OK) return -1;
+    for (int b = 0; b < p->B; ++b) {  // robot b's [T][O_b] block, zero-padded to O columns
+      const int Ob = std::max(p->margins_O[b], 0);
+      for (int k = 0; k < p->T; ++k)
+        for (int o = 0; o < O; ++o)
+          m[((size_t)b * p->T + k) * O + o] = o < Ob ? tmp[b * stride + (size_t)k * Ob + o] : 0.0;
+    }
   }
-  return p->margins_O;
+  return O;
 }
 int gpmppi_planner_set_thresholds(gpmppi_planner* p, const double* r_bar, const double* margins,
                                   int n_obstacles) {
   if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
   return guarded([&] {
     if (n_obstacles < 0 || n_obstacles > gpm::kMaxObstacles) invalid("set_thresholds: bad obstacle count");
-    if (r_bar) {
-      CK(cudaMemcpyAsync(p->d_rbar, r_bar, sizeof(double) * p->T, cudaMemcpyHostToDevice, p->stream));
-      p->rbar_init = true;
-    }
-    if (margins) {
-      CK(cudaMemcpyAsync(p->d_margins, margins, sizeof(double) * p->T * n_obstacles, cudaMemcpyHostToDevice, p->stream));
-      p->margins_O = n_obstacles;
-    }
     CK(cudaStreamSynchronize(p->stream));
+    for (int b = 0; b < p->B; ++b) {
+      if (r_bar) {
+        CK(cudaMemcpy(p->d_rbar + (size_t)b * gpm::BatchStrides::rbar(p->T), r_bar + (size_t)b * p->T,
+                      sizeof(double) * p->T, cudaMemcpyHostToDevice));
+        p->rbar_init[b] = 1;
+      }
+      if (margins) {
+        CK(cudaMemcpy(p->d_margins + (size_t)b * gpm::BatchStrides::marg(p->T),
+                      margins + (size_t)b * p->T * n_obstacles, sizeof(double) * p->T * n_obstacles,
+                      cudaMemcpyHostToDevice));
+        p->margins_O[b] = n_obstacles;
+      }
+    }
   });
 }
 uint64_t gpmppi_planner_tick(const gpmppi_planner* p) { return p ? p->tick : 0; }
@@ -1023,9 +1138,10 @@ int gpmppi_planner_set_noise_mode(gpmppi_planner* p, int mode) {
 int gpmppi_planner_inject_noise(gpmppi_planner* p, const double* eps) {
   if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
   return guarded([&] {
-    if (!p->d_eps) p->d_eps = p->dalloc<double>((size_t)p->K_local * p->T * 2);
-    CK(cudaMemcpyAsync(p->d_eps, eps, sizeof(double) * p->K_local * p->T * 2, cudaMemcpyHostToDevice, p->stream));
+    const size_t cnt = (size_t)p->slots() * p->T * 2;
+    if (!p->d_eps) p->d_eps = p->dalloc<double>(cnt);
     CK(cudaStreamSynchronize(p->stream));
+    CK(cudaMemcpy(p->d_eps, eps, sizeof(double) * cnt, cudaMemcpyHostToDevice));
     p->injected_set = true;
     p->noise_mode = gpm::NOISE_INJECTED;
   });
@@ -1037,11 +1153,13 @@ int gpmppi_planner_philox_noise(const gpmppi_planner* p, uint64_t tick, double* 
     double* d = nullptr;
     const size_t cnt = (size_t)p->K_local * p->T * 2;
     CK(cudaMalloc(&d, sizeof(double) * cnt));
-    cudaError_t e = gpm::launch_philox_noise(gpm::philox_key(p->cfg.seed, tick), p->s_begin,
-                                             (int)p->K_local, p->T, std::sqrt(p->cfg.sigma_v2),
-                                             std::sqrt(p->cfg.sigma_w2), d, p->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
-    if (e == cudaSuccess) e = cudaMemcpy(eps, d, sizeof(double) * cnt, cudaMemcpyDeviceToHost);
+    cudaError_t e = cudaSuccess;
+    for (int b = 0; b < p->B && e == cudaSuccess; ++b) {
+      e = gpm::launch_philox_noise(gpm::philox_key(p->seeds[b], tick), p->s_begin, (int)p->K_local, p->T,
+                                   std::sqrt(p->cfg.sigma_v2), std::sqrt(p->cfg.sigma_w2), d, p->stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+      if (e == cudaSuccess) e = cudaMemcpy(eps + b * cnt, d, sizeof(double) * cnt, cudaMemcpyDeviceToHost);
+    }
     cudaFree(d);
     if (e != cudaSuccess) throw CudaError{e, "philox_noise_kernel"};
   });
@@ -1049,7 +1167,7 @@ int gpmppi_planner_philox_noise(const gpmppi_planner* p, uint64_t tick, double* 
 
 int gpmppi_planner_sample_costs(const gpmppi_planner* p, double* costs) {
   if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
-  return copy_back(p, costs, p->d_costs, sizeof(double) * p->K_local);
+  return copy_back(p, costs, p->d_costs, sizeof(double) * p->slots());
 }
 int gpmppi_planner_sample_weights(const gpmppi_planner* p, double* w) {
   if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
@@ -1057,16 +1175,22 @@ int gpmppi_planner_sample_weights(const gpmppi_planner* p, double* w) {
     CK(cudaSetDevice(p->device));
     CK(cudaStreamSynchronize(p->stream));
     const int W = gpm::tuple_doubles(p->T);
-    std::vector<double> e(p->K_local), parts((size_t)p->reduce_blocks * W), tup(W);
-    CK(cudaMemcpy(e.data(), p->d_e, sizeof(double) * p->K_local, cudaMemcpyDeviceToHost));
+    const int BP = p->reduce_blocks;
+    std::vector<double> e(p->slots()), parts((size_t)p->B * BP * W), tup((size_t)p->B * W);
+    CK(cudaMemcpy(e.data(), p->d_e, sizeof(double) * e.size(), cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(parts.data(), p->d_partials, sizeof(double) * parts.size(), cudaMemcpyDeviceToHost));
-    const double* src = p->K_local == p->K_total ? p->d_rank_tuple : p->d_combined;
-    CK(cudaMemcpy(tup.data(), src, sizeof(double) * W, cudaMemcpyDeviceToHost));
-    const int per = (int)((p->K_local + p->reduce_blocks - 1) / p->reduce_blocks);
-    for (long long s = 0; s < p->K_local; ++s) {
-      const int b = (int)(s / per);
-      const double mb = parts[(size_t)b * W];
-      w[s] = (e[s] == 0.0 || !(tup[1] > 0.0)) ? 0.0 : e[s] * std::exp(-(mb - tup[0]) / p->cfg.lambda) / tup[1];
+    if (p->K_local == p->K_total)
+      CK(cudaMemcpy(tup.data(), p->d_rank_tuple, sizeof(double) * tup.size(), cudaMemcpyDeviceToHost));
+    else
+      CK(cudaMemcpy(tup.data(), p->d_combined, sizeof(double) * W, cudaMemcpyDeviceToHost));
+    const int per = (int)((p->K_local + BP - 1) / BP);
+    for (int b = 0; b < p->B; ++b) {
+      const double* tb = tup.data() + (size_t)b * W;
+      for (long long s = 0; s < p->K_local; ++s) {
+        const size_t q = (size_t)b * p->K_local + s;
+        const double mb = parts[((size_t)b * BP + s / per) * W];
+        w[q] = (e[q] == 0.0 || !(tb[1] > 0.0)) ? 0.0 : e[q] * std::exp(-(mb - tb[0]) / p->cfg.lambda) / tb[1];
+      }
     }
   });
 }
@@ -1076,18 +1200,19 @@ int gpmppi_planner_flags(const gpmppi_planner* p, uint8_t* viol, uint8_t* coll, 
   return guarded([&] {
     CK(cudaSetDevice(p->device));
     CK(cudaStreamSynchronize(p->stream));
-    const size_t nw = (size_t)p->K_local * p->words;
+    const long long S = p->slots();
+    const size_t nw = (size_t)S * p->words;
     std::vector<uint32_t> vb(nw), cb(nw);
     CK(cudaMemcpy(vb.data(), p->d_viol, sizeof(uint32_t) * nw, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(cb.data(), p->d_coll, sizeof(uint32_t) * nw, cudaMemcpyDeviceToHost));
-    for (long long s = 0; s < p->K_local; ++s)
+    for (long long s = 0; s < S; ++s)
       for (int k = 0; k < p->T; ++k) {
-        const uint32_t word = (uint32_t)(s * p->words + (k >> 5));
+        const size_t word = (size_t)s * p->words + (k >> 5);
         if (viol) viol[s * p->T + k] = (vb[word] >> (k & 31)) & 1u;
         if (coll) coll[s * p->T + k] = (cb[word] >> (k & 31)) & 1u;
       }
-    if (terminal) CK(cudaMemcpy(terminal, p->d_term, p->K_local, cudaMemcpyDeviceToHost));
-    if (alive) CK(cudaMemcpy(alive, p->d_alive, p->K_local, cudaMemcpyDeviceToHost));
+    if (terminal) CK(cudaMemcpy(terminal, p->d_term, S, cudaMemcpyDeviceToHost));
+    if (alive) CK(cudaMemcpy(alive, p->d_alive, S, cudaMemcpyDeviceToHost));
   });
 }
 
@@ -1099,15 +1224,14 @@ int gpmppi_planner_set_variance_path(gpmppi_planner* p, int path) {
 }
 int gpmppi_planner_variance_path(const gpmppi_planner* p) { return p ? p->var_path : -1; }
 
-int gpmppi_planner_bench_device(gpmppi_planner* p, const double x0[5], const gpmppi_task* task,
+int gpmppi_planner_bench_device(gpmppi_planner* p, const double* x0, const gpmppi_task* tasks,
                                 int ticks, int flush_l2, double* tick_ms, double* phase_ms) {
   if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
   return guarded([&] {
     CK(cudaSetDevice(p->device));
     if (ticks < 1) invalid("bench_device: ticks must be >= 1");
-    stage_tick(p, x0, task);
-    const int n_obs = task->kind == GPMPPI_TASK_TRACKING ? 0 : task->n_obstacles;
-    const double vw = task_var_weight(task);
+    if (p->K_local != p->K_total) invalid("bench_device: sharded planner");
+    stage_tick(p, x0, tasks);
     void* flush = nullptr;
     size_t flush_bytes = 0;
     if (flush_l2) {
@@ -1121,10 +1245,10 @@ int gpmppi_planner_bench_device(gpmppi_planner* p, const double x0[5], const gpm
     for (int t = 0; t < ticks; ++t) {
       cudaEvent_t* E = &evs[(size_t)t * 5];
       if (flush) CK(cudaMemsetAsync(flush, t & 0xff, flush_bytes, p->stream));  // outside the timed span
-      enqueue_samples(p, n_obs, vw, 1, E);
+      enqueue_samples(p, 1, E);
       enqueue_tighten(p);
       CK(cudaEventRecord(E[4], p->stream));
-      ++p->tick;
+      ++p->tick;  // the staged keys stay at the first tick: same work, fixed noise
     }
     cudaError_t se = cudaStreamSynchronize(p->stream);
     if (flush) cudaFree(flush);
@@ -1164,8 +1288,8 @@ int gpmppi_flush_l2(int device) {
 
 int gpmppi_planner_io_bytes(const gpmppi_planner* p, int64_t* h2d, int64_t* d2h) {
   if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
-  if (h2d) *h2d = (int64_t)(sizeof(gpm::TaskDev) + 5 * sizeof(double));
-  if (d2h) *d2h = (int64_t)(8 * sizeof(double) + sizeof(int));
+  if (h2d) *h2d = (int64_t)p->B * (int64_t)(sizeof(gpm::TaskDev) + gpm::BatchStrides::X0 * sizeof(double));
+  if (d2h) *d2h = (int64_t)p->B * (int64_t)(gpm::BatchStrides::OUT * sizeof(double) + sizeof(int));
   return GPMPPI_OK;
 }
 
@@ -1178,6 +1302,7 @@ int gpmppi_tuple_doubles(int horizon) { return gpm::tuple_doubles(horizon); }
 int gpmppi_planner_set_shard(gpmppi_planner* p, int64_t begin, int64_t count) {
   if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
   return guarded([&] {
+    if (p->B != 1) invalid("set_shard: batched planners shard by robot, not by sample");
     if (begin < 0 || count < 1 || begin + count > p->K_total) invalid("set_shard: range outside [0, samples)");
     CK(cudaSetDevice(p->device));
     CK(cudaStreamSynchronize(p->stream));
@@ -1195,10 +1320,10 @@ int gpmppi_planner_plan_partial(gpmppi_planner* p, const double x0[5], const gpm
   if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
   return guarded([&] {
     CK(cudaSetDevice(p->device));
+    if (p->B != 1) invalid("plan_partial: batched planner");
     if (p->noise_mode == gpm::NOISE_INJECTED && !p->injected_set) invalid("plan_partial: injected noise mode without noise");
     stage_tick(p, x0, task);
-    enqueue_samples(p, task->kind == GPMPPI_TASK_TRACKING ? 0 : task->n_obstacles,
-                    task_var_weight(task), 0, nullptr);
+    enqueue_samples(p, 0, nullptr);
     CK(cudaMemcpyAsync(device_tuple_out, p->d_rank_tuple, sizeof(double) * gpm::tuple_doubles(p->T),
                        cudaMemcpyDeviceToDevice, p->stream));
     CK(cudaStreamSynchronize(p->stream));
@@ -1211,12 +1336,13 @@ int gpmppi_planner_plan_finish(gpmppi_planner* p, const void* device_tuples, int
   return guarded([&] {
     const auto t0 = Clock::now();
     CK(cudaSetDevice(p->device));
+    if (p->B != 1) invalid("plan_finish: batched planner");
     if (n_ranks < 1) invalid("plan_finish: n_ranks must be >= 1");
     check(gpm::launch_finish(static_cast<const double*>(device_tuples), n_ranks, p->T,
                              p->cfg.lambda, p->d_nom, p->cfg.lo, p->cfg.hi, p->d_out, p->K_total,
                              p->d_combined, p->stream),
           "finish kernel");
-    CK(cudaMemcpyAsync(p->h_out, p->d_out, sizeof(double) * 8, cudaMemcpyDeviceToHost, p->stream));
+    copy_out_async(p);
     CK(cudaEventRecord(p->ev[0], p->stream));
     enqueue_tighten(p);
     CK(cudaMemcpyAsync(p->h_infeasible, p->d_infeasible, sizeof(int), cudaMemcpyDeviceToHost, p->stream));

@@ -33,30 +33,45 @@ struct ModelDev {
 
 enum { NOISE_PHILOX = 0, NOISE_INJECTED = 1 };
 
+// Per-robot strides of the batched planner state (B independent planners that
+// share one GP model; B = 1 is the single Planner). Robot b's slice of an array
+// with stride S starts at b*S.
+struct BatchStrides {
+  // per-robot tick block: x0[0..4], [5] variance weight of the task, [6] Philox key
+  // (bit pattern), [7] pad -- one H2D copy stages everything a robot's tick needs
+  static constexpr int X0 = 8;
+  static constexpr int TW = kMaxTerrains;         // terrain weights
+  static constexpr int OUT = 16;                  // command + diagnostics
+  GPM_HD static int nom(int T) { return 2 * T; }
+  GPM_HD static int rbar(int T) { return T; }
+  GPM_HD static int marg(int T) { return T * kMaxObstacles; }  // [T][n_obs] inside
+};
+
 struct RolloutArgs {
   ModelDev model;
   int model_kind;
   NominalDev nom;
   Edd5Dev edd5;
-  int K_local;
+  int B;              // robots
+  int K_local;        // samples per robot on this device
+  long long K_total;  // samples per robot in the whole (possibly sharded) solve
   long long s_begin;
   int T;
-  int n_obs;
+  int n_obs_max;      // max obstacles over the robots (shared-memory sizing)
   double lo[2], hi[2];
   double sv, sw;  // noise standard deviations
   int noise_mode;
-  const double* eps;  // injected [K_local][T][2]
-  uint64_t key;
-  const double* nominal_seq;
-  const double* tw;
+  const double* eps;  // injected [B][K_local][T][2]
+  const double* nominal_seq;  // [B][2T]
+  const double* tw;           // [B][kMaxTerrains]
   int R;
-  const TaskDev* task;
-  const double* r_bar;
-  const double* margins;
-  const double* x0;
-  double* cost_mean;
-  float4* queries;
-  uint32_t* viol_bits;
+  const TaskDev* task;        // [B]
+  const double* r_bar;        // [B][T]
+  const double* margins;      // [B][T*kMaxObstacles]
+  const double* x0;           // [B][8]
+  double* cost_mean;          // [B*K_local]
+  float4* queries;            // [B*K_local*T]
+  uint32_t* viol_bits;        // [B*K_local*words]
   uint32_t* coll_bits;
   uint8_t* term;
   uint8_t* alive;
@@ -69,55 +84,62 @@ struct VarianceArgs {
   long long KT;
   int n;
   GroupDev g;
-  double coef;   // Σ over the group's outputs of w_terrain^2 (trace coefficient)
-  int accumulate; // 0: trace = coef*var, 1: trace += coef*var
-  double* trace; // [KT]
+  double coef;    // multiplier of var (1 in the solve: the reduce applies Σ w² per robot)
+  int accumulate; // 0: out = coef*var, 1: out += coef*var
+  double* trace;  // [KT] (this group's slice)
 };
 
 struct ReduceArgs {
+  int B;
   int K_local;
+  long long K_total;
   long long s_begin;
   int T;
+  int bpr;  // blocks per robot
   double lambda;
-  const double* cost_mean;
-  const double* trace;  // may be null (no GP)
-  double var_w;
+  const double* cost_mean;  // [B*K_local]
+  const double* var;        // [G][B*K_local*T] raw per-group variances (null: no GP)
+  int G;
+  const double* tw;         // [B][kMaxTerrains] terrain weights
+  // trace coefficient of group g for robot b: Σ_o tw[b][coef_terrain[g][o]]² over
+  // the group's outputs (mppi.cpp:34-49 combine); -1 ends the list
+  signed char coef_terrain[kMaxGroups][8];
+  const double* x0;         // [B][8] robot tick blocks (variance weight, key)
   int noise_mode;
   const double* eps;
-  uint64_t key;
   double sv, sw;
   double* costs_out;
   double* e_out;
-  double* partials;
-  unsigned int* ticket;
-  double* rank_tuple;
+  double* partials;       // [B*bpr][W]
+  unsigned int* ticket;   // [B]
+  double* rank_tuple;     // [B][W]
   int finish;
-  double* nominal_seq;
+  double* nominal_seq;    // [B][2T]
   double lo[2], hi[2];
-  double* out;  // [2 + 6]: command, best, mean, ess, entropy, nonfinite, N
-  long long K_total;
+  double* out;            // [B][16]: command, best, mean, ess, entropy, nonfinite, N
 };
 
 struct TightenArgs {
   ModelDev model;
   int model_kind;
   NominalDev nom;
+  int B;
   int T;
-  const double* tw;
+  const double* tw;  // [B][kMaxTerrains]
   int R;
-  const double* x0;
-  const double* nominal_seq;
-  const TaskDev* task;
+  const double* x0;           // [B][8]
+  const double* nominal_seq;  // [B][2T]
+  const TaskDev* task;        // [B]
   double chi2, z;
-  double* horizon_cov;
-  double* r_bar;
-  double* margins;
-  int* infeasible;
+  double* horizon_cov;  // [B][25T]
+  double* r_bar;        // [B][T]
+  double* margins;      // [B][T*kMaxObstacles]
+  int* infeasible;      // [B]
   // scratch of the three-phase pass
-  double* tq;         // [T][4] GP queries at the belief means
-  double* tmu;        // [T+1][5] belief means
-  double* tJ;         // [T][25] Jacobians
-  double* tvar_part;  // [T][G][splits] partial ||L^{-1}k*||^2
+  double* tq;         // [B][T][4] GP queries at the belief means
+  double* tmu;        // [B][T+1][5] belief means
+  double* tJ;         // [B][T][25] Jacobians
+  double* tvar_part;  // [B][T][G][splits] partial ||L^{-1}k*||^2
 };
 
 // launchers (kernels.cu); all enqueue on `st` and return cudaGetLastError()
@@ -127,6 +149,7 @@ cudaError_t launch_reduce(const ReduceArgs& a, int blocks, cudaStream_t st);
 cudaError_t launch_finish(const double* tuples, int n, int T, double lambda, double* nominal_seq,
                           const double lo[2], const double hi[2], double* out, long long K_total,
                           double* combined, cudaStream_t st);
+int rollout_samples_per_block(int K_local, int num_sms, int* lps, int* threads);
 cudaError_t launch_tighten(const TightenArgs& a, cudaStream_t st);
 cudaError_t launch_predict(const ModelDev& m, const double* q, long long S, double* mean,
                            double* var, cudaStream_t st);
@@ -134,7 +157,7 @@ cudaError_t launch_philox_noise(uint64_t key, long long s_begin, int K, int T, d
                                 double sw, double* eps, cudaStream_t st);
 size_t rollout_smem_bytes(const RolloutArgs& a);
 size_t rollout_scratch_doubles(int T, int num_sms);
-int reduce_blocks_for(int K_local, int num_sms);
+int reduce_blocks_for(int K_local, int B, int num_sms);
 int tighten_splits(int n);
 void build_tc_operand(const double* ilt, int n, std::vector<float>& data, std::vector<int4>& meta,
                       int& n_pad, int& np, int& n_pass);

@@ -80,7 +80,7 @@ GPM_D double exp_tab(double x, const double* tab) {
 // Rollout, GP ensemble model. NO = max outputs per kernel group (compile time).
 size_t rollout_smem_bytes(const RolloutArgs& a) {
   size_t b = sizeof(TaskDev);
-  b += sizeof(double) * (size_t)(2 * a.T + a.T + a.T * (a.n_obs > 0 ? a.n_obs : 1) + a.R + 2 + 32);
+  b += sizeof(double) * (size_t)(2 * a.T + a.T + a.T * (a.n_obs_max > 0 ? a.n_obs_max : 1) + a.R + 2 + 32);
   b = (b + 15) & ~(size_t)15;
   if (a.model_kind == MODEL_GP)
     for (int g = 0; g < a.model.G; ++g) b += sizeof(double) * (size_t)(5 + a.model.g[g].n_out) * a.model.ns;
@@ -97,7 +97,7 @@ struct SmemView {
   double* pts;   // groups back to back
 };
 
-GPM_D SmemView load_common_smem(const RolloutArgs& a, unsigned char* smem) {
+GPM_D SmemView carve_smem(const RolloutArgs& a, unsigned char* smem) {
   SmemView v;
   v.task = reinterpret_cast<TaskDev*>(smem);
   double* p = reinterpret_cast<double*>(smem + sizeof(TaskDev));
@@ -106,7 +106,7 @@ GPM_D SmemView load_common_smem(const RolloutArgs& a, unsigned char* smem) {
   v.rbar = p;
   p += a.T;
   v.marg = p;
-  p += a.T * (a.n_obs > 0 ? a.n_obs : 1);
+  p += a.T * (a.n_obs_max > 0 ? a.n_obs_max : 1);
   v.tw = p;
   p += a.R + 2;
   v.etab = p;
@@ -116,30 +116,36 @@ GPM_D SmemView load_common_smem(const RolloutArgs& a, unsigned char* smem) {
   size_t off = (size_t)(reinterpret_cast<unsigned char*>(p) - smem);
   off = (off + 15) & ~(size_t)15;
   v.pts = reinterpret_cast<double*>(smem + off);
-  {  // task (plain words)
-    const int nw = sizeof(TaskDev) / 8;
-    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(a.task);
-    unsigned long long* dst = reinterpret_cast<unsigned long long*>(v.task);
-    for (int i = threadIdx.x; i < nw; i += blockDim.x) dst[i] = src[i];
-  }
-  for (int i = threadIdx.x; i < 2 * a.T; i += blockDim.x) v.nom[i] = a.nominal_seq[i];
-  if (a.r_bar)
-    for (int i = threadIdx.x; i < a.T; i += blockDim.x) v.rbar[i] = a.r_bar[i];
-  if (a.margins)
-    for (int i = threadIdx.x; i < a.T * a.n_obs; i += blockDim.x) v.marg[i] = a.margins[i];
-  for (int i = threadIdx.x; i < a.R; i += blockDim.x) v.tw[i] = a.tw[i];
   for (int i = threadIdx.x; i < 32; i += blockDim.x) v.etab[i] = kExp2Frac[i];
   return v;
 }
 
-GPM_D void sample_noise(const RolloutArgs& a, int sl, long long s, int k, double* e0, double* e1) {
+// Robot b's per-tick view (task, nominal sequence, thresholds, terrain weights).
+GPM_D void load_robot_smem(const RolloutArgs& a, const SmemView& v, int b) {
+  const int nw = sizeof(TaskDev) / 8;
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(a.task + b);
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(v.task);
+  for (int i = threadIdx.x; i < nw; i += blockDim.x) dst[i] = src[i];
+  const double* nom = a.nominal_seq + (size_t)b * BatchStrides::nom(a.T);
+  for (int i = threadIdx.x; i < 2 * a.T; i += blockDim.x) v.nom[i] = nom[i];
+  const double* rb = a.r_bar + (size_t)b * BatchStrides::rbar(a.T);
+  for (int i = threadIdx.x; i < a.T; i += blockDim.x) v.rbar[i] = rb[i];
+  const double* mg = a.margins + (size_t)b * BatchStrides::marg(a.T);
+  for (int i = threadIdx.x; i < a.T * a.n_obs_max; i += blockDim.x) v.marg[i] = mg[i];
+  const double* tw = a.tw + (size_t)b * BatchStrides::TW;
+  for (int i = threadIdx.x; i < a.R; i += blockDim.x) v.tw[i] = tw[i];
+}
+
+// sl = robot-major local sample index (b*K_local + local s); s = global counter index
+GPM_D void sample_noise(const RolloutArgs& a, uint64_t key, long long sl, long long s, int k, double* e0,
+                        double* e1) {
   if (a.noise_mode == NOISE_INJECTED) {
     const double2 e = reinterpret_cast<const double2*>(a.eps)[(size_t)sl * a.T + k];
     *e0 = e.x;
     *e1 = e.y;
   } else {
     double z1, z2;
-    philox_gaussian_pair(a.key, (uint64_t)s, (uint32_t)k, &z1, &z2);
+    philox_gaussian_pair(key, (uint64_t)s, (uint32_t)k, &z1, &z2);
     *e0 = a.sv * z1;
     *e1 = a.sw * z2;
   }
@@ -164,9 +170,9 @@ constexpr int SCR_ARRAYS = 9;
 template <int NO, int LPS>
 __global__ void __launch_bounds__(256, 1) rollout_gp_kernel(const RolloutArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  SmemView sv = load_common_smem(a, smem);
+  const SmemView sv = carve_smem(a, smem);
   const int ns = a.model.ns;  // even SoA stride (padding points contribute exactly 0)
-  {  // stage Z / alpha of every group (SoA) into shared memory
+  {  // stage Z / alpha of every group (SoA) into shared memory, once per block
     double* dst = sv.pts;
     for (int g = 0; g < a.model.G; ++g) {
       const int cnt = (5 + a.model.g[g].n_out) * ns;
@@ -177,14 +183,12 @@ __global__ void __launch_bounds__(256, 1) rollout_gp_kernel(const RolloutArgs a)
       dst += cnt;
     }
   }
-  __syncthreads();
   const TaskDev& task = *sv.task;
   const int gl = threadIdx.x % LPS;  // lane inside the sample group
   const int groups_per_block = blockDim.x / LPS;
-  const int gid = blockIdx.x * groups_per_block + threadIdx.x / LPS;
-  const int ngroups = gridDim.x * groups_per_block;
+  const int gib = threadIdx.x / LPS;  // group index in the block
+  const int gid = blockIdx.x * groups_per_block + gib;
   const int T = a.T;
-  const int O = a.n_obs;
   const int stride = T + 1;
   double* scr = a.scratch + (size_t)gid * SCR_ARRAYS * stride;
   double* su0 = scr;
@@ -197,22 +201,36 @@ __global__ void __launch_bounds__(256, 1) rollout_gp_kernel(const RolloutArgs a)
   double* sx = scr + 7 * stride;
   double* sy = scr + 8 * stride;
   const double av = a.nom.dt / a.nom.tau_v, aw = a.nom.dt / a.nom.tau_omega;
-  // every lane of the warp runs the same trip count (samples beyond K are masked)
-  const int rounds = (a.K_local + ngroups - 1) / ngroups;
+  // work items: (robot, chunk of groups_per_block samples); every lane of the block
+  // runs the same item sequence (samples beyond K are masked, never early-exit)
+  const int chunks = (a.K_local + groups_per_block - 1) / groups_per_block;
+  const long long items = (long long)a.B * chunks;
+  int loaded = -1;
 
-  for (int r = 0; r < rounds; ++r) {
-    const int sl = gid + r * ngroups;
-    const bool valid = sl < a.K_local;
-    const long long s = a.s_begin + (valid ? sl : 0);
+  for (long long item = blockIdx.x; item < items; item += gridDim.x) {
+    const int b = (int)(item / chunks);
+    const int ls = (int)(item % chunks) * groups_per_block + gib;  // local sample of robot b
+    if (b != loaded) {
+      __syncthreads();  // previous item's readers are done with the robot view
+      load_robot_smem(a, sv, b);
+      __syncthreads();
+      loaded = b;
+    }
+    const bool valid = ls < a.K_local;
+    const long long sl = (long long)b * a.K_local + (valid ? ls : 0);         // output slot
+    const long long s = a.s_begin + (valid ? ls : 0);  // noise counter (per-robot key)
+    const double* x0 = a.x0 + (size_t)b * BatchStrides::X0;
+    const uint64_t key = (uint64_t)__double_as_longlong(x0[6]);
+    const int O = task.n_obs;
     // ---------------- phase 1: serial (v, omega) chain with the GP mean
-    double v = a.x0[3], w = a.x0[4];
+    double v = x0[3], w = x0[4];
     if (gl == 0) {
       sv_[0] = v;
       sw[0] = w;
     }
     for (int k = 0; k < T; ++k) {
       double e0 = 0.0, e1 = 0.0;
-      if (valid) sample_noise(a, sl, s, k, &e0, &e1);
+      if (valid) sample_noise(a, key, sl, s, k, &e0, &e1);
       const double u0 = clampd(sv.nom[2 * k] + e0, a.lo[0], a.hi[0]);  // mppi.cpp:298-308
       const double u1 = clampd(sv.nom[2 * k + 1] + e1, a.lo[1], a.hi[1]);
       if (valid && gl == 0) {
@@ -240,7 +258,9 @@ __global__ void __launch_bounds__(256, 1) rollout_gp_kernel(const RolloutArgs a)
         const double2* zn = reinterpret_cast<const double2*>(gp + 4 * ns);
         const double2* al = reinterpret_cast<const double2*>(gp + 5 * ns);
         const int half = ns >> 1;
-#pragma unroll 2
+        // K/148 samples per SM leave ~7 warps per SM; registers are plentiful, so
+        // unroll for ILP (8 independent exp chains in flight per lane)
+#pragma unroll 4
         for (int jp = gl; jp < half; jp += LPS) {
           // gp.cpp:177-179: k*_j = exp(q_aug · inputs_aug_j)
           const double2 a0 = z0[jp], a1 = z1[jp], a2 = z2[jp], a3 = z3[jp], an = zn[jp];
@@ -278,7 +298,7 @@ __global__ void __launch_bounds__(256, 1) rollout_gp_kernel(const RolloutArgs a)
     __syncwarp();
     // ---------------- phase 2a: heading recursion (arc_advance: theta = wrap(theta + omega dt))
     if (gl == 0) {
-      double th = a.x0[2];
+      double th = x0[2];
       sth[0] = th;
       for (int k = 0; k < T; ++k) {
         th = wrap_angle(th + sw[k] * a.nom.dt);
@@ -302,7 +322,7 @@ __global__ void __launch_bounds__(256, 1) rollout_gp_kernel(const RolloutArgs a)
     // ---------------- phase 2c: positions in step order + first non-finite state
     int kd = T;  // states k > kd are frozen at state kd (mppi.cpp:343-346)
     if (gl == 0) {
-      double x = a.x0[0], y = a.x0[1];
+      double x = x0[0], y = x0[1];
       sx[0] = x;
       sy[0] = y;
       for (int k = 0; k < T; ++k) {
@@ -362,23 +382,38 @@ __global__ void __launch_bounds__(256, 1) rollout_gp_kernel(const RolloutArgs a)
   }
 }
 
-// GP-free models (mppi.cpp:351-368): one thread per sample.
-__global__ void __launch_bounds__(256) rollout_base_kernel(const RolloutArgs a) {
+// GP-free models (mppi.cpp:351-368): one thread per sample; block = one robot chunk.
+__global__ void __launch_bounds__(128) rollout_base_kernel(const RolloutArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  SmemView sv = load_common_smem(a, smem);
-  __syncthreads();
+  const SmemView sv = carve_smem(a, smem);
   const TaskDev& task = *sv.task;
-  const int T = a.T, O = a.n_obs;
-  for (int sl = blockIdx.x * blockDim.x + threadIdx.x; sl < a.K_local; sl += gridDim.x * blockDim.x) {
-    const long long s = a.s_begin + sl;
+  const int T = a.T;
+  const int chunks = (a.K_local + blockDim.x - 1) / blockDim.x;
+  const long long items = (long long)a.B * chunks;
+  int loaded = -1;
+  for (long long item = blockIdx.x; item < items; item += gridDim.x) {
+    const int b = (int)(item / chunks);
+    const int ls = (int)(item % chunks) * blockDim.x + threadIdx.x;
+    if (b != loaded) {
+      __syncthreads();
+      load_robot_smem(a, sv, b);
+      __syncthreads();
+      loaded = b;
+    }
+    if (ls >= a.K_local) continue;
+    const long long sl = (long long)b * a.K_local + ls;
+    const long long s = a.s_begin + ls;
+    const double* x0 = a.x0 + (size_t)b * BatchStrides::X0;
+    const uint64_t key = (uint64_t)__double_as_longlong(x0[6]);
+    const int O = task.n_obs;
     double st[5];
-    for (int i = 0; i < 5; ++i) st[i] = a.x0[i];
+    for (int i = 0; i < 5; ++i) st[i] = x0[i];
     bool alive = true;
     double cost = 0.0, decay = 1.0;
     uint32_t vb = 0, cb = 0;
     for (int k = 0; k < T; ++k) {
       double e0, e1;
-      sample_noise(a, sl, s, k, &e0, &e1);
+      sample_noise(a, key, sl, s, k, &e0, &e1);
       const double u[2] = {clampd(sv.nom[2 * k] + e0, a.lo[0], a.hi[0]),
                            clampd(sv.nom[2 * k + 1] + e1, a.lo[1], a.hi[1])};
       double nx[5];
@@ -444,21 +479,29 @@ size_t rollout_scratch_doubles(int T, int num_sms) {
   return (size_t)num_sms * 64 * SCR_ARRAYS * (size_t)(T + 1);
 }
 
+// lane groups per block for the GP rollout: spread one robot's samples over every
+// SM in a single wave when possible (one block per SM)
+int rollout_samples_per_block(int K_local, int num_sms, int* lps_out, int* threads_out) {
+  const int lps = rollout_lanes_per_sample(K_local, num_sms);
+  const int spw = 32 / lps;
+  const long long warps = ((long long)K_local + spw - 1) / spw;
+  int wpb = (int)((warps + num_sms - 1) / num_sms);
+  wpb = wpb < 1 ? 1 : (wpb > 8 ? 8 : wpb);
+  if (lps_out) *lps_out = lps;
+  if (threads_out) *threads_out = wpb * 32;
+  return wpb * spw;
+}
+
 cudaError_t launch_rollout(const RolloutArgs& a, int num_sms, cudaStream_t st) {
   const size_t smem = rollout_smem_bytes(a);
-  if (a.K_local <= 0) return cudaSuccess;
+  if (a.K_local <= 0 || a.B <= 0) return cudaSuccess;
   if (a.model_kind == MODEL_GP) {
     int no = 0;
     for (int g = 0; g < a.model.G; ++g) no = a.model.g[g].n_out > no ? a.model.g[g].n_out : no;
-    int lps = rollout_lanes_per_sample(a.K_local, num_sms);
-    // groups per block: spread the samples evenly over the SMs (one block per SM)
-    const int spw = 32 / lps;
-    long long warps = ((long long)a.K_local + spw - 1) / spw;
-    int wpb = (int)((warps + num_sms - 1) / num_sms);
-    wpb = wpb < 1 ? 1 : (wpb > 8 ? 8 : wpb);
-    long long blocks = (warps + wpb - 1) / wpb;
-    if (blocks > num_sms) blocks = num_sms;
-    const int threads = wpb * 32;
+    int lps = 8, threads = 32;
+    const int spb = rollout_samples_per_block(a.K_local, num_sms, &lps, &threads);
+    const long long items = (long long)a.B * ((a.K_local + spb - 1) / spb);
+    const long long blocks = items < num_sms ? items : num_sms;
     using KF = void (*)(const RolloutArgs);
     KF table[4][4] = {
         {rollout_gp_kernel<2, 4>, rollout_gp_kernel<2, 8>, rollout_gp_kernel<2, 16>, rollout_gp_kernel<2, 32>},
@@ -473,10 +516,11 @@ cudaError_t launch_rollout(const RolloutArgs& a, int num_sms, cudaStream_t st) {
     kern<<<(unsigned)blocks, threads, smem, st>>>(a);
   } else {
     const int threads = 128;
-    int blocks = (a.K_local + threads - 1) / threads;
+    const long long items = (long long)a.B * ((a.K_local + threads - 1) / threads);
+    const long long blocks = items < (long long)num_sms * 8 ? items : (long long)num_sms * 8;
     cudaError_t e = cudaFuncSetAttribute(rollout_base_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    rollout_base_kernel<<<blocks, threads, smem, st>>>(a);
+    rollout_base_kernel<<<(unsigned)blocks, threads, smem, st>>>(a);
   }
   count_launch();
   return cudaGetLastError();
@@ -599,9 +643,11 @@ cudaError_t launch_variance(const VarianceArgs& a, int path, cudaStream_t st) {
 
 // -------------------------------------------------------------------------
 // Reduction: tuple per block, last block combines (+ update/shift/diag).
-int reduce_blocks_for(int K_local, int num_sms) {
+int reduce_blocks_for(int K_local, int B, int num_sms) {
+  // blocks per robot: ~16+ samples per block, at most one wave in total
   int b = (K_local + 15) / 16;
-  if (b > num_sms) b = num_sms;
+  const int cap = num_sms / (B < num_sms ? B : num_sms);
+  if (b > cap) b = cap;
   return b < 1 ? 1 : b;
 }
 
@@ -655,27 +701,51 @@ GPM_D void apply_tuple(const double* tup, int T, double lambda, double* nominal_
   __syncthreads();
 }
 
+// grid = B * bpr; block (b, j) reduces robot b's samples [j*per, (j+1)*per);
+// the last block of each robot combines that robot's bpr tuples in block order.
 __global__ void __launch_bounds__(256) reduce_kernel(const ReduceArgs a) {
   extern __shared__ __align__(16) double dsm[];
   __shared__ double red[32 * 5];
   __shared__ unsigned int s_last;
   const int T = a.T;
-  const int per = (a.K_local + gridDim.x - 1) / gridDim.x;
-  const int b0 = blockIdx.x * per;
+  const int b = blockIdx.x / a.bpr, j = blockIdx.x % a.bpr;
+  const int per = (a.K_local + a.bpr - 1) / a.bpr;
+  const long long base = (long long)b * a.K_local;  // robot-major sample slots
+  const int b0 = j * per;
   const int b1 = min(a.K_local, b0 + per);
   const int W = tuple_doubles(T);
-  // pass 1: costs (cost_mean + var_w * Σ_k trace), block min over finite
+  const long long KT = (long long)a.B * a.K_local * T;
+  const double* rt = a.x0 + (size_t)b * BatchStrides::X0;
+  const double var_w = rt[5];
+  const uint64_t key = (uint64_t)__double_as_longlong(rt[6]);
+  double cg[kMaxGroups];
+#pragma unroll
+  for (int g = 0; g < kMaxGroups; ++g) {
+    double c = 0.0;
+    if (g < a.G)
+      for (int o = 0; o < 8 && a.coef_terrain[g][o] >= 0; ++o) {
+        const double w = a.tw[(size_t)b * BatchStrides::TW + a.coef_terrain[g][o]];
+        c += w * w;
+      }
+    cg[g] = c;
+  }
+  // pass 1: costs (cost_mean + var_w * Σ_k Σ_g coef_g var_g), block min over finite
   double lmin = INFINITY;
   for (int s = b0 + threadIdx.x; s < b1; s += blockDim.x) {
-    double c = a.cost_mean[s];
-    if (a.trace) {
+    const long long q = base + s;
+    double c = a.cost_mean[q];
+    if (a.var) {
       double vsum = 0.0;
-      const double* tr = a.trace + (size_t)s * T;
+      for (int g = 0; g < a.G; ++g) {
+        const double* tr = a.var + (size_t)g * KT + (size_t)q * T;
+        double gsum = 0.0;
 #pragma unroll 8
-      for (int k = 0; k < T; ++k) vsum += __ldcg(tr + k);
-      c += a.var_w * vsum;
+        for (int k = 0; k < T; ++k) gsum += __ldcg(tr + k);
+        vsum += cg[g] * gsum;  // tracking/avoidance trace (mppi.cpp:34-49 combine, costs.cpp:141)
+      }
+      c += var_w * vsum;
     }
-    a.costs_out[s] = c;
+    a.costs_out[q] = c;
     if (isfinite(c)) lmin = fmin(lmin, c);
   }
   lmin = warp_min(lmin);
@@ -692,7 +762,7 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceArgs a) {
   // pass 2: e_s = exp(-(c - m_b)/lambda) (mppi.cpp:137-142) and scalar sums
   double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // Z, E2, H, N, C
   for (int s = b0 + threadIdx.x; s < b1; s += blockDim.x) {
-    const double c = a.costs_out[s];
+    const double c = a.costs_out[base + s];
     double e = 0.0;
     if (isfinite(c)) {
       e = exp(-(c - mb) / a.lambda);
@@ -702,7 +772,7 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceArgs a) {
       v[3] += 1.0;
       v[4] += c;
     }
-    a.e_out[s] = e;
+    a.e_out[base + s] = e;
   }
   block_reduce_5(v, red);
   // pass 3: S[k][c] = Σ_s e_s eps[s][k][c]; thread = (k, slice)
@@ -712,16 +782,16 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceArgs a) {
     const int k = idx % T, sl = idx / T;
     double s0 = 0.0, s1 = 0.0;
     for (int s = b0 + sl; s < b1; s += nsl) {
-      const double e = a.e_out[s];
+      const double e = a.e_out[base + s];
       if (e == 0.0) continue;
       double e0, e1;
       if (a.noise_mode == NOISE_INJECTED) {
-        const double2 ep = reinterpret_cast<const double2*>(a.eps)[(size_t)s * T + k];
+        const double2 ep = reinterpret_cast<const double2*>(a.eps)[(size_t)(base + s) * T + k];
         e0 = ep.x;
         e1 = ep.y;
       } else {
         double z1, z2;
-        philox_gaussian_pair(a.key, (uint64_t)(a.s_begin + s), (uint32_t)k, &z1, &z2);
+        philox_gaussian_pair(key, (uint64_t)(a.s_begin + s), (uint32_t)k, &z1, &z2);
         e0 = a.sv * z1;
         e1 = a.sw * z2;
       }
@@ -748,38 +818,38 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceArgs a) {
   }
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) s_last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1);
+  if (threadIdx.x == 0) s_last = (atomicAdd(a.ticket + b, 1u) == (unsigned)a.bpr - 1);
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  // last block: combine the block tuples in block order (heads staged in smem)
-  double* tup = a.rank_tuple;
-  const int B = gridDim.x;
-  double* heads = dsm;          // [B][6]   (dsm holds >= 7*B + 2T doubles, see launch_reduce)
-  double* sc = dsm + 6 * B;     // [B] rescale factors
-  for (int i = threadIdx.x; i < 6 * B; i += blockDim.x)
-    heads[i] = __ldcg(a.partials + (size_t)(i / 6) * W + (i % 6));
+  // last block of robot b: combine its block tuples in block order (heads staged in smem)
+  double* tup = a.rank_tuple + (size_t)b * W;
+  const double* parts = a.partials + (size_t)b * a.bpr * W;
+  const int BP = a.bpr;
+  double* heads = dsm;       // [BP][6]  (dsm holds >= 7*BP + 2T doubles, see launch_reduce)
+  double* sc = dsm + 6 * BP; // [BP] rescale factors
+  for (int i = threadIdx.x; i < 6 * BP; i += blockDim.x) heads[i] = __ldcg(parts + (size_t)(i / 6) * W + (i % 6));
   __syncthreads();
   if (threadIdx.x == 0) {
     double m = INFINITY;
-    for (int b = 0; b < B; ++b) m = fmin(m, heads[b * 6]);
+    for (int q = 0; q < BP; ++q) m = fmin(m, heads[q * 6]);
     red[0] = m;
   }
   __syncthreads();
   const double m = red[0];
-  for (int b = threadIdx.x; b < B; b += blockDim.x)
-    sc[b] = heads[b * 6 + 4] > 0.0 ? exp(-(heads[b * 6] - m) / a.lambda) : 0.0;
+  for (int q = threadIdx.x; q < BP; q += blockDim.x)
+    sc[q] = heads[q * 6 + 4] > 0.0 ? exp(-(heads[q * 6] - m) / a.lambda) : 0.0;
   __syncthreads();
   if (threadIdx.x == 0) {
     double Z = 0.0, E2 = 0.0, H = 0.0, N = 0.0, C = 0.0;
-    for (int b = 0; b < B; ++b) {
-      const double* p = heads + b * 6;
+    for (int q = 0; q < BP; ++q) {
+      const double* p = heads + q * 6;
       N += p[4];
       C += p[5];
       if (!(p[4] > 0.0)) continue;
-      Z += sc[b] * p[1];
-      E2 += sc[b] * sc[b] * p[2];
-      H += sc[b] * (p[3] + (p[0] - m) * p[1]);
+      Z += sc[q] * p[1];
+      E2 += sc[q] * sc[q] * p[2];
+      H += sc[q] * (p[3] + (p[0] - m) * p[1]);
     }
     tup[0] = m;
     tup[1] = Z;
@@ -787,23 +857,25 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceArgs a) {
     tup[3] = H;
     tup[4] = N;
     tup[5] = C;
-    *a.ticket = 0u;  // re-arm for the next launch
+    a.ticket[b] = 0u;  // re-arm for the next launch
   }
   for (int r = threadIdx.x; r < 2 * T; r += blockDim.x) {
     double acc = 0.0;
-    for (int b = 0; b < B; ++b) acc = fma(sc[b], __ldcg(a.partials + (size_t)b * W + kTupleHead + r), acc);
+    for (int q = 0; q < BP; ++q) acc = fma(sc[q], __ldcg(parts + (size_t)q * W + kTupleHead + r), acc);
     tup[kTupleHead + r] = acc;
   }
   __syncthreads();
-  double* tmp = dsm + 7 * B;  // 2T doubles
-  if (a.finish) apply_tuple(tup, T, a.lambda, a.nominal_seq, a.lo, a.hi, a.out, a.K_total, tmp);
+  double* tmp = dsm + 7 * BP;  // 2T doubles
+  if (a.finish)
+    apply_tuple(tup, T, a.lambda, a.nominal_seq + (size_t)b * BatchStrides::nom(T), a.lo, a.hi,
+                a.out + (size_t)b * BatchStrides::OUT, a.K_total, tmp);
 }
 
 cudaError_t launch_reduce(const ReduceArgs& a, int blocks, cudaStream_t st) {
   const int threads = 256;
   const int nsl = threads / a.T > 1 ? threads / a.T : 1;
   size_t smem = sizeof(double) * (size_t)nsl * a.T * 2;
-  const size_t need = sizeof(double) * ((size_t)7 * blocks + 2 * a.T);
+  const size_t need = sizeof(double) * ((size_t)7 * a.bpr + 2 * a.T);
   if (smem < need) smem = need;
   cudaFuncSetAttribute(reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   reduce_kernel<<<blocks, threads, smem, st>>>(a);
@@ -933,6 +1005,11 @@ constexpr int TIGHT_COLS = 256;  // columns of L^{-T} per variance block
 constexpr int TMEAN_THREADS = 128;
 template <int NO>
 __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const TightenArgs a) {
+  const int rb = blockIdx.x;  // robot
+  const double* ax0 = a.x0 + (size_t)rb * BatchStrides::X0;
+  double* atq = a.tq + (size_t)rb * 4 * a.T;
+  double* atJ = a.tJ + (size_t)rb * 25 * a.T;
+  double* atmu = a.tmu + (size_t)rb * 5 * (a.T + 1);
   extern __shared__ __align__(16) double tsm[];  // [2T nominal][T+1 v][T+1 w][T+1 th][T dx][T dy][pts]
   __shared__ double tw[kMaxTerrains];
   __shared__ double etab[32];
@@ -946,12 +1023,12 @@ __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const Tight
   double* dx = th + (T + 1);
   double* dy = dx + T;
   double* pts = dy + T + ((7 * T + 3) & 1);  // 16-byte aligned for the vectorised staging
-  if (threadIdx.x < a.R) tw[threadIdx.x] = a.tw[threadIdx.x];
-  for (int i = threadIdx.x; i < 2 * T; i += blockDim.x) nom[i] = a.nominal_seq[i];
+  if (threadIdx.x < a.R) tw[threadIdx.x] = a.tw[(size_t)rb * BatchStrides::TW + threadIdx.x];
+  for (int i = threadIdx.x; i < 2 * T; i += blockDim.x) nom[i] = a.nominal_seq[(size_t)rb * BatchStrides::nom(T) + i];
   if (threadIdx.x == 0) {
-    vv[0] = a.x0[3];
-    ww[0] = a.x0[4];
-    th[0] = a.x0[2];
+    vv[0] = ax0[3];
+    ww[0] = ax0[4];
+    th[0] = ax0[2];
   }
   if (a.model_kind == MODEL_GP) {  // vectorised staging of Z / alpha
     double* dst = pts;
@@ -1034,10 +1111,10 @@ __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const Tight
       }
     }
     if (threadIdx.x == 0) {
-      a.tq[k * 4 + 0] = v;
-      a.tq[k * 4 + 1] = om;
-      a.tq[k * 4 + 2] = u0;
-      a.tq[k * 4 + 3] = u1;
+      atq[k * 4 + 0] = v;
+      atq[k * 4 + 1] = om;
+      atq[k * 4 + 2] = u0;
+      atq[k * 4 + 3] = u1;
     }
     v = v + av * (u0 - v) + c0;  // step_nominal lag (dynamics.cpp:63-64) + correction mean
     om = om + aw * (u1 - om) + c1;
@@ -1060,17 +1137,17 @@ __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const Tight
     dy[k] = y;
     double J[25];
     jacobian_nominal(m0, a.nom, J);
-    for (int i = 0; i < 25; ++i) a.tJ[k * 25 + i] = J[i];
+    for (int i = 0; i < 25; ++i) atJ[k * 25 + i] = J[i];
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double x = a.x0[0], y = a.x0[1];
+    double x = ax0[0], y = ax0[1];
     for (int k = 0; k <= T; ++k) {
-      a.tmu[k * 5 + 0] = x;
-      a.tmu[k * 5 + 1] = y;
-      a.tmu[k * 5 + 2] = th[k];
-      a.tmu[k * 5 + 3] = vv[k];
-      a.tmu[k * 5 + 4] = ww[k];
+      atmu[k * 5 + 0] = x;
+      atmu[k * 5 + 1] = y;
+      atmu[k * 5 + 2] = th[k];
+      atmu[k * 5 + 3] = vv[k];
+      atmu[k * 5 + 4] = ww[k];
       if (k < T) {
         x += dx[k];
         y += dy[k];
@@ -1083,11 +1160,11 @@ __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const Tight
 __global__ void __launch_bounds__(TIGHT_COLS) tighten_var_kernel(const TightenArgs a) {
   extern __shared__ __align__(16) double kst[];
   __shared__ double red[TIGHT_COLS / 32];
-  const int k = blockIdx.x, g = blockIdx.y, c = blockIdx.z;
+  const int k = blockIdx.x, g = blockIdx.y % a.model.G, rb = blockIdx.y / a.model.G, c = blockIdx.z;
   const int n = a.model.n;
   if (a.model_kind != MODEL_GP) return;
   const GroupDev& G = a.model.g[g];
-  const double* q = a.tq + k * 4;
+  const double* q = a.tq + (size_t)rb * 4 * a.T + k * 4;
   const double q0 = q[0] / G.ls[0], q1 = q[1] / G.ls[1], q2 = q[2] / G.ls[2], q3 = q[3] / G.ls[3];
   const double qn = -0.5 * (q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
   const int j0 = c * TIGHT_COLS;
@@ -1116,23 +1193,31 @@ __global__ void __launch_bounds__(TIGHT_COLS) tighten_var_kernel(const TightenAr
   if (threadIdx.x == 0) {
     double s = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
-    a.tvar_part[((size_t)k * a.model.G + g) * gridDim.z + c] = s;
+    a.tvar_part[(((size_t)rb * a.T + k) * a.model.G + g) * gridDim.z + c] = s;
   }
 }
 
 // one warp: Σ_{k+1} = J Σ Jᵀ + diag(0,0,0,cv0,cv1), symmetrised; r̄_k and margins.
 __global__ void __launch_bounds__(32) tighten_cov_kernel(const TightenArgs a, int nsplit) {
+  const int rb = blockIdx.x;  // robot
+  const double* atJ = a.tJ + (size_t)rb * 25 * a.T;
+  const double* atmu = a.tmu + (size_t)rb * 5 * (a.T + 1);
+  const double* atvar = a.tvar_part + (size_t)rb * a.T * (a.model_kind == MODEL_GP ? a.model.G : 1) * nsplit;
+  const double* atw = a.tw + (size_t)rb * BatchStrides::TW;
+  double* ahcov = a.horizon_cov + (size_t)rb * 25 * a.T;
+  double* arbar = a.r_bar + (size_t)rb * BatchStrides::rbar(a.T);
+  double* amarg = a.margins + (size_t)rb * BatchStrides::marg(a.T);
   extern __shared__ __align__(16) double csm[];  // [T][25] J, [T][2] cv, [T+1][5] mu
   __shared__ double S[25], JS[25], C[25];
   __shared__ int infeasible;
   const int l = threadIdx.x;
-  const TaskDev& t = *a.task;
+  const TaskDev& t = a.task[rb];
   const int T = a.T;
   double* Js = csm;
   double* cvs = csm + 25 * T;
   double* mus = cvs + 2 * T;
-  for (int i = l; i < 25 * T; i += 32) Js[i] = a.tJ[i];
-  for (int i = l; i < 5 * (T + 1); i += 32) mus[i] = a.tmu[i];
+  for (int i = l; i < 25 * T; i += 32) Js[i] = atJ[i];
+  for (int i = l; i < 5 * (T + 1); i += 32) mus[i] = atmu[i];
   // per-step combined correction variance (gp.cpp:187-191 + ensemble_combine gp.cpp:380-386)
   for (int k = l; k < T; k += 32) {
     double c0 = 0.0, c1 = 0.0;
@@ -1140,12 +1225,12 @@ __global__ void __launch_bounds__(32) tighten_cov_kernel(const TightenArgs a, in
       double vg[kMaxGroups];
       for (int g = 0; g < a.model.G; ++g) {
         double s = 0.0;
-        for (int c = 0; c < nsplit; ++c) s += a.tvar_part[((size_t)k * a.model.G + g) * nsplit + c];
+        for (int c = 0; c < nsplit; ++c) s += atvar[((size_t)k * a.model.G + g) * nsplit + c];
         const double v = a.model.g[g].sv - s;
         vg[g] = v > 0.0 ? v : 0.0;
       }
       for (int i = 0; i < a.R; ++i) {
-        const double wi = a.tw[i];
+        const double wi = atw[i];
         int g0 = 0, g1 = 0;
         for (int g = 0; g < a.model.G; ++g)
           for (int o = 0; o < a.model.g[g].n_out; ++o) {
@@ -1188,7 +1273,7 @@ __global__ void __launch_bounds__(32) tighten_cov_kernel(const TightenArgs a, in
     }
     __syncwarp();
   }
-  for (int i = l; i < 25 * T; i += 32) a.horizon_cov[i] = Ss[i];
+  for (int i = l; i < 25 * T; i += 32) ahcov[i] = Ss[i];
   for (int k = l; k < T; k += 32) {  // tighten_lane_radius (uncertainty.cpp:90-96), parallel in k
     if (t.kind == TASK_AVOIDANCE) break;
     const double* Sk = Ss + 25 * k;
@@ -1198,7 +1283,7 @@ __global__ void __launch_bounds__(32) tighten_cov_kernel(const TightenArgs a, in
     double lm = half_tr + sqrt(disc > 0.0 ? disc : 0.0);
     lm = lm > 0.0 ? lm : 0.0;
     const double r = t.half_width - sqrt(a.chi2 * lm);
-    a.r_bar[k] = r;
+    arbar[k] = r;
     if (r <= 0.0) atomicOr(&infeasible, 1);
   }
   if (t.kind != TASK_TRACKING)  // tighten_obstacle_distance (uncertainty.cpp:98-116), parallel in (k, o)
@@ -1223,11 +1308,11 @@ __global__ void __launch_bounds__(32) tighten_cov_kernel(const TightenArgs a, in
       double dv = n0 * cn0 + n1 * cn1;
       dv = dv > 0.0 ? dv : 0.0;
       const double dbar = d - a.z * sqrt(dv);
-      a.margins[(size_t)k * t.n_obs + o] = d - dbar;
+      amarg[(size_t)k * t.n_obs + o] = d - dbar;
       if (dbar <= 0.0) atomicOr(&infeasible, 1);
     }
   __syncwarp();
-  if (l == 0) *a.infeasible = infeasible;
+  if (l == 0) a.infeasible[rb] = infeasible;
 }
 
 int tighten_splits(int n) { return n > 0 ? (n + TIGHT_COLS - 1) / TIGHT_COLS : 1; }
@@ -1242,15 +1327,15 @@ cudaError_t launch_tighten(const TightenArgs& a, cudaStream_t st) {
   void (*mk)(const TightenArgs) = no <= 2 ? tighten_mean_kernel<2> : no <= 4 ? tighten_mean_kernel<4>
                                   : no <= 6 ? tighten_mean_kernel<6> : tighten_mean_kernel<8>;
   cudaFuncSetAttribute(mk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm);  // static + dynamic may exceed 48 KB
-  mk<<<1, TMEAN_THREADS, msm, st>>>(a);
+  mk<<<a.B, TMEAN_THREADS, msm, st>>>(a);
   const int G = a.model_kind == MODEL_GP ? a.model.G : 1;
   const int ns = a.model_kind == MODEL_GP ? tighten_splits(a.model.n) : 1;
   const size_t smem = sizeof(double) * (size_t)(a.model.n > 0 ? a.model.n : 1);
   cudaFuncSetAttribute(tighten_var_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (a.model_kind == MODEL_GP) tighten_var_kernel<<<dim3(a.T, G, ns), TIGHT_COLS, smem, st>>>(a);
+  if (a.model_kind == MODEL_GP) tighten_var_kernel<<<dim3(a.T, G * a.B, ns), TIGHT_COLS, smem, st>>>(a);
   const size_t csmem = sizeof(double) * (size_t)(25 * a.T + 2 * a.T + 5 * (a.T + 1) + 25 * a.T);
   cudaFuncSetAttribute(tighten_cov_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem);
-  tighten_cov_kernel<<<1, 32, csmem, st>>>(a, ns);
+  tighten_cov_kernel<<<a.B, 32, csmem, st>>>(a, ns);
   count_launch(3);
   return cudaGetLastError();
 }

@@ -258,6 +258,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
           if (!(dbg & 16)) mbar_wait_prof(smem_u32(&full_a[sa]), (ia / SA) & 1, 2, dbg);
           if (!(dbg & 32)) mbar_wait_prof(smem_u32(&full_b[sb]), (ib / STAGES_B) & 1, 3, dbg);
           tc_after();
+          const unsigned long long tm0 = clock64();
           const int4 meta = G.tc_meta[chunk0 + kb];
           const int ncols = meta.y, col0 = meta.z;
           const uint32_t a_hi = smem_u32(sA + (size_t)sa * 2 * A_STAGE_FLOATS);
@@ -283,6 +284,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
           }
           mma_commit(smem_u32(&empty_a[sa]));  // stages free once these MMAs complete
           mma_commit(smem_u32(&empty_b[sb]));
+          prof_add(13, clock64() - tm0, dbg);
         }
         mma_commit(smem_u32(tfull));  // accumulator of this pass ready
         chunk0 += nk;
@@ -309,6 +311,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
           const uint32_t ph = (it / SA) & 1;
           if (lane == 0 && !(dbg & 64)) mbar_wait_prof(smem_u32(&empty_a[s]), ph ^ 1, 4, dbg);
           __syncwarp();
+          const unsigned long long tp0 = clock64();
           float* ahi = sA + (size_t)s * 2 * A_STAGE_FLOATS;
           float* alo = ahi + A_STAGE_FLOATS;
           const int row_off = (m >> 3) * (SBO / 4) + (m & 7) * 4;
@@ -333,7 +336,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
           }
           if (!(dbg & 128)) fence_proxy_async();  // generic-proxy smem writes -> visible to tcgen05
           __syncwarp();
-          if (lane == 0) mbar_arrive(smem_u32(&full_a[s]));
+          if (lane == 0) {
+            mbar_arrive(smem_u32(&full_a[s]));
+            prof_add(12, clock64() - tp0, dbg);
+          }
         }
       }
     }
@@ -348,6 +354,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
         const int npw = min(NP, n_pad - p * NP);
         if (lane == 0) mbar_wait_prof(smem_u32(tfull), uc & 1, 5, dbg);
         __syncwarp();
+        const unsigned long long te0 = clock64();
         tc_after();
         const uint32_t trow = tmem_base + ((uint32_t)(e * 32) << 16);
         int c = (dbg & 8) ? npw : 0;
@@ -374,6 +381,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
         tc_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(tempty));
+        if (lane == 0) prof_add(14, clock64() - te0, dbg);
       }
       const long long q = (long long)tile * M + m;
       if (q < a.KT) {

@@ -521,6 +521,143 @@ class Planner:
         return cmd
 
 
+class BatchPlanner(Planner):
+    """B independent planners sharing one model (BASELINE config 4).
+
+    Robot b is exactly ``Planner`` with ``cfg.seed = seeds[b]`` (default cfg.seed + b);
+    all robots tick together through one launch sequence. Per-robot arrays are
+    robot-major: ``plan_step(x0[B,5], tasks[B]) -> commands[B,2]``.
+    """
+
+    def __init__(self, cfg: MppiConfig, model, n_robots: int, nominal: NominalParams = None,
+                 p_x: float = 0.95, seeds=None, device: int = 0):
+        nominal = nominal or NominalParams()
+        self.cfg = cfg
+        self._model_ref = model
+        self._cfg_c = cfg.to_c()
+        self._pm_c = _model_c(model)
+        self._nom_c = A.NominalC(nominal.tau_v, nominal.tau_omega, nominal.dt)
+        sd = None
+        if seeds is not None:
+            sd = (C.c_uint64 * n_robots)(*[int(s) for s in seeds])
+        h = C.c_void_p()
+        A.check(A.lib().gpmppi_planner_create_batch(C.byref(self._cfg_c), C.byref(self._pm_c),
+                                                    C.byref(self._nom_c), p_x, n_robots, sd, device,
+                                                    C.byref(h)))
+        self._h = h
+        self.T = cfg.horizon
+        self.K = cfg.samples
+        self.B = n_robots
+
+    def robots(self) -> int:
+        return A.lib().gpmppi_planner_robots(self._h)
+
+    def _tasks_c(self, tasks):
+        if len(tasks) != self.B:
+            raise ValueError("BatchPlanner: need one task per robot")
+        arr = (A.TaskC * self.B)()
+        for b, t in enumerate(tasks):
+            arr[b] = t.to_c()
+        return arr
+
+    def plan_step(self, x0, tasks, diags=None):
+        x = _f64(x0, (self.B, 5))
+        tc = self._tasks_c(tasks)
+        cmd = np.empty((self.B, 2))
+        d = (A.DiagC * self.B)()
+        A.check(A.lib().gpmppi_planner_plan_step_batch(self._h, A.dptr(x), tc, A.dptr(cmd), d))
+        if diags is not None:
+            for b in range(self.B):
+                for k, _ in A.DiagC._fields_:
+                    setattr(diags[b], k, getattr(d[b], k))
+                diags[b].tightening_infeasible = bool(d[b].tightening_infeasible)
+        return cmd
+
+    def set_robot_terrain_weights(self, robot: int, w):
+        w = _f64(w, (-1,))
+        A.check(A.lib().gpmppi_planner_set_robot_terrain_weights(self._h, robot, A.dptr(w), w.shape[0]))
+
+    def terrain_weights(self):
+        buf = np.empty(self.B * A.MAX_TERRAINS)
+        R = A.lib().gpmppi_planner_terrain_weights(self._h, A.dptr(buf))
+        return buf[: self.B * R].reshape(self.B, R).copy()
+
+    def nominal_sequence(self):
+        s = np.empty((self.B, self.T, 2))
+        A.check(A.lib().gpmppi_planner_nominal_sequence(self._h, A.dptr(s)))
+        return s
+
+    def set_nominal_sequence(self, seq):
+        s = _f64(seq, (self.B, self.T, 2))
+        A.check(A.lib().gpmppi_planner_set_nominal_sequence(self._h, A.dptr(s)))
+
+    def horizon_covariances(self):
+        c = np.empty((self.B, self.T, 5, 5))
+        A.check(A.lib().gpmppi_planner_horizon_covariances(self._h, A.dptr(c)))
+        return c
+
+    def lane_radii(self):
+        r = np.empty((self.B, self.T))
+        n = A.lib().gpmppi_planner_lane_radii(self._h, A.dptr(r))
+        if n < 0:
+            A.check(A.CUDA_ERROR)
+        return r if n else np.zeros((self.B, 0))
+
+    def obstacle_margins(self):
+        m = np.empty(self.B * self.T * A.MAX_OBSTACLES)
+        O = A.lib().gpmppi_planner_obstacle_margins(self._h, A.dptr(m))
+        if O < 0:
+            A.check(A.CUDA_ERROR)
+        return m[: self.B * self.T * O].reshape(self.B, self.T, O).copy()
+
+    def set_thresholds(self, r_bar=None, margins=None):
+        r = None if r_bar is None else _f64(r_bar, (self.B, self.T))
+        m = None if margins is None else _f64(margins, (self.B, self.T, -1))
+        O = 0 if m is None else m.shape[2]
+        A.check(A.lib().gpmppi_planner_set_thresholds(self._h, A.dptr(r), A.dptr(m), O))
+
+    def inject_noise(self, eps):
+        e = _f64(eps, (self.B, self.samples_local(), self.T, 2))
+        A.check(A.lib().gpmppi_planner_inject_noise(self._h, A.dptr(e)))
+
+    def philox_noise(self, tick: int):
+        e = np.empty((self.B, self.samples_local(), self.T, 2))
+        A.check(A.lib().gpmppi_planner_philox_noise(self._h, tick, A.dptr(e)))
+        return e
+
+    def sample_costs(self):
+        c = np.empty((self.B, self.samples_local()))
+        A.check(A.lib().gpmppi_planner_sample_costs(self._h, A.dptr(c)))
+        return c
+
+    def sample_weights(self):
+        w = np.empty((self.B, self.samples_local()))
+        A.check(A.lib().gpmppi_planner_sample_weights(self._h, A.dptr(w)))
+        return w
+
+    def flags(self):
+        B, K, T = self.B, self.samples_local(), self.T
+        v = np.empty((B, K, T), np.uint8)
+        c = np.empty((B, K, T), np.uint8)
+        t = np.empty((B, K), np.uint8)
+        a = np.empty((B, K), np.uint8)
+        A.check(A.lib().gpmppi_planner_flags(self._h, A.u8ptr(v), A.u8ptr(c), A.u8ptr(t),
+                                             A.u8ptr(a)))
+        return dict(viol=v, coll=c, terminal=t, alive=a)
+
+    def bench_device(self, x0, tasks, ticks: int, flush_l2: bool = True):
+        x = _f64(x0, (self.B, 5))
+        tc = self._tasks_c(tasks)
+        tick_ms = np.zeros(ticks)
+        ph = np.zeros(4)
+        A.check(A.lib().gpmppi_planner_bench_device(self._h, A.dptr(x), tc, ticks, int(flush_l2),
+                                                    A.dptr(tick_ms), A.dptr(ph)))
+        return tick_ms, ph
+
+    def set_shard(self, begin: int, count: int):
+        raise ValueError("BatchPlanner: batched planners shard by robot, not by sample")
+
+
 def shard_range(total: int, world: int, rank: int):
     """Contiguous global sample range of `rank`: [begin, begin+count)."""
     base, extra = divmod(total, world)

@@ -66,10 +66,11 @@ class Workload:
     lam: float = 0.1
     sigma_sim: tuple = (0.09, 0.25)
     seed: int = 11  # planner seed (acceptance.cpp:430)
+    robots: int = 1  # independent planners sharing the model (config 4)
 
     @property
     def sample_steps(self) -> int:
-        return self.samples * self.horizon
+        return self.robots * self.samples * self.horizon
 
     def flops_per_sample_step(self) -> int:
         """F = n² + 24n algorithmic FLOP per sample-rollout-step."""
@@ -87,6 +88,9 @@ CONFIGS = {
     # configs[2]: multi-terrain, GP-variance heavy
     "config3": Workload("config3", 16384, 60, 2048, 3, "tracking", "circle", 0,
                         (2.0, 0.0, np.pi / 2, 0.0, 0.0)),
+    # configs[3]: 256 independent robots sharing one GP model, one solve each per launch
+    "config4": Workload("config4", 4096, 40, 512, 3, "combined", "lane", 10,
+                        (0.0, 0.0, 0.0, 0.0, 0.0), robots=256),
     # configs[4] unit: K per GPU in the sharded sweep
     "config5": Workload("config5", 65536, 40, 512, 3, "combined", "lane", 10,
                         (0.0, 0.0, 0.0, 0.0, 0.0)),

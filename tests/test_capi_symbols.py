@@ -33,7 +33,7 @@ def test_library_loads_and_fails_loudly_without_gpu():
     import numpy as np
     import pytest
     import paper_2411_03289_b200 as G
-    assert G._capi.lib().gpmppi_abi_version() == 1
+    assert G._capi.lib().gpmppi_abi_version() == 2
     try:
         import torch
         has_gpu = torch.cuda.is_available()

@@ -23,8 +23,12 @@ A.lib().gpmppi_debug_tc_profile(A.dptr(out))
 ctas = out[11]
 names = ["B wait empty_b", "MMA wait tempty", "MMA wait full_a", "MMA wait full_b",
          "A wait empty_a (lane0/warp)", "EPI wait tfull (lane0/warp)", "B total", "MMA total",
-         "producers total (per warp)", "epilogue total (per warp)"]
-per = {0: ctas, 1: ctas, 2: ctas, 3: ctas, 4: ctas * 8, 5: ctas * 4, 6: ctas, 7: ctas, 8: ctas * 8, 9: ctas * 4}
+         "producers total (per warp)", "epilogue total (per warp)", "-", "-",
+         "producer compute+store (per warp)", "MMA issue (excl. waits)", "epilogue drain (per warp)"]
+per = {0: ctas, 1: ctas, 2: ctas, 3: ctas, 4: ctas * 8, 5: ctas * 4, 6: ctas, 7: ctas, 8: ctas * 8, 9: ctas * 4,
+       10: 1, 11: 1, 12: ctas * 8, 13: ctas, 14: ctas * 4}
 print(f"variance phase {ph[1] / ticks * 1e3:.1f} us/tick; CTAs {ctas:.0f}")
 for i, nm in enumerate(names):
+    if nm == "-":
+        continue
     print(f"{nm:32s} {out[i] / per[i] / 1.965e3:9.1f} us per role-instance")
