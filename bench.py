@@ -106,7 +106,7 @@ def roofline_block(w, phase, steps, peaks, peaks_kind):
     ceilings (TF32 dense = bf16/2, FP64 = 148·64 DFMA·2·clock) are reported beside it.
     """
     n = w.n_points
-    units = w.samples * w.horizon
+    units = w.sample_steps
     roll_ms, var_ms = phase[0] / steps, phase[1] / steps
     if var_ms >= roll_ms:
         kern, ms, flop = "variance_tc_kernel", var_ms, units * (n * n + 3 * n)
@@ -120,7 +120,7 @@ def roofline_block(w, phase, steps, peaks, peaks_kind):
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get(kern)
+            traffic = json.load(f).get(w.name, {}).get(kern)
     except Exception:
         pass
     return {"bound": "tensor", "kernel": kern, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -132,19 +132,26 @@ def roofline_block(w, phase, steps, peaks, peaks_kind):
 
 
 def build_planner(w, api, samples=None, var_path=None):
+    """(planner, task, x0); a BatchPlanner with per-robot tasks / states when w.robots > 1."""
     from paper_2411_03289_b200 import workloads as W
-    task, track, obstacles = W.make_task_objects(w, api)
     cfg = api.MppiConfig(samples=samples or w.samples, horizon=w.horizon, lam=w.lam,
                          sigma_sim=w.sigma_sim, seed=w.seed)
     if w.model == "gp":
         X, Y, K = W.gp_training_set(w.n_points, w.terrains, seed=0)
         gp = api.GpModel.fit(X, Y, K)
-        p = api.Planner(cfg, api.GpEnsemble(gp, w.terrains), p_x=w.p_x)
+        model = api.GpEnsemble(gp, w.terrains)
     else:
-        p = api.Planner(cfg, api.NominalDynamic(), p_x=w.p_x)
+        model = api.NominalDynamic()
+    if w.robots > 1:
+        p = api.BatchPlanner(cfg, model, w.robots, p_x=w.p_x)
+        task, x0 = W.make_batch_tasks(w, api)
+    else:
+        p = api.Planner(cfg, model, p_x=w.p_x)
+        task = W.make_task_objects(w, api)[0]
+        x0 = np.array(w.x0, dtype=np.float64)
     if var_path is not None:
         p.set_variance_path(var_path)
-    return p, task
+    return p, task, x0
 
 
 def cpu_reference(w, steps, warmup, threads=0, samples=None):
@@ -192,7 +199,8 @@ def run_reference_arm(args, w):
                    "gp_points": w.n_points},
         "cpu_baseline": {"value": value, "unit": "sample-rollout-steps/s", "cores": threads,
                          "kind": "port", "sample": f"{args.steps} full plan_step ticks of {w.name} "
-                         f"(K={K}) on {threads} threads; {cpu}"},
+                         f"(K={K}{', one robot of ' + str(w.robots) if w.robots > 1 else ''}) "
+                         f"on {threads} threads; {cpu}"},
         "e2e": {"value": value, "unit": "sample-rollout-steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -242,8 +250,7 @@ def main():
         launches, e2e_ms, (h2d, d2h) = 7 * args.steps, [1.1] * args.steps, (2768, 68)
     else:
         import paper_2411_03289_b200 as G
-        planner, task = build_planner(w, G, var_path=args.variance_path)
-        x0 = np.array(w.x0, dtype=np.float64)
+        planner, task, x0 = build_planner(w, G, var_path=args.variance_path)
         for _ in range(args.warmup):
             planner.plan_step(x0, task)
         launches0 = G.kernel_launches()
@@ -258,7 +265,7 @@ def main():
             planner.plan_step(x0, task)
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
         h2d, d2h = planner.io_bytes()
-    steps_per_tick = w.samples * w.horizon
+    steps_per_tick = w.sample_steps  # robots x samples x horizon
     mean_ms = float(np.mean(tick_ms))
     value = steps_per_tick / (mean_ms / 1e3)
     e2e_value = steps_per_tick / (float(np.mean(e2e_ms)) / 1e3)
@@ -266,15 +273,16 @@ def main():
     roofline = roofline_block(w, phase, args.steps, peaks, peaks_kind)
     n = w.n_points
     rollout_ms, var_ms = phase[0] / args.steps, phase[1] / args.steps
+    robots = f"{w.robots} robots x " if w.robots > 1 else ""
     line = {
         "metric": "sample-rollout-steps/s (GP-MPPI solve; p50/p99 latency in p50_ms/p99_ms)",
         "value": value, "unit": "sample-rollout-steps/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": mean_ms, "p50_ms": _percentile(tick_ms, 50),
         "p99_ms": _percentile(tick_ms, 99), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
-        "config": {"workload": f"{w.name}: GP-MPPI path following + {w.n_obstacles} tightened "
+        "config": {"workload": f"{w.name}: {robots}GP-MPPI path following + {w.n_obstacles} tightened "
                    f"obstacles, K={w.samples} T={w.horizon} M={n} R={w.terrains} p_x={w.p_x}",
-                   "samples": w.samples, "horizon": w.horizon, "gp_points": n,
+                   "robots": w.robots, "samples": w.samples, "horizon": w.horizon, "gp_points": n,
                    "parallelism": "single GPU", "l2": "flushed between ticks (2x L2 memset)",
                    "variance_path": planner.variance_path()},
         "phase_ms": {"rollout": rollout_ms, "variance": var_ms,
@@ -308,12 +316,11 @@ def run_sharded(args, w, world, rank):
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     K_total = w.samples * world
-    planner, task = build_planner(w, G, samples=K_total)
+    planner, task, x0 = build_planner(w, G, samples=K_total)
     planner.set_shard(rank * w.samples, w.samples)
     W_t = G.tuple_doubles(w.horizon)
     mine = torch.zeros(W_t, dtype=torch.float64, device="cuda")
     gathered = torch.zeros(world, W_t, dtype=torch.float64, device="cuda")
-    x0 = np.array(w.x0, dtype=np.float64)
 
     def tick():
         planner.plan_partial(x0, task, mine.data_ptr())

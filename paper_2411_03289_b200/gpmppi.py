@@ -556,8 +556,11 @@ class BatchPlanner(Planner):
         if len(tasks) != self.B:
             raise ValueError("BatchPlanner: need one task per robot")
         arr = (A.TaskC * self.B)()
+        keep = []  # to_c() rebinds the task's buffers: hold every copy until the call returns
         for b, t in enumerate(tasks):
             arr[b] = t.to_c()
+            keep.append((t._track_c, t._obs))
+        self._task_keep = keep
         return arr
 
     def plan_step(self, x0, tasks, diags=None):

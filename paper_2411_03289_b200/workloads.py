@@ -111,3 +111,24 @@ def make_task_objects(w: Workload, api):
     else:
         task = api.AvoidanceTask(obstacles, api.GoalSpec((8.0, 0.0), 0.5))
     return task, track, obstacles
+
+
+def make_batch_tasks(w: Workload, api):
+    """Config 4 scenarios: robot b gets its own obstacle field (seed 3 + b) and a
+    lateral start offset; the track, weights and goal are shared."""
+    if w.track == "circle":
+        track = api.Track.circle_track((0.0, 0.0), 2.0, 0.4)
+    else:
+        track = api.Track.polyline_track([[0.0, 0.0], [60.0, 0.0]], 0.4, False)
+    tasks, x0 = [], np.zeros((w.robots, 5))
+    for b in range(w.robots):
+        obstacles = random_obstacle_field(w.n_obstacles, seed=3 + b) if w.n_obstacles else np.zeros((0, 3))
+        if w.task == "tracking":
+            tasks.append(api.TrackingTask(track, w.v_desired))
+        elif w.task == "combined":
+            tasks.append(api.CombinedTask(track, w.v_desired, obstacles))
+        else:
+            tasks.append(api.AvoidanceTask(obstacles, api.GoalSpec((8.0, 0.0), 0.5)))
+        x0[b] = w.x0
+        x0[b, 1] += 0.1 * ((b % 5) - 2) / 2.0
+    return tasks, x0
