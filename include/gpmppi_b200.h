@@ -235,6 +235,9 @@ int gpmppi_planner_io_bytes(const gpmppi_planner* p, int64_t* h2d, int64_t* d2h)
 /* diagnostics: per-role cycle counters of the tensor-core variance kernel,
  * filled when GPMPPI_TC_DEBUG has bit 512 set; read-and-reset */
 int gpmppi_debug_tc_profile(double* out16);
+/* diagnostics: clock64 timeline of CTA 0 of the last tensor-core variance launch
+ * (GPMPPI_TC_DEBUG bit 4096): entry, role tile starts, accumulator hand-offs */
+int gpmppi_debug_tc_trace(double* out64);
 int gpmppi_tuple_doubles(int horizon);
 int gpmppi_planner_set_shard(gpmppi_planner* p, int64_t begin, int64_t count);
 int gpmppi_planner_plan_partial(gpmppi_planner* p, const double x0[5], const gpmppi_task* task,

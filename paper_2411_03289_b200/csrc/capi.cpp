@@ -1297,6 +1297,10 @@ int gpmppi_debug_tc_profile(double* out16) {
   return guarded([&] { gpm::tc_profile_read(out16); });
 }
 
+int gpmppi_debug_tc_trace(double* out64) {
+  return guarded([&] { gpm::tc_trace_read(out64); });
+}
+
 int gpmppi_tuple_doubles(int horizon) { return gpm::tuple_doubles(horizon); }
 
 int gpmppi_planner_set_shard(gpmppi_planner* p, int64_t begin, int64_t count) {

@@ -162,6 +162,7 @@ int tighten_splits(int n);
 void build_tc_operand(const double* ilt, int n, std::vector<float>& data, std::vector<int4>& meta,
                       int& n_pad, int& np, int& n_pass);
 void tc_profile_read(double* out);
+void tc_trace_read(double* out);  // 64 clock64 stamps of CTA 0 (GPMPPI_TC_DEBUG bit 4096)
 void count_launch(int n = 1);
 unsigned long long launches_total();
 

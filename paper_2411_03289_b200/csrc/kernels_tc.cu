@@ -11,11 +11,13 @@
 // loses 2-8% relative variance to cancellation). 1xTF32 (hi·hi only) is the
 // optional fast path, gated by the tolerance harness.
 //
-// Warp roles (12 warps): w0 bulk-copies the pre-tiled B chunk (host-arranged in
+// Warp roles (16 warps): w0 bulk-copies the pre-tiled B blocks (host-arranged in
 // the UMMA K-major no-swizzle canonical layout), w1 issues tcgen05.mma from one
 // thread and owns the TMEM allocation, w4-7 drain TMEM (tcgen05.ld) into
-// Σ a_j^2, w8-11 produce A (exp, hi/lo split) into shared memory.
-// Pipelines: smem ring (full_a/full_b -> MMA -> empty), TMEM (full -> epilogue -> empty).
+// Σ a_j^2, w8-15 produce A (exp, hi/lo split) into shared memory.
+// Pipelines: smem rings (full_a/full_b -> MMA -> empty), TMEM (full -> epilogue -> empty).
+// B moves in 8-point K blocks (<= 32 KB hi+lo) through a 4-5 deep ring: the L2 ->
+// SMEM stream of L^{-T} is the kernel's critical feed, so it keeps ~100 KB in flight.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -33,11 +35,13 @@ namespace tc {
 constexpr int M = 128;      // queries per tile (UMMA M, TMEM lanes)
 constexpr int KC = 16;      // points per K chunk (two K=8 TF32 MMAs)
 constexpr int STAGES_A = 4; // k* ring, max (16 KB per stage: hi + lo); 3 when n is large
-constexpr int STAGES_B = 2; // L^{-T} ring (<= 64 KB per stage)
+constexpr int KB = 8;       // points per B block (one K=8 TF32 MMA step)
+constexpr int STAGES_B = 4; // L^{-T} ring (<= 32 KB per stage), 5 when shared memory allows
 constexpr int PRODUCER_WARPS = 8;
 constexpr int THREADS = 256 + 32 * PRODUCER_WARPS;
 constexpr int A_STAGE_FLOATS = M * KC;       // per hi or lo
-constexpr int SBO = (KC / 4) * 128;          // bytes between 8-row groups
+constexpr int SBO = (KC / 4) * 128;          // A: bytes between 8-row groups
+constexpr int SBO_B = (KB / 4) * 128;        // B: bytes between 8-row groups
 constexpr int LBO = 128;                     // bytes between 16-byte K chunks
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -82,29 +86,34 @@ __device__ __forceinline__ void fence_barrier_init() {
 __device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t sbo = SBO) {
   // UMMA shared-memory descriptor, K-major, SWIZZLE_NONE (cute::UMMA::SmemDescriptor):
   // [0,14) addr>>4, [16,30) LBO>>4, [32,46) SBO>>4, [46,48) version=1, [61,64) layout=0
   return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)((LBO >> 4) & 0x3FFFu) << 16) |
-         ((uint64_t)((SBO >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
 }
 __device__ __forceinline__ uint32_t instr_desc(int n) {
   // kind::tf32, D f32 ([4,6)=1), A/B TF32 ([7,10)=2, [10,13)=2), K-major A/B,
   // N>>3 at [17,23), M>>4 at [24,29)
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
+// Issued by the whole (converged) MMA warp; elect.sync lets exactly one lane issue.
 __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
                                          uint32_t accumulate) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\t"
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
       : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-               : "memory");
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
+      : "memory");
 }
 __device__ __forceinline__ float exp2f_approx(float x) {  // MUFU.EX2, ~2 ulp
   float r;
@@ -138,10 +147,18 @@ __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t* r) {
 
 // per-role cycle counters (diagnostics, env GPMPPI_TC_DEBUG bit 512)
 __device__ unsigned long long g_prof[16];
+__device__ unsigned long long g_trace[64];  // CTA 0 timeline (dbg 4096)
+__device__ __forceinline__ void trace_at(int i, int dbg) {
+  if ((dbg & 4096) && blockIdx.x == 0 && i < 64) g_trace[i] = clock64();
+}
 __device__ __forceinline__ void prof_add(int slot, unsigned long long v, int dbg) {
   if (dbg & 512) atomicAdd(&g_prof[slot], v);
 }
 __device__ __forceinline__ void mbar_wait_prof(uint32_t bar, uint32_t parity, int slot, int dbg) {
+  if (!(dbg & 512)) {
+    mbar_wait(bar, parity);
+    return;
+  }
   const unsigned long long t0 = clock64();
   while (!mbar_try_wait(bar, parity)) {
   }
@@ -159,7 +176,7 @@ __device__ __forceinline__ int pass_chunks(int p, int np, int n_pad) {
 // dbg (diagnostics only, env GPMPPI_TC_DEBUG): 1 = skip B copies, 2 = skip k* math,
 // 4 = skip MMAs, 8 = skip TMEM reads. Results are garbage when set.
 __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const VarianceArgs a, int one_pass, int dbg,
-                                                                  int SA) {
+                                                                  int SA, int SB) {
   using namespace tc;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const GroupDev& G = a.g;
@@ -168,18 +185,21 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
   // (a size_t round trip turns every access into a generic LD/ST).
   unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* sA = reinterpret_cast<float*>(base);                  // [SA][2][M*KC]
-  float* sB = sA + SA * 2 * A_STAGE_FLOATS;              // [SB][2][NP*KC]
-  float* zs = sB + (size_t)STAGES_B * 2 * NP * KC;             // [5][n_pad] log2e-scaled aug. inputs
+  float* sB = sA + SA * 2 * A_STAGE_FLOATS;              // [SB][2][NP*KB]
+  float* zs = sB + (size_t)SB * 2 * NP * KB;                   // [5][n_pad] log2e-scaled aug. inputs
   uint64_t* bars = reinterpret_cast<uint64_t*>(zs + 5 * n_pad);
   uint64_t* full_a = bars;
   uint64_t* empty_a = full_a + SA;
   uint64_t* full_b = empty_a + SA;
-  uint64_t* empty_b = full_b + STAGES_B;
-  uint64_t* tfull = empty_b + STAGES_B;
+  uint64_t* empty_b = full_b + SB;
+  uint64_t* tfull = empty_b + SB;
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) trace_at(0, dbg);
+  // warp index through a shuffle: the compiler then knows every role branch is
+  // warp-uniform and keeps the MMA warp's descriptors in uniform registers
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int n_tiles = (int)((a.KT + M - 1) / M);
   const uint32_t tmem_cols = NP <= 32 ? 32 : NP <= 64 ? 64 : NP <= 128 ? 128 : NP <= 256 ? 256 : 512;
 
@@ -201,7 +221,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
       mbar_init(smem_u32(&full_a[s]), PRODUCER_WARPS);
       mbar_init(smem_u32(&empty_a[s]), 1);
     }
-    for (int s = 0; s < STAGES_B; ++s) {
+    for (int s = 0; s < SB; ++s) {
       mbar_init(smem_u32(&full_b[s]), 1);
       mbar_init(smem_u32(&empty_b[s]), 1);
     }
@@ -218,76 +238,86 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
   tc_before();
   __syncthreads();
   tc_after();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
   const unsigned long long t_start = clock64();
+  if (threadIdx.x == 0) trace_at(1, dbg);
 
   if (warp == 0 && lane == 0) {
-    // ---------------- B producer: one bulk copy (hi + lo) per chunk
+    // ---------------- B producer: one bulk copy (hi + lo) per 8-point block. The
+    // block table is read one block ahead so no global load sits between the
+    // empty-slot wait and the copy issue.
+    int nbt = 0;  // blocks per tile (same sequence for every tile)
+    for (int p = 0; p < n_pass; ++p) nbt += 2 * pass_chunks(p, NP, n_pad);
     uint32_t it = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      int chunk0 = 0;
-      for (int p = 0; p < n_pass; ++p) {
-        const int nk = pass_chunks(p, NP, n_pad);
-        for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = it % STAGES_B;
-          const uint32_t ph = (it / STAGES_B) & 1;
+    int4 next = G.tc_meta[0];
+    int ti = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++ti) {
+      if (ti < 10) trace_at(48 + ti, dbg);
+      for (int kb = 0; kb < nbt; ++kb, ++it) {
+        {
+          const int s = it % SB;
+          const uint32_t ph = (it / SB) & 1;
+          const int4 meta = next;
+          next = G.tc_meta[kb + 1 < nbt ? kb + 1 : 0];
           if (!(dbg & 64)) mbar_wait_prof(smem_u32(&empty_b[s]), ph ^ 1, 0, dbg);
-          const int4 meta = G.tc_meta[chunk0 + kb];
-          const uint32_t bytes = (uint32_t)meta.y * KC * 4 * 2;
+          const uint32_t bytes = (uint32_t)meta.y * KB * 4 * 2;
           if (dbg & 1) {
             mbar_arrive(smem_u32(&full_b[s]));
           } else {
             mbar_arrive_tx(smem_u32(&full_b[s]), bytes);
-            bulk_g2s(smem_u32(sB + (size_t)s * 2 * NP * KC), G.tc_b + meta.x, bytes, smem_u32(&full_b[s]));
+            bulk_g2s(smem_u32(sB + (size_t)s * 2 * NP * KB), G.tc_b + meta.x, bytes, smem_u32(&full_b[s]));
           }
         }
-        chunk0 += nk;
       }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer (single thread)
+  } else if (warp == 1) {
+    // ---------------- MMA issuer: the whole warp runs the loop (warp-uniform
+    // descriptors live in uniform registers) and elect.sync picks the lane that
+    // issues each tcgen05.mma / commit. A single-lane branch made every MMA a
+    // waterfall of R2UR broadcasts (~780 cycles per 8-point block).
     uint32_t ia = 0, ib = 0, uc = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      int chunk0 = 0;
       for (int p = 0; p < n_pass; ++p, ++uc) {
-        mbar_wait_prof(smem_u32(tempty), (uc & 1) ^ 1, 1, dbg);  // epilogue drained the accumulator
+        mbar_wait_prof(smem_u32(tempty), (uc & 1) ^ 1, 1, dbg & ~512);  // epilogue drained the accumulator
         tc_after();
+        if (lane == 0 && uc < 10) trace_at(2 + 2 * (int)uc, dbg);
         const int nk = pass_chunks(p, NP, n_pad);
-        for (int kb = 0; kb < nk; ++kb, ++ia, ++ib) {
-          const int sa = ia % SA, sb = ib % STAGES_B;
-          if (!(dbg & 16)) mbar_wait_prof(smem_u32(&full_a[sa]), (ia / SA) & 1, 2, dbg);
-          if (!(dbg & 32)) mbar_wait_prof(smem_u32(&full_b[sb]), (ib / STAGES_B) & 1, 3, dbg);
-          tc_after();
-          const unsigned long long tm0 = clock64();
-          const int4 meta = G.tc_meta[chunk0 + kb];
-          const int ncols = meta.y, col0 = meta.z;
+        const int npw = min(NP, n_pad - p * NP);
+        for (int kb = 0; kb < nk; ++kb, ++ia) {
+          const int sa = ia % SA;
+          if (!(dbg & 16)) mbar_wait(smem_u32(&full_a[sa]), (ia / SA) & 1);
           const uint32_t a_hi = smem_u32(sA + (size_t)sa * 2 * A_STAGE_FLOATS);
           const uint32_t a_lo = a_hi + A_STAGE_FLOATS * 4;
-          const uint32_t b_hi = smem_u32(sB + (size_t)sb * 2 * NP * KC);
-          const uint32_t b_lo = b_hi + (uint32_t)ncols * KC * 4;
+          const int col0 = max(0, kb * KC - p * NP);  // build_tc_operand's column start
+          const int ncols = npw - col0;
 #pragma unroll
-          for (int kk = 0; kk < KC / 8; ++kk) {
-            for (int c = 0; c < ncols; c += 256) {
-              const int nn = min(256, ncols - c);
-              const uint32_t idesc = instr_desc(nn);
-              const uint32_t d = tmem_base + (uint32_t)(col0 + c);
-              const uint32_t aoff = kk * 256;                        // two 16-byte K chunks per K=8 step
-              const uint32_t boff = (uint32_t)(c / 8) * SBO + kk * 256;
-              const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
-              if (dbg & 4) continue;
-              mma_tf32(d, smem_desc(a_hi + aoff), smem_desc(b_hi + boff), idesc, acc0);
-              if (!one_pass) {
-                mma_tf32(d, smem_desc(a_hi + aoff), smem_desc(b_lo + boff), idesc, 1u);
-                mma_tf32(d, smem_desc(a_lo + aoff), smem_desc(b_hi + boff), idesc, 1u);
+          for (int kk = 0; kk < KC / KB; ++kk, ++ib) {  // one B block per K=8 step
+            const int sb = ib % SB;
+            if (!(dbg & 32)) mbar_wait(smem_u32(&full_b[sb]), (ib / SB) & 1);
+            // no tcgen05 fence here: the MMAs read smem through the async proxy, which
+            // the bulk-copy completion and the producers' fence.proxy.async order
+            const uint32_t b_hi = smem_u32(sB + (size_t)sb * 2 * NP * KB);
+            const uint32_t b_lo = b_hi + (uint32_t)ncols * KB * 4;
+            const uint32_t aoff = kk * 256;  // two 16-byte K chunks per K=8 step
+            const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
+            if (!(dbg & 4)) {
+              for (int c = 0; c < ncols; c += 256) {
+                const uint32_t idesc = instr_desc(min(256, ncols - c));
+                const uint32_t d = tmem_base + (uint32_t)(col0 + c);
+                const uint32_t boff = (uint32_t)(c / 8) * SBO_B;
+                mma_tf32(d, smem_desc(a_hi + aoff), smem_desc(b_hi + boff, SBO_B), idesc, acc0);
+                if (!one_pass) {
+                  mma_tf32(d, smem_desc(a_hi + aoff), smem_desc(b_lo + boff, SBO_B), idesc, 1u);
+                  mma_tf32(d, smem_desc(a_lo + aoff), smem_desc(b_hi + boff, SBO_B), idesc, 1u);
+                }
               }
             }
+            mma_commit(smem_u32(&empty_b[sb]));  // B block free once these MMAs complete
           }
-          mma_commit(smem_u32(&empty_a[sa]));  // stages free once these MMAs complete
-          mma_commit(smem_u32(&empty_b[sb]));
-          prof_add(13, clock64() - tm0, dbg);
+          mma_commit(smem_u32(&empty_a[sa]));
         }
         mma_commit(smem_u32(tfull));  // accumulator of this pass ready
-        chunk0 += nk;
+        if (lane == 0 && uc < 10) trace_at(3 + 2 * (int)uc, dbg);
       }
     }
   } else if (warp >= 8) {
@@ -297,7 +327,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
     const int m = (pw & 3) * 32 + lane;  // tile row == TMEM lane
     const int h = pw >> 2;
     uint32_t it = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    int ti = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++ti) {
+      if (pw == 0 && lane == 0 && ti < 10) trace_at(36 + ti, dbg);
       const long long q = (long long)tile * M + m;
       const bool valid = q < a.KT;
       float4 qv = valid ? a.queries[q] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -311,7 +343,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
           const uint32_t ph = (it / SA) & 1;
           if (lane == 0 && !(dbg & 64)) mbar_wait_prof(smem_u32(&empty_a[s]), ph ^ 1, 4, dbg);
           __syncwarp();
-          const unsigned long long tp0 = clock64();
+          const unsigned long long tp0 = (dbg & 512) ? clock64() : 0ull;
           float* ahi = sA + (size_t)s * 2 * A_STAGE_FLOATS;
           float* alo = ahi + A_STAGE_FLOATS;
           const int row_off = (m >> 3) * (SBO / 4) + (m & 7) * 4;
@@ -353,8 +385,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
       for (int p = 0; p < n_pass; ++p, ++uc) {
         const int npw = min(NP, n_pad - p * NP);
         if (lane == 0) mbar_wait_prof(smem_u32(tfull), uc & 1, 5, dbg);
+        if (lane == 0 && e == 0 && uc < 10) trace_at(24 + (int)uc, dbg);
         __syncwarp();
-        const unsigned long long te0 = clock64();
+        const unsigned long long te0 = (dbg & 512) ? clock64() : 0ull;
         tc_after();
         const uint32_t trow = tmem_base + ((uint32_t)(e * 32) << 16);
         int c = (dbg & 8) ? npw : 0;
@@ -392,6 +425,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
       }
     }
   }
+  if (lane == 0 && warp == 1) trace_at(60, dbg);
+  if (lane == 0 && warp == 4) trace_at(61, dbg);
+  if (lane == 0 && warp == 8) trace_at(62, dbg);
   if (lane == 0) {
     const int slot = warp == 0 ? 6 : warp == 1 ? 7 : warp >= 8 ? 8 : warp >= 4 ? 9 : 10;
     prof_add(slot, clock64() - t_start, dbg);
@@ -400,18 +436,25 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
   tc_before();
   __syncthreads();
   tc_after();
+  if (threadIdx.x == 0) trace_at(63, dbg);
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols)
                  : "memory");
 }
 
-size_t tc_smem_bytes(const GroupDev& g, int stages_a) {
+size_t tc_smem_bytes(const GroupDev& g, int stages_a, int stages_b) {
   size_t b = 1024;  // alignment slack
   b += sizeof(float) * (size_t)stages_a * 2 * tc::A_STAGE_FLOATS;
-  b += sizeof(float) * (size_t)tc::STAGES_B * 2 * g.tc_np * tc::KC;
+  b += sizeof(float) * (size_t)stages_b * 2 * g.tc_np * tc::KB;
   b += sizeof(float) * (size_t)5 * g.tc_npad;
-  b += sizeof(uint64_t) * (2 * stages_a + 2 * tc::STAGES_B + 2) + 16;
+  b += sizeof(uint64_t) * (2 * stages_a + 2 * stages_b + 2) + 16;
   return b;
+}
+
+void tc_trace_read(double* out) {
+  unsigned long long h[64];
+  cudaMemcpyFromSymbol(h, tc::g_trace, sizeof h);
+  for (int i = 0; i < 64; ++i) out[i] = (double)h[i];
 }
 
 void tc_profile_read(double* out) {
@@ -424,9 +467,17 @@ void tc_profile_read(double* out) {
 
 cudaError_t launch_tc_variance(const VarianceArgs& a, int one_pass, cudaStream_t st) {
   if (!a.g.tc_b || !a.g.tc_meta) return cudaErrorNotSupported;
-  int SA = tc::STAGES_A;
-  while (SA > 2 && tc_smem_bytes(a.g, SA) > 227 * 1024) --SA;
-  const size_t smem = tc_smem_bytes(a.g, SA);
+  constexpr size_t kSmemMax = 227 * 1024;
+  static int sb_env = -1;  // diagnostics: GPMPPI_TC_SB forces the B ring depth
+  if (sb_env < 0) {
+    const char* e = getenv("GPMPPI_TC_SB");
+    sb_env = e ? atoi(e) : 0;
+  }
+  int SA = tc::STAGES_A, SB = sb_env >= 2 ? sb_env : tc::STAGES_B + 1;
+  while (sb_env < 2 && SB > tc::STAGES_B && tc_smem_bytes(a.g, SA, SB) > kSmemMax) --SB;
+  while (SA > 2 && tc_smem_bytes(a.g, SA, SB) > kSmemMax) --SA;
+  while (SB > 2 && tc_smem_bytes(a.g, SA, SB) > kSmemMax) --SB;
+  const size_t smem = tc_smem_bytes(a.g, SA, SB);
   cudaError_t e = cudaFuncSetAttribute(variance_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
@@ -439,13 +490,14 @@ cudaError_t launch_tc_variance(const VarianceArgs& a, int one_pass, cudaStream_t
     const char* e = getenv("GPMPPI_TC_DEBUG");
     dbg = e ? atoi(e) : 0;
   }
-  variance_tc_kernel<<<grid, tc::THREADS, smem, st>>>(a, one_pass, dbg, SA);
+  variance_tc_kernel<<<grid, tc::THREADS, smem, st>>>(a, one_pass, dbg, SA, SB);
   count_launch();
   return cudaGetLastError();
 }
 
-// Host: L^{-T} (n×n FP64, row-major, upper) → per-(pass, chunk) TF32 hi/lo blocks
-// in the UMMA K-major canonical layout ((8,n),(4,KC/4)) with SBO=(KC/4)·128 B, LBO=128 B.
+// Host: L^{-T} (n×n FP64, row-major, upper) → per-(pass, 8-point block) TF32 hi/lo
+// blocks in the UMMA K-major canonical layout ((8,n),(4,KB/4)) with SBO=(KB/4)·128 B,
+// LBO=128 B. Columns start at the 16-point chunk's diagonal (N multiple of 16).
 void build_tc_operand(const double* ilt, int n, std::vector<float>& data, std::vector<int4>& meta,
                       int& n_pad, int& np, int& n_pass) {
   const int KC = tc::KC;
@@ -468,21 +520,22 @@ void build_tc_operand(const double* ilt, int n, std::vector<float>& data, std::v
   for (int p = 0; p < n_pass; ++p) {
     const int npw = std::min(np, n_pad - p * np);
     const int nk = std::min(n_pad, (p + 1) * np) / KC;
-    for (int kb = 0; kb < nk; ++kb) {
-      const int col0 = std::max(0, kb * KC - p * np);
+    for (int kb = 0; kb < 2 * nk; ++kb) {
+      const int KB = tc::KB;
+      const int col0 = std::max(0, (kb / 2) * KC - p * np);
       const int ncols = npw - col0;
       const size_t off = data.size();
-      data.resize(off + (size_t)2 * ncols * KC, 0.f);
+      data.resize(off + (size_t)2 * ncols * KB, 0.f);
       float* hi = data.data() + off;
-      float* lo = hi + (size_t)ncols * KC;
+      float* lo = hi + (size_t)ncols * KB;
       for (int r = 0; r < ncols; ++r) {
         const int j = p * np + col0 + r;
-        for (int k = 0; k < KC; ++k) {
-          const int i = kb * KC + k;
+        for (int k = 0; k < KB; ++k) {
+          const int i = kb * KB + k;
           const double v = (i < n && j < n) ? ilt[(size_t)i * n + j] : 0.0;
           const float h = tf32((float)v);
           const float l = tf32((float)(v - (double)h));
-          const size_t o = (size_t)(r >> 3) * (KC / 4) * 32 + (size_t)(k >> 2) * 32 + (r & 7) * 4 + (k & 3);
+          const size_t o = (size_t)(r >> 3) * (KB / 4) * 32 + (size_t)(k >> 2) * 32 + (r & 7) * 4 + (k & 3);
           hi[o] = h;
           lo[o] = l;
         }

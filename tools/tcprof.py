@@ -12,8 +12,7 @@ from paper_2411_03289_b200 import workloads as W  # noqa: E402
 from bench import build_planner  # noqa: E402
 
 w = W.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "config2"]
-p, task = build_planner(w, G, var_path=1)
-x0 = np.array(w.x0)
+p, task, x0 = build_planner(w, G, var_path=1)
 p.bench_device(x0, task, 2)
 out = np.zeros(16)
 A.lib().gpmppi_debug_tc_profile(A.dptr(out))
