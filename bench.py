@@ -107,6 +107,17 @@ def roofline_block(w, phase, steps, peaks, peaks_kind):
     """
     n = w.n_points
     units = w.sample_steps
+    if n == 0:  # GP-free model (config 1): one wave of thread-per-sample rollouts
+        ms = phase[0] / steps
+        words = (w.horizon + 31) // 32
+        byts = w.robots * w.samples * (8 + 2 + 8 * words)  # costs, alive/terminal, flag words
+        achieved = byts / (ms / 1e3) / 1e9
+        peak = peaks.get("hbm_gbs", 6650.0)
+        return {"bound": "hbm", "kernel": "rollout_base_kernel", "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                "peak_kind": f"{peaks_kind} HBM copy (MEASURED_PEAKS.json)", "bytes_per_launch": byts,
+                "launch_ms": ms, "phase_share": ms / (sum(phase) / steps),
+                "note": "latency-bound: K=1024 samples are one wave of 40 serial FP64 steps"}
     roll_ms, var_ms = phase[0] / steps, phase[1] / steps
     if var_ms >= roll_ms:
         kern, ms, flop = "variance_tc_kernel", var_ms, units * (n * n + 3 * n)

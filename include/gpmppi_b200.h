@@ -249,6 +249,23 @@ int gpmppi_planner_plan_finish(gpmppi_planner* p, const void* device_tuples, int
 int gpmppi_combine_tuples_host(const double* tuples, int n_ranks, int horizon, double lambda,
                                double* out);
 
+/* ---- reference free functions (mppi.hpp:60-79), computed on `device` ----
+ * Host buffers in and out; each call synchronises. */
+/* rollout (mppi.cpp:80-111): mean-only rollout of one sequence seq[T][2];
+ * states[(T+1)][5], corrections[T][4] = (mean_v, mean_w, var_v, var_w) (GaussianCorrection) */
+int gpmppi_rollout(const gpmppi_prediction_model* model, const gpmppi_nominal* nominal,
+                   const double* terrain_weights, int R, const double x0[5], const double* seq, int T,
+                   int device, double* states, double* corrections);
+/* sample_perturbations (mppi.cpp:113-123) with the production Philox sampler: eps[K][T][2] */
+int gpmppi_sample_perturbations(const gpmppi_mppi_config* cfg, uint64_t tick, int device, double* eps);
+/* trajectory_weights (mppi.cpp:125-145) */
+int gpmppi_trajectory_weights(const double* costs, int64_t K, double lambda, int device, double* w);
+/* update_controls (mppi.cpp:147-164): nominal[T][2], eps[K][T][2], w[K] -> out[T][2] */
+int gpmppi_update_controls(const double* nominal, int T, const double* eps, const double* w, int64_t K,
+                           const double lo[2], const double hi[2], int device, double* out);
+/* shift_horizon (mppi.cpp:166-173) */
+int gpmppi_shift_horizon(const double* seq, int T, int device, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -548,6 +548,52 @@ int orc_ensemble_combine(const double* means, const double* vars, const double* 
   return ORC_OK;
 }
 
+/* mppi.cpp:80-111 rollout(): mean-only rollout of one control sequence. GP ensemble:
+ * predict at (v, w, u) -> combine_terrains -> step_nominal + mean correction;
+ * baselines: baseline_step (mppi.cpp:23-29); NOMINAL (repo extension): step_nominal.
+ * states (T+1)x5, corr Tx4 = (mean_v, mean_w, var_v, var_w). */
+int orc_rollout(int kind, const orc_gp* gp, int R, const double* w, const orc_nominal* nom,
+                const orc_edd5* edd, double track_width, const double x0[5], const double* seq,
+                int T, double* states, double* corr) {
+  if (kind == ORC_MODEL_GP) {
+    if (!gp || R < 1 || gp->m != 2 * R) return fail(ORC_INVALID_ARGUMENT, "rollout: bad GP ensemble");
+    if (!on_simplex(w, R, 1e-6))
+      return fail(ORC_INVALID_ARGUMENT, "rollout: terrain weights must lie on the simplex");
+  }
+  for (int i = 0; i < 5; ++i) states[i] = x0[i];
+  double* mean = kind == ORC_MODEL_GP ? (double*)malloc(sizeof(double) * gp->m) : NULL;
+  double* var = kind == ORC_MODEL_GP ? (double*)malloc(sizeof(double) * gp->m) : NULL;
+  double* ws = kind == ORC_MODEL_GP ? (double*)malloc(sizeof(double) * 2 * (size_t)gp->n) : NULL;
+  for (int k = 0; k < T; ++k) {
+    const double* s = states + 5 * k;
+    double* nx = states + 5 * (k + 1);
+    const double* u = seq + 2 * k;
+    double cm[2] = {0.0, 0.0}, cv[2] = {0.0, 0.0};
+    if (kind == ORC_MODEL_GP) {
+      const double q[4] = {s[3], s[4], u[0], u[1]};
+      predict_block(gp, q, 1, mean, var, ws);
+      combine(w, R, mean, var, cm, cv);
+      orc_step_nominal(s, u, nom, nx);
+      nx[3] += cm[0];
+      nx[4] += cm[1];
+    } else if (kind == ORC_MODEL_EDD5) {
+      orc_step_edd5(s, u, edd, track_width, nom->dt, nx);
+    } else if (kind == ORC_MODEL_UNICYCLE) {
+      orc_step_kinematic(s, u, nom->dt, nx);
+    } else {
+      orc_step_nominal(s, u, nom, nx);
+    }
+    corr[4 * k] = cm[0];
+    corr[4 * k + 1] = cm[1];
+    corr[4 * k + 2] = cv[0];
+    corr[4 * k + 3] = cv[1];
+  }
+  free(mean);
+  free(var);
+  free(ws);
+  return ORC_OK;
+}
+
 /* ======================= uncertainty.cpp ======================= */
 double orc_chi2_quantile_2dof(double p) { return -2.0 * log1p(-p); } /* :8-13 */
 double orc_normal_cdf(double x) { return 0.5 * erfc(-x * M_SQRT1_2); } /* :15 */

@@ -138,6 +138,10 @@ void orc_trajectory_weights(const double* costs, int K, double lambda, double* w
 void orc_update_controls(const double* nominal, const double* eps, const double* w, int K,
                          int T, const double lo[2], const double hi[2], double* out);
 void orc_shift_horizon(const double* seq, int T, double* out);
+/* mppi.cpp:80-111 rollout (mean-only, one sequence): states (T+1)x5, corr Tx4 */
+int orc_rollout(int kind, const orc_gp* gp, int R, const double* w, const orc_nominal* nom,
+                const orc_edd5* edd, double track_width, const double x0[5], const double* seq,
+                int T, double* states, double* corr);
 
 enum { ORC_MODEL_GP = 0, ORC_MODEL_EDD5 = 1, ORC_MODEL_UNICYCLE = 2, ORC_MODEL_NOMINAL = 3 };
 enum { ORC_TASK_TRACKING = 0, ORC_TASK_AVOIDANCE = 1, ORC_TASK_COMBINED = 2 };

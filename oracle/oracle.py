@@ -170,6 +170,8 @@ def lib(native: bool = False):
     L.orc_trajectory_weights.argtypes = [_dp, C.c_int, C.c_double, _dp]
     L.orc_update_controls.argtypes = [_dp, _dp, _dp, C.c_int, C.c_int, _dp, _dp, _dp]
     L.orc_shift_horizon.argtypes = [_dp, C.c_int, _dp]
+    L.orc_rollout.argtypes = [C.c_int, C.c_void_p, C.c_int, _dp, C.POINTER(Nominal), C.POINTER(Edd5),
+                              C.c_double, _dp, _dp, C.c_int, _dp, _dp]
     L.orc_planner_create.argtypes = [C.POINTER(MppiConfig), C.c_int, C.c_void_p, C.c_int,
                                      C.POINTER(Edd5), C.c_double, C.POINTER(Nominal), C.c_double,
                                      C.POINTER(C.c_void_p)]
@@ -210,6 +212,42 @@ def sample_perturbations(K, T, sigma_sim, seed, tick):
     eps = np.empty((K, T, 2))
     lib().orc_sample_perturbations(K, T, sigma_sim[0], sigma_sim[1], seed, tick, _ptr(eps))
     return eps
+
+
+def trajectory_weights(costs, lam):  # mppi.cpp:125-145
+    c = f64(costs)
+    w = np.empty_like(c)
+    lib().orc_trajectory_weights(_ptr(c), c.shape[0], lam, _ptr(w))
+    return w
+
+
+def update_controls(nominal, eps, w, lo=(-0.5, -2.0), hi=(2.0, 2.0)):  # mppi.cpp:147-164
+    nom, e, ww = f64(nominal), f64(eps), f64(w)
+    out = np.empty_like(nom)
+    lib().orc_update_controls(_ptr(nom), _ptr(e), _ptr(ww), e.shape[0], nom.shape[0],
+                              _ptr(f64(lo)), _ptr(f64(hi)), _ptr(out))
+    return out
+
+
+def shift_horizon(seq):  # mppi.cpp:166-173
+    s = f64(seq)
+    out = np.empty_like(s)
+    lib().orc_shift_horizon(_ptr(s), s.shape[0], _ptr(out))
+    return out
+
+
+def rollout(x0, seq, kind=ORC_MODEL_GP, gp=None, R=0, w=None, nominal=(0.5, 0.35, 0.05),
+            edd5=(1.0, 1.0, 0.0, -0.2, 0.2), track_width=0.4):
+    """mppi.cpp:80-111: (states (T+1)x5, corrections Tx4 = mean_v, mean_w, var_v, var_w)."""
+    sq = f64(seq).reshape(-1, 2)
+    T = sq.shape[0]
+    states = np.empty((T + 1, 5))
+    corr = np.empty((T, 4))
+    ww = f64(w if w is not None else np.full(max(R, 1), 1.0 / max(R, 1)))
+    _check(lib().orc_rollout(kind, gp.h if gp is not None else None, R, _ptr(ww), Nominal(*nominal),
+                             Edd5(*edd5), track_width, _ptr(f64(x0)), _ptr(sq), T, _ptr(states),
+                             _ptr(corr)))
+    return states, corr
 
 
 class GP:

@@ -136,6 +136,12 @@ SIGNATURES = [
     ("gpmppi_planner_plan_partial", C.c_int, [_vp, _dp, C.POINTER(TaskC), _vp]),
     ("gpmppi_planner_plan_finish", C.c_int, [_vp, _vp, C.c_int, _dp, C.POINTER(DiagC)]),
     ("gpmppi_combine_tuples_host", C.c_int, [_dp, C.c_int, C.c_int, C.c_double, _dp]),
+    ("gpmppi_rollout", C.c_int, [C.POINTER(PredictionModelC), C.POINTER(NominalC), _dp, C.c_int, _dp, _dp,
+                                 C.c_int, C.c_int, _dp, _dp]),
+    ("gpmppi_sample_perturbations", C.c_int, [C.POINTER(MppiConfigC), C.c_uint64, C.c_int, _dp]),
+    ("gpmppi_trajectory_weights", C.c_int, [_dp, C.c_int64, C.c_double, C.c_int, _dp]),
+    ("gpmppi_update_controls", C.c_int, [_dp, C.c_int, _dp, _dp, C.c_int64, _dp, _dp, C.c_int, _dp]),
+    ("gpmppi_shift_horizon", C.c_int, [_dp, C.c_int, C.c_int, _dp]),
 ]
 
 

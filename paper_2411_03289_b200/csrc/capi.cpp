@@ -1358,6 +1358,123 @@ int gpmppi_planner_plan_finish(gpmppi_planner* p, const void* device_tuples, int
   });
 }
 
+// ---- reference free functions (mppi.hpp:60-79) on the device ----
+}  // extern "C"
+namespace {
+struct DevBuf {  // scoped device allocation for the one-shot free functions
+  void* p = nullptr;
+  explicit DevBuf(size_t bytes) { CK(cudaMalloc(&p, std::max<size_t>(bytes, 8))); }
+  ~DevBuf() { cudaFree(p); }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+void h2d(void* d, const void* h, size_t bytes) { CK(cudaMemcpy(d, h, bytes, cudaMemcpyHostToDevice)); }
+void d2h(void* h, const void* d, size_t bytes) { CK(cudaMemcpy(h, d, bytes, cudaMemcpyDeviceToHost)); }
+}  // namespace
+extern "C" {
+
+int gpmppi_rollout(const gpmppi_prediction_model* pm, const gpmppi_nominal* nominal,
+                   const double* terrain_weights, int R, const double x0[5], const double* seq, int T,
+                   int device, double* states, double* corrections) {
+  return guarded([&] {  // mppi.cpp:80-111
+    if (!pm || !nominal || !x0 || !seq || !states || !corrections) invalid("rollout: null argument");
+    if (T < 0) invalid("rollout: negative horizon");
+    if (pm->kind < 0 || pm->kind > 3) invalid("rollout: unknown prediction model");
+    const bool gp = pm->kind == GPMPPI_MODEL_GP_ENSEMBLE;
+    if (gp) {
+      if (!pm->gp || pm->n_terrains < 1 || pm->gp->m != 2 * pm->n_terrains || R != pm->n_terrains)
+        invalid("rollout: GP ensemble needs a model with 2M outputs and M weights");
+      if (!terrain_weights || !on_simplex(terrain_weights, R, 1e-6))
+        invalid("rollout: terrain weights must lie on the simplex");
+      if (pm->gp->device != device) invalid("rollout: GP model lives on another device");
+    }
+    require_device(device);
+    for (int i = 0; i < 5; ++i) states[i] = x0[i];
+    if (T == 0) return;
+    DevBuf dx(sizeof(double) * 5), ds(sizeof(double) * 2 * T), dw(sizeof(double) * std::max(R, 1)),
+        dst(sizeof(double) * 5 * (T + 1)), dc(sizeof(double) * 4 * T);
+    h2d(dx.p, x0, sizeof(double) * 5);
+    h2d(ds.p, seq, sizeof(double) * 2 * T);
+    if (gp) h2d(dw.p, terrain_weights, sizeof(double) * R);
+    const gpm::NominalDev nom{nominal->tau_v, nominal->tau_omega, nominal->dt};
+    const gpm::Edd5Dev edd{pm->edd5.alpha_l, pm->edd5.alpha_r, pm->edd5.x_icr, pm->edd5.y_icr_l,
+                           pm->edd5.y_icr_r, pm->track_width};
+    gpm::ModelDev M{};
+    if (gp) M = pm->gp->dev;
+    check(gpm::launch_rollout_one(M, pm->kind, nom, edd, dx.as<double>(), ds.as<double>(), T, dw.as<double>(),
+                                  gp ? R : 0, dst.as<double>(), dc.as<double>(), 0),
+          "rollout_one_kernel");
+    CK(cudaDeviceSynchronize());
+    d2h(states, dst.p, sizeof(double) * 5 * (T + 1));
+    d2h(corrections, dc.p, sizeof(double) * 4 * T);
+  });
+}
+
+int gpmppi_sample_perturbations(const gpmppi_mppi_config* cfg, uint64_t tick, int device, double* eps) {
+  return guarded([&] {  // mppi.cpp:113-123 with the production (Philox) sampler
+    if (!cfg || !eps) invalid("sample_perturbations: null argument");
+    if (cfg->samples < 1 || cfg->horizon < 1) invalid("MppiConfig: samples and horizon must be >= 1");
+    if (!(cfg->sigma_v2 > 0.0) || !(cfg->sigma_w2 > 0.0)) invalid("MppiConfig: sampling variances must be positive");
+    require_device(device);
+    const size_t cnt = (size_t)cfg->samples * cfg->horizon * 2;
+    DevBuf d(sizeof(double) * cnt);
+    check(gpm::launch_philox_noise(gpm::philox_key(cfg->seed, tick), 0, cfg->samples, cfg->horizon,
+                                   std::sqrt(cfg->sigma_v2), std::sqrt(cfg->sigma_w2), d.as<double>(), 0),
+          "philox_noise_kernel");
+    CK(cudaDeviceSynchronize());
+    d2h(eps, d.p, sizeof(double) * cnt);
+  });
+}
+
+int gpmppi_trajectory_weights(const double* costs, int64_t K, double lambda, int device, double* w) {
+  return guarded([&] {  // mppi.cpp:125-145
+    if (!(lambda > 0.0)) invalid("trajectory_weights: lambda must be positive");
+    if (K < 0 || (K > 0 && (!costs || !w))) invalid("trajectory_weights: bad arguments");
+    if (K == 0) return;
+    require_device(device);
+    DevBuf dc(sizeof(double) * K), dw(sizeof(double) * K);
+    h2d(dc.p, costs, sizeof(double) * K);
+    check(gpm::launch_trajectory_weights(dc.as<double>(), K, lambda, dw.as<double>(), 0), "trajectory_weights_kernel");
+    CK(cudaDeviceSynchronize());
+    d2h(w, dw.p, sizeof(double) * K);
+  });
+}
+
+int gpmppi_update_controls(const double* nominal, int T, const double* eps, const double* w, int64_t K,
+                           const double lo[2], const double hi[2], int device, double* out) {
+  return guarded([&] {  // mppi.cpp:147-164
+    if (!nominal || !eps || !w || !lo || !hi || !out || T < 0 || K < 0)
+      invalid("update_controls: one weight per sample required");
+    if (T == 0) return;
+    require_device(device);
+    DevBuf dn(sizeof(double) * 2 * T), de(sizeof(double) * 2 * T * std::max<int64_t>(K, 1)),
+        dw(sizeof(double) * std::max<int64_t>(K, 1)), dout(sizeof(double) * 2 * T);
+    h2d(dn.p, nominal, sizeof(double) * 2 * T);
+    if (K > 0) {
+      h2d(de.p, eps, sizeof(double) * 2 * T * K);
+      h2d(dw.p, w, sizeof(double) * K);
+    }
+    check(gpm::launch_update_controls(dn.as<double>(), T, de.as<double>(), dw.as<double>(), K, lo, hi,
+                                      dout.as<double>(), 0),
+          "update_controls_kernel");
+    CK(cudaDeviceSynchronize());
+    d2h(out, dout.p, sizeof(double) * 2 * T);
+  });
+}
+
+int gpmppi_shift_horizon(const double* seq, int T, int device, double* out) {
+  return guarded([&] {  // mppi.cpp:166-173
+    if (T < 1) invalid("shift_horizon: empty sequence");
+    if (!seq || !out) invalid("shift_horizon: null argument");
+    require_device(device);
+    DevBuf ds(sizeof(double) * 2 * T), dout(sizeof(double) * 2 * T);
+    h2d(ds.p, seq, sizeof(double) * 2 * T);
+    check(gpm::launch_shift_horizon(ds.as<double>(), T, dout.as<double>(), 0), "shift_horizon_kernel");
+    CK(cudaDeviceSynchronize());
+    d2h(out, dout.p, sizeof(double) * 2 * T);
+  });
+}
+
 int gpmppi_combine_tuples_host(const double* tuples, int n_ranks, int horizon, double lambda,
                                double* out) {
   if (!tuples || !out || n_ranks < 1 || horizon < 1 || !(lambda > 0.0))

@@ -153,6 +153,14 @@ int rollout_samples_per_block(int K_local, int num_sms, int* lps, int* threads);
 cudaError_t launch_tighten(const TightenArgs& a, cudaStream_t st);
 cudaError_t launch_predict(const ModelDev& m, const double* q, long long S, double* mean,
                            double* var, cudaStream_t st);
+// reference free functions (mppi.hpp:60-79)
+cudaError_t launch_rollout_one(const ModelDev& M, int model_kind, const NominalDev& nom, const Edd5Dev& edd,
+                               const double* x0, const double* seq, int T, const double* w, int R,
+                               double* states, double* corr, cudaStream_t st);
+cudaError_t launch_trajectory_weights(const double* c, long long K, double lambda, double* w, cudaStream_t st);
+cudaError_t launch_update_controls(const double* nom, int T, const double* eps, const double* w, long long K,
+                                   const double lo[2], const double hi[2], double* out, cudaStream_t st);
+cudaError_t launch_shift_horizon(const double* seq, int T, double* out, cudaStream_t st);
 cudaError_t launch_philox_noise(uint64_t key, long long s_begin, int K, int T, double sv,
                                 double sw, double* eps, cudaStream_t st);
 size_t rollout_smem_bytes(const RolloutArgs& a);

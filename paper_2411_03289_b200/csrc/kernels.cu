@@ -501,6 +501,8 @@ cudaError_t launch_rollout(const RolloutArgs& a, int num_sms, cudaStream_t st) {
     int lps = 8, threads = 32;
     const int spb = rollout_samples_per_block(a.K_local, num_sms, &lps, &threads);
     const long long items = (long long)a.B * ((a.K_local + spb - 1) / spb);
+    // one block per SM: capping registers for a second resident block (122 instead of
+    // ~200) costs more ILP than the extra warps recover (config2 0.34 -> 0.52 ms)
     const long long blocks = items < num_sms ? items : num_sms;
     using KF = void (*)(const RolloutArgs);
     KF table[4][4] = {
@@ -1341,6 +1343,153 @@ cudaError_t launch_tighten(const TightenArgs& a, cudaStream_t st) {
 }
 
 // -------------------------------------------------------------------------
+// -------------------------------------------------------------------------
+// Reference free functions (mppi.hpp:60-79) as device kernels behind the C ABI.
+
+// mppi.cpp:80-111 rollout(): one block walks the T steps; the GP query of each
+// step is the block-wide FP64 predict used by the tightening pass.
+__global__ void __launch_bounds__(256) rollout_one_kernel(const ModelDev M, int model_kind, NominalDev nom,
+                                                          Edd5Dev edd, const double* x0, const double* seq,
+                                                          int T, const double* w, int R, double* states,
+                                                          double* corr) {
+  extern __shared__ __align__(16) double kst[];
+  __shared__ double red[32 * 8];
+  __shared__ double smean[kMaxGroups * kMaxOutPerGroup];
+  __shared__ double svar[kMaxGroups];
+  __shared__ double st[5];
+  if (threadIdx.x < 5) {
+    st[threadIdx.x] = x0[threadIdx.x];
+    states[threadIdx.x] = x0[threadIdx.x];
+  }
+  __syncthreads();
+  for (int k = 0; k < T; ++k) {
+    const double u[2] = {seq[2 * k], seq[2 * k + 1]};
+    if (model_kind == MODEL_GP) {
+      const double q[4] = {st[3], st[4], u[0], u[1]};
+      block_gp_predict(M, q, kst, red, smean, svar);
+    }
+    if (threadIdx.x == 0) {
+      double s5[5], nx[5];
+      for (int i = 0; i < 5; ++i) s5[i] = st[i];
+      double cm0 = 0.0, cm1 = 0.0, vv = 0.0, vw = 0.0;
+      if (model_kind == MODEL_GP) {
+        double vout[kMaxGroups * kMaxOutPerGroup];
+        for (int g = 0; g < M.G; ++g)
+          for (int o = 0; o < M.g[g].n_out; ++o) vout[M.g[g].out_idx[o]] = svar[g];
+        for (int i = 0; i < R; ++i) {  // combine_terrains, ascending i (mppi.cpp:34-49)
+          const double wi = w[i];
+          cm0 += wi * smean[2 * i];
+          cm1 += wi * smean[2 * i + 1];
+          vv += wi * wi * vout[2 * i];
+          vw += wi * wi * vout[2 * i + 1];
+        }
+        double sp, cp;
+        sincos(s5[2], &sp, &cp);
+        step_nominal(s5, u, nom, nx, sp, cp);
+        nx[3] += cm0;
+        nx[4] += cm1;
+      } else if (model_kind == MODEL_EDD5) {
+        step_edd5(s5, u, edd, nom.dt, nx);
+      } else if (model_kind == MODEL_UNICYCLE) {
+        step_kinematic(s5, u, nom.dt, nx);
+      } else {
+        double sp, cp;
+        sincos(s5[2], &sp, &cp);
+        step_nominal(s5, u, nom, nx, sp, cp);
+      }
+      for (int i = 0; i < 5; ++i) {
+        st[i] = nx[i];
+        states[5 * (k + 1) + i] = nx[i];
+      }
+      corr[4 * k] = cm0;
+      corr[4 * k + 1] = cm1;
+      corr[4 * k + 2] = vv;
+      corr[4 * k + 3] = vw;
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_rollout_one(const ModelDev& M, int model_kind, const NominalDev& nom, const Edd5Dev& edd,
+                               const double* x0, const double* seq, int T, const double* w, int R,
+                               double* states, double* corr, cudaStream_t st) {
+  const size_t smem = sizeof(double) * (size_t)(model_kind == MODEL_GP ? M.n : 1);
+  cudaError_t e = cudaFuncSetAttribute(rollout_one_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  rollout_one_kernel<<<1, 256, smem, st>>>(M, model_kind, nom, edd, x0, seq, T, w, R, states, corr);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// mppi.cpp:125-145 trajectory_weights: one block (block min, exp, sum, scale).
+__global__ void __launch_bounds__(1024) trajectory_weights_kernel(const double* c, long long K, double lambda,
+                                                                  double* w) {
+  __shared__ double red[32 * 5];
+  double lmin = INFINITY;
+  for (long long i = threadIdx.x; i < K; i += blockDim.x)
+    if (isfinite(c[i])) lmin = fmin(lmin, c[i]);
+  lmin = warp_min(lmin);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = lmin;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = INFINITY;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) m = fmin(m, red[i]);
+    red[31 * 5] = m;
+  }
+  __syncthreads();
+  const double m = red[31 * 5];
+  __syncthreads();
+  if (!isfinite(m)) {  // no valid sample this tick: all zeros
+    for (long long i = threadIdx.x; i < K; i += blockDim.x) w[i] = 0.0;
+    return;
+  }
+  double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (long long i = threadIdx.x; i < K; i += blockDim.x) {
+    const double e = isfinite(c[i]) ? exp(-(c[i] - m) / lambda) : 0.0;
+    w[i] = e;
+    v[0] += e;
+  }
+  block_reduce_5(v, red);
+  const double Z = v[0];
+  for (long long i = threadIdx.x; i < K; i += blockDim.x) w[i] = w[i] / Z;
+}
+
+// mppi.cpp:147-164 update_controls: thread per (k, component), samples in index order.
+__global__ void update_controls_kernel(const double* nom, int T, const double* eps, const double* w, long long K,
+                                       double lo0, double lo1, double hi0, double hi1, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 2 * T) return;
+  const int k = i >> 1, c = i & 1;
+  double d = 0.0;
+  for (long long s = 0; s < K; ++s) d += w[s] * eps[((size_t)s * T + k) * 2 + c];
+  out[i] = clampd(nom[i] + d, c ? lo1 : lo0, c ? hi1 : hi0);
+}
+
+// mppi.cpp:166-173 shift_horizon
+__global__ void shift_horizon_kernel(const double* seq, int T, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 2 * T) return;
+  const int k = i >> 1;
+  out[i] = seq[2 * (k + 1 < T ? k + 1 : T - 1) + (i & 1)];
+}
+
+cudaError_t launch_trajectory_weights(const double* c, long long K, double lambda, double* w, cudaStream_t st) {
+  trajectory_weights_kernel<<<1, 1024, 0, st>>>(c, K, lambda, w);
+  count_launch();
+  return cudaGetLastError();
+}
+cudaError_t launch_update_controls(const double* nom, int T, const double* eps, const double* w, long long K,
+                                   const double lo[2], const double hi[2], double* out, cudaStream_t st) {
+  update_controls_kernel<<<(2 * T + 127) / 128, 128, 0, st>>>(nom, T, eps, w, K, lo[0], lo[1], hi[0], hi[1], out);
+  count_launch();
+  return cudaGetLastError();
+}
+cudaError_t launch_shift_horizon(const double* seq, int T, double* out, cudaStream_t st) {
+  shift_horizon_kernel<<<(2 * T + 127) / 128, 128, 0, st>>>(seq, T, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
 __global__ void philox_noise_kernel(uint64_t key, long long s_begin, int K, int T, double sv,
                                     double sw, double* eps) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;

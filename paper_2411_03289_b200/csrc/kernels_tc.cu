@@ -108,6 +108,39 @@ __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// All MMAs of one 8-point B block in one statement (one elect, shared operand
+// moves): 3xTF32 = A_hi·B_hi + A_hi·B_lo + A_lo·B_hi over one or two 256-column
+// pieces (the second piece's descriptors sit 512 16-byte units further on).
+__device__ __forceinline__ void mma_block_3x(uint32_t d, uint64_t ahi, uint64_t alo, uint64_t bhi, uint64_t blo,
+                                             uint32_t idesc0, uint32_t idesc1, uint32_t acc, int two) {
+  if (two) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b32 d1;\n\t.reg .b64 bh1, bl1;\n\t"
+        "add.u32 d1, %0, 256;\n\t"
+        "add.s64 bh1, %3, 512;\n\t"
+        "add.s64 bl1, %4, 512;\n\t"
+        "setp.ne.b32 p, %7, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %3, %5, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %4, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], %1, bh1, %6, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], %1, bl1, %6, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], %2, bh1, %6, 1;\n\t}" ::"r"(d),
+        "l"(ahi), "l"(alo), "l"(bhi), "l"(blo), "r"(idesc0), "r"(idesc1), "r"(acc)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %3, %5, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %4, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %5, 1;\n\t}" ::"r"(d),
+        "l"(ahi), "l"(alo), "l"(bhi), "l"(blo), "r"(idesc0), "r"(acc)
+        : "memory");
+  }
+}
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
@@ -301,15 +334,15 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
             const uint32_t aoff = kk * 256;  // two 16-byte K chunks per K=8 step
             const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
             if (!(dbg & 4)) {
-              for (int c = 0; c < ncols; c += 256) {
-                const uint32_t idesc = instr_desc(min(256, ncols - c));
-                const uint32_t d = tmem_base + (uint32_t)(col0 + c);
-                const uint32_t boff = (uint32_t)(c / 8) * SBO_B;
-                mma_tf32(d, smem_desc(a_hi + aoff), smem_desc(b_hi + boff, SBO_B), idesc, acc0);
-                if (!one_pass) {
-                  mma_tf32(d, smem_desc(a_hi + aoff), smem_desc(b_lo + boff, SBO_B), idesc, 1u);
-                  mma_tf32(d, smem_desc(a_lo + aoff), smem_desc(b_hi + boff, SBO_B), idesc, 1u);
-                }
+              const uint32_t d = tmem_base + (uint32_t)col0;
+              if (!one_pass) {
+                mma_block_3x(d, smem_desc(a_hi + aoff), smem_desc(a_lo + aoff), smem_desc(b_hi, SBO_B),
+                             smem_desc(b_lo, SBO_B), instr_desc(min(256, ncols)),
+                             instr_desc(ncols > 256 ? ncols - 256 : 16), acc0, ncols > 256);
+              } else {
+                for (int c = 0; c < ncols; c += 256)
+                  mma_tf32(d + c, smem_desc(a_hi + aoff), smem_desc(b_hi + (uint32_t)(c / 8) * SBO_B, SBO_B),
+                           instr_desc(min(256, ncols - c)), acc0);
               }
             }
             mma_commit(smem_u32(&empty_b[sb]));  // B block free once these MMAs complete

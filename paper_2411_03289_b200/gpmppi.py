@@ -661,6 +661,69 @@ class BatchPlanner(Planner):
         raise ValueError("BatchPlanner: batched planners shard by robot, not by sample")
 
 
+# ----------------------------------------------------------------- free functions
+# Reference free functions (mppi.hpp:60-79), computed on the device.
+@dataclass
+class RolloutResult:  # mppi.hpp:53-56
+    states: np.ndarray       # (T+1) x 5
+    corrections: np.ndarray  # T x 4: mean_v, mean_w, var_v (cov 0,0), var_w (cov 1,1)
+
+
+def rollout(x0, seq, model, weights=None, nominal: NominalParams = None, device: int = 0) -> RolloutResult:
+    """Mean-only rollout of one control sequence (mppi.cpp:80-111)."""
+    nominal = nominal or NominalParams()
+    x = _f64(x0, (5,))
+    sq = _f64(seq, (-1, 2))
+    T = sq.shape[0]
+    R = model.n_terrains if isinstance(model, GpEnsemble) else 0
+    w = _f64(weights if weights is not None else np.full(max(R, 1), 1.0 / max(R, 1)), (-1,))
+    states, corr = np.empty((T + 1, 5)), np.empty((T, 4))
+    pm = _model_c(model)
+    nom = A.NominalC(nominal.tau_v, nominal.tau_omega, nominal.dt)
+    A.check(A.lib().gpmppi_rollout(C.byref(pm), C.byref(nom), A.dptr(w), w.shape[0] if R else 0,
+                                   A.dptr(x), A.dptr(sq), T, device, A.dptr(states), A.dptr(corr)))
+    return RolloutResult(states, corr)
+
+
+def sample_perturbations(cfg: MppiConfig, tick: int, device: int = 0):
+    """K x T x 2 Gaussian perturbations (mppi.cpp:113-123), Philox sampler keyed by (seed, tick, s)."""
+    c = cfg.to_c()
+    eps = np.empty((cfg.samples, cfg.horizon, 2))
+    A.check(A.lib().gpmppi_sample_perturbations(C.byref(c), tick, device, A.dptr(eps)))
+    return eps
+
+
+def trajectory_weights(costs, lam: float, device: int = 0):
+    """Softmax weights with a min-cost baseline (mppi.cpp:125-145)."""
+    c = _f64(costs, (-1,))
+    w = np.empty_like(c)
+    A.check(A.lib().gpmppi_trajectory_weights(A.dptr(c), c.shape[0], lam, device, A.dptr(w)))
+    return w
+
+
+def update_controls(nominal, eps, weights, bounds: ControlBounds = None, device: int = 0):
+    """Perturbation-weighted update, clamped (mppi.cpp:147-164)."""
+    bounds = bounds or ControlBounds()
+    nom = _f64(nominal, (-1, 2))
+    e = _f64(eps, (-1, nom.shape[0], 2))
+    w = _f64(weights, (-1,))
+    if e.shape[0] != w.shape[0]:
+        raise ValueError("update_controls: one weight per sample required")
+    out = np.empty_like(nom)
+    lo, hi = _f64(bounds.lo), _f64(bounds.hi)
+    A.check(A.lib().gpmppi_update_controls(A.dptr(nom), nom.shape[0], A.dptr(e), A.dptr(w), w.shape[0],
+                                           A.dptr(lo), A.dptr(hi), device, A.dptr(out)))
+    return out
+
+
+def shift_horizon(seq, device: int = 0):
+    """Drop the first control, repeat the last (mppi.cpp:166-173)."""
+    s = _f64(seq, (-1, 2))
+    out = np.empty_like(s)
+    A.check(A.lib().gpmppi_shift_horizon(A.dptr(s), s.shape[0], device, A.dptr(out)))
+    return out
+
+
 def shard_range(total: int, world: int, rank: int):
     """Contiguous global sample range of `rank`: [begin, begin+count)."""
     base, extra = divmod(total, world)

@@ -549,3 +549,22 @@ def test_zero_residual_planner_first_step_matches_scalar_path():  # test_mppi.cp
     p.plan_step(x0, task)
     assert np.isfinite(p.costs()).all()
     assert p.weights().sum() == pytest.approx(1.0, rel=1e-12)
+
+
+def test_zero_residual_rollout_equals_nominal():  # test_mppi.cpp:162-179
+    gp = zero_residual_gp(3)
+    r = np.random.default_rng(9)
+    seq = np.column_stack([r.uniform(0, 2, 10), r.uniform(-1, 1, 10)])
+    x0 = np.array([0.0, 0.0, 0.3, 1.0, 0.2])
+    states, corr = O.rollout(x0, seq, O.ORC_MODEL_GP, gp, 3, [1 / 3] * 3)
+    s = x0.copy()
+    for k in range(10):
+        nxt = np.empty(5)
+        O.lib().orc_step_nominal(P(s), P(f(seq[k])), O.Nominal(0.5, 0.35, 0.05), P(nxt))
+        s = nxt
+        assert abs(states[k + 1, 0] - s[0]) <= 1e-9 and abs(states[k + 1, 3] - s[3]) <= 1e-9
+        assert np.abs(corr[k, :2]).max() <= 1e-9
+    with pytest.raises(ValueError):
+        O.rollout(x0, seq, O.ORC_MODEL_GP, gp, 3, [0.5, 0.5, 0.5])
+    st_k, _ = O.rollout(x0, seq, O.ORC_MODEL_UNICYCLE)
+    assert st_k.shape == (11, 5) and np.isfinite(st_k).all()
