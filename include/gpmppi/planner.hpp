@@ -125,6 +125,11 @@ class GpModel {
     return p;
   }
   const gpmppi_model* handle() const { return h_; }
+  static GpModel adopt(gpmppi_model* h) {  // takes ownership of a C-ABI handle
+    GpModel g;
+    g.h_ = h;
+    return g;
+  }
 
  private:
   gpmppi_model* h_ = nullptr;
@@ -198,26 +203,33 @@ struct StepDiagnostics {  // mppi.hpp:81-89
   double command_ms{0.0};
 };
 
+namespace detail {
+inline gpmppi_prediction_model model_c(const PredictionModel& model) {
+  gpmppi_prediction_model pm{};
+  if (auto* g = std::get_if<GpEnsemble>(&model)) {
+    pm.kind = GPMPPI_MODEL_GP_ENSEMBLE;
+    pm.gp = g->model ? g->model->handle() : nullptr;
+    pm.n_terrains = g->n_terrains;
+  } else if (auto* e = std::get_if<Edd5Baseline>(&model)) {
+    pm.kind = GPMPPI_MODEL_EDD5;
+    pm.edd5 = {e->params.alpha_l, e->params.alpha_r, e->params.x_icr, e->params.y_icr_l, e->params.y_icr_r};
+    pm.track_width = e->track_width;
+  } else if (std::holds_alternative<UnicycleBaseline>(model)) {
+    pm.kind = GPMPPI_MODEL_UNICYCLE;
+  } else {
+    pm.kind = GPMPPI_MODEL_NOMINAL;
+  }
+  return pm;
+}
+}  // namespace detail
+
 // Planner (mppi.hpp:96-143)
 class Planner {
  public:
   Planner(const MppiConfig& cfg, PredictionModel model, NominalParams nominal, double p_x,
           int device = 0)
       : cfg_(cfg) {
-    gpmppi_prediction_model pm{};
-    if (auto* g = std::get_if<GpEnsemble>(&model)) {
-      pm.kind = GPMPPI_MODEL_GP_ENSEMBLE;
-      pm.gp = g->model ? g->model->handle() : nullptr;
-      pm.n_terrains = g->n_terrains;
-    } else if (auto* e = std::get_if<Edd5Baseline>(&model)) {
-      pm.kind = GPMPPI_MODEL_EDD5;
-      pm.edd5 = {e->params.alpha_l, e->params.alpha_r, e->params.x_icr, e->params.y_icr_l, e->params.y_icr_r};
-      pm.track_width = e->track_width;
-    } else if (std::holds_alternative<UnicycleBaseline>(model)) {
-      pm.kind = GPMPPI_MODEL_UNICYCLE;
-    } else {
-      pm.kind = GPMPPI_MODEL_NOMINAL;
-    }
+    const gpmppi_prediction_model pm = detail::model_c(model);
     const gpmppi_mppi_config c = cfg.c();
     const gpmppi_nominal nom{nominal.tau_v, nominal.tau_omega, nominal.dt};
     detail::check(gpmppi_planner_create(&c, &pm, &nom, p_x, device, &h_));
@@ -348,6 +360,219 @@ class Planner {
   static inline thread_local gpmppi_track track_c_{};
   static inline thread_local std::vector<double> wp_;
   static inline thread_local std::vector<double> obs_;
+};
+
+// ---- models file GPMPPIM1 (harness.hpp:41-53, harness.cpp:249-284) ----
+struct TrainedModels {
+  bool has_gp{false};
+  GpModel gp;
+  Edd5Params edd5{Edd5Params::ideal(0.37)};
+  NominalParams nominal;
+};
+inline TrainedModels load_models(const std::string& path, int device = 0) {
+  gpmppi_edd5 e{};
+  gpmppi_nominal n{};
+  gpmppi_model* h = nullptr;
+  detail::check(gpmppi_models_load(path.c_str(), device, &e, &n, &h));
+  TrainedModels m;
+  m.has_gp = h != nullptr;
+  m.gp = GpModel::adopt(h);
+  m.edd5 = {e.alpha_l, e.alpha_r, e.x_icr, e.y_icr_l, e.y_icr_r};
+  m.nominal = {n.tau_v, n.tau_omega, n.dt};
+  return m;
+}
+inline void save_models(const std::string& path, const TrainedModels& m) {
+  const gpmppi_edd5 e{m.edd5.alpha_l, m.edd5.alpha_r, m.edd5.x_icr, m.edd5.y_icr_l, m.edd5.y_icr_r};
+  const gpmppi_nominal n{m.nominal.tau_v, m.nominal.tau_omega, m.nominal.dt};
+  detail::check(gpmppi_models_save(path.c_str(), &e, &n, m.has_gp ? m.gp.handle() : nullptr));
+}
+
+// ---- free functions (mppi.hpp:60-79), computed on the device ----
+struct GaussianCorrection {  // core.hpp:89-94 (diagonal covariance, as combine_terrains fills it)
+  Vec2 mean{0.0, 0.0};
+  std::array<double, 4> cov{0.0, 0.0, 0.0, 0.0};  // row-major 2x2
+  double trace() const { return cov[0] + cov[3]; }
+};
+struct RolloutResult {  // mppi.hpp:53-56
+  std::vector<RobotState> states;
+  std::vector<GaussianCorrection> corrections;
+};
+using Perturbations = std::vector<std::vector<Vec2>>;  // S x N x 2 (one T x 2 block per sample)
+
+inline RolloutResult rollout(const RobotState& x0, const ControlSequence& seq, const PredictionModel& model,
+                             const std::vector<double>& weights, const NominalParams& nominal,
+                             int device = 0) {
+  const gpmppi_prediction_model pm = detail::model_c(model);
+  const gpmppi_nominal nom{nominal.tau_v, nominal.tau_omega, nominal.dt};
+  const int T = static_cast<int>(seq.size());
+  std::vector<double> sq(2 * seq.size()), st(5 * (seq.size() + 1)), corr(4 * seq.size());
+  for (size_t k = 0; k < seq.size(); ++k) {
+    sq[2 * k] = seq[k].v_ref;
+    sq[2 * k + 1] = seq[k].omega_ref;
+  }
+  const auto x = x0.vec();
+  const int R = pm.kind == GPMPPI_MODEL_GP_ENSEMBLE ? static_cast<int>(weights.size()) : 0;
+  detail::check(gpmppi_rollout(&pm, &nom, weights.data(), R, x.data(), sq.data(), T, device, st.data(),
+                               corr.data()));
+  RolloutResult r;
+  for (int k = 0; k <= T; ++k) r.states.push_back({st[5 * k], st[5 * k + 1], st[5 * k + 2], st[5 * k + 3], st[5 * k + 4]});
+  for (int k = 0; k < T; ++k) {
+    GaussianCorrection c;
+    c.mean = {corr[4 * k], corr[4 * k + 1]};
+    c.cov = {corr[4 * k + 2], 0.0, 0.0, corr[4 * k + 3]};
+    r.corrections.push_back(c);
+  }
+  return r;
+}
+
+inline Perturbations sample_perturbations(const MppiConfig& cfg, std::uint64_t tick, int device = 0) {
+  const gpmppi_mppi_config c = cfg.c();
+  std::vector<double> e(static_cast<size_t>(cfg.samples) * cfg.horizon * 2);
+  detail::check(gpmppi_sample_perturbations(&c, tick, device, e.data()));
+  Perturbations out(cfg.samples, std::vector<Vec2>(cfg.horizon));
+  for (int s = 0; s < cfg.samples; ++s)
+    for (int k = 0; k < cfg.horizon; ++k)
+      out[s][k] = {e[(static_cast<size_t>(s) * cfg.horizon + k) * 2], e[(static_cast<size_t>(s) * cfg.horizon + k) * 2 + 1]};
+  return out;
+}
+
+inline std::vector<double> trajectory_weights(const std::vector<double>& costs, double lambda, int device = 0) {
+  std::vector<double> w(costs.size());
+  detail::check(gpmppi_trajectory_weights(costs.data(), static_cast<int64_t>(costs.size()), lambda, device, w.data()));
+  return w;
+}
+
+inline ControlSequence update_controls(const ControlSequence& nominal, const Perturbations& eps,
+                                       const std::vector<double>& weights, const ControlBounds& bounds,
+                                       int device = 0) {
+  if (eps.size() != weights.size()) throw std::invalid_argument("update_controls: one weight per sample required");
+  const int T = static_cast<int>(nominal.size());
+  std::vector<double> nom(2 * nominal.size()), e(eps.size() * 2 * nominal.size()), out(2 * nominal.size());
+  for (int k = 0; k < T; ++k) {
+    nom[2 * k] = nominal[k].v_ref;
+    nom[2 * k + 1] = nominal[k].omega_ref;
+  }
+  for (size_t s = 0; s < eps.size(); ++s)
+    for (int k = 0; k < T; ++k) {
+      e[(s * T + k) * 2] = eps[s][k][0];
+      e[(s * T + k) * 2 + 1] = eps[s][k][1];
+    }
+  const double lo[2] = {bounds.lo.v_ref, bounds.lo.omega_ref}, hi[2] = {bounds.hi.v_ref, bounds.hi.omega_ref};
+  detail::check(gpmppi_update_controls(nom.data(), T, e.data(), weights.data(), static_cast<int64_t>(weights.size()),
+                                       lo, hi, device, out.data()));
+  ControlSequence r(T);
+  for (int k = 0; k < T; ++k) r[k] = {out[2 * k], out[2 * k + 1]};
+  return r;
+}
+
+inline ControlSequence shift_horizon(const ControlSequence& seq, int device = 0) {
+  if (seq.empty()) throw std::invalid_argument("shift_horizon: empty sequence");
+  const int T = static_cast<int>(seq.size());
+  std::vector<double> s(2 * seq.size()), out(2 * seq.size());
+  for (int k = 0; k < T; ++k) {
+    s[2 * k] = seq[k].v_ref;
+    s[2 * k + 1] = seq[k].omega_ref;
+  }
+  detail::check(gpmppi_shift_horizon(s.data(), T, device, out.data()));
+  ControlSequence r(T);
+  for (int k = 0; k < T; ++k) r[k] = {out[2 * k], out[2 * k + 1]};
+  return r;
+}
+
+// B independent planners sharing one model (BASELINE config 4): robot b behaves as a
+// Planner with seed seeds[b] (default cfg.seed + b). Combined tasks per robot.
+class BatchPlanner {
+ public:
+  BatchPlanner(const MppiConfig& cfg, PredictionModel model, NominalParams nominal, double p_x, int robots,
+               const std::vector<std::uint64_t>& seeds = {}, int device = 0)
+      : cfg_(cfg), robots_(robots) {
+    const gpmppi_prediction_model pm = detail::model_c(model);
+    const gpmppi_mppi_config c = cfg.c();
+    const gpmppi_nominal nom{nominal.tau_v, nominal.tau_omega, nominal.dt};
+    if (!seeds.empty() && static_cast<int>(seeds.size()) != robots)
+      throw std::invalid_argument("BatchPlanner: one seed per robot");
+    detail::check(gpmppi_planner_create_batch(&c, &pm, &nom, p_x, robots, seeds.empty() ? nullptr : seeds.data(),
+                                              device, &h_));
+  }
+  BatchPlanner(BatchPlanner&& o) noexcept : cfg_(o.cfg_), robots_(o.robots_), h_(std::exchange(o.h_, nullptr)) {}
+  BatchPlanner(const BatchPlanner&) = delete;
+  ~BatchPlanner() { gpmppi_planner_free(h_); }
+
+  // one tick of every robot: states[b], tasks[b] -> commands[b]
+  std::vector<Control> plan_step(const std::vector<RobotState>& x0, const std::vector<CombinedTask>& tasks,
+                                 std::vector<StepDiagnostics>* diags = nullptr) {
+    if (static_cast<int>(x0.size()) != robots_ || static_cast<int>(tasks.size()) != robots_)
+      throw std::invalid_argument("BatchPlanner: one state and one task per robot");
+    std::vector<double> xs(5 * x0.size());
+    for (size_t b = 0; b < x0.size(); ++b) {
+      const auto v = x0[b].vec();
+      for (int i = 0; i < 5; ++i) xs[5 * b + i] = v[i];
+    }
+    std::vector<gpmppi_track> tr(robots_);
+    std::vector<std::vector<double>> wp(robots_), ob(robots_);
+    std::vector<gpmppi_task> t(robots_);
+    for (int b = 0; b < robots_; ++b) {
+      const CombinedTask& k = tasks[b];
+      if (!k.track || !k.obstacles) throw std::invalid_argument("BatchPlanner: combined task needs track and obstacles");
+      tr[b] = {};
+      tr[b].is_circle = k.track->is_circle;
+      tr[b].cx = k.track->center[0];
+      tr[b].cy = k.track->center[1];
+      tr[b].radius = k.track->radius;
+      for (const auto& p : k.track->waypoints) {
+        wp[b].push_back(p[0]);
+        wp[b].push_back(p[1]);
+      }
+      tr[b].n_waypoints = static_cast<int>(k.track->waypoints.size());
+      tr[b].waypoints = wp[b].data();
+      tr[b].closed = k.track->closed;
+      tr[b].half_width = k.track->half_width;
+      for (const auto& o : *k.obstacles) {
+        ob[b].push_back(o.center[0]);
+        ob[b].push_back(o.center[1]);
+        ob[b].push_back(o.radius);
+      }
+      t[b] = {};
+      t[b].kind = GPMPPI_TASK_COMBINED;
+      t[b].track = &tr[b];
+      t[b].v_desired = k.v_desired;
+      t[b].tracking = {k.weights.variance, k.weights.deviation, k.weights.slip, k.weights.safety, k.weights.speed};
+      t[b].obstacles = ob[b].data();
+      t[b].n_obstacles = static_cast<int>(k.obstacles->size());
+      t[b].avoidance.obstacle = k.obstacle_weight;
+      t[b].high_cost = 1e4;
+    }
+    std::vector<double> cmd(2 * robots_);
+    std::vector<gpmppi_diag> d(robots_);
+    detail::check(gpmppi_planner_plan_step_batch(h_, xs.data(), t.data(), cmd.data(), d.data()));
+    std::vector<Control> out(robots_);
+    for (int b = 0; b < robots_; ++b) out[b] = {cmd[2 * b], cmd[2 * b + 1]};
+    if (diags) {
+      diags->resize(robots_);
+      for (int b = 0; b < robots_; ++b) {
+        (*diags)[b].best_cost = d[b].best_cost;
+        (*diags)[b].mean_cost = d[b].mean_cost;
+        (*diags)[b].ess = d[b].ess;
+        (*diags)[b].weight_entropy = d[b].weight_entropy;
+        (*diags)[b].nonfinite_samples = d[b].nonfinite_samples;
+        (*diags)[b].tightening_infeasible = d[b].tightening_infeasible != 0;
+        (*diags)[b].plan_ms = d[b].plan_ms;
+        (*diags)[b].command_ms = d[b].command_ms;
+      }
+    }
+    return out;
+  }
+  void set_terrain_weights(int robot, const std::vector<double>& w) {
+    detail::check(gpmppi_planner_set_robot_terrain_weights(h_, robot, w.data(), static_cast<int>(w.size())));
+  }
+  int robots() const { return robots_; }
+  std::uint64_t tick() const { return gpmppi_planner_tick(h_); }
+  gpmppi_planner* handle() { return h_; }
+
+ private:
+  MppiConfig cfg_;
+  int robots_;
+  gpmppi_planner* h_ = nullptr;
 };
 
 }  // namespace gpmppi

@@ -109,6 +109,14 @@ typedef struct {
   double track_width;
 } gpmppi_prediction_model;
 
+/* Models file GPMPPIM1 (harness.cpp:249-284): magic, EDD5 params (5 f64),
+ * nominal (3 f64), has_gp byte, then a GPMPPIG1 record. gp is NULL when the file
+ * carries no GP. */
+int gpmppi_models_load(const char* path, int device, gpmppi_edd5* edd5, gpmppi_nominal* nominal,
+                       gpmppi_model** gp);
+int gpmppi_models_save(const char* path, const gpmppi_edd5* edd5, const gpmppi_nominal* nominal,
+                       const gpmppi_model* gp);
+
 typedef struct { /* Track (costs.hpp:13-27) */
   int is_circle;
   double cx, cy, radius;

@@ -87,6 +87,8 @@ SIGNATURES = [
     ("gpmppi_model_fit", C.c_int, [_dp, _dp, C.c_int64, C.c_int64, _dp, C.c_int, C.POINTER(_vp)]),
     ("gpmppi_model_load", C.c_int, [C.c_char_p, C.c_int, C.POINTER(_vp)]),
     ("gpmppi_model_save", C.c_int, [_vp, C.c_char_p]),
+    ("gpmppi_models_load", C.c_int, [C.c_char_p, C.c_int, C.POINTER(Edd5C), C.POINTER(NominalC), C.POINTER(_vp)]),
+    ("gpmppi_models_save", C.c_int, [C.c_char_p, C.POINTER(Edd5C), C.POINTER(NominalC), _vp]),
     ("gpmppi_model_free", None, [_vp]),
     ("gpmppi_model_n_points", C.c_int, [_vp]),
     ("gpmppi_model_n_outputs", C.c_int, [_vp]),

@@ -307,7 +307,49 @@ gpmppi_model* build_model(const double* X, const double* Y, int64_t n64, int64_t
   return M;
 }
 
-const char kGpMagic[8] = {'G', 'P', 'M', 'P', 'P', 'I', 'G', '1'};  // gp.cpp:19
+const char kGpMagic[8] = {'G', 'P', 'M', 'P', 'P', 'I', 'G', '1'};      // gp.cpp:19
+const char kModelsMagic[8] = {'G', 'P', 'M', 'P', 'P', 'I', 'M', '1'};  // harness.cpp:19
+
+// GpModel::load(std::istream&) (gp.cpp:250-272): column-major f64 records, refit.
+gpmppi_model* load_gp_stream(std::istream& is, int device) {
+  auto read_raw = [&](void* p, size_t bytes) {
+    is.read(static_cast<char*>(p), (std::streamsize)bytes);
+    if (!is) runtime("GpModel::load: truncated record");
+  };
+  char magic[8];
+  read_raw(magic, 8);
+  if (std::memcmp(magic, kGpMagic, 8) != 0) runtime("GpModel::load: bad magic");
+  int64_t n = 0, m = 0;
+  read_raw(&n, 8);
+  read_raw(&m, 8);
+  if (n < 1 || m < 1 || n > (1 << 24) || m > (1 << 16)) runtime("GpModel::load: implausible dimensions");
+  std::vector<double> cin((size_t)n * 4), cout((size_t)n * m), kern((size_t)m * 6);
+  read_raw(cin.data(), sizeof(double) * cin.size());
+  read_raw(cout.data(), sizeof(double) * cout.size());
+  read_raw(kern.data(), sizeof(double) * kern.size());  // per output: sv, l0..l3, nv
+  std::vector<double> X((size_t)n * 4), Y((size_t)n * m);  // column-major -> row-major
+  for (int64_t i = 0; i < n; ++i) {
+    for (int d = 0; d < 4; ++d) X[(size_t)i * 4 + d] = cin[(size_t)d * n + i];
+    for (int64_t j = 0; j < m; ++j) Y[(size_t)i * m + j] = cout[(size_t)j * n + i];
+  }
+  return build_model(X.data(), Y.data(), n, m, kern.data(), device);
+}
+
+// GpModel::save(std::ostream&) (gp.cpp:230-242)
+void save_gp_stream(std::ostream& os, const gpmppi_model* M) {
+  const int64_t n = M->n, m = M->m;
+  os.write(kGpMagic, 8);
+  os.write(reinterpret_cast<const char*>(&n), 8);
+  os.write(reinterpret_cast<const char*>(&m), 8);
+  std::vector<double> cin((size_t)n * 4), cout((size_t)n * m);
+  for (int64_t i = 0; i < n; ++i) {
+    for (int d = 0; d < 4; ++d) cin[(size_t)d * n + i] = M->inputs[(size_t)i * 4 + d];
+    for (int64_t j = 0; j < m; ++j) cout[(size_t)j * n + i] = M->outputs[(size_t)i * m + j];
+  }
+  os.write(reinterpret_cast<const char*>(cin.data()), sizeof(double) * cin.size());
+  os.write(reinterpret_cast<const char*>(cout.data()), sizeof(double) * cout.size());
+  os.write(reinterpret_cast<const char*>(M->kernels.data()), sizeof(double) * M->kernels.size());
+}
 
 }  // namespace
 
@@ -324,54 +366,64 @@ int gpmppi_model_fit(const double* inputs, const double* outputs, int64_t n, int
   return guarded([&] { *out = build_model(inputs, outputs, n, m, kernels, device); });
 }
 
-int gpmppi_model_load(const char* path, int device, gpmppi_model** out) {  // gp.cpp:244-272
+int gpmppi_model_load(const char* path, int device, gpmppi_model** out) {  // gp.cpp:244-248
   if (!out) return fail(GPMPPI_INVALID_ARGUMENT, "null output handle");
   *out = nullptr;
   return guarded([&] {
     std::ifstream is(path ? path : "", std::ios::binary);
     if (!is) runtime(std::string("GpModel::load: cannot open ") + (path ? path : ""));
-    auto read_raw = [&](void* p, size_t bytes) {
-      is.read(static_cast<char*>(p), (std::streamsize)bytes);
-      if (!is) runtime("GpModel::load: truncated record");
-    };
-    char magic[8];
-    read_raw(magic, 8);
-    if (std::memcmp(magic, kGpMagic, 8) != 0) runtime("GpModel::load: bad magic");
-    int64_t n = 0, m = 0;
-    read_raw(&n, 8);
-    read_raw(&m, 8);
-    if (n < 1 || m < 1 || n > (1 << 24) || m > (1 << 16)) runtime("GpModel::load: implausible dimensions");
-    std::vector<double> cin((size_t)n * 4), cout((size_t)n * m), kern((size_t)m * 6);
-    read_raw(cin.data(), sizeof(double) * cin.size());
-    read_raw(cout.data(), sizeof(double) * cout.size());
-    read_raw(kern.data(), sizeof(double) * kern.size());  // per output: sv, l0..l3, nv
-    std::vector<double> X((size_t)n * 4), Y((size_t)n * m);  // column-major → row-major
-    for (int64_t i = 0; i < n; ++i) {
-      for (int d = 0; d < 4; ++d) X[(size_t)i * 4 + d] = cin[(size_t)d * n + i];
-      for (int64_t j = 0; j < m; ++j) Y[(size_t)i * m + j] = cout[(size_t)j * n + i];
-    }
-    *out = build_model(X.data(), Y.data(), n, m, kern.data(), device);
+    *out = load_gp_stream(is, device);
   });
 }
 
-int gpmppi_model_save(const gpmppi_model* M, const char* path) {  // gp.cpp:223-242
+int gpmppi_model_save(const gpmppi_model* M, const char* path) {  // gp.cpp:223-228
   if (!M) return fail(GPMPPI_INVALID_ARGUMENT, "null model");
   return guarded([&] {
     std::ofstream os(path ? path : "", std::ios::binary);
     if (!os) runtime(std::string("GpModel::save: cannot open ") + (path ? path : ""));
-    const int64_t n = M->n, m = M->m;
-    os.write(kGpMagic, 8);
-    os.write(reinterpret_cast<const char*>(&n), 8);
-    os.write(reinterpret_cast<const char*>(&m), 8);
-    std::vector<double> cin((size_t)n * 4), cout((size_t)n * m);
-    for (int64_t i = 0; i < n; ++i) {
-      for (int d = 0; d < 4; ++d) cin[(size_t)d * n + i] = M->inputs[(size_t)i * 4 + d];
-      for (int64_t j = 0; j < m; ++j) cout[(size_t)j * n + i] = M->outputs[(size_t)i * m + j];
-    }
-    os.write(reinterpret_cast<const char*>(cin.data()), sizeof(double) * cin.size());
-    os.write(reinterpret_cast<const char*>(cout.data()), sizeof(double) * cout.size());
-    os.write(reinterpret_cast<const char*>(M->kernels.data()), sizeof(double) * M->kernels.size());
+    save_gp_stream(os, M);
     if (!os) runtime(std::string("GpModel::save: write failed for ") + path);
+  });
+}
+
+int gpmppi_models_load(const char* path, int device, gpmppi_edd5* edd5, gpmppi_nominal* nominal,
+                       gpmppi_model** gp) {  // harness.cpp:264-284
+  if (!gp) return fail(GPMPPI_INVALID_ARGUMENT, "null output handle");
+  *gp = nullptr;
+  return guarded([&] {
+    std::ifstream is(path ? path : "", std::ios::binary);
+    if (!is) runtime(std::string("load_models: cannot open ") + (path ? path : ""));
+    char magic[8];
+    is.read(magic, 8);
+    if (!is || std::memcmp(magic, kModelsMagic, 8) != 0)
+      runtime(std::string("load_models: bad magic in ") + (path ? path : ""));
+    double e[5], nm[3];
+    char has_gp = 0;
+    is.read(reinterpret_cast<char*>(e), sizeof e);
+    is.read(reinterpret_cast<char*>(nm), sizeof nm);
+    is.read(&has_gp, 1);
+    if (!is) runtime(std::string("load_models: truncated file ") + (path ? path : ""));
+    if (edd5) *edd5 = {e[0], e[1], e[2], e[3], e[4]};
+    if (nominal) *nominal = {nm[0], nm[1], nm[2]};
+    if (has_gp) *gp = load_gp_stream(is, device);
+  });
+}
+
+int gpmppi_models_save(const char* path, const gpmppi_edd5* edd5, const gpmppi_nominal* nominal,
+                       const gpmppi_model* gp) {  // harness.cpp:249-262
+  if (!edd5 || !nominal) return fail(GPMPPI_INVALID_ARGUMENT, "save_models: null argument");
+  return guarded([&] {
+    std::ofstream os(path ? path : "", std::ios::binary);
+    if (!os) runtime(std::string("save_models: cannot open ") + (path ? path : ""));
+    os.write(kModelsMagic, 8);
+    const double e[5] = {edd5->alpha_l, edd5->alpha_r, edd5->x_icr, edd5->y_icr_l, edd5->y_icr_r};
+    const double nm[3] = {nominal->tau_v, nominal->tau_omega, nominal->dt};
+    os.write(reinterpret_cast<const char*>(e), sizeof e);
+    os.write(reinterpret_cast<const char*>(nm), sizeof nm);
+    const char has_gp = gp ? 1 : 0;
+    os.write(&has_gp, 1);
+    if (gp) save_gp_stream(os, gp);
+    if (!os) runtime(std::string("save_models: write failed for ") + path);
   });
 }
 

@@ -317,6 +317,32 @@ class GpModel:
 
 
 # ----------------------------------------------------------------- planner
+@dataclass
+class TrainedModels:  # harness.hpp:41-46
+    has_gp: bool = False
+    gp: Optional[GpModel] = None
+    edd5: Edd5Params = field(default_factory=lambda: Edd5Params.ideal(0.37))
+    nominal: NominalParams = field(default_factory=NominalParams)
+
+
+def load_models(path: str, device: int = 0) -> TrainedModels:
+    """Models file GPMPPIM1 (harness.cpp:264-284); the GP is refit on load as GpModel::load."""
+    e, n, h = A.Edd5C(), A.NominalC(), C.c_void_p()
+    A.check(A.lib().gpmppi_models_load(path.encode(), device, C.byref(e), C.byref(n), C.byref(h)))
+    gp = GpModel(h, device) if h.value else None
+    return TrainedModels(gp is not None, gp, Edd5Params(e.alpha_l, e.alpha_r, e.x_icr, e.y_icr_l, e.y_icr_r),
+                         NominalParams(n.tau_v, n.tau_omega, n.dt))
+
+
+def save_models(path: str, models: TrainedModels) -> None:
+    """Models file GPMPPIM1 (harness.cpp:249-262)."""
+    p = models.edd5
+    e = A.Edd5C(p.alpha_l, p.alpha_r, p.x_icr, p.y_icr_l, p.y_icr_r)
+    n = A.NominalC(models.nominal.tau_v, models.nominal.tau_omega, models.nominal.dt)
+    gp = models.gp.handle if (models.has_gp and models.gp is not None) else None
+    A.check(A.lib().gpmppi_models_save(path.encode(), C.byref(e), C.byref(n), gp))
+
+
 class GpEnsemble:  # mppi.hpp:30-33
     def __init__(self, model: GpModel, n_terrains: int):
         self.model = model

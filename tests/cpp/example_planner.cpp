@@ -41,6 +41,21 @@ int main() {
     u = planner.plan_step(RobotState{}, CombinedTask{&lane, 2.0, {}, &obs, 1.0}, &d);
     std::printf("combined  u=(%.6f, %.6f) tick=%llu radii=%zu\n", u.v_ref, u.omega_ref,
                 (unsigned long long)planner.tick(), planner.lane_radii().size());
+    // free functions (mppi.hpp:60-79)
+    const std::vector<double> w = trajectory_weights({0.0, 0.1}, 0.1);
+    const ControlSequence seq = planner.nominal_sequence();
+    const RolloutResult r = rollout(RobotState{}, seq, GpEnsemble{&gp, R}, {1.0 / 3, 1.0 / 3, 1.0 / 3}, NominalParams{});
+    const Perturbations eps = sample_perturbations(cfg, 0);
+    const ControlSequence up = update_controls(seq, eps, std::vector<double>(eps.size(), 1.0 / eps.size()), ControlBounds{});
+    const ControlSequence sh = shift_horizon(seq);
+    std::printf("free      w0=%.12f states=%zu eps=%zux%zu upd=%zu shift=%zu\n", w[0], r.states.size(), eps.size(),
+                eps[0].size(), up.size(), sh.size());
+    // batched planner (config 4 API)
+    BatchPlanner batch(cfg, GpEnsemble{&gp, R}, NominalParams{}, 0.95, 3);
+    std::vector<Control> us = batch.plan_step({RobotState{}, RobotState{0.0, 0.1}, RobotState{0.0, -0.1}},
+                                              {CombinedTask{&lane, 2.0, {}, &obs, 1.0}, CombinedTask{&lane, 1.5, {}, &obs, 1.0},
+                                               CombinedTask{&lane, 1.0, {}, &obs, 1.0}});
+    std::printf("batch     robots=%d u0=(%.6f, %.6f)\n", batch.robots(), us[0].v_ref, us[0].omega_ref);
   } catch (const std::runtime_error& e) {
     std::printf("runtime_error: %s\n", e.what());
     return 2;

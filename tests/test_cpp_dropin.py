@@ -43,3 +43,5 @@ def test_header_plan_step_on_gpu(tmp_path):
     lines = r.stdout.strip().splitlines()
     assert lines[0].startswith("tracking") and lines[2].startswith("combined")
     assert "radii=20" in lines[2]
+    assert lines[3].startswith("free") and "w0=0.731058578630" in lines[3] and "states=21" in lines[3]
+    assert "eps=512x20" in lines[3] and lines[4].startswith("batch") and "robots=3" in lines[4]
