@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libgpmppi_b200.so")
+# GPMPPI_LIB selects an in-tree A/B experiment build (lib/libgpmppi_b200_<variant>.so)
+LIB_PATH = os.environ.get("GPMPPI_LIB") or os.path.join(_PKG, "lib", "libgpmppi_b200.so")
 
 _dp = C.POINTER(C.c_double)
 _u8p = C.POINTER(C.c_uint8)

@@ -149,7 +149,7 @@ cudaError_t launch_reduce(const ReduceArgs& a, int blocks, cudaStream_t st);
 cudaError_t launch_finish(const double* tuples, int n, int T, double lambda, double* nominal_seq,
                           const double lo[2], const double hi[2], double* out, long long K_total,
                           double* combined, cudaStream_t st);
-int rollout_samples_per_block(int K_local, int num_sms, int* lps, int* threads);
+int rollout_samples_per_block(int K_local, int B, int num_sms, int* lps, int* threads, int* spg);
 cudaError_t launch_tighten(const TightenArgs& a, cudaStream_t st);
 cudaError_t launch_predict(const ModelDev& m, const double* q, long long S, double* mean,
                            double* var, cudaStream_t st);

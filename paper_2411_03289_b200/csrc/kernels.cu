@@ -158,17 +158,23 @@ GPM_D double group_sum(double v) {  // xor butterfly inside an LPS-lane group
   return v;
 }
 
-// One LPS-lane group per sample (32/LPS samples per warp share every Z/alpha
-// shared-memory read). The GP query of step k needs only (v_k, omega_k, u_k), so:
+// One LPS-lane group per SPG samples (32/LPS groups per warp share every Z/alpha
+// shared-memory read; each lane reuses its loaded points for its group's SPG samples,
+// which halves the LDS per FP64 op at SPG=2 and gives SPG independent exp chains).
+// The GP query of step k needs only (v_k, omega_k, u_k), so:
 //  phase 1 (serial in k): noise, clamp, GP mean k*·alpha (lanes split the n
 //          points, butterfly sum), first-order lag update of (v, omega);
-//  phase 2 (lanes split the steps k): heading recursion, FP64 sincos / exact-arc
-//          increments, x/y in step order, non-finite freeze (mppi.cpp:343-346),
-//          per-step costs and flags (costs.cpp:127-171) and their group sums.
-// Per-group trajectory scratch lives in L2 (scr, 9 arrays of T+1 doubles).
+//  phase 2 (lanes split the steps k, one sample after the other): heading recursion,
+//          FP64 sincos / exact-arc increments, x/y in step order, non-finite freeze
+//          (mppi.cpp:343-346), per-step costs and flags (costs.cpp:127-171).
+// Per-sample trajectory scratch lives in L2 (scr, 9 arrays of T+1 doubles).
 constexpr int SCR_ARRAYS = 9;
-template <int NO, int LPS>
-__global__ void __launch_bounds__(256, 1) rollout_gp_kernel(const RolloutArgs a) {
+constexpr int kMaxSampleSlotsPerBlock = 128;  // groups per block (<= 64) x SPG (<= 2)
+#ifndef GPM_ROLLOUT_MINB
+#define GPM_ROLLOUT_MINB 1
+#endif
+template <int NO, int LPS, int SPG>
+__global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const RolloutArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const SmemView sv = carve_smem(a, smem);
   const int ns = a.model.ns;  // even SoA stride (padding points contribute exactly 0)
@@ -187,68 +193,84 @@ __global__ void __launch_bounds__(256, 1) rollout_gp_kernel(const RolloutArgs a)
   const int gl = threadIdx.x % LPS;  // lane inside the sample group
   const int groups_per_block = blockDim.x / LPS;
   const int gib = threadIdx.x / LPS;  // group index in the block
-  const int gid = blockIdx.x * groups_per_block + gib;
   const int T = a.T;
   const int stride = T + 1;
-  double* scr = a.scratch + (size_t)gid * SCR_ARRAYS * stride;
-  double* su0 = scr;
-  double* su1 = scr + stride;
-  double* sv_ = scr + 2 * stride;
-  double* sw = scr + 3 * stride;
-  double* sth = scr + 4 * stride;
-  double* ssin = scr + 5 * stride;
-  double* scos = scr + 6 * stride;
-  double* sx = scr + 7 * stride;
-  double* sy = scr + 8 * stride;
+  // scratch slot of sample j of this group
+  double* const scr0 = a.scratch + ((size_t)blockIdx.x * kMaxSampleSlotsPerBlock + (size_t)gib * SPG) *
+                                       SCR_ARRAYS * stride;
   const double av = a.nom.dt / a.nom.tau_v, aw = a.nom.dt / a.nom.tau_omega;
-  // work items: (robot, chunk of groups_per_block samples); every lane of the block
+  // work items: (robot, chunk of groups_per_block*SPG samples); every lane of the block
   // runs the same item sequence (samples beyond K are masked, never early-exit)
-  const int chunks = (a.K_local + groups_per_block - 1) / groups_per_block;
+  const int spb = groups_per_block * SPG;
+  const int chunks = (a.K_local + spb - 1) / spb;
   const long long items = (long long)a.B * chunks;
   int loaded = -1;
 
   for (long long item = blockIdx.x; item < items; item += gridDim.x) {
     const int b = (int)(item / chunks);
-    const int ls = (int)(item % chunks) * groups_per_block + gib;  // local sample of robot b
+    const int ls0 = (int)(item % chunks) * spb + gib * SPG;  // first local sample of the group
     if (b != loaded) {
       __syncthreads();  // previous item's readers are done with the robot view
       load_robot_smem(a, sv, b);
       __syncthreads();
       loaded = b;
     }
-    const bool valid = ls < a.K_local;
-    const long long sl = (long long)b * a.K_local + (valid ? ls : 0);         // output slot
-    const long long s = a.s_begin + (valid ? ls : 0);  // noise counter (per-robot key)
     const double* x0 = a.x0 + (size_t)b * BatchStrides::X0;
     const uint64_t key = (uint64_t)__double_as_longlong(x0[6]);
     const int O = task.n_obs;
-    // ---------------- phase 1: serial (v, omega) chain with the GP mean
-    double v = x0[3], w = x0[4];
-    if (gl == 0) {
-      sv_[0] = v;
-      sw[0] = w;
-    }
-    for (int k = 0; k < T; ++k) {
-      double e0 = 0.0, e1 = 0.0;
-      if (valid) sample_noise(a, key, sl, s, k, &e0, &e1);
-      const double u0 = clampd(sv.nom[2 * k] + e0, a.lo[0], a.hi[0]);  // mppi.cpp:298-308
-      const double u1 = clampd(sv.nom[2 * k + 1] + e1, a.lo[1], a.hi[1]);
-      if (valid && gl == 0) {
-        a.queries[(size_t)sl * T + k] = make_float4((float)v, (float)w, (float)u0, (float)u1);
-        su0[k] = u0;
-        su1[k] = u1;
+    bool valid[SPG];
+    long long sl[SPG], s[SPG];
+    double v[SPG], w[SPG];
+#pragma unroll
+    for (int j = 0; j < SPG; ++j) {
+      const int ls = ls0 + j;
+      valid[j] = ls < a.K_local;
+      sl[j] = (long long)b * a.K_local + (valid[j] ? ls : 0);  // output slot
+      s[j] = a.s_begin + (valid[j] ? ls : 0);                  // noise counter (per-robot key)
+      v[j] = x0[3];
+      w[j] = x0[4];
+      if (gl == 0) {
+        double* scr = scr0 + (size_t)j * SCR_ARRAYS * stride;
+        scr[2 * stride] = v[j];
+        scr[3 * stride] = w[j];
       }
-      double cm0 = 0.0, cm1 = 0.0;  // combine_terrains (mppi.cpp:34-49)
+    }
+    // ---------------- phase 1: serial (v, omega) chains with the GP mean
+    for (int k = 0; k < T; ++k) {
+      double u0[SPG], u1[SPG];
+#pragma unroll
+      for (int j = 0; j < SPG; ++j) {
+        double e0 = 0.0, e1 = 0.0;
+        if (valid[j]) sample_noise(a, key, sl[j], s[j], k, &e0, &e1);
+        u0[j] = clampd(sv.nom[2 * k] + e0, a.lo[0], a.hi[0]);  // mppi.cpp:298-308
+        u1[j] = clampd(sv.nom[2 * k + 1] + e1, a.lo[1], a.hi[1]);
+        if (valid[j] && gl == 0) {
+          a.queries[(size_t)sl[j] * T + k] = make_float4((float)v[j], (float)w[j], (float)u0[j], (float)u1[j]);
+          double* scr = scr0 + (size_t)j * SCR_ARRAYS * stride;
+          scr[k] = u0[j];
+          scr[stride + k] = u1[j];
+        }
+      }
+      double cm0[SPG], cm1[SPG];  // combine_terrains (mppi.cpp:34-49)
+#pragma unroll
+      for (int j = 0; j < SPG; ++j) cm0[j] = cm1[j] = 0.0;
       const double* gp = sv.pts;
       for (int g = 0; g < a.model.G; ++g) {
         const GroupDev& G = a.model.g[g];
         const int nout = G.n_out;
         // gp.cpp:172-176 augmented query [q/l | -1/2|q/l|^2 | 1]
-        const double q0 = v / G.ls[0], q1 = w / G.ls[1], q2 = u0 / G.ls[2], q3 = u1 / G.ls[3];
-        const double qn = -0.5 * (q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
-        double acc[NO];
+        double q0[SPG], q1[SPG], q2[SPG], q3[SPG], qn[SPG];
+        double acc[SPG][NO];
 #pragma unroll
-        for (int o = 0; o < NO; ++o) acc[o] = 0.0;
+        for (int j = 0; j < SPG; ++j) {
+          q0[j] = v[j] / G.ls[0];
+          q1[j] = w[j] / G.ls[1];
+          q2[j] = u0[j] / G.ls[2];
+          q3[j] = u1[j] / G.ls[3];
+          qn[j] = -0.5 * (q0[j] * q0[j] + q1[j] * q1[j] + q2[j] * q2[j] + q3[j] * q3[j]);
+#pragma unroll
+          for (int o = 0; o < NO; ++o) acc[j][o] = 0.0;
+        }
         // two adjacent points per lane and load (LDS.128): the 32/LPS sample groups of a
         // warp read the same addresses, so a 16-byte access doubles the bytes per wavefront
         const double2* z0 = reinterpret_cast<const double2*>(gp);
@@ -258,127 +280,151 @@ __global__ void __launch_bounds__(256, 1) rollout_gp_kernel(const RolloutArgs a)
         const double2* zn = reinterpret_cast<const double2*>(gp + 4 * ns);
         const double2* al = reinterpret_cast<const double2*>(gp + 5 * ns);
         const int half = ns >> 1;
-        // K/148 samples per SM leave ~7 warps per SM; registers are plentiful, so
-        // unroll for ILP (8 independent exp chains in flight per lane)
-#pragma unroll 4
+#pragma unroll(4 / SPG)
         for (int jp = gl; jp < half; jp += LPS) {
           // gp.cpp:177-179: k*_j = exp(q_aug · inputs_aug_j)
           const double2 a0 = z0[jp], a1 = z1[jp], a2 = z2[jp], a3 = z3[jp], an = zn[jp];
-          const double d0 = q0 * a0.x + q1 * a1.x + q2 * a2.x + q3 * a3.x + qn + an.x;
-          const double d1 = q0 * a0.y + q1 * a1.y + q2 * a2.y + q3 * a3.y + qn + an.y;
-          const double k0 = exp_tab(d0, sv.etab), k1 = exp_tab(d1, sv.etab);
+          double k0[SPG], k1[SPG];
+#pragma unroll
+          for (int j = 0; j < SPG; ++j) {
+            const double d0 = q0[j] * a0.x + q1[j] * a1.x + q2[j] * a2.x + q3[j] * a3.x + qn[j] + an.x;
+            const double d1 = q0[j] * a0.y + q1[j] * a1.y + q2[j] * a2.y + q3[j] * a3.y + qn[j] + an.y;
+            k0[j] = exp_tab(d0, sv.etab);
+            k1[j] = exp_tab(d1, sv.etab);
+          }
 #pragma unroll
           for (int o = 0; o < NO; ++o)
             if (o < nout) {
               const double2 ao = al[o * half + jp];
-              acc[o] = fma(k1, ao.y, fma(k0, ao.x, acc[o]));  // gp.cpp:181-182
+#pragma unroll
+              for (int j = 0; j < SPG; ++j) acc[j][o] = fma(k1[j], ao.y, fma(k0[j], ao.x, acc[j][o]));  // gp.cpp:181-182
             }
         }
 #pragma unroll
         for (int o = 0; o < NO; ++o) {
           if (o < nout) {
-            const double mo = group_sum<LPS>(acc[o]);
             const int gi = G.out_idx[o];
             const double wt = sv.tw[gi >> 1];
-            if (gi & 1)
-              cm1 += wt * mo;
-            else
-              cm0 += wt * mo;
+#pragma unroll
+            for (int j = 0; j < SPG; ++j) {
+              const double mo = group_sum<LPS>(acc[j][o]);
+              if (gi & 1)
+                cm1[j] += wt * mo;
+              else
+                cm0[j] += wt * mo;
+            }
           }
         }
         gp += (size_t)(5 + nout) * ns;
       }
-      v = v + av * (u0 - v) + cm0;  // step_nominal lag (dynamics.cpp:63-64) + mppi.cpp:341-342
-      w = w + aw * (u1 - w) + cm1;
-      if (gl == 0) {
-        sv_[k + 1] = v;
-        sw[k + 1] = w;
-      }
-    }
-    __syncwarp();
-    // ---------------- phase 2a: heading recursion (arc_advance: theta = wrap(theta + omega dt))
-    if (gl == 0) {
-      double th = x0[2];
-      sth[0] = th;
-      for (int k = 0; k < T; ++k) {
-        th = wrap_angle(th + sw[k] * a.nom.dt);
-        sth[k + 1] = th;
-      }
-    }
-    __syncwarp();
-    // ---------------- phase 2b: sincos and exact-arc increments, lanes split the steps
-    for (int k = gl; k < T; k += LPS) {
-      const double th = sth[k], vk = sv_[k], wk = sw[k];
-      double sp, cp;
-      sincos(th, &sp, &cp);
-      ssin[k] = sp;
-      scos[k] = cp;
-      double dx = 0.0, dy = 0.0, t2 = th;
-      arc_advance(dx, dy, t2, vk, 0.0, wk, a.nom.dt, sp, cp);
-      sx[k + 1] = dx;
-      sy[k + 1] = dy;
-    }
-    __syncwarp();
-    // ---------------- phase 2c: positions in step order + first non-finite state
-    int kd = T;  // states k > kd are frozen at state kd (mppi.cpp:343-346)
-    if (gl == 0) {
-      double x = x0[0], y = x0[1];
-      sx[0] = x;
-      sy[0] = y;
-      for (int k = 0; k < T; ++k) {
-        x += sx[k + 1];
-        y += sy[k + 1];
-        sx[k + 1] = x;
-        sy[k + 1] = y;
-        if (kd == T && !(isfinite(x) && isfinite(y) && isfinite(sth[k + 1]) && isfinite(sv_[k + 1]) &&
-                         isfinite(sw[k + 1])))
-          kd = k;
-      }
-    }
-    kd = __shfl_sync(0xffffffffu, kd, (threadIdx.x & 31) & ~(LPS - 1));
-    __syncwarp();
-    // ---------------- phase 2d: per-step costs and flags (costs.cpp:127-171), lanes split the steps
-    double cost = 0.0;
-    for (int wd = 0; wd < a.words; ++wd) {
-      uint32_t vb = 0, cb = 0;
-      const int kend = min(T, 32 * wd + 32);
-      for (int k = 32 * wd + gl; k < kend; k += LPS) {
-        const int ip = min(k, kd), in = min(k + 1, kd);
-        const double prev[5] = {sx[ip], sy[ip], sth[ip], sv_[ip], sw[ip]};
-        const double next[5] = {sx[in], sy[in], sth[in], sv_[in], sw[in]};
-        double decay = 1.0;  // 0.9^k by repeated multiplication, as costs.cpp:146
-        for (int i = 0; i < k; ++i) decay *= 0.9;
-        const StepCost c = step_cost(task, prev, next, ssin[ip], scos[ip], sv.rbar[k],
-                                     sv.marg + (size_t)k * O, su0[k], decay);
-        cost += c.cost;
-        vb |= (uint32_t)c.viol << (k & 31);
-        cb |= (uint32_t)c.coll << (k & 31);
-      }
 #pragma unroll
-      for (int o = LPS / 2; o > 0; o >>= 1) {
-        vb |= __shfl_xor_sync(0xffffffffu, vb, o);
-        cb |= __shfl_xor_sync(0xffffffffu, cb, o);
+      for (int j = 0; j < SPG; ++j) {
+        v[j] = v[j] + av * (u0[j] - v[j]) + cm0[j];  // step_nominal lag (dynamics.cpp:63-64) + mppi.cpp:341-342
+        w[j] = w[j] + aw * (u1[j] - w[j]) + cm1[j];
+        if (gl == 0) {
+          double* scr = scr0 + (size_t)j * SCR_ARRAYS * stride;
+          scr[2 * stride + k + 1] = v[j];
+          scr[3 * stride + k + 1] = w[j];
+        }
       }
-      if (valid && gl == 0) {
-        a.viol_bits[(size_t)sl * a.words + wd] = vb;
-        a.coll_bits[(size_t)sl * a.words + wd] = cb;
-      }
-    }
-    cost = group_sum<LPS>(cost);
-    const bool alive = valid && kd == T;
-    bool term = false;
-    if (task.kind == TASK_AVOIDANCE) {  // costs.cpp:169 terminal_cost
-      const int il = min(T, kd);
-      const double gx = sx[il] - task.goal[0], gy = sy[il] - task.goal[1];
-      term = sqrt(gx * gx + gy * gy) <= task.goal[2];
-      cost += task.aw[3] * (term ? 0.0 : task.high_cost);
-    }
-    if (valid && gl == 0) {
-      a.cost_mean[sl] = alive ? cost : __longlong_as_double(0x7ff8000000000000LL);
-      a.term[sl] = term;
-      a.alive[sl] = alive;
     }
     __syncwarp();
+    for (int j = 0; j < SPG; ++j) {  // phase 2, one sample after the other
+      double* scr = scr0 + (size_t)j * SCR_ARRAYS * stride;
+      double* su0 = scr;
+      double* su1 = scr + stride;
+      double* sv_ = scr + 2 * stride;
+      double* sw = scr + 3 * stride;
+      double* sth = scr + 4 * stride;
+      double* ssin = scr + 5 * stride;
+      double* scos = scr + 6 * stride;
+      double* sx = scr + 7 * stride;
+      double* sy = scr + 8 * stride;
+      (void)su1;
+      // ---------------- phase 2a: heading recursion (arc_advance: theta = wrap(theta + omega dt))
+      if (gl == 0) {
+        double th = x0[2];
+        sth[0] = th;
+        for (int k = 0; k < T; ++k) {
+          th = wrap_angle(th + sw[k] * a.nom.dt);
+          sth[k + 1] = th;
+        }
+      }
+      __syncwarp();
+      // ---------------- phase 2b: sincos and exact-arc increments, lanes split the steps
+      for (int k = gl; k < T; k += LPS) {
+        const double th = sth[k], vk = sv_[k], wk = sw[k];
+        double sp, cp;
+        sincos(th, &sp, &cp);
+        ssin[k] = sp;
+        scos[k] = cp;
+        double dx = 0.0, dy = 0.0, t2 = th;
+        arc_advance(dx, dy, t2, vk, 0.0, wk, a.nom.dt, sp, cp);
+        sx[k + 1] = dx;
+        sy[k + 1] = dy;
+      }
+      __syncwarp();
+      // ---------------- phase 2c: positions in step order + first non-finite state
+      int kd = T;  // states k > kd are frozen at state kd (mppi.cpp:343-346)
+      if (gl == 0) {
+        double x = x0[0], y = x0[1];
+        sx[0] = x;
+        sy[0] = y;
+        for (int k = 0; k < T; ++k) {
+          x += sx[k + 1];
+          y += sy[k + 1];
+          sx[k + 1] = x;
+          sy[k + 1] = y;
+          if (kd == T && !(isfinite(x) && isfinite(y) && isfinite(sth[k + 1]) && isfinite(sv_[k + 1]) &&
+                           isfinite(sw[k + 1])))
+            kd = k;
+        }
+      }
+      kd = __shfl_sync(0xffffffffu, kd, (threadIdx.x & 31) & ~(LPS - 1));
+      __syncwarp();
+      // ---------------- phase 2d: per-step costs and flags (costs.cpp:127-171), lanes split the steps
+      double cost = 0.0;
+      for (int wd = 0; wd < a.words; ++wd) {
+        uint32_t vb = 0, cb = 0;
+        const int kend = min(T, 32 * wd + 32);
+        for (int k = 32 * wd + gl; k < kend; k += LPS) {
+          const int ip = min(k, kd), in = min(k + 1, kd);
+          const double prev[5] = {sx[ip], sy[ip], sth[ip], sv_[ip], sw[ip]};
+          const double next[5] = {sx[in], sy[in], sth[in], sv_[in], sw[in]};
+          double decay = 1.0;  // 0.9^k by repeated multiplication, as costs.cpp:146
+          for (int i = 0; i < k; ++i) decay *= 0.9;
+          const StepCost c = step_cost(task, prev, next, ssin[ip], scos[ip], sv.rbar[k],
+                                       sv.marg + (size_t)k * O, su0[k], decay);
+          cost += c.cost;
+          vb |= (uint32_t)c.viol << (k & 31);
+          cb |= (uint32_t)c.coll << (k & 31);
+        }
+#pragma unroll
+        for (int o = LPS / 2; o > 0; o >>= 1) {
+          vb |= __shfl_xor_sync(0xffffffffu, vb, o);
+          cb |= __shfl_xor_sync(0xffffffffu, cb, o);
+        }
+        if (valid[j] && gl == 0) {
+          a.viol_bits[(size_t)sl[j] * a.words + wd] = vb;
+          a.coll_bits[(size_t)sl[j] * a.words + wd] = cb;
+        }
+      }
+      cost = group_sum<LPS>(cost);
+      const bool alive = valid[j] && kd == T;
+      bool term = false;
+      if (task.kind == TASK_AVOIDANCE) {  // costs.cpp:169 terminal_cost
+        const int il = min(T, kd);
+        const double gx = sx[il] - task.goal[0], gy = sy[il] - task.goal[1];
+        term = sqrt(gx * gx + gy * gy) <= task.goal[2];
+        cost += task.aw[3] * (term ? 0.0 : task.high_cost);
+      }
+      if (valid[j] && gl == 0) {
+        a.cost_mean[sl[j]] = alive ? cost : __longlong_as_double(0x7ff8000000000000LL);
+        a.term[sl[j]] = term;
+        a.alive[sl[j]] = alive;
+      }
+      __syncwarp();
+    }
   }
 }
 
@@ -460,12 +506,13 @@ __global__ void __launch_bounds__(128) rollout_base_kernel(const RolloutArgs a) 
   }
 }
 
+// lanes per sample group and samples per group (env GPMPPI_LPS / GPMPPI_SPG force them)
+static int env_int(const char* name) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : 0;
+}
 int rollout_lanes_per_sample(int K, int num_sms) {
-  static int forced = -1;
-  if (forced < 0) {
-    const char* e = getenv("GPMPPI_LPS");
-    forced = e ? atoi(e) : 0;
-  }
+  static const int forced = env_int("GPMPPI_LPS");
   if (forced == 4 || forced == 8 || forced == 16 || forced == 32) return forced;
   // aim for >= ~7 warps per SM before widening the lane groups
   const long long per_sm = ((long long)K + num_sms - 1) / num_sms;
@@ -473,22 +520,35 @@ int rollout_lanes_per_sample(int K, int num_sms) {
   if (per_sm >= 14) return 16;
   return 32;
 }
-
-// trajectory scratch for every lane group the launcher can create (<= 64 per block)
-size_t rollout_scratch_doubles(int T, int num_sms) {
-  return (size_t)num_sms * 64 * SCR_ARRAYS * (size_t)(T + 1);
+int rollout_samples_per_group(int lps, long long total, int num_sms) {
+  static const int forced = env_int("GPMPPI_SPG");
+  if (lps == 4) return 1;
+  if (forced == 1 || forced == 2) return forced;
+  // beyond one wave (>= 64 samples per SM) the rollout is FP64-throughput bound and
+  // halving the LDS per FP64 op wins (config5 rollout 5.1 -> 3.7 ms); below it the
+  // single-sample latency chain decides and SPG = 1 is faster (config2 0.339 vs 0.376 ms)
+  return total >= 64LL * num_sms ? 2 : 1;
 }
 
-// lane groups per block for the GP rollout: spread one robot's samples over every
-// SM in a single wave when possible (one block per SM)
-int rollout_samples_per_block(int K_local, int num_sms, int* lps_out, int* threads_out) {
-  const int lps = rollout_lanes_per_sample(K_local, num_sms);
-  const int spw = 32 / lps;
-  const long long warps = ((long long)K_local + spw - 1) / spw;
+// trajectory scratch for every sample slot the launcher can create
+size_t rollout_scratch_doubles(int T, int num_sms) {
+  return (size_t)GPM_ROLLOUT_MINB * num_sms * kMaxSampleSlotsPerBlock * SCR_ARRAYS * (size_t)(T + 1);
+}
+
+// samples per block for the GP rollout: spread one robot's samples over every SM in a
+// single wave when possible (one block per SM)
+int rollout_samples_per_block(int K_local, int B, int num_sms, int* lps_out, int* threads_out, int* spg_out) {
+  const long long total = (long long)K_local * B;
+  const int lps = rollout_lanes_per_sample(total >= 64LL * num_sms ? (int)std::min<long long>(total, 1 << 30) : K_local,
+                                           num_sms);
+  const int spg = rollout_samples_per_group(lps, total, num_sms);
+  const int spw = 32 / lps * spg;
+  const long long warps = (total + spw - 1) / spw;  // all robots' samples share the wave
   int wpb = (int)((warps + num_sms - 1) / num_sms);
   wpb = wpb < 1 ? 1 : (wpb > 8 ? 8 : wpb);
   if (lps_out) *lps_out = lps;
   if (threads_out) *threads_out = wpb * 32;
+  if (spg_out) *spg_out = spg;
   return wpb * spw;
 }
 
@@ -498,21 +558,22 @@ cudaError_t launch_rollout(const RolloutArgs& a, int num_sms, cudaStream_t st) {
   if (a.model_kind == MODEL_GP) {
     int no = 0;
     for (int g = 0; g < a.model.G; ++g) no = a.model.g[g].n_out > no ? a.model.g[g].n_out : no;
-    int lps = 8, threads = 32;
-    const int spb = rollout_samples_per_block(a.K_local, num_sms, &lps, &threads);
+    int lps = 8, threads = 32, spg = 1;
+    const int spb = rollout_samples_per_block(a.K_local, a.B, num_sms, &lps, &threads, &spg);
     const long long items = (long long)a.B * ((a.K_local + spb - 1) / spb);
     // one block per SM: capping registers for a second resident block (122 instead of
     // ~200) costs more ILP than the extra warps recover (config2 0.34 -> 0.52 ms)
-    const long long blocks = items < num_sms ? items : num_sms;
+    const long long cap = (long long)GPM_ROLLOUT_MINB * num_sms;
+    const long long blocks = items < cap ? items : cap;
     using KF = void (*)(const RolloutArgs);
-    KF table[4][4] = {
-        {rollout_gp_kernel<2, 4>, rollout_gp_kernel<2, 8>, rollout_gp_kernel<2, 16>, rollout_gp_kernel<2, 32>},
-        {rollout_gp_kernel<4, 4>, rollout_gp_kernel<4, 8>, rollout_gp_kernel<4, 16>, rollout_gp_kernel<4, 32>},
-        {rollout_gp_kernel<6, 4>, rollout_gp_kernel<6, 8>, rollout_gp_kernel<6, 16>, rollout_gp_kernel<6, 32>},
-        {rollout_gp_kernel<8, 4>, rollout_gp_kernel<8, 8>, rollout_gp_kernel<8, 16>, rollout_gp_kernel<8, 32>}};
+#define GPM_ROW(NO, S) \
+  {rollout_gp_kernel<NO, 4, 1>, rollout_gp_kernel<NO, 8, S>, rollout_gp_kernel<NO, 16, S>, rollout_gp_kernel<NO, 32, S>}
+    KF table[2][4][4] = {{GPM_ROW(2, 1), GPM_ROW(4, 1), GPM_ROW(6, 1), GPM_ROW(8, 1)},
+                         {GPM_ROW(2, 2), GPM_ROW(4, 2), GPM_ROW(6, 2), GPM_ROW(8, 2)}};
+#undef GPM_ROW
     const int ni = no <= 2 ? 0 : no <= 4 ? 1 : no <= 6 ? 2 : 3;
     const int li = lps == 4 ? 0 : lps == 8 ? 1 : lps == 16 ? 2 : 3;
-    KF kern = table[ni][li];
+    KF kern = table[spg == 2 ? 1 : 0][ni][li];
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<(unsigned)blocks, threads, smem, st>>>(a);
