@@ -141,6 +141,65 @@ __device__ __forceinline__ void mma_block_3x(uint32_t d, uint64_t ahi, uint64_t 
         : "memory");
   }
 }
+// One 16-point A chunk: two K=8 steps (B blocks b0/b1) x 3xTF32 x one or two
+// 256-column pieces, then the three stage releases -- one elect and one operand
+// marshalling for 6 or 12 MMAs (the issuing warp's per-instruction overhead, not
+// the tensor pipe, bounded the kernel at one asm statement per MMA).
+__device__ __forceinline__ void mma_chunk_3x(uint32_t d, uint64_t ahi, uint64_t alo, uint64_t bh0, uint64_t bl0,
+                                             uint64_t bh1, uint64_t bl1, uint32_t idesc0, uint32_t idesc1,
+                                             uint32_t acc, int two, uint32_t bar_b0, uint32_t bar_b1,
+                                             uint32_t bar_a) {
+  if (two) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b32 d1;\n\t.reg .b64 ah1, al1, x0, y0, x1, y1;\n\t"
+        "add.u32 d1, %0, 256;\n\t"
+        "add.s64 ah1, %1, 16;\n\t"
+        "add.s64 al1, %2, 16;\n\t"
+        "add.s64 x0, %3, 512;\n\t"
+        "add.s64 y0, %4, 512;\n\t"
+        "add.s64 x1, %5, 512;\n\t"
+        "add.s64 y1, %6, 512;\n\t"
+        "setp.ne.b32 p, %9, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %3, %7, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %4, %7, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %7, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], %1, x0, %8, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], %1, y0, %8, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], %2, x0, %8, 1;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%10];\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah1, %5, %7, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah1, %6, %7, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al1, %5, %7, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], ah1, x1, %8, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], ah1, y1, %8, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], al1, x1, %8, 1;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%11];\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%12];\n\t}" ::"r"(d),
+        "l"(ahi), "l"(alo), "l"(bh0), "l"(bl0), "l"(bh1), "l"(bl1), "r"(idesc0), "r"(idesc1), "r"(acc),
+        "r"(bar_b0), "r"(bar_b1), "r"(bar_a)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 ah1, al1;\n\t"
+        "add.s64 ah1, %1, 16;\n\t"
+        "add.s64 al1, %2, 16;\n\t"
+        "setp.ne.b32 p, %8, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %3, %7, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %4, %7, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %7, 1;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%9];\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah1, %5, %7, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah1, %6, %7, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al1, %5, %7, 1;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%10];\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%11];\n\t}" ::"r"(d),
+        "l"(ahi), "l"(alo), "l"(bh0), "l"(bl0), "l"(bh1), "l"(bl1), "r"(idesc0), "r"(acc), "r"(bar_b0),
+        "r"(bar_b1), "r"(bar_a)
+        : "memory");
+  }
+}
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
@@ -197,6 +256,21 @@ __device__ __forceinline__ void mbar_wait_prof(uint32_t bar, uint32_t parity, in
   }
   prof_add(slot, clock64() - t0, dbg);
 }
+
+// Pipeline position in an n-stage ring: stage index + parity, advanced without
+// division (a runtime `%`/`/` per block cost ~30% of the MMA warp's issue time).
+struct Ring {
+  int s = 0;
+  uint32_t ph = 0;
+  int n;
+  __device__ explicit Ring(int stages) : n(stages) {}
+  __device__ __forceinline__ void next() {
+    if (++s == n) {
+      s = 0;
+      ph ^= 1u;
+    }
+  }
+};
 
 // chunks of pass p: every 16-point chunk whose rows can reach a column of the pass
 __device__ __forceinline__ int pass_chunks(int p, int np, int n_pad) {
@@ -281,15 +355,15 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
     // empty-slot wait and the copy issue.
     int nbt = 0;  // blocks per tile (same sequence for every tile)
     for (int p = 0; p < n_pass; ++p) nbt += 2 * pass_chunks(p, NP, n_pad);
-    uint32_t it = 0;
+    Ring rb(SB);
     int4 next = G.tc_meta[0];
     int ti = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++ti) {
       if (ti < 10) trace_at(48 + ti, dbg);
-      for (int kb = 0; kb < nbt; ++kb, ++it) {
+      for (int kb = 0; kb < nbt; ++kb, rb.next()) {
         {
-          const int s = it % SB;
-          const uint32_t ph = (it / SB) & 1;
+          const int s = rb.s;
+          const uint32_t ph = rb.ph;
           const int4 meta = next;
           next = G.tc_meta[kb + 1 < nbt ? kb + 1 : 0];
           if (!(dbg & 64)) mbar_wait_prof(smem_u32(&empty_b[s]), ph ^ 1, 0, dbg);
@@ -308,7 +382,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
     // descriptors live in uniform registers) and elect.sync picks the lane that
     // issues each tcgen05.mma / commit. A single-lane branch made every MMA a
     // waterfall of R2UR broadcasts (~780 cycles per 8-point block).
-    uint32_t ia = 0, ib = 0, uc = 0;
+    Ring ra(SA), rbb(SB);
+    uint32_t uc = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       for (int p = 0; p < n_pass; ++p, ++uc) {
         mbar_wait_prof(smem_u32(tempty), (uc & 1) ^ 1, 1, dbg & ~512);  // epilogue drained the accumulator
@@ -316,34 +391,48 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
         if (lane == 0 && uc < 10) trace_at(2 + 2 * (int)uc, dbg);
         const int nk = pass_chunks(p, NP, n_pad);
         const int npw = min(NP, n_pad - p * NP);
-        for (int kb = 0; kb < nk; ++kb, ++ia) {
-          const int sa = ia % SA;
-          if (!(dbg & 16)) mbar_wait(smem_u32(&full_a[sa]), (ia / SA) & 1);
+        for (int kb = 0; kb < nk; ++kb, ra.next()) {
+          const int sa = ra.s;
+          if (!(dbg & 16)) mbar_wait(smem_u32(&full_a[sa]), ra.ph);
           const uint32_t a_hi = smem_u32(sA + (size_t)sa * 2 * A_STAGE_FLOATS);
           const uint32_t a_lo = a_hi + A_STAGE_FLOATS * 4;
           const int col0 = max(0, kb * KC - p * NP);  // build_tc_operand's column start
           const int ncols = npw - col0;
-#pragma unroll
-          for (int kk = 0; kk < KC / KB; ++kk, ++ib) {  // one B block per K=8 step
-            const int sb = ib % SB;
-            if (!(dbg & 32)) mbar_wait(smem_u32(&full_b[sb]), (ib / SB) & 1);
+          if (!one_pass && !(dbg & 4)) {  // both B blocks of the chunk, then one statement
+            const int sb0 = rbb.s;
+            const uint32_t ph0 = rbb.ph;
+            rbb.next();
+            const int sb1 = rbb.s;
+            const uint32_t ph1 = rbb.ph;
+            rbb.next();
+            if (!(dbg & 32)) {
+              mbar_wait(smem_u32(&full_b[sb0]), ph0);
+              mbar_wait(smem_u32(&full_b[sb1]), ph1);
+            }
             // no tcgen05 fence here: the MMAs read smem through the async proxy, which
             // the bulk-copy completion and the producers' fence.proxy.async order
+            const uint32_t bh0 = smem_u32(sB + (size_t)sb0 * 2 * NP * KB);
+            const uint32_t bh1 = smem_u32(sB + (size_t)sb1 * 2 * NP * KB);
+            const uint32_t blen = (uint32_t)ncols * KB * 4;
+            mma_chunk_3x(tmem_base + (uint32_t)col0, smem_desc(a_hi), smem_desc(a_lo), smem_desc(bh0, SBO_B),
+                         smem_desc(bh0 + blen, SBO_B), smem_desc(bh1, SBO_B), smem_desc(bh1 + blen, SBO_B),
+                         instr_desc(min(256, ncols)), instr_desc(ncols > 256 ? ncols - 256 : 16),
+                         kb > 0 ? 1u : 0u, ncols > 256, smem_u32(&empty_b[sb0]), smem_u32(&empty_b[sb1]),
+                         smem_u32(&empty_a[sa]));
+            continue;
+          }
+#pragma unroll
+          for (int kk = 0; kk < KC / KB; ++kk, rbb.next()) {  // one B block per K=8 step
+            const int sb = rbb.s;
+            if (!(dbg & 32)) mbar_wait(smem_u32(&full_b[sb]), rbb.ph);
             const uint32_t b_hi = smem_u32(sB + (size_t)sb * 2 * NP * KB);
-            const uint32_t b_lo = b_hi + (uint32_t)ncols * KB * 4;
             const uint32_t aoff = kk * 256;  // two 16-byte K chunks per K=8 step
             const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
             if (!(dbg & 4)) {
               const uint32_t d = tmem_base + (uint32_t)col0;
-              if (!one_pass) {
-                mma_block_3x(d, smem_desc(a_hi + aoff), smem_desc(a_lo + aoff), smem_desc(b_hi, SBO_B),
-                             smem_desc(b_lo, SBO_B), instr_desc(min(256, ncols)),
-                             instr_desc(ncols > 256 ? ncols - 256 : 16), acc0, ncols > 256);
-              } else {
-                for (int c = 0; c < ncols; c += 256)
-                  mma_tf32(d + c, smem_desc(a_hi + aoff), smem_desc(b_hi + (uint32_t)(c / 8) * SBO_B, SBO_B),
-                           instr_desc(min(256, ncols - c)), acc0);
-              }
+              for (int c = 0; c < ncols; c += 256)
+                mma_tf32(d + c, smem_desc(a_hi + aoff), smem_desc(b_hi + (uint32_t)(c / 8) * SBO_B, SBO_B),
+                         instr_desc(min(256, ncols - c)), acc0);
             }
             mma_commit(smem_u32(&empty_b[sb]));  // B block free once these MMAs complete
           }
@@ -359,7 +448,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
     const int pw = warp - 8;
     const int m = (pw & 3) * 32 + lane;  // tile row == TMEM lane
     const int h = pw >> 2;
-    uint32_t it = 0;
+    Ring ra(SA);
     int ti = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++ti) {
       if (pw == 0 && lane == 0 && ti < 10) trace_at(36 + ti, dbg);
@@ -371,9 +460,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
       const float qn = valid ? -0.5f * L2E * (q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3) : -1e30f;
       for (int p = 0; p < n_pass; ++p) {
         const int nk = pass_chunks(p, NP, n_pad);
-        for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = it % SA;
-          const uint32_t ph = (it / SA) & 1;
+        for (int kb = 0; kb < nk; ++kb, ra.next()) {
+          const int s = ra.s;
+          const uint32_t ph = ra.ph;
           if (lane == 0 && !(dbg & 64)) mbar_wait_prof(smem_u32(&empty_a[s]), ph ^ 1, 4, dbg);
           __syncwarp();
           const unsigned long long tp0 = (dbg & 512) ? clock64() : 0ull;
@@ -384,11 +473,17 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
           for (int cc = 0; cc < 2; ++cc) {
             const int c = 2 * h + cc;
             float hi[4], lo[4];
+            const int i0 = kb * KC + c * 4;  // four consecutive points: one LDS.128 per input row
+            const float4 z0 = *reinterpret_cast<const float4*>(zs + i0);
+            const float4 z1 = *reinterpret_cast<const float4*>(zs + n_pad + i0);
+            const float4 z2 = *reinterpret_cast<const float4*>(zs + 2 * n_pad + i0);
+            const float4 z3 = *reinterpret_cast<const float4*>(zs + 3 * n_pad + i0);
+            const float4 zq = *reinterpret_cast<const float4*>(zs + 4 * n_pad + i0);
+            const float za[4][5] = {{z0.x, z1.x, z2.x, z3.x, zq.x}, {z0.y, z1.y, z2.y, z3.y, zq.y},
+                                    {z0.z, z1.z, z2.z, z3.z, zq.z}, {z0.w, z1.w, z2.w, z3.w, zq.w}};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              const int i = kb * KC + c * 4 + e;
-              float x = fmaf(q0, zs[i], fmaf(q1, zs[n_pad + i], fmaf(q2, zs[2 * n_pad + i],
-                             fmaf(q3, zs[3 * n_pad + i], qn + zs[4 * n_pad + i]))));
+              float x = fmaf(q0, za[e][0], fmaf(q1, za[e][1], fmaf(q2, za[e][2], fmaf(q3, za[e][3], qn + za[e][4]))));
               if (dbg & 2) x = -1e30f;
               const float kv = exp2f_approx(x);
               hi[e] = tf32_rna(kv);
