@@ -601,9 +601,15 @@ cudaError_t launch_tc_variance(const VarianceArgs& a, int one_pass, cudaStream_t
     const char* e = getenv("GPMPPI_TC_SB");
     sb_env = e ? atoi(e) : 0;
   }
-  int SA = tc::STAGES_A, SB = sb_env >= 2 ? sb_env : tc::STAGES_B + 1;
+  static int sa_env = -1;  // diagnostics: GPMPPI_TC_SA forces the A ring depth
+  if (sa_env < 0) {
+    const char* e = getenv("GPMPPI_TC_SA");
+    sa_env = e ? atoi(e) : 0;
+  }
+  int SA = sa_env >= 2 ? sa_env : tc::STAGES_A, SB = sb_env >= 2 ? sb_env : tc::STAGES_B + 1;
   while (sb_env < 2 && SB > tc::STAGES_B && tc_smem_bytes(a.g, SA, SB) > kSmemMax) --SB;
   while (SA > 2 && tc_smem_bytes(a.g, SA, SB) > kSmemMax) --SA;
+  if (sa_env >= 2) SA = std::min(SA, sa_env);
   while (SB > 2 && tc_smem_bytes(a.g, SA, SB) > kSmemMax) --SB;
   const size_t smem = tc_smem_bytes(a.g, SA, SB);
   cudaError_t e = cudaFuncSetAttribute(variance_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
