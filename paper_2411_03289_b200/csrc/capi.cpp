@@ -285,6 +285,12 @@ gpmppi_model* build_model(const double* X, const double* Y, int64_t n64, int64_t
         for (int d = 0; d < 4; ++d) zs32[(size_t)d * n + j] = (float)G.aug[(size_t)j * 6 + d];
       D.pts = M->upload(pts);
       D.ilt64 = M->upload(G.ilt);
+      {  // L^{-1} row-major: the tightening variance reads row j contiguously (coalesced)
+        std::vector<double> linv((size_t)n * n);
+        for (int i = 0; i < n; ++i)
+          for (int j = 0; j < n; ++j) linv[(size_t)j * n + i] = G.ilt[(size_t)i * n + j];
+        D.linv64 = M->upload(linv);
+      }
       D.ilt32 = M->upload(ilt32);
       D.zs32 = M->upload(zs32);
       {  // tensor-core operand (pre-tiled TF32 hi/lo L^{-T}, kernels_tc.cu)

@@ -15,6 +15,7 @@ namespace gpm {
 struct GroupDev {
   const double* pts;   // FP64 SoA [(5 + n_out)][ns]: zs0..zs3, zn(+ln sv), alpha_0..alpha_{n_out-1}
   const double* ilt64; // FP64 L^{-T} [n][n] row-major (upper triangular, zeros below)
+  const double* linv64; // FP64 L^{-1} [n][n] row-major (lower): row j = column j of L^{-T}
   const float* ilt32;  // FP32 copy of L^{-T}
   const float* zs32;   // FP32 scaled inputs [4][n]
   const float* tc_b;   // tensor-core operand: L^{-T} hi/lo TF32 tiles (see kernels_tc.cu)

@@ -169,7 +169,7 @@ GPM_D double group_sum(double v) {  // xor butterfly inside an LPS-lane group
 //          (mppi.cpp:343-346), per-step costs and flags (costs.cpp:127-171).
 // Per-sample trajectory scratch lives in L2 (scr, 9 arrays of T+1 doubles).
 constexpr int SCR_ARRAYS = 9;
-constexpr int kMaxSampleSlotsPerBlock = 128;  // groups per block (<= 64) x SPG (<= 2)
+constexpr int kMaxSampleSlotsPerBlock = 128;  // groups per block x SPG: <= 64 x 2, 8 x 4
 #ifndef GPM_ROLLOUT_MINB
 #define GPM_ROLLOUT_MINB 1
 #endif
@@ -523,6 +523,7 @@ int rollout_lanes_per_sample(int K, int num_sms) {
 int rollout_samples_per_group(int lps, long long total, int num_sms) {
   static const int forced = env_int("GPMPPI_SPG");
   if (lps == 4) return 1;
+  if (forced == 4) return lps == 32 ? 4 : 2;
   if (forced == 1 || forced == 2) return forced;
   // beyond one wave (>= 64 samples per SM) the rollout is FP64-throughput bound and
   // halving the LDS per FP64 op wins (config5 rollout 5.1 -> 3.7 ms); below it the
@@ -571,9 +572,13 @@ cudaError_t launch_rollout(const RolloutArgs& a, int num_sms, cudaStream_t st) {
     KF table[2][4][4] = {{GPM_ROW(2, 1), GPM_ROW(4, 1), GPM_ROW(6, 1), GPM_ROW(8, 1)},
                          {GPM_ROW(2, 2), GPM_ROW(4, 2), GPM_ROW(6, 2), GPM_ROW(8, 2)}};
 #undef GPM_ROW
+    // one 32-lane group per warp carrying four samples: no duplicate addresses inside a
+    // warp's Z/alpha loads, a quarter of the LDS instructions of the 8-lane layout
+    KF table4[4] = {rollout_gp_kernel<2, 32, 4>, rollout_gp_kernel<4, 32, 4>, rollout_gp_kernel<6, 32, 4>,
+                    rollout_gp_kernel<8, 32, 4>};
     const int ni = no <= 2 ? 0 : no <= 4 ? 1 : no <= 6 ? 2 : 3;
     const int li = lps == 4 ? 0 : lps == 8 ? 1 : lps == 16 ? 2 : 3;
-    KF kern = table[spg == 2 ? 1 : 0][ni][li];
+    KF kern = spg == 4 ? table4[ni] : table[spg == 2 ? 1 : 0][ni][li];
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<(unsigned)blocks, threads, smem, st>>>(a);
@@ -1058,7 +1063,7 @@ cudaError_t launch_predict(const ModelDev& m, const double* q, long long S, doub
 // one block), then every step's GP variance and Jacobian in parallel (one block
 // per (step, group, column slice)), then the 5×5 covariance recursion and the
 // thresholds (one warp).
-constexpr int TIGHT_COLS = 256;  // columns of L^{-T} per variance block
+constexpr int TIGHT_ROWS = 64;  // rows of L^{-1} per variance block
 
 // Belief-mean chain. The GP query of step k needs only (v_k, omega_k, u_k) and
 // the lag update of (v, omega) is cheap, so the serial part carries (v, omega)
@@ -1219,10 +1224,12 @@ __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const Tight
   }
 }
 
-// grid (T, G, ceil(n / TIGHT_COLS)): partial ||L^{-1} k*||^2 over a column slice.
-__global__ void __launch_bounds__(TIGHT_COLS) tighten_var_kernel(const TightenArgs a) {
+// grid (T, G*B, ceil(n / TIGHT_ROWS)): partial ||L^{-1} k*||^2 over a slice of rows of
+// L^{-1}. One warp per row: a_j = sum_{i<=j} k_i L^{-1}[j][i] with the lanes striding
+// the contiguous row (coalesced), then a_j^2 (gp.cpp:184-191).
+__global__ void __launch_bounds__(256) tighten_var_kernel(const TightenArgs a) {
   extern __shared__ __align__(16) double kst[];
-  __shared__ double red[TIGHT_COLS / 32];
+  __shared__ double red[8];
   const int k = blockIdx.x, g = blockIdx.y % a.model.G, rb = blockIdx.y / a.model.G, c = blockIdx.z;
   const int n = a.model.n;
   if (a.model_kind != MODEL_GP) return;
@@ -1230,32 +1237,32 @@ __global__ void __launch_bounds__(TIGHT_COLS) tighten_var_kernel(const TightenAr
   const double* q = a.tq + (size_t)rb * 4 * a.T + k * 4;
   const double q0 = q[0] / G.ls[0], q1 = q[1] / G.ls[1], q2 = q[2] / G.ls[2], q3 = q[3] / G.ls[3];
   const double qn = -0.5 * (q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
-  const int j0 = c * TIGHT_COLS;
-  const int jend = min(n, j0 + TIGHT_COLS);
+  const int j0 = c * TIGHT_ROWS;
+  const int jend = min(n, j0 + TIGHT_ROWS);
   const double* p = G.pts;
   const int ns = a.model.ns;
-  for (int i = threadIdx.x; i < jend; i += blockDim.x)  // rows i <= j only
+  for (int i = threadIdx.x; i < jend; i += blockDim.x)  // columns i <= j only
     kst[i] = exp(q0 * p[i] + q1 * p[ns + i] + q2 * p[2 * ns + i] + q3 * p[3 * ns + i] + qn + p[4 * ns + i]);
   __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   double ssq = 0.0;
-  const int j = j0 + threadIdx.x;
-  if (j < n) {
-    double a0 = 0.0, a1 = 0.0;  // a_j = Σ_{i<=j} k_i L^{-T}[i][j]  (gp.cpp:184-185)
-    int i = 0;
-    for (; i + 1 <= j; i += 2) {
-      a0 = fma(kst[i], G.ilt64[(size_t)i * n + j], a0);
-      a1 = fma(kst[i + 1], G.ilt64[(size_t)(i + 1) * n + j], a1);
+  for (int j = j0 + w; j < jend; j += 8) {
+    const double* row = G.linv64 + (size_t)j * n;
+    double a0 = 0.0, a1 = 0.0;
+    int i = lane;
+    for (; i + 32 <= j; i += 64) {
+      a0 = fma(kst[i], __ldg(row + i), a0);
+      a1 = fma(kst[i + 32], __ldg(row + i + 32), a1);
     }
-    if (i <= j) a0 = fma(kst[i], G.ilt64[(size_t)i * n + j], a0);
-    const double aj = a0 + a1;
-    ssq = aj * aj;
+    if (i <= j) a0 = fma(kst[i], __ldg(row + i), a0);
+    const double aj = warp_sum(a0 + a1);
+    ssq = fma(aj, aj, ssq);
   }
-  ssq = warp_sum(ssq);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ssq;
+  if (lane == 0) red[w] = ssq;
   __syncthreads();
   if (threadIdx.x == 0) {
     double s = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    for (int i = 0; i < 8; ++i) s += red[i];
     a.tvar_part[(((size_t)rb * a.T + k) * a.model.G + g) * gridDim.z + c] = s;
   }
 }
@@ -1271,7 +1278,6 @@ __global__ void __launch_bounds__(32) tighten_cov_kernel(const TightenArgs a, in
   double* arbar = a.r_bar + (size_t)rb * BatchStrides::rbar(a.T);
   double* amarg = a.margins + (size_t)rb * BatchStrides::marg(a.T);
   extern __shared__ __align__(16) double csm[];  // [T][25] J, [T][2] cv, [T+1][5] mu
-  __shared__ double S[25], JS[25], C[25];
   __shared__ int infeasible;
   const int l = threadIdx.x;
   const TaskDev& t = a.task[rb];
@@ -1307,35 +1313,33 @@ __global__ void __launch_bounds__(32) tighten_cov_kernel(const TightenArgs a, in
     cvs[2 * k] = c0;
     cvs[2 * k + 1] = c1;
   }
-  if (l < 25) S[l] = 0.0;
   if (l == 0) infeasible = 0;
   double* Ss = mus + 5 * (T + 1);  // [T][25] propagated covariances
   __syncwarp();
-  const int i5 = l / 5, j5 = l % 5;
+  // lane l < 25 owns Σ[i5][j5] in a register; the two 5-term products per step pull
+  // their operands with shuffles (no shared-memory round trips on the serial chain)
+  const int i5 = l < 25 ? l / 5 : 4, j5 = l < 25 ? l % 5 : 4;
+  double Sr = 0.0;
   for (int k = 0; k < a.T; ++k) {  // Σ' = J Σ Jᵀ + diag(0,0,0,cv0,cv1), symmetrised (uncertainty.cpp:83-87)
     const double* J = Js + 25 * k;
-    const double* cv = cvs + 2 * k;
-    if (l < 25) {
-      double s = 0.0;
-      for (int q = 0; q < 5; ++q) s += J[i5 * 5 + q] * S[q * 5 + j5];
-      JS[l] = s;
+    double Ji[5], Jj[5];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      Ji[q] = J[i5 * 5 + q];
+      Jj[q] = J[j5 * 5 + q];
     }
-    __syncwarp();
-    if (l < 25) {
-      double s = 0.0;
-      for (int q = 0; q < 5; ++q) s += JS[i5 * 5 + q] * J[j5 * 5 + q];
-      if (l == 18) s += cv[0];
-      if (l == 24) s += cv[1];
-      C[l] = s;
-    }
-    __syncwarp();
-    if (l < 25) {
-      const double v = 0.5 * (C[i5 * 5 + j5] + C[j5 * 5 + i5]);
-      S[l] = v;
-      Ss[k * 25 + l] = v;
-    }
-    __syncwarp();
+    double js = 0.0;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) js = fma(Ji[q], __shfl_sync(0xffffffffu, Sr, q * 5 + j5), js);
+    double c = 0.0;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) c = fma(__shfl_sync(0xffffffffu, js, i5 * 5 + q), Jj[q], c);
+    if (l == 18) c += cvs[2 * k];
+    if (l == 24) c += cvs[2 * k + 1];
+    Sr = 0.5 * (c + __shfl_sync(0xffffffffu, c, j5 * 5 + i5));
+    if (l < 25) Ss[k * 25 + l] = Sr;
   }
+  __syncwarp();
   for (int i = l; i < 25 * T; i += 32) ahcov[i] = Ss[i];
   for (int k = l; k < T; k += 32) {  // tighten_lane_radius (uncertainty.cpp:90-96), parallel in k
     if (t.kind == TASK_AVOIDANCE) break;
@@ -1378,7 +1382,7 @@ __global__ void __launch_bounds__(32) tighten_cov_kernel(const TightenArgs a, in
   if (l == 0) a.infeasible[rb] = infeasible;
 }
 
-int tighten_splits(int n) { return n > 0 ? (n + TIGHT_COLS - 1) / TIGHT_COLS : 1; }
+int tighten_splits(int n) { return n > 0 ? (n + TIGHT_ROWS - 1) / TIGHT_ROWS : 1; }
 
 cudaError_t launch_tighten(const TightenArgs& a, cudaStream_t st) {
   size_t msm = sizeof(double) * (size_t)(2 * a.T + 3 * (a.T + 1) + 2 * a.T + 1);
@@ -1395,7 +1399,7 @@ cudaError_t launch_tighten(const TightenArgs& a, cudaStream_t st) {
   const int ns = a.model_kind == MODEL_GP ? tighten_splits(a.model.n) : 1;
   const size_t smem = sizeof(double) * (size_t)(a.model.n > 0 ? a.model.n : 1);
   cudaFuncSetAttribute(tighten_var_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (a.model_kind == MODEL_GP) tighten_var_kernel<<<dim3(a.T, G * a.B, ns), TIGHT_COLS, smem, st>>>(a);
+  if (a.model_kind == MODEL_GP) tighten_var_kernel<<<dim3(a.T, G * a.B, ns), 256, smem, st>>>(a);
   const size_t csmem = sizeof(double) * (size_t)(25 * a.T + 2 * a.T + 5 * (a.T + 1) + 25 * a.T);
   cudaFuncSetAttribute(tighten_cov_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem);
   tighten_cov_kernel<<<a.B, 32, csmem, st>>>(a, ns);
