@@ -1117,8 +1117,8 @@ __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const Tight
   // reference's division) to keep FP64 divides off the serial path.
   __shared__ double red[2][TMEAN_THREADS / 32][kMaxGroups * NO];
   __shared__ double gil[kMaxGroups][4];       // reciprocal lengthscales
-  __shared__ double gwt[kMaxGroups][NO];      // terrain weight of each output
-  __shared__ int gch[kMaxGroups][NO];         // 0: v channel, 1: omega channel, -1: unused
+  __shared__ double gw0[kMaxGroups][NO];      // terrain weight of each v-channel output, else 0
+  __shared__ double gw1[kMaxGroups][NO];      // terrain weight of each omega-channel output, else 0
   __shared__ int gno[kMaxGroups];
   const int nwarps = blockDim.x >> 5;
   const int ns = a.model.ns;
@@ -1130,8 +1130,8 @@ __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const Tight
       for (int o = 0; o < NO; ++o) {
         const bool used = o < a.model.g[g].n_out;
         const int gi = used ? a.model.g[g].out_idx[o] : 0;
-        gwt[g][o] = used ? tw[gi >> 1] : 0.0;
-        gch[g][o] = used ? (gi & 1) : -1;
+        gw0[g][o] = (used && !(gi & 1)) ? tw[gi >> 1] : 0.0;
+        gw1[g][o] = (used && (gi & 1)) ? tw[gi >> 1] : 0.0;
       }
     }
   }
@@ -1157,24 +1157,49 @@ __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const Tight
           for (int o = 0; o < NO; ++o)
             if (o < no) acc[o] = fma(kj, p[(5 + o) * ns + j], acc[o]);
         }
+        {  // transpose-reduce the NO (<= 8) sums across the warp: 9 double shuffles
+           // instead of 5 per output; lane 4*o ends with the warp total of output o
+          double v8[8];
 #pragma unroll
-        for (int o = 0; o < NO; ++o) {
-          const double sm = warp_sum(acc[o]);
-          if (lane == 0) red[k & 1][w][g * NO + o] = sm;
+          for (int o = 0; o < 8; ++o) v8[o] = o < NO ? acc[o] : 0.0;
+          const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+          double w4[4], w2[2];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const double send = b4 ? v8[i] : v8[i + 4];
+            w4[i] = (b4 ? v8[i + 4] : v8[i]) + __shfl_xor_sync(0xffffffffu, send, 16);
+          }
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const double send = b3 ? w4[i] : w4[i + 2];
+            w2[i] = (b3 ? w4[i + 2] : w4[i]) + __shfl_xor_sync(0xffffffffu, send, 8);
+          }
+          double y = (b2 ? w2[1] : w2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? w2[0] : w2[1], 4);
+          y += __shfl_xor_sync(0xffffffffu, y, 2);
+          y += __shfl_xor_sync(0xffffffffu, y, 1);
+          const int o = (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);
+          if ((lane & 3) == 0 && o < NO) red[k & 1][w][g * NO + o] = y;
         }
         p += (size_t)(5 + no) * ns;
       }
       __syncthreads();
       for (int g = 0; g < G; ++g) {
+        // every thread sums the per-warp partials in warp order (identical bits
+        // everywhere), loads first so the 4 x NO shared reads overlap; the channel
+        // weights are zero for the other channel, so one FMA chain per channel keeps
+        // the ascending-output order without branches (ensemble_combine)
+        double part[TMEAN_THREADS / 32][NO];
+#pragma unroll
+        for (int q = 0; q < TMEAN_THREADS / 32; ++q)
+#pragma unroll
+          for (int o = 0; o < NO; ++o) part[q][o] = red[k & 1][q][g * NO + o];
 #pragma unroll
         for (int o = 0; o < NO; ++o) {
-          // full 32-lane butterfly: every lane of every warp ends with the same bits
-          const double x = warp_sum(lane < nwarps ? red[k & 1][lane][g * NO + o] : 0.0);
-          const int ch = gch[g][o];
-          if (ch == 1)
-            c1 += gwt[g][o] * x;  // ensemble_combine, ascending terrains
-          else if (ch == 0)
-            c0 += gwt[g][o] * x;
+          double x = part[0][o];
+#pragma unroll
+          for (int q = 1; q < TMEAN_THREADS / 32; ++q) x += part[q][o];
+          c0 = fma(gw0[g][o], x, c0);
+          c1 = fma(gw1[g][o], x, c1);
         }
       }
     }
