@@ -1292,8 +1292,10 @@ __global__ void __launch_bounds__(256) tighten_var_kernel(const TightenArgs a) {
   }
 }
 
-// one warp: Σ_{k+1} = J Σ Jᵀ + diag(0,0,0,cv0,cv1), symmetrised; r̄_k and margins.
-__global__ void __launch_bounds__(32) tighten_cov_kernel(const TightenArgs a, int nsplit) {
+// 256 threads stage J / mu / the per-step correction variances, warp 0 runs the
+// serial recursion Σ_{k+1} = J Σ Jᵀ + diag(0,0,0,cv0,cv1) (symmetrised), then all
+// threads evaluate r̄_k and the margins in parallel.
+__global__ void __launch_bounds__(256) tighten_cov_kernel(const TightenArgs a, int nsplit) {
   const int rb = blockIdx.x;  // robot
   const double* atJ = a.tJ + (size_t)rb * 25 * a.T;
   const double* atmu = a.tmu + (size_t)rb * 5 * (a.T + 1);
@@ -1304,69 +1306,84 @@ __global__ void __launch_bounds__(32) tighten_cov_kernel(const TightenArgs a, in
   double* amarg = a.margins + (size_t)rb * BatchStrides::marg(a.T);
   extern __shared__ __align__(16) double csm[];  // [T][25] J, [T][2] cv, [T+1][5] mu
   __shared__ int infeasible;
+  __shared__ int gof[2 * kMaxTerrains];  // kernel group of each GP output
   const int l = threadIdx.x;
+  const int nt = blockDim.x;
   const TaskDev& t = a.task[rb];
   const int T = a.T;
   double* Js = csm;
   double* cvs = csm + 25 * T;
   double* mus = cvs + 2 * T;
-  for (int i = l; i < 25 * T; i += 32) Js[i] = atJ[i];
-  for (int i = l; i < 5 * (T + 1); i += 32) mus[i] = atmu[i];
+  for (int i = l; i < 25 * T; i += nt) Js[i] = atJ[i];
+  for (int i = l; i < 5 * (T + 1); i += nt) mus[i] = atmu[i];
+  const int G = a.model_kind == MODEL_GP ? a.model.G : 0;
+  if (l == 0) {
+    infeasible = 0;
+    for (int g = 0; g < G; ++g)
+      for (int o = 0; o < a.model.g[g].n_out; ++o) gof[a.model.g[g].out_idx[o]] = g;
+  }
+  __syncthreads();
   // per-step combined correction variance (gp.cpp:187-191 + ensemble_combine gp.cpp:380-386)
-  for (int k = l; k < T; k += 32) {
+  for (int k = l; k < T; k += nt) {
     double c0 = 0.0, c1 = 0.0;
-    if (a.model_kind == MODEL_GP) {
+    if (G > 0) {
       double vg[kMaxGroups];
-      for (int g = 0; g < a.model.G; ++g) {
-        double s = 0.0;
-        for (int c = 0; c < nsplit; ++c) s += atvar[((size_t)k * a.model.G + g) * nsplit + c];
-        const double v = a.model.g[g].sv - s;
+#pragma unroll
+      for (int g = 0; g < kMaxGroups; ++g) {
+        double v = 0.0;
+        if (g < G) {
+          double s = 0.0;
+          for (int c = 0; c < nsplit; ++c) s += atvar[((size_t)k * G + g) * nsplit + c];
+          v = a.model.g[g].sv - s;
+        }
         vg[g] = v > 0.0 ? v : 0.0;
       }
       for (int i = 0; i < a.R; ++i) {
         const double wi = atw[i];
-        int g0 = 0, g1 = 0;
-        for (int g = 0; g < a.model.G; ++g)
-          for (int o = 0; o < a.model.g[g].n_out; ++o) {
-            if (a.model.g[g].out_idx[o] == 2 * i) g0 = g;
-            if (a.model.g[g].out_idx[o] == 2 * i + 1) g1 = g;
-          }
-        c0 += wi * wi * vg[g0];
-        c1 += wi * wi * vg[g1];
+        const int g0 = gof[2 * i], g1 = gof[2 * i + 1];
+        double v0 = vg[0], v1 = vg[0];  // register select (no local-memory indexing)
+#pragma unroll
+        for (int g = 1; g < kMaxGroups; ++g) {
+          v0 = g0 == g ? vg[g] : v0;
+          v1 = g1 == g ? vg[g] : v1;
+        }
+        c0 += wi * wi * v0;
+        c1 += wi * wi * v1;
       }
     }
     cvs[2 * k] = c0;
     cvs[2 * k + 1] = c1;
   }
-  if (l == 0) infeasible = 0;
   double* Ss = mus + 5 * (T + 1);  // [T][25] propagated covariances
-  __syncwarp();
-  // lane l < 25 owns Σ[i5][j5] in a register; the two 5-term products per step pull
-  // their operands with shuffles (no shared-memory round trips on the serial chain)
-  const int i5 = l < 25 ? l / 5 : 4, j5 = l < 25 ? l % 5 : 4;
-  double Sr = 0.0;
-  for (int k = 0; k < a.T; ++k) {  // Σ' = J Σ Jᵀ + diag(0,0,0,cv0,cv1), symmetrised (uncertainty.cpp:83-87)
-    const double* J = Js + 25 * k;
-    double Ji[5], Jj[5];
+  __syncthreads();
+  if (l < 32) {  // warp 0: the serial recursion
+    // lane l < 25 owns Σ[i5][j5] in a register; the two 5-term products per step pull
+    // their operands with shuffles (no shared-memory round trips on the serial chain)
+    const int i5 = l < 25 ? l / 5 : 4, j5 = l < 25 ? l % 5 : 4;
+    double Sr = 0.0;
+    for (int k = 0; k < a.T; ++k) {  // Σ' = J Σ Jᵀ + diag(0,0,0,cv0,cv1), symmetrised (uncertainty.cpp:83-87)
+      const double* J = Js + 25 * k;
+      double Ji[5], Jj[5];
 #pragma unroll
-    for (int q = 0; q < 5; ++q) {
-      Ji[q] = J[i5 * 5 + q];
-      Jj[q] = J[j5 * 5 + q];
+      for (int q = 0; q < 5; ++q) {
+        Ji[q] = J[i5 * 5 + q];
+        Jj[q] = J[j5 * 5 + q];
+      }
+      double js = 0.0;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) js = fma(Ji[q], __shfl_sync(0xffffffffu, Sr, q * 5 + j5), js);
+      double c = 0.0;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) c = fma(__shfl_sync(0xffffffffu, js, i5 * 5 + q), Jj[q], c);
+      if (l == 18) c += cvs[2 * k];
+      if (l == 24) c += cvs[2 * k + 1];
+      Sr = 0.5 * (c + __shfl_sync(0xffffffffu, c, j5 * 5 + i5));
+      if (l < 25) Ss[k * 25 + l] = Sr;
     }
-    double js = 0.0;
-#pragma unroll
-    for (int q = 0; q < 5; ++q) js = fma(Ji[q], __shfl_sync(0xffffffffu, Sr, q * 5 + j5), js);
-    double c = 0.0;
-#pragma unroll
-    for (int q = 0; q < 5; ++q) c = fma(__shfl_sync(0xffffffffu, js, i5 * 5 + q), Jj[q], c);
-    if (l == 18) c += cvs[2 * k];
-    if (l == 24) c += cvs[2 * k + 1];
-    Sr = 0.5 * (c + __shfl_sync(0xffffffffu, c, j5 * 5 + i5));
-    if (l < 25) Ss[k * 25 + l] = Sr;
   }
-  __syncwarp();
-  for (int i = l; i < 25 * T; i += 32) ahcov[i] = Ss[i];
-  for (int k = l; k < T; k += 32) {  // tighten_lane_radius (uncertainty.cpp:90-96), parallel in k
+  __syncthreads();
+  for (int i = l; i < 25 * T; i += nt) ahcov[i] = Ss[i];
+  for (int k = l; k < T; k += nt) {  // tighten_lane_radius (uncertainty.cpp:90-96), parallel in k
     if (t.kind == TASK_AVOIDANCE) break;
     const double* Sk = Ss + 25 * k;
     const double c00 = Sk[0], c01 = Sk[1], c10 = Sk[5], c11 = Sk[6];
@@ -1379,7 +1396,7 @@ __global__ void __launch_bounds__(32) tighten_cov_kernel(const TightenArgs a, in
     if (r <= 0.0) atomicOr(&infeasible, 1);
   }
   if (t.kind != TASK_TRACKING)  // tighten_obstacle_distance (uncertainty.cpp:98-116), parallel in (k, o)
-    for (int idx = l; idx < T * t.n_obs; idx += 32) {
+    for (int idx = l; idx < T * t.n_obs; idx += nt) {
       const int k = idx / t.n_obs, o = idx % t.n_obs;
       const double* Sk = Ss + 25 * k;
       const double c00 = Sk[0], c01 = Sk[1], c10 = Sk[5], c11 = Sk[6];
@@ -1403,7 +1420,7 @@ __global__ void __launch_bounds__(32) tighten_cov_kernel(const TightenArgs a, in
       amarg[(size_t)k * t.n_obs + o] = d - dbar;
       if (dbar <= 0.0) atomicOr(&infeasible, 1);
     }
-  __syncwarp();
+  __syncthreads();
   if (l == 0) a.infeasible[rb] = infeasible;
 }
 
@@ -1427,7 +1444,7 @@ cudaError_t launch_tighten(const TightenArgs& a, cudaStream_t st) {
   if (a.model_kind == MODEL_GP) tighten_var_kernel<<<dim3(a.T, G * a.B, ns), 256, smem, st>>>(a);
   const size_t csmem = sizeof(double) * (size_t)(25 * a.T + 2 * a.T + 5 * (a.T + 1) + 25 * a.T);
   cudaFuncSetAttribute(tighten_cov_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem);
-  tighten_cov_kernel<<<a.B, 32, csmem, st>>>(a, ns);
+  tighten_cov_kernel<<<a.B, 256, csmem, st>>>(a, ns);
   count_launch(3);
   return cudaGetLastError();
 }
