@@ -173,6 +173,106 @@ constexpr int kMaxSampleSlotsPerBlock = 128;  // groups per block x SPG: <= 64 x
 #ifndef GPM_ROLLOUT_MINB
 #define GPM_ROLLOUT_MINB 1
 #endif
+// Phase 2 of one sample (lanes split the steps): heading recursion, FP64 sincos /
+// exact-arc increments, x/y in step order, non-finite freeze (mppi.cpp:343-346),
+// per-step costs and flags (costs.cpp:127-171); scr holds the sample's phase-1 chain.
+template <int LPS>
+GPM_D void rollout_phase2(const RolloutArgs& a, const SmemView& sv, const TaskDev& task, double* scr,
+                          const double* x0, int T, int stride, int gl, bool valid, long long sl, int O) {
+  double* su0 = scr;
+  double* su1 = scr + stride;
+  double* sv_ = scr + 2 * stride;
+  double* sw = scr + 3 * stride;
+  double* sth = scr + 4 * stride;
+  double* ssin = scr + 5 * stride;
+  double* scos = scr + 6 * stride;
+  double* sx = scr + 7 * stride;
+  double* sy = scr + 8 * stride;
+  (void)su1;
+  // ---------------- phase 2a: heading recursion (arc_advance: theta = wrap(theta + omega dt))
+  if (gl == 0) {
+    double th = x0[2];
+    sth[0] = th;
+    for (int k = 0; k < T; ++k) {
+      th = wrap_angle(th + sw[k] * a.nom.dt);
+      sth[k + 1] = th;
+    }
+  }
+  __syncwarp();
+  // ---------------- phase 2b: sincos and exact-arc increments, lanes split the steps
+  for (int k = gl; k < T; k += LPS) {
+    const double th = sth[k], vk = sv_[k], wk = sw[k];
+    double sp, cp;
+    sincos(th, &sp, &cp);
+    ssin[k] = sp;
+    scos[k] = cp;
+    double dx = 0.0, dy = 0.0, t2 = th;
+    arc_advance(dx, dy, t2, vk, 0.0, wk, a.nom.dt, sp, cp);
+    sx[k + 1] = dx;
+    sy[k + 1] = dy;
+  }
+  __syncwarp();
+  // ---------------- phase 2c: positions in step order + first non-finite state
+  int kd = T;  // states k > kd are frozen at state kd (mppi.cpp:343-346)
+  if (gl == 0) {
+    double x = x0[0], y = x0[1];
+    sx[0] = x;
+    sy[0] = y;
+    for (int k = 0; k < T; ++k) {
+      x += sx[k + 1];
+      y += sy[k + 1];
+      sx[k + 1] = x;
+      sy[k + 1] = y;
+      if (kd == T && !(isfinite(x) && isfinite(y) && isfinite(sth[k + 1]) && isfinite(sv_[k + 1]) &&
+                       isfinite(sw[k + 1])))
+        kd = k;
+    }
+  }
+  kd = __shfl_sync(0xffffffffu, kd, (threadIdx.x & 31) & ~(LPS - 1));
+  __syncwarp();
+  // ---------------- phase 2d: per-step costs and flags (costs.cpp:127-171), lanes split the steps
+  double cost = 0.0;
+  for (int wd = 0; wd < a.words; ++wd) {
+    uint32_t vb = 0, cb = 0;
+    const int kend = min(T, 32 * wd + 32);
+    for (int k = 32 * wd + gl; k < kend; k += LPS) {
+      const int ip = min(k, kd), in = min(k + 1, kd);
+      const double prev[5] = {sx[ip], sy[ip], sth[ip], sv_[ip], sw[ip]};
+      const double next[5] = {sx[in], sy[in], sth[in], sv_[in], sw[in]};
+      double decay = 1.0;  // 0.9^k by repeated multiplication, as costs.cpp:146
+      for (int i = 0; i < k; ++i) decay *= 0.9;
+      const StepCost c = step_cost(task, prev, next, ssin[ip], scos[ip], sv.rbar[k],
+                                   sv.marg + (size_t)k * O, su0[k], decay);
+      cost += c.cost;
+      vb |= (uint32_t)c.viol << (k & 31);
+      cb |= (uint32_t)c.coll << (k & 31);
+    }
+#pragma unroll
+    for (int o = LPS / 2; o > 0; o >>= 1) {
+      vb |= __shfl_xor_sync(0xffffffffu, vb, o);
+      cb |= __shfl_xor_sync(0xffffffffu, cb, o);
+    }
+    if (valid && gl == 0) {
+      a.viol_bits[(size_t)sl * a.words + wd] = vb;
+      a.coll_bits[(size_t)sl * a.words + wd] = cb;
+    }
+  }
+  cost = group_sum<LPS>(cost);
+  const bool alive = valid && kd == T;
+  bool term = false;
+  if (task.kind == TASK_AVOIDANCE) {  // costs.cpp:169 terminal_cost
+    const int il = min(T, kd);
+    const double gx = sx[il] - task.goal[0], gy = sy[il] - task.goal[1];
+    term = sqrt(gx * gx + gy * gy) <= task.goal[2];
+    cost += task.aw[3] * (term ? 0.0 : task.high_cost);
+  }
+  if (valid && gl == 0) {
+    a.cost_mean[sl] = alive ? cost : __longlong_as_double(0x7ff8000000000000LL);
+    a.term[sl] = term;
+    a.alive[sl] = alive;
+  }
+}
+
 template <int NO, int LPS, int SPG>
 __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const RolloutArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -330,99 +430,7 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
     }
     __syncwarp();
     for (int j = 0; j < SPG; ++j) {  // phase 2, one sample after the other
-      double* scr = scr0 + (size_t)j * SCR_ARRAYS * stride;
-      double* su0 = scr;
-      double* su1 = scr + stride;
-      double* sv_ = scr + 2 * stride;
-      double* sw = scr + 3 * stride;
-      double* sth = scr + 4 * stride;
-      double* ssin = scr + 5 * stride;
-      double* scos = scr + 6 * stride;
-      double* sx = scr + 7 * stride;
-      double* sy = scr + 8 * stride;
-      (void)su1;
-      // ---------------- phase 2a: heading recursion (arc_advance: theta = wrap(theta + omega dt))
-      if (gl == 0) {
-        double th = x0[2];
-        sth[0] = th;
-        for (int k = 0; k < T; ++k) {
-          th = wrap_angle(th + sw[k] * a.nom.dt);
-          sth[k + 1] = th;
-        }
-      }
-      __syncwarp();
-      // ---------------- phase 2b: sincos and exact-arc increments, lanes split the steps
-      for (int k = gl; k < T; k += LPS) {
-        const double th = sth[k], vk = sv_[k], wk = sw[k];
-        double sp, cp;
-        sincos(th, &sp, &cp);
-        ssin[k] = sp;
-        scos[k] = cp;
-        double dx = 0.0, dy = 0.0, t2 = th;
-        arc_advance(dx, dy, t2, vk, 0.0, wk, a.nom.dt, sp, cp);
-        sx[k + 1] = dx;
-        sy[k + 1] = dy;
-      }
-      __syncwarp();
-      // ---------------- phase 2c: positions in step order + first non-finite state
-      int kd = T;  // states k > kd are frozen at state kd (mppi.cpp:343-346)
-      if (gl == 0) {
-        double x = x0[0], y = x0[1];
-        sx[0] = x;
-        sy[0] = y;
-        for (int k = 0; k < T; ++k) {
-          x += sx[k + 1];
-          y += sy[k + 1];
-          sx[k + 1] = x;
-          sy[k + 1] = y;
-          if (kd == T && !(isfinite(x) && isfinite(y) && isfinite(sth[k + 1]) && isfinite(sv_[k + 1]) &&
-                           isfinite(sw[k + 1])))
-            kd = k;
-        }
-      }
-      kd = __shfl_sync(0xffffffffu, kd, (threadIdx.x & 31) & ~(LPS - 1));
-      __syncwarp();
-      // ---------------- phase 2d: per-step costs and flags (costs.cpp:127-171), lanes split the steps
-      double cost = 0.0;
-      for (int wd = 0; wd < a.words; ++wd) {
-        uint32_t vb = 0, cb = 0;
-        const int kend = min(T, 32 * wd + 32);
-        for (int k = 32 * wd + gl; k < kend; k += LPS) {
-          const int ip = min(k, kd), in = min(k + 1, kd);
-          const double prev[5] = {sx[ip], sy[ip], sth[ip], sv_[ip], sw[ip]};
-          const double next[5] = {sx[in], sy[in], sth[in], sv_[in], sw[in]};
-          double decay = 1.0;  // 0.9^k by repeated multiplication, as costs.cpp:146
-          for (int i = 0; i < k; ++i) decay *= 0.9;
-          const StepCost c = step_cost(task, prev, next, ssin[ip], scos[ip], sv.rbar[k],
-                                       sv.marg + (size_t)k * O, su0[k], decay);
-          cost += c.cost;
-          vb |= (uint32_t)c.viol << (k & 31);
-          cb |= (uint32_t)c.coll << (k & 31);
-        }
-#pragma unroll
-        for (int o = LPS / 2; o > 0; o >>= 1) {
-          vb |= __shfl_xor_sync(0xffffffffu, vb, o);
-          cb |= __shfl_xor_sync(0xffffffffu, cb, o);
-        }
-        if (valid[j] && gl == 0) {
-          a.viol_bits[(size_t)sl[j] * a.words + wd] = vb;
-          a.coll_bits[(size_t)sl[j] * a.words + wd] = cb;
-        }
-      }
-      cost = group_sum<LPS>(cost);
-      const bool alive = valid[j] && kd == T;
-      bool term = false;
-      if (task.kind == TASK_AVOIDANCE) {  // costs.cpp:169 terminal_cost
-        const int il = min(T, kd);
-        const double gx = sx[il] - task.goal[0], gy = sy[il] - task.goal[1];
-        term = sqrt(gx * gx + gy * gy) <= task.goal[2];
-        cost += task.aw[3] * (term ? 0.0 : task.high_cost);
-      }
-      if (valid[j] && gl == 0) {
-        a.cost_mean[sl[j]] = alive ? cost : __longlong_as_double(0x7ff8000000000000LL);
-        a.term[sl[j]] = term;
-        a.alive[sl[j]] = alive;
-      }
+      rollout_phase2<LPS>(a, sv, task, scr0 + (size_t)j * SCR_ARRAYS * stride, x0, T, stride, gl, valid[j], sl[j], O);
       __syncwarp();
     }
   }
