@@ -559,6 +559,13 @@ struct gpmppi_planner {
   double* h_out = nullptr;         // [B][16]
   int* h_infeasible = nullptr;     // [B]
   cudaEvent_t ev[8] = {};
+  // one CUDA graph per tick configuration: H2D staging, the six kernels, the command
+  // and diagnostics D2H (GPMPPI_NO_GRAPH=1 launches them one by one instead)
+  cudaGraph_t tick_graph = nullptr;
+  cudaGraphExec_t tick_exec = nullptr;
+  long long graph_key = -1;
+  int graph_launches = 0;
+  bool use_graph = getenv("GPMPPI_NO_GRAPH") == nullptr;
 
   template <class T>
   T* dalloc(size_t count) {
@@ -578,6 +585,8 @@ struct gpmppi_planner {
     if (h_infeasible) cudaFreeHost(h_infeasible);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    if (tick_exec) cudaGraphExecDestroy(tick_exec);
+    if (tick_graph) cudaGraphDestroy(tick_graph);
     if (stream) cudaStreamDestroy(stream);
   }
   long long slots() const { return (long long)B * K_local; }
@@ -714,8 +723,8 @@ double task_var_weight(const gpmppi_task* t) {
   return t->kind == GPMPPI_TASK_AVOIDANCE ? t->avoidance.variance : t->tracking.variance;
 }
 
-// mppi.cpp:235-248 ensure_thresholds + the per-tick upload of every robot's state,
-// task, variance weight and Philox key (two H2D copies for all B robots).
+// mppi.cpp:235-248 ensure_thresholds + the per-tick staging of every robot's state,
+// task, variance weight and Philox key into pinned memory (enqueue_h2d copies them).
 void stage_tick(gpmppi_planner* p, const double* x0, const gpmppi_task* tasks) {
   if (!x0 || !tasks) invalid("plan_step: null state or task");
   const int T = p->T;
@@ -757,6 +766,10 @@ void stage_tick(gpmppi_planner* p, const double* x0, const gpmppi_task* tasks) {
     blk[7] = 0.0;
   }
   p->n_obs_max = omax;
+}
+
+// the tick's two H2D copies from the pinned staging buffers (captured in the tick graph)
+void enqueue_h2d(gpmppi_planner* p) {
   CK(cudaMemcpyAsync(p->d_task, p->h_task, sizeof(gpm::TaskDev) * p->B, cudaMemcpyHostToDevice, p->stream));
   CK(cudaMemcpyAsync(p->d_x0, p->h_x0, sizeof(double) * gpm::BatchStrides::X0 * p->B,
                      cudaMemcpyHostToDevice, p->stream));
@@ -1018,6 +1031,58 @@ gpmppi_planner* create_planner(const gpmppi_mppi_config* cfg, const gpmppi_predi
   return p;
 }
 
+// The device work of one tick after staging: H2D, samples + update, command D2H (event
+// ev[0] marks the command), tightening (mppi.cpp:433), infeasibility D2H.
+void enqueue_tick(gpmppi_planner* p, bool capturing) {
+  enqueue_h2d(p);
+  enqueue_samples(p, 1, nullptr);
+  copy_out_async(p);
+  if (capturing)
+    CK(cudaEventRecordWithFlags(p->ev[0], p->stream, cudaEventRecordExternal));
+  else
+    CK(cudaEventRecord(p->ev[0], p->stream));
+  enqueue_tighten(p);
+  CK(cudaMemcpyAsync(p->h_infeasible, p->d_infeasible, sizeof(int) * p->B, cudaMemcpyDeviceToHost, p->stream));
+}
+
+// Capture the tick into a graph (one launch instead of eight stream operations). Any
+// capture failure leaves the planner on the per-operation path.
+void capture_tick(gpmppi_planner* p, long long key) {
+  if (p->tick_exec) cudaGraphExecDestroy(p->tick_exec);
+  if (p->tick_graph) cudaGraphDestroy(p->tick_graph);
+  p->tick_exec = nullptr;
+  p->tick_graph = nullptr;
+  const unsigned long long l0 = gpm::launches_total();
+  bool ok = cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+  if (ok) {
+    try {
+      enqueue_tick(p, true);
+    } catch (...) {
+      ok = false;
+    }
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(p->stream, &g);
+    ok = ok && e == cudaSuccess && g != nullptr;
+    if (ok) {
+      p->tick_graph = g;
+      ok = cudaGraphInstantiate(&p->tick_exec, g, 0) == cudaSuccess;
+    } else if (g) {
+      cudaGraphDestroy(g);
+    }
+  }
+  const int n = (int)(gpm::launches_total() - l0);  // counted while capturing, launched on replay
+  gpm::count_launch(-n);
+  cudaGetLastError();  // clear a failed capture's error state
+  if (!ok) {
+    if (p->tick_exec) cudaGraphExecDestroy(p->tick_exec);
+    p->tick_exec = nullptr;
+    p->use_graph = false;
+    return;
+  }
+  p->graph_launches = n;
+  p->graph_key = key;
+}
+
 // One tick of every robot: mppi.cpp:389-462 (plan_step_impl) for B planners at once.
 void plan_tick(gpmppi_planner* p, const double* x0, const gpmppi_task* tasks, double* command,
                gpmppi_diag* diag) {
@@ -1027,11 +1092,16 @@ void plan_tick(gpmppi_planner* p, const double* x0, const gpmppi_task* tasks, do
   if (p->K_local != p->K_total) invalid("plan_step: sharded planner; use plan_partial/plan_finish");
   if (p->noise_mode == gpm::NOISE_INJECTED && !p->injected_set) invalid("plan_step: injected noise mode without noise");
   stage_tick(p, x0, tasks);
-  enqueue_samples(p, 1, nullptr);
-  copy_out_async(p);
-  CK(cudaEventRecord(p->ev[0], p->stream));
-  enqueue_tighten(p);  // mppi.cpp:433
-  CK(cudaMemcpyAsync(p->h_infeasible, p->d_infeasible, sizeof(int) * p->B, cudaMemcpyDeviceToHost, p->stream));
+  // everything a captured kernel argument depends on (device buffers are fixed per planner)
+  const long long key = (long long)p->n_obs_max | ((long long)p->noise_mode << 8) | ((long long)p->var_path << 10) |
+                        ((long long)p->R << 16);
+  if (p->use_graph && (!p->tick_exec || p->graph_key != key)) capture_tick(p, key);
+  if (p->use_graph && p->tick_exec) {
+    CK(cudaGraphLaunch(p->tick_exec, p->stream));
+    gpm::count_launch(p->graph_launches);
+  } else {
+    enqueue_tick(p, false);
+  }
   CK(cudaEventSynchronize(p->ev[0]));
   const double t_cmd = ms_since(t0);
   CK(cudaStreamSynchronize(p->stream));
@@ -1290,6 +1360,7 @@ int gpmppi_planner_bench_device(gpmppi_planner* p, const double* x0, const gpmpp
     if (ticks < 1) invalid("bench_device: ticks must be >= 1");
     if (p->K_local != p->K_total) invalid("bench_device: sharded planner");
     stage_tick(p, x0, tasks);
+    enqueue_h2d(p);
     void* flush = nullptr;
     size_t flush_bytes = 0;
     if (flush_l2) {
@@ -1385,6 +1456,7 @@ int gpmppi_planner_plan_partial(gpmppi_planner* p, const double x0[5], const gpm
     if (p->B != 1) invalid("plan_partial: batched planner");
     if (p->noise_mode == gpm::NOISE_INJECTED && !p->injected_set) invalid("plan_partial: injected noise mode without noise");
     stage_tick(p, x0, task);
+    enqueue_h2d(p);
     enqueue_samples(p, 0, nullptr);
     CK(cudaMemcpyAsync(device_tuple_out, p->d_rank_tuple, sizeof(double) * gpm::tuple_doubles(p->T),
                        cudaMemcpyDeviceToDevice, p->stream));
