@@ -720,8 +720,11 @@ cudaError_t launch_variance(const VarianceArgs& a, int path, cudaStream_t st) {
 // -------------------------------------------------------------------------
 // Reduction: tuple per block, last block combines (+ update/shift/diag).
 int reduce_blocks_for(int K_local, int B, int num_sms) {
-  // blocks per robot: ~16+ samples per block, at most one wave in total
-  int b = (K_local + 15) / 16;
+  static const int forced = env_int("GPMPPI_REDUCE_BPR");
+  if (forced > 0) return forced;
+  // blocks per robot: ~64 samples per block (measured: 148 blocks of 28 samples 34.8 us,
+  // 64 blocks of 64 samples 28.6 us at K = 4096), at most one wave in total
+  int b = (K_local + 63) / 64;
   const int cap = num_sms / (B < num_sms ? B : num_sms);
   if (b > cap) b = cap;
   return b < 1 ? 1 : b;
