@@ -200,6 +200,40 @@ __device__ __forceinline__ void mma_chunk_3x(uint32_t d, uint64_t ahi, uint64_t 
         : "memory");
   }
 }
+// Two M tiles (TMEM columns d and d + dt) share one 16-point B chunk of <= 256
+// columns: 2 tiles x 2 K=8 steps x 3xTF32 = 12 MMAs, then the three stage releases.
+__device__ __forceinline__ void mma_chunk_pair_3x(uint32_t d, uint32_t dt, uint64_t a0hi, uint64_t a0lo,
+                                                  uint64_t a1hi, uint64_t a1lo, uint64_t bh0, uint64_t bl0,
+                                                  uint64_t bh1, uint64_t bl1, uint32_t idesc, uint32_t acc,
+                                                  uint32_t bar_b0, uint32_t bar_b1, uint32_t bar_a) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 d1;\n\t.reg .b64 x0h, x0l, x1h, x1l;\n\t"
+      "add.u32 d1, %0, %1;\n\t"
+      "add.s64 x0h, %2, 16;\n\t"
+      "add.s64 x0l, %3, 16;\n\t"
+      "add.s64 x1h, %4, 16;\n\t"
+      "add.s64 x1l, %5, 16;\n\t"
+      "setp.ne.b32 p, %11, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %6, %10, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %7, %10, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %3, %6, %10, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], %4, %6, %10, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], %4, %7, %10, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], %5, %6, %10, 1;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%12];\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], x0h, %8, %10, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], x0h, %9, %10, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], x0l, %8, %10, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], x1h, %8, %10, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], x1h, %9, %10, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], x1l, %8, %10, 1;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%13];\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%14];\n\t}" ::"r"(d),
+      "r"(dt), "l"(a0hi), "l"(a0lo), "l"(a1hi), "l"(a1lo), "l"(bh0), "l"(bl0), "l"(bh1), "l"(bl1), "r"(idesc),
+      "r"(acc), "r"(bar_b0), "r"(bar_b1), "r"(bar_a)
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
@@ -282,6 +316,9 @@ __device__ __forceinline__ int pass_chunks(int p, int np, int n_pad) {
 
 // dbg (diagnostics only, env GPMPPI_TC_DEBUG): 1 = skip B copies, 2 = skip k* math,
 // 4 = skip MMAs, 8 = skip TMEM reads. Results are garbage when set.
+// TPC = query tiles per CTA iteration. TPC = 2 (NP <= 256): two 128-query tiles share
+// every B chunk (half the L^{-T} stream per query, fewer stage hand-offs per MMA).
+template <int TPC>
 __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const VarianceArgs a, int one_pass, int dbg,
                                                                   int SA, int SB) {
   using namespace tc;
@@ -291,8 +328,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
   // ---- shared memory carve-up. Align with pointer arithmetic on the shared array
   // (a size_t round trip turns every access into a generic LD/ST).
   unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  float* sA = reinterpret_cast<float*>(base);                  // [SA][2][M*KC]
-  float* sB = sA + SA * 2 * A_STAGE_FLOATS;              // [SB][2][NP*KB]
+  float* sA = reinterpret_cast<float*>(base);                  // [SA][TPC][2][M*KC]
+  float* sB = sA + SA * TPC * 2 * A_STAGE_FLOATS;              // [SB][2][NP*KB]
   float* zs = sB + (size_t)SB * 2 * NP * KB;                   // [5][n_pad] log2e-scaled aug. inputs
   uint64_t* bars = reinterpret_cast<uint64_t*>(zs + 5 * n_pad);
   uint64_t* full_a = bars;
@@ -308,7 +345,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
   // warp-uniform and keeps the MMA warp's descriptors in uniform registers
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int n_tiles = (int)((a.KT + M - 1) / M);
-  const uint32_t tmem_cols = NP <= 32 ? 32 : NP <= 64 ? 64 : NP <= 128 ? 128 : NP <= 256 ? 256 : 512;
+  const int n_units = (n_tiles + TPC - 1) / TPC;  // groups of TPC tiles
+  const int acc_cols = TPC * NP;
+  const uint32_t tmem_cols = acc_cols <= 32 ? 32 : acc_cols <= 64 ? 64 : acc_cols <= 128 ? 128 : acc_cols <= 256 ? 256 : 512;
 
   // exponent in base 2: log2(k*) = q'·z' + qn' + zn'  with z' = log2e·z/l, zn' = log2e·(-|z/l|²/2 + ln sf2)
   const float L2E = 1.4426950408889634f;
@@ -358,7 +397,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
     Ring rb(SB);
     int4 next = G.tc_meta[0];
     int ti = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++ti) {
+    for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x, ++ti) {
       if (ti < 10) trace_at(48 + ti, dbg);
       for (int kb = 0; kb < nbt; ++kb, rb.next()) {
         {
@@ -384,7 +423,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
     // waterfall of R2UR broadcasts (~780 cycles per 8-point block).
     Ring ra(SA), rbb(SB);
     uint32_t uc = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
       for (int p = 0; p < n_pass; ++p, ++uc) {
         mbar_wait_prof(smem_u32(tempty), (uc & 1) ^ 1, 1, dbg & ~512);  // epilogue drained the accumulator
         tc_after();
@@ -394,11 +433,33 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
         for (int kb = 0; kb < nk; ++kb, ra.next()) {
           const int sa = ra.s;
           if (!(dbg & 16)) mbar_wait(smem_u32(&full_a[sa]), ra.ph);
-          const uint32_t a_hi = smem_u32(sA + (size_t)sa * 2 * A_STAGE_FLOATS);
+          const uint32_t a_hi = smem_u32(sA + (size_t)sa * TPC * 2 * A_STAGE_FLOATS);
           const uint32_t a_lo = a_hi + A_STAGE_FLOATS * 4;
           const int col0 = max(0, kb * KC - p * NP);  // build_tc_operand's column start
           const int ncols = npw - col0;
-          if (!one_pass && !(dbg & 4)) {  // both B blocks of the chunk, then one statement
+          if (TPC == 2 && !one_pass && !(dbg & 4)) {  // two tiles share both B blocks of the chunk
+            const int sb0 = rbb.s;
+            const uint32_t ph0 = rbb.ph;
+            rbb.next();
+            const int sb1 = rbb.s;
+            const uint32_t ph1 = rbb.ph;
+            rbb.next();
+            if (!(dbg & 32)) {
+              mbar_wait(smem_u32(&full_b[sb0]), ph0);
+              mbar_wait(smem_u32(&full_b[sb1]), ph1);
+            }
+            const uint32_t bh0 = smem_u32(sB + (size_t)sb0 * 2 * NP * KB);
+            const uint32_t bh1 = smem_u32(sB + (size_t)sb1 * 2 * NP * KB);
+            const uint32_t blen = (uint32_t)ncols * KB * 4;
+            const uint32_t a1 = a_hi + 2 * A_STAGE_FLOATS * 4;  // second tile's hi/lo
+            mma_chunk_pair_3x(tmem_base + (uint32_t)col0, (uint32_t)NP, smem_desc(a_hi), smem_desc(a_lo),
+                              smem_desc(a1), smem_desc(a1 + A_STAGE_FLOATS * 4), smem_desc(bh0, SBO_B),
+                              smem_desc(bh0 + blen, SBO_B), smem_desc(bh1, SBO_B), smem_desc(bh1 + blen, SBO_B),
+                              instr_desc(ncols), kb > 0 ? 1u : 0u, smem_u32(&empty_b[sb0]),
+                              smem_u32(&empty_b[sb1]), smem_u32(&empty_a[sa]));
+            continue;
+          }
+          if (TPC == 1 && !one_pass && !(dbg & 4)) {  // both B blocks of the chunk, then one statement
             const int sb0 = rbb.s;
             const uint32_t ph0 = rbb.ph;
             rbb.next();
@@ -444,15 +505,18 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
     }
   } else if (warp >= 8) {
     // ---------------- A producers: k* rows, hi/lo TF32 split, canonical layout.
-    // Two warps per 32 rows: warp half h produces K sub-chunks 2h and 2h+1.
+    // TPC = 1: two warps per 32 rows, warp half h produces K sub-chunks 2h, 2h+1;
+    // TPC = 2: one warp per 32 rows of tile t = pw / 4, all four sub-chunks.
     const int pw = warp - 8;
     const int m = (pw & 3) * 32 + lane;  // tile row == TMEM lane
-    const int h = pw >> 2;
+    const int h = TPC == 2 ? 0 : pw >> 2;
+    const int t = TPC == 2 ? pw >> 2 : 0;
+    constexpr int SUBS = 2 * TPC;  // 4-point sub-chunks per warp and chunk
     Ring ra(SA);
     int ti = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++ti) {
+    for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x, ++ti) {
       if (pw == 0 && lane == 0 && ti < 10) trace_at(36 + ti, dbg);
-      const long long q = (long long)tile * M + m;
+      const long long q = ((long long)unit * TPC + t) * M + m;
       const bool valid = q < a.KT;
       float4 qv = valid ? a.queries[q] : make_float4(0.f, 0.f, 0.f, 0.f);
       const float q0 = qv.x / (float)G.ls[0], q1 = qv.y / (float)G.ls[1];
@@ -466,12 +530,12 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
           if (lane == 0 && !(dbg & 64)) mbar_wait_prof(smem_u32(&empty_a[s]), ph ^ 1, 4, dbg);
           __syncwarp();
           const unsigned long long tp0 = (dbg & 512) ? clock64() : 0ull;
-          float* ahi = sA + (size_t)s * 2 * A_STAGE_FLOATS;
+          float* ahi = sA + ((size_t)s * TPC + t) * 2 * A_STAGE_FLOATS;
           float* alo = ahi + A_STAGE_FLOATS;
           const int row_off = (m >> 3) * (SBO / 4) + (m & 7) * 4;
 #pragma unroll
-          for (int cc = 0; cc < 2; ++cc) {
-            const int c = 2 * h + cc;
+          for (int cc = 0; cc < SUBS; ++cc) {
+            const int c = SUBS * h + cc;
             float hi[4], lo[4];
             const int i0 = kb * KC + c * 4;  // four consecutive points: one LDS.128 per input row
             const float4 z0 = *reinterpret_cast<const float4*>(zs + i0);
@@ -508,8 +572,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
     const int e = warp - 4;  // TMEM lanes 32e..32e+31 (warp % 4 == e)
     const int m = e * 32 + lane;
     uint32_t uc = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      double ssq = 0.0;
+    for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
+      double ssqs[TPC];
+#pragma unroll
+      for (int tt = 0; tt < TPC; ++tt) ssqs[tt] = 0.0;
       for (int p = 0; p < n_pass; ++p, ++uc) {
         const int npw = min(NP, n_pad - p * NP);
         if (lane == 0) mbar_wait_prof(smem_u32(tfull), uc & 1, 5, dbg);
@@ -517,7 +583,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
         __syncwarp();
         const unsigned long long te0 = (dbg & 512) ? clock64() : 0ull;
         tc_after();
-        const uint32_t trow = tmem_base + ((uint32_t)(e * 32) << 16);
+#pragma unroll
+        for (int tt = 0; tt < TPC; ++tt) {
+        double ssq = 0.0;
+        const uint32_t trow = tmem_base + ((uint32_t)(e * 32) << 16) + (uint32_t)(tt * NP);
         int c = (dbg & 8) ? npw : 0;
         for (; c + 64 <= npw; c += 64) {  // four loads in flight per wait
           uint32_t r[64];
@@ -539,17 +608,22 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
           for (int i = 0; i < 16; ++i) part = fmaf(v[i], v[i], part);
           ssq += (double)part;
         }
+        ssqs[tt] += ssq;
+        }
         tc_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(tempty));
         if (lane == 0) prof_add(14, clock64() - te0, dbg);
       }
-      const long long q = (long long)tile * M + m;
-      if (q < a.KT) {
-        double var = G.sv - ssq;  // gp.cpp:187-191
-        var = var > 0.0 ? var : 0.0;
-        const double c = a.coef * var;
-        a.trace[q] = a.accumulate ? a.trace[q] + c : c;
+#pragma unroll
+      for (int tt = 0; tt < TPC; ++tt) {
+        const long long q = ((long long)unit * TPC + tt) * M + m;
+        if (q < a.KT) {
+          double var = G.sv - ssqs[tt];  // gp.cpp:187-191
+          var = var > 0.0 ? var : 0.0;
+          const double c = a.coef * var;
+          a.trace[q] = a.accumulate ? a.trace[q] + c : c;
+        }
       }
     }
   }
@@ -570,9 +644,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
                  : "memory");
 }
 
-size_t tc_smem_bytes(const GroupDev& g, int stages_a, int stages_b) {
+size_t tc_smem_bytes(const GroupDev& g, int stages_a, int stages_b, int tpc) {
   size_t b = 1024;  // alignment slack
-  b += sizeof(float) * (size_t)stages_a * 2 * tc::A_STAGE_FLOATS;
+  b += sizeof(float) * (size_t)stages_a * tpc * 2 * tc::A_STAGE_FLOATS;
   b += sizeof(float) * (size_t)stages_b * 2 * g.tc_np * tc::KB;
   b += sizeof(float) * (size_t)5 * g.tc_npad;
   b += sizeof(uint64_t) * (2 * stages_a + 2 * stages_b + 2) + 16;
@@ -606,25 +680,34 @@ cudaError_t launch_tc_variance(const VarianceArgs& a, int one_pass, cudaStream_t
     const char* e = getenv("GPMPPI_TC_SA");
     sa_env = e ? atoi(e) : 0;
   }
-  int SA = sa_env >= 2 ? sa_env : tc::STAGES_A, SB = sb_env >= 2 ? sb_env : tc::STAGES_B + 1;
-  while (sb_env < 2 && SB > tc::STAGES_B && tc_smem_bytes(a.g, SA, SB) > kSmemMax) --SB;
-  while (SA > 2 && tc_smem_bytes(a.g, SA, SB) > kSmemMax) --SA;
+  static int tpc_env = -1;  // GPMPPI_TC_TPC=1 forces one tile per iteration
+  if (tpc_env < 0) {
+    const char* e = getenv("GPMPPI_TC_TPC");
+    tpc_env = e ? atoi(e) : 0;
+  }
+  const int tpc = (tpc_env == 1 || a.g.tc_np > 256 || one_pass) ? 1 : 2;
+  int SA = sa_env >= 2 ? sa_env : (tpc == 2 ? 3 : tc::STAGES_A);
+  int SB = sb_env >= 2 ? sb_env : (tpc == 2 ? 8 : tc::STAGES_B + 1);
+  while (sb_env < 2 && SB > tc::STAGES_B && tc_smem_bytes(a.g, SA, SB, tpc) > kSmemMax) --SB;
+  while (SA > 2 && tc_smem_bytes(a.g, SA, SB, tpc) > kSmemMax) --SA;
   if (sa_env >= 2) SA = std::min(SA, sa_env);
-  while (SB > 2 && tc_smem_bytes(a.g, SA, SB) > kSmemMax) --SB;
-  const size_t smem = tc_smem_bytes(a.g, SA, SB);
-  cudaError_t e = cudaFuncSetAttribute(variance_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  while (SB > 2 && tc_smem_bytes(a.g, SA, SB, tpc) > kSmemMax) --SB;
+  const size_t smem = tc_smem_bytes(a.g, SA, SB, tpc);
+  void (*kern)(const VarianceArgs, int, int, int, int) = tpc == 2 ? variance_tc_kernel<2> : variance_tc_kernel<1>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long tiles = (a.KT + tc::M - 1) / tc::M;
-  const int grid = (int)(tiles < sms ? tiles : sms);
+  const long long units = (tiles + tpc - 1) / tpc;
+  const int grid = (int)(units < sms ? units : sms);
   static int dbg = -1;
   if (dbg < 0) {
     const char* e = getenv("GPMPPI_TC_DEBUG");
     dbg = e ? atoi(e) : 0;
   }
-  variance_tc_kernel<<<grid, tc::THREADS, smem, st>>>(a, one_pass, dbg, SA, SB);
+  kern<<<grid, tc::THREADS, smem, st>>>(a, one_pass, dbg, SA, SB);
   count_launch();
   return cudaGetLastError();
 }
@@ -636,7 +719,7 @@ void build_tc_operand(const double* ilt, int n, std::vector<float>& data, std::v
                       int& n_pad, int& np, int& n_pass) {
   const int KC = tc::KC;
   n_pad = (n + 15) / 16 * 16;
-  np = n_pad < 512 ? n_pad : 512;
+  np = n_pad < 256 ? n_pad : 256;  // <= 256 columns per pass: two tiles fill the 512 TMEM columns
   n_pass = (n_pad + np - 1) / np;
   auto tf32 = [](float x) {
     uint32_t u;
