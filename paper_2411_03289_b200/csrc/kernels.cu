@@ -158,6 +158,31 @@ GPM_D double group_sum(double v) {  // xor butterfly inside an LPS-lane group
   return v;
 }
 
+// Sums NV (<= LPS) values across an LPS-lane group and returns every total in every
+// lane: a transpose reduction (LPS-1 shuffles: each level halves the values a lane
+// carries) leaves total i in lane i of the group, then NV broadcasts. A butterfly
+// per value costs NV*log2(LPS) shuffles.
+template <int LPS, int NV>
+GPM_D void group_allsum(double (&val)[NV]) {
+  static_assert(NV <= LPS, "group_allsum: at most one value per lane");
+  const int gl = threadIdx.x & (LPS - 1);
+  double t[LPS];
+#pragma unroll
+  for (int i = 0; i < LPS; ++i) t[i] = i < NV ? val[i] : 0.0;
+#pragma unroll
+  for (int lvl = LPS / 2; lvl >= 1; lvl >>= 1) {
+    const bool up = gl & lvl;
+#pragma unroll
+    for (int i = 0; i < lvl; ++i) {
+      const double send = up ? t[i] : t[i + lvl];
+      t[i] = (up ? t[i + lvl] : t[i]) + __shfl_xor_sync(0xffffffffu, send, lvl);
+    }
+  }
+  const int base = (threadIdx.x & 31) & ~(LPS - 1);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) val[i] = __shfl_sync(0xffffffffu, t[0], base + i);
+}
+
 // One LPS-lane group per SPG samples (32/LPS groups per warp share every Z/alpha
 // shared-memory read; each lane reuses its loaded points for its group's SPG samples,
 // which halves the LDS per FP64 op at SPG=2 and gives SPG independent exp chains).
@@ -400,18 +425,41 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
               for (int j = 0; j < SPG; ++j) acc[j][o] = fma(k1[j], ao.y, fma(k0[j], ao.x, acc[j][o]));  // gp.cpp:181-182
             }
         }
+        if constexpr (SPG * NO <= LPS) {  // all group sums at once (transpose reduction)
+          double tot[SPG * NO];
 #pragma unroll
-        for (int o = 0; o < NO; ++o) {
-          if (o < nout) {
-            const int gi = G.out_idx[o];
-            const double wt = sv.tw[gi >> 1];
+          for (int j = 0; j < SPG; ++j)
 #pragma unroll
-            for (int j = 0; j < SPG; ++j) {
-              const double mo = group_sum<LPS>(acc[j][o]);
-              if (gi & 1)
-                cm1[j] += wt * mo;
-              else
-                cm0[j] += wt * mo;
+            for (int o = 0; o < NO; ++o) tot[j * NO + o] = acc[j][o];
+          group_allsum<LPS, SPG * NO>(tot);
+#pragma unroll
+          for (int o = 0; o < NO; ++o) {
+            if (o < nout) {
+              const int gi = G.out_idx[o];
+              const double wt = sv.tw[gi >> 1];
+#pragma unroll
+              for (int j = 0; j < SPG; ++j) {
+                if (gi & 1)
+                  cm1[j] += wt * tot[j * NO + o];
+                else
+                  cm0[j] += wt * tot[j * NO + o];
+              }
+            }
+          }
+        } else {
+#pragma unroll
+          for (int o = 0; o < NO; ++o) {
+            if (o < nout) {
+              const int gi = G.out_idx[o];
+              const double wt = sv.tw[gi >> 1];
+#pragma unroll
+              for (int j = 0; j < SPG; ++j) {
+                const double mo = group_sum<LPS>(acc[j][o]);
+                if (gi & 1)
+                  cm1[j] += wt * mo;
+                else
+                  cm0[j] += wt * mo;
+              }
             }
           }
         }
