@@ -303,6 +303,11 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
   extern __shared__ __align__(16) unsigned char smem[];
   const SmemView sv = carve_smem(a, smem);
   const int ns = a.model.ns;  // even SoA stride (padding points contribute exactly 0)
+  const int T = a.T;
+  const int gl = threadIdx.x % LPS;  // lane inside the sample group
+  const int groups_per_block = blockDim.x / LPS;
+  const int gib = threadIdx.x / LPS;  // group index in the block
+  double2* ubuf;  // this group's clamped controls u[SPG][T], drawn before the serial chain
   {  // stage Z / alpha of every group (SoA) into shared memory, once per block
     double* dst = sv.pts;
     for (int g = 0; g < a.model.G; ++g) {
@@ -313,12 +318,9 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
       for (int i = threadIdx.x; i < cnt / 2; i += blockDim.x) d2[i] = __ldg(src + i);
       dst += cnt;
     }
+    ubuf = reinterpret_cast<double2*>(dst) + (size_t)gib * SPG * T;
   }
   const TaskDev& task = *sv.task;
-  const int gl = threadIdx.x % LPS;  // lane inside the sample group
-  const int groups_per_block = blockDim.x / LPS;
-  const int gib = threadIdx.x / LPS;  // group index in the block
-  const int T = a.T;
   const int stride = T + 1;
   // scratch slot of sample j of this group
   double* const scr0 = a.scratch + ((size_t)blockIdx.x * kMaxSampleSlotsPerBlock + (size_t)gib * SPG) *
@@ -360,21 +362,33 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
         scr[3 * stride] = w[j];
       }
     }
+    // noise + clamp of every (sample, step) up front, lanes split the pairs: the draws
+    // do not depend on the chain, so they leave the serial path (mppi.cpp:298-308)
+    for (int idx = gl; idx < SPG * T; idx += LPS) {
+      const int j = SPG == 1 ? 0 : idx / T, k = SPG == 1 ? idx : idx % T;
+      const bool vj = j == 0 ? valid[0] : valid[SPG - 1];
+      double e0 = 0.0, e1 = 0.0;
+      if (vj) sample_noise(a, key, j == 0 ? sl[0] : sl[SPG - 1], j == 0 ? s[0] : s[SPG - 1], k, &e0, &e1);
+      const double u0 = clampd(sv.nom[2 * k] + e0, a.lo[0], a.hi[0]);
+      const double u1 = clampd(sv.nom[2 * k + 1] + e1, a.lo[1], a.hi[1]);
+      ubuf[j * T + k] = make_double2(u0, u1);
+      if (vj) {
+        double* scr = scr0 + (size_t)j * SCR_ARRAYS * stride;
+        scr[k] = u0;
+        scr[stride + k] = u1;
+      }
+    }
+    __syncwarp();
     // ---------------- phase 1: serial (v, omega) chains with the GP mean
     for (int k = 0; k < T; ++k) {
       double u0[SPG], u1[SPG];
 #pragma unroll
       for (int j = 0; j < SPG; ++j) {
-        double e0 = 0.0, e1 = 0.0;
-        if (valid[j]) sample_noise(a, key, sl[j], s[j], k, &e0, &e1);
-        u0[j] = clampd(sv.nom[2 * k] + e0, a.lo[0], a.hi[0]);  // mppi.cpp:298-308
-        u1[j] = clampd(sv.nom[2 * k + 1] + e1, a.lo[1], a.hi[1]);
-        if (valid[j] && gl == 0) {
+        const double2 u = ubuf[j * T + k];
+        u0[j] = u.x;
+        u1[j] = u.y;
+        if (valid[j] && gl == 0)
           a.queries[(size_t)sl[j] * T + k] = make_float4((float)v[j], (float)w[j], (float)u0[j], (float)u1[j]);
-          double* scr = scr0 + (size_t)j * SCR_ARRAYS * stride;
-          scr[k] = u0[j];
-          scr[stride + k] = u1[j];
-        }
       }
       double cm0[SPG], cm1[SPG];  // combine_terrains (mppi.cpp:34-49)
 #pragma unroll
@@ -617,6 +631,7 @@ cudaError_t launch_rollout(const RolloutArgs& a, int num_sms, cudaStream_t st) {
     for (int g = 0; g < a.model.G; ++g) no = a.model.g[g].n_out > no ? a.model.g[g].n_out : no;
     int lps = 8, threads = 32, spg = 1;
     const int spb = rollout_samples_per_block(a.K_local, a.B, num_sms, &lps, &threads, &spg);
+    const size_t smem_u = smem + sizeof(double2) * (size_t)(threads / lps) * spg * a.T;  // + control buffers
     const long long items = (long long)a.B * ((a.K_local + spb - 1) / spb);
     // one block per SM: capping registers for a second resident block (122 instead of
     // ~200) costs more ILP than the extra warps recover (config2 0.34 -> 0.52 ms)
@@ -635,9 +650,9 @@ cudaError_t launch_rollout(const RolloutArgs& a, int num_sms, cudaStream_t st) {
     const int ni = no <= 2 ? 0 : no <= 4 ? 1 : no <= 6 ? 2 : 3;
     const int li = lps == 4 ? 0 : lps == 8 ? 1 : lps == 16 ? 2 : 3;
     KF kern = spg == 4 ? table4[ni] : table[spg == 2 ? 1 : 0][ni][li];
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_u);
     if (e != cudaSuccess) return e;
-    kern<<<(unsigned)blocks, threads, smem, st>>>(a);
+    kern<<<(unsigned)blocks, threads, smem_u, st>>>(a);
   } else {
     const int threads = 128;
     const long long items = (long long)a.B * ((a.K_local + threads - 1) / threads);
