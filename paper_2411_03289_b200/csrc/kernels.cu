@@ -320,6 +320,8 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
     }
     ubuf = reinterpret_cast<double2*>(dst) + (size_t)gib * SPG * T;
   }
+  __shared__ double gil[kMaxGroups][4];  // reciprocal lengthscales: no FP64 divide on the chain
+  if (threadIdx.x < 4 * a.model.G) gil[threadIdx.x >> 2][threadIdx.x & 3] = 1.0 / a.model.g[threadIdx.x >> 2].ls[threadIdx.x & 3];
   const TaskDev& task = *sv.task;
   const int stride = T + 1;
   // scratch slot of sample j of this group
@@ -402,10 +404,10 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
         double acc[SPG][NO];
 #pragma unroll
         for (int j = 0; j < SPG; ++j) {
-          q0[j] = v[j] / G.ls[0];
-          q1[j] = w[j] / G.ls[1];
-          q2[j] = u0[j] / G.ls[2];
-          q3[j] = u1[j] / G.ls[3];
+          q0[j] = v[j] * gil[g][0];  // q/l (gp.cpp:172-176) by reciprocal: <= 1 ulp from the division
+          q1[j] = w[j] * gil[g][1];
+          q2[j] = u0[j] * gil[g][2];
+          q3[j] = u1[j] * gil[g][3];
           qn[j] = -0.5 * (q0[j] * q0[j] + q1[j] * q1[j] + q2[j] * q2[j] + q3[j] * q3[j]);
 #pragma unroll
           for (int o = 0; o < NO; ++o) acc[j][o] = 0.0;
