@@ -583,24 +583,23 @@ static int env_int(const char* name) {
   const char* e = getenv(name);
   return e ? atoi(e) : 0;
 }
-int rollout_lanes_per_sample(int K, int num_sms) {
-  static const int forced = env_int("GPMPPI_LPS");
-  if (forced == 4 || forced == 8 || forced == 16 || forced == 32) return forced;
-  // aim for >= ~7 warps per SM before widening the lane groups
-  const long long per_sm = ((long long)K + num_sms - 1) / num_sms;
-  if (per_sm >= 28) return 8;
-  if (per_sm >= 14) return 16;
-  return 32;
-}
-int rollout_samples_per_group(int lps, long long total, int num_sms) {
-  static const int forced = env_int("GPMPPI_SPG");
-  if (lps == 4) return 1;
-  if (forced == 4) return lps == 32 ? 4 : 2;
-  if (forced == 1 || forced == 2) return forced;
-  // beyond one wave (>= 64 samples per SM) the rollout is FP64-throughput bound and
-  // halving the LDS per FP64 op wins (config5 rollout 5.1 -> 3.7 ms); below it the
-  // single-sample latency chain decides and SPG = 1 is faster (config2 0.339 vs 0.376 ms)
-  return total >= 64LL * num_sms ? 2 : 1;
+// Lane-group layout of the GP rollout: LPS lanes per group, SPG samples per group.
+// Measured on B200 (rollout ms): config2 (28 samples/SM) (8,1) 0.309, (16,2) 0.280,
+// (8,2) 0.342; config5 (443/SM) (8,2) 3.31, (16,2) 3.70, (8,1) 4.54; config3 (16,2) 5.14,
+// (8,1) 6.99. The 8-lane layout reads every Z/alpha byte four times per warp (LDS.128
+// costs four wavefronts regardless of duplicate addresses) and is shared-memory bound;
+// SPG = 2 halves the loads per FP64 op. GPMPPI_LPS / GPMPPI_SPG force a layout.
+void rollout_layout(long long total, int num_sms, int* lps, int* spg) {
+  static const int f_lps = env_int("GPMPPI_LPS"), f_spg = env_int("GPMPPI_SPG");
+  const long long per_sm = (total + num_sms - 1) / num_sms;
+  int l = per_sm >= 64 ? 8 : per_sm >= 7 ? 16 : 32;
+  int g = 2;
+  if (f_lps == 4 || f_lps == 8 || f_lps == 16 || f_lps == 32) l = f_lps;
+  if (f_spg == 1 || f_spg == 2) g = f_spg;
+  if (f_spg == 4) g = l == 32 ? 4 : 2;
+  if (l == 4) g = 1;
+  *lps = l;
+  *spg = g;
 }
 
 // trajectory scratch for every sample slot the launcher can create
@@ -612,9 +611,8 @@ size_t rollout_scratch_doubles(int T, int num_sms) {
 // single wave when possible (one block per SM)
 int rollout_samples_per_block(int K_local, int B, int num_sms, int* lps_out, int* threads_out, int* spg_out) {
   const long long total = (long long)K_local * B;
-  const int lps = rollout_lanes_per_sample(total >= 64LL * num_sms ? (int)std::min<long long>(total, 1 << 30) : K_local,
-                                           num_sms);
-  const int spg = rollout_samples_per_group(lps, total, num_sms);
+  int lps = 8, spg = 1;
+  rollout_layout(total, num_sms, &lps, &spg);
   const int spw = 32 / lps * spg;
   const long long warps = (total + spw - 1) / spw;  // all robots' samples share the wave
   int wpb = (int)((warps + num_sms - 1) / num_sms);
@@ -632,8 +630,19 @@ cudaError_t launch_rollout(const RolloutArgs& a, int num_sms, cudaStream_t st) {
     int no = 0;
     for (int g = 0; g < a.model.G; ++g) no = a.model.g[g].n_out > no ? a.model.g[g].n_out : no;
     int lps = 8, threads = 32, spg = 1;
-    const int spb = rollout_samples_per_block(a.K_local, a.B, num_sms, &lps, &threads, &spg);
-    const size_t smem_u = smem + sizeof(double2) * (size_t)(threads / lps) * spg * a.T;  // + control buffers
+    int spb = rollout_samples_per_block(a.K_local, a.B, num_sms, &lps, &threads, &spg);
+    size_t smem_u = smem + sizeof(double2) * (size_t)(threads / lps) * spg * a.T;  // + control buffers
+    while (smem_u > 227 * 1024 && lps < 32) {  // large n*T: wider groups, fewer control buffers
+      lps *= 2;
+      const int spw = 32 / lps * spg;
+      const long long total = (long long)a.K_local * a.B;
+      const long long warps = (total + spw - 1) / spw;
+      int wpb = (int)((warps + num_sms - 1) / num_sms);
+      wpb = wpb < 1 ? 1 : (wpb > 8 ? 8 : wpb);
+      threads = wpb * 32;
+      spb = wpb * spw;
+      smem_u = smem + sizeof(double2) * (size_t)(threads / lps) * spg * a.T;
+    }
     const long long items = (long long)a.B * ((a.K_local + spb - 1) / spb);
     // one block per SM: capping registers for a second resident block (122 instead of
     // ~200) costs more ILP than the extra warps recover (config2 0.34 -> 0.52 ms)
