@@ -125,7 +125,14 @@ class Track:  # costs.hpp:13-27
     def polyline_track(points, half_width, closed):
         return Track(False, waypoints=points, closed=closed, half_width=half_width)
 
+    def __setattr__(self, name, value):  # any public change invalidates the cached C view
+        if not name.startswith("_"):
+            object.__setattr__(self, "_c", None)
+        object.__setattr__(self, name, value)
+
     def to_c(self):
+        if getattr(self, "_c", None) is not None:
+            return self._c
         t = A.TrackC()
         t.is_circle = int(self.is_circle)
         t.cx, t.cy = self.center
@@ -135,6 +142,7 @@ class Track:  # costs.hpp:13-27
             t.waypoints = A.dptr(self.waypoints)
         t.closed = int(self.closed)
         t.half_width = self.half_width
+        self._c = t
         return t
 
 
@@ -151,6 +159,8 @@ def _obstacle_array(obstacles):
 
 
 class TrackingTask:  # mppi.hpp:42-46
+    """Task views are marshalled to C once per state: assigning any attribute (or the
+    track's) rebuilds the view; edit obstacle arrays by re-assigning them, not in place."""
     kind = A.TASK_TRACKING
 
     def __init__(self, track: Track, v_desired: float, weights: TrackingWeights = None):
@@ -162,7 +172,16 @@ class TrackingTask:  # mppi.hpp:42-46
         self.avoidance = AvoidanceWeights()
         self.high_cost = 1e4
 
+    def __setattr__(self, name, value):  # any public change invalidates the cached C view
+        if not name.startswith("_"):
+            object.__setattr__(self, "_c", None)
+        object.__setattr__(self, name, value)
+
     def to_c(self):
+        # the C view is built once per task state (plan_step's Python overhead was ~45 us
+        # of re-marshalling the same task every tick); the track's own cache is checked too
+        if getattr(self, "_c", None) is not None and (self.track is None or self.track._c is self._track_c):
+            return self._c
         t = A.TaskC()
         t.kind = self.kind
         self._track_c = self.track.to_c() if self.track is not None else None
