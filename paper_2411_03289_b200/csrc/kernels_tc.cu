@@ -345,7 +345,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
   // warp-uniform and keeps the MMA warp's descriptors in uniform registers
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int n_tiles = (int)((a.KT + M - 1) / M);
-  const int n_units = (n_tiles + TPC - 1) / TPC;  // groups of TPC tiles
+  // contiguous, balanced tile range per CTA, walked in units of TPC tiles; a trailing
+  // single tile runs alone (half the MMAs) instead of costing a whole pair
+  const int tb = (int)((long long)blockIdx.x * n_tiles / gridDim.x);
+  const int te = (int)((long long)(blockIdx.x + 1) * n_tiles / gridDim.x);
   const int acc_cols = TPC * NP;
   const uint32_t tmem_cols = acc_cols <= 32 ? 32 : acc_cols <= 64 ? 64 : acc_cols <= 128 ? 128 : acc_cols <= 256 ? 256 : 512;
 
@@ -397,7 +400,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
     Ring rb(SB);
     int4 next = G.tc_meta[0];
     int ti = 0;
-    for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x, ++ti) {
+    for (int t0 = tb; t0 < te; t0 += TPC, ++ti) {
       if (ti < 10) trace_at(48 + ti, dbg);
       for (int kb = 0; kb < nbt; ++kb, rb.next()) {
         {
@@ -423,7 +426,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
     // waterfall of R2UR broadcasts (~780 cycles per 8-point block).
     Ring ra(SA), rbb(SB);
     uint32_t uc = 0;
-    for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
+    for (int t0 = tb; t0 < te; t0 += TPC) {
+      const bool two = TPC == 2 && t0 + 1 < te;
       for (int p = 0; p < n_pass; ++p, ++uc) {
         mbar_wait_prof(smem_u32(tempty), (uc & 1) ^ 1, 1, dbg & ~512);  // epilogue drained the accumulator
         tc_after();
@@ -437,7 +441,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
           const uint32_t a_lo = a_hi + A_STAGE_FLOATS * 4;
           const int col0 = max(0, kb * KC - p * NP);  // build_tc_operand's column start
           const int ncols = npw - col0;
-          if (TPC == 2 && !one_pass && !(dbg & 4)) {  // two tiles share both B blocks of the chunk
+          if (TPC == 2 && two && !one_pass && !(dbg & 4)) {  // two tiles share both B blocks of the chunk
             const int sb0 = rbb.s;
             const uint32_t ph0 = rbb.ph;
             rbb.next();
@@ -459,7 +463,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
                               smem_u32(&empty_b[sb1]), smem_u32(&empty_a[sa]));
             continue;
           }
-          if (TPC == 1 && !one_pass && !(dbg & 4)) {  // both B blocks of the chunk, then one statement
+          if (!one_pass && !(dbg & 4)) {  // one tile: both B blocks of the chunk, then one statement
             const int sb0 = rbb.s;
             const uint32_t ph0 = rbb.ph;
             rbb.next();
@@ -514,10 +518,11 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
     constexpr int SUBS = 2 * TPC;  // 4-point sub-chunks per warp and chunk
     Ring ra(SA);
     int ti = 0;
-    for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x, ++ti) {
+    for (int t0 = tb; t0 < te; t0 += TPC, ++ti) {
       if (pw == 0 && lane == 0 && ti < 10) trace_at(36 + ti, dbg);
-      const long long q = ((long long)unit * TPC + t) * M + m;
-      const bool valid = q < a.KT;
+      const bool present = t0 + t < te;  // this warp's tile exists in the unit
+      const long long q = (long long)(t0 + t) * M + m;
+      const bool valid = present && q < a.KT;
       float4 qv = valid ? a.queries[q] : make_float4(0.f, 0.f, 0.f, 0.f);
       const float q0 = qv.x / (float)G.ls[0], q1 = qv.y / (float)G.ls[1];
       const float q2 = qv.z / (float)G.ls[2], q3 = qv.w / (float)G.ls[3];
@@ -535,6 +540,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
           const int row_off = (m >> 3) * (SBO / 4) + (m & 7) * 4;
 #pragma unroll
           for (int cc = 0; cc < SUBS; ++cc) {
+            if (!present) break;  // a lone tile's partner: nothing to produce, still arrive
             const int c = SUBS * h + cc;
             float hi[4], lo[4];
             const int i0 = kb * KC + c * 4;  // four consecutive points: one LDS.128 per input row
@@ -572,7 +578,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
     const int e = warp - 4;  // TMEM lanes 32e..32e+31 (warp % 4 == e)
     const int m = e * 32 + lane;
     uint32_t uc = 0;
-    for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
+    for (int t0 = tb; t0 < te; t0 += TPC) {
+      const int ntile = min(TPC, te - t0);
       double ssqs[TPC];
 #pragma unroll
       for (int tt = 0; tt < TPC; ++tt) ssqs[tt] = 0.0;
@@ -585,6 +592,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
         tc_after();
 #pragma unroll
         for (int tt = 0; tt < TPC; ++tt) {
+        if (tt >= ntile) continue;
         double ssq = 0.0;
         const uint32_t trow = tmem_base + ((uint32_t)(e * 32) << 16) + (uint32_t)(tt * NP);
         int c = (dbg & 8) ? npw : 0;
@@ -617,8 +625,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
       }
 #pragma unroll
       for (int tt = 0; tt < TPC; ++tt) {
-        const long long q = ((long long)unit * TPC + tt) * M + m;
-        if (q < a.KT) {
+        const long long q = (long long)(t0 + tt) * M + m;
+        if (tt < ntile && q < a.KT) {
           double var = G.sv - ssqs[tt];  // gp.cpp:187-191
           var = var > 0.0 ? var : 0.0;
           const double c = a.coef * var;
@@ -701,7 +709,7 @@ cudaError_t launch_tc_variance(const VarianceArgs& a, int one_pass, cudaStream_t
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long tiles = (a.KT + tc::M - 1) / tc::M;
   const long long units = (tiles + tpc - 1) / tpc;
-  const int grid = (int)(units < sms ? units : sms);
+  const int grid = (int)(units < sms ? units : sms);  // every CTA gets >= tpc tiles when units >= sms
   static int dbg = -1;
   if (dbg < 0) {
     const char* e = getenv("GPMPPI_TC_DEBUG");
