@@ -542,6 +542,7 @@ struct gpmppi_planner {
   std::vector<void*> allocs;
   double *d_nom = nullptr, *d_tw = nullptr, *d_x0 = nullptr, *d_rbar = nullptr, *d_margins = nullptr;
   double* d_eps = nullptr;
+  double* d_noise = nullptr;  // Philox noise drawn by the rollout, read back by the reduce [B][K][T][2]
   gpm::TaskDev* d_task = nullptr;
   double *d_cost_mean = nullptr, *d_var = nullptr, *d_costs = nullptr, *d_e = nullptr;
   float4* d_queries = nullptr;
@@ -600,6 +601,7 @@ struct gpmppi_planner {
     d_coll = dalloc<uint32_t>((size_t)S * words);
     d_term = dalloc<uint8_t>(S);
     d_alive = dalloc<uint8_t>(S);
+    d_noise = dalloc<double>((size_t)S * T * 2);
     if (model_kind == GPMPPI_MODEL_GP_ENSEMBLE) {
       d_queries = dalloc<float4>((size_t)S * T);
       d_var = dalloc<double>((size_t)groups() * S * T);
@@ -798,6 +800,7 @@ void enqueue_samples(gpmppi_planner* p, int finish, cudaEvent_t* evs) {
   a.sw = std::sqrt(p->cfg.sigma_w2);
   a.noise_mode = p->noise_mode;
   a.eps = p->d_eps;
+  a.noise_out = p->noise_mode == gpm::NOISE_PHILOX ? p->d_noise : nullptr;
   a.nominal_seq = p->d_nom;
   a.tw = p->d_tw;
   a.R = p->R;
@@ -846,8 +849,9 @@ void enqueue_samples(gpmppi_planner* p, int finish, cudaEvent_t* evs) {
   r.tw = p->d_tw;
   std::memcpy(r.coef_terrain, p->coef_terrain, sizeof r.coef_terrain);
   r.x0 = p->d_x0;
-  r.noise_mode = p->noise_mode;
-  r.eps = p->d_eps;
+  // Philox mode: the rollout materialised the noise, so the reduce reads it like injected noise
+  r.noise_mode = p->d_noise && p->noise_mode == gpm::NOISE_PHILOX ? gpm::NOISE_INJECTED : p->noise_mode;
+  r.eps = p->noise_mode == gpm::NOISE_PHILOX ? p->d_noise : p->d_eps;
   r.sv = a.sv;
   r.sw = a.sw;
   r.costs_out = p->d_costs;

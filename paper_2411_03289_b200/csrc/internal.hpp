@@ -63,6 +63,7 @@ struct RolloutArgs {
   double sv, sw;  // noise standard deviations
   int noise_mode;
   const double* eps;  // injected [B][K_local][T][2]
+  double* noise_out;  // Philox mode: the drawn noise, same layout (the reduce reads it back)
   const double* nominal_seq;  // [B][2T]
   const double* tw;           // [B][kMaxTerrains]
   int R;

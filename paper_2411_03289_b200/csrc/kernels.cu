@@ -370,7 +370,11 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
       const int j = SPG == 1 ? 0 : idx / T, k = SPG == 1 ? idx : idx % T;
       const bool vj = j == 0 ? valid[0] : valid[SPG - 1];
       double e0 = 0.0, e1 = 0.0;
-      if (vj) sample_noise(a, key, j == 0 ? sl[0] : sl[SPG - 1], j == 0 ? s[0] : s[SPG - 1], k, &e0, &e1);
+      const long long slj = j == 0 ? sl[0] : sl[SPG - 1];
+      if (vj) {
+        sample_noise(a, key, slj, j == 0 ? s[0] : s[SPG - 1], k, &e0, &e1);
+        if (a.noise_out) reinterpret_cast<double2*>(a.noise_out)[(size_t)slj * T + k] = make_double2(e0, e1);
+      }
       const double u0 = clampd(sv.nom[2 * k] + e0, a.lo[0], a.hi[0]);
       const double u1 = clampd(sv.nom[2 * k + 1] + e1, a.lo[1], a.hi[1]);
       ubuf[j * T + k] = make_double2(u0, u1);
@@ -532,6 +536,7 @@ __global__ void __launch_bounds__(128) rollout_base_kernel(const RolloutArgs a) 
     for (int k = 0; k < T; ++k) {
       double e0, e1;
       sample_noise(a, key, sl, s, k, &e0, &e1);
+      if (a.noise_out) reinterpret_cast<double2*>(a.noise_out)[(size_t)sl * T + k] = make_double2(e0, e1);
       const double u[2] = {clampd(sv.nom[2 * k] + e0, a.lo[0], a.hi[0]),
                            clampd(sv.nom[2 * k + 1] + e1, a.lo[1], a.hi[1])};
       double nx[5];
