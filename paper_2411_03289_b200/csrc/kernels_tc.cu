@@ -234,6 +234,57 @@ __device__ __forceinline__ void mma_chunk_pair_3x(uint32_t d, uint32_t dt, uint6
       "r"(acc), "r"(bar_b0), "r"(bar_b1), "r"(bar_a)
       : "memory");
 }
+// Unified-stage variants: the chunk's A and both B blocks live in one ring stage, so a
+// single commit releases it. d1 = d + dt is the second tile's accumulator.
+__device__ __forceinline__ void mma_stage_pair_3x(uint32_t d, uint32_t dt, uint64_t a0hi, uint64_t a0lo,
+                                                  uint64_t a1hi, uint64_t a1lo, uint64_t bh0, uint64_t bl0,
+                                                  uint64_t bh1, uint64_t bl1, uint32_t idesc, uint32_t acc,
+                                                  uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 d1;\n\t.reg .b64 x0h, x0l, x1h, x1l;\n\t"
+      "add.u32 d1, %0, %1;\n\t"
+      "add.s64 x0h, %2, 16;\n\t"
+      "add.s64 x0l, %3, 16;\n\t"
+      "add.s64 x1h, %4, 16;\n\t"
+      "add.s64 x1l, %5, 16;\n\t"
+      "setp.ne.b32 p, %11, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %6, %10, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %7, %10, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %3, %6, %10, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], %4, %6, %10, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], %4, %7, %10, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], %5, %6, %10, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], x0h, %8, %10, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], x0h, %9, %10, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], x0l, %8, %10, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], x1h, %8, %10, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], x1h, %9, %10, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], x1l, %8, %10, 1;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%12];\n\t}" ::"r"(d),
+      "r"(dt), "l"(a0hi), "l"(a0lo), "l"(a1hi), "l"(a1lo), "l"(bh0), "l"(bl0), "l"(bh1), "l"(bl1), "r"(idesc),
+      "r"(acc), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mma_stage_single_3x(uint32_t d, uint64_t ahi, uint64_t alo, uint64_t bh0,
+                                                    uint64_t bl0, uint64_t bh1, uint64_t bl1, uint32_t idesc,
+                                                    uint32_t acc, uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 ah1, al1;\n\t"
+      "add.s64 ah1, %1, 16;\n\t"
+      "add.s64 al1, %2, 16;\n\t"
+      "setp.ne.b32 p, %8, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %3, %7, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %4, %7, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %7, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah1, %5, %7, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah1, %6, %7, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al1, %5, %7, 1;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%9];\n\t}" ::"r"(d),
+      "l"(ahi), "l"(alo), "l"(bh0), "l"(bl0), "l"(bh1), "l"(bl1), "r"(idesc), "r"(acc), "r"(bar)
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
@@ -652,6 +703,248 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
                  : "memory");
 }
 
+// Unified-stage two-tile kernel (3xTF32, NP <= 256): every ring stage holds one
+// 16-point chunk of both tiles' k* (hi/lo) and the chunk's two 8-point L^{-T} blocks.
+// A stage is filled by the 8 producer warps plus one bulk copy (one full barrier:
+// 8 arrivals + the copy's transaction bytes) and released by one MMA commit, so a
+// chunk costs one wait and one commit in the MMA warp instead of three of each
+// (the per-chunk hand-offs, not the tensor pipe, bounded the split-ring kernel).
+__global__ void __launch_bounds__(tc::THREADS, 1) variance_tc2u_kernel(const VarianceArgs a, int dbg, int S) {
+  using namespace tc;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const GroupDev& G = a.g;
+  const int n = a.n, n_pad = G.tc_npad, NP = G.tc_np, n_pass = G.tc_npass;
+  constexpr int A_FLOATS = 2 * 2 * A_STAGE_FLOATS;  // two tiles x (hi, lo)
+  const int stage_floats = A_FLOATS + 2 * 2 * NP * KB;
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  float* stg = reinterpret_cast<float*>(base);          // [S][A | B]
+  float* zs = stg + (size_t)S * stage_floats;           // [5][n_pad]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(zs + 5 * n_pad);
+  uint64_t* full = bars;
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  if (threadIdx.x == 0) trace_at(0, dbg);
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int n_tiles = (int)((a.KT + M - 1) / M);
+  const int tb = (int)((long long)blockIdx.x * n_tiles / gridDim.x);
+  const int te = (int)((long long)(blockIdx.x + 1) * n_tiles / gridDim.x);
+  const float L2E = 1.4426950408889634f;
+  for (int i = threadIdx.x; i < n_pad; i += blockDim.x) {
+    float z[4], sq = 0.f;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      z[d] = i < n ? G.zs32[(size_t)d * n + i] : 0.f;
+      sq += z[d] * z[d];
+    }
+#pragma unroll
+    for (int d = 0; d < 4; ++d) zs[d * n_pad + i] = L2E * z[d];
+    zs[4 * n_pad + i] = i < n ? L2E * (-0.5f * sq + (float)G.log_sv) : -1e30f;
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(smem_u32(&full[s]), PRODUCER_WARPS + 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    mbar_init(smem_u32(tfull), 1);
+    mbar_init(smem_u32(tempty), 4);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  if (threadIdx.x == 0) trace_at(1, dbg);
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- B producer: one bulk copy per chunk (its two 8-point blocks are
+    // adjacent in the pre-tiled operand)
+    Ring r(S);
+    int ti = 0;
+    for (int t0 = tb; t0 < te; t0 += 2, ++ti) {
+      if (ti < 10) trace_at(48 + ti, dbg);
+      int m = 0;  // block index in the per-unit sequence
+      for (int p = 0; p < n_pass; ++p) {
+        const int nk = pass_chunks(p, NP, n_pad);
+        for (int kb = 0; kb < nk; ++kb, m += 2, r.next()) {
+          const int4 meta = G.tc_meta[m];
+          mbar_wait(smem_u32(&empty[r.s]), r.ph ^ 1);
+          const uint32_t bytes = (uint32_t)meta.y * KB * 4 * 2 * 2;
+          const uint32_t fb = smem_u32(&full[r.s]);
+          if (dbg & 1) {
+            mbar_arrive(fb);
+          } else {
+            mbar_arrive_tx(fb, bytes);
+            bulk_g2s(smem_u32(stg + (size_t)r.s * stage_floats + A_FLOATS), G.tc_b + meta.x, bytes, fb);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (converged warp, elect.sync inside the statements)
+    Ring r(S);
+    uint32_t uc = 0;
+    for (int t0 = tb; t0 < te; t0 += 2) {
+      const bool two = t0 + 1 < te;
+      for (int p = 0; p < n_pass; ++p, ++uc) {
+        mbar_wait(smem_u32(tempty), (uc & 1) ^ 1);  // epilogue drained the accumulators
+        tc_after();
+        if (lane == 0 && uc < 10) trace_at(2 + 2 * (int)uc, dbg);
+        const int nk = pass_chunks(p, NP, n_pad);
+        const int npw = min(NP, n_pad - p * NP);
+        for (int kb = 0; kb < nk; ++kb, r.next()) {
+          mbar_wait(smem_u32(&full[r.s]), r.ph);
+          const int col0 = max(0, kb * KC - p * NP);
+          const int ncols = npw - col0;
+          const uint32_t st = smem_u32(stg + (size_t)r.s * stage_floats);
+          const uint32_t bh0 = st + A_FLOATS * 4;
+          const uint32_t blk = (uint32_t)ncols * KB * 4;  // bytes of one hi (or lo) block
+          const uint32_t bar = smem_u32(&empty[r.s]);
+          if (dbg & 4) {
+            mma_commit(bar);
+            continue;
+          }
+          if (two)
+            mma_stage_pair_3x(tmem_base + (uint32_t)col0, (uint32_t)NP, smem_desc(st), smem_desc(st + A_STAGE_FLOATS * 4),
+                              smem_desc(st + 2 * A_STAGE_FLOATS * 4), smem_desc(st + 3 * A_STAGE_FLOATS * 4),
+                              smem_desc(bh0, SBO_B), smem_desc(bh0 + blk, SBO_B), smem_desc(bh0 + 2 * blk, SBO_B),
+                              smem_desc(bh0 + 3 * blk, SBO_B), instr_desc(ncols), kb > 0 ? 1u : 0u, bar);
+          else
+            mma_stage_single_3x(tmem_base + (uint32_t)col0, smem_desc(st), smem_desc(st + A_STAGE_FLOATS * 4),
+                                smem_desc(bh0, SBO_B), smem_desc(bh0 + blk, SBO_B), smem_desc(bh0 + 2 * blk, SBO_B),
+                                smem_desc(bh0 + 3 * blk, SBO_B), instr_desc(ncols), kb > 0 ? 1u : 0u, bar);
+        }
+        mma_commit(smem_u32(tfull));
+        if (lane == 0 && uc < 10) trace_at(3 + 2 * (int)uc, dbg);
+      }
+    }
+  } else if (warp >= 8) {
+    // ---------------- A producers: one warp per 32 rows of tile pw / 4, 16 points per chunk
+    const int pw = warp - 8;
+    const int m = (pw & 3) * 32 + lane;
+    const int t = pw >> 2;
+    Ring r(S);
+    int ti = 0;
+    for (int t0 = tb; t0 < te; t0 += 2, ++ti) {
+      if (pw == 0 && lane == 0 && ti < 10) trace_at(36 + ti, dbg);
+      const bool present = t0 + t < te;
+      const long long q = (long long)(t0 + t) * M + m;
+      const bool valid = present && q < a.KT;
+      float4 qv = valid ? a.queries[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float q0 = qv.x / (float)G.ls[0], q1 = qv.y / (float)G.ls[1];
+      const float q2 = qv.z / (float)G.ls[2], q3 = qv.w / (float)G.ls[3];
+      const float qn = valid ? -0.5f * L2E * (q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3) : -1e30f;
+      for (int p = 0; p < n_pass; ++p) {
+        const int nk = pass_chunks(p, NP, n_pad);
+        for (int kb = 0; kb < nk; ++kb, r.next()) {
+          if (lane == 0) mbar_wait(smem_u32(&empty[r.s]), r.ph ^ 1);
+          __syncwarp();
+          if (present && !(dbg & 256)) {
+            float* ahi = stg + (size_t)r.s * stage_floats + (size_t)t * 2 * A_STAGE_FLOATS;
+            float* alo = ahi + A_STAGE_FLOATS;
+            const int row_off = (m >> 3) * (SBO / 4) + (m & 7) * 4;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const int i0 = kb * KC + c * 4;
+              const float4 z0 = *reinterpret_cast<const float4*>(zs + i0);
+              const float4 z1 = *reinterpret_cast<const float4*>(zs + n_pad + i0);
+              const float4 z2 = *reinterpret_cast<const float4*>(zs + 2 * n_pad + i0);
+              const float4 z3 = *reinterpret_cast<const float4*>(zs + 3 * n_pad + i0);
+              const float4 zq = *reinterpret_cast<const float4*>(zs + 4 * n_pad + i0);
+              const float za[4][5] = {{z0.x, z1.x, z2.x, z3.x, zq.x}, {z0.y, z1.y, z2.y, z3.y, zq.y},
+                                      {z0.z, z1.z, z2.z, z3.z, zq.z}, {z0.w, z1.w, z2.w, z3.w, zq.w}};
+              float hi[4], lo[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float x = fmaf(q0, za[e][0], fmaf(q1, za[e][1], fmaf(q2, za[e][2], fmaf(q3, za[e][3], qn + za[e][4]))));
+                const float kv = exp2f_approx(x);
+                hi[e] = tf32_rna(kv);
+                lo[e] = kv - hi[e];
+              }
+              *reinterpret_cast<float4*>(ahi + row_off + c * 32) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+              *reinterpret_cast<float4*>(alo + row_off + c * 32) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+            }
+            fence_proxy_async();
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&full[r.s]));
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: TMEM -> sum a_j^2 -> var, both tiles
+    const int e = warp - 4;
+    const int m = e * 32 + lane;
+    uint32_t uc = 0;
+    for (int t0 = tb; t0 < te; t0 += 2) {
+      const int ntile = min(2, te - t0);
+      double ssqs[2] = {0.0, 0.0};
+      for (int p = 0; p < n_pass; ++p, ++uc) {
+        const int npw = min(NP, n_pad - p * NP);
+        if (lane == 0) mbar_wait(smem_u32(tfull), uc & 1);
+        if (lane == 0 && e == 0 && uc < 10) trace_at(24 + (int)uc, dbg);
+        __syncwarp();
+        tc_after();
+        for (int tt = 0; tt < ntile; ++tt) {
+          const uint32_t trow = tmem_base + ((uint32_t)(e * 32) << 16) + (uint32_t)(tt * NP);
+          double ssq = 0.0;
+          int c = (dbg & 8) ? npw : 0;
+          for (; c + 64 <= npw; c += 64) {
+            uint32_t rr[64];
+            tmem_ld16_nowait(trow + c, rr);
+            tmem_ld16_nowait(trow + c + 16, rr + 16);
+            tmem_ld16_nowait(trow + c + 32, rr + 32);
+            tmem_ld16_nowait(trow + c + 48, rr + 48);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            float part = 0.f;
+#pragma unroll
+            for (int i = 0; i < 64; ++i) part = fmaf(__uint_as_float(rr[i]), __uint_as_float(rr[i]), part);
+            ssq += (double)part;
+          }
+          for (; c < npw; c += 16) {
+            float v[16];
+            tmem_ld16(trow + c, v);
+            float part = 0.f;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) part = fmaf(v[i], v[i], part);
+            ssq += (double)part;
+          }
+          ssqs[tt] += ssq;
+        }
+        tc_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(tempty));
+      }
+      for (int tt = 0; tt < ntile; ++tt) {
+        const long long q = (long long)(t0 + tt) * M + m;
+        if (q < a.KT) {
+          double var = G.sv - ssqs[tt];  // gp.cpp:187-191
+          var = var > 0.0 ? var : 0.0;
+          const double c = a.coef * var;
+          a.trace[q] = a.accumulate ? a.trace[q] + c : c;
+        }
+      }
+    }
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (threadIdx.x == 0) trace_at(63, dbg);
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512) : "memory");
+}
+
+size_t tc2u_smem_bytes(const GroupDev& g, int stages) {
+  return 1024 + sizeof(float) * ((size_t)stages * (2 * 2 * tc::A_STAGE_FLOATS + 2 * 2 * g.tc_np * tc::KB) + 5 * (size_t)g.tc_npad) +
+         sizeof(uint64_t) * (2 * stages + 2) + 16;
+}
+
 size_t tc_smem_bytes(const GroupDev& g, int stages_a, int stages_b, int tpc) {
   size_t b = 1024;  // alignment slack
   b += sizeof(float) * (size_t)stages_a * tpc * 2 * tc::A_STAGE_FLOATS;
@@ -701,6 +994,32 @@ cudaError_t launch_tc_variance(const VarianceArgs& a, int one_pass, cudaStream_t
   if (sa_env >= 2) SA = std::min(SA, sa_env);
   while (SB > 2 && tc_smem_bytes(a.g, SA, SB, tpc) > kSmemMax) --SB;
   const size_t smem = tc_smem_bytes(a.g, SA, SB, tpc);
+  static int uni_env = -1;  // GPMPPI_TC_UNIFIED=0 keeps the split A/B rings
+  if (uni_env < 0) {
+    const char* e = getenv("GPMPPI_TC_UNIFIED");
+    uni_env = e ? atoi(e) : 1;
+  }
+  int stages = 6;
+  while (stages > 3 && tc2u_smem_bytes(a.g, stages) > kSmemMax) --stages;
+  if (tpc == 2 && uni_env != 0 && tc2u_smem_bytes(a.g, stages) <= kSmemMax) {
+    const size_t usm = tc2u_smem_bytes(a.g, stages);
+    cudaError_t eu = cudaFuncSetAttribute(variance_tc2u_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm);
+    if (eu != cudaSuccess) return eu;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long tiles = (a.KT + tc::M - 1) / tc::M;
+    const long long units = (tiles + 1) / 2;
+    const int grid = (int)(units < sms ? units : sms);
+    static int dbg_u = -1;
+    if (dbg_u < 0) {
+      const char* e = getenv("GPMPPI_TC_DEBUG");
+      dbg_u = e ? atoi(e) : 0;
+    }
+    variance_tc2u_kernel<<<grid, tc::THREADS, usm, st>>>(a, dbg_u, stages);
+    count_launch();
+    return cudaGetLastError();
+  }
   void (*kern)(const VarianceArgs, int, int, int, int) = tpc == 2 ? variance_tc_kernel<2> : variance_tc_kernel<1>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
