@@ -825,21 +825,35 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc2u_kernel(const Var
       }
     }
   } else if (warp >= 8) {
-    // ---------------- A producers: one warp per 32 rows of tile pw / 4, 16 points per chunk
+    // ---------------- A producers: one warp per 32 rows of tile pw / 4, 16 points per
+    // chunk. Lane (qi, pg) owns rows qi + 8j (j < 4) x points 4pg..4pg+3 of the chunk:
+    // the query terms stay in registers for the whole tile and a lane reads only its
+    // 4 points' 5 coordinates per chunk (5 LDS.128, 20 wavefronts per warp instead of
+    // 80 when every lane walks all 16 points); each quarter-warp's STS.128 covers one
+    // 128-byte row group of the canonical layout (conflict-free).
     const int pw = warp - 8;
-    const int m = (pw & 3) * 32 + lane;
     const int t = pw >> 2;
+    const int qi = lane & 7, pg = lane >> 3;
+    const int mb = (pw & 3) * 32 + qi;
     Ring r(S);
     int ti = 0;
     for (int t0 = tb; t0 < te; t0 += 2, ++ti) {
       if (pw == 0 && lane == 0 && ti < 10) trace_at(36 + ti, dbg);
       const bool present = t0 + t < te;
-      const long long q = (long long)(t0 + t) * M + m;
-      const bool valid = present && q < a.KT;
-      float4 qv = valid ? a.queries[q] : make_float4(0.f, 0.f, 0.f, 0.f);
-      const float q0 = qv.x / (float)G.ls[0], q1 = qv.y / (float)G.ls[1];
-      const float q2 = qv.z / (float)G.ls[2], q3 = qv.w / (float)G.ls[3];
-      const float qn = valid ? -0.5f * L2E * (q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3) : -1e30f;
+      float qq[4][5];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const long long q = (long long)(t0 + t) * M + mb + 8 * j;
+        const bool valid = present && q < a.KT;
+        const float4 qv = valid ? a.queries[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+        qq[j][0] = qv.x / (float)G.ls[0];
+        qq[j][1] = qv.y / (float)G.ls[1];
+        qq[j][2] = qv.z / (float)G.ls[2];
+        qq[j][3] = qv.w / (float)G.ls[3];
+        qq[j][4] = valid ? -0.5f * L2E * (qq[j][0] * qq[j][0] + qq[j][1] * qq[j][1] + qq[j][2] * qq[j][2] +
+                                          qq[j][3] * qq[j][3])
+                         : -1e30f;
+      }
       for (int p = 0; p < n_pass; ++p) {
         const int nk = pass_chunks(p, NP, n_pad);
         for (int kb = 0; kb < nk; ++kb, r.next()) {
@@ -848,27 +862,29 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc2u_kernel(const Var
           if (present && !(dbg & 256)) {
             float* ahi = stg + (size_t)r.s * stage_floats + (size_t)t * 2 * A_STAGE_FLOATS;
             float* alo = ahi + A_STAGE_FLOATS;
-            const int row_off = (m >> 3) * (SBO / 4) + (m & 7) * 4;
+            const int i0 = kb * KC + pg * 4;
+            const float4 z0 = *reinterpret_cast<const float4*>(zs + i0);
+            const float4 z1 = *reinterpret_cast<const float4*>(zs + n_pad + i0);
+            const float4 z2 = *reinterpret_cast<const float4*>(zs + 2 * n_pad + i0);
+            const float4 z3 = *reinterpret_cast<const float4*>(zs + 3 * n_pad + i0);
+            const float4 zq = *reinterpret_cast<const float4*>(zs + 4 * n_pad + i0);
+            const float za[4][5] = {{z0.x, z1.x, z2.x, z3.x, zq.x}, {z0.y, z1.y, z2.y, z3.y, zq.y},
+                                    {z0.z, z1.z, z2.z, z3.z, zq.z}, {z0.w, z1.w, z2.w, z3.w, zq.w}};
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              const int i0 = kb * KC + c * 4;
-              const float4 z0 = *reinterpret_cast<const float4*>(zs + i0);
-              const float4 z1 = *reinterpret_cast<const float4*>(zs + n_pad + i0);
-              const float4 z2 = *reinterpret_cast<const float4*>(zs + 2 * n_pad + i0);
-              const float4 z3 = *reinterpret_cast<const float4*>(zs + 3 * n_pad + i0);
-              const float4 zq = *reinterpret_cast<const float4*>(zs + 4 * n_pad + i0);
-              const float za[4][5] = {{z0.x, z1.x, z2.x, z3.x, zq.x}, {z0.y, z1.y, z2.y, z3.y, zq.y},
-                                      {z0.z, z1.z, z2.z, z3.z, zq.z}, {z0.w, z1.w, z2.w, z3.w, zq.w}};
+            for (int j = 0; j < 4; ++j) {
               float hi[4], lo[4];
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
-                const float x = fmaf(q0, za[e][0], fmaf(q1, za[e][1], fmaf(q2, za[e][2], fmaf(q3, za[e][3], qn + za[e][4]))));
+                const float x = fmaf(qq[j][0], za[e][0],
+                                     fmaf(qq[j][1], za[e][1],
+                                          fmaf(qq[j][2], za[e][2], fmaf(qq[j][3], za[e][3], qq[j][4] + za[e][4]))));
                 const float kv = exp2f_approx(x);
                 hi[e] = tf32_rna(kv);
                 lo[e] = kv - hi[e];
               }
-              *reinterpret_cast<float4*>(ahi + row_off + c * 32) = make_float4(hi[0], hi[1], hi[2], hi[3]);
-              *reinterpret_cast<float4*>(alo + row_off + c * 32) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+              const int off = (((pw & 3) * 32 + 8 * j) >> 3) * (SBO / 4) + pg * 32 + qi * 4;
+              *reinterpret_cast<float4*>(ahi + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+              *reinterpret_cast<float4*>(alo + off) = make_float4(lo[0], lo[1], lo[2], lo[3]);
             }
             fence_proxy_async();
           }
