@@ -216,7 +216,7 @@ int gpmppi_planner_flags(const gpmppi_planner* p, uint8_t* viol, uint8_t* coll,
                          uint8_t* terminal, uint8_t* alive);
 
 /* ---- variance path (north star: tensor cores only where tolerance allows) ---- */
-enum { GPMPPI_VAR_FFMA = 0, GPMPPI_VAR_TC_3XTF32 = 1, GPMPPI_VAR_TC_1XTF32 = 2 };
+enum { GPMPPI_VAR_FFMA = 0, GPMPPI_VAR_TC_3XTF32 = 1, GPMPPI_VAR_TC_1XTF32 = 2, GPMPPI_VAR_TC_3XF16 = 3 };
 int gpmppi_planner_set_variance_path(gpmppi_planner* p, int path);
 int gpmppi_planner_variance_path(const gpmppi_planner* p);
 

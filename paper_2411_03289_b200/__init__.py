@@ -9,6 +9,6 @@ from .gpmppi import (  # noqa: F401
     kernel_launches, shard_range, tuple_doubles, RolloutResult, rollout, sample_perturbations,
     trajectory_weights, update_controls, shift_horizon, TrainedModels, load_models, save_models)
 from ._capi import (  # noqa: F401
-    NOISE_INJECTED, NOISE_PHILOX, VAR_FFMA, VAR_TC_1XTF32, VAR_TC_3XTF32, CudaError)
+    NOISE_INJECTED, NOISE_PHILOX, VAR_FFMA, VAR_TC_1XTF32, VAR_TC_3XF16, VAR_TC_3XTF32, CudaError)
 
 __version__ = "0.1.0"

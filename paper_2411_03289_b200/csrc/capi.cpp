@@ -299,6 +299,11 @@ gpmppi_model* build_model(const double* X, const double* Y, int64_t n64, int64_t
         gpm::build_tc_operand(G.ilt.data(), n, tcd, tcm, D.tc_npad, D.tc_np, D.tc_npass);
         D.tc_b = M->upload(tcd);
         D.tc_meta = M->upload(tcm);
+        std::vector<uint16_t> tch;
+        std::vector<int4> tchm;
+        gpm::build_tc_operand_f16(G.ilt.data(), n, G.kernel[0], D.tc_npad, D.tc_np, D.tc_npass, tch, tchm, D.tc_hfac);
+        D.tc_h = M->upload(tch);
+        D.tc_hmeta = M->upload(tchm);
       }
       for (int d = 0; d < 4; ++d) D.ls[d] = G.kernel[1 + d];
       D.sv = G.kernel[0];
@@ -477,7 +482,7 @@ int gpmppi_model_predict_batch(const gpmppi_model* M, const double* q, int64_t S
 int gpmppi_model_variance_batch(const gpmppi_model* M, const double* q, int64_t S, int path,
                                 double* var) {
   if (!M) return fail(GPMPPI_LOGIC_ERROR, "GpModel::predict_batch: model not fitted");
-  if (S < 0 || path < 0 || path > 2) return fail(GPMPPI_INVALID_ARGUMENT, "variance_batch: bad arguments");
+  if (S < 0 || path < 0 || path > 3) return fail(GPMPPI_INVALID_ARGUMENT, "variance_batch: bad arguments");
   if (S == 0) return GPMPPI_OK;
   return guarded([&] {
     CK(cudaSetDevice(M->device));
@@ -530,7 +535,7 @@ struct gpmppi_planner {
   uint64_t tick = 0;
   int noise_mode = gpm::NOISE_PHILOX;
   bool injected_set = false;
-  int var_path = GPMPPI_VAR_TC_3XTF32;  // tensor cores within the stated tolerance
+  int var_path = GPMPPI_VAR_TC_3XF16;  // tensor cores within the stated tolerance
   long long s_begin = 0, K_local = 0, K_total = 0;
   std::vector<uint8_t> rbar_init;  // [B]
   std::vector<int> margins_O;      // [B] obstacle count the margins were sized for
@@ -1350,7 +1355,7 @@ int gpmppi_planner_flags(const gpmppi_planner* p, uint8_t* viol, uint8_t* coll, 
 
 int gpmppi_planner_set_variance_path(gpmppi_planner* p, int path) {
   if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
-  if (path < 0 || path > 2) return fail(GPMPPI_INVALID_ARGUMENT, "unknown variance path");
+  if (path < 0 || path > 3) return fail(GPMPPI_INVALID_ARGUMENT, "unknown variance path");
   p->var_path = path;
   return GPMPPI_OK;
 }

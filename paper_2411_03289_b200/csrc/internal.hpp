@@ -21,6 +21,9 @@ struct GroupDev {
   const float* tc_b;   // tensor-core operand: L^{-T} hi/lo TF32 tiles (see kernels_tc.cu)
   const int4* tc_meta; // per (pass, chunk): float offset, ncols, col0
   int tc_npad, tc_np, tc_npass;
+  const uint16_t* tc_h;  // 3xFP16 operand: scaled L^{-T} hi/lo FP16 blocks (build_tc_operand_f16)
+  const int4* tc_hmeta;  // per (pass, chunk): fp16 offset, ncols, col0
+  double tc_hfac;        // (sf2 / operand scale)^2
   double ls[4];
   double sv, log_sv;
   int n_out;
@@ -169,6 +172,8 @@ size_t rollout_smem_bytes(const RolloutArgs& a);
 size_t rollout_scratch_doubles(int T, int num_sms);
 int reduce_blocks_for(int K_local, int B, int num_sms);
 int tighten_splits(int n);
+void build_tc_operand_f16(const double* ilt, int n, double sv, int n_pad, int np, int n_pass,
+                          std::vector<uint16_t>& data, std::vector<int4>& meta, double& hfac);
 void build_tc_operand(const double* ilt, int n, std::vector<float>& data, std::vector<int4>& meta,
                       int& n_pad, int& np, int& n_pass);
 void tc_profile_read(double* out);

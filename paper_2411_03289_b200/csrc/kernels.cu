@@ -785,11 +785,11 @@ __global__ void __launch_bounds__(256) variance_ffma_kernel(const VarianceArgs a
   }
 }
 
-cudaError_t launch_tc_variance(const VarianceArgs& a, int one_pass, cudaStream_t st);  // kernels_tc.cu
+cudaError_t launch_tc_variance(const VarianceArgs& a, int mode, cudaStream_t st);  // kernels_tc.cu
 
 cudaError_t launch_variance(const VarianceArgs& a, int path, cudaStream_t st) {
   if (a.KT <= 0) return cudaSuccess;
-  if (path != 0) return launch_tc_variance(a, path == 2, st);
+  if (path != 0) return launch_tc_variance(a, path == 3 ? 2 : path == 2 ? 1 : 0, st);
   const long long blocks = (a.KT + VQ - 1) / VQ;
   variance_ffma_kernel<<<(unsigned)blocks, 256, 0, st>>>(a);
   count_launch();

@@ -18,9 +18,11 @@
 // Pipelines: smem rings (full_a/full_b -> MMA -> empty), TMEM (full -> epilogue -> empty).
 // B moves in 8-point K blocks (<= 32 KB hi+lo) through a 4-5 deep ring: the L2 ->
 // SMEM stream of L^{-T} is the kernel's critical feed, so it keeps ~100 KB in flight.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -956,6 +958,295 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc2u_kernel(const Var
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512) : "memory");
 }
 
+// ---------------------------------------------------------------------------
+// 3xFP16 variant (variance path GPMPPI_VAR_TC_3XF16). FP16 carries the same 11-bit
+// significand as TF32, so hi/lo FP16 splits give the same ~22-bit operands as
+// 3xTF32 once both operands are scaled into FP16's exponent range: A = k*/sf2 in
+// (0, 1] (exp without the ln sf2 term), B = L^{-T}·2^-e with max |B| <= 1 (one
+// power-of-two scale, build_tc_operand_f16). kind::f16 runs at twice the TF32
+// rate with K = 16 per MMA, so a 16-point chunk is ONE MMA per product (6 per
+// chunk for two tiles instead of 12), and every operand byte count halves (A 16 KB +
+// B 16 KB per stage), which also halves the shared-memory traffic that bounds the
+// TF32 kernel. The epilogue rescales: ||L^{-1}k*||^2 = (sf2 / 2^-e)^2 · Σ D^2.
+namespace tc {
+constexpr int H_TILE_BYTES = M * KC * 2;  // one tile's hi (or lo) chunk: 128 rows x 16 fp16
+constexpr int H_SBO = 256;                // 8-row groups: two 128-byte core matrices along K
+__device__ __forceinline__ uint32_t instr_desc_f16(int n) {
+  // kind::f16, D f32 ([4,6)=1), A/B F16 ([7,10)=0, [10,13)=0), K-major, N>>3 at [17,23), M>>4 at [24,29)
+  return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_f16_pair_3x(uint32_t d, uint32_t dt, uint64_t a0h, uint64_t a0l, uint64_t a1h,
+                                                uint64_t a1l, uint64_t bh, uint64_t bl, uint32_t idesc, uint32_t acc,
+                                                uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 d1;\n\t"
+      "add.u32 d1, %0, %1;\n\t"
+      "setp.ne.b32 p, %9, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %6, %8, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %7, %8, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %3, %6, %8, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [d1], %4, %6, %8, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [d1], %4, %7, %8, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [d1], %5, %6, %8, 1;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%10];\n\t}" ::"r"(d),
+      "r"(dt), "l"(a0h), "l"(a0l), "l"(a1h), "l"(a1l), "l"(bh), "l"(bl), "r"(idesc), "r"(acc), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mma_f16_single_3x(uint32_t d, uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl,
+                                                  uint32_t idesc, uint32_t acc, uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %3, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %4, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %3, %5, 1;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n\t}" ::"r"(d),
+      "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(acc), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t half2_bits(__half2 h) {
+  uint32_t u;
+  memcpy(&u, &h, 4);
+  return u;
+}
+}  // namespace tc
+
+__global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const VarianceArgs a, int dbg, int S) {
+  using namespace tc;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const GroupDev& G = a.g;
+  const int n = a.n, n_pad = G.tc_npad, NP = G.tc_np, n_pass = G.tc_npass;
+  constexpr int A_BYTES = 2 * 2 * H_TILE_BYTES;  // two tiles x (hi, lo)
+  const int stage_bytes = A_BYTES + 2 * NP * KC * 2;
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char* stg = base;                                            // [S][A | B]
+  float* zs = reinterpret_cast<float*>(stg + (size_t)S * stage_bytes);  // [5][n_pad]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(zs + 5 * n_pad);
+  uint64_t* full = bars;
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int n_tiles = (int)((a.KT + M - 1) / M);
+  const int tb = (int)((long long)blockIdx.x * n_tiles / gridDim.x);
+  const int te = (int)((long long)(blockIdx.x + 1) * n_tiles / gridDim.x);
+  const float L2E = 1.4426950408889634f;
+  for (int i = threadIdx.x; i < n_pad; i += blockDim.x) {
+    float z[4], sq = 0.f;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      z[d] = i < n ? G.zs32[(size_t)d * n + i] : 0.f;
+      sq += z[d] * z[d];
+    }
+#pragma unroll
+    for (int d = 0; d < 4; ++d) zs[d * n_pad + i] = L2E * z[d];
+    zs[4 * n_pad + i] = i < n ? L2E * (-0.5f * sq) : -1e30f;  // k*/sf2: no ln sf2 term
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(smem_u32(&full[s]), PRODUCER_WARPS + 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    mbar_init(smem_u32(tfull), 1);
+    mbar_init(smem_u32(tempty), 4);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- B producer: one bulk copy (hi + lo K=16 block) per chunk
+    Ring r(S);
+    for (int t0 = tb; t0 < te; t0 += 2) {
+      int m = 0;
+      for (int p = 0; p < n_pass; ++p) {
+        const int nk = pass_chunks(p, NP, n_pad);
+        for (int kb = 0; kb < nk; ++kb, ++m, r.next()) {
+          const int4 meta = G.tc_hmeta[m];
+          mbar_wait(smem_u32(&empty[r.s]), r.ph ^ 1);
+          const uint32_t bytes = (uint32_t)meta.y * KC * 2 * 2;
+          const uint32_t fb = smem_u32(&full[r.s]);
+          mbar_arrive_tx(fb, bytes);
+          bulk_g2s(smem_u32(stg + (size_t)r.s * stage_bytes + A_BYTES), G.tc_h + meta.x, bytes, fb);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    Ring r(S);
+    uint32_t uc = 0;
+    for (int t0 = tb; t0 < te; t0 += 2) {
+      const bool two = t0 + 1 < te;
+      for (int p = 0; p < n_pass; ++p, ++uc) {
+        mbar_wait(smem_u32(tempty), (uc & 1) ^ 1);
+        tc_after();
+        const int nk = pass_chunks(p, NP, n_pad);
+        const int npw = min(NP, n_pad - p * NP);
+        for (int kb = 0; kb < nk; ++kb, r.next()) {
+          mbar_wait(smem_u32(&full[r.s]), r.ph);
+          const int col0 = max(0, kb * KC - p * NP);
+          const int ncols = npw - col0;
+          const uint32_t st = smem_u32(stg + (size_t)r.s * stage_bytes);
+          const uint32_t bh = st + A_BYTES;
+          const uint32_t bl = bh + (uint32_t)ncols * KC * 2;
+          const uint32_t bar = smem_u32(&empty[r.s]);
+          if (dbg & 4) {
+            mma_commit(bar);
+            continue;
+          }
+          if (two)
+            mma_f16_pair_3x(tmem_base + (uint32_t)col0, (uint32_t)NP, smem_desc(st, H_SBO),
+                            smem_desc(st + H_TILE_BYTES, H_SBO), smem_desc(st + 2 * H_TILE_BYTES, H_SBO),
+                            smem_desc(st + 3 * H_TILE_BYTES, H_SBO), smem_desc(bh, H_SBO), smem_desc(bl, H_SBO),
+                            instr_desc_f16(ncols), kb > 0 ? 1u : 0u, bar);
+          else
+            mma_f16_single_3x(tmem_base + (uint32_t)col0, smem_desc(st, H_SBO), smem_desc(st + H_TILE_BYTES, H_SBO),
+                              smem_desc(bh, H_SBO), smem_desc(bl, H_SBO), instr_desc_f16(ncols), kb > 0 ? 1u : 0u,
+                              bar);
+        }
+        mma_commit(smem_u32(tfull));
+      }
+    }
+  } else if (warp >= 8) {
+    // ---------------- A producers (lane = 4 rows x 4 points, as variance_tc2u_kernel):
+    // k*/sf2 split into FP16 hi + lo, 8-byte stores covering 256 contiguous bytes per warp
+    const int pw = warp - 8;
+    const int t = pw >> 2;
+    const int qi = lane & 7, pg = lane >> 3;
+    const int mb = (pw & 3) * 32 + qi;
+    Ring r(S);
+    for (int t0 = tb; t0 < te; t0 += 2) {
+      const bool present = t0 + t < te;
+      float qq[4][5];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const long long q = (long long)(t0 + t) * M + mb + 8 * j;
+        const bool valid = present && q < a.KT;
+        const float4 qv = valid ? a.queries[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+        qq[j][0] = qv.x / (float)G.ls[0];
+        qq[j][1] = qv.y / (float)G.ls[1];
+        qq[j][2] = qv.z / (float)G.ls[2];
+        qq[j][3] = qv.w / (float)G.ls[3];
+        qq[j][4] = valid ? -0.5f * L2E * (qq[j][0] * qq[j][0] + qq[j][1] * qq[j][1] + qq[j][2] * qq[j][2] +
+                                          qq[j][3] * qq[j][3])
+                         : -1e30f;
+      }
+      for (int p = 0; p < n_pass; ++p) {
+        const int nk = pass_chunks(p, NP, n_pad);
+        for (int kb = 0; kb < nk; ++kb, r.next()) {
+          if (lane == 0) mbar_wait(smem_u32(&empty[r.s]), r.ph ^ 1);
+          __syncwarp();
+          if (present) {
+            unsigned char* ahi = stg + (size_t)r.s * stage_bytes + (size_t)t * 2 * H_TILE_BYTES;
+            unsigned char* alo = ahi + H_TILE_BYTES;
+            const int i0 = kb * KC + pg * 4;
+            const float4 z0 = *reinterpret_cast<const float4*>(zs + i0);
+            const float4 z1 = *reinterpret_cast<const float4*>(zs + n_pad + i0);
+            const float4 z2 = *reinterpret_cast<const float4*>(zs + 2 * n_pad + i0);
+            const float4 z3 = *reinterpret_cast<const float4*>(zs + 3 * n_pad + i0);
+            const float4 zq = *reinterpret_cast<const float4*>(zs + 4 * n_pad + i0);
+            const float za[4][5] = {{z0.x, z1.x, z2.x, z3.x, zq.x}, {z0.y, z1.y, z2.y, z3.y, zq.y},
+                                    {z0.z, z1.z, z2.z, z3.z, zq.z}, {z0.w, z1.w, z2.w, z3.w, zq.w}};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              float kv[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                kv[e] = exp2f_approx(fmaf(qq[j][0], za[e][0],
+                                          fmaf(qq[j][1], za[e][1],
+                                               fmaf(qq[j][2], za[e][2], fmaf(qq[j][3], za[e][3], qq[j][4] + za[e][4])))));
+              const __half2 h01 = __floats2half2_rn(kv[0], kv[1]), h23 = __floats2half2_rn(kv[2], kv[3]);
+              const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+              const __half2 l01 = __floats2half2_rn(kv[0] - f01.x, kv[1] - f01.y);
+              const __half2 l23 = __floats2half2_rn(kv[2] - f23.x, kv[3] - f23.y);
+              // row m = mb + 8j, points 4pg..4pg+3: byte (m>>3)*256 + (pg>>1)*128 + (m&7)*16 + (pg&1)*8
+              const int off = (((pw & 3) * 32 + 8 * j) >> 3) * H_SBO + (pg >> 1) * 128 + qi * 16 + (pg & 1) * 8;
+              *reinterpret_cast<uint2*>(ahi + off) = make_uint2(half2_bits(h01), half2_bits(h23));
+              *reinterpret_cast<uint2*>(alo + off) = make_uint2(half2_bits(l01), half2_bits(l23));
+            }
+            fence_proxy_async();
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&full[r.s]));
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: TMEM -> Σ D^2 -> var = sf2 - hfac·Σ D^2, both tiles
+    const int e = warp - 4;
+    const int m = e * 32 + lane;
+    uint32_t uc = 0;
+    for (int t0 = tb; t0 < te; t0 += 2) {
+      const int ntile = min(2, te - t0);
+      double ssqs[2] = {0.0, 0.0};
+      for (int p = 0; p < n_pass; ++p, ++uc) {
+        const int npw = min(NP, n_pad - p * NP);
+        if (lane == 0) mbar_wait(smem_u32(tfull), uc & 1);
+        __syncwarp();
+        tc_after();
+        for (int tt = 0; tt < ntile; ++tt) {
+          const uint32_t trow = tmem_base + ((uint32_t)(e * 32) << 16) + (uint32_t)(tt * NP);
+          double ssq = 0.0;
+          int c = 0;
+          for (; c + 64 <= npw; c += 64) {
+            uint32_t rr[64];
+            tmem_ld16_nowait(trow + c, rr);
+            tmem_ld16_nowait(trow + c + 16, rr + 16);
+            tmem_ld16_nowait(trow + c + 32, rr + 32);
+            tmem_ld16_nowait(trow + c + 48, rr + 48);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            float part = 0.f;
+#pragma unroll
+            for (int i = 0; i < 64; ++i) part = fmaf(__uint_as_float(rr[i]), __uint_as_float(rr[i]), part);
+            ssq += (double)part;
+          }
+          for (; c < npw; c += 16) {
+            float v[16];
+            tmem_ld16(trow + c, v);
+            float part = 0.f;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) part = fmaf(v[i], v[i], part);
+            ssq += (double)part;
+          }
+          ssqs[tt] += ssq;
+        }
+        tc_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(tempty));
+      }
+      for (int tt = 0; tt < ntile; ++tt) {
+        const long long q = (long long)(t0 + tt) * M + m;
+        if (q < a.KT) {
+          double var = G.sv - G.tc_hfac * ssqs[tt];  // gp.cpp:187-191
+          var = var > 0.0 ? var : 0.0;
+          const double c = a.coef * var;
+          a.trace[q] = a.accumulate ? a.trace[q] + c : c;
+        }
+      }
+    }
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512) : "memory");
+}
+
+size_t f16_smem_bytes(const GroupDev& g, int stages) {
+  return 1024 + (size_t)stages * (2 * 2 * tc::H_TILE_BYTES + 2 * (size_t)g.tc_np * tc::KC * 2) +
+         sizeof(float) * 5 * (size_t)g.tc_npad + sizeof(uint64_t) * (2 * stages + 2) + 16;
+}
+
 size_t tc2u_smem_bytes(const GroupDev& g, int stages) {
   return 1024 + sizeof(float) * ((size_t)stages * (2 * 2 * tc::A_STAGE_FLOATS + 2 * 2 * g.tc_np * tc::KB) + 5 * (size_t)g.tc_npad) +
          sizeof(uint64_t) * (2 * stages + 2) + 16;
@@ -984,9 +1275,33 @@ void tc_profile_read(double* out) {
   cudaMemcpyToSymbol(tc::g_prof, z, sizeof z);
 }
 
-cudaError_t launch_tc_variance(const VarianceArgs& a, int one_pass, cudaStream_t st) {
+// mode: 0 = 3xTF32, 1 = 1xTF32 (one pass), 2 = 3xFP16 (scaled operands)
+cudaError_t launch_tc_variance(const VarianceArgs& a, int mode, cudaStream_t st) {
   if (!a.g.tc_b || !a.g.tc_meta) return cudaErrorNotSupported;
   constexpr size_t kSmemMax = 227 * 1024;
+  const int one_pass = mode == 1;
+  static int dbg_h = -1;
+  if (dbg_h < 0) {
+    const char* e = getenv("GPMPPI_TC_DEBUG");
+    dbg_h = e ? atoi(e) : 0;
+  }
+  if (mode == 2 && a.g.tc_h && a.g.tc_hmeta && a.g.tc_np <= 256) {
+    int stages = 8;
+    while (stages > 3 && f16_smem_bytes(a.g, stages) > kSmemMax) --stages;
+    if (f16_smem_bytes(a.g, stages) <= kSmemMax) {
+      const size_t hsm = f16_smem_bytes(a.g, stages);
+      cudaError_t eh = cudaFuncSetAttribute(variance_f16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
+      if (eh != cudaSuccess) return eh;
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const long long units = ((a.KT + tc::M - 1) / tc::M + 1) / 2;
+      const int grid = (int)(units < sms ? units : sms);
+      variance_f16_kernel<<<grid, tc::THREADS, hsm, st>>>(a, dbg_h, stages);
+      count_launch();
+      return cudaGetLastError();
+    }
+  }
   static int sb_env = -1;  // diagnostics: GPMPPI_TC_SB forces the B ring depth
   if (sb_env < 0) {
     const char* e = getenv("GPMPPI_TC_SB");
@@ -1098,6 +1413,51 @@ void build_tc_operand(const double* ilt, int n, std::vector<float>& data, std::v
           const size_t o = (size_t)(r >> 3) * (KB / 4) * 32 + (size_t)(k >> 2) * 32 + (r & 7) * 4 + (k & 3);
           hi[o] = h;
           lo[o] = l;
+        }
+      }
+      meta.push_back(make_int4((int)off, ncols, col0, 0));
+    }
+  }
+}
+
+// Host: the 3xFP16 operand. One power-of-two scale 2^-e puts max |L^{-T}| in (1/2, 1];
+// per (pass, 16-point chunk) a hi block then a lo block of ncols x 16 FP16 in the
+// K-major canonical layout (8-row groups of two 128-byte core matrices: SBO 256 B,
+// LBO 128 B). hfac = (sf2 / 2^-e)^2 undoes both scales on Σ D^2 in the epilogue.
+void build_tc_operand_f16(const double* ilt, int n, double sv, int n_pad, int np, int n_pass,
+                          std::vector<uint16_t>& data, std::vector<int4>& meta, double& hfac) {
+  const int KC = tc::KC;
+  double mx = 0.0;
+  for (size_t i = 0; i < (size_t)n * n; ++i) mx = std::max(mx, std::fabs(ilt[i]));
+  const double scale = mx > 0.0 ? std::ldexp(1.0, -(int)std::ceil(std::log2(mx))) : 1.0;
+  hfac = (sv / scale) * (sv / scale);
+  auto bits = [](__half h) {
+    uint16_t u;
+    std::memcpy(&u, &h, 2);
+    return u;
+  };
+  data.clear();
+  meta.clear();
+  for (int p = 0; p < n_pass; ++p) {
+    const int npw = std::min(np, n_pad - p * np);
+    const int nk = std::min(n_pad, (p + 1) * np) / KC;
+    for (int kb = 0; kb < nk; ++kb) {
+      const int col0 = std::max(0, kb * KC - p * np);
+      const int ncols = npw - col0;
+      const size_t off = data.size();
+      data.resize(off + (size_t)2 * ncols * KC, 0);
+      uint16_t* hi = data.data() + off;
+      uint16_t* lo = hi + (size_t)ncols * KC;
+      for (int r = 0; r < ncols; ++r) {
+        const int j = p * np + col0 + r;
+        for (int k = 0; k < KC; ++k) {
+          const int i = kb * KC + k;
+          const double v = (i < n && j < n) ? ilt[(size_t)i * n + j] * scale : 0.0;
+          const __half h = __float2half_rn((float)v);
+          const __half l = __float2half_rn((float)(v - (double)__half2float(h)));
+          const size_t o = (size_t)(r >> 3) * 128 + (size_t)(k >> 3) * 64 + (r & 7) * 8 + (k & 7);
+          hi[o] = bits(h);
+          lo[o] = bits(l);
         }
       }
       meta.push_back(make_int4((int)off, ncols, col0, 0));

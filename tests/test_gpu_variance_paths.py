@@ -1,4 +1,4 @@
-"""Variance paths of the solve (FFMA, tcgen05 3xTF32, tcgen05 1xTF32) vs FP64.
+"""Variance paths of the solve (FFMA, tcgen05 3xTF32, tcgen05 1xTF32, tcgen05 3xFP16) vs FP64.
 
 var = sf2 - ||L^{-1} k*||^2 (gp.cpp:184-191) on FP32-rounded queries. Tolerances
 are absolute on var (sf2 = 4e-3 for the synthetic kernel) and stated per path.
@@ -10,12 +10,13 @@ pytestmark = pytest.mark.gpu
 
 # absolute var error bounds (sf2 = 4e-3), measured on B200 with margin:
 #   FFMA ≤ 1.1e-8; 3xTF32 ≤ 1.6e-7 (fp32 tensor-core accumulation, grows with n);
-#   1xTF32 ~ 8e-6 (single-pass TF32 — not a parity path, reported for the record)
-TOL = {0: 3e-8, 1: 4e-7, 2: 2e-5}
+#   1xTF32 ~ 8e-6 (single-pass TF32 — not a parity path, reported for the record);
+#   3xFP16 (scaled operands, same 22-bit hi+lo significands as 3xTF32) shares the 3xTF32 bound
+TOL = {0: 3e-8, 1: 4e-7, 2: 2e-5, 3: 4e-7}
 
 
 @pytest.mark.parametrize("n", [60, 512, 700, 2048])
-@pytest.mark.parametrize("path", [0, 1, 2])
+@pytest.mark.parametrize("path", [0, 1, 2, 3])
 def test_variance_path_accuracy(n, path):
     import paper_2411_03289_b200 as G
     from paper_2411_03289_b200 import workloads as W
@@ -29,4 +30,5 @@ def test_variance_path_accuracy(n, path):
     _, v64 = m.predict_batch(q32)
     v = m.variance_batch(q32, path)[:, 0]
     err = np.abs(v - v64[:, 0])
+    print(f"n={n} path={path} max={err.max():.3e} median={np.median(err):.3e}")
     assert err.max() <= TOL[path], (n, path, err.max(), np.median(err))
