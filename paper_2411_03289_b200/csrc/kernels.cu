@@ -83,7 +83,7 @@ size_t rollout_smem_bytes(const RolloutArgs& a) {
   b += sizeof(double) * (size_t)(2 * a.T + a.T + a.T * (a.n_obs_max > 0 ? a.n_obs_max : 1) + a.R + 2 + 32);
   b = (b + 15) & ~(size_t)15;
   if (a.model_kind == MODEL_GP)
-    for (int g = 0; g < a.model.G; ++g) b += sizeof(double) * (size_t)(5 + a.model.g[g].n_out) * a.model.ns;
+    b += sizeof(double) * (size_t)7 * a.model.ns * a.model.G;  // per group: Z (5 rows) + combined alpha (2 rows)
   return b;
 }
 
@@ -134,6 +134,31 @@ GPM_D void load_robot_smem(const RolloutArgs& a, const SmemView& v, int b) {
   for (int i = threadIdx.x; i < a.T * a.n_obs_max; i += blockDim.x) v.marg[i] = mg[i];
   const double* tw = a.tw + (size_t)b * BatchStrides::TW;
   for (int i = threadIdx.x; i < a.R; i += blockDim.x) v.tw[i] = tw[i];
+  if (a.model_kind == MODEL_GP) {
+    // combine_terrains (mppi.cpp:34-49) is linear in the per-output GP means, so it is
+    // folded into alpha once per robot and tick: alpha~_v = Σ_o w(o) alpha_o over the
+    // v-channel outputs (ascending o), likewise omega. The serial chain then carries 2
+    // sums per group instead of n_out (2 FMAs and 2 loads per point-sample, not n_out).
+    double* gp = v.pts;
+    const int ns = a.model.ns;
+    for (int g = 0; g < a.model.G; ++g) {
+      const GroupDev& G = a.model.g[g];
+      for (int j = threadIdx.x; j < ns; j += blockDim.x) {
+        double s0 = 0.0, s1 = 0.0;
+        for (int o = 0; o < G.n_out; ++o) {
+          const int gi = G.out_idx[o];
+          const double al = __ldg(G.pts + (size_t)(5 + o) * ns + j);
+          if (gi & 1)
+            s1 = fma(tw[gi >> 1], al, s1);
+          else
+            s0 = fma(tw[gi >> 1], al, s0);
+        }
+        gp[5 * ns + j] = s0;
+        gp[6 * ns + j] = s1;
+      }
+      gp += 7 * ns;
+    }
+  }
 }
 
 // sl = robot-major local sample index (b*K_local + local s); s = global counter index
@@ -311,12 +336,12 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
   {  // stage Z / alpha of every group (SoA) into shared memory, once per block
     double* dst = sv.pts;
     for (int g = 0; g < a.model.G; ++g) {
-      const int cnt = (5 + a.model.g[g].n_out) * ns;
+      const int cnt = 5 * ns;  // Z rows; the combined alpha rows are per robot (load_robot_smem)
       const double2* src = reinterpret_cast<const double2*>(a.model.g[g].pts);
       double2* d2 = reinterpret_cast<double2*>(dst);
 #pragma unroll 4
       for (int i = threadIdx.x; i < cnt / 2; i += blockDim.x) d2[i] = __ldg(src + i);
-      dst += cnt;
+      dst += 7 * ns;
     }
     ubuf = reinterpret_cast<double2*>(dst) + (size_t)gib * SPG * T;
   }
@@ -401,11 +426,9 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
       for (int j = 0; j < SPG; ++j) cm0[j] = cm1[j] = 0.0;
       const double* gp = sv.pts;
       for (int g = 0; g < a.model.G; ++g) {
-        const GroupDev& G = a.model.g[g];
-        const int nout = G.n_out;
         // gp.cpp:172-176 augmented query [q/l | -1/2|q/l|^2 | 1]
         double q0[SPG], q1[SPG], q2[SPG], q3[SPG], qn[SPG];
-        double acc[SPG][NO];
+        double acc[SPG][2];  // terrain-combined v / omega means (load_robot_smem)
 #pragma unroll
         for (int j = 0; j < SPG; ++j) {
           q0[j] = v[j] * gil[g][0];  // q/l (gp.cpp:172-176) by reciprocal: <= 1 ulp from the division
@@ -413,8 +436,7 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
           q2[j] = u0[j] * gil[g][2];
           q3[j] = u1[j] * gil[g][3];
           qn[j] = -0.5 * (q0[j] * q0[j] + q1[j] * q1[j] + q2[j] * q2[j] + q3[j] * q3[j]);
-#pragma unroll
-          for (int o = 0; o < NO; ++o) acc[j][o] = 0.0;
+          acc[j][0] = acc[j][1] = 0.0;
         }
         // two adjacent points per lane and load (LDS.128): the 32/LPS sample groups of a
         // warp read the same addresses, so a 16-byte access doubles the bytes per wavefront
@@ -423,67 +445,44 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
         const double2* z2 = reinterpret_cast<const double2*>(gp + 2 * ns);
         const double2* z3 = reinterpret_cast<const double2*>(gp + 3 * ns);
         const double2* zn = reinterpret_cast<const double2*>(gp + 4 * ns);
-        const double2* al = reinterpret_cast<const double2*>(gp + 5 * ns);
+        const double2* cv = reinterpret_cast<const double2*>(gp + 5 * ns);
+        const double2* cw = reinterpret_cast<const double2*>(gp + 6 * ns);
         const int half = ns >> 1;
 #pragma unroll(4 / SPG)
         for (int jp = gl; jp < half; jp += LPS) {
           // gp.cpp:177-179: k*_j = exp(q_aug · inputs_aug_j)
           const double2 a0 = z0[jp], a1 = z1[jp], a2 = z2[jp], a3 = z3[jp], an = zn[jp];
-          double k0[SPG], k1[SPG];
+          const double2 av = cv[jp], aw = cw[jp];
 #pragma unroll
           for (int j = 0; j < SPG; ++j) {
             const double d0 = q0[j] * a0.x + q1[j] * a1.x + q2[j] * a2.x + q3[j] * a3.x + qn[j] + an.x;
             const double d1 = q0[j] * a0.y + q1[j] * a1.y + q2[j] * a2.y + q3[j] * a3.y + qn[j] + an.y;
-            k0[j] = exp_tab(d0, sv.etab);
-            k1[j] = exp_tab(d1, sv.etab);
+            const double k0 = exp_tab(d0, sv.etab), k1 = exp_tab(d1, sv.etab);
+            acc[j][0] = fma(k1, av.y, fma(k0, av.x, acc[j][0]));  // gp.cpp:181-182, terrain-combined
+            acc[j][1] = fma(k1, aw.y, fma(k0, aw.x, acc[j][1]));
           }
-#pragma unroll
-          for (int o = 0; o < NO; ++o)
-            if (o < nout) {
-              const double2 ao = al[o * half + jp];
-#pragma unroll
-              for (int j = 0; j < SPG; ++j) acc[j][o] = fma(k1[j], ao.y, fma(k0[j], ao.x, acc[j][o]));  // gp.cpp:181-182
-            }
         }
-        if constexpr (SPG * NO <= LPS) {  // all group sums at once (transpose reduction)
-          double tot[SPG * NO];
+        if constexpr (SPG * 2 <= LPS) {  // all group sums at once (transpose reduction)
+          double tot[SPG * 2];
 #pragma unroll
-          for (int j = 0; j < SPG; ++j)
+          for (int j = 0; j < SPG; ++j) {
+            tot[2 * j] = acc[j][0];
+            tot[2 * j + 1] = acc[j][1];
+          }
+          group_allsum<LPS, SPG * 2>(tot);
 #pragma unroll
-            for (int o = 0; o < NO; ++o) tot[j * NO + o] = acc[j][o];
-          group_allsum<LPS, SPG * NO>(tot);
-#pragma unroll
-          for (int o = 0; o < NO; ++o) {
-            if (o < nout) {
-              const int gi = G.out_idx[o];
-              const double wt = sv.tw[gi >> 1];
-#pragma unroll
-              for (int j = 0; j < SPG; ++j) {
-                if (gi & 1)
-                  cm1[j] += wt * tot[j * NO + o];
-                else
-                  cm0[j] += wt * tot[j * NO + o];
-              }
-            }
+          for (int j = 0; j < SPG; ++j) {
+            cm0[j] += tot[2 * j];
+            cm1[j] += tot[2 * j + 1];
           }
         } else {
 #pragma unroll
-          for (int o = 0; o < NO; ++o) {
-            if (o < nout) {
-              const int gi = G.out_idx[o];
-              const double wt = sv.tw[gi >> 1];
-#pragma unroll
-              for (int j = 0; j < SPG; ++j) {
-                const double mo = group_sum<LPS>(acc[j][o]);
-                if (gi & 1)
-                  cm1[j] += wt * mo;
-                else
-                  cm0[j] += wt * mo;
-              }
-            }
+          for (int j = 0; j < SPG; ++j) {
+            cm0[j] += group_sum<LPS>(acc[j][0]);
+            cm1[j] += group_sum<LPS>(acc[j][1]);
           }
         }
-        gp += (size_t)(5 + nout) * ns;
+        gp += (size_t)7 * ns;
       }
 #pragma unroll
       for (int j = 0; j < SPG; ++j) {
