@@ -1187,15 +1187,31 @@ __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const Tight
     ww[0] = ax0[4];
     th[0] = ax0[2];
   }
-  if (a.model_kind == MODEL_GP) {  // vectorised staging of Z / alpha
+  if (a.model_kind == MODEL_GP) {  // vectorised staging of Z + terrain-combined alpha
     double* dst = pts;
+    const int ns = a.model.ns;
+    const double* rtw = a.tw + (size_t)rb * BatchStrides::TW;
     for (int g = 0; g < a.model.G; ++g) {
-      const int cnt = (5 + a.model.g[g].n_out) * a.model.ns;
-      const double2* src = reinterpret_cast<const double2*>(a.model.g[g].pts);
+      const GroupDev& Gd = a.model.g[g];
+      const double2* src = reinterpret_cast<const double2*>(Gd.pts);
       double2* d2 = reinterpret_cast<double2*>(dst);
 #pragma unroll 4
-      for (int i = threadIdx.x; i < cnt / 2; i += blockDim.x) d2[i] = __ldg(src + i);
-      dst += cnt;
+      for (int i = threadIdx.x; i < 5 * ns / 2; i += blockDim.x) d2[i] = __ldg(src + i);
+      // combine_terrains (mppi.cpp:34-49) folded into alpha, as in the rollout (load_robot_smem)
+      for (int j = threadIdx.x; j < ns; j += blockDim.x) {
+        double s0 = 0.0, s1 = 0.0;
+        for (int o = 0; o < Gd.n_out; ++o) {
+          const int gi = Gd.out_idx[o];
+          const double al = __ldg(Gd.pts + (size_t)(5 + o) * ns + j);
+          if (gi & 1)
+            s1 = fma(rtw[gi >> 1], al, s1);
+          else
+            s0 = fma(rtw[gi >> 1], al, s0);
+        }
+        dst[5 * ns + j] = s0;
+        dst[6 * ns + j] = s1;
+      }
+      dst += 7 * ns;
     }
   }
   __syncthreads();
@@ -1204,26 +1220,12 @@ __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const Tight
   // n points; every warp reduces the per-warp partials itself (double-buffered), so a
   // step costs one block barrier. q/l uses reciprocal lengthscales (<= 1 ulp from the
   // reference's division) to keep FP64 divides off the serial path.
-  __shared__ double red[2][TMEAN_THREADS / 32][kMaxGroups * NO];
-  __shared__ double gil[kMaxGroups][4];       // reciprocal lengthscales
-  __shared__ double gw0[kMaxGroups][NO];      // terrain weight of each v-channel output, else 0
-  __shared__ double gw1[kMaxGroups][NO];      // terrain weight of each omega-channel output, else 0
-  __shared__ int gno[kMaxGroups];
+  __shared__ double red[2][TMEAN_THREADS / 32][kMaxGroups * 2];
+  __shared__ double gil[kMaxGroups][4];  // reciprocal lengthscales
   const int nwarps = blockDim.x >> 5;
   const int ns = a.model.ns;
   const int G = a.model_kind == MODEL_GP ? a.model.G : 0;
-  if (threadIdx.x == 0) {  // group constants out of the (register-indexed) parameter space
-    for (int g = 0; g < G; ++g) {
-      gno[g] = a.model.g[g].n_out;
-      for (int d = 0; d < 4; ++d) gil[g][d] = 1.0 / a.model.g[g].ls[d];
-      for (int o = 0; o < NO; ++o) {
-        const bool used = o < a.model.g[g].n_out;
-        const int gi = used ? a.model.g[g].out_idx[o] : 0;
-        gw0[g][o] = (used && !(gi & 1)) ? tw[gi >> 1] : 0.0;
-        gw1[g][o] = (used && (gi & 1)) ? tw[gi >> 1] : 0.0;
-      }
-    }
-  }
+  if (threadIdx.x < 4 * G) gil[threadIdx.x >> 2][threadIdx.x & 3] = 1.0 / a.model.g[threadIdx.x >> 2].ls[threadIdx.x & 3];
   __syncthreads();
   double v = vv[0], om = ww[0];
   for (int k = 0; k < T; ++k) {
@@ -1235,61 +1237,36 @@ __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const Tight
         const double q0 = v * gil[g][0], q1 = om * gil[g][1];
         const double q2 = u0 * gil[g][2], q3 = u1 * gil[g][3];
         const double qn = -0.5 * (q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
-        const int no = gno[g];
-        double acc[NO];
-#pragma unroll
-        for (int o = 0; o < NO; ++o) acc[o] = 0.0;
+        double acc0 = 0.0, acc1 = 0.0;  // terrain-combined v / omega means
 #pragma unroll 4
         for (int j = threadIdx.x; j < n; j += TMEAN_THREADS) {
           const double kj = exp_tab(q0 * p[j] + q1 * p[ns + j] + q2 * p[2 * ns + j] + q3 * p[3 * ns + j] + qn + p[4 * ns + j], etab);
-#pragma unroll
-          for (int o = 0; o < NO; ++o)
-            if (o < no) acc[o] = fma(kj, p[(5 + o) * ns + j], acc[o]);
+          acc0 = fma(kj, p[5 * ns + j], acc0);
+          acc1 = fma(kj, p[6 * ns + j], acc1);
         }
-        {  // transpose-reduce the NO (<= 8) sums across the warp: 9 double shuffles
-           // instead of 5 per output; lane 4*o ends with the warp total of output o
-          double v8[8];
-#pragma unroll
-          for (int o = 0; o < 8; ++o) v8[o] = o < NO ? acc[o] : 0.0;
-          const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
-          double w4[4], w2[2];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const double send = b4 ? v8[i] : v8[i + 4];
-            w4[i] = (b4 ? v8[i + 4] : v8[i]) + __shfl_xor_sync(0xffffffffu, send, 16);
-          }
-#pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            const double send = b3 ? w4[i] : w4[i + 2];
-            w2[i] = (b3 ? w4[i + 2] : w4[i]) + __shfl_xor_sync(0xffffffffu, send, 8);
-          }
-          double y = (b2 ? w2[1] : w2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? w2[0] : w2[1], 4);
+        {  // transpose-reduce the two sums across the warp (5 shuffles): lanes 0-15
+           // end with the v total, lanes 16-31 with the omega total
+          const bool b4 = lane & 16;
+          double y = (b4 ? acc1 : acc0) + __shfl_xor_sync(0xffffffffu, b4 ? acc0 : acc1, 16);
+          y += __shfl_xor_sync(0xffffffffu, y, 8);
+          y += __shfl_xor_sync(0xffffffffu, y, 4);
           y += __shfl_xor_sync(0xffffffffu, y, 2);
           y += __shfl_xor_sync(0xffffffffu, y, 1);
-          const int o = (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);
-          if ((lane & 3) == 0 && o < NO) red[k & 1][w][g * NO + o] = y;
+          if ((lane & 15) == 0) red[k & 1][w][g * 2 + (lane >> 4)] = y;
         }
-        p += (size_t)(5 + no) * ns;
+        p += (size_t)7 * ns;
       }
       __syncthreads();
       for (int g = 0; g < G; ++g) {
-        // every thread sums the per-warp partials in warp order (identical bits
-        // everywhere), loads first so the 4 x NO shared reads overlap; the channel
-        // weights are zero for the other channel, so one FMA chain per channel keeps
-        // the ascending-output order without branches (ensemble_combine)
-        double part[TMEAN_THREADS / 32][NO];
+        // every thread sums the per-warp partials in warp order (identical bits everywhere)
+        double x0 = red[k & 1][0][g * 2], x1 = red[k & 1][0][g * 2 + 1];
 #pragma unroll
-        for (int q = 0; q < TMEAN_THREADS / 32; ++q)
-#pragma unroll
-          for (int o = 0; o < NO; ++o) part[q][o] = red[k & 1][q][g * NO + o];
-#pragma unroll
-        for (int o = 0; o < NO; ++o) {
-          double x = part[0][o];
-#pragma unroll
-          for (int q = 1; q < TMEAN_THREADS / 32; ++q) x += part[q][o];
-          c0 = fma(gw0[g][o], x, c0);
-          c1 = fma(gw1[g][o], x, c1);
+        for (int q = 1; q < TMEAN_THREADS / 32; ++q) {
+          x0 += red[k & 1][q][g * 2];
+          x1 += red[k & 1][q][g * 2 + 1];
         }
+        c0 += x0;
+        c1 += x1;
       }
     }
     if (threadIdx.x == 0) {
@@ -1518,7 +1495,7 @@ int tighten_splits(int n) { return n > 0 ? (n + TIGHT_ROWS - 1) / TIGHT_ROWS : 1
 cudaError_t launch_tighten(const TightenArgs& a, cudaStream_t st) {
   size_t msm = sizeof(double) * (size_t)(2 * a.T + 3 * (a.T + 1) + 2 * a.T + 1);
   if (a.model_kind == MODEL_GP)
-    for (int g = 0; g < a.model.G; ++g) msm += sizeof(double) * (size_t)(5 + a.model.g[g].n_out) * a.model.ns;
+    msm += sizeof(double) * (size_t)7 * a.model.ns * a.model.G;  // Z + combined alpha per group
   int no = 1;
   if (a.model_kind == MODEL_GP)
     for (int g = 0; g < a.model.G; ++g) no = a.model.g[g].n_out > no ? a.model.g[g].n_out : no;
