@@ -57,6 +57,21 @@ GPM_HD double wrap_angle(double a) {
   if (r <= -kPi) r += 2.0 * kPi;
   return r;
 }
+// wrap_angle without the library remainder (~200-cycle dependent chain per call; the
+// rollout's heading recursion is serial in k): n = rint(a / 2π) by the 1.5·2^52
+// rounding trick, r = fma(-n, 2π, a) -- exact, since an IEEE remainder is
+// representable -- and one select each way when n was off by one. Bit-identical to
+// wrap_angle, including the sign of a zero result (tests/test_wrap_angle.py).
+GPM_HD double wrap_angle_fast(double a) {
+  const double P = 2.0 * kPi, magic = 6755399441055744.0;
+  if (!(fabs(a) < 0x1p50)) return wrap_angle(a);  // huge or non-finite
+  const double n = fma(a, 1.0 / (2.0 * kPi), magic) - magic;
+  double r = fma(-n, P, a);
+  r = r > kPi ? r - P : r;  // Sterbenz: exact
+  r = r < -kPi ? r + P : r;
+  r = r == 0.0 ? copysign(0.0, a) : r;
+  return r <= -kPi ? r + P : r;
+}
 
 // dynamics.cpp:39-57 (sin/cos of theta passed in: s0 = sin(theta), c0 = cos(theta)).
 GPM_HD void arc_advance(double& x, double& y, double& th, double vx, double vy, double om,

@@ -82,6 +82,7 @@ struct RolloutArgs {
   uint8_t* alive;
   int words;  // ceil(T/32)
   double* scratch;  // per lane-group trajectory scratch (rollout_scratch_doubles)
+  int scratch_smem;  // set by launch_rollout: the trajectory scratch fits in shared memory (after ubuf)
 };
 
 struct VarianceArgs {

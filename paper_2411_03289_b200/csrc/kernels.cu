@@ -239,16 +239,31 @@ GPM_D void rollout_phase2(const RolloutArgs& a, const SmemView& sv, const TaskDe
   double* sx = scr + 7 * stride;
   double* sy = scr + 8 * stride;
   (void)su1;
+#ifdef GPM_ROLLOUT_TRACE
+  const bool trc = blockIdx.x == 0 && threadIdx.x == 0;
+  long long p2t[5];
+  p2t[0] = clock64();
+#endif
   // ---------------- phase 2a: heading recursion (arc_advance: theta = wrap(theta + omega dt))
-  if (gl == 0) {
+  if (gl == 0) {  // omega read 8 steps ahead of the chain (one load latency per 8 steps)
     double th = x0[2];
     sth[0] = th;
-    for (int k = 0; k < T; ++k) {
-      th = wrap_angle(th + sw[k] * a.nom.dt);
-      sth[k + 1] = th;
+    for (int k0 = 0; k0 < T; k0 += 8) {
+      double wv[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) wv[i] = k0 + i < T ? sw[k0 + i] : 0.0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (k0 + i < T) {
+          th = wrap_angle_fast(th + wv[i] * a.nom.dt);
+          sth[k0 + i + 1] = th;
+        }
     }
   }
   __syncwarp();
+#ifdef GPM_ROLLOUT_TRACE
+  p2t[1] = clock64();
+#endif
   // ---------------- phase 2b: sincos and exact-arc increments, lanes split the steps
   for (int k = gl; k < T; k += LPS) {
     const double th = sth[k], vk = sv_[k], wk = sw[k];
@@ -262,24 +277,41 @@ GPM_D void rollout_phase2(const RolloutArgs& a, const SmemView& sv, const TaskDe
     sy[k + 1] = dy;
   }
   __syncwarp();
+#ifdef GPM_ROLLOUT_TRACE
+  p2t[2] = clock64();
+#endif
   // ---------------- phase 2c: positions in step order + first non-finite state
   int kd = T;  // states k > kd are frozen at state kd (mppi.cpp:343-346)
-  if (gl == 0) {
+  if (gl == 0) {  // increments and finiteness of 8 steps loaded ahead of the prefix sum
     double x = x0[0], y = x0[1];
     sx[0] = x;
     sy[0] = y;
-    for (int k = 0; k < T; ++k) {
-      x += sx[k + 1];
-      y += sy[k + 1];
-      sx[k + 1] = x;
-      sy[k + 1] = y;
-      if (kd == T && !(isfinite(x) && isfinite(y) && isfinite(sth[k + 1]) && isfinite(sv_[k + 1]) &&
-                       isfinite(sw[k + 1])))
-        kd = k;
+    for (int k0 = 0; k0 < T; k0 += 8) {
+      double dxv[8], dyv[8];
+      bool fin[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int k = k0 + i < T ? k0 + i : T - 1;
+        dxv[i] = sx[k + 1];
+        dyv[i] = sy[k + 1];
+        fin[i] = isfinite(sth[k + 1]) && isfinite(sv_[k + 1]) && isfinite(sw[k + 1]);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (k0 + i < T) {
+          x += dxv[i];
+          y += dyv[i];
+          sx[k0 + i + 1] = x;
+          sy[k0 + i + 1] = y;
+          if (kd == T && !(isfinite(x) && isfinite(y) && fin[i])) kd = k0 + i;
+        }
     }
   }
   kd = __shfl_sync(0xffffffffu, kd, (threadIdx.x & 31) & ~(LPS - 1));
   __syncwarp();
+#ifdef GPM_ROLLOUT_TRACE
+  p2t[3] = clock64();
+#endif
   // ---------------- phase 2d: per-step costs and flags (costs.cpp:127-171), lanes split the steps
   double cost = 0.0;
   for (int wd = 0; wd < a.words; ++wd) {
@@ -321,6 +353,13 @@ GPM_D void rollout_phase2(const RolloutArgs& a, const SmemView& sv, const TaskDe
     a.term[sl] = term;
     a.alive[sl] = alive;
   }
+#ifdef GPM_ROLLOUT_TRACE
+  if (trc) {
+    p2t[4] = clock64();
+    printf("phase2: heading %lld arcs %lld positions %lld costs %lld\n", p2t[1] - p2t[0], p2t[2] - p2t[1],
+           p2t[3] - p2t[2], p2t[4] - p2t[3]);
+  }
+#endif
 }
 
 template <int NO, int LPS, int SPG>
@@ -333,6 +372,7 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
   const int groups_per_block = blockDim.x / LPS;
   const int gib = threadIdx.x / LPS;  // group index in the block
   double2* ubuf;  // this group's clamped controls u[SPG][T], drawn before the serial chain
+  double* scr_sm;  // shared-memory trajectory scratch (a.scratch_smem), after every ubuf
   {  // stage Z / alpha of every group (SoA) into shared memory, once per block
     double* dst = sv.pts;
     for (int g = 0; g < a.model.G; ++g) {
@@ -344,14 +384,18 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
       dst += 7 * ns;
     }
     ubuf = reinterpret_cast<double2*>(dst) + (size_t)gib * SPG * T;
+    scr_sm = reinterpret_cast<double*>(reinterpret_cast<double2*>(dst) + (size_t)groups_per_block * SPG * T);
   }
   __shared__ double gil[kMaxGroups][4];  // reciprocal lengthscales: no FP64 divide on the chain
   if (threadIdx.x < 4 * a.model.G) gil[threadIdx.x >> 2][threadIdx.x & 3] = 1.0 / a.model.g[threadIdx.x >> 2].ls[threadIdx.x & 3];
   const TaskDev& task = *sv.task;
   const int stride = T + 1;
   // scratch slot of sample j of this group
-  double* const scr0 = a.scratch + ((size_t)blockIdx.x * kMaxSampleSlotsPerBlock + (size_t)gib * SPG) *
-                                       SCR_ARRAYS * stride;
+  // (shared memory when the launcher found room: the phase-2 serial loops then wait on
+  // LDS latency instead of L2 round trips)
+  double* const scr0 = a.scratch_smem ? scr_sm + (size_t)gib * SPG * SCR_ARRAYS * stride
+                                      : a.scratch + ((size_t)blockIdx.x * kMaxSampleSlotsPerBlock + (size_t)gib * SPG) *
+                                                        SCR_ARRAYS * stride;
   const double av = a.nom.dt / a.nom.tau_v, aw = a.nom.dt / a.nom.tau_omega;
   // work items: (robot, chunk of groups_per_block*SPG samples); every lane of the block
   // runs the same item sequence (samples beyond K are masked, never early-exit)
@@ -361,6 +405,9 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
   int loaded = -1;
 
   for (long long item = blockIdx.x; item < items; item += gridDim.x) {
+#ifdef GPM_ROLLOUT_TRACE
+    const long long t_item = clock64();
+#endif
     const int b = (int)(item / chunks);
     const int ls0 = (int)(item % chunks) * spb + gib * SPG;  // first local sample of the group
     if (b != loaded) {
@@ -410,6 +457,9 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
       }
     }
     __syncwarp();
+#ifdef GPM_ROLLOUT_TRACE
+    const long long t_p1 = clock64();
+#endif
     // ---------------- phase 1: serial (v, omega) chains with the GP mean
     for (int k = 0; k < T; ++k) {
       double u0[SPG], u1[SPG];
@@ -496,6 +546,11 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
       }
     }
     __syncwarp();
+#ifdef GPM_ROLLOUT_TRACE
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+      printf("rollout item %lld: prologue %lld phase1 %lld (per step %lld)\n", item, t_p1 - t_item, clock64() - t_p1,
+             (clock64() - t_p1) / T);
+#endif
     for (int j = 0; j < SPG; ++j) {  // phase 2, one sample after the other
       rollout_phase2<LPS>(a, sv, task, scr0 + (size_t)j * SCR_ARRAYS * stride, x0, T, stride, gl, valid[j], sl[j], O);
       __syncwarp();
@@ -665,9 +720,18 @@ cudaError_t launch_rollout(const RolloutArgs& a, int num_sms, cudaStream_t st) {
     const int ni = no <= 2 ? 0 : no <= 4 ? 1 : no <= 6 ? 2 : 3;
     const int li = lps == 4 ? 0 : lps == 8 ? 1 : lps == 16 ? 2 : 3;
     KF kern = spg == 4 ? table4[ni] : table[spg == 2 ? 1 : 0][ni][li];
+    static int scr_env = -1;  // GPMPPI_SCR_GLOBAL=1 keeps the trajectory scratch in global memory
+    if (scr_env < 0) {
+      const char* e = getenv("GPMPPI_SCR_GLOBAL");
+      scr_env = e ? atoi(e) : 0;
+    }
+    RolloutArgs ra = a;
+    const size_t scr_bytes = sizeof(double) * (size_t)(threads / lps) * spg * SCR_ARRAYS * (a.T + 1);
+    ra.scratch_smem = (!scr_env && smem_u + scr_bytes <= 227 * 1024) ? 1 : 0;
+    if (ra.scratch_smem) smem_u += scr_bytes;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_u);
     if (e != cudaSuccess) return e;
-    kern<<<(unsigned)blocks, threads, smem_u, st>>>(a);
+    kern<<<(unsigned)blocks, threads, smem_u, st>>>(ra);
   } else {
     const int threads = 128;
     const long long items = (long long)a.B * ((a.K_local + threads - 1) / threads);
@@ -1159,10 +1223,16 @@ constexpr int TIGHT_ROWS = 64;  // rows of L^{-1} per variance block
 // only; theta is a cheap wrap recursion; the FP64 sincos / arc increments /
 // Jacobians are then evaluated for all k in parallel and x, y accumulated in
 // step order exactly as arc_advance does (dynamics.cpp:39-66).
-constexpr int TMEAN_THREADS = 128;
+#ifndef GPM_TMEAN_THREADS
+#define GPM_TMEAN_THREADS 128
+#endif
+constexpr int TMEAN_THREADS = GPM_TMEAN_THREADS;
 template <int NO>
 __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const TightenArgs a) {
   const int rb = blockIdx.x;  // robot
+#ifdef GPM_TMEAN_TRACE
+  const long long tk0 = clock64();
+#endif
   const double* ax0 = a.x0 + (size_t)rb * BatchStrides::X0;
   double* atq = a.tq + (size_t)rb * 4 * a.T;
   double* atJ = a.tJ + (size_t)rb * 25 * a.T;
@@ -1199,14 +1269,19 @@ __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const Tight
       for (int i = threadIdx.x; i < 5 * ns / 2; i += blockDim.x) d2[i] = __ldg(src + i);
       // combine_terrains (mppi.cpp:34-49) folded into alpha, as in the rollout (load_robot_smem)
       for (int j = threadIdx.x; j < ns; j += blockDim.x) {
+        double al[NO];  // all loads in flight before the combine (cold L2 after the rollout)
+#pragma unroll
+        for (int o = 0; o < NO; ++o) al[o] = o < Gd.n_out ? __ldg(Gd.pts + (size_t)(5 + o) * ns + j) : 0.0;
         double s0 = 0.0, s1 = 0.0;
-        for (int o = 0; o < Gd.n_out; ++o) {
-          const int gi = Gd.out_idx[o];
-          const double al = __ldg(Gd.pts + (size_t)(5 + o) * ns + j);
-          if (gi & 1)
-            s1 = fma(rtw[gi >> 1], al, s1);
-          else
-            s0 = fma(rtw[gi >> 1], al, s0);
+#pragma unroll
+        for (int o = 0; o < NO; ++o) {
+          if (o < Gd.n_out) {
+            const int gi = Gd.out_idx[o];
+            if (gi & 1)
+              s1 = fma(rtw[gi >> 1], al[o], s1);
+            else
+              s0 = fma(rtw[gi >> 1], al[o], s0);
+          }
         }
         dst[5 * ns + j] = s0;
         dst[6 * ns + j] = s1;
@@ -1220,7 +1295,7 @@ __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const Tight
   // n points; every warp reduces the per-warp partials itself (double-buffered), so a
   // step costs one block barrier. q/l uses reciprocal lengthscales (<= 1 ulp from the
   // reference's division) to keep FP64 divides off the serial path.
-  __shared__ double red[2][TMEAN_THREADS / 32][kMaxGroups * 2];
+  __shared__ __align__(16) double red[2][kMaxGroups][TMEAN_THREADS / 32][2];  // [parity][group][warp][v, omega]
   __shared__ double gil[kMaxGroups][4];  // reciprocal lengthscales
   const int nwarps = blockDim.x >> 5;
   const int ns = a.model.ns;
@@ -1228,7 +1303,15 @@ __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const Tight
   if (threadIdx.x < 4 * G) gil[threadIdx.x >> 2][threadIdx.x & 3] = 1.0 / a.model.g[threadIdx.x >> 2].ls[threadIdx.x & 3];
   __syncthreads();
   double v = vv[0], om = ww[0];
+#ifdef GPM_TMEAN_TRACE
+  const long long tk1 = clock64();
+  long long tr[8] = {};
+#define TRC(i) if (k == 5) tr[i] = clock64()
+#else
+#define TRC(i)
+#endif
   for (int k = 0; k < T; ++k) {
+    TRC(0);
     const double u0 = nom[2 * k], u1 = nom[2 * k + 1];
     double c0 = 0.0, c1 = 0.0;
     if (G > 0) {
@@ -1244,6 +1327,7 @@ __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const Tight
           acc0 = fma(kj, p[5 * ns + j], acc0);
           acc1 = fma(kj, p[6 * ns + j], acc1);
         }
+        TRC(1);
         {  // transpose-reduce the two sums across the warp (5 shuffles): lanes 0-15
            // end with the v total, lanes 16-31 with the omega total
           const bool b4 = lane & 16;
@@ -1252,23 +1336,29 @@ __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const Tight
           y += __shfl_xor_sync(0xffffffffu, y, 4);
           y += __shfl_xor_sync(0xffffffffu, y, 2);
           y += __shfl_xor_sync(0xffffffffu, y, 1);
-          if ((lane & 15) == 0) red[k & 1][w][g * 2 + (lane >> 4)] = y;
+          if ((lane & 15) == 0) red[k & 1][g][w][lane >> 4] = y;
         }
+        TRC(2);
         p += (size_t)7 * ns;
       }
       __syncthreads();
+      TRC(3);
       for (int g = 0; g < G; ++g) {
         // every thread sums the per-warp partials in warp order (identical bits everywhere)
-        double x0 = red[k & 1][0][g * 2], x1 = red[k & 1][0][g * 2 + 1];
+        double2 pr[TMEAN_THREADS / 32];  // 16-byte loads, all issued before the sums
+#pragma unroll
+        for (int q = 0; q < TMEAN_THREADS / 32; ++q) pr[q] = *reinterpret_cast<const double2*>(&red[k & 1][g][q][0]);
+        double x0 = pr[0].x, x1 = pr[0].y;
 #pragma unroll
         for (int q = 1; q < TMEAN_THREADS / 32; ++q) {
-          x0 += red[k & 1][q][g * 2];
-          x1 += red[k & 1][q][g * 2 + 1];
+          x0 += pr[q].x;
+          x1 += pr[q].y;
         }
         c0 += x0;
         c1 += x1;
       }
     }
+    TRC(4);
     if (threadIdx.x == 0) {
       atq[k * 4 + 0] = v;
       atq[k * 4 + 1] = om;
@@ -1277,14 +1367,24 @@ __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const Tight
     }
     v = v + av * (u0 - v) + c0;  // step_nominal lag (dynamics.cpp:63-64) + correction mean
     om = om + aw * (u1 - om) + c1;
+#ifdef GPM_TMEAN_TRACE
+    if (k == 5 && (threadIdx.x & 31) == 0) {
+      const long long t5 = clock64();
+      printf("tmean w%d: loop %lld shfl %lld bar %lld sum %lld upd %lld total %lld (v %.3e)\n", (int)(threadIdx.x >> 5),
+             tr[1] - tr[0], tr[2] - tr[1], tr[3] - tr[2], tr[4] - tr[3], t5 - tr[4], t5 - tr[0], v);
+    }
+#endif
     if (threadIdx.x == 0) {
       vv[k + 1] = v;
       ww[k + 1] = om;
     }
   }
   __syncthreads();
+#ifdef GPM_TMEAN_TRACE
+  const long long tk2 = clock64();
+#endif
   if (threadIdx.x == 0)  // heading recursion (arc_advance: theta = wrap(theta + omega dt))
-    for (int k = 0; k < T; ++k) th[k + 1] = wrap_angle(th[k] + ww[k] * a.nom.dt);
+    for (int k = 0; k < T; ++k) th[k + 1] = wrap_angle_fast(th[k] + ww[k] * a.nom.dt);
   __syncthreads();
   for (int k = threadIdx.x; k < T; k += blockDim.x) {  // arc increments + Jacobians, parallel in k
     const double m0[5] = {0.0, 0.0, th[k], vv[k], ww[k]};
@@ -1313,6 +1413,12 @@ __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const Tight
       }
     }
   }
+#ifdef GPM_TMEAN_TRACE
+  if (threadIdx.x == 0) {
+    const long long tk3 = clock64();
+    printf("tmean kernel: staging %lld chain %lld tail %lld total %lld\n", tk1 - tk0, tk2 - tk1, tk3 - tk2, tk3 - tk0);
+  }
+#endif
 }
 
 // grid (T, G*B, ceil(n / TIGHT_ROWS)): partial ||L^{-1} k*||^2 over a slice of rows of
