@@ -96,14 +96,15 @@ def load_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
-def roofline_block(w, phase, steps, peaks, peaks_kind):
+def roofline_block(w, phase, steps, peaks, peaks_kind, var_path=3):
     """Roofline of the dominant kernel (SURVEY §8(d) algorithmic work per unit).
 
     unit = one sample-rollout-step; F = n² + 24n FLOP split as
       variance kernel: n(n+1) (triangular ||L^-1 k*||²) + 2n (squares, sum)
       rollout kernel:  22n (kernel-row dot 4n FMA + exponent offsets, mean 6n FMA) + n exp
     The contract's denominator is the measured bf16 dense peak; the path's own
-    ceilings (TF32 dense = bf16/2, FP64 = 148·64 DFMA·2·clock) are reported beside it.
+    ceilings (FP16 dense = bf16 for the default 3xFP16 variance, TF32 dense = bf16/2 for
+    3xTF32, FP64 = 148·64 DFMA·2·clock) are reported beside it.
     """
     n = w.n_points
     units = w.sample_steps
@@ -126,15 +127,23 @@ def roofline_block(w, phase, steps, peaks, peaks_kind):
     except Exception:
         traffic_tab = {}
     tick_ms = sum(phase) / steps
-    # 3xTF32 issues three tensor products per algorithmic MAC; the TF32 dense rate is half bf16
-    var = {"kernel": "variance_tc_kernel", "bound": "tensor", "launch_ms": var_ms,
-           "flop_per_launch": units * (n * n + 3 * n),
-           "own_peak": peaks.get("bf16_tflops", 1590.0) / 2, "own_peak_kind": "tf32_dense_tflops (bf16/2)",
-           "tensor_issue_factor": 3}
+    # 3xFP16 / 3xTF32 issue three tensor products per algorithmic MAC; FP16 runs at the bf16
+    # dense rate, TF32 at half of it
+    bf16 = peaks.get("bf16_tflops", 1590.0)
+    if var_path == 3:
+        var = {"kernel": "variance_f16_kernel", "own_peak": bf16, "own_peak_kind": "fp16_dense_tflops (= bf16 dense)"}
+    elif var_path in (1, 2):
+        var = {"kernel": "variance_tc2u_kernel", "own_peak": bf16 / 2, "own_peak_kind": "tf32_dense_tflops (bf16/2)"}
+    else:
+        var = {"kernel": "variance_ffma_kernel", "own_peak": 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12,
+               "own_peak_kind": "fp32_tflops (148 SM x 128 FFMA x 2 x max clock)"}
+    var.update({"bound": "tensor" if var_path else "fp32", "launch_ms": var_ms, "flop_per_launch": units * (n * n + 3 * n),
+                "tensor_issue_factor": 3 if var_path in (1, 3) else 1})
     roll = {"kernel": "rollout_gp_kernel", "bound": "tensor", "launch_ms": roll_ms, "flop_per_launch": units * 22 * n,
             "own_peak": 148 * 64 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12,
             "own_peak_kind": "fp64_tflops (148 SM x 64 DFMA x 2 x max clock)",
-            "binding_resource": "FP64 pipe + shared-memory wavefronts (ncu: LSU shared 73%, FP64 38% at config2)"}
+            "binding_resource": "FP64 pipe + shared-memory wavefronts + issue (ncu: FP64 46%/60%, LSU shared 50%/62%, "
+                                "issue 49%/56% at config2/config5)"}
     for k in (var, roll):
         k["achieved"] = k["flop_per_launch"] / (k["launch_ms"] / 1e3) / 1e12
         k["peak"] = peak
@@ -149,7 +158,7 @@ def roofline_block(w, phase, steps, peaks, peaks_kind):
                 "flop_per_launch": dom["flop_per_launch"], "launch_ms": dom["launch_ms"],
                 "own_peak": dom["own_peak"], "own_peak_kind": dom["own_peak_kind"],
                 "frac_of_own_peak": dom["frac_of_own_peak"], "phase_share": dom["phase_share"],
-                "kernels": {"rollout_gp_kernel": roll, "variance_tc_kernel": var}})
+                "kernels": {"rollout_gp_kernel": roll, var["kernel"]: var}})
     return out
 
 
@@ -292,7 +301,7 @@ def main():
     value = steps_per_tick / (mean_ms / 1e3)
     e2e_value = steps_per_tick / (float(np.mean(e2e_ms)) / 1e3)
     peaks, peaks_kind = load_peaks()
-    roofline = roofline_block(w, phase, args.steps, peaks, peaks_kind)
+    roofline = roofline_block(w, phase, args.steps, peaks, peaks_kind, planner.variance_path())
     n = w.n_points
     rollout_ms, var_ms = phase[0] / args.steps, phase[1] / args.steps
     robots = f"{w.robots} robots x " if w.robots > 1 else ""
