@@ -215,7 +215,11 @@ int gpmppi_planner_sample_weights(const gpmppi_planner* p, double* w);     /* [B
 int gpmppi_planner_flags(const gpmppi_planner* p, uint8_t* viol, uint8_t* coll,
                          uint8_t* terminal, uint8_t* alive);
 
-/* ---- variance path (north star: tensor cores only where tolerance allows) ---- */
+/* ---- variance path (north star: tensor cores only where tolerance allows) ----
+ * FFMA: FP32 CUDA cores. TC_3XTF32: tcgen05 kind::tf32, hi/lo splits, three products.
+ * TC_1XTF32: one TF32 product (not a parity path). TC_3XF16 (default): tcgen05 kind::f16
+ * on scaled hi/lo FP16 operands -- the same 22-bit splits at twice the TF32 rate.
+ * Measured bounds: tests/test_gpu_variance_paths.py. */
 enum { GPMPPI_VAR_FFMA = 0, GPMPPI_VAR_TC_3XTF32 = 1, GPMPPI_VAR_TC_1XTF32 = 2, GPMPPI_VAR_TC_3XF16 = 3 };
 int gpmppi_planner_set_variance_path(gpmppi_planner* p, int path);
 int gpmppi_planner_variance_path(const gpmppi_planner* p);
