@@ -612,7 +612,7 @@ struct gpmppi_planner {
       d_var = dalloc<double>((size_t)groups() * S * T);
       if (!d_scratch) d_scratch = dalloc<double>(gpm::rollout_scratch_doubles(T, num_sms));
     }
-    reduce_blocks = gpm::reduce_blocks_for((int)K_local, B, num_sms);
+    reduce_blocks = gpm::reduce_blocks_for((int)K_local, B, num_sms, T);
     d_partials = dalloc<double>((size_t)B * reduce_blocks * gpm::tuple_doubles(T));
   }
 };

@@ -861,14 +861,17 @@ cudaError_t launch_variance(const VarianceArgs& a, int path, cudaStream_t st) {
 
 // -------------------------------------------------------------------------
 // Reduction: tuple per block, last block combines (+ update/shift/diag).
-int reduce_blocks_for(int K_local, int B, int num_sms) {
+int reduce_blocks_for(int K_local, int B, int num_sms, int T) {
   static const int forced = env_int("GPMPPI_REDUCE_BPR");
-  if (forced > 0) return forced;
+  // the last block of a robot stages every block tuple in shared memory (<= 160 KB)
+  const int smem_cap = (int)((160 * 1024 / sizeof(double) - 2 * T) / (tuple_doubles(T) + 1));
+  if (forced > 0) return forced < smem_cap ? forced : smem_cap;
   // blocks per robot: ~64 samples per block (measured: 148 blocks of 28 samples 34.8 us,
   // 64 blocks of 64 samples 28.6 us at K = 4096), at most one wave in total
   int b = (K_local + 63) / 64;
   const int cap = num_sms / (B < num_sms ? B : num_sms);
   if (b > cap) b = cap;
+  if (b > smem_cap) b = smem_cap;
   return b < 1 ? 1 : b;
 }
 
@@ -924,10 +927,23 @@ GPM_D void apply_tuple(const double* tup, int T, double lambda, double* nominal_
 
 // grid = B * bpr; block (b, j) reduces robot b's samples [j*per, (j+1)*per);
 // the last block of each robot combines that robot's bpr tuples in block order.
+// samples per pass-1 trace slab of the reduction (<= 96 KB of shared memory)
+GPM_HD int reduce_slab_samples(int T, int threads) {
+  const int cap = (int)(96 * 1024 / (sizeof(double) * (T + 1)));
+  return cap < threads ? (cap < 1 ? 1 : cap) : threads;
+}
+
 __global__ void __launch_bounds__(256) reduce_kernel(const ReduceArgs a) {
   extern __shared__ __align__(16) double dsm[];
   __shared__ double red[32 * 5];
   __shared__ unsigned int s_last;
+#ifdef GPM_REDUCE_TRACE
+  long long rt_[10];
+  rt_[0] = clock64();
+#define RTR(i) rt_[i] = clock64()
+#else
+#define RTR(i)
+#endif
   const int T = a.T;
   const int b = blockIdx.x / a.bpr, j = blockIdx.x % a.bpr;
   const int per = (a.K_local + a.bpr - 1) / a.bpr;
@@ -950,25 +966,51 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceArgs a) {
       }
     cg[g] = c;
   }
-  // pass 1: costs (cost_mean + var_w * Σ_k Σ_g coef_g var_g), block min over finite
+  // pass 1: costs (cost_mean + var_w * Σ_k Σ_g coef_g var_g), block min over finite.
+  // Per chunk of <= kReduceSlab samples, the trace slab of each group is staged into
+  // shared memory by one coalesced sweep (row stride T+1: conflict-free), then every
+  // sample sums its T values in step order (mppi.cpp:34-49 combine, costs.cpp:141).
+  const int chunk = reduce_slab_samples(T, blockDim.x);
   double lmin = INFINITY;
-  for (int s = b0 + threadIdx.x; s < b1; s += blockDim.x) {
-    const long long q = base + s;
-    double c = a.cost_mean[q];
+  for (int c0 = b0; c0 < b1; c0 += chunk) {
+    const int nc = min(chunk, b1 - c0);
+    double vsum = 0.0;
     if (a.var) {
-      double vsum = 0.0;
       for (int g = 0; g < a.G; ++g) {
-        const double* tr = a.var + (size_t)g * KT + (size_t)q * T;
-        double gsum = 0.0;
-#pragma unroll 8
-        for (int k = 0; k < T; ++k) gsum += __ldcg(tr + k);
-        vsum += cg[g] * gsum;  // tracking/avoidance trace (mppi.cpp:34-49 combine, costs.cpp:141)
+        const double* src = a.var + (size_t)g * KT + (size_t)(base + c0) * T;
+        const int cnt = nc * T;
+        __syncthreads();
+        for (int i0 = threadIdx.x; i0 < cnt; i0 += 8 * blockDim.x) {
+          double x[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * blockDim.x;
+            x[u] = i < cnt ? __ldcg(src + i) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * blockDim.x;
+            if (i < cnt) dsm[(i / T) * (T + 1) + i % T] = x[u];
+          }
+        }
+        __syncthreads();
+        if ((int)threadIdx.x < nc) {
+          const double* row = dsm + (size_t)threadIdx.x * (T + 1);
+          double gsum = 0.0;
+          for (int k = 0; k < T; ++k) gsum += row[k];
+          vsum += cg[g] * gsum;
+        }
       }
-      c += var_w * vsum;
     }
-    a.costs_out[q] = c;
-    if (isfinite(c)) lmin = fmin(lmin, c);
+    if ((int)threadIdx.x < nc) {
+      const long long q = base + c0 + threadIdx.x;
+      double c = a.cost_mean[q];
+      if (a.var) c += var_w * vsum;
+      a.costs_out[q] = c;
+      if (isfinite(c)) lmin = fmin(lmin, c);
+    }
   }
+  __syncthreads();  // the slab area is reused below
   lmin = warp_min(lmin);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = lmin;
   __syncthreads();
@@ -980,6 +1022,7 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceArgs a) {
   __syncthreads();
   const double mb = red[31 * 5];
   __syncthreads();
+  RTR(1);
   // pass 2: e_s = exp(-(c - m_b)/lambda) (mppi.cpp:137-142) and scalar sums
   double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // Z, E2, H, N, C
   for (int s = b0 + threadIdx.x; s < b1; s += blockDim.x) {
@@ -996,33 +1039,46 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceArgs a) {
     a.e_out[base + s] = e;
   }
   block_reduce_5(v, red);
+  RTR(2);
   // pass 3: S[k][c] = Σ_s e_s eps[s][k][c]; thread = (k, slice)
   const int nsl = max(1, (int)blockDim.x / T);
   double* Ssl = dsm;  // [nsl][T][2]
   for (int idx = threadIdx.x; idx < T * nsl; idx += blockDim.x) {
     const int k = idx % T, sl = idx / T;
     double s0 = 0.0, s1 = 0.0;
-    for (int s = b0 + sl; s < b1; s += nsl) {
-      const double e = a.e_out[base + s];
-      if (e == 0.0) continue;
-      double e0, e1;
-      if (a.noise_mode == NOISE_INJECTED) {
-        const double2 ep = reinterpret_cast<const double2*>(a.eps)[(size_t)(base + s) * T + k];
-        e0 = ep.x;
-        e1 = ep.y;
-      } else {
+    if (a.noise_mode == NOISE_INJECTED) {  // 4 samples' loads in flight per thread
+      const double2* eps2 = reinterpret_cast<const double2*>(a.eps);
+      for (int s = b0 + sl; s < b1; s += 4 * nsl) {
+        double ev[4];
+        double2 ep[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int su = s + u * nsl;
+          ev[u] = su < b1 ? a.e_out[base + su] : 0.0;
+          ep[u] = su < b1 ? eps2[(size_t)(base + su) * T + k] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (ev[u] != 0.0) {  // skipped, not multiplied: eps of a dead sample may be non-finite
+            s0 += ev[u] * ep[u].x;
+            s1 += ev[u] * ep[u].y;
+          }
+      }
+    } else {
+      for (int s = b0 + sl; s < b1; s += nsl) {
+        const double e = a.e_out[base + s];
+        if (e == 0.0) continue;
         double z1, z2;
         philox_gaussian_pair(key, (uint64_t)(a.s_begin + s), (uint32_t)k, &z1, &z2);
-        e0 = a.sv * z1;
-        e1 = a.sw * z2;
+        s0 += e * (a.sv * z1);
+        s1 += e * (a.sw * z2);
       }
-      s0 += e * e0;
-      s1 += e * e1;
     }
     Ssl[(sl * T + k) * 2] = s0;
     Ssl[(sl * T + k) * 2 + 1] = s1;
   }
   __syncthreads();
+  RTR(3);
   double* mine = a.partials + (size_t)blockIdx.x * W;
   for (int r = threadIdx.x; r < 2 * T; r += blockDim.x) {
     double acc = 0.0;
@@ -1041,30 +1097,53 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceArgs a) {
   __syncthreads();
   if (threadIdx.x == 0) s_last = (atomicAdd(a.ticket + b, 1u) == (unsigned)a.bpr - 1);
   __syncthreads();
+  RTR(4);
+#ifdef GPM_REDUCE_TRACE
+  if (threadIdx.x == 0 && (blockIdx.x == 0 || s_last))
+    printf("reduce blk %d%s: pass1 %lld pass2 %lld pass3 %lld tuple+ticket %lld\n", blockIdx.x, s_last ? " (last)" : "",
+           rt_[1] - rt_[0], rt_[2] - rt_[1], rt_[3] - rt_[2], rt_[4] - rt_[3]);
+#endif
   if (!s_last) return;
   __threadfence();
   // last block of robot b: combine its block tuples in block order (heads staged in smem)
   double* tup = a.rank_tuple + (size_t)b * W;
   const double* parts = a.partials + (size_t)b * a.bpr * W;
   const int BP = a.bpr;
-  double* heads = dsm;       // [BP][6]  (dsm holds >= 7*BP + 2T doubles, see launch_reduce)
-  double* sc = dsm + 6 * BP; // [BP] rescale factors
-  for (int i = threadIdx.x; i < 6 * BP; i += blockDim.x) heads[i] = __ldcg(parts + (size_t)(i / 6) * W + (i % 6));
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double m = INFINITY;
-    for (int q = 0; q < BP; ++q) m = fmin(m, heads[q * 6]);
-    red[0] = m;
+  double* pall = dsm;          // [BP][W] every block tuple (dsm holds >= BP*W + BP + 2T doubles)
+  double* sc = dsm + (size_t)BP * W;  // [BP] rescale factors
+  for (int i0 = threadIdx.x; i0 < BP * W; i0 += 8 * blockDim.x) {  // one coalesced sweep, 8 loads in flight
+    double x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * blockDim.x;
+      x[u] = i < BP * W ? __ldcg(parts + i) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i < BP * W) pall[i] = x[u];
+    }
   }
   __syncthreads();
+  const int HW = W;  // head q at pall[q * W]
+  double* heads = pall;
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (threadIdx.x < 32) {  // global min of the block minima (exact in any order)
+    double m = INFINITY;
+    for (int q = lane; q < BP; q += 32) m = fmin(m, heads[q * HW]);
+    m = warp_min(m);
+    if (lane == 0) red[0] = m;
+  }
+  __syncthreads();
+  RTR(5);
   const double m = red[0];
   for (int q = threadIdx.x; q < BP; q += blockDim.x)
-    sc[q] = heads[q * 6 + 4] > 0.0 ? exp(-(heads[q * 6] - m) / a.lambda) : 0.0;
+    sc[q] = heads[q * HW + 4] > 0.0 ? exp(-(heads[q * HW] - m) / a.lambda) : 0.0;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if ((int)(threadIdx.x >> 5) == nw - 1) {  // last warp: the scalar sums, lane-strided then a fixed shuffle tree
     double Z = 0.0, E2 = 0.0, H = 0.0, N = 0.0, C = 0.0;
-    for (int q = 0; q < BP; ++q) {
-      const double* p = heads + q * 6;
+    for (int q = lane; q < BP; q += 32) {
+      const double* p = heads + (size_t)q * HW;
       N += p[4];
       C += p[5];
       if (!(p[4] > 0.0)) continue;
@@ -1072,31 +1151,48 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceArgs a) {
       E2 += sc[q] * sc[q] * p[2];
       H += sc[q] * (p[3] + (p[0] - m) * p[1]);
     }
-    tup[0] = m;
-    tup[1] = Z;
-    tup[2] = E2;
-    tup[3] = H;
-    tup[4] = N;
-    tup[5] = C;
-    a.ticket[b] = 0u;  // re-arm for the next launch
+    Z = warp_sum(Z);
+    E2 = warp_sum(E2);
+    H = warp_sum(H);
+    N = warp_sum(N);
+    C = warp_sum(C);
+    if (lane == 0) {
+      tup[0] = m;
+      tup[1] = Z;
+      tup[2] = E2;
+      tup[3] = H;
+      tup[4] = N;
+      tup[5] = C;
+      a.ticket[b] = 0u;  // re-arm for the next launch
+    }
   }
   for (int r = threadIdx.x; r < 2 * T; r += blockDim.x) {
     double acc = 0.0;
-    for (int q = 0; q < BP; ++q) acc = fma(sc[q], __ldcg(parts + (size_t)q * W + kTupleHead + r), acc);
+    for (int q = 0; q < BP; ++q) acc = fma(sc[q], pall[(size_t)q * W + kTupleHead + r], acc);
     tup[kTupleHead + r] = acc;
   }
   __syncthreads();
-  double* tmp = dsm + 7 * BP;  // 2T doubles
+  RTR(6);
+  double* tmp = sc + BP;  // 2T doubles
   if (a.finish)
     apply_tuple(tup, T, a.lambda, a.nominal_seq + (size_t)b * BatchStrides::nom(T), a.lo, a.hi,
                 a.out + (size_t)b * BatchStrides::OUT, a.K_total, tmp);
+#ifdef GPM_REDUCE_TRACE
+  RTR(7);
+  if (threadIdx.x == 0)
+    printf("reduce last: heads %lld combine+S %lld apply %lld\n", rt_[5] - rt_[4], rt_[6] - rt_[5], rt_[7] - rt_[6]);
+#endif
 }
 
 cudaError_t launch_reduce(const ReduceArgs& a, int blocks, cudaStream_t st) {
   const int threads = 256;
   const int nsl = threads / a.T > 1 ? threads / a.T : 1;
   size_t smem = sizeof(double) * (size_t)nsl * a.T * 2;
-  const size_t need = sizeof(double) * ((size_t)7 * a.bpr + 2 * a.T);
+  const int per = (a.K_local + a.bpr - 1) / a.bpr;
+  const int ch = reduce_slab_samples(a.T, threads);
+  const size_t slab = sizeof(double) * (size_t)(per < ch ? per : ch) * (a.T + 1);  // pass-1 trace slab
+  if (smem < slab) smem = slab;
+  const size_t need = sizeof(double) * ((size_t)a.bpr * tuple_doubles(a.T) + a.bpr + 2 * a.T);
   if (smem < need) smem = need;
   cudaFuncSetAttribute(reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   reduce_kernel<<<blocks, threads, smem, st>>>(a);
