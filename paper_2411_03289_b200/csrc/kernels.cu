@@ -1541,14 +1541,17 @@ __global__ void __launch_bounds__(256) tighten_var_kernel(const TightenArgs a) {
   double ssq = 0.0;
   for (int j = j0 + w; j < jend; j += 8) {
     const double* row = G.linv64 + (size_t)j * n;
-    double a0 = 0.0, a1 = 0.0;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     int i = lane;
-    for (; i + 32 <= j; i += 64) {
-      a0 = fma(kst[i], __ldg(row + i), a0);
-      a1 = fma(kst[i + 32], __ldg(row + i + 32), a1);
+    for (; i + 96 <= j; i += 128) {  // four independent loads in flight per lane
+      const double r0 = __ldg(row + i), r1 = __ldg(row + i + 32), r2 = __ldg(row + i + 64), r3 = __ldg(row + i + 96);
+      a0 = fma(kst[i], r0, a0);
+      a1 = fma(kst[i + 32], r1, a1);
+      a2 = fma(kst[i + 64], r2, a2);
+      a3 = fma(kst[i + 96], r3, a3);
     }
-    if (i <= j) a0 = fma(kst[i], __ldg(row + i), a0);
-    const double aj = warp_sum(a0 + a1);
+    for (; i <= j; i += 32) a0 = fma(kst[i], __ldg(row + i), a0);
+    const double aj = warp_sum((a0 + a1) + (a2 + a3));
     ssq = fma(aj, aj, ssq);
   }
   if (lane == 0) red[w] = ssq;
@@ -1565,6 +1568,10 @@ __global__ void __launch_bounds__(256) tighten_var_kernel(const TightenArgs a) {
 // threads evaluate r̄_k and the margins in parallel.
 __global__ void __launch_bounds__(256) tighten_cov_kernel(const TightenArgs a, int nsplit) {
   const int rb = blockIdx.x;  // robot
+#ifdef GPM_TCOV_TRACE
+  long long ct[6];
+  ct[0] = clock64();
+#endif
   const double* atJ = a.tJ + (size_t)rb * 25 * a.T;
   const double* atmu = a.tmu + (size_t)rb * 5 * (a.T + 1);
   const double* atvar = a.tvar_part + (size_t)rb * a.T * (a.model_kind == MODEL_GP ? a.model.G : 1) * nsplit;
@@ -1600,8 +1607,17 @@ __global__ void __launch_bounds__(256) tighten_cov_kernel(const TightenArgs a, i
       for (int g = 0; g < kMaxGroups; ++g) {
         double v = 0.0;
         if (g < G) {
+          const double* pv = atvar + ((size_t)k * G + g) * nsplit;
           double s = 0.0;
-          for (int c = 0; c < nsplit; ++c) s += atvar[((size_t)k * G + g) * nsplit + c];
+          int c = 0;
+          for (; c + 8 <= nsplit; c += 8) {  // eight loads in flight, summed in split order
+            double x[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) x[u] = pv[c + u];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s += x[u];
+          }
+          for (; c < nsplit; ++c) s += pv[c];
           v = a.model.g[g].sv - s;
         }
         vg[g] = v > 0.0 ? v : 0.0;
@@ -1624,18 +1640,32 @@ __global__ void __launch_bounds__(256) tighten_cov_kernel(const TightenArgs a, i
   }
   double* Ss = mus + 5 * (T + 1);  // [T][25] propagated covariances
   __syncthreads();
+#ifdef GPM_TCOV_TRACE
+  ct[1] = clock64();
+#endif
   if (l < 32) {  // warp 0: the serial recursion
     // lane l < 25 owns Σ[i5][j5] in a register; the two 5-term products per step pull
     // their operands with shuffles (no shared-memory round trips on the serial chain)
     const int i5 = l < 25 ? l / 5 : 4, j5 = l < 25 ? l % 5 : 4;
     double Sr = 0.0;
+    double Jin[5], Jjn[5];  // step k's J rows, loaded one step ahead (off the serial chain)
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      Jin[q] = Js[i5 * 5 + q];
+      Jjn[q] = Js[j5 * 5 + q];
+    }
     for (int k = 0; k < a.T; ++k) {  // Σ' = J Σ Jᵀ + diag(0,0,0,cv0,cv1), symmetrised (uncertainty.cpp:83-87)
-      const double* J = Js + 25 * k;
       double Ji[5], Jj[5];
 #pragma unroll
       for (int q = 0; q < 5; ++q) {
-        Ji[q] = J[i5 * 5 + q];
-        Jj[q] = J[j5 * 5 + q];
+        Ji[q] = Jin[q];
+        Jj[q] = Jjn[q];
+      }
+      const double* Jn = Js + 25 * (k + 1 < a.T ? k + 1 : k);
+#pragma unroll
+      for (int q = 0; q < 5; ++q) {
+        Jin[q] = Jn[i5 * 5 + q];
+        Jjn[q] = Jn[j5 * 5 + q];
       }
       double js = 0.0;
 #pragma unroll
@@ -1650,6 +1680,9 @@ __global__ void __launch_bounds__(256) tighten_cov_kernel(const TightenArgs a, i
     }
   }
   __syncthreads();
+#ifdef GPM_TCOV_TRACE
+  ct[2] = clock64();
+#endif
   for (int i = l; i < 25 * T; i += nt) ahcov[i] = Ss[i];
   for (int k = l; k < T; k += nt) {  // tighten_lane_radius (uncertainty.cpp:90-96), parallel in k
     if (t.kind == TASK_AVOIDANCE) break;
@@ -1690,6 +1723,9 @@ __global__ void __launch_bounds__(256) tighten_cov_kernel(const TightenArgs a, i
     }
   __syncthreads();
   if (l == 0) a.infeasible[rb] = infeasible;
+#ifdef GPM_TCOV_TRACE
+  if (l == 0) printf("tcov: staging+cv %lld recursion %lld thresholds %lld\n", ct[1] - ct[0], ct[2] - ct[1], clock64() - ct[2]);
+#endif
 }
 
 int tighten_splits(int n) { return n > 0 ? (n + TIGHT_ROWS - 1) / TIGHT_ROWS : 1; }
