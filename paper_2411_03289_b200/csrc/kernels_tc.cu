@@ -656,10 +656,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc_kernel(const Varia
           tmem_ld16_nowait(trow + c + 32, r + 32);
           tmem_ld16_nowait(trow + c + 48, r + 48);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          float part = 0.f;
+          float pp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 8 independent chains
 #pragma unroll
-          for (int i = 0; i < 64; ++i) part = fmaf(__uint_as_float(r[i]), __uint_as_float(r[i]), part);
-          ssq += (double)part;
+          for (int i = 0; i < 64; ++i) pp[i & 7] = fmaf(__uint_as_float(r[i]), __uint_as_float(r[i]), pp[i & 7]);
+          ssq += (double)(((pp[0] + pp[1]) + (pp[2] + pp[3])) + ((pp[4] + pp[5]) + (pp[6] + pp[7])));
         }
         for (; c < npw; c += 16) {
           float v[16];
@@ -920,10 +920,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_tc2u_kernel(const Var
             tmem_ld16_nowait(trow + c + 32, rr + 32);
             tmem_ld16_nowait(trow + c + 48, rr + 48);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            float part = 0.f;
+            float pp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 8 independent chains
 #pragma unroll
-            for (int i = 0; i < 64; ++i) part = fmaf(__uint_as_float(rr[i]), __uint_as_float(rr[i]), part);
-            ssq += (double)part;
+            for (int i = 0; i < 64; ++i) pp[i & 7] = fmaf(__uint_as_float(rr[i]), __uint_as_float(rr[i]), pp[i & 7]);
+            ssq += (double)(((pp[0] + pp[1]) + (pp[2] + pp[3])) + ((pp[4] + pp[5]) + (pp[6] + pp[7])));
           }
           for (; c < npw; c += 16) {
             float v[16];
@@ -1029,6 +1029,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const Vari
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  if (threadIdx.x == 0) trace_at(0, dbg);
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int n_tiles = (int)((a.KT + M - 1) / M);
   const int tb = (int)((long long)blockIdx.x * n_tiles / gridDim.x);
@@ -1063,11 +1064,14 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const Vari
   __syncthreads();
   tc_after();
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  if (threadIdx.x == 0) trace_at(1, dbg);
 
   if (warp == 0 && lane == 0) {
     // ---------------- B producer: one bulk copy (hi + lo K=16 block) per chunk
     Ring r(S);
-    for (int t0 = tb; t0 < te; t0 += 2) {
+    int ti = 0;
+    for (int t0 = tb; t0 < te; t0 += 2, ++ti) {
+      if (ti < 10) trace_at(48 + ti, dbg);
       int m = 0;
       for (int p = 0; p < n_pass; ++p) {
         const int nk = pass_chunks(p, NP, n_pad);
@@ -1076,8 +1080,12 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const Vari
           mbar_wait(smem_u32(&empty[r.s]), r.ph ^ 1);
           const uint32_t bytes = (uint32_t)meta.y * KC * 2 * 2;
           const uint32_t fb = smem_u32(&full[r.s]);
-          mbar_arrive_tx(fb, bytes);
-          bulk_g2s(smem_u32(stg + (size_t)r.s * stage_bytes + A_BYTES), G.tc_h + meta.x, bytes, fb);
+          if (dbg & 1) {  // diagnostics: no operand copy
+            mbar_arrive(fb);
+          } else {
+            mbar_arrive_tx(fb, bytes);
+            bulk_g2s(smem_u32(stg + (size_t)r.s * stage_bytes + A_BYTES), G.tc_h + meta.x, bytes, fb);
+          }
         }
       }
     }
@@ -1090,6 +1098,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const Vari
       for (int p = 0; p < n_pass; ++p, ++uc) {
         mbar_wait(smem_u32(tempty), (uc & 1) ^ 1);
         tc_after();
+        if (lane == 0 && uc < 10) trace_at(2 + 2 * (int)uc, dbg);
         const int nk = pass_chunks(p, NP, n_pad);
         const int npw = min(NP, n_pad - p * NP);
         for (int kb = 0; kb < nk; ++kb, r.next()) {
@@ -1115,8 +1124,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const Vari
                               bar);
         }
         mma_commit(smem_u32(tfull));
+        if (lane == 0 && uc < 10) trace_at(3 + 2 * (int)uc, dbg);
       }
     }
+    if (lane == 0) trace_at(60, dbg);
   } else if (warp >= 8) {
     // ---------------- A producers (lane = 4 rows x 4 points, as variance_tc2u_kernel):
     // k*/sf2 split into FP16 hi + lo, 8-byte stores covering 256 contiguous bytes per warp
@@ -1125,7 +1136,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const Vari
     const int qi = lane & 7, pg = lane >> 3;
     const int mb = (pw & 3) * 32 + qi;
     Ring r(S);
-    for (int t0 = tb; t0 < te; t0 += 2) {
+    int ti = 0;
+    for (int t0 = tb; t0 < te; t0 += 2, ++ti) {
+      if (pw == 0 && lane == 0 && ti < 10) trace_at(36 + ti, dbg);
       const bool present = t0 + t < te;
       float qq[4][5];
 #pragma unroll
@@ -1146,7 +1159,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const Vari
         for (int kb = 0; kb < nk; ++kb, r.next()) {
           if (lane == 0) mbar_wait(smem_u32(&empty[r.s]), r.ph ^ 1);
           __syncwarp();
-          if (present) {
+          if (present && !(dbg & 256)) {
             unsigned char* ahi = stg + (size_t)r.s * stage_bytes + (size_t)t * 2 * H_TILE_BYTES;
             unsigned char* alo = ahi + H_TILE_BYTES;
             const int i0 = kb * KC + pg * 4;
@@ -1192,6 +1205,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const Vari
       for (int p = 0; p < n_pass; ++p, ++uc) {
         const int npw = min(NP, n_pad - p * NP);
         if (lane == 0) mbar_wait(smem_u32(tfull), uc & 1);
+        if (lane == 0 && e == 0 && uc < 10) trace_at(24 + (int)uc, dbg);
         __syncwarp();
         tc_after();
         for (int tt = 0; tt < ntile; ++tt) {
@@ -1205,10 +1219,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const Vari
             tmem_ld16_nowait(trow + c + 32, rr + 32);
             tmem_ld16_nowait(trow + c + 48, rr + 48);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            float part = 0.f;
+            float pp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 8 independent chains
 #pragma unroll
-            for (int i = 0; i < 64; ++i) part = fmaf(__uint_as_float(rr[i]), __uint_as_float(rr[i]), part);
-            ssq += (double)part;
+            for (int i = 0; i < 64; ++i) pp[i & 7] = fmaf(__uint_as_float(rr[i]), __uint_as_float(rr[i]), pp[i & 7]);
+            ssq += (double)(((pp[0] + pp[1]) + (pp[2] + pp[3])) + ((pp[4] + pp[5]) + (pp[6] + pp[7])));
           }
           for (; c < npw; c += 16) {
             float v[16];
@@ -1223,6 +1237,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const Vari
         tc_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(tempty));
+        if (lane == 0 && e == 0 && uc < 4) trace_at(uc < 2 ? 22 + (int)uc : 32 + (int)uc, dbg);
       }
       for (int tt = 0; tt < ntile; ++tt) {
         const long long q = (long long)(t0 + tt) * M + m;
@@ -1238,6 +1253,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const Vari
   tc_before();
   __syncthreads();
   tc_after();
+  if (threadIdx.x == 0) trace_at(63, dbg);
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512) : "memory");
 }

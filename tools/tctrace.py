@@ -12,7 +12,7 @@ from paper_2411_03289_b200 import workloads as W  # noqa: E402
 from bench import build_planner  # noqa: E402
 
 w = W.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "config2"]
-p, task, x0 = build_planner(w, G, var_path=1)
+p, task, x0 = build_planner(w, G, var_path=int(os.environ.get("VAR_PATH", "3")))
 p.bench_device(x0, task, 3)
 t = np.zeros(64)
 A.lib().gpmppi_debug_tc_trace(A.dptr(t))
@@ -23,3 +23,4 @@ for k in range(10):
     print(f"tile {k}: B start {rel(48 + k):9.0f}  A start {rel(36 + k):9.0f}  MMA start {rel(2 + 2 * k):9.0f}"
           f"  tfull commit {rel(3 + 2 * k):9.0f}  epi wake {rel(24 + k):9.0f}")
 print(f"MMA end {rel(60):9.0f} epi end {rel(61):9.0f} producer end {rel(62):9.0f} dealloc {rel(63):9.0f}")
+print("epilogue done (passes 0-3):", [f"{rel(i):.0f}" for i in (22, 23, 34, 35)])
