@@ -1006,6 +1006,20 @@ __device__ __forceinline__ void mma_f16_single_3x(uint32_t d, uint64_t ah, uint6
       "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(acc), "r"(bar)
       : "memory");
 }
+// packed FP32 pair ops (FFMA2 / FADD2): two lanes of work per issue slot
+__device__ __forceinline__ unsigned long long f2_pack(float lo, float hi) {
+  return ((unsigned long long)__float_as_uint(hi) << 32) | __float_as_uint(lo);
+}
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ unsigned long long fadd2(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
 __device__ __forceinline__ uint32_t half2_bits(__half2 h) {
   uint32_t u;
   memcpy(&u, &h, 4);
@@ -1154,6 +1168,11 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const Vari
                                           qq[j][3] * qq[j][3])
                          : -1e30f;
       }
+      unsigned long long qp[4][5];  // query terms duplicated into both halves of a pair
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int c = 0; c < 5; ++c) qp[j][c] = f2_pack(qq[j][c], qq[j][c]);
       for (int p = 0; p < n_pass; ++p) {
         const int nk = pass_chunks(p, NP, n_pad);
         for (int kb = 0; kb < nk; ++kb, r.next()) {
@@ -1168,16 +1187,23 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const Vari
             const float4 z2 = *reinterpret_cast<const float4*>(zs + 2 * n_pad + i0);
             const float4 z3 = *reinterpret_cast<const float4*>(zs + 3 * n_pad + i0);
             const float4 zq = *reinterpret_cast<const float4*>(zs + 4 * n_pad + i0);
-            const float za[4][5] = {{z0.x, z1.x, z2.x, z3.x, zq.x}, {z0.y, z1.y, z2.y, z3.y, zq.y},
-                                    {z0.z, z1.z, z2.z, z3.z, zq.z}, {z0.w, z1.w, z2.w, z3.w, zq.w}};
+            // point pairs (0,1) and (2,3) as packed FP32x2 operands: FADD2 + 4 FFMA2 per pair
+            const unsigned long long zp[2][5] = {
+                {f2_pack(z0.x, z0.y), f2_pack(z1.x, z1.y), f2_pack(z2.x, z2.y), f2_pack(z3.x, z3.y), f2_pack(zq.x, zq.y)},
+                {f2_pack(z0.z, z0.w), f2_pack(z1.z, z1.w), f2_pack(z2.z, z2.w), f2_pack(z3.z, z3.w), f2_pack(zq.z, zq.w)}};
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               float kv[4];
 #pragma unroll
-              for (int e = 0; e < 4; ++e)
-                kv[e] = exp2f_approx(fmaf(qq[j][0], za[e][0],
-                                          fmaf(qq[j][1], za[e][1],
-                                               fmaf(qq[j][2], za[e][2], fmaf(qq[j][3], za[e][3], qq[j][4] + za[e][4])))));
+              for (int h = 0; h < 2; ++h) {
+                unsigned long long d = fadd2(qp[j][4], zp[h][4]);
+                d = ffma2(qp[j][3], zp[h][3], d);
+                d = ffma2(qp[j][2], zp[h][2], d);
+                d = ffma2(qp[j][1], zp[h][1], d);
+                d = ffma2(qp[j][0], zp[h][0], d);
+                kv[2 * h] = exp2f_approx(__uint_as_float((uint32_t)d));
+                kv[2 * h + 1] = exp2f_approx(__uint_as_float((uint32_t)(d >> 32)));
+              }
               const __half2 h01 = __floats2half2_rn(kv[0], kv[1]), h23 = __floats2half2_rn(kv[2], kv[3]);
               const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
               const __half2 l01 = __floats2half2_rn(kv[0] - f01.x, kv[1] - f01.y);
