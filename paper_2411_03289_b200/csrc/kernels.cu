@@ -314,6 +314,8 @@ GPM_D void rollout_phase2(const RolloutArgs& a, const SmemView& sv, const TaskDe
 #endif
   // ---------------- phase 2d: per-step costs and flags (costs.cpp:127-171), lanes split the steps
   double cost = 0.0;
+  double decay = 1.0;  // 0.9^k by repeated multiplication, as costs.cpp:146 (continued across
+  int kdec = 0;        // this lane's increasing steps: the same product sequence, fewer multiplies)
   for (int wd = 0; wd < a.words; ++wd) {
     uint32_t vb = 0, cb = 0;
     const int kend = min(T, 32 * wd + 32);
@@ -321,8 +323,7 @@ GPM_D void rollout_phase2(const RolloutArgs& a, const SmemView& sv, const TaskDe
       const int ip = min(k, kd), in = min(k + 1, kd);
       const double prev[5] = {sx[ip], sy[ip], sth[ip], sv_[ip], sw[ip]};
       const double next[5] = {sx[in], sy[in], sth[in], sv_[in], sw[in]};
-      double decay = 1.0;  // 0.9^k by repeated multiplication, as costs.cpp:146
-      for (int i = 0; i < k; ++i) decay *= 0.9;
+      for (; kdec < k; ++kdec) decay *= 0.9;
       const StepCost c = step_cost(task, prev, next, ssin[ip], scos[ip], sv.rbar[k],
                                    sv.marg + (size_t)k * O, su0[k], decay);
       cost += c.cost;
@@ -551,9 +552,25 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
       printf("rollout item %lld: prologue %lld phase1 %lld (per step %lld)\n", item, t_p1 - t_item, clock64() - t_p1,
              (clock64() - t_p1) / T);
 #endif
-    for (int j = 0; j < SPG; ++j) {  // phase 2, one sample after the other
-      rollout_phase2<LPS>(a, sv, task, scr0 + (size_t)j * SCR_ARRAYS * stride, x0, T, stride, gl, valid[j], sl[j], O);
+    if constexpr (SPG > 1 && LPS / SPG >= 2) {
+      // phase 2 of the group's SPG samples side by side, LPS/SPG lanes each: their serial
+      // heading / position recursions run in the same instructions instead of in turn
+      constexpr int SUB = LPS / SPG;
+      const int h = gl / SUB;
+      bool vh = valid[0];
+      long long slh = sl[0];
+#pragma unroll
+      for (int j = 1; j < SPG; ++j) {
+        vh = h == j ? valid[j] : vh;
+        slh = h == j ? sl[j] : slh;
+      }
+      rollout_phase2<SUB>(a, sv, task, scr0 + (size_t)h * SCR_ARRAYS * stride, x0, T, stride, gl % SUB, vh, slh, O);
       __syncwarp();
+    } else {
+      for (int j = 0; j < SPG; ++j) {  // phase 2, one sample after the other
+        rollout_phase2<LPS>(a, sv, task, scr0 + (size_t)j * SCR_ARRAYS * stride, x0, T, stride, gl, valid[j], sl[j], O);
+        __syncwarp();
+      }
     }
   }
 }
