@@ -255,7 +255,8 @@ GPM_D void rollout_phase2(const RolloutArgs& a, const SmemView& sv, const TaskDe
 #pragma unroll
       for (int i = 0; i < 8; ++i)
         if (k0 + i < T) {
-          th = wrap_angle_fast(th + wv[i] * a.nom.dt);
+          th = th + wv[i] * a.nom.dt;
+          if (!(th > -kPi && th <= kPi)) th = wrap_angle_fast(th);  // remainder is the identity on (-π, π]
           sth[k0 + i + 1] = th;
         }
     }
