@@ -144,14 +144,19 @@ GPM_D void load_robot_smem(const RolloutArgs& a, const SmemView& v, int b) {
     for (int g = 0; g < a.model.G; ++g) {
       const GroupDev& G = a.model.g[g];
       for (int j = threadIdx.x; j < ns; j += blockDim.x) {
+        double al[kMaxOutPerGroup];  // every output's alpha in flight before the combine
+#pragma unroll
+        for (int o = 0; o < kMaxOutPerGroup; ++o) al[o] = o < G.n_out ? __ldg(G.pts + (size_t)(5 + o) * ns + j) : 0.0;
         double s0 = 0.0, s1 = 0.0;
-        for (int o = 0; o < G.n_out; ++o) {
-          const int gi = G.out_idx[o];
-          const double al = __ldg(G.pts + (size_t)(5 + o) * ns + j);
-          if (gi & 1)
-            s1 = fma(tw[gi >> 1], al, s1);
-          else
-            s0 = fma(tw[gi >> 1], al, s0);
+#pragma unroll
+        for (int o = 0; o < kMaxOutPerGroup; ++o) {
+          if (o < G.n_out) {
+            const int gi = G.out_idx[o];
+            if (gi & 1)
+              s1 = fma(tw[gi >> 1], al[o], s1);
+            else
+              s0 = fma(tw[gi >> 1], al[o], s0);
+          }
         }
         gp[5 * ns + j] = s0;
         gp[6 * ns + j] = s1;
@@ -440,22 +445,45 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
     }
     // noise + clamp of every (sample, step) up front, lanes split the pairs: the draws
     // do not depend on the chain, so they leave the serial path (mppi.cpp:298-308)
-    for (int idx = gl; idx < SPG * T; idx += LPS) {
-      const int j = SPG == 1 ? 0 : idx / T, k = SPG == 1 ? idx : idx % T;
-      const bool vj = j == 0 ? valid[0] : valid[SPG - 1];
-      double e0 = 0.0, e1 = 0.0;
-      const long long slj = j == 0 ? sl[0] : sl[SPG - 1];
-      if (vj) {
-        sample_noise(a, key, slj, j == 0 ? s[0] : s[SPG - 1], k, &e0, &e1);
-        if (a.noise_out) reinterpret_cast<double2*>(a.noise_out)[(size_t)slj * T + k] = make_double2(e0, e1);
+    for (int idx0 = gl; idx0 < SPG * T; idx0 += 2 * LPS) {  // two draws per lane in flight (ILP)
+      double e0[2], e1[2];
+      int jj[2], kk[2];
+      bool vjs[2], in[2];
+      long long slj[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int idx = idx0 + u * LPS;
+        in[u] = idx < SPG * T;
+        const int j = (SPG == 1 || !in[u]) ? 0 : idx / T;
+        kk[u] = SPG == 1 ? idx : (in[u] ? idx % T : 0);
+        jj[u] = j;
+        bool vj = valid[0];
+        long long sj = sl[0], cj = s[0];
+#pragma unroll
+        for (int q = 1; q < SPG; ++q) {
+          vj = j == q ? valid[q] : vj;
+          sj = j == q ? sl[q] : sj;
+          cj = j == q ? s[q] : cj;
+        }
+        vjs[u] = in[u] && vj;
+        slj[u] = sj;
+        e0[u] = e1[u] = 0.0;
+        if (vjs[u]) sample_noise(a, key, sj, cj, kk[u], &e0[u], &e1[u]);
       }
-      const double u0 = clampd(sv.nom[2 * k] + e0, a.lo[0], a.hi[0]);
-      const double u1 = clampd(sv.nom[2 * k + 1] + e1, a.lo[1], a.hi[1]);
-      ubuf[j * T + k] = make_double2(u0, u1);
-      if (vj) {
-        double* scr = scr0 + (size_t)j * SCR_ARRAYS * stride;
-        scr[k] = u0;
-        scr[stride + k] = u1;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (!in[u]) continue;
+        const int j = jj[u], k = kk[u];
+        if (vjs[u] && a.noise_out)
+          reinterpret_cast<double2*>(a.noise_out)[(size_t)slj[u] * T + k] = make_double2(e0[u], e1[u]);
+        const double u0 = clampd(sv.nom[2 * k] + e0[u], a.lo[0], a.hi[0]);
+        const double u1 = clampd(sv.nom[2 * k + 1] + e1[u], a.lo[1], a.hi[1]);
+        ubuf[j * T + k] = make_double2(u0, u1);
+        if (vjs[u]) {
+          double* scr = scr0 + (size_t)j * SCR_ARRAYS * stride;
+          scr[k] = u0;
+          scr[stride + k] = u1;
+        }
       }
     }
     __syncwarp();
