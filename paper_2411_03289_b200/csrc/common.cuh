@@ -225,7 +225,12 @@ GPM_HD double slip_ratio(const double a[5], const double b[5], double sa, double
 GPM_HD bool collides(const TaskDev& t, double x, double y, const double* margins_k) {
   for (int i = 0; i < t.n_obs; ++i) {
     const double dx = x - t.obs[i][0], dy = y - t.obs[i][1];
-    const double d = sqrt(dx * dx + dy * dy) - t.obs[i][2];
+    const double s = dx * dx + dy * dy;
+    // far obstacle: s > 4R^2 (R = radius + margin > 0) gives sqrt(s) - r - m >= R(1 - 1e-15) > 0,
+    // the same "no collision" the exact test below returns, without the FP64 sqrt
+    const double R = t.obs[i][2] + margins_k[i];
+    if (R > 0.0 && s > 4.0 * R * R) continue;
+    const double d = sqrt(s) - t.obs[i][2];
     if (d - margins_k[i] <= 0.0) return true;
   }
   return false;
