@@ -288,19 +288,17 @@ GPM_D void rollout_phase2(const RolloutArgs& a, const SmemView& sv, const TaskDe
 #endif
   // ---------------- phase 2c: positions in step order + first non-finite state
   int kd = T;  // states k > kd are frozen at state kd (mppi.cpp:343-346)
-  if (gl == 0) {  // increments and finiteness of 8 steps loaded ahead of the prefix sum
+  if (gl == 0) {  // increments of 8 steps loaded ahead of the prefix sum (step order)
     double x = x0[0], y = x0[1];
     sx[0] = x;
     sy[0] = y;
     for (int k0 = 0; k0 < T; k0 += 8) {
       double dxv[8], dyv[8];
-      bool fin[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int k = k0 + i < T ? k0 + i : T - 1;
         dxv[i] = sx[k + 1];
         dyv[i] = sy[k + 1];
-        fin[i] = isfinite(sth[k + 1]) && isfinite(sv_[k + 1]) && isfinite(sw[k + 1]);
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i)
@@ -309,11 +307,19 @@ GPM_D void rollout_phase2(const RolloutArgs& a, const SmemView& sv, const TaskDe
           y += dyv[i];
           sx[k0 + i + 1] = x;
           sy[k0 + i + 1] = y;
-          if (kd == T && !(isfinite(x) && isfinite(y) && fin[i])) kd = k0 + i;
         }
     }
   }
-  kd = __shfl_sync(0xffffffffu, kd, (threadIdx.x & 31) & ~(LPS - 1));
+  __syncwarp();
+  // first non-finite state (mppi.cpp:343-346): lanes check their steps, group minimum
+  for (int k = gl; k < T; k += LPS)
+    if (!(isfinite(sx[k + 1]) && isfinite(sy[k + 1]) && isfinite(sth[k + 1]) && isfinite(sv_[k + 1]) &&
+          isfinite(sw[k + 1]))) {
+      kd = k;
+      break;
+    }
+#pragma unroll
+  for (int o = LPS / 2; o > 0; o >>= 1) kd = min(kd, __shfl_xor_sync(0xffffffffu, kd, o));
   __syncwarp();
 #ifdef GPM_ROLLOUT_TRACE
   p2t[3] = clock64();
