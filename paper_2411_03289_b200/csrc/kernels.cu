@@ -41,10 +41,7 @@ GPM_D double warp_min(double v) {
 }
 
 // -------------------------------------------------------------------------
-// FP64 exp for the GP kernel row: exp(x) = 2^(n/32)·e^r, n = rint(32x/ln2),
-// |r| <= ln2/64, degree-6 Taylor (truncation < 4e-18) and a 32-entry 2^(j/32)
-// table in shared memory. ~12 FP64 ops instead of ~22 for libm's exp, within
-// ~2 ulp of it; arguments below -700 flush to 0 (k* < 1e-304).
+// 2^(j/32), j < 32: the exp_tab table (common.cuh), staged into shared memory per block
 __constant__ double kExp2Frac[32] = {
     0x1.0000000000000p+0, 0x1.059b0d3158574p+0, 0x1.0b5586cf9890fp+0, 0x1.11301d0125b51p+0,
     0x1.172b83c7d517bp+0, 0x1.1d4873168b9aap+0, 0x1.2387a6e756238p+0, 0x1.29e9df51fdee1p+0,
@@ -54,27 +51,6 @@ __constant__ double kExp2Frac[32] = {
     0x1.8ace5422aa0dbp+0, 0x1.93737b0cdc5e5p+0, 0x1.9c49182a3f090p+0, 0x1.a5503b23e255dp+0,
     0x1.ae89f995ad3adp+0, 0x1.b7f76f2fb5e47p+0, 0x1.c199bdd85529cp+0, 0x1.cb720dcef9069p+0,
     0x1.d5818dcfba487p+0, 0x1.dfc97337b9b5fp+0, 0x1.ea4afa2a490dap+0, 0x1.f50765b6e4540p+0};
-constexpr double kInvLn2x32 = 0x1.71547652b82fep+5;
-constexpr double kLn2d32Hi = 0x1.62e42fee00000p-6;  // 32 significant bits: n·hi exact for |n| < 2^21
-constexpr double kLn2d32Lo = 0x1.a39ef35793c76p-38;
-GPM_D double exp_tab(double x, const double* tab) {
-  const double magic = 6755399441055744.0;  // 1.5·2^52: round-to-nearest integer trick
-  const double t = fma(x, kInvLn2x32, magic);
-  const int n = __double2loint(t);
-  const double nd = t - magic;
-  double r = fma(nd, -kLn2d32Hi, x);
-  r = fma(nd, -kLn2d32Lo, r);
-  double p = fma(r, 1.0 / 720.0, 1.0 / 120.0);
-  p = fma(r, p, 1.0 / 24.0);
-  p = fma(r, p, 1.0 / 6.0);
-  p = fma(r, p, 0.5);
-  p = fma(r, p, 1.0);
-  p *= r;  // e^r - 1
-  const double tj = tab[n & 31];
-  const double res = fma(tj, p, tj);
-  const double scaled = __hiloint2double(__double2hiint(res) + ((n >> 5) << 20), __double2loint(res));
-  return x < -700.0 ? 0.0 : scaled;
-}
 
 // -------------------------------------------------------------------------
 // Rollout, GP ensemble model. NO = max outputs per kernel group (compile time).
@@ -541,8 +517,9 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
           const double2 av = cv[jp], aw = cw[jp];
 #pragma unroll
           for (int j = 0; j < SPG; ++j) {
-            const double d0 = q0[j] * a0.x + q1[j] * a1.x + q2[j] * a2.x + q3[j] * a3.x + qn[j] + an.x;
-            const double d1 = q0[j] * a0.y + q1[j] * a1.y + q2[j] * a2.y + q3[j] * a3.y + qn[j] + an.y;
+            // q·z + (qn + zn) as one DADD and four DFMAs (gp.cpp:177-179)
+            const double d0 = fma(q0[j], a0.x, fma(q1[j], a1.x, fma(q2[j], a2.x, fma(q3[j], a3.x, qn[j] + an.x))));
+            const double d1 = fma(q0[j], a0.y, fma(q1[j], a1.y, fma(q2[j], a2.y, fma(q3[j], a3.y, qn[j] + an.y))));
             const double k0 = exp_tab(d0, sv.etab), k1 = exp_tab(d1, sv.etab);
             acc[j][0] = fma(k1, av.y, fma(k0, av.x, acc[j][0]));  // gp.cpp:181-182, terrain-combined
             acc[j][1] = fma(k1, aw.y, fma(k0, aw.x, acc[j][1]));
@@ -1471,7 +1448,7 @@ __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const Tight
         double acc0 = 0.0, acc1 = 0.0;  // terrain-combined v / omega means
 #pragma unroll 4
         for (int j = threadIdx.x; j < n; j += TMEAN_THREADS) {
-          const double kj = exp_tab(q0 * p[j] + q1 * p[ns + j] + q2 * p[2 * ns + j] + q3 * p[3 * ns + j] + qn + p[4 * ns + j], etab);
+          const double kj = exp_tab(fma(q0, p[j], fma(q1, p[ns + j], fma(q2, p[2 * ns + j], fma(q3, p[3 * ns + j], qn + p[4 * ns + j])))), etab);
           acc0 = fma(kj, p[5 * ns + j], acc0);
           acc1 = fma(kj, p[6 * ns + j], acc1);
         }
