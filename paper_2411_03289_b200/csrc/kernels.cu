@@ -1341,7 +1341,9 @@ cudaError_t launch_predict(const ModelDev& m, const double* q, long long S, doub
 // one block), then every step's GP variance and Jacobian in parallel (one block
 // per (step, group, column slice)), then the 5×5 covariance recursion and the
 // thresholds (one warp).
-constexpr int TIGHT_ROWS = 64;  // rows of L^{-1} per variance block
+// rows of L^{-1} per tightening-variance block: short slices (more, shorter blocks: the
+// per-warp row loop is L2-latency bound) while the per-block k* recomputation is cheap
+GPM_HD int tight_rows(int n) { return n <= 1024 ? 16 : 64; }
 
 // Belief-mean chain. The GP query of step k needs only (v_k, omega_k, u_k) and
 // the lag update of (v, omega) is cheap, so the serial part carries (v, omega)
@@ -1546,7 +1548,7 @@ __global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const Tight
 #endif
 }
 
-// grid (T, G*B, ceil(n / TIGHT_ROWS)): partial ||L^{-1} k*||^2 over a slice of rows of
+// grid (T, G*B, ceil(n / tight_rows(n))): partial ||L^{-1} k*||^2 over a slice of rows of
 // L^{-1}. One warp per row: a_j = sum_{i<=j} k_i L^{-1}[j][i] with the lanes striding
 // the contiguous row (coalesced), then a_j^2 (gp.cpp:184-191).
 __global__ void __launch_bounds__(256) tighten_var_kernel(const TightenArgs a) {
@@ -1559,8 +1561,8 @@ __global__ void __launch_bounds__(256) tighten_var_kernel(const TightenArgs a) {
   const double* q = a.tq + (size_t)rb * 4 * a.T + k * 4;
   const double q0 = q[0] / G.ls[0], q1 = q[1] / G.ls[1], q2 = q[2] / G.ls[2], q3 = q[3] / G.ls[3];
   const double qn = -0.5 * (q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
-  const int j0 = c * TIGHT_ROWS;
-  const int jend = min(n, j0 + TIGHT_ROWS);
+  const int j0 = c * tight_rows(n);
+  const int jend = min(n, j0 + tight_rows(n));
   const double* p = G.pts;
   const int ns = a.model.ns;
   for (int i = threadIdx.x; i < jend; i += blockDim.x)  // columns i <= j only
@@ -1757,7 +1759,7 @@ __global__ void __launch_bounds__(256) tighten_cov_kernel(const TightenArgs a, i
 #endif
 }
 
-int tighten_splits(int n) { return n > 0 ? (n + TIGHT_ROWS - 1) / TIGHT_ROWS : 1; }
+int tighten_splits(int n) { return n > 0 ? (n + tight_rows(n) - 1) / tight_rows(n) : 1; }
 
 cudaError_t launch_tighten(const TightenArgs& a, cudaStream_t st) {
   size_t msm = sizeof(double) * (size_t)(2 * a.T + 3 * (a.T + 1) + 2 * a.T + 1);
