@@ -200,6 +200,10 @@ GPM_D void group_allsum(double (&val)[NV]) {
 //          (mppi.cpp:343-346), per-step costs and flags (costs.cpp:127-171).
 // Per-sample trajectory scratch lives in L2 (scr, 9 arrays of T+1 doubles).
 constexpr int SCR_ARRAYS = 9;
+#ifndef GPM_ROLL_UNROLL
+#define GPM_ROLL_UNROLL 16
+#endif
+constexpr int kRollUnroll = GPM_ROLL_UNROLL;  // point pairs in flight per lane and sample in the GP loop
 constexpr int kMaxSampleSlotsPerBlock = 128;  // groups per block x SPG: <= 64 x 2, 8 x 4
 #ifndef GPM_ROLLOUT_MINB
 #define GPM_ROLLOUT_MINB 1
@@ -510,7 +514,7 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
         const double2* cv = reinterpret_cast<const double2*>(gp + 5 * ns);
         const double2* cw = reinterpret_cast<const double2*>(gp + 6 * ns);
         const int half = ns >> 1;
-#pragma unroll(4 / SPG)
+#pragma unroll(kRollUnroll / SPG)
         for (int jp = gl; jp < half; jp += LPS) {
           // gp.cpp:177-179: k*_j = exp(q_aug · inputs_aug_j)
           const double2 a0 = z0[jp], a1 = z1[jp], a2 = z2[jp], a3 = z3[jp], an = zn[jp];
