@@ -1415,12 +1415,13 @@ int gpmppi_flush_l2(int device) {
     int l2 = 0;
     CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device));
     const size_t bytes = (size_t)std::max(l2, 1 << 20) * 2;
-    void* buf = nullptr;
-    CK(cudaMalloc(&buf, bytes));
-    cudaError_t e = cudaMemset(buf, 0x5a, bytes);
-    if (e == cudaSuccess) e = cudaDeviceSynchronize();
-    cudaFree(buf);
-    CK(e);
+    // one flush buffer per device, kept for the process (an allocate/free per flush also
+    // unmaps pages and cold-starts the TLBs, which is not what the flush is meant to model)
+    static void* bufs[64] = {};
+    if (device >= 64) invalid("flush_l2: device index too large");
+    if (!bufs[device]) CK(cudaMalloc(&bufs[device], bytes));
+    CK(cudaMemset(bufs[device], 0x5a, bytes));
+    CK(cudaDeviceSynchronize());
   });
 }
 

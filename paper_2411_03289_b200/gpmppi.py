@@ -427,12 +427,16 @@ class Planner:
 
     # -- Planner::plan_step (mppi.cpp:464-475)
     def plan_step(self, x0, task, diag: Optional[StepDiagnostics] = None):
-        x = _f64(x0, (5,))
+        st = self.__dict__.get("_step_io")
+        if st is None:  # per-planner call buffers and their C pointers, built once
+            xb, cb, db = np.empty(5), np.empty(2), A.DiagC()
+            st = (xb, A.dptr(xb), cb, A.dptr(cb), db, C.byref(db), A.lib().gpmppi_planner_plan_step)
+            self.__dict__["_step_io"] = st
+        xb, xp, cb, cp, d, dref, fn = st
+        xb[:] = np.asarray(x0, dtype=np.float64).reshape(5)
         tc = task.to_c()
-        cmd = np.empty(2)
-        d = A.DiagC()
-        A.check(A.lib().gpmppi_planner_plan_step(self._h, A.dptr(x), C.byref(tc), A.dptr(cmd),
-                                                 C.byref(d)))
+        A.check(fn(self._h, xp, C.byref(tc), cp, dref))
+        cmd = cb.copy()
         if diag is not None:
             for k, _ in A.DiagC._fields_:
                 setattr(diag, k, getattr(d, k))
