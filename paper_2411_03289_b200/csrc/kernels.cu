@@ -1359,7 +1359,7 @@ GPM_HD int tight_rows(int n) { return n <= 1024 ? 16 : 64; }
 #endif
 constexpr int TMEAN_THREADS = GPM_TMEAN_THREADS;
 template <int NO>
-__global__ void __launch_bounds__(TMEAN_THREADS) tighten_mean_kernel(const TightenArgs a) {
+__global__ void __launch_bounds__(TMEAN_THREADS, 1) tighten_mean_kernel(const TightenArgs a) {
   const int rb = blockIdx.x;  // robot
 #ifdef GPM_TMEAN_TRACE
   const long long tk0 = clock64();
