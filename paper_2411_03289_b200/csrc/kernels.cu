@@ -1452,11 +1452,24 @@ __global__ void __launch_bounds__(TMEAN_THREADS, 1) tighten_mean_kernel(const Ti
         const double q2 = u0 * gil[g][2], q3 = u1 * gil[g][3];
         const double qn = -0.5 * (q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
         double acc0 = 0.0, acc1 = 0.0;  // terrain-combined v / omega means
-#pragma unroll 4
-        for (int j = threadIdx.x; j < n; j += TMEAN_THREADS) {
-          const double kj = exp_tab(fma(q0, p[j], fma(q1, p[ns + j], fma(q2, p[2 * ns + j], fma(q3, p[3 * ns + j], qn + p[4 * ns + j])))), etab);
-          acc0 = fma(kj, p[5 * ns + j], acc0);
-          acc1 = fma(kj, p[6 * ns + j], acc1);
+        // four points per round with their exponentials side by side
+        for (int j0 = threadIdx.x; j0 < n; j0 += 4 * TMEAN_THREADS) {
+          double kj[4], av[4], aw[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int j = j0 + i * TMEAN_THREADS;
+            const bool in = j < n;
+            const int jc = in ? j : j0;
+            const double d = fma(q0, p[jc], fma(q1, p[ns + jc], fma(q2, p[2 * ns + jc], fma(q3, p[3 * ns + jc], qn + p[4 * ns + jc]))));
+            kj[i] = exp_tab(d, etab);
+            av[i] = in ? p[5 * ns + jc] : 0.0;
+            aw[i] = in ? p[6 * ns + jc] : 0.0;
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            acc0 = fma(kj[i], av[i], acc0);
+            acc1 = fma(kj[i], aw[i], acc1);
+          }
         }
         TRC(1);
         {  // transpose-reduce the two sums across the warp (5 shuffles): lanes 0-15
