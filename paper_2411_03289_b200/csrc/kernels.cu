@@ -966,7 +966,7 @@ GPM_HD int reduce_slab_samples(int T, int threads) {
   return cap < threads ? (cap < 1 ? 1 : cap) : threads;
 }
 
-__global__ void __launch_bounds__(256) reduce_kernel(const ReduceArgs a) {
+__global__ void __launch_bounds__(256, 1) reduce_kernel(const ReduceArgs a) {
   extern __shared__ __align__(16) double dsm[];
   __shared__ double red[32 * 5];
   __shared__ unsigned int s_last;
@@ -1614,7 +1614,7 @@ __global__ void __launch_bounds__(256) tighten_var_kernel(const TightenArgs a) {
 // 256 threads stage J / mu / the per-step correction variances, warp 0 runs the
 // serial recursion Σ_{k+1} = J Σ Jᵀ + diag(0,0,0,cv0,cv1) (symmetrised), then all
 // threads evaluate r̄_k and the margins in parallel.
-__global__ void __launch_bounds__(256) tighten_cov_kernel(const TightenArgs a, int nsplit) {
+__global__ void __launch_bounds__(256, 1) tighten_cov_kernel(const TightenArgs a, int nsplit) {
   const int rb = blockIdx.x;  // robot
 #ifdef GPM_TCOV_TRACE
   long long ct[6];
