@@ -1582,8 +1582,11 @@ __global__ void __launch_bounds__(256) tighten_var_kernel(const TightenArgs a) {
   const int jend = min(n, j0 + tight_rows(n));
   const double* p = G.pts;
   const int ns = a.model.ns;
+  __shared__ double etab[32];
+  if (threadIdx.x < 32) etab[threadIdx.x] = kExp2Frac[threadIdx.x];
+  __syncthreads();
   for (int i = threadIdx.x; i < jend; i += blockDim.x)  // columns i <= j only
-    kst[i] = exp(q0 * p[i] + q1 * p[ns + i] + q2 * p[2 * ns + i] + q3 * p[3 * ns + i] + qn + p[4 * ns + i]);
+    kst[i] = exp_tab(fma(q0, p[i], fma(q1, p[ns + i], fma(q2, p[2 * ns + i], fma(q3, p[3 * ns + i], qn + p[4 * ns + i])))), etab);
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   double ssq = 0.0;
