@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -147,6 +148,30 @@ struct TightenArgs {
   double* tJ;         // [B][T][25] Jacobians
   double* tvar_part;  // [B][T][G][splits] partial ||L^{-1}k*||^2
 };
+
+// Programmatic dependent launch: the kernel may be scheduled while its stream
+// predecessor finishes; it must execute pdl_wait() (griddepcontrol.wait) before it
+// reads anything the predecessor wrote. Predecessors call pdl_trigger() once all their
+// CTAs are resident (single-wave kernels: at entry).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+#if defined(__CUDACC__)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+#endif
 
 // launchers (kernels.cu); all enqueue on `st` and return cudaGetLastError()
 cudaError_t launch_rollout(const RolloutArgs& a, int num_sms, cudaStream_t st);

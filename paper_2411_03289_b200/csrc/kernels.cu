@@ -357,6 +357,7 @@ GPM_D void rollout_phase2(const RolloutArgs& a, const SmemView& sv, const TaskDe
 
 template <int NO, int LPS, int SPG>
 __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const RolloutArgs a) {
+  pdl_trigger();  // single wave: the variance grid may be scheduled (it waits for this grid)
   extern __shared__ __align__(16) unsigned char smem[];
   const SmemView sv = carve_smem(a, smem);
   const int ns = a.model.ns;  // even SoA stride (padding points contribute exactly 0)
@@ -967,6 +968,8 @@ GPM_HD int reduce_slab_samples(int T, int threads) {
 }
 
 __global__ void __launch_bounds__(256, 1) reduce_kernel(const ReduceArgs a) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) double dsm[];
   __shared__ double red[32 * 5];
   __shared__ unsigned int s_last;
@@ -1228,7 +1231,8 @@ cudaError_t launch_reduce(const ReduceArgs& a, int blocks, cudaStream_t st) {
   const size_t need = sizeof(double) * ((size_t)a.bpr * tuple_doubles(a.T) + a.bpr + 2 * a.T);
   if (smem < need) smem = need;
   cudaFuncSetAttribute(reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  reduce_kernel<<<blocks, threads, smem, st>>>(a);
+  cudaError_t el = launch_pdl(reduce_kernel, dim3(blocks), dim3(threads), smem, st, a);
+  if (el != cudaSuccess) return el;
   count_launch();
   return cudaGetLastError();
 }
@@ -1360,6 +1364,8 @@ GPM_HD int tight_rows(int n) { return n <= 1024 ? 16 : 64; }
 constexpr int TMEAN_THREADS = GPM_TMEAN_THREADS;
 template <int NO>
 __global__ void __launch_bounds__(TMEAN_THREADS, 1) tighten_mean_kernel(const TightenArgs a) {
+  pdl_wait();
+  pdl_trigger();
   const int rb = blockIdx.x;  // robot
 #ifdef GPM_TMEAN_TRACE
   const long long tk0 = clock64();
@@ -1569,6 +1575,8 @@ __global__ void __launch_bounds__(TMEAN_THREADS, 1) tighten_mean_kernel(const Ti
 // L^{-1}. One warp per row: a_j = sum_{i<=j} k_i L^{-1}[j][i] with the lanes striding
 // the contiguous row (coalesced), then a_j^2 (gp.cpp:184-191).
 __global__ void __launch_bounds__(256) tighten_var_kernel(const TightenArgs a) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) double kst[];
   __shared__ double red[8];
   const int k = blockIdx.x, g = blockIdx.y % a.model.G, rb = blockIdx.y / a.model.G, c = blockIdx.z;
@@ -1618,6 +1626,7 @@ __global__ void __launch_bounds__(256) tighten_var_kernel(const TightenArgs a) {
 // serial recursion Σ_{k+1} = J Σ Jᵀ + diag(0,0,0,cv0,cv1) (symmetrised), then all
 // threads evaluate r̄_k and the margins in parallel.
 __global__ void __launch_bounds__(256, 1) tighten_cov_kernel(const TightenArgs a, int nsplit) {
+  pdl_wait();
   const int rb = blockIdx.x;  // robot
 #ifdef GPM_TCOV_TRACE
   long long ct[6];
@@ -1791,15 +1800,20 @@ cudaError_t launch_tighten(const TightenArgs& a, cudaStream_t st) {
   void (*mk)(const TightenArgs) = no <= 2 ? tighten_mean_kernel<2> : no <= 4 ? tighten_mean_kernel<4>
                                   : no <= 6 ? tighten_mean_kernel<6> : tighten_mean_kernel<8>;
   cudaFuncSetAttribute(mk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm);  // static + dynamic may exceed 48 KB
-  mk<<<a.B, TMEAN_THREADS, msm, st>>>(a);
+  cudaError_t el = launch_pdl(mk, dim3(a.B), dim3(TMEAN_THREADS), msm, st, a);
+  if (el != cudaSuccess) return el;
   const int G = a.model_kind == MODEL_GP ? a.model.G : 1;
   const int ns = a.model_kind == MODEL_GP ? tighten_splits(a.model.n) : 1;
   const size_t smem = sizeof(double) * (size_t)(a.model.n > 0 ? a.model.n : 1);
   cudaFuncSetAttribute(tighten_var_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (a.model_kind == MODEL_GP) tighten_var_kernel<<<dim3(a.T, G * a.B, ns), 256, smem, st>>>(a);
+  if (a.model_kind == MODEL_GP) {
+    el = launch_pdl(tighten_var_kernel, dim3(a.T, G * a.B, ns), dim3(256), smem, st, a);
+    if (el != cudaSuccess) return el;
+  }
   const size_t csmem = sizeof(double) * (size_t)(25 * a.T + 2 * a.T + 5 * (a.T + 1) + 25 * a.T);
   cudaFuncSetAttribute(tighten_cov_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem);
-  tighten_cov_kernel<<<a.B, 256, csmem, st>>>(a, ns);
+  el = launch_pdl(tighten_cov_kernel, dim3(a.B), dim3(256), csmem, st, a, ns);
+  if (el != cudaSuccess) return el;
   count_launch(3);
   return cudaGetLastError();
 }

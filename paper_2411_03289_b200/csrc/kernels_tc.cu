@@ -1029,6 +1029,8 @@ __device__ __forceinline__ uint32_t half2_bits(__half2 h) {
 
 __global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const VarianceArgs a, int dbg, int S) {
   using namespace tc;
+  pdl_wait();  // queries come from the rollout grid
+  pdl_trigger();
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const GroupDev& G = a.g;
   const int n = a.n, n_pad = G.tc_npad, NP = G.tc_np, n_pass = G.tc_npass;
@@ -1339,7 +1341,8 @@ cudaError_t launch_tc_variance(const VarianceArgs& a, int mode, cudaStream_t st)
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       const long long units = ((a.KT + tc::M - 1) / tc::M + 1) / 2;
       const int grid = (int)(units < sms ? units : sms);
-      variance_f16_kernel<<<grid, tc::THREADS, hsm, st>>>(a, dbg_h, stages);
+      cudaError_t el = launch_pdl(variance_f16_kernel, dim3(grid), dim3(tc::THREADS), hsm, st, a, dbg_h, stages);
+      if (el != cudaSuccess) return el;
       count_launch();
       return cudaGetLastError();
     }
