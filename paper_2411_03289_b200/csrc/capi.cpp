@@ -521,6 +521,8 @@ int gpmppi_model_variance_batch(const gpmppi_model* M, const double* q, int64_t 
 struct gpmppi_planner {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;                   // command readback branch (concurrent with tightening)
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   int num_sms = 148;
   gpmppi_mppi_config cfg{};
   int model_kind = 0;
@@ -593,6 +595,9 @@ struct gpmppi_planner {
       if (e) cudaEventDestroy(e);
     if (tick_exec) cudaGraphExecDestroy(tick_exec);
     if (tick_graph) cudaGraphDestroy(tick_graph);
+    if (fork_ev) cudaEventDestroy(fork_ev);
+    if (join_ev) cudaEventDestroy(join_ev);
+    if (side) cudaStreamDestroy(side);
     if (stream) cudaStreamDestroy(stream);
   }
   long long slots() const { return (long long)B * K_local; }
@@ -971,6 +976,9 @@ gpmppi_planner* create_planner(const gpmppi_mppi_config* cfg, const gpmppi_predi
   try {
     p->device = device;
     CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&p->fork_ev, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&p->join_ev, cudaEventDisableTiming));
     CK(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device));
     p->cfg = *cfg;
     p->B = n_robots;
@@ -1045,12 +1053,19 @@ gpmppi_planner* create_planner(const gpmppi_mppi_config* cfg, const gpmppi_predi
 void enqueue_tick(gpmppi_planner* p, bool capturing) {
   enqueue_h2d(p);
   enqueue_samples(p, 1, nullptr);
-  copy_out_async(p);
+  // the command / diagnostics readback forks off onto the side stream, so the tightening
+  // follows the reduction directly on the main stream (no copy on its critical path)
+  CK(cudaEventRecord(p->fork_ev, p->stream));
+  CK(cudaStreamWaitEvent(p->side, p->fork_ev, 0));
+  CK(cudaMemcpyAsync(p->h_out, p->d_out, sizeof(double) * gpm::BatchStrides::OUT * p->B, cudaMemcpyDeviceToHost,
+                     p->side));
   if (capturing)
-    CK(cudaEventRecordWithFlags(p->ev[0], p->stream, cudaEventRecordExternal));
+    CK(cudaEventRecordWithFlags(p->ev[0], p->side, cudaEventRecordExternal));
   else
-    CK(cudaEventRecord(p->ev[0], p->stream));
+    CK(cudaEventRecord(p->ev[0], p->side));
+  CK(cudaEventRecord(p->join_ev, p->side));
   enqueue_tighten(p);
+  CK(cudaStreamWaitEvent(p->stream, p->join_ev, 0));
   CK(cudaMemcpyAsync(p->h_infeasible, p->d_infeasible, sizeof(int) * p->B, cudaMemcpyDeviceToHost, p->stream));
 }
 
