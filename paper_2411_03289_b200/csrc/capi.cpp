@@ -1393,29 +1393,41 @@ int gpmppi_planner_bench_device(gpmppi_planner* p, const double* x0, const gpmpp
       flush_bytes = (size_t)std::max(l2, 1 << 20) * 2;
       CK(cudaMalloc(&flush, flush_bytes));
     }
-    std::vector<cudaEvent_t> evs((size_t)ticks * 5);
+    // pass 1: per-phase events (an event between two kernels also breaks their
+    // programmatic-dependent-launch overlap, so these sum to slightly more than a tick);
+    // pass 2: the tick itself, one event pair around the unbroken kernel sequence
+    std::vector<cudaEvent_t> evs((size_t)ticks * 7);
     for (auto& e : evs) CK(cudaEventCreate(&e));
     for (int t = 0; t < ticks; ++t) {
-      cudaEvent_t* E = &evs[(size_t)t * 5];
+      cudaEvent_t* E = &evs[(size_t)t * 7];
       if (flush) CK(cudaMemsetAsync(flush, t & 0xff, flush_bytes, p->stream));  // outside the timed span
       enqueue_samples(p, 1, E);
       enqueue_tighten(p);
       CK(cudaEventRecord(E[4], p->stream));
       ++p->tick;  // the staged keys stay at the first tick: same work, fixed noise
     }
+    for (int t = 0; t < ticks; ++t) {
+      cudaEvent_t* E = &evs[(size_t)t * 7];
+      if (flush) CK(cudaMemsetAsync(flush, (t + 7) & 0xff, flush_bytes, p->stream));
+      CK(cudaEventRecord(E[5], p->stream));
+      enqueue_samples(p, 1, nullptr);
+      enqueue_tighten(p);
+      CK(cudaEventRecord(E[6], p->stream));
+      ++p->tick;
+    }
     cudaError_t se = cudaStreamSynchronize(p->stream);
     if (flush) cudaFree(flush);
     CK(se);
     double ph[4] = {0, 0, 0, 0};
     for (int t = 0; t < ticks; ++t) {
-      cudaEvent_t* E = &evs[(size_t)t * 5];
+      cudaEvent_t* E = &evs[(size_t)t * 7];
       for (int i = 0; i < 4; ++i) {
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, E[i], E[i + 1]));
         ph[i] += ms;
       }
       float tot = 0.f;
-      CK(cudaEventElapsedTime(&tot, E[0], E[4]));
+      CK(cudaEventElapsedTime(&tot, E[5], E[6]));
       if (tick_ms) tick_ms[t] = tot;
     }
     for (auto& e : evs) cudaEventDestroy(e);
