@@ -357,6 +357,7 @@ GPM_D void rollout_phase2(const RolloutArgs& a, const SmemView& sv, const TaskDe
 
 template <int NO, int LPS, int SPG>
 __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const RolloutArgs a) {
+  pdl_wait();     // previous tick's thresholds / nominal (when launched after a kernel)
   pdl_trigger();  // single wave: the variance grid may be scheduled (it waits for this grid)
   extern __shared__ __align__(16) unsigned char smem[];
   const SmemView sv = carve_smem(a, smem);
@@ -765,7 +766,8 @@ cudaError_t launch_rollout(const RolloutArgs& a, int num_sms, cudaStream_t st) {
     if (ra.scratch_smem) smem_u += scr_bytes;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_u);
     if (e != cudaSuccess) return e;
-    kern<<<(unsigned)blocks, threads, smem_u, st>>>(ra);
+    e = launch_pdl(kern, dim3((unsigned)blocks), dim3(threads), smem_u, st, ra);
+    if (e != cudaSuccess) return e;
   } else {
     const int threads = 128;
     const long long items = (long long)a.B * ((a.K_local + threads - 1) / threads);
@@ -1627,6 +1629,7 @@ __global__ void __launch_bounds__(256) tighten_var_kernel(const TightenArgs a) {
 // threads evaluate r̄_k and the margins in parallel.
 __global__ void __launch_bounds__(256, 1) tighten_cov_kernel(const TightenArgs a, int nsplit) {
   pdl_wait();
+  pdl_trigger();
   const int rb = blockIdx.x;  // robot
 #ifdef GPM_TCOV_TRACE
   long long ct[6];
