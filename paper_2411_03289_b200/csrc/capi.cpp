@@ -1031,7 +1031,7 @@ gpmppi_planner* create_planner(const gpmppi_mppi_config* cfg, const gpmppi_predi
     p->d_tJ = p->dalloc<double>((size_t)B * T * 25);
     {
       const int G = p->model ? p->groups() : 1;
-      const int ns = p->model ? gpm::tighten_splits(p->model->n) : 1;
+      const int ns = p->model ? gpm::tighten_splits(p->model->n, B) : 1;
       p->d_tvar = p->dalloc<double>((size_t)B * T * G * ns);
     }
     p->alloc_sample_buffers();

@@ -197,7 +197,7 @@ cudaError_t launch_philox_noise(uint64_t key, long long s_begin, int K, int T, d
 size_t rollout_smem_bytes(const RolloutArgs& a);
 size_t rollout_scratch_doubles(int T, int num_sms);
 int reduce_blocks_for(int K_local, int B, int num_sms, int T);
-int tighten_splits(int n);
+int tighten_splits(int n, int B);
 void build_tc_operand_f16(const double* ilt, int n, double sv, int n_pad, int np, int n_pass,
                           std::vector<uint16_t>& data, std::vector<int4>& meta, double& hfac);
 void build_tc_operand(const double* ilt, int n, std::vector<float>& data, std::vector<int4>& meta,

@@ -1353,7 +1353,8 @@ cudaError_t launch_predict(const ModelDev& m, const double* q, long long S, doub
 // thresholds (one warp).
 // rows of L^{-1} per tightening-variance block: short slices (more, shorter blocks: the
 // per-warp row loop is L2-latency bound) while the per-block k* recomputation is cheap
-GPM_HD int tight_rows(int n) { return n <= 1024 ? 16 : 64; }
+// (one robot only: with many robots the grid is already wide and 64-row slices recompute less)
+GPM_HD int tight_rows(int n, int B) { return (B == 1 && n <= 1024) ? 16 : 64; }
 
 // Belief-mean chain. The GP query of step k needs only (v_k, omega_k, u_k) and
 // the lag update of (v, omega) is cheap, so the serial part carries (v, omega)
@@ -1573,7 +1574,7 @@ __global__ void __launch_bounds__(TMEAN_THREADS, 1) tighten_mean_kernel(const Ti
 #endif
 }
 
-// grid (T, G*B, ceil(n / tight_rows(n))): partial ||L^{-1} k*||^2 over a slice of rows of
+// grid (T, G*B, ceil(n / tight_rows(n, B))): partial ||L^{-1} k*||^2 over a slice of rows of
 // L^{-1}. One warp per row: a_j = sum_{i<=j} k_i L^{-1}[j][i] with the lanes striding
 // the contiguous row (coalesced), then a_j^2 (gp.cpp:184-191).
 __global__ void __launch_bounds__(256) tighten_var_kernel(const TightenArgs a) {
@@ -1588,8 +1589,9 @@ __global__ void __launch_bounds__(256) tighten_var_kernel(const TightenArgs a) {
   const double* q = a.tq + (size_t)rb * 4 * a.T + k * 4;
   const double q0 = q[0] / G.ls[0], q1 = q[1] / G.ls[1], q2 = q[2] / G.ls[2], q3 = q[3] / G.ls[3];
   const double qn = -0.5 * (q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
-  const int j0 = c * tight_rows(n);
-  const int jend = min(n, j0 + tight_rows(n));
+  const int rows = tight_rows(n, a.B);
+  const int j0 = c * rows;
+  const int jend = min(n, j0 + rows);
   const double* p = G.pts;
   const int ns = a.model.ns;
   __shared__ double etab[32];
@@ -1791,7 +1793,7 @@ __global__ void __launch_bounds__(256, 1) tighten_cov_kernel(const TightenArgs a
 #endif
 }
 
-int tighten_splits(int n) { return n > 0 ? (n + tight_rows(n) - 1) / tight_rows(n) : 1; }
+int tighten_splits(int n, int B) { return n > 0 ? (n + tight_rows(n, B) - 1) / tight_rows(n, B) : 1; }
 
 cudaError_t launch_tighten(const TightenArgs& a, cudaStream_t st) {
   size_t msm = sizeof(double) * (size_t)(2 * a.T + 3 * (a.T + 1) + 2 * a.T + 1);
@@ -1806,7 +1808,7 @@ cudaError_t launch_tighten(const TightenArgs& a, cudaStream_t st) {
   cudaError_t el = launch_pdl(mk, dim3(a.B), dim3(TMEAN_THREADS), msm, st, a);
   if (el != cudaSuccess) return el;
   const int G = a.model_kind == MODEL_GP ? a.model.G : 1;
-  const int ns = a.model_kind == MODEL_GP ? tighten_splits(a.model.n) : 1;
+  const int ns = a.model_kind == MODEL_GP ? tighten_splits(a.model.n, a.B) : 1;
   const size_t smem = sizeof(double) * (size_t)(a.model.n > 0 ? a.model.n : 1);
   cudaFuncSetAttribute(tighten_var_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (a.model_kind == MODEL_GP) {
