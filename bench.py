@@ -142,8 +142,8 @@ def roofline_block(w, phase, steps, peaks, peaks_kind, var_path=3):
     roll = {"kernel": "rollout_gp_kernel", "bound": "tensor", "launch_ms": roll_ms, "flop_per_launch": units * 22 * n,
             "own_peak": 148 * 64 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12,
             "own_peak_kind": "fp64_tflops (148 SM x 64 DFMA x 2 x max clock)",
-            "binding_resource": "FP64 pipe + shared-memory wavefronts + issue (ncu: FP64 46%/60%, LSU shared 50%/62%, "
-                                "issue 49%/56% at config2/config5)"}
+            "binding_resource": "FP64 pipe + shared-memory wavefronts + issue (ncu at config2: FP64 51%, LSU shared 60%; "
+                                "7 warps/SM, latency-bound; config5: FP64 60%)"}
     for k in (var, roll):
         k["achieved"] = k["flop_per_launch"] / (k["launch_ms"] / 1e3) / 1e12
         k["peak"] = peak
