@@ -1367,7 +1367,6 @@ GPM_HD int tight_rows(int n, int B) { return (B == 1 && n <= 1024) ? 16 : 64; }
 constexpr int TMEAN_THREADS = GPM_TMEAN_THREADS;
 template <int NO>
 __global__ void __launch_bounds__(TMEAN_THREADS, 1) tighten_mean_kernel(const TightenArgs a) {
-  pdl_wait();
   pdl_trigger();
   const int rb = blockIdx.x;  // robot
 #ifdef GPM_TMEAN_TRACE
@@ -1390,13 +1389,9 @@ __global__ void __launch_bounds__(TMEAN_THREADS, 1) tighten_mean_kernel(const Ti
   double* dx = th + (T + 1);
   double* dy = dx + T;
   double* pts = dy + T + ((7 * T + 3) & 1);  // 16-byte aligned for the vectorised staging
+  // model data and the host-staged terrain weights are ready before the predecessor
+  // grid ends: staged ahead of griddepcontrol.wait (overlapping the reduction's tail)
   if (threadIdx.x < a.R) tw[threadIdx.x] = a.tw[(size_t)rb * BatchStrides::TW + threadIdx.x];
-  for (int i = threadIdx.x; i < 2 * T; i += blockDim.x) nom[i] = a.nominal_seq[(size_t)rb * BatchStrides::nom(T) + i];
-  if (threadIdx.x == 0) {
-    vv[0] = ax0[3];
-    ww[0] = ax0[4];
-    th[0] = ax0[2];
-  }
   if (a.model_kind == MODEL_GP) {  // vectorised staging of Z + terrain-combined alpha
     double* dst = pts;
     const int ns = a.model.ns;
@@ -1405,7 +1400,7 @@ __global__ void __launch_bounds__(TMEAN_THREADS, 1) tighten_mean_kernel(const Ti
       const GroupDev& Gd = a.model.g[g];
       const double2* src = reinterpret_cast<const double2*>(Gd.pts);
       double2* d2 = reinterpret_cast<double2*>(dst);
-#pragma unroll 4
+#pragma unroll 10
       for (int i = threadIdx.x; i < 5 * ns / 2; i += blockDim.x) d2[i] = __ldg(src + i);
       // combine_terrains (mppi.cpp:34-49) folded into alpha, as in the rollout (load_robot_smem)
       for (int j = threadIdx.x; j < ns; j += blockDim.x) {
@@ -1428,6 +1423,13 @@ __global__ void __launch_bounds__(TMEAN_THREADS, 1) tighten_mean_kernel(const Ti
       }
       dst += 7 * ns;
     }
+  }
+  pdl_wait();  // the nominal sequence comes from the reduction
+  for (int i = threadIdx.x; i < 2 * T; i += blockDim.x) nom[i] = a.nominal_seq[(size_t)rb * BatchStrides::nom(T) + i];
+  if (threadIdx.x == 0) {
+    vv[0] = ax0[3];
+    ww[0] = ax0[4];
+    th[0] = ax0[2];
   }
   __syncthreads();
   const double av = a.nom.dt / a.nom.tau_v, aw = a.nom.dt / a.nom.tau_omega;
