@@ -357,7 +357,6 @@ GPM_D void rollout_phase2(const RolloutArgs& a, const SmemView& sv, const TaskDe
 
 template <int NO, int LPS, int SPG>
 __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const RolloutArgs a) {
-  pdl_wait();     // previous tick's thresholds / nominal (when launched after a kernel)
   pdl_trigger();  // single wave: the variance grid may be scheduled (it waits for this grid)
   extern __shared__ __align__(16) unsigned char smem[];
   const SmemView sv = carve_smem(a, smem);
@@ -383,6 +382,7 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
   }
   __shared__ double gil[kMaxGroups][4];  // reciprocal lengthscales: no FP64 divide on the chain
   if (threadIdx.x < 4 * a.model.G) gil[threadIdx.x >> 2][threadIdx.x & 3] = 1.0 / a.model.g[threadIdx.x >> 2].ls[threadIdx.x & 3];
+  pdl_wait();  // model staging above overlapped the predecessor; per-tick inputs below
   const TaskDev& task = *sv.task;
   const int stride = T + 1;
   // scratch slot of sample j of this group

@@ -1029,7 +1029,6 @@ __device__ __forceinline__ uint32_t half2_bits(__half2 h) {
 
 __global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const VarianceArgs a, int dbg, int S) {
   using namespace tc;
-  pdl_wait();  // queries come from the rollout grid
   pdl_trigger();
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const GroupDev& G = a.g;
@@ -1080,6 +1079,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const Vari
   __syncthreads();
   tc_after();
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  pdl_wait();  // prologue (model operands, barriers, TMEM) overlapped the rollout's tail; queries next
   if (threadIdx.x == 0) trace_at(1, dbg);
 
   if (warp == 0 && lane == 0) {
