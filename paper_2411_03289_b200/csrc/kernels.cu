@@ -1632,7 +1632,9 @@ __global__ void __launch_bounds__(256) tighten_var_kernel(const TightenArgs a) {
 // serial recursion Σ_{k+1} = J Σ Jᵀ + diag(0,0,0,cv0,cv1) (symmetrised), then all
 // threads evaluate r̄_k and the margins in parallel.
 __global__ void __launch_bounds__(256, 1) tighten_cov_kernel(const TightenArgs a, int nsplit) {
-  pdl_wait();
+  // with a GP the predecessor is the variance grid and the mean kernel's J / belief
+  // means are already complete; without one the mean kernel is the predecessor
+  if (a.model_kind != MODEL_GP) pdl_wait();
   pdl_trigger();
   const int rb = blockIdx.x;  // robot
 #ifdef GPM_TCOV_TRACE
@@ -1664,6 +1666,7 @@ __global__ void __launch_bounds__(256, 1) tighten_cov_kernel(const TightenArgs a
     for (int g = 0; g < G; ++g)
       for (int o = 0; o < a.model.g[g].n_out; ++o) gof[a.model.g[g].out_idx[o]] = g;
   }
+  pdl_wait();  // J / belief means come from the mean kernel (complete); the variance partials next
   __syncthreads();
   // per-step combined correction variance (gp.cpp:187-191 + ensemble_combine gp.cpp:380-386)
   for (int k = l; k < T; k += nt) {
