@@ -1718,6 +1718,7 @@ __global__ void __launch_bounds__(256, 1) tighten_cov_kernel(const TightenArgs a
     // their operands with shuffles (no shared-memory round trips on the serial chain)
     const int i5 = l < 25 ? l / 5 : 4, j5 = l < 25 ? l % 5 : 4;
     double Sr = 0.0;
+    double cvk = (l == 18 || l == 24) ? cvs[l == 24] : 0.0;
     double Jin[5], Jjn[5];  // step k's J rows, loaded one step ahead (off the serial chain)
 #pragma unroll
     for (int q = 0; q < 5; ++q) {
@@ -1743,8 +1744,8 @@ __global__ void __launch_bounds__(256, 1) tighten_cov_kernel(const TightenArgs a
       double c = 0.0;
 #pragma unroll
       for (int q = 0; q < 5; ++q) c = fma(__shfl_sync(0xffffffffu, js, i5 * 5 + q), Jj[q], c);
-      if (l == 18) c += cvs[2 * k];
-      if (l == 24) c += cvs[2 * k + 1];
+      c += cvk;  // diag(0,0,0,cv0,cv1) entry of this lane, loaded a step ahead
+      cvk = (l == 18 || l == 24) && k + 1 < a.T ? cvs[2 * (k + 1) + (l == 24)] : 0.0;
       Sr = 0.5 * (c + __shfl_sync(0xffffffffu, c, j5 * 5 + i5));
       if (l < 25) Ss[k * 25 + l] = Sr;
     }
