@@ -1538,8 +1538,21 @@ __global__ void __launch_bounds__(TMEAN_THREADS, 1) tighten_mean_kernel(const Ti
 #ifdef GPM_TMEAN_TRACE
   const long long tk2 = clock64();
 #endif
-  if (threadIdx.x == 0)  // heading recursion (arc_advance: theta = wrap(theta + omega dt))
-    for (int k = 0; k < T; ++k) th[k + 1] = wrap_angle_fast(th[k] + ww[k] * a.nom.dt);
+  if (threadIdx.x == 0) {  // heading recursion (arc_advance: theta = wrap(theta + omega dt))
+    double t = th[0];
+    for (int k0 = 0; k0 < T; k0 += 8) {  // omega read 8 steps ahead; wrap only off (-pi, pi]
+      double wv[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) wv[i] = k0 + i < T ? ww[k0 + i] : 0.0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (k0 + i < T) {
+          t = t + wv[i] * a.nom.dt;
+          if (!(t > -kPi && t <= kPi)) t = wrap_angle_fast(t);
+          th[k0 + i + 1] = t;
+        }
+    }
+  }
   __syncthreads();
   for (int k = threadIdx.x; k < T; k += blockDim.x) {  // arc increments + Jacobians, parallel in k
     const double m0[5] = {0.0, 0.0, th[k], vv[k], ww[k]};
