@@ -1567,18 +1567,30 @@ __global__ void __launch_bounds__(TMEAN_THREADS, 1) tighten_mean_kernel(const Ti
     for (int i = 0; i < 25; ++i) atJ[k * 25 + i] = J[i];
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  for (int k = threadIdx.x; k <= T; k += blockDim.x) {  // heading / speeds of every belief mean
+    atmu[k * 5 + 2] = th[k];
+    atmu[k * 5 + 3] = vv[k];
+    atmu[k * 5 + 4] = ww[k];
+  }
+  if (threadIdx.x == 0) {  // positions: prefix sum in step order, increments read 8 ahead
     double x = ax0[0], y = ax0[1];
-    for (int k = 0; k <= T; ++k) {
-      atmu[k * 5 + 0] = x;
-      atmu[k * 5 + 1] = y;
-      atmu[k * 5 + 2] = th[k];
-      atmu[k * 5 + 3] = vv[k];
-      atmu[k * 5 + 4] = ww[k];
-      if (k < T) {
-        x += dx[k];
-        y += dy[k];
+    atmu[0] = x;
+    atmu[1] = y;
+    for (int k0 = 0; k0 < T; k0 += 8) {
+      double ddx[8], ddy[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        ddx[i] = k0 + i < T ? dx[k0 + i] : 0.0;
+        ddy[i] = k0 + i < T ? dy[k0 + i] : 0.0;
       }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (k0 + i < T) {
+          x += ddx[i];
+          y += ddy[i];
+          atmu[(k0 + i + 1) * 5 + 0] = x;
+          atmu[(k0 + i + 1) * 5 + 1] = y;
+        }
     }
   }
 #ifdef GPM_TMEAN_TRACE
