@@ -1633,14 +1633,30 @@ __global__ void __launch_bounds__(256) tighten_var_kernel(const TightenArgs a) {
     const double* row = G.linv64 + (size_t)j * n;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     int i = lane;
-    for (; i + 96 <= j; i += 128) {  // four independent loads in flight per lane
-      const double r0 = __ldg(row + i), r1 = __ldg(row + i + 32), r2 = __ldg(row + i + 64), r3 = __ldg(row + i + 96);
-      a0 = fma(kst[i], r0, a0);
-      a1 = fma(kst[i + 32], r1, a1);
-      a2 = fma(kst[i + 64], r2, a2);
-      a3 = fma(kst[i + 96], r3, a3);
+    for (; i + 480 <= j; i += 512) {  // sixteen independent loads in flight per lane
+      double r[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) r[u] = __ldg(row + i + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 16; u += 4) {
+        a0 = fma(kst[i + 32 * u], r[u], a0);
+        a1 = fma(kst[i + 32 * (u + 1)], r[u + 1], a1);
+        a2 = fma(kst[i + 32 * (u + 2)], r[u + 2], a2);
+        a3 = fma(kst[i + 32 * (u + 3)], r[u + 3], a3);
+      }
     }
-    for (; i <= j; i += 32) a0 = fma(kst[i], __ldg(row + i), a0);
+    {  // the remaining < 16 column strides of the row, loads predicated, all in flight
+      double r[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) r[u] = i + 32 * u <= j ? __ldg(row + i + 32 * u) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 16; u += 4) {
+        if (i + 32 * u <= j) a0 = fma(kst[i + 32 * u], r[u], a0);
+        if (i + 32 * (u + 1) <= j) a1 = fma(kst[i + 32 * (u + 1)], r[u + 1], a1);
+        if (i + 32 * (u + 2) <= j) a2 = fma(kst[i + 32 * (u + 2)], r[u + 2], a2);
+        if (i + 32 * (u + 3) <= j) a3 = fma(kst[i + 32 * (u + 3)], r[u + 3], a3);
+      }
+    }
     const double aj = warp_sum((a0 + a1) + (a2 + a3));
     ssq = fma(aj, aj, ssq);
   }
