@@ -495,7 +495,7 @@ def solve_weights(buf: HistoryBuffer, prev, cfg: WeightSolverConfig) -> WeightSo
 def per_terrain_mean_prediction(model: G.GpModel, query, nominal: G.NominalParams):
     """Nominal next (v, ω) + each terrain's GP residual mean (terrain.cpp:234-257); the
     GP mean is evaluated by the device model."""
-    m2 = model.n_outputs()
+    m2 = model.n_outputs
     if m2 < 2 or m2 % 2:
         raise ValueError("per_terrain_mean_prediction: model must have 2M outputs")
     q = np.asarray(query, dtype=np.float64).reshape(4)
