@@ -11,6 +11,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <limits>
@@ -103,6 +104,15 @@ bool cholesky_lower(std::vector<double>& A, int n) {  // Eigen LLT: fail iff a p
   return true;
 }
 
+// Device factorisation (fit.cu) for n >= 1024, where the O(n^3) host loops take
+// seconds; GPMPPI_FIT=host|device overrides.
+bool device_fit(int n) {
+  const char* e = std::getenv("GPMPPI_FIT");
+  if (e && std::strcmp(e, "host") == 0) return false;
+  if (e && std::strcmp(e, "device") == 0) return true;
+  return n >= 1024;
+}
+
 void factor_group(HostGroup& G, const double* X, const double* Y, int n, int m,
                   std::vector<double>& lml) {
   const double sv = G.kernel[0], nv = G.kernel[5];
@@ -132,35 +142,52 @@ void factor_group(HostGroup& G, const double* X, const double* Y, int n, int m,
       const double s = 0.5 * (K[(size_t)i * n + j] + K[(size_t)j * n + i]);
       K[(size_t)i * n + j] = K[(size_t)j * n + i] = s;
     }
-  bool ok = false;  // gp.cpp:116-133 jitter ladder
-  double jitter = 0.0;
-  for (int attempt = 0; attempt <= 5 && !ok; ++attempt) {
-    jitter = attempt == 0 ? 0.0 : std::pow(10.0, -11 + attempt);
-    G.chol = K;
-    for (int i = 0; i < n; ++i) G.chol[(size_t)i * n + i] += nv + jitter;
-    ok = cholesky_lower(G.chol, n);
-  }
-  if (!ok) {
-    std::ostringstream msg;
-    msg << "GpModel::fit: Cholesky failed for kernel group after jitter up to 1e-6"
-        << " (signal_var=" << sv << ", noise_var=" << nv << ")";
-    runtime(msg.str());
-  }
-  G.jitter = jitter;
-  const std::vector<double>& L = G.chol;
-  // L^{-1} row by row (axpy form), then transpose (gp.cpp:135-138)
-  std::vector<double> Xi((size_t)n * n, 0.0);
-  for (int i = 0; i < n; ++i) {
-    double* xi = &Xi[(size_t)i * n];
-    xi[i] = 1.0;
-    for (int k = 0; k < i; ++k) {
-      const double l = L[(size_t)i * n + k];
-      const double* xk = &Xi[(size_t)k * n];
-      for (int c = 0; c <= k; ++c) xi[c] -= l * xk[c];
+  std::vector<double> Xi;  // L^{-1}, row-major lower
+  if (device_fit(n)) {  // gp.cpp:116-138 on the device (fit.cu)
+    bool ok = false;
+    double jitter = 0.0;
+    G.chol.assign((size_t)n * n, 0.0);
+    Xi.assign((size_t)n * n, 0.0);
+    CK(gpm::device_factor(K.data(), n, nv, G.chol.data(), Xi.data(), &jitter, &ok));
+    if (!ok) {
+      std::ostringstream msg;
+      msg << "GpModel::fit: Cholesky failed for kernel group after jitter up to 1e-6"
+          << " (signal_var=" << sv << ", noise_var=" << nv << ")";
+      runtime(msg.str());
     }
-    const double d = L[(size_t)i * n + i];
-    for (int c = 0; c <= i; ++c) xi[c] /= d;
+    G.jitter = jitter;
+  } else {
+    bool ok = false;  // gp.cpp:116-133 jitter ladder
+    double jitter = 0.0;
+    for (int attempt = 0; attempt <= 5 && !ok; ++attempt) {
+      jitter = attempt == 0 ? 0.0 : std::pow(10.0, -11 + attempt);
+      G.chol = K;
+      for (int i = 0; i < n; ++i) G.chol[(size_t)i * n + i] += nv + jitter;
+      ok = cholesky_lower(G.chol, n);
+    }
+    if (!ok) {
+      std::ostringstream msg;
+      msg << "GpModel::fit: Cholesky failed for kernel group after jitter up to 1e-6"
+          << " (signal_var=" << sv << ", noise_var=" << nv << ")";
+      runtime(msg.str());
+    }
+    G.jitter = jitter;
+    const std::vector<double>& Lh = G.chol;
+    // L^{-1} row by row (axpy form), then transpose (gp.cpp:135-138)
+    Xi.assign((size_t)n * n, 0.0);
+    for (int i = 0; i < n; ++i) {
+      double* xi = &Xi[(size_t)i * n];
+      xi[i] = 1.0;
+      for (int k = 0; k < i; ++k) {
+        const double l = Lh[(size_t)i * n + k];
+        const double* xk = &Xi[(size_t)k * n];
+        for (int c = 0; c <= k; ++c) xi[c] -= l * xk[c];
+      }
+      const double d = Lh[(size_t)i * n + i];
+      for (int c = 0; c <= i; ++c) xi[c] /= d;
+    }
   }
+  const std::vector<double>& L = G.chol;
   G.ilt.assign((size_t)n * n, 0.0);
   for (int i = 0; i < n; ++i)
     for (int j = i; j < n; ++j) G.ilt[(size_t)i * n + j] = Xi[(size_t)j * n + i];

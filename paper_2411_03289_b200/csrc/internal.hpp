@@ -205,6 +205,9 @@ void build_tc_operand(const double* ilt, int n, std::vector<float>& data, std::v
 void tc_profile_read(double* out);
 void tc_trace_read(double* out);  // 64 clock64 stamps of CTA 0 (GPMPPI_TC_DEBUG bit 4096)
 void count_launch(int n = 1);
+// fit.cu: device Cholesky (jitter ladder) + L^{-1} for GpModel::fit at large n.
+cudaError_t device_factor(const double* K, int n, double noise_var, double* L_out, double* X_out,
+                          double* jitter_out, bool* ok);
 unsigned long long launches_total();
 
 }  // namespace gpm
