@@ -11,4 +11,9 @@ from .gpmppi import (  # noqa: F401
 from ._capi import (  # noqa: F401
     NOISE_INJECTED, NOISE_PHILOX, VAR_FFMA, VAR_TC_1XTF32, VAR_TC_3XF16, VAR_TC_3XTF32, CudaError)
 
+from .harness import (  # noqa: F401
+    ExperimentConfig, HistoryBuffer, RunMetrics, Scenario, TerrainProfile, WeightSolverConfig,
+    make_scenario, per_terrain_mean_prediction, project_simplex, run_avoidance,
+    run_avoidance_experiment, run_tracking, run_tracking_experiment, solve_weights, train_models)
+
 __version__ = "0.1.0"

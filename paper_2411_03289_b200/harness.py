@@ -794,3 +794,36 @@ def run_avoidance_experiment(cfg: ExperimentConfig, scenario: Scenario, models: 
     met.mean_speed = lp.path_len / lp.t if lp.t > 0.0 else 0.0
     met.latency = summarize_latency(lp.latencies)
     return met
+
+
+# ----------------------------------------------------------------- Python entry points
+def _metrics_to_dict(m: RunMetrics) -> dict:  # module.cpp:22-36
+    return {"rmse": m.rmse, "success": m.success, "time_to_goal": m.time_to_goal,
+            "min_obstacle_clearance": m.min_obstacle_clearance, "mean_speed": m.mean_speed,
+            "collision_count": m.collision_count, "ticks": m.ticks, "aborted": m.aborted,
+            "abort_reason": m.abort_reason, "latency_median_ms": m.latency.median_ms}
+
+
+def _run(kind: str, config_path: str, seed: int, planner: str, **scenario):
+    if config_path:
+        raise ValueError("run_%s: JSON config files are not supported by this build; pass "
+                         "config_path='' for the default configuration" % kind)
+    cfg = ExperimentConfig(seed=seed)
+    if planner:
+        if planner not in ("gp", "edd5", "unicycle"):
+            raise ValueError(f"unknown planner {planner!r}")
+        cfg.planner = planner
+    models = G.TrainedModels() if cfg.planner == "unicycle" else train_models(cfg, seed)
+    sc = make_scenario(kind, seed=seed, **scenario)
+    run = run_tracking_experiment if kind == "tracking" else run_avoidance_experiment
+    return _metrics_to_dict(run(cfg, sc, models, seed))
+
+
+def run_tracking(config_path: str = "", seed: int = 0, planner: str = "", **scenario) -> dict:
+    """module.cpp:183-196: default config, train, closed-loop tracking, metrics dict."""
+    return _run("tracking", config_path, seed, planner, **scenario)
+
+
+def run_avoidance(config_path: str = "", seed: int = 0, planner: str = "", **scenario) -> dict:
+    """module.cpp:197-210: default config, train, closed-loop avoidance, metrics dict."""
+    return _run("avoidance", config_path, seed, planner, **scenario)

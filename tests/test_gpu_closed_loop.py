@@ -67,3 +67,13 @@ def test_kind_mismatch_raises(trained):
         H.run_tracking_experiment(cfg, H.make_scenario("avoidance"), models, 0)
     with pytest.raises(ValueError):
         H.run_avoidance_experiment(cfg, H.make_scenario("tracking"), models, 0)
+
+
+def test_python_entry_points_match_reference_bindings():  # module.cpp:183-210, test_smoke.py
+    m = H.run_tracking(seed=1, planner="unicycle", distance_budget=5.0)
+    assert set(m) >= {"rmse", "success", "ticks", "latency_median_ms", "abort_reason"}
+    assert m["success"] and not m["aborted"]
+    a = H.run_avoidance(seed=2, planner="gp", max_duration=20.0)
+    assert a["ticks"] > 0 and not a["aborted"]
+    with pytest.raises(ValueError):
+        H.run_tracking(config_path="cfg.json")
