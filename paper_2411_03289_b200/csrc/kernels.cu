@@ -1754,41 +1754,60 @@ __global__ void __launch_bounds__(256, 1) tighten_cov_kernel(const TightenArgs a
 #ifdef GPM_TCOV_TRACE
   ct[1] = clock64();
 #endif
-  if (l < 32) {  // warp 0: the serial recursion
-    // lane l < 25 owns Σ[i5][j5] in a register; the two 5-term products per step pull
-    // their operands with shuffles (no shared-memory round trips on the serial chain)
-    const int i5 = l < 25 ? l / 5 : 4, j5 = l < 25 ? l % 5 : 4;
-    double Sr = 0.0;
-    double cvk = (l == 18 || l == 24) ? cvs[l == 24] : 0.0;
-    double Jin[5], Jjn[5];  // step k's J rows, loaded one step ahead (off the serial chain)
-#pragma unroll
-    for (int q = 0; q < 5; ++q) {
-      Jin[q] = Js[i5 * 5 + q];
-      Jjn[q] = Js[j5 * 5 + q];
-    }
-    for (int k = 0; k < a.T; ++k) {  // Σ' = J Σ Jᵀ + diag(0,0,0,cv0,cv1), symmetrised (uncertainty.cpp:83-87)
-      double Ji[5], Jj[5];
-#pragma unroll
-      for (int q = 0; q < 5; ++q) {
-        Ji[q] = Jin[q];
-        Jj[q] = Jjn[q];
+  if (l == 0) {
+    // The serial recursion Σ' = J Σ Jᵀ + diag(0,0,0,cv0,cv1) (uncertainty.cpp:83-87) in one
+    // thread's registers. jacobian_nominal (dynamics.cpp:68-98) is structurally sparse:
+    //   J = [1 0 a b c; 0 1 d e f; 0 0 1 0 g; 0 0 0 h 0; 0 0 0 0 i],
+    // so one step is P = JΣ (3-FMA rows) then the 15 upper entries of PJᵀ: a 6-FMA-deep
+    // chain with no shuffles. Σ stays exactly symmetric, so the reference's
+    // symmetrisation is the identity here. J and cv of step k+1 load during step k.
+    double s00 = 0, s01 = 0, s02 = 0, s03 = 0, s04 = 0, s11 = 0, s12 = 0, s13 = 0, s14 = 0;
+    double s22 = 0, s23 = 0, s24 = 0, s33 = 0, s34 = 0, s44 = 0;
+    double na = Js[2], nb = Js[3], nc = Js[4], nd = Js[7], ne = Js[8], nf = Js[9];
+    double ng = Js[14], nh = Js[18], ni = Js[24], ncv0 = cvs[0], ncv1 = cvs[1];
+    for (int k = 0; k < T; ++k) {
+      const double ja = na, jb = nb, jc = nc, jd = nd, je = ne, jf = nf, jg = ng, jh = nh, ji = ni;
+      const double cv0 = ncv0, cv1 = ncv1;
+      if (k + 1 < T) {
+        const double* Jn = Js + 25 * (k + 1);
+        na = Jn[2], nb = Jn[3], nc = Jn[4], nd = Jn[7], ne = Jn[8], nf = Jn[9];
+        ng = Jn[14], nh = Jn[18], ni = Jn[24];
+        ncv0 = cvs[2 * k + 2], ncv1 = cvs[2 * k + 3];
       }
-      const double* Jn = Js + 25 * (k + 1 < a.T ? k + 1 : k);
-#pragma unroll
-      for (int q = 0; q < 5; ++q) {
-        Jin[q] = Jn[i5 * 5 + q];
-        Jjn[q] = Jn[j5 * 5 + q];
-      }
-      double js = 0.0;
-#pragma unroll
-      for (int q = 0; q < 5; ++q) js = fma(Ji[q], __shfl_sync(0xffffffffu, Sr, q * 5 + j5), js);
-      double c = 0.0;
-#pragma unroll
-      for (int q = 0; q < 5; ++q) c = fma(__shfl_sync(0xffffffffu, js, i5 * 5 + q), Jj[q], c);
-      c += cvk;  // diag(0,0,0,cv0,cv1) entry of this lane, loaded a step ahead
-      cvk = (l == 18 || l == 24) && k + 1 < a.T ? cvs[2 * (k + 1) + (l == 24)] : 0.0;
-      Sr = 0.5 * (c + __shfl_sync(0xffffffffu, c, j5 * 5 + i5));
-      if (l < 25) Ss[k * 25 + l] = Sr;
+      // P = J Σ (rows 0..4; only the entries P Jᵀ's upper triangle reads)
+      const double p00 = fma(jc, s04, fma(jb, s03, fma(ja, s02, s00)));
+      const double p01 = fma(jc, s14, fma(jb, s13, fma(ja, s12, s01)));
+      const double p02 = fma(jc, s24, fma(jb, s23, fma(ja, s22, s02)));
+      const double p03 = fma(jc, s34, fma(jb, s33, fma(ja, s23, s03)));
+      const double p04 = fma(jc, s44, fma(jb, s34, fma(ja, s24, s04)));
+      const double p11 = fma(jf, s14, fma(je, s13, fma(jd, s12, s11)));
+      const double p12 = fma(jf, s24, fma(je, s23, fma(jd, s22, s12)));
+      const double p13 = fma(jf, s34, fma(je, s33, fma(jd, s23, s13)));
+      const double p14 = fma(jf, s44, fma(je, s34, fma(jd, s24, s14)));
+      const double p22 = fma(jg, s24, s22), p23 = fma(jg, s34, s23), p24 = fma(jg, s44, s24);
+      const double p33 = jh * s33, p34 = jh * s34, p44 = ji * s44;
+      // Σ' = P Jᵀ (+ the correction variances on the (3,3), (4,4) diagonal)
+      s00 = fma(jc, p04, fma(jb, p03, fma(ja, p02, p00)));
+      s01 = fma(jf, p04, fma(je, p03, fma(jd, p02, p01)));
+      s02 = fma(jg, p04, p02);
+      s03 = jh * p03;
+      s04 = ji * p04;
+      s11 = fma(jf, p14, fma(je, p13, fma(jd, p12, p11)));
+      s12 = fma(jg, p14, p12);
+      s13 = jh * p13;
+      s14 = ji * p14;
+      s22 = fma(jg, p24, p22);
+      s23 = jh * p23;
+      s24 = ji * p24;
+      s33 = fma(jh, p33, cv0);
+      s34 = ji * p34;
+      s44 = fma(ji, p44, cv1);
+      double* Sk = Ss + 25 * k;
+      Sk[0] = s00, Sk[1] = s01, Sk[2] = s02, Sk[3] = s03, Sk[4] = s04;
+      Sk[5] = s01, Sk[6] = s11, Sk[7] = s12, Sk[8] = s13, Sk[9] = s14;
+      Sk[10] = s02, Sk[11] = s12, Sk[12] = s22, Sk[13] = s23, Sk[14] = s24;
+      Sk[15] = s03, Sk[16] = s13, Sk[17] = s23, Sk[18] = s33, Sk[19] = s34;
+      Sk[20] = s04, Sk[21] = s14, Sk[22] = s24, Sk[23] = s34, Sk[24] = s44;
     }
   }
   __syncthreads();
