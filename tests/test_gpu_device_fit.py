@@ -69,3 +69,17 @@ def test_default_fit_at_config3_size_is_device_and_fast():
     mean, var = m.predict_batch(X[:4])
     assert np.isfinite(mean).all() and (var >= 0).all()
     assert 0.0 <= m.group_jitter(0) <= 1e-6
+
+
+def test_device_fit_matches_oracle_at_config3_size():
+    """The default (device) fit at n = 2048 predicts like the FP64 oracle's host fit."""
+    from oracle import oracle as O
+    X, Y, K = W.gp_training_set(2048, 3, seed=5)
+    gd, go = G.GpModel.fit(X, Y, K), O.GP(X, Y, K)
+    q = np.random.default_rng(2).uniform([-0.5, -2, -0.5, -2], [2, 2, 2, 2], size=(128, 4))
+    md, vd = gd.predict_batch(q)
+    mo, vo = go.predict_batch(q)
+    np.testing.assert_allclose(md, mo, rtol=1e-8, atol=1e-11)
+    np.testing.assert_allclose(vd, vo, rtol=0, atol=1e-10)
+    for o in range(Y.shape[1]):
+        assert gd.log_marginal_likelihood(o) == pytest.approx(go.lml(o), rel=1e-9)
