@@ -256,6 +256,27 @@ int gpmppi_planner_plan_partial(gpmppi_planner* p, const double x0[5], const gpm
                                 void* device_tuple_out);
 int gpmppi_planner_plan_finish(gpmppi_planner* p, const void* device_tuples, int n_ranks,
                                double command[2], gpmppi_diag* diag);
+/* In-library NCCL exchange (replaces the reference's single exchange point, the
+ * softmax reduction of mppi.cpp:428-429, for a solve sharded over GPUs):
+ * gpmppi_nccl_unique_id fills a 128-byte ncclUniqueId on one rank (the caller
+ * broadcasts it); every rank then calls gpmppi_planner_attach_comm (collective), which
+ * takes the rank's contiguous global sample range of cfg.samples. From then on
+ * gpmppi_planner_plan_step runs the sharded tick on the planner stream: rollout ->
+ * variance -> reduce -> ncclAllGather of the (2T+6)-double tuples -> rank-order combine
+ * + update + shift (identical on every rank) -> command -> tightening. No host sync
+ * inside the tick; it is captured in the tick's CUDA graph like the single-GPU tick. */
+int gpmppi_nccl_unique_id(void* out128);
+int gpmppi_planner_attach_comm(gpmppi_planner* p, const void* unique_id, int n_ranks, int rank);
+int gpmppi_planner_shard(const gpmppi_planner* p, int64_t* begin, int64_t* count, int* n_ranks,
+                         int* rank);
+/* Command-first mode (default off = reference semantics): plan_step returns as soon as the
+ * command and the sample diagnostics are on the host; the tightening pass, which only the
+ * next tick consumes (mppi.cpp:235-248), completes behind the return. Its outputs are
+ * waited for by the next plan_step, by every accessor, and by wait_tightening, which also
+ * completes that tick's diag (tightening_infeasible; plan_ms = launch latency + device
+ * span of the whole tick). diag.command_ms is the time to command in both modes. */
+int gpmppi_planner_set_command_first(gpmppi_planner* p, int on);
+int gpmppi_planner_wait_tightening(gpmppi_planner* p, gpmppi_diag* diag);
 /* Host restatement of the tuple combine the device runs (for CPU multi-rank tests):
  * tuples n_ranks×gpmppi_tuple_doubles(T) → combined tuple. */
 int gpmppi_combine_tuples_host(const double* tuples, int n_ranks, int horizon, double lambda,

@@ -13,6 +13,7 @@
 #include "gpmppi_oracle.h"
 
 #include <math.h>
+#include <dlfcn.h>
 #include <pthread.h>
 #include <stdarg.h>
 #include <stdio.h>
@@ -434,6 +435,88 @@ void orc_gp_group_export(const orc_gp* g, int grp, double* ilt, double* chol, do
   if (kernel6) memcpy(kernel6, G->kernel, sizeof(double) * 6);
 }
 
+/* Optional BLAS for the timed CPU baseline (bench.py's reference arm only; the parity
+ * checker keeps the scalar loops below). The reference evaluates the kernel row, the
+ * mean and the variance with Eigen GEMM / GEMM / TRMM (gp.cpp:178, 182, 185); an
+ * optimised BLAS (OpenBLAS, loaded with dlopen) stands in for Eigen's kernels, which
+ * cannot be built here (no Eigen in the image). Single-threaded BLAS inside each of the
+ * reference's per-chunk worker threads, as Eigen runs there. */
+typedef void (*orc_dgemm_fn)(int, int, int, int, int, int, double, const double*, int,
+                             const double*, int, double, double*, int);
+typedef void (*orc_dtrmm_fn)(int, int, int, int, int, int, int, double, const double*, int,
+                             double*, int);
+static orc_dgemm_fn g_dgemm = NULL;
+static orc_dtrmm_fn g_dtrmm = NULL;
+enum { CB_ROW = 101, CB_NOTRANS = 111, CB_TRANS = 112, CB_UPPER = 121, CB_NONUNIT = 131,
+       CB_RIGHT = 142 };
+
+int orc_use_blas(const char* so_path, const char* prefix) {
+  if (!so_path) {
+    g_dgemm = NULL;
+    g_dtrmm = NULL;
+    return 0;
+  }
+  void* h = dlopen(so_path, RTLD_NOW | RTLD_LOCAL);
+  if (!h) return -1;
+  char name[128];
+  snprintf(name, sizeof name, "%scblas_dgemm", prefix ? prefix : "");
+  orc_dgemm_fn gm = (orc_dgemm_fn)dlsym(h, name);
+  snprintf(name, sizeof name, "%scblas_dtrmm", prefix ? prefix : "");
+  orc_dtrmm_fn tm = (orc_dtrmm_fn)dlsym(h, name);
+  snprintf(name, sizeof name, "%sopenblas_set_num_threads", prefix ? prefix : "");
+  void (*nt)(int) = (void (*)(int))dlsym(h, name);
+  if (!gm || !tm) return -2;
+  if (nt) nt(1);
+  g_dgemm = gm;
+  g_dtrmm = tm;
+  return 0;
+}
+
+/* gp.cpp:152-198 with the BLAS stand-in for Eigen: K* = exp(Q_aug · aug^T) (GEMM),
+ * mean = K* · alphas (GEMM), a = K* · L^{-T} (TRMM), var = max(sv - |a|^2, 0). */
+static void predict_block_blas(const orc_gp* g, const double* q, int S, double* mean,
+                               double* var, double* ws) {
+  const int n = g->n, m = g->m;
+  double* kstar = ws;
+  double* a = ws + (size_t)S * n;
+  double qa[6 * 128];
+  double mo[8 * 128];
+  for (int gi = 0; gi < g->n_groups; ++gi) {
+    const orc_group* G = &g->groups[gi];
+    for (int s0 = 0; s0 < S; s0 += 128) {
+      const int cs = (S - s0) < 128 ? (S - s0) : 128;
+      for (int s = 0; s < cs; ++s) {
+        double sq = 0.0;
+        for (int d = 0; d < 4; ++d) {
+          qa[s * 6 + d] = q[(size_t)(s0 + s) * 4 + d] / G->kernel[1 + d];
+          sq += qa[s * 6 + d] * qa[s * 6 + d];
+        }
+        qa[s * 6 + 4] = -0.5 * sq;
+        qa[s * 6 + 5] = 1.0;
+      }
+      double* kr = kstar + (size_t)s0 * n;
+      g_dgemm(CB_ROW, CB_NOTRANS, CB_TRANS, cs, n, 6, 1.0, qa, 6, G->inputs_aug, 6, 0.0, kr, n);
+      for (size_t i = 0; i < (size_t)cs * n; ++i) kr[i] = exp(kr[i]);
+      for (int c0 = 0; c0 < G->n_out; c0 += 8) {
+        const int nc = (G->n_out - c0) < 8 ? (G->n_out - c0) : 8;
+        g_dgemm(CB_ROW, CB_NOTRANS, CB_NOTRANS, cs, nc, n, 1.0, kr, n, G->alphas + c0, G->n_out, 0.0,
+                mo, nc);
+        for (int s = 0; s < cs; ++s)
+          for (int c = 0; c < nc; ++c) mean[(size_t)(s0 + s) * m + G->outputs[c0 + c]] = mo[s * nc + c];
+      }
+    }
+    memcpy(a, kstar, sizeof(double) * (size_t)S * n);
+    g_dtrmm(CB_ROW, CB_RIGHT, CB_UPPER, CB_NOTRANS, CB_NONUNIT, S, n, 1.0, G->inv_lower_t, n, a, n);
+    for (int s = 0; s < S; ++s) {
+      double v = G->kernel[0];
+      const double* ar = a + (size_t)s * n;
+      for (int j = 0; j < n; ++j) v -= ar[j] * ar[j];
+      v = v > 0.0 ? v : 0.0;
+      for (int c = 0; c < G->n_out; ++c) var[(size_t)s * m + G->outputs[c]] = v;
+    }
+  }
+}
+
 /* gp.cpp:152-198 for S queries (row-major S×4) into mean/var (S×m).
  * ws must hold S*n*2 doubles. The TRMM is blocked 8 rows of L^{-T} at a time so
  * the inner loop streams contiguous rows (vectorisable at -O3). */
@@ -442,6 +525,10 @@ static void predict_block(const orc_gp* g, const double* q, int S, double* mean,
   const int n = g->n, m = g->m;
   double* kstar = ws;
   double* a = ws + (size_t)S * n;
+  if (g_dgemm && g_dtrmm) {
+    predict_block_blas(g, q, S, mean, var, ws);
+    return;
+  }
   for (int gi = 0; gi < g->n_groups; ++gi) {
     const orc_group* G = &g->groups[gi];
     const double* aug = G->inputs_aug;

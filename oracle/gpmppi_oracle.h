@@ -200,6 +200,9 @@ void orc_planner_set_nominal_sequence(orc_planner* p, const double* seq);
 void orc_planner_set_thresholds(orc_planner* p, const double* r_bar, const double* margins,
                                 int O);
 int orc_rollout_threads_used(const orc_planner* p);
+/* Timed CPU baseline only: route gp.cpp's GEMM / GEMM / TRMM through a dlopen'd CBLAS
+ * (symbol prefix e.g. "scipy_"); NULL path restores the scalar checker loops. */
+int orc_use_blas(const char* so_path, const char* prefix);
 
 #ifdef __cplusplus
 }

@@ -102,15 +102,46 @@ class Diag(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+def blas_library():
+    """(path, symbol prefix) of the optimised CBLAS bundled with scipy (OpenBLAS), or None."""
+    try:
+        import glob
+
+        import scipy
+        libs = sorted(glob.glob(os.path.join(os.path.dirname(scipy.__file__), "..", "scipy.libs",
+                                             "libscipy_openblas-*.so")))
+        return (os.path.realpath(libs[0]), "scipy_") if libs else None
+    except Exception:
+        return None
+
+
+def use_blas(on: bool = True, native: bool = None) -> str:
+    """Timed CPU baseline only: OpenBLAS GEMM/TRMM in place of Eigen's (gp.cpp:178-185).
+    Returns a description of what is in use."""
+    L = lib(native)
+    if not on:
+        L.orc_use_blas(None, None)
+        return "scalar loops"
+    b = blas_library()
+    if b is None or L.orc_use_blas(b[0].encode(), b[1].encode()) != 0:
+        L.orc_use_blas(None, None)
+        return "scalar loops (OpenBLAS not found)"
+    return "OpenBLAS " + os.path.basename(b[0])
+
+
 def build(native: bool = False) -> str:
     target = "liboracle_native.so" if native else "liboracle.so"
     subprocess.run(["make", "-s", "-C", _HERE, "native" if native else "all"], check=True)
     return os.path.join(_HERE, target)
 
 
-def lib(native: bool = False):
+def lib(native: bool = None):
+    """The oracle library. native=None follows GPMPPI_ORACLE_NATIVE=1 (the bench's timed
+    CPU arm builds and loads a -march=native copy on the host that runs it)."""
     global _LIB
-    if _LIB is not None and not native:
+    if native is None:
+        native = os.environ.get("GPMPPI_ORACLE_NATIVE") == "1"
+    if _LIB is not None:
         return _LIB
     path = os.path.join(_HERE, "liboracle_native.so" if native else "liboracle.so")
     src = os.path.join(_HERE, "gpmppi_oracle.c")
@@ -129,6 +160,7 @@ def lib(native: bool = False):
     for f in ("orc_wrap_angle", "orc_chi2_quantile_2dof", "orc_normal_cdf", "orc_normal_quantile"):
         getattr(L, f).restype = C.c_double
         getattr(L, f).argtypes = [C.c_double]
+    L.orc_use_blas.argtypes = [C.c_char_p, C.c_char_p]
     L.orc_kernel_eval.restype = C.c_double
     L.orc_kernel_eval.argtypes = [_dp, _dp, _dp]
     L.orc_gp_fit.argtypes = [_dp, _dp, C.c_int, C.c_int, _dp, C.POINTER(C.c_void_p)]
@@ -191,8 +223,7 @@ def lib(native: bool = False):
     L.orc_planner_set_nominal_sequence.argtypes = [C.c_void_p, _dp]
     L.orc_planner_set_thresholds.argtypes = [C.c_void_p, _dp, _dp, C.c_int]
     L.orc_rollout_threads_used.argtypes = [C.c_void_p]
-    if not native:
-        _LIB = L
+    _LIB = L
     return L
 
 
@@ -328,7 +359,7 @@ class Planner:
     def __init__(self, samples, horizon, model_kind=ORC_MODEL_GP, gp=None, n_terrains=0,
                  lam=0.1, sigma_sim=(0.09, 0.25), lo=(-0.5, -2.0), hi=(2.0, 2.0), seed=0,
                  threads=0, nominal=(0.5, 0.35, 0.05), p_x=0.95, edd5=None, track_width=0.4,
-                 native=False):
+                 native=None):
         self.L = lib(native)
         self.cfg = MppiConfig(samples, horizon, lam, sigma_sim[0], sigma_sim[1],
                               (C.c_double * 2)(*lo), (C.c_double * 2)(*hi), seed, threads)

@@ -138,6 +138,12 @@ SIGNATURES = [
     ("gpmppi_planner_set_shard", C.c_int, [_vp, C.c_int64, C.c_int64]),
     ("gpmppi_planner_plan_partial", C.c_int, [_vp, _dp, C.POINTER(TaskC), _vp]),
     ("gpmppi_planner_plan_finish", C.c_int, [_vp, _vp, C.c_int, _dp, C.POINTER(DiagC)]),
+    ("gpmppi_nccl_unique_id", C.c_int, [_vp]),
+    ("gpmppi_planner_attach_comm", C.c_int, [_vp, _vp, C.c_int, C.c_int]),
+    ("gpmppi_planner_shard", C.c_int, [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                       C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    ("gpmppi_planner_set_command_first", C.c_int, [_vp, C.c_int]),
+    ("gpmppi_planner_wait_tightening", C.c_int, [_vp, C.POINTER(DiagC)]),
     ("gpmppi_combine_tuples_host", C.c_int, [_dp, C.c_int, C.c_int, C.c_double, _dp]),
     ("gpmppi_rollout", C.c_int, [C.POINTER(PredictionModelC), C.POINTER(NominalC), _dp, C.c_int, _dp, _dp,
                                  C.c_int, C.c_int, _dp, _dp]),

@@ -46,18 +46,20 @@ def build(force: bool = False, verbose: bool = False, variant: str = "", defines
     common = [nvcc(), "-O3", "-std=c++17", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC,-O3",
               "-I", os.path.join(ROOT, "include"), "-I", CSRC, "--expt-relaxed-constexpr",
               *[f"-D{d}" for d in defines]]
-    objs = []
-    for s in SOURCES:
+    objs, procs = [], []
+    for s in SOURCES:  # the translation units compile in parallel
         obj = os.path.join(objdir, os.path.splitext(s)[0] + ".o")
         cmd = common + ["-x", "cu", "-c", os.path.join(CSRC, s), "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            raise RuntimeError(f"nvcc failed for {s}:\n{r.stdout}\n{r.stderr}")
-        if verbose:
-            print(r.stderr)
+        procs.append((s, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
         objs.append(obj)
+    for s, pr in procs:
+        sout, err = pr.communicate()
+        if pr.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {s}:\n{sout}\n{err}")
+        if verbose:
+            print(err)
     tmp = out + ".tmp"
     cmd = [nvcc(), "-shared", *ARCH, "-o", tmp, *objs, "-cudart", "static", "-lpthread", "-ldl", "-lrt"]
     r = subprocess.run(cmd, capture_output=True, text=True)

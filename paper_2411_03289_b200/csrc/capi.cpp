@@ -6,6 +6,8 @@
 #include "gpmppi_b200.h"
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -41,6 +43,10 @@ struct CudaError {
     if (e__ != cudaSuccess) throw CudaError{e__, #call};                  \
   } while (0)
 
+struct NcclError {
+  std::string msg;
+};
+
 struct ArgError {
   int code;
   std::string msg;
@@ -58,6 +64,8 @@ int guarded(F&& f) {
   } catch (const CudaError& e) {
     return fail(GPMPPI_CUDA_ERROR, std::string("CUDA error in ") + e.where + ": " +
                                        cudaGetErrorString(e.e));
+  } catch (const NcclError& e) {
+    return fail(GPMPPI_RUNTIME_ERROR, e.msg);
   } catch (const std::bad_alloc&) {
     return fail(GPMPPI_RUNTIME_ERROR, "host allocation failed");
   }
@@ -70,6 +78,51 @@ void require_device(int device) {
     throw CudaError{e == cudaSuccess ? cudaErrorNoDevice : e, "cudaGetDeviceCount (no CUDA device)"};
   if (device < 0 || device >= count) invalid("device index out of range");
   CK(cudaSetDevice(device));
+}
+
+// ---------------------------------------------------------------------------
+// NCCL, resolved at run time from the libnccl.so.2 the process already has (torch's) or
+// the system one: the sharded solve's one collective (mppi.cpp:428-429 is the reference's
+// only exchange point) runs on the planner stream inside the library.
+struct NcclApi {
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+  std::string why;
+};
+const NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      a.why = std::string("cannot load libnccl.so.2: ") + dlerror();
+      return a;
+    }
+    a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(h, "ncclAllGather"));
+    a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+    if (!a.get_unique_id || !a.comm_init_rank || !a.all_gather || !a.comm_destroy) a.why = "libnccl lacks a symbol";
+    return a;
+  }();
+  return api;
+}
+void nccl_check(ncclResult_t r, const char* where) {
+  if (r != ncclSuccess) {
+    const NcclApi& a = nccl_api();
+    throw NcclError{std::string("NCCL error in ") + where + ": " +
+                    (a.error_string ? a.error_string(r) : std::to_string((int)r))};
+  }
+}
+const NcclApi& nccl_required() {
+  const NcclApi& a = nccl_api();
+  if (!a.why.empty()) throw NcclError{a.why};
+  return a;
 }
 
 // ---------------------------------------------------------------------------
@@ -571,7 +624,7 @@ struct gpmppi_planner {
   int n_obs_max = 0;
   int reduce_blocks = 1;  // per robot
   int T = 0, words = 1;
-  signed char coef_terrain[gpm::kMaxGroups][8];
+  signed char coef_terrain[gpm::kMaxGroups][gpm::kMaxOutPerGroup];
   // device buffers (robot-major, strides in gpm::BatchStrides)
   std::vector<void*> allocs;
   double *d_nom = nullptr, *d_tw = nullptr, *d_x0 = nullptr, *d_rbar = nullptr, *d_margins = nullptr;
@@ -601,19 +654,41 @@ struct gpmppi_planner {
   long long graph_key = -1;
   int graph_launches = 0;
   bool use_graph = getenv("GPMPPI_NO_GRAPH") == nullptr;
+  // sharded solve over NCCL (gpmppi_planner_attach_comm): this rank rolls out its global
+  // sample range, the (2T+6)-double tuples are all-gathered on `stream`, every rank combines
+  ncclComm_t comm = nullptr;
+  int n_ranks = 1, rank = 0;
+  double* d_gathered = nullptr;  // [n_ranks][W]
+  // command-first mode: plan_step returns once the command is on the host; the tightening
+  // pass (consumed only by the next tick, mppi.cpp:235-248) completes behind it
+  bool command_first = false;
+  bool tightening_pending = false;
+  double pending_cmd_ms = 0.0;
+  std::chrono::steady_clock::time_point pending_t0;
+  std::vector<gpmppi_diag> pending_diag;  // [B], completed by wait_tightening
 
+  std::vector<void*> sample_allocs;  // per-sample buffers, reallocated by set_shard
   template <class T>
-  T* dalloc(size_t count) {
+  T* dalloc(size_t count, std::vector<void*>* owner = nullptr) {
     void* p = nullptr;
     CK(cudaMalloc(&p, sizeof(T) * std::max<size_t>(count, 1)));
-    allocs.push_back(p);
+    (owner ? owner : &allocs)->push_back(p);
     CK(cudaMemsetAsync(p, 0, sizeof(T) * std::max<size_t>(count, 1), stream));
     return static_cast<T*>(p);
+  }
+  // drop the captured tick: its kernel arguments name buffers and shard bounds
+  void invalidate_graph() {
+    if (tick_exec) cudaGraphExecDestroy(tick_exec);
+    if (tick_graph) cudaGraphDestroy(tick_graph);
+    tick_exec = nullptr;
+    tick_graph = nullptr;
+    graph_key = -1;
   }
   ~gpmppi_planner() {
     cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
     for (void* p : allocs) cudaFree(p);
+    for (void* p : sample_allocs) cudaFree(p);
     if (h_task) cudaFreeHost(h_task);
     if (h_x0) cudaFreeHost(h_x0);
     if (h_out) cudaFreeHost(h_out);
@@ -624,32 +699,52 @@ struct gpmppi_planner {
     if (tick_graph) cudaGraphDestroy(tick_graph);
     if (fork_ev) cudaEventDestroy(fork_ev);
     if (join_ev) cudaEventDestroy(join_ev);
+    if (comm && nccl_api().comm_destroy) nccl_api().comm_destroy(comm);
     if (side) cudaStreamDestroy(side);
     if (stream) cudaStreamDestroy(stream);
   }
   long long slots() const { return (long long)B * K_local; }
   int groups() const { return model ? model->dev.G : 0; }
+  // (Re)allocate every buffer sized by the local sample count; the previous set (if any)
+  // is freed and the captured tick graph dropped (set_shard changes the count).
   void alloc_sample_buffers() {
+    CK(cudaStreamSynchronize(stream));
+    invalidate_graph();
+    for (void* q : sample_allocs) CK(cudaFree(q));
+    sample_allocs.clear();
+    d_eps = nullptr;
+    injected_set = false;
+    d_queries = nullptr;
+    d_var = nullptr;
+    std::vector<void*>* o = &sample_allocs;
     const long long S = slots();
-    d_cost_mean = dalloc<double>(S);
-    d_costs = dalloc<double>(S);
-    d_e = dalloc<double>(S);
-    d_viol = dalloc<uint32_t>((size_t)S * words);
-    d_coll = dalloc<uint32_t>((size_t)S * words);
-    d_term = dalloc<uint8_t>(S);
-    d_alive = dalloc<uint8_t>(S);
-    d_noise = dalloc<double>((size_t)S * T * 2);
+    d_cost_mean = dalloc<double>(S, o);
+    d_costs = dalloc<double>(S, o);
+    d_e = dalloc<double>(S, o);
+    d_viol = dalloc<uint32_t>((size_t)S * words, o);
+    d_coll = dalloc<uint32_t>((size_t)S * words, o);
+    d_term = dalloc<uint8_t>(S, o);
+    d_alive = dalloc<uint8_t>(S, o);
+    d_noise = dalloc<double>((size_t)S * T * 2, o);
     if (model_kind == GPMPPI_MODEL_GP_ENSEMBLE) {
-      d_queries = dalloc<float4>((size_t)S * T);
-      d_var = dalloc<double>((size_t)groups() * S * T);
+      d_queries = dalloc<float4>((size_t)S * T, o);
+      d_var = dalloc<double>((size_t)groups() * S * T, o);
       if (!d_scratch) d_scratch = dalloc<double>(gpm::rollout_scratch_doubles(T, num_sms));
     }
     reduce_blocks = gpm::reduce_blocks_for((int)K_local, B, num_sms, T);
-    d_partials = dalloc<double>((size_t)B * reduce_blocks * gpm::tuple_doubles(T));
+    d_partials = dalloc<double>((size_t)B * reduce_blocks * gpm::tuple_doubles(T), o);
   }
 };
 
 namespace {
+
+// Host -> device update of planner state on the planner's own (non-blocking) stream, so it
+// is ordered after every kernel already enqueued there; returns once the copy has landed
+// (the source may be pageable and is reused by the caller).
+void h2d_sync(gpmppi_planner* p, void* dst, const void* src, size_t bytes) {
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+}
 
 double normal_quantile(double p) {  // uncertainty.cpp:19-60 (Acklam + one Newton step)
   static const double a[] = {-3.969683028665376e+01, 2.209460984245205e+02, -2.759285104469687e+02,
@@ -762,6 +857,8 @@ double task_var_weight(const gpmppi_task* t) {
   return t->kind == GPMPPI_TASK_AVOIDANCE ? t->avoidance.variance : t->tracking.variance;
 }
 
+void finish_pending(gpmppi_planner* p, gpmppi_diag* diag);
+
 // mppi.cpp:235-248 ensure_thresholds + the per-tick staging of every robot's state,
 // task, variance weight and Philox key into pinned memory (enqueue_h2d copies them).
 void stage_tick(gpmppi_planner* p, const double* x0, const gpmppi_task* tasks) {
@@ -782,8 +879,7 @@ void stage_tick(gpmppi_planner* p, const double* x0, const gpmppi_task* tasks) {
         synced = true;
       }
       std::vector<double> r(T, task->track->half_width);
-      CK(cudaMemcpy(p->d_rbar + (size_t)b * gpm::BatchStrides::rbar(T), r.data(), sizeof(double) * T,
-                    cudaMemcpyHostToDevice));
+      h2d_sync(p, p->d_rbar + (size_t)b * gpm::BatchStrides::rbar(T), r.data(), sizeof(double) * T);
       p->rbar_init[b] = 1;
     }
     const int O = task->kind == GPMPPI_TASK_TRACKING ? 0 : task->n_obstacles;
@@ -794,7 +890,7 @@ void stage_tick(gpmppi_planner* p, const double* x0, const gpmppi_task* tasks) {
     }
     omax = std::max(omax, O);
   }
-  CK(cudaStreamSynchronize(p->stream));  // previous tick's staging copies are done
+  finish_pending(p, nullptr);  // previous tick's staging copies (and tightening) are done
   for (int b = 0; b < p->B; ++b) {
     fill_task(p->h_task[b], &tasks[b]);
     double* blk = p->h_x0 + (size_t)b * gpm::BatchStrides::X0;
@@ -907,6 +1003,26 @@ void enqueue_samples(gpmppi_planner* p, int finish, cudaEvent_t* evs) {
   if (evs) CK(cudaEventRecord(evs[3], p->stream));
 }
 
+// Samples + update of one tick. Single rank: the reduce's last CTA applies the update.
+// Sharded (NCCL attached): the reduce leaves this rank's tuple, one ncclAllGather on the
+// planner stream exchanges the (2T+6)-double tuples, and finish_kernel
+// combines them in rank order and applies update / clamp / shift identically on every
+// rank -- no host synchronisation between the rollout and the command.
+void enqueue_update(gpmppi_planner* p, cudaEvent_t* evs) {
+  if (!p->comm) {
+    enqueue_samples(p, 1, evs);
+    return;
+  }
+  enqueue_samples(p, 0, evs);
+  const int W = gpm::tuple_doubles(p->T);
+  nccl_check(nccl_api().all_gather(p->d_rank_tuple, p->d_gathered, (size_t)W, ncclDouble, p->comm, p->stream),
+             "ncclAllGather");
+  check(gpm::launch_finish(p->d_gathered, p->n_ranks, p->T, p->cfg.lambda, p->d_nom, p->cfg.lo, p->cfg.hi,
+                           p->d_out, p->K_total, p->d_combined, p->stream),
+        "finish kernel");
+  if (evs) CK(cudaEventRecord(evs[3], p->stream));  // the exchange counts to the reduce phase
+}
+
 void enqueue_tighten(gpmppi_planner* p) {
   gpm::TightenArgs t{};
   if (p->model) t.model = p->model->dev;
@@ -965,8 +1081,7 @@ void upload_terrain_weights(gpmppi_planner* p) {
   std::vector<double> w((size_t)p->B * gpm::BatchStrides::TW, 0.0);
   for (int b = 0; b < p->B; ++b)
     for (int i = 0; i < p->R; ++i) w[(size_t)b * gpm::BatchStrides::TW + i] = p->tw[(size_t)b * p->R + i];
-  CK(cudaStreamSynchronize(p->stream));
-  CK(cudaMemcpy(p->d_tw, w.data(), sizeof(double) * w.size(), cudaMemcpyHostToDevice));
+  h2d_sync(p, p->d_tw, w.data(), sizeof(double) * w.size());
 }
 
 gpmppi_planner* create_planner(const gpmppi_mppi_config* cfg, const gpmppi_prediction_model* pm,
@@ -1017,7 +1132,7 @@ gpmppi_planner* create_planner(const gpmppi_mppi_config* cfg, const gpmppi_predi
     p->R = pm->kind == GPMPPI_MODEL_GP_ENSEMBLE ? pm->n_terrains : 1;
     std::memset(p->coef_terrain, -1, sizeof p->coef_terrain);
     for (int g = 0; g < p->groups(); ++g)
-      for (int o = 0; o < p->model->dev.g[g].n_out && o < 8; ++o)
+      for (int o = 0; o < p->model->dev.g[g].n_out && o < gpm::kMaxOutPerGroup; ++o)
         p->coef_terrain[g][o] = (signed char)(p->model->dev.g[g].out_idx[o] >> 1);
     p->edd5 = {pm->edd5.alpha_l, pm->edd5.alpha_r, pm->edd5.x_icr, pm->edd5.y_icr_l,
                pm->edd5.y_icr_r, pm->track_width};
@@ -1078,8 +1193,15 @@ gpmppi_planner* create_planner(const gpmppi_mppi_config* cfg, const gpmppi_predi
 // The device work of one tick after staging: H2D, samples + update, command D2H (event
 // ev[0] marks the command), tightening (mppi.cpp:433), infeasibility D2H.
 void enqueue_tick(gpmppi_planner* p, bool capturing) {
+  auto rec = [&](cudaEvent_t e, cudaStream_t st) {
+    if (capturing)
+      CK(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
+    else
+      CK(cudaEventRecord(e, st));
+  };
+  rec(p->ev[1], p->stream);  // device start of the tick (plan_ms in command-first mode)
   enqueue_h2d(p);
-  enqueue_samples(p, 1, nullptr);
+  enqueue_update(p, nullptr);
   // the command / diagnostics readback forks off onto the side stream, so the tightening
   // follows the reduction directly on the main stream (no copy on its critical path)
   CK(cudaEventRecord(p->fork_ev, p->stream));
@@ -1094,6 +1216,7 @@ void enqueue_tick(gpmppi_planner* p, bool capturing) {
   enqueue_tighten(p);
   CK(cudaStreamWaitEvent(p->stream, p->join_ev, 0));
   CK(cudaMemcpyAsync(p->h_infeasible, p->d_infeasible, sizeof(int) * p->B, cudaMemcpyDeviceToHost, p->stream));
+  rec(p->ev[2], p->stream);  // tightening and its readback done
 }
 
 // Capture the tick into a graph (one launch instead of eight stream operations). Any
@@ -1140,12 +1263,13 @@ void plan_tick(gpmppi_planner* p, const double* x0, const gpmppi_task* tasks, do
   const auto t0 = Clock::now();  // mppi.cpp:391
   CK(cudaSetDevice(p->device));
   if (!command) invalid("plan_step: null command output");
-  if (p->K_local != p->K_total) invalid("plan_step: sharded planner; use plan_partial/plan_finish");
+  if (p->K_local != p->K_total && !p->comm)
+    invalid("plan_step: sharded planner without a communicator; attach one or use plan_partial/plan_finish");
   if (p->noise_mode == gpm::NOISE_INJECTED && !p->injected_set) invalid("plan_step: injected noise mode without noise");
   stage_tick(p, x0, tasks);
   // everything a captured kernel argument depends on (device buffers are fixed per planner)
   const long long key = (long long)p->n_obs_max | ((long long)p->noise_mode << 8) | ((long long)p->var_path << 10) |
-                        ((long long)p->R << 16);
+                        ((long long)p->R << 16) | ((long long)(p->comm != nullptr) << 24);
   if (p->use_graph && (!p->tick_exec || p->graph_key != key)) capture_tick(p, key);
   if (p->use_graph && p->tick_exec) {
     CK(cudaGraphLaunch(p->tick_exec, p->stream));
@@ -1153,11 +1277,42 @@ void plan_tick(gpmppi_planner* p, const double* x0, const gpmppi_task* tasks, do
   } else {
     enqueue_tick(p, false);
   }
+  const double t_launch = ms_since(t0);
   CK(cudaEventSynchronize(p->ev[0]));
   const double t_cmd = ms_since(t0);
-  CK(cudaStreamSynchronize(p->stream));
-  fill_diag(p, command, diag, t_cmd, ms_since(t0));
+  if (p->command_first) {
+    // command and diagnostics are on the host; the tightening (next tick's thresholds)
+    // finishes behind the return. stage_tick / accessors / wait_tightening wait for it.
+    p->pending_diag.assign(p->B, gpmppi_diag{});
+    fill_diag(p, command, p->pending_diag.data(), t_cmd, t_cmd);  // h_infeasible is still in flight
+    for (int b = 0; b < p->B; ++b) {
+      p->pending_diag[b].tightening_infeasible = 0;  // known at completion
+      p->pending_diag[b].plan_ms = t_launch;         // + device span at completion
+    }
+    if (diag)
+      for (int b = 0; b < p->B; ++b) diag[b] = p->pending_diag[b];
+    p->tightening_pending = true;
+  } else {
+    CK(cudaStreamSynchronize(p->stream));
+    fill_diag(p, command, diag, t_cmd, ms_since(t0));
+  }
   ++p->tick;  // mppi.cpp:460
+}
+
+// command-first mode: wait for the last tick's tightening and complete its diagnostics
+// (tightening_infeasible, plan_ms = host launch latency + device span of the whole tick)
+void finish_pending(gpmppi_planner* p, gpmppi_diag* diag) {
+  CK(cudaStreamSynchronize(p->stream));
+  if (!p->tightening_pending) return;
+  p->tightening_pending = false;
+  float dev_ms = 0.f;
+  if (cudaEventElapsedTime(&dev_ms, p->ev[1], p->ev[2]) != cudaSuccess) dev_ms = 0.f;
+  for (int b = 0; b < p->B; ++b) {
+    gpmppi_diag& d = p->pending_diag[b];
+    d.tightening_infeasible = p->h_infeasible[b];
+    d.plan_ms = std::max(d.plan_ms + (double)dev_ms, d.command_ms);
+    if (diag) diag[b] = d;
+  }
 }
 
 void set_weights(gpmppi_planner* p, int robot, const double* w, int R) {  // mppi.cpp:208-218
@@ -1237,8 +1392,8 @@ int gpmppi_planner_terrain_weights(const gpmppi_planner* p, double* w) {
 static int copy_back(const gpmppi_planner* p, void* dst, const void* src, size_t bytes) {
   return guarded([&] {
     CK(cudaSetDevice(p->device));
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, p->stream));  // after the tick's kernels
     CK(cudaStreamSynchronize(p->stream));
-    CK(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
   });
 }
 
@@ -1249,8 +1404,7 @@ int gpmppi_planner_nominal_sequence(const gpmppi_planner* p, double* seq) {
 int gpmppi_planner_set_nominal_sequence(gpmppi_planner* p, const double* seq) {
   if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
   return guarded([&] {
-    CK(cudaStreamSynchronize(p->stream));
-    CK(cudaMemcpy(p->d_nom, seq, sizeof(double) * 2 * p->T * p->B, cudaMemcpyHostToDevice));
+    h2d_sync(p, p->d_nom, seq, sizeof(double) * 2 * p->T * p->B);
   });
 }
 int gpmppi_planner_horizon_covariances(const gpmppi_planner* p, double* cov) {
@@ -1291,14 +1445,13 @@ int gpmppi_planner_set_thresholds(gpmppi_planner* p, const double* r_bar, const 
     CK(cudaStreamSynchronize(p->stream));
     for (int b = 0; b < p->B; ++b) {
       if (r_bar) {
-        CK(cudaMemcpy(p->d_rbar + (size_t)b * gpm::BatchStrides::rbar(p->T), r_bar + (size_t)b * p->T,
-                      sizeof(double) * p->T, cudaMemcpyHostToDevice));
+        h2d_sync(p, p->d_rbar + (size_t)b * gpm::BatchStrides::rbar(p->T), r_bar + (size_t)b * p->T,
+                 sizeof(double) * p->T);
         p->rbar_init[b] = 1;
       }
       if (margins) {
-        CK(cudaMemcpy(p->d_margins + (size_t)b * gpm::BatchStrides::marg(p->T),
-                      margins + (size_t)b * p->T * n_obstacles, sizeof(double) * p->T * n_obstacles,
-                      cudaMemcpyHostToDevice));
+        h2d_sync(p, p->d_margins + (size_t)b * gpm::BatchStrides::marg(p->T),
+                 margins + (size_t)b * p->T * n_obstacles, sizeof(double) * p->T * n_obstacles);
         p->margins_O[b] = n_obstacles;
       }
     }
@@ -1318,9 +1471,11 @@ int gpmppi_planner_inject_noise(gpmppi_planner* p, const double* eps) {
   if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
   return guarded([&] {
     const size_t cnt = (size_t)p->slots() * p->T * 2;
-    if (!p->d_eps) p->d_eps = p->dalloc<double>(cnt);
-    CK(cudaStreamSynchronize(p->stream));
-    CK(cudaMemcpy(p->d_eps, eps, sizeof(double) * cnt, cudaMemcpyHostToDevice));
+    if (!p->d_eps) {
+      p->d_eps = p->dalloc<double>(cnt, &p->sample_allocs);
+      p->invalidate_graph();  // the captured rollout / reduce name the injected buffer
+    }
+    h2d_sync(p, p->d_eps, eps, sizeof(double) * cnt);
     p->injected_set = true;
     p->noise_mode = gpm::NOISE_INJECTED;
   });
@@ -1409,7 +1564,7 @@ int gpmppi_planner_bench_device(gpmppi_planner* p, const double* x0, const gpmpp
   return guarded([&] {
     CK(cudaSetDevice(p->device));
     if (ticks < 1) invalid("bench_device: ticks must be >= 1");
-    if (p->K_local != p->K_total) invalid("bench_device: sharded planner");
+    if (p->K_local != p->K_total && !p->comm) invalid("bench_device: sharded planner without a communicator");
     stage_tick(p, x0, tasks);
     enqueue_h2d(p);
     void* flush = nullptr;
@@ -1428,7 +1583,7 @@ int gpmppi_planner_bench_device(gpmppi_planner* p, const double* x0, const gpmpp
     for (int t = 0; t < ticks; ++t) {
       cudaEvent_t* E = &evs[(size_t)t * 7];
       if (flush) CK(cudaMemsetAsync(flush, t & 0xff, flush_bytes, p->stream));  // outside the timed span
-      enqueue_samples(p, 1, E);
+      enqueue_update(p, E);
       enqueue_tighten(p);
       CK(cudaEventRecord(E[4], p->stream));
       ++p->tick;  // the staged keys stay at the first tick: same work, fixed noise
@@ -1437,7 +1592,7 @@ int gpmppi_planner_bench_device(gpmppi_planner* p, const double* x0, const gpmpp
       cudaEvent_t* E = &evs[(size_t)t * 7];
       if (flush) CK(cudaMemsetAsync(flush, (t + 7) & 0xff, flush_bytes, p->stream));
       CK(cudaEventRecord(E[5], p->stream));
-      enqueue_samples(p, 1, nullptr);
+      enqueue_update(p, nullptr);
       enqueue_tighten(p);
       CK(cudaEventRecord(E[6], p->stream));
       ++p->tick;
@@ -1505,9 +1660,7 @@ int gpmppi_planner_set_shard(gpmppi_planner* p, int64_t begin, int64_t count) {
     CK(cudaStreamSynchronize(p->stream));
     p->s_begin = begin;
     p->K_local = count;
-    p->d_eps = nullptr;
-    p->injected_set = false;
-    p->alloc_sample_buffers();
+    p->alloc_sample_buffers();  // frees the previous per-sample set, drops the tick graph
     CK(cudaStreamSynchronize(p->stream));
   });
 }
@@ -1666,6 +1819,70 @@ int gpmppi_shift_horizon(const double* seq, int T, int device, double* out) {
     check(gpm::launch_shift_horizon(ds.as<double>(), T, dout.as<double>(), 0), "shift_horizon_kernel");
     CK(cudaDeviceSynchronize());
     d2h(out, dout.p, sizeof(double) * 2 * T);
+  });
+}
+
+int gpmppi_nccl_unique_id(void* out) {
+  if (!out) return fail(GPMPPI_INVALID_ARGUMENT, "nccl_unique_id: null output");
+  return guarded([&] {
+    ncclUniqueId id;
+    nccl_check(nccl_required().get_unique_id(&id), "ncclGetUniqueId");
+    std::memcpy(out, &id, sizeof id);
+  });
+}
+
+int gpmppi_planner_attach_comm(gpmppi_planner* p, const void* unique_id, int n_ranks, int rank) {
+  if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
+  return guarded([&] {
+    if (!unique_id) invalid("attach_comm: null unique id");
+    if (p->B != 1) invalid("attach_comm: batched planners shard by robot, not by sample");
+    if (n_ranks < 1 || rank < 0 || rank >= n_ranks) invalid("attach_comm: bad rank / world size");
+    if (p->comm) invalid("attach_comm: a communicator is already attached");
+    if (p->K_total < n_ranks) invalid("attach_comm: fewer samples than ranks");
+    const NcclApi& api = nccl_required();
+    CK(cudaSetDevice(p->device));
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id, sizeof id);
+    ncclComm_t c = nullptr;
+    nccl_check(api.comm_init_rank(&c, n_ranks, id, rank), "ncclCommInitRank");  // collective
+    // contiguous global sample range of this rank (gpmppi.shard_range)
+    const long long base = p->K_total / n_ranks, extra = p->K_total % n_ranks;
+    p->s_begin = (long long)rank * base + std::min<long long>(rank, extra);
+    p->K_local = base + (rank < extra ? 1 : 0);
+    p->alloc_sample_buffers();  // drops any captured tick graph
+    p->d_gathered = p->dalloc<double>((size_t)n_ranks * gpm::tuple_doubles(p->T));
+    p->comm = c;
+    p->n_ranks = n_ranks;
+    p->rank = rank;
+    CK(cudaStreamSynchronize(p->stream));
+  });
+}
+
+int gpmppi_planner_shard(const gpmppi_planner* p, int64_t* begin, int64_t* count, int* n_ranks, int* rank) {
+  if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
+  if (begin) *begin = p->s_begin;
+  if (count) *count = p->K_local;
+  if (n_ranks) *n_ranks = p->n_ranks;
+  if (rank) *rank = p->rank;
+  return GPMPPI_OK;
+}
+
+int gpmppi_planner_set_command_first(gpmppi_planner* p, int on) {
+  if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
+  return guarded([&] {
+    finish_pending(p, nullptr);
+    p->command_first = on != 0;
+  });
+}
+
+int gpmppi_planner_wait_tightening(gpmppi_planner* p, gpmppi_diag* diag) {
+  if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
+  return guarded([&] {
+    CK(cudaSetDevice(p->device));
+    const bool had = p->tightening_pending;
+    finish_pending(p, diag);
+    if (!had && diag)  // nothing pending: the last tick's completed diagnostics, if any
+      for (int b = 0; b < (int)p->pending_diag.size(); ++b) diag[b] = p->pending_diag[b];
   });
 }
 

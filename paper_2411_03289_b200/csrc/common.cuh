@@ -22,7 +22,8 @@ constexpr int kMaxWaypoints = 64;
 constexpr int kMaxObstacles = 64;
 constexpr int kMaxTerrains = 16;
 constexpr int kMaxGroups = 4;
-constexpr int kMaxOutPerGroup = 8;
+constexpr int kMaxOutPerGroup = 2 * kMaxTerrains;  // one shared kernel over every terrain (harness.cpp:242-244)
+constexpr int kOutChunk = 8;  // outputs whose alpha loads are kept in flight together
 
 enum { TASK_TRACKING = 0, TASK_AVOIDANCE = 1, TASK_COMBINED = 2 };
 enum { MODEL_GP = 0, MODEL_EDD5 = 1, MODEL_UNICYCLE = 2, MODEL_NOMINAL = 3 };

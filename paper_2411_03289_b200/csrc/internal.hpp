@@ -110,7 +110,7 @@ struct ReduceArgs {
   const double* tw;         // [B][kMaxTerrains] terrain weights
   // trace coefficient of group g for robot b: Σ_o tw[b][coef_terrain[g][o]]² over
   // the group's outputs (mppi.cpp:34-49 combine); -1 ends the list
-  signed char coef_terrain[kMaxGroups][8];
+  signed char coef_terrain[kMaxGroups][kMaxOutPerGroup];
   const double* x0;         // [B][8] robot tick blocks (variance weight, key)
   int noise_mode;
   const double* eps;

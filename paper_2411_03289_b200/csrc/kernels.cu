@@ -120,18 +120,21 @@ GPM_D void load_robot_smem(const RolloutArgs& a, const SmemView& v, int b) {
     for (int g = 0; g < a.model.G; ++g) {
       const GroupDev& G = a.model.g[g];
       for (int j = threadIdx.x; j < ns; j += blockDim.x) {
-        double al[kMaxOutPerGroup];  // every output's alpha in flight before the combine
-#pragma unroll
-        for (int o = 0; o < kMaxOutPerGroup; ++o) al[o] = o < G.n_out ? __ldg(G.pts + (size_t)(5 + o) * ns + j) : 0.0;
         double s0 = 0.0, s1 = 0.0;
+        for (int o0 = 0; o0 < G.n_out; o0 += kOutChunk) {  // ascending o, kOutChunk loads in flight
+          double al[kOutChunk];
 #pragma unroll
-        for (int o = 0; o < kMaxOutPerGroup; ++o) {
-          if (o < G.n_out) {
-            const int gi = G.out_idx[o];
-            if (gi & 1)
-              s1 = fma(tw[gi >> 1], al[o], s1);
-            else
-              s0 = fma(tw[gi >> 1], al[o], s0);
+          for (int o = 0; o < kOutChunk; ++o)
+            al[o] = o0 + o < G.n_out ? __ldg(G.pts + (size_t)(5 + o0 + o) * ns + j) : 0.0;
+#pragma unroll
+          for (int o = 0; o < kOutChunk; ++o) {
+            if (o0 + o < G.n_out) {
+              const int gi = G.out_idx[o0 + o];
+              if (gi & 1)
+                s1 = fma(tw[gi >> 1], al[o], s1);
+              else
+                s0 = fma(tw[gi >> 1], al[o], s0);
+            }
           }
         }
         gp[5 * ns + j] = s0;
@@ -998,7 +1001,7 @@ __global__ void __launch_bounds__(256, 1) reduce_kernel(const ReduceArgs a) {
   for (int g = 0; g < kMaxGroups; ++g) {
     double c = 0.0;
     if (g < a.G)
-      for (int o = 0; o < 8 && a.coef_terrain[g][o] >= 0; ++o) {
+      for (int o = 0; o < kMaxOutPerGroup && a.coef_terrain[g][o] >= 0; ++o) {
         const double w = a.tw[(size_t)b * BatchStrides::TW + a.coef_terrain[g][o]];
         c += w * w;
       }
@@ -1273,26 +1276,31 @@ GPM_D void block_gp_predict(const ModelDev& M, const double q[4], double* kst /*
     const double q0 = q[0] / G.ls[0], q1 = q[1] / G.ls[1], q2 = q[2] / G.ls[2], q3 = q[3] / G.ls[3];
     const double qn = -0.5 * (q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
     const double* p = G.pts;
-    double acc[kMaxOutPerGroup];
-    for (int o = 0; o < kMaxOutPerGroup; ++o) acc[o] = 0.0;
     for (int j = threadIdx.x; j < n; j += blockDim.x) {
       const double d = q0 * p[j] + q1 * p[ns + j] + q2 * p[2 * ns + j] + q3 * p[3 * ns + j] + qn + p[4 * ns + j];
-      const double kj = exp(d);
-      kst[j] = kj;
-      for (int o = 0; o < G.n_out; ++o) acc[o] = fma(kj, p[(5 + o) * ns + j], acc[o]);
+      kst[j] = exp(d);  // each thread re-reads only its own entries below
     }
-    for (int o = 0; o < G.n_out; ++o) {
-      const double s = warp_sum(acc[o]);
-      if (lane == 0) red[w * 8 + o] = s;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0)
-      for (int o = 0; o < G.n_out; ++o) {
-        double s = 0.0;
-        for (int q2i = 0; q2i < nw; ++q2i) s += red[q2i * 8 + o];
-        mean[G.out_idx[o]] = s;
+    for (int o0 = 0; o0 < G.n_out; o0 += kOutChunk) {  // k*.alpha, kOutChunk outputs per pass
+      double acc[kOutChunk];
+      for (int o = 0; o < kOutChunk; ++o) acc[o] = 0.0;
+      const int no = min(kOutChunk, G.n_out - o0);
+      for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        const double kj = kst[j];
+        for (int o = 0; o < no; ++o) acc[o] = fma(kj, p[(5 + o0 + o) * ns + j], acc[o]);
       }
-    __syncthreads();
+      for (int o = 0; o < no; ++o) {
+        const double s = warp_sum(acc[o]);
+        if (lane == 0) red[w * 8 + o] = s;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0)
+        for (int o = 0; o < no; ++o) {
+          double s = 0.0;
+          for (int q2i = 0; q2i < nw; ++q2i) s += red[q2i * 8 + o];
+          mean[G.out_idx[o0 + o]] = s;
+        }
+      __syncthreads();
+    }
     // a_j = Σ_{i<=j} k_i L^{-T}[i][j]; ssq = Σ a_j^2
     double ssq = 0.0;
     for (int j = threadIdx.x; j < n; j += blockDim.x) {
@@ -1404,18 +1412,21 @@ __global__ void __launch_bounds__(TMEAN_THREADS, 1) tighten_mean_kernel(const Ti
       for (int i = threadIdx.x; i < 5 * ns / 2; i += blockDim.x) d2[i] = __ldg(src + i);
       // combine_terrains (mppi.cpp:34-49) folded into alpha, as in the rollout (load_robot_smem)
       for (int j = threadIdx.x; j < ns; j += blockDim.x) {
-        double al[NO];  // all loads in flight before the combine (cold L2 after the rollout)
-#pragma unroll
-        for (int o = 0; o < NO; ++o) al[o] = o < Gd.n_out ? __ldg(Gd.pts + (size_t)(5 + o) * ns + j) : 0.0;
         double s0 = 0.0, s1 = 0.0;
+        for (int o0 = 0; o0 < Gd.n_out; o0 += NO) {  // NO loads in flight (cold L2 after the rollout)
+          double al[NO];
 #pragma unroll
-        for (int o = 0; o < NO; ++o) {
-          if (o < Gd.n_out) {
-            const int gi = Gd.out_idx[o];
-            if (gi & 1)
-              s1 = fma(rtw[gi >> 1], al[o], s1);
-            else
-              s0 = fma(rtw[gi >> 1], al[o], s0);
+          for (int o = 0; o < NO; ++o)
+            al[o] = o0 + o < Gd.n_out ? __ldg(Gd.pts + (size_t)(5 + o0 + o) * ns + j) : 0.0;
+#pragma unroll
+          for (int o = 0; o < NO; ++o) {
+            if (o0 + o < Gd.n_out) {
+              const int gi = Gd.out_idx[o0 + o];
+              if (gi & 1)
+                s1 = fma(rtw[gi >> 1], al[o], s1);
+              else
+                s0 = fma(rtw[gi >> 1], al[o], s0);
+            }
           }
         }
         dst[5 * ns + j] = s0;
@@ -1699,15 +1710,18 @@ __global__ void __launch_bounds__(256, 1) tighten_cov_kernel(const TightenArgs a
   double* Js = csm;
   double* cvs = csm + 25 * T;
   double* mus = cvs + 2 * T;
-  for (int i = l; i < 25 * T; i += nt) Js[i] = atJ[i];
-  for (int i = l; i < 5 * (T + 1); i += nt) mus[i] = atmu[i];
   const int G = a.model_kind == MODEL_GP ? a.model.G : 0;
   if (l == 0) {
     infeasible = 0;
     for (int g = 0; g < G; ++g)
       for (int o = 0; o < a.model.g[g].n_out; ++o) gof[a.model.g[g].out_idx[o]] = g;
   }
-  pdl_wait();  // J / belief means come from the mean kernel (complete); the variance partials next
+  // J and the belief means are written by tighten_mean_kernel, two launches back: PTX
+  // guarantees their visibility only after this grid's own griddepcontrol.wait, so the
+  // staging follows it (it does not rely on the variance grid's wait-before-trigger order)
+  pdl_wait();
+  for (int i = l; i < 25 * T; i += nt) Js[i] = atJ[i];
+  for (int i = l; i < 5 * (T + 1); i += nt) mus[i] = atmu[i];
   __syncthreads();
   // per-step combined correction variance (gp.cpp:187-191 + ensemble_combine gp.cpp:380-386)
   for (int k = l; k < T; k += nt) {

@@ -559,6 +559,32 @@ class Planner:
         A.check(A.lib().gpmppi_planner_plan_partial(self._h, A.dptr(x), C.byref(tc),
                                                     C.c_void_p(device_tuple_ptr)))
 
+    def attach_comm(self, unique_id: bytes, n_ranks: int, rank: int):
+        """Shard this planner's samples over an NCCL communicator (collective: every rank
+        calls it with the same id). plan_step then runs the sharded tick in the library."""
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        A.check(A.lib().gpmppi_planner_attach_comm(self._h, buf, n_ranks, rank))
+
+    def shard(self):
+        """(begin, count, n_ranks, rank) of this planner's global sample range."""
+        b, c, n, r = C.c_int64(), C.c_int64(), C.c_int(), C.c_int()
+        A.check(A.lib().gpmppi_planner_shard(self._h, C.byref(b), C.byref(c), C.byref(n), C.byref(r)))
+        return b.value, c.value, n.value, r.value
+
+    def set_command_first(self, on: bool = True):
+        """plan_step returns at the command; the tightening pass completes behind it."""
+        A.check(A.lib().gpmppi_planner_set_command_first(self._h, int(bool(on))))
+
+    def wait_tightening(self, diag: Optional[StepDiagnostics] = None):
+        """Wait for the last tick's tightening; completes its diagnostics (command-first mode)."""
+        d = A.DiagC()
+        A.check(A.lib().gpmppi_planner_wait_tightening(self._h, C.byref(d)))
+        if diag is not None:
+            for k, _ in A.DiagC._fields_:
+                setattr(diag, k, getattr(d, k))
+            diag.tightening_infeasible = bool(d.tightening_infeasible)
+        return diag
+
     def plan_finish(self, device_tuples_ptr: int, n_ranks: int, diag=None):
         cmd = np.empty(2)
         d = A.DiagC()
@@ -788,6 +814,13 @@ def apply_tuple(tup, nominal, lo=(-0.5, -2.0), hi=(2.0, 2.0)):
     dv = tup[6:].reshape(T, 2) / Z if Z > 0 else np.zeros((T, 2))
     upd = np.clip(np.asarray(nominal) + dv, lo, hi)
     return upd[0].copy(), np.vstack([upd[1:], upd[-1:]])
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh ncclUniqueId (128 bytes) for Planner.attach_comm; broadcast it to every rank."""
+    buf = C.create_string_buffer(128)
+    A.check(A.lib().gpmppi_nccl_unique_id(buf))
+    return buf.raw
 
 
 def tuple_doubles(horizon: int) -> int:

@@ -20,7 +20,26 @@ def test_bench_json_contract_dry_run():
     rf = line["roofline"]
     for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
         assert k in rf
-    assert rf["bound"] in ("hbm", "tensor")
+    assert rf["bound"] in ("hbm", "tensor", "fp64")  # the FP64 rollout is labelled by its own pipe
     e = line["e2e"]
     assert e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert "workload" in line["config"]
+    assert e["ticks"] >= 200 and "command_first" in e
+
+
+def test_bench_metric_same_for_both_arms():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    src = open(os.path.join(ROOT, "bench.py")).read()
+    assert src.count('"metric": METRIC') >= 3 and '"metric": "' not in src
+
+
+def test_bench_dry_run_gpus_n():
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--dry-run", "--gpus", "8",
+                        "--steps", "4"], capture_output=True, text=True, timeout=120,
+                       env={k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK")})
+    assert r.returncode == 0, r.stderr
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 8
