@@ -1099,11 +1099,10 @@ __global__ void __launch_bounds__(256, 1) reduce_kernel(const ReduceArgs a) {
           ep[u] = su < b1 ? eps2[(size_t)(base + su) * T + k] : make_double2(0.0, 0.0);
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (ev[u] != 0.0) {  // skipped, not multiplied: eps of a dead sample may be non-finite
-            s0 += ev[u] * ep[u].x;
-            s1 += ev[u] * ep[u].y;
-          }
+        for (int u = 0; u < 4; ++u) {  // multiplied even when e = 0: a non-finite injected eps
+          s0 += ev[u] * ep[u].x;       // poisons the update exactly as mppi.cpp:157-160 does
+          s1 += ev[u] * ep[u].y;
+        }
       }
     } else {
       for (int s = b0 + sl; s < b1; s += nsl) {

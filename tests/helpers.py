@@ -6,14 +6,43 @@ import numpy as np
 from oracle import oracle as O
 from paper_2411_03289_b200 import workloads as W
 
-# Parity tolerances (stated; see DESIGN.md §Parity):
-#  - GP-mean / dynamics / tightening are FP64 on both sides → 1e-9 relative.
-#  - the per-sample variance term comes from the FP32 variance kernel: its cost
-#    contribution is α0·Σ_k trace ≤ ~1e-2 with relative error ≤ ~1e-4, so the
-#    cost tolerance is atol 1e-6 + rtol 1e-9.
+# Parity tolerances (stated; see DESIGN.md §7):
+#  - GP mean / dynamics / tightening are FP64 on both sides (agree to ~1e-12).
+#  - the per-sample variance term comes from the tensor-core variance kernel (default
+#    3xFP16; 3xTF32 and FFMA selectable). Its per-step error is bounded relative to the
+#    signal variance: |Δvar| <= VAR_REL * sf2 (measured 2.0e-5 * sf2 for 3xFP16 at n=2048,
+#    tests/test_gpu_variance_paths.py). The cost adds α0 · Σ_k Σ_g (Σ_o w_o²) var_g, so a
+#    cost differs by at most α0 · T · sf2 · VAR_REL (Σ w² <= 1 on the simplex):
+#    cost_atol(w) = COST_ATOL + α0·T·sf2·VAR_REL; at the test kernel (sf2 = 4e-3, T = 40,
+#    α0 = 0.1) that is 1e-6 + 8e-9.
 COST_ATOL, COST_RTOL = 1e-6, 1e-9
+VAR_REL = 5e-5
 SEQ_ATOL = 1e-6          # nominal sequence / command (softmax amplifies cost error by 1/λ)
 TIGHT_RTOL = 1e-7        # r̄, margins, horizon covariances
+# diagnostics: best / mean cost carry the cost tolerance; ESS and entropy are sums of the
+# softmax weights, whose relative error is |Δc|/λ <= 1e-5 at λ = 0.1 (same bound as the
+# weights, which are checked at rtol 1e-4)
+DIAG_RTOL = 1e-5
+
+
+def cost_atol(alpha0=0.1, T=40, sf2=4e-3):
+    return COST_ATOL + alpha0 * T * sf2 * VAR_REL
+
+
+def assert_diag_parity(do_, dd, label="", cost_tol=COST_ATOL):
+    """StepDiagnostics of one tick (mppi.cpp:435-459) against the oracle's."""
+    assert dd.nonfinite_samples == do_["nonfinite_samples"], f"{label}: nonfinite count"
+    assert bool(dd.tightening_infeasible) == bool(do_["tightening_infeasible"]), f"{label}: infeasible"
+    for k in ("best_cost", "mean_cost"):
+        a, b = getattr(dd, k), do_[k]
+        if np.isfinite(b):
+            assert abs(a - b) <= cost_tol + COST_RTOL * abs(b), f"{label}: {k} {a} vs {b}"
+        else:
+            assert (np.isnan(a) and np.isnan(b)) or a == b, f"{label}: {k} {a} vs {b}"
+    for k in ("ess", "weight_entropy"):
+        a, b = getattr(dd, k), do_[k]
+        assert abs(a - b) <= DIAG_RTOL * abs(b) + 1e-12, f"{label}: {k} {a} vs {b}"
+    assert dd.command_ms > 0.0 and dd.plan_ms >= dd.command_ms, f"{label}: timings"
 
 
 def oracle_task(w, obstacles):
@@ -59,11 +88,11 @@ def build_pair(w, gp_seed=0, samples=None, threads=0, var_path=None):
     return po, pd, task_o, task_d, data
 
 
-def assert_tick_parity(po, pd, flags_exact=True, label=""):
+def assert_tick_parity(po, pd, flags_exact=True, label="", cost_tol=None):
     co, cd = po.costs(), pd.sample_costs()
     fin_o, fin_d = np.isfinite(co), np.isfinite(cd)
     assert np.array_equal(fin_o, fin_d), f"{label}: finite masks differ"
-    np.testing.assert_allclose(cd[fin_d], co[fin_o], rtol=COST_RTOL, atol=COST_ATOL,
+    np.testing.assert_allclose(cd[fin_d], co[fin_o], rtol=COST_RTOL, atol=cost_tol or COST_ATOL,
                                err_msg=f"{label}: per-sample costs")
     if fin_o.any():
         assert int(np.nanargmin(co)) == int(np.nanargmin(cd)), f"{label}: argmin sample"

@@ -12,12 +12,14 @@ import pytest
 
 from oracle import oracle as O
 from paper_2411_03289_b200 import workloads as W
-from tests.helpers import (COST_ATOL, SEQ_ATOL, TIGHT_RTOL, assert_tick_parity, build_pair)
+from tests.helpers import (COST_ATOL, SEQ_ATOL, TIGHT_RTOL, assert_diag_parity, assert_tick_parity,
+                           build_pair)
 
 pytestmark = pytest.mark.gpu
 
 
 def _run_ticks(w, ticks=3, samples=None, philox=False, gp_seed=0, flags_exact=True, var_path=None):
+    import paper_2411_03289_b200 as G
     po, pd, to, td, _ = build_pair(w, gp_seed=gp_seed, samples=samples, var_path=var_path)
     K, T = po.K, po.T
     x = np.array(w.x0, dtype=np.float64)
@@ -28,9 +30,11 @@ def _run_ticks(w, ticks=3, samples=None, philox=False, gp_seed=0, flags_exact=Tr
             eps = O.sample_perturbations(K, T, w.sigma_sim, w.seed, t)
             pd.inject_noise(eps)
         co, do_ = po.plan_step(x, to, eps)
-        cd = pd.plan_step(x, td)
+        dd = G.StepDiagnostics()
+        cd = pd.plan_step(x, td, dd)
         label = f"{w.name} tick {t}"
         assert_tick_parity(po, pd, flags_exact=flags_exact, label=label)
+        assert_diag_parity(do_, dd, label=label)
         np.testing.assert_allclose(cd, co, atol=SEQ_ATOL, err_msg=label + ": command")
         if w.task != "avoidance":
             np.testing.assert_allclose(pd.lane_radii(), po.lane_radii(), rtol=TIGHT_RTOL,
@@ -118,9 +122,16 @@ def test_config2_variance_paths_parity(var_path):
     _run_ticks(W.CONFIGS["config2"], ticks=2, samples=2048, var_path=var_path)
 
 
-def test_config3_shape_parity_tc():
-    """n=2048, T=60 multi-terrain (BASELINE config 3 shape) at reduced K, 3xTF32 variance."""
-    _run_ticks(W.CONFIGS["config3"], ticks=1, samples=512, var_path=1)
+@pytest.mark.parametrize("var_path", [1, 3])
+def test_config3_shape_parity_tc(var_path):
+    """n=2048, T=60 multi-terrain (BASELINE config 3 shape) at reduced K: 3xTF32 and the
+    default 3xFP16 variance through plan_step."""
+    _run_ticks(W.CONFIGS["config3"], ticks=1, samples=512, var_path=var_path)
+
+
+def test_config3_default_path_k4096():
+    """Config 3 (T=60, n=2048) through plan_step on the default 3xFP16 variance at K=4096."""
+    _run_ticks(W.CONFIGS["config3"], ticks=1, samples=4096)
 
 
 def test_config2_philox_noise_parity():
