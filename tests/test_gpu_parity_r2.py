@@ -78,15 +78,21 @@ def test_overflow_deaths_at_different_steps():
     The gap to DBL_MAX is chosen on the oracle so that some, not all, samples die."""
     w = dataclasses.replace(W.CONFIGS["config1"], model="nominal", samples=512, horizon=30)
     eps = O.sample_perturbations(512, 30, w.sigma_sim, w.seed, 0)
-    x = None
-    for gap in (2e305, 4e305, 8e305, 1.6e306, 3.2e306, 6.4e306):
-        cand = np.array([1.7976931348623157e308 - gap, 0.0, 1.0, 2.0e306, 0.0])
-        po, pd, to, td, _ = build_pair(w)
-        po.plan_step(cand, to, eps)
-        alive = po.flags()["alive"]
-        if 0.1 * 512 < alive.sum() < 0.9 * 512:
-            x = cand
+    to_probe = build_pair(w)[2]
+
+    def alive_count(gap):
+        po = O.Planner(512, 30, O.ORC_MODEL_NOMINAL, None, 0, lam=w.lam, sigma_sim=w.sigma_sim, seed=w.seed)
+        po.plan_step(np.array([1.7976931348623157e308 - gap, 0.0, 1.0, 2.0e306, 0.0]), to_probe, eps)
+        return int(po.flags()["alive"].sum())
+
+    lo, hi, x = 1e304, 1e307, None  # bisection: fewer survivors at a smaller gap
+    for _ in range(60):
+        gap = 0.5 * (lo + hi)
+        a = alive_count(gap)
+        if 0.1 * 512 < a < 0.9 * 512:
+            x = np.array([1.7976931348623157e308 - gap, 0.0, 1.0, 2.0e306, 0.0])
             break
+        lo, hi = (gap, hi) if a <= 0.1 * 512 else (lo, gap)
     assert x is not None, "no gap left a mixed alive set"
     po, pd, to, td, _ = build_pair(w)
     pd.inject_noise(eps)
