@@ -88,7 +88,7 @@ def build_pair(w, gp_seed=0, samples=None, threads=0, var_path=None):
     return po, pd, task_o, task_d, data
 
 
-def assert_tick_parity(po, pd, flags_exact=True, label="", cost_tol=None):
+def assert_tick_parity(po, pd, flags_exact=True, label="", cost_tol=None, seq_tol=None):
     co, cd = po.costs(), pd.sample_costs()
     fin_o, fin_d = np.isfinite(co), np.isfinite(cd)
     assert np.array_equal(fin_o, fin_d), f"{label}: finite masks differ"
@@ -104,5 +104,5 @@ def assert_tick_parity(po, pd, flags_exact=True, label="", cost_tol=None):
         assert np.array_equal(fo["coll"], fd["coll"]), f"{label}: collision flags"
     wo, wd = po.weights(), pd.sample_weights()
     np.testing.assert_allclose(wd, wo, rtol=1e-4, atol=1e-9, err_msg=f"{label}: weights")
-    np.testing.assert_allclose(pd.nominal_sequence(), po.nominal_sequence(), atol=SEQ_ATOL,
+    np.testing.assert_allclose(pd.nominal_sequence(), po.nominal_sequence(), atol=seq_tol or SEQ_ATOL,
                                rtol=0, err_msg=f"{label}: nominal sequence")
