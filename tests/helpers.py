@@ -39,9 +39,10 @@ def assert_diag_parity(do_, dd, label="", cost_tol=COST_ATOL):
             assert abs(a - b) <= cost_tol + COST_RTOL * abs(b), f"{label}: {k} {a} vs {b}"
         else:
             assert (np.isnan(a) and np.isnan(b)) or a == b, f"{label}: {k} {a} vs {b}"
+    rtol = DIAG_RTOL * max(1.0, cost_tol / COST_ATOL)  # weight error scales with the cost error
     for k in ("ess", "weight_entropy"):
         a, b = getattr(dd, k), do_[k]
-        assert abs(a - b) <= DIAG_RTOL * abs(b) + 1e-12, f"{label}: {k} {a} vs {b}"
+        assert abs(a - b) <= rtol * abs(b) + 1e-12, f"{label}: {k} {a} vs {b}"
     assert dd.command_ms > 0.0 and dd.plan_ms >= dd.command_ms, f"{label}: timings"
 
 
