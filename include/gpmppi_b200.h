@@ -299,6 +299,30 @@ int gpmppi_update_controls(const double* nominal, int T, const double* eps, cons
 /* shift_horizon (mppi.cpp:166-173) */
 int gpmppi_shift_horizon(const double* seq, int T, int device, double* out);
 
+/* ---- the reference's scalar helpers (bindings/module.cpp:40-181), host C++ ----
+ * Same arithmetic as the planner's kernels (common.cuh); return GPMPPI_INVALID_ARGUMENT
+ * with the reference's message where the reference throws std::invalid_argument. */
+double gpmppi_wrap_angle(double angle);                                               /* core.hpp:18-27 */
+int gpmppi_step_nominal(const double s[5], const double u[2], const gpmppi_nominal* p, double out[5]);
+int gpmppi_step_kinematic_unicycle(const double s[5], const double u[2], double dt, double out[5]);
+int gpmppi_step_edd5(const double s[5], const double u[2], const gpmppi_edd5* p, double track_width, double dt,
+                     double out[5]);                                                   /* dynamics.cpp:59-127 */
+int gpmppi_jacobian_nominal(const double s[5], const double u[2], const gpmppi_nominal* p,
+                            double J[25]);                                             /* dynamics.cpp:68-98, row-major */
+int gpmppi_body_frame_displacement(const double from[5], const double to[5], double out[2]); /* core.hpp:117-126 */
+int gpmppi_kernel_eval(const double a[4], const double b[4], const double kernel6[6], double* out); /* gp.cpp:53-60 */
+/* gp.cpp:368-389: means / var_diags m x 2 row-major, weights m on the simplex (1e-6) */
+int gpmppi_ensemble_combine(const double* means, const double* var_diags, const double* weights, int m,
+                            double mean[2], double cov[4]);
+int gpmppi_project_simplex(const double* z, int m, double* out);                       /* terrain.cpp:72-92 */
+int gpmppi_chi2_quantile_2dof(double p, double* out);                                   /* uncertainty.cpp:8-13 */
+int gpmppi_normal_quantile(double p, double* out);                                      /* uncertainty.cpp:54-60 */
+double gpmppi_normal_cdf(double x);                                                     /* uncertainty.cpp:15 */
+int gpmppi_tighten_lane_radius(double r, const double cov_xy[4], double p_x, double* out); /* :90-96 */
+int gpmppi_tighten_obstacle_distance(const double robot_xy[2], const double center[2], double radius,
+                                     const double cov_xy[4], double p_x, double* d_bar, double normal[2],
+                                     int* degenerate, double* d);                        /* :98-116 */
+
 #ifdef __cplusplus
 }
 #endif

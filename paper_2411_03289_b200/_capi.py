@@ -151,6 +151,21 @@ SIGNATURES = [
     ("gpmppi_trajectory_weights", C.c_int, [_dp, C.c_int64, C.c_double, C.c_int, _dp]),
     ("gpmppi_update_controls", C.c_int, [_dp, C.c_int, _dp, _dp, C.c_int64, _dp, _dp, C.c_int, _dp]),
     ("gpmppi_shift_horizon", C.c_int, [_dp, C.c_int, C.c_int, _dp]),
+    ("gpmppi_wrap_angle", C.c_double, [C.c_double]),
+    ("gpmppi_step_nominal", C.c_int, [_dp, _dp, C.POINTER(NominalC), _dp]),
+    ("gpmppi_step_kinematic_unicycle", C.c_int, [_dp, _dp, C.c_double, _dp]),
+    ("gpmppi_step_edd5", C.c_int, [_dp, _dp, C.POINTER(Edd5C), C.c_double, C.c_double, _dp]),
+    ("gpmppi_jacobian_nominal", C.c_int, [_dp, _dp, C.POINTER(NominalC), _dp]),
+    ("gpmppi_body_frame_displacement", C.c_int, [_dp, _dp, _dp]),
+    ("gpmppi_kernel_eval", C.c_int, [_dp, _dp, _dp, _dp]),
+    ("gpmppi_ensemble_combine", C.c_int, [_dp, _dp, _dp, C.c_int, _dp, _dp]),
+    ("gpmppi_project_simplex", C.c_int, [_dp, C.c_int, _dp]),
+    ("gpmppi_chi2_quantile_2dof", C.c_int, [C.c_double, _dp]),
+    ("gpmppi_normal_quantile", C.c_int, [C.c_double, _dp]),
+    ("gpmppi_normal_cdf", C.c_double, [C.c_double]),
+    ("gpmppi_tighten_lane_radius", C.c_int, [C.c_double, _dp, C.c_double, _dp]),
+    ("gpmppi_tighten_obstacle_distance", C.c_int, [_dp, _dp, C.c_double, _dp, C.c_double, _dp, _dp,
+                                                   C.POINTER(C.c_int), _dp]),
 ]
 
 

@@ -9,7 +9,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "lib", "libgpmppi_b200.so")
-SOURCES = ["kernels.cu", "kernels_tc.cu", "fit.cu", "capi.cpp"]
+SOURCES = ["kernels.cu", "kernels_tc.cu", "fit.cu", "capi.cpp", "hostapi.cpp"]
 HEADERS = ["common.cuh", "internal.hpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -272,6 +272,10 @@ void factor_group(HostGroup& G, const double* X, const double* Y, int n, int m,
 
 }  // namespace
 
+namespace gpm_host {  // error channel for the other translation units (hostapi.cpp)
+int set_error(int code, const std::string& msg) { return fail(code, msg); }
+}  // namespace gpm_host
+
 // ===========================================================================
 struct gpmppi_model {
   int device = 0;

@@ -573,32 +573,52 @@ def random_obstacle_field(rng: RngStream, count=5, x_range=(1.5, 6.5), y_range=(
 def make_scenario(kind: str = "tracking", track: str = "circle", seed: int = 0,
                   v_desired: float = 2.0, schedule=None, distance_budget: float = 100.0,
                   max_duration: float = 120.0, n_obstacles: int = 5,
-                  goal: G.GoalSpec = None) -> Scenario:
-    """Canonical geometry of config.hpp:43-54 (harness.cpp:146-188)."""
+                  goal: G.GoalSpec = None, geometry: dict = None, start=None, obstacles=None,
+                  random_obstacles: dict = None) -> Scenario:
+    """Scenario from the config's geometry (config.hpp:43-54, harness.cpp:146-188).
+    geometry / random_obstacles take the JSON config's sections (paper_2411_03289_b200.config);
+    start (x, y, theta) overrides the canonical start; obstacles (list of (x, y, r)) replaces
+    the random field."""
     goal = goal or G.GoalSpec((8.0, 0.0), 0.5)
+    geo = geometry or {}
+    circ = {"center": [0.0, 0.0], "radius": 2.0, "half_width": 0.4, **geo.get("circle", {})}
+    sq = {"center": [0.0, 0.0], "side": 6.25, "half_width": 0.4, **geo.get("square", {})}
+    lane = {"from": [0.0, 0.0], "to": [60.0, 0.0], "half_width": 0.4, **geo.get("lane", {})}
     sc = Scenario(kind=kind, v_desired=v_desired, goal=goal,
                   schedule=list(schedule or [(0.0, 0)]), distance_budget=distance_budget,
                   max_duration=max_duration)
     if track == "circle":
-        sc.track = G.Track.circle_track((0.0, 0.0), 2.0, 0.4)
-        start = (2.0, 0.0, 0.5 * math.pi)
+        c, r = circ["center"], circ["radius"]
+        sc.track = G.Track.circle_track(tuple(c), r, circ["half_width"])
+        st = (c[0] + r, c[1], 0.5 * math.pi)
     elif track == "square":
-        h = 0.5 * 6.25
-        sc.track = G.Track.polyline_track([(h, -h), (h, h), (-h, h), (-h, -h)], 0.4, True)
-        start = (0.0, -h, 0.0)
+        h, c = 0.5 * sq["side"], sq["center"]
+        sc.track = G.Track.polyline_track([(c[0] + h, c[1] - h), (c[0] + h, c[1] + h), (c[0] - h, c[1] + h),
+                                           (c[0] - h, c[1] - h)], sq["half_width"], True)
+        st = (c[0], c[1] - h, 0.0)
     elif track == "lane":
-        sc.track = G.Track.polyline_track([(0.0, 0.0), (60.0, 0.0)], 0.4, False)
-        start = (0.0, 0.0, 0.0)
+        a, b = lane["from"], lane["to"]
+        sc.track = G.Track.polyline_track([tuple(a), tuple(b)], lane["half_width"], False)
+        st = (a[0], a[1], math.atan2(b[1] - a[1], b[0] - a[0]))
     else:
         raise ValueError(f"make_scenario: unknown track {track!r}")
     if kind == "avoidance":
-        start = (0.0, 0.0, math.atan2(goal.position[1], goal.position[0]))
+        st = (0.0, 0.0, math.atan2(goal.position[1], goal.position[0]))
     elif kind != "tracking":
         raise ValueError(f"make_scenario: unknown kind {kind!r}")
-    sc.start = (start[0], start[1], wrap_angle(start[2]), 0.0, 0.0)
+    if start is not None:
+        st = tuple(start)
+    sc.start = (st[0], st[1], wrap_angle(st[2]), 0.0, 0.0)
     if kind == "avoidance":
-        rng = RngStream(derive_seed(seed, 3))
-        sc.obstacles = random_obstacle_field(rng, n_obstacles, start=start[:2], goal=goal)
+        if obstacles is not None:
+            sc.obstacles = [G.CircleObstacle((float(o[0]), float(o[1])), float(o[2])) for o in obstacles]
+        else:
+            ro = {"count": n_obstacles, "x_min": 1.5, "x_max": 6.5, "y_min": -2.5, "y_max": 2.5,
+                  "radius_min": 0.25, "radius_max": 0.5, "min_gap": 0.5, **(random_obstacles or {})}
+            rng = RngStream(derive_seed(seed, 3))
+            sc.obstacles = random_obstacle_field(rng, ro["count"], (ro["x_min"], ro["x_max"]),
+                                                 (ro["y_min"], ro["y_max"]), (ro["radius_min"], ro["radius_max"]),
+                                                 ro["min_gap"], start=sc.start[:2], goal=goal)
     return sc
 
 
@@ -805,25 +825,28 @@ def _metrics_to_dict(m: RunMetrics) -> dict:  # module.cpp:22-36
 
 
 def _run(kind: str, config_path: str, seed: int, planner: str, **scenario):
-    if config_path:
-        raise ValueError("run_%s: JSON config files are not supported by this build; pass "
-                         "config_path='' for the default configuration" % kind)
-    cfg = ExperimentConfig(seed=seed)
+    """module.cpp:183-208: the JSON config (or the default one), seed and planner overrides,
+    models trained unless the planner is the unicycle, then one closed-loop run."""
+    from . import config as CF
+    jc = CF.load_config(config_path) if config_path else CF.default_config()
+    jc["seed"] = seed
     if planner:
-        if planner not in ("gp", "edd5", "unicycle"):
-            raise ValueError(f"unknown planner {planner!r}")
-        cfg.planner = planner
+        CF.planner_kind(planner)
+        jc["planner"] = planner
+    jc["scenario"]["kind"] = kind
+    cfg, sc_kwargs = CF.to_experiment(jc)
+    sc_kwargs.update(scenario)
     models = G.TrainedModels() if cfg.planner == "unicycle" else train_models(cfg, seed)
-    sc = make_scenario(kind, seed=seed, **scenario)
+    sc = make_scenario(seed=seed, **sc_kwargs)
     run = run_tracking_experiment if kind == "tracking" else run_avoidance_experiment
     return _metrics_to_dict(run(cfg, sc, models, seed))
 
 
 def run_tracking(config_path: str = "", seed: int = 0, planner: str = "", **scenario) -> dict:
-    """module.cpp:183-196: default config, train, closed-loop tracking, metrics dict."""
+    """module.cpp:183-196: config, train, closed-loop tracking, metrics dict."""
     return _run("tracking", config_path, seed, planner, **scenario)
 
 
 def run_avoidance(config_path: str = "", seed: int = 0, planner: str = "", **scenario) -> dict:
-    """module.cpp:197-210: default config, train, closed-loop avoidance, metrics dict."""
+    """module.cpp:197-210: config, train, closed-loop avoidance, metrics dict."""
     return _run("avoidance", config_path, seed, planner, **scenario)

@@ -75,5 +75,5 @@ def test_python_entry_points_match_reference_bindings():  # module.cpp:183-210, 
     assert m["success"] and not m["aborted"]
     a = H.run_avoidance(seed=2, planner="gp", max_duration=20.0)
     assert a["ticks"] > 0 and not a["aborted"]
-    with pytest.raises(ValueError):
-        H.run_tracking(config_path="cfg.json")
+    with pytest.raises(RuntimeError, match="cannot open"):  # std::runtime_error, config.cpp:189-191
+        H.run_tracking(config_path="no-such-cfg.json")
