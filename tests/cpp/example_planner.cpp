@@ -48,8 +48,8 @@ int main() {
     const Perturbations eps = sample_perturbations(cfg, 0);
     const ControlSequence up = update_controls(seq, eps, std::vector<double>(eps.size(), 1.0 / eps.size()), ControlBounds{});
     const ControlSequence sh = shift_horizon(seq);
-    std::printf("free      w0=%.12f states=%zu eps=%zux%zu upd=%zu shift=%zu\n", w[0], r.states.size(), eps.size(),
-                eps[0].size(), up.size(), sh.size());
+    std::printf("free      w0=%.12f states=%zu eps=%zux%ld upd=%zu shift=%zu\n", w[0], r.states.size(), eps.size(),
+                eps[0].rows(), up.size(), sh.size());
     // batched planner (config 4 API)
     BatchPlanner batch(cfg, GpEnsemble{&gp, R}, NominalParams{}, 0.95, 3);
     std::vector<Control> us = batch.plan_step({RobotState{}, RobotState{0.0, 0.1}, RobotState{0.0, -0.1}},
