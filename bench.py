@@ -357,6 +357,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--e2e-ticks", type=int, default=None)
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the sharded (in-library NCCL) path even at one rank")
     ap.add_argument("--dry-run", action="store_true",
                     help="CPU contract check only: fake timings, no GPU, never a result")
     args = ap.parse_args()
@@ -371,8 +373,8 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     if args.gpus > 1 and world == 1 and not args.dry_run:
         sys.exit(spawn_ranks(args))
-    if world > 1 or (args.dry_run and args.gpus > 1):
-        run_sharded(args, w, max(world, args.gpus), rank)
+    if world > 1 or args.sharded or (args.dry_run and args.gpus > 1):
+        run_sharded(args, w, max(world, args.gpus if args.dry_run else world), rank)
         return
 
     e2e_ticks = args.e2e_ticks or max(args.steps, E2E_MIN_TICKS)
@@ -475,6 +477,8 @@ def run_sharded(args, w, world, rank):
     import paper_2411_03289_b200 as G
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
+    if "MASTER_ADDR" not in os.environ:  # --sharded at one rank without torchrun
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()), RANK="0", WORLD_SIZE="1")
     dist.init_process_group("gloo")
     planner, task, x0 = build_planner(w, G)
     uid = [G.nccl_unique_id() if rank == 0 else None]
