@@ -6,7 +6,7 @@ from .gpmppi import (  # noqa: F401
     Edd5Params, GoalSpec, GpEnsemble, GpModel, KernelParams, MppiConfig, NominalDynamic,
     NominalParams, Planner, BatchPlanner, StepDiagnostics, Track, TrackingTask, TrackingWeights,
     UnicycleBaseline, apply_tuple, chi2_quantile_2dof, combine_tuples, flush_l2,
-    kernel_launches, shard_range, tuple_doubles, RolloutResult, rollout, sample_perturbations,
+    kernel_launches, nccl_unique_id, shard_range, tuple_doubles, RolloutResult, rollout, sample_perturbations,
     trajectory_weights, update_controls, shift_horizon, TrainedModels, load_models, save_models)
 from ._capi import (  # noqa: F401
     NOISE_INJECTED, NOISE_PHILOX, VAR_FFMA, VAR_TC_1XTF32, VAR_TC_3XF16, VAR_TC_3XTF32, CudaError)

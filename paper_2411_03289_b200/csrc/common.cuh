@@ -22,7 +22,10 @@ constexpr int kMaxWaypoints = 64;
 constexpr int kMaxObstacles = 64;
 constexpr int kMaxTerrains = 16;
 constexpr int kMaxGroups = 4;
-constexpr int kMaxOutPerGroup = 2 * kMaxTerrains;  // one shared kernel over every terrain (harness.cpp:242-244)
+#ifndef GPM_MAX_OUT_PER_GROUP
+#define GPM_MAX_OUT_PER_GROUP (2 * kMaxTerrains)
+#endif
+constexpr int kMaxOutPerGroup = GPM_MAX_OUT_PER_GROUP;  // one shared kernel over every terrain (harness.cpp:242-244)
 constexpr int kOutChunk = 8;  // outputs whose alpha loads are kept in flight together
 
 enum { TASK_TRACKING = 0, TASK_AVOIDANCE = 1, TASK_COMBINED = 2 };
