@@ -321,6 +321,16 @@ def spawn_ranks(args):
     return subprocess.run(cmd).returncode
 
 
+def _device_mem_used_gb():
+    """Device memory in use (whole GPU, cudaMemGetInfo) after the planner is built and warm."""
+    try:
+        import torch
+        free, total = torch.cuda.mem_get_info(0)
+        return (total - free) / 1e9
+    except Exception:
+        return None
+
+
 def e2e_loop(planner, task, x0, ticks, api, nominal, command_first=False):
     """Closed loop through the public plan_step: x <- step_nominal(x, u) after each tick
     (acceptance.cpp:437-442), L2 flushed between ticks (outside the span)."""
@@ -385,11 +395,13 @@ def main():
         e2e_wall, e2e_cmd, e2e_plan = [1.1] * e2e_ticks, [0.9] * e2e_ticks, [1.0] * e2e_ticks
         cf_wall = [0.95] * e2e_ticks
         h2d, d2h = 2792, 132
+        mem_gb = None
     else:
         import paper_2411_03289_b200 as G
         planner, task, x0 = build_planner(w, G, var_path=args.variance_path)
         for _ in range(args.warmup):
             planner.plan_step(x0, task)
+        mem_gb = _device_mem_used_gb()
         launches0 = G.kernel_launches()
         with ClockSampler(0) as clk:
             tick_ms, phase = planner.bench_device(x0, task, args.steps, flush_l2=True)
@@ -439,7 +451,8 @@ def main():
                    f"obstacles, K={w.samples} T={w.horizon} M={n} R={w.terrains} p_x={w.p_x}",
                    "robots": w.robots, "samples": w.samples, "horizon": w.horizon, "gp_points": n,
                    "parallelism": "single GPU", "l2": "flushed between ticks (2x L2 memset)",
-                   "variance_path": planner.variance_path()},
+                   "variance_path": planner.variance_path(), "device_mem_used_gb": mem_gb,
+                   "philox_noise": os.environ.get("GPMPPI_NOISE_MAT", "auto")},
         "phase_ms": {"rollout": phase[0] / args.steps, "variance": phase[1] / args.steps,
                      "reduce_update": phase[2] / args.steps, "tightening": phase[3] / args.steps},
         "e2e": e2e,

@@ -628,7 +628,6 @@ struct gpmppi_planner {
   int n_obs_max = 0;
   int reduce_blocks = 1;  // per robot
   int T = 0, words = 1;
-  signed char coef_terrain[gpm::kMaxGroups][gpm::kMaxOutPerGroup];
   // device buffers (robot-major, strides in gpm::BatchStrides)
   std::vector<void*> allocs;
   double *d_nom = nullptr, *d_tw = nullptr, *d_x0 = nullptr, *d_rbar = nullptr, *d_margins = nullptr;
@@ -672,6 +671,7 @@ struct gpmppi_planner {
   std::vector<gpmppi_diag> pending_diag;  // [B], completed by wait_tightening
 
   std::vector<void*> sample_allocs;  // per-sample buffers, reallocated by set_shard
+  static constexpr long long kNoiseMatMax = 1LL << 24;  // sample-steps (tuned by the config-5 sweep)
   template <class T>
   T* dalloc(size_t count, std::vector<void*>* owner = nullptr) {
     void* p = nullptr;
@@ -717,6 +717,7 @@ struct gpmppi_planner {
     for (void* q : sample_allocs) CK(cudaFree(q));
     sample_allocs.clear();
     d_eps = nullptr;
+    d_noise = nullptr;
     injected_set = false;
     d_queries = nullptr;
     d_var = nullptr;
@@ -729,7 +730,13 @@ struct gpmppi_planner {
     d_coll = dalloc<uint32_t>((size_t)S * words, o);
     d_term = dalloc<uint8_t>(S, o);
     d_alive = dalloc<uint8_t>(S, o);
-    d_noise = dalloc<double>((size_t)S * T * 2, o);
+    // Philox noise materialised by the rollout for the reduce (16 B per sample-step written +
+    // read) while K*T is moderate; above kNoiseMatMax sample-steps the reduce regenerates it
+    // from the counter instead (no K*T*16-byte round trip through HBM).
+    // GPMPPI_NOISE_MAT=0/1 forces either.
+    static const int mat_env = getenv("GPMPPI_NOISE_MAT") ? atoi(getenv("GPMPPI_NOISE_MAT")) : -1;
+    const bool mat = mat_env >= 0 ? mat_env != 0 : (long long)S * T <= kNoiseMatMax;
+    d_noise = mat ? dalloc<double>((size_t)S * T * 2, o) : nullptr;
     if (model_kind == GPMPPI_MODEL_GP_ENSEMBLE) {
       d_queries = dalloc<float4>((size_t)S * T, o);
       d_var = dalloc<double>((size_t)groups() * S * T, o);
@@ -984,11 +991,10 @@ void enqueue_samples(gpmppi_planner* p, int finish, cudaEvent_t* evs) {
   r.var = gp ? p->d_var : nullptr;
   r.G = gp ? p->groups() : 0;
   r.tw = p->d_tw;
-  std::memcpy(r.coef_terrain, p->coef_terrain, sizeof r.coef_terrain);
   r.x0 = p->d_x0;
   // Philox mode: the rollout materialised the noise, so the reduce reads it like injected noise
   r.noise_mode = p->d_noise && p->noise_mode == gpm::NOISE_PHILOX ? gpm::NOISE_INJECTED : p->noise_mode;
-  r.eps = p->noise_mode == gpm::NOISE_PHILOX ? p->d_noise : p->d_eps;
+  r.eps = p->noise_mode == gpm::NOISE_PHILOX ? p->d_noise : p->d_eps;  // null: regenerated from the counter
   r.sv = a.sv;
   r.sw = a.sw;
   r.costs_out = p->d_costs;
@@ -1083,8 +1089,21 @@ double ms_since(Clock::time_point t0) {
 
 void upload_terrain_weights(gpmppi_planner* p) {
   std::vector<double> w((size_t)p->B * gpm::BatchStrides::TW, 0.0);
-  for (int b = 0; b < p->B; ++b)
-    for (int i = 0; i < p->R; ++i) w[(size_t)b * gpm::BatchStrides::TW + i] = p->tw[(size_t)b * p->R + i];
+  for (int b = 0; b < p->B; ++b) {
+    double* row = &w[(size_t)b * gpm::BatchStrides::TW];
+    for (int i = 0; i < p->R; ++i) row[i] = p->tw[(size_t)b * p->R + i];
+    // variance trace coefficient of each kernel group: Σ over the group's outputs (ascending)
+    // of w(terrain of the output)² -- ensemble_combine's Σ w_i² var (gp.cpp:380-386)
+    for (int g = 0; g < p->groups(); ++g) {
+      const gpm::GroupDev& G = p->model->dev.g[g];
+      double c = 0.0;
+      for (int o = 0; o < G.n_out; ++o) {
+        const double wi = row[G.out_idx[o] >> 1];
+        c = std::fma(wi, wi, c);
+      }
+      row[gpm::BatchStrides::TW_COEF + g] = c;
+    }
+  }
   h2d_sync(p, p->d_tw, w.data(), sizeof(double) * w.size());
 }
 
@@ -1134,10 +1153,6 @@ gpmppi_planner* create_planner(const gpmppi_mppi_config* cfg, const gpmppi_predi
     p->model = pm->kind == GPMPPI_MODEL_GP_ENSEMBLE ? pm->gp : nullptr;
     if (p->model && p->model->device != device) invalid("Planner: GP model lives on another device");
     p->R = pm->kind == GPMPPI_MODEL_GP_ENSEMBLE ? pm->n_terrains : 1;
-    std::memset(p->coef_terrain, -1, sizeof p->coef_terrain);
-    for (int g = 0; g < p->groups(); ++g)
-      for (int o = 0; o < p->model->dev.g[g].n_out && o < gpm::kMaxOutPerGroup; ++o)
-        p->coef_terrain[g][o] = (signed char)(p->model->dev.g[g].out_idx[o] >> 1);
     p->edd5 = {pm->edd5.alpha_l, pm->edd5.alpha_r, pm->edd5.x_icr, pm->edd5.y_icr_l,
                pm->edd5.y_icr_r, pm->track_width};
     p->nom = {nominal->tau_v, nominal->tau_omega, nominal->dt};

@@ -45,7 +45,10 @@ struct BatchStrides {
   // per-robot tick block: x0[0..4], [5] variance weight of the task, [6] Philox key
   // (bit pattern), [7] pad -- one H2D copy stages everything a robot's tick needs
   static constexpr int X0 = 8;
-  static constexpr int TW = kMaxTerrains;         // terrain weights
+  // terrain weights [kMaxTerrains], then the per-group variance coefficients
+  // Σ_o w(o)² over each kernel group's outputs [kMaxGroups] (mppi.cpp:34-49; host-computed)
+  static constexpr int TW = kMaxTerrains + kMaxGroups;
+  static constexpr int TW_COEF = kMaxTerrains;
   static constexpr int OUT = 16;                  // command + diagnostics
   GPM_HD static int nom(int T) { return 2 * T; }
   GPM_HD static int rbar(int T) { return T; }
@@ -107,10 +110,7 @@ struct ReduceArgs {
   const double* cost_mean;  // [B*K_local]
   const double* var;        // [G][B*K_local*T] raw per-group variances (null: no GP)
   int G;
-  const double* tw;         // [B][kMaxTerrains] terrain weights
-  // trace coefficient of group g for robot b: Σ_o tw[b][coef_terrain[g][o]]² over
-  // the group's outputs (mppi.cpp:34-49 combine); -1 ends the list
-  signed char coef_terrain[kMaxGroups][kMaxOutPerGroup];
+  const double* tw;         // [B][TW] terrain weights + per-group trace coefficients (BatchStrides::TW_COEF)
   const double* x0;         // [B][8] robot tick blocks (variance weight, key)
   int noise_mode;
   const double* eps;

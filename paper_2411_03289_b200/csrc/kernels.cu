@@ -996,17 +996,9 @@ __global__ void __launch_bounds__(256, 1) reduce_kernel(const ReduceArgs a) {
   const double* rt = a.x0 + (size_t)b * BatchStrides::X0;
   const double var_w = rt[5];
   const uint64_t key = (uint64_t)__double_as_longlong(rt[6]);
-  double cg[kMaxGroups];
+  double cg[kMaxGroups];  // Σ_o w(o)² of each group's outputs, computed with the weights on the host
 #pragma unroll
-  for (int g = 0; g < kMaxGroups; ++g) {
-    double c = 0.0;
-    if (g < a.G)
-      for (int o = 0; o < kMaxOutPerGroup && a.coef_terrain[g][o] >= 0; ++o) {
-        const double w = a.tw[(size_t)b * BatchStrides::TW + a.coef_terrain[g][o]];
-        c += w * w;
-      }
-    cg[g] = c;
-  }
+  for (int g = 0; g < kMaxGroups; ++g) cg[g] = g < a.G ? a.tw[(size_t)b * BatchStrides::TW + BatchStrides::TW_COEF + g] : 0.0;
   // pass 1: costs (cost_mean + var_w * Σ_k Σ_g coef_g var_g), block min over finite.
   // Per chunk of <= kReduceSlab samples, the trace slab of each group is staged into
   // shared memory by one coalesced sweep (row stride T+1: conflict-free), then every
