@@ -299,6 +299,13 @@ int gpmppi_update_controls(const double* nominal, int T, const double* eps, cons
 /* shift_horizon (mppi.cpp:166-173) */
 int gpmppi_shift_horizon(const double* seq, int T, int device, double* out);
 
+/* select_kernel_grid (gp.cpp:274-366): shared-kernel hyperparameters by the reference's
+ * coarse 5x7x5 LML grid plus one 5x7x5 refinement; every cell's Cholesky and LML on the
+ * device. inputs n x 4, outputs n x m row-major; kernel6 = (sv, l0..l3, nv) of the winner,
+ * best_lml (optional) its summed log marginal likelihood. */
+int gpmppi_select_kernel_grid(const double* inputs, const double* outputs, int64_t n, int64_t m, int device,
+                              double kernel6[6], double* best_lml);
+
 /* ---- the reference's scalar helpers (bindings/module.cpp:40-181), host C++ ----
  * Same arithmetic as the planner's kernels (common.cuh); return GPMPPI_INVALID_ARGUMENT
  * with the reference's message where the reference throws std::invalid_argument. */

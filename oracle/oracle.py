@@ -7,6 +7,7 @@ this module.
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 import subprocess
 
@@ -461,3 +462,55 @@ def make_task(kind, track=None, v_desired=2.0, tracking_weights=(0.1, 1.0, 0.3, 
     t.high_cost = high_cost
     t._keep = (obs, track)
     return t
+
+
+def select_kernel_grid(inputs, outputs):
+    """CPU restatement of select_kernel_grid (gp.cpp:274-366): numpy Cholesky per cell,
+    the reference's sweep order and strict-greater argmax. Returns (sv, lengthscales, nv, lml).
+    Checker for the device grid (tests only)."""
+    X = np.asarray(inputs, dtype=np.float64)
+    Y = np.asarray(outputs, dtype=np.float64)
+    n, m = X.shape[0], Y.shape[1]
+    if n < 2:
+        raise ValueError("select_kernel_grid: need at least 2 points")
+    base = np.maximum(np.sqrt(((X - X.mean(0)) ** 2).sum(0) / (n - 1)), 1e-3)
+    pooled = max(float(sum(((Y[:, j] - Y[:, j].mean()) ** 2).sum() / (n - 1) for j in range(m))) / m,
+                 1e-10)
+    S = X / base
+    sq = (S * S).sum(1)
+    d2 = -2.0 * S @ S.T + sq[:, None] + sq[None, :]
+    d2 = np.maximum(0.5 * (d2 + d2.T), 0.0)
+    log2pi = math.log(2.0 * math.pi)
+
+    def score(sv, scale, nv):
+        K = sv * np.exp(-d2 / (2.0 * scale * scale))
+        K[np.diag_indices(n)] += nv
+        try:
+            L = np.linalg.cholesky(K)
+        except np.linalg.LinAlgError:
+            return -math.inf
+        logdet = float(np.log(np.diag(L)).sum())
+        A = np.linalg.solve(L.T, np.linalg.solve(L, Y))
+        return float(sum(-0.5 * Y[:, j] @ A[:, j] - logdet - 0.5 * n * log2pi for j in range(m)))
+
+    def logspace(lo, hi, k):
+        return [10.0 ** (lo + (hi - lo) * (0.0 if k == 1 else i / (k - 1))) for i in range(k)]
+
+    best = [-math.inf, pooled, 1.0, pooled * 0.1]
+
+    def sweep(svs, ss, nvs):
+        for sv in svs:
+            for s in ss:
+                for nv in nvs:
+                    val = score(sv, s, nv)
+                    if val > best[0]:
+                        best[:] = [val, sv, s, nv]
+
+    sweep([pooled * f for f in logspace(-1.5, 1.5, 5)], logspace(-1.0, 1.0, 7),
+          [pooled * f for f in logspace(-3.0, 0.5, 5)])
+    sv0, s0, nv0 = best[1], best[2], best[3]
+    sweep([sv0 * f for f in logspace(-0.5, 0.5, 5)], [s0 * f for f in logspace(-0.35, 0.35, 7)],
+          [nv0 * f for f in logspace(-0.6, 0.6, 5)])
+    return best[1], tuple(float(b * best[2]) for b in base), best[3], best[0]
+
+

@@ -151,6 +151,7 @@ SIGNATURES = [
     ("gpmppi_trajectory_weights", C.c_int, [_dp, C.c_int64, C.c_double, C.c_int, _dp]),
     ("gpmppi_update_controls", C.c_int, [_dp, C.c_int, _dp, _dp, C.c_int64, _dp, _dp, C.c_int, _dp]),
     ("gpmppi_shift_horizon", C.c_int, [_dp, C.c_int, C.c_int, _dp]),
+    ("gpmppi_select_kernel_grid", C.c_int, [_dp, _dp, C.c_int64, C.c_int64, C.c_int, _dp, _dp]),
     ("gpmppi_wrap_angle", C.c_double, [C.c_double]),
     ("gpmppi_step_nominal", C.c_int, [_dp, _dp, C.POINTER(NominalC), _dp]),
     ("gpmppi_step_kinematic_unicycle", C.c_int, [_dp, _dp, C.c_double, _dp]),

@@ -1905,6 +1905,105 @@ int gpmppi_planner_wait_tightening(gpmppi_planner* p, gpmppi_diag* diag) {
   });
 }
 
+// select_kernel_grid (gp.cpp:274-366): base lengthscales and pooled output variance on the
+// host, every cell's Cholesky + LML on the device (fit.cu), the reference's sweep order and
+// first-strictly-greater argmax across both passes on the host.
+int gpmppi_select_kernel_grid(const double* inputs, const double* outputs, int64_t n64, int64_t m64, int device,
+                              double kernel6[6], double* best_lml) {
+  return guarded([&] {
+    if (!inputs || !outputs || !kernel6) invalid("select_kernel_grid: null argument");
+    if (n64 < 2) invalid("select_kernel_grid: need at least 2 points");
+    if (m64 < 1) invalid("select_kernel_grid: outputs must be n x m with m >= 1");
+    if (n64 > 8192) invalid("select_kernel_grid: n too large for the device grid");
+    const int n = (int)n64, m = (int)m64;
+    require_device(device);
+    double base[4];
+    for (int d = 0; d < 4; ++d) {  // gp.cpp:281-285
+      double mu = 0.0;
+      for (int i = 0; i < n; ++i) mu += inputs[(size_t)i * 4 + d];
+      mu /= n;
+      double var = 0.0;
+      for (int i = 0; i < n; ++i) var += (inputs[(size_t)i * 4 + d] - mu) * (inputs[(size_t)i * 4 + d] - mu);
+      base[d] = std::max(std::sqrt(var / (double)(n - 1)), 1e-3);
+    }
+    double pooled = 0.0;  // gp.cpp:286-291
+    for (int j = 0; j < m; ++j) {
+      double mu = 0.0;
+      for (int i = 0; i < n; ++i) mu += outputs[(size_t)i * m + j];
+      mu /= n;
+      double v = 0.0;
+      for (int i = 0; i < n; ++i) v += (outputs[(size_t)i * m + j] - mu) * (outputs[(size_t)i * m + j] - mu);
+      pooled += v / (double)(n - 1);
+    }
+    pooled = std::max(pooled / (double)m, 1e-10);
+    std::vector<double> sc((size_t)n * 4), sq(n), d2((size_t)n * n);  // gp.cpp:294-299
+    for (int i = 0; i < n; ++i) {
+      double q = 0.0;
+      for (int d = 0; d < 4; ++d) {
+        sc[(size_t)i * 4 + d] = inputs[(size_t)i * 4 + d] / base[d];
+        q += sc[(size_t)i * 4 + d] * sc[(size_t)i * 4 + d];
+      }
+      sq[i] = q;
+    }
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        double dot = 0.0;
+        for (int d = 0; d < 4; ++d) dot += sc[(size_t)i * 4 + d] * sc[(size_t)j * 4 + d];
+        d2[(size_t)i * n + j] = -2.0 * dot + sq[i] + sq[j];
+      }
+    for (int i = 0; i < n; ++i)
+      for (int j = i; j < n; ++j) {
+        const double v = std::max(0.5 * (d2[(size_t)i * n + j] + d2[(size_t)j * n + i]), 0.0);
+        d2[(size_t)i * n + j] = d2[(size_t)j * n + i] = v;
+      }
+    auto logspace = [](double lo, double hi, int k) {
+      std::vector<double> v(k);
+      for (int i = 0; i < k; ++i) v[i] = std::pow(10.0, lo + (hi - lo) * (k == 1 ? 0.0 : (double)i / (k - 1)));
+      return v;
+    };
+    double best = -std::numeric_limits<double>::infinity();
+    double best_sv = pooled, best_s = 1.0, best_nv = pooled * 0.1;
+    auto sweep = [&](const std::vector<double>& svs, const std::vector<double>& ss, const std::vector<double>& nvs) {
+      std::vector<double> cells;
+      for (double sv : svs)
+        for (double s : ss)
+          for (double nv : nvs) {
+            cells.push_back(sv);
+            cells.push_back(s);
+            cells.push_back(nv);
+          }
+      const int nc = (int)(cells.size() / 3);
+      std::vector<double> scores(nc);
+      CK(gpm::device_lml_grid(d2.data(), outputs, n, m, cells.data(), nc, scores.data()));
+      for (int c = 0; c < nc; ++c)  // sweep order, strictly greater (gp.cpp:331-340)
+        if (scores[c] > best) {
+          best = scores[c];
+          best_sv = cells[3 * c];
+          best_s = cells[3 * c + 1];
+          best_nv = cells[3 * c + 2];
+        }
+    };
+    {
+      std::vector<double> svs, nvs;
+      for (double f : logspace(-1.5, 1.5, 5)) svs.push_back(pooled * f);
+      for (double f : logspace(-3.0, 0.5, 5)) nvs.push_back(pooled * f);
+      sweep(svs, logspace(-1.0, 1.0, 7), nvs);
+    }
+    {
+      const double sv0 = best_sv, s0 = best_s, nv0 = best_nv;
+      std::vector<double> svs, ss, nvs;
+      for (double f : logspace(-0.5, 0.5, 5)) svs.push_back(sv0 * f);
+      for (double f : logspace(-0.35, 0.35, 7)) ss.push_back(s0 * f);
+      for (double f : logspace(-0.6, 0.6, 5)) nvs.push_back(nv0 * f);
+      sweep(svs, ss, nvs);
+    }
+    kernel6[0] = best_sv;
+    for (int d = 0; d < 4; ++d) kernel6[1 + d] = base[d] * best_s;
+    kernel6[5] = best_nv;
+    if (best_lml) *best_lml = best;
+  });
+}
+
 int gpmppi_combine_tuples_host(const double* tuples, int n_ranks, int horizon, double lambda,
                                double* out) {
   if (!tuples || !out || n_ranks < 1 || horizon < 1 || !(lambda > 0.0))

@@ -158,3 +158,204 @@ done:
 }
 
 }  // namespace gpm
+
+// ---------------------------------------------------------------------------
+// Hyperparameter grid (select_kernel_grid, gp.cpp:274-366) on the device: every grid
+// cell (signal_var, shared scale, noise_var) is one CTA that builds its kernel matrix
+// K = sv·exp(-d2 / 2s²) + nv·I from the shared scaled squared distances, factors it
+// (blocked left-looking Cholesky, 32-column panels; failure = a pivot not > 0, as
+// Eigen's LLT) and scores the summed log marginal likelihood
+//   Σ_j -½ y_jᵀ K⁻¹ y_j - Σ log L_ii - ½ n log 2π,  y_jᵀ K⁻¹ y_j = ‖L⁻¹ y_j‖²
+// (one forward solve per output). Load-time work, FP64 throughout; the cell order and
+// the first-strictly-greater argmax stay on the host as in the reference.
+namespace {
+
+constexpr int GB = 32;   // panel width
+constexpr int GK = 64;   // k-chunk of the panel update staged in shared memory
+
+__global__ void __launch_bounds__(256, 1) lml_grid_kernel(const double* __restrict__ d2, const double* __restrict__ yc,
+                                                          int n, int m, const double* __restrict__ cells,
+                                                          double* __restrict__ work, double* __restrict__ score) {
+  __shared__ double bt[GB][GK + 1];  // panel rows' k-chunk (the 32 pivot rows of block J)
+  __shared__ double dblk[GB][GB + 1];
+  __shared__ int fail;
+  __shared__ double red[8];
+  const int cell = blockIdx.x;
+  const double sv = cells[3 * cell], s = cells[3 * cell + 1], nv = cells[3 * cell + 2];
+  const double cexp = -1.0 / (2.0 * s * s);
+  double* M = work + (size_t)cell * n * n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // K, lower triangle (gp.cpp:304-305): sv * exp(-d2 / (2 s^2)), + nv on the diagonal
+  for (size_t idx = tid; idx < (size_t)n * n; idx += blockDim.x) {
+    const int i = (int)(idx / n), j = (int)(idx % n);
+    if (j <= i) M[idx] = sv * exp(d2[idx] * cexp) + (i == j ? nv : 0.0);
+  }
+  if (tid == 0) fail = 0;
+  __syncthreads();
+  for (int j0 = 0; j0 < n; j0 += GB) {
+    const int w = min(GB, n - j0);
+    // (a) panel update: M[i][j0 + c] -= Σ_{k < j0} M[i][k] M[j0 + c][k], rows i >= j0
+    //     lane = panel column c, warps stride the rows; pivot rows staged per k-chunk
+    double acc[8];  // rows warp + 8 r of this pass
+    for (int ib = j0; ib < n; ib += 64) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r) acc[r] = 0.0;
+      for (int k0 = 0; k0 < j0; k0 += GK) {
+        const int kw = min(GK, j0 - k0);
+        __syncthreads();
+        for (int t = tid; t < GB * GK; t += blockDim.x) {
+          const int c = t / GK, k = t % GK;
+          bt[c][k] = (c < w && k < kw) ? M[(size_t)(j0 + c) * n + k0 + k] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const int i = ib + warp + 8 * r;
+          if (i < n) {
+            const double* mi = M + (size_t)i * n + k0;
+            double a = acc[r];
+            for (int k = 0; k < kw; ++k) a = fma(mi[k], bt[lane][k], a);  // mi[k]: one broadcast load per warp
+            acc[r] = a;
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int i = ib + warp + 8 * r;
+        if (i < n && lane < w && j0 + lane <= i) M[(size_t)i * n + j0 + lane] -= acc[r];
+      }
+    }
+    __syncthreads();
+    // (b) diagonal block: unblocked Cholesky by warp 0 (lane = row)
+    for (int t = tid; t < GB * GB; t += blockDim.x) {
+      const int r = t / GB, c = t % GB;
+      dblk[r][c] = (r < w && c <= r) ? M[(size_t)(j0 + r) * n + j0 + c] : 0.0;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      for (int c = 0; c < w; ++c) {
+        double p = dblk[c][c];
+        for (int k = 0; k < c; ++k) p -= dblk[c][k] * dblk[c][k];
+        if (!(p > 0.0)) {
+          if (lane == 0) fail = 1;
+          break;
+        }
+        const double d = sqrt(p);
+        if (lane > c && lane < w) {
+          double v = dblk[lane][c];
+          for (int k = 0; k < c; ++k) v -= dblk[lane][k] * dblk[c][k];
+          dblk[lane][c] = v / d;
+        }
+        __syncwarp();
+        if (lane == 0) dblk[c][c] = d;
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    if (fail) break;
+    for (int t = tid; t < GB * GB; t += blockDim.x) {
+      const int r = t / GB, c = t % GB;
+      if (r < w && c <= r) M[(size_t)(j0 + r) * n + j0 + c] = dblk[r][c];
+    }
+    // (c) rows below the block: L[i][j0 + c] = (M[i][j0 + c] - Σ_{k<c} L[i][j0+k] D[c][k]) / D[c][c]
+    for (int i = j0 + w + warp; i < n; i += 8) {
+      double x = lane < w ? M[(size_t)i * n + j0 + lane] : 0.0;
+      for (int c = 0; c < w; ++c) {
+        const double xc = __shfl_sync(0xffffffffu, x / dblk[c][c], c);
+        if (lane == c) x = xc;
+        if (lane > c) x -= xc * dblk[lane][c];
+      }
+      if (lane < w) M[(size_t)i * n + j0 + lane] = x;
+    }
+    __syncthreads();
+  }
+  if (fail) {
+    if (tid == 0) score[cell] = -INFINITY;
+    return;
+  }
+  // logdet = Σ log L_ii (gp.cpp:307)
+  double ld = 0.0;
+  for (int i = tid; i < n; i += blockDim.x) ld += log(M[(size_t)i * n + i]);
+  for (int o = 16; o; o >>= 1) ld += __shfl_xor_sync(0xffffffffu, ld, o);
+  if (lane == 0) red[warp] = ld;
+  __syncthreads();
+  double logdet = 0.0;
+  for (int q = 0; q < 8; ++q) logdet += red[q];
+  __syncthreads();
+  // forward solves, one warp per output: z = L^{-1} y_j, quad_j = ‖z‖² (written over y's slot)
+  extern __shared__ double zbuf[];  // [8][n]
+  double* z = zbuf + (size_t)warp * n;
+  double quad_sum = 0.0;
+  for (int j = warp; j < m; j += 8) {
+    const double* y = yc + (size_t)j * n;
+    double q = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const double* li = M + (size_t)i * n;
+      double sdot = 0.0;
+      for (int k = lane; k < i; k += 32) sdot = fma(li[k], z[k], sdot);
+      for (int o = 16; o; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
+      const double zi = (y[i] - sdot) / li[i];
+      if (lane == 0) z[i] = zi;
+      q = fma(zi, zi, q);
+      __syncwarp();
+    }
+    quad_sum += q;
+  }
+  if (lane == 0) red[warp] = quad_sum;
+  __syncthreads();
+  if (tid == 0) {
+    double qs = 0.0;
+    for (int q = 0; q < 8; ++q) qs += red[q];
+    const double log2pi = log(2.0 * gpm::kPi);
+    score[cell] = -0.5 * qs - (double)m * logdet - 0.5 * (double)m * (double)n * log2pi;
+  }
+}
+
+}  // namespace
+
+namespace gpm {
+
+// Scores of the given cells ((sv, s, nv) triples) for scaled squared distances d2 (n x n,
+// host) and outputs Y (n x m, row-major, host). -inf marks a failed factorisation.
+cudaError_t device_lml_grid(const double* d2, const double* Y, int n, int m, const double* cells, int n_cells,
+                            double* scores) {
+  double *dd2 = nullptr, *dy = nullptr, *dc = nullptr, *dw = nullptr, *ds = nullptr;
+  cudaStream_t st = nullptr;
+  cudaError_t e = cudaSuccess;
+  std::vector<double> yc((size_t)n * m);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < m; ++j) yc[(size_t)j * n + i] = Y[(size_t)i * m + j];
+  const size_t smem = sizeof(double) * 8 * (size_t)n;
+#define GRID_CK(call)                  \
+  do {                                 \
+    if ((e = (call)) != cudaSuccess) { \
+      goto done;                       \
+    }                                  \
+  } while (0)
+  GRID_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  GRID_CK(cudaMalloc(&dd2, sizeof(double) * (size_t)n * n));
+  GRID_CK(cudaMalloc(&dy, sizeof(double) * yc.size()));
+  GRID_CK(cudaMalloc(&dc, sizeof(double) * 3 * (size_t)n_cells));
+  GRID_CK(cudaMalloc(&dw, sizeof(double) * (size_t)n * n * n_cells));
+  GRID_CK(cudaMalloc(&ds, sizeof(double) * (size_t)n_cells));
+  GRID_CK(cudaMemcpyAsync(dd2, d2, sizeof(double) * (size_t)n * n, cudaMemcpyHostToDevice, st));
+  GRID_CK(cudaMemcpyAsync(dy, yc.data(), sizeof(double) * yc.size(), cudaMemcpyHostToDevice, st));
+  GRID_CK(cudaMemcpyAsync(dc, cells, sizeof(double) * 3 * (size_t)n_cells, cudaMemcpyHostToDevice, st));
+  GRID_CK(cudaFuncSetAttribute(lml_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  lml_grid_kernel<<<n_cells, 256, smem, st>>>(dd2, dy, n, m, dc, dw, ds);
+  count_launch();
+  GRID_CK(cudaGetLastError());
+  GRID_CK(cudaMemcpyAsync(scores, ds, sizeof(double) * (size_t)n_cells, cudaMemcpyDeviceToHost, st));
+  GRID_CK(cudaStreamSynchronize(st));
+#undef GRID_CK
+done:
+  cudaFree(dd2);
+  cudaFree(dy);
+  cudaFree(dc);
+  cudaFree(dw);
+  cudaFree(ds);
+  if (st) cudaStreamDestroy(st);
+  return e;
+}
+
+}  // namespace gpm

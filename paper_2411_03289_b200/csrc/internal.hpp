@@ -209,5 +209,8 @@ void count_launch(int n = 1);
 cudaError_t device_factor(const double* K, int n, double noise_var, double* L_out, double* X_out,
                           double* jitter_out, bool* ok);
 unsigned long long launches_total();
+// fit.cu: summed LML of each hyperparameter grid cell (sv, s, nv) on the device (-inf: LLT failed)
+cudaError_t device_lml_grid(const double* d2, const double* Y, int n, int m, const double* cells, int n_cells,
+                            double* scores);
 
 }  // namespace gpm

@@ -11,7 +11,7 @@ Follows, function by function:
   TerrainProfile / step_true_terrain     dynamics.hpp:23-34, dynamics.cpp:129-139
   default_terrains                       config.cpp:116-124
   generate_training_data                 dynamics.cpp:141-170
-  select_kernel_grid                     gp.cpp:274-366
+  select_kernel_grid                     gp.cpp:274-366 (cells scored on the device)
   train_models (GP part)                 harness.cpp:190-243
   HistoryBuffer                          terrain.cpp:10-70
   project_simplex                        terrain.cpp:72-92
@@ -213,53 +213,18 @@ def generate_training_data(profile: TerrainProfile, nominal: G.NominalParams,
 
 
 # ----------------------------------------------------------------- GP hyperparameters
-def select_kernel_grid(inputs, outputs) -> G.KernelParams:
-    """Shared-kernel LML grid search, coarse 5x7x5 then a 5x7x5 refinement (gp.cpp:274-366).
-    Load-time host work (numpy Cholesky), not on the per-tick path."""
-    X = np.asarray(inputs, dtype=np.float64)
-    Y = np.asarray(outputs, dtype=np.float64)
-    n, m = X.shape[0], Y.shape[1]
-    if n < 2:
-        raise ValueError("select_kernel_grid: need at least 2 points")
-    base = np.maximum(np.sqrt(((X - X.mean(0)) ** 2).sum(0) / (n - 1)), 1e-3)
-    pooled = max(float(sum(((Y[:, j] - Y[:, j].mean()) ** 2).sum() / (n - 1) for j in range(m))) / m,
-                 1e-10)
-    S = X / base
-    sq = (S * S).sum(1)
-    d2 = -2.0 * S @ S.T + sq[:, None] + sq[None, :]
-    d2 = np.maximum(0.5 * (d2 + d2.T), 0.0)
-    log2pi = math.log(2.0 * math.pi)
-
-    def score(sv, scale, nv):
-        K = sv * np.exp(-d2 / (2.0 * scale * scale))
-        K[np.diag_indices(n)] += nv
-        try:
-            L = np.linalg.cholesky(K)
-        except np.linalg.LinAlgError:
-            return -math.inf
-        logdet = float(np.log(np.diag(L)).sum())
-        A = np.linalg.solve(L.T, np.linalg.solve(L, Y))
-        return float(sum(-0.5 * Y[:, j] @ A[:, j] - logdet - 0.5 * n * log2pi for j in range(m)))
-
-    def logspace(lo, hi, k):
-        return [10.0 ** (lo + (hi - lo) * (0.0 if k == 1 else i / (k - 1))) for i in range(k)]
-
-    best = [-math.inf, pooled, 1.0, pooled * 0.1]
-
-    def sweep(svs, ss, nvs):
-        for sv in svs:
-            for s in ss:
-                for nv in nvs:
-                    val = score(sv, s, nv)
-                    if val > best[0]:
-                        best[:] = [val, sv, s, nv]
-
-    sweep([pooled * f for f in logspace(-1.5, 1.5, 5)], logspace(-1.0, 1.0, 7),
-          [pooled * f for f in logspace(-3.0, 0.5, 5)])
-    sv0, s0, nv0 = best[1], best[2], best[3]
-    sweep([sv0 * f for f in logspace(-0.5, 0.5, 5)], [s0 * f for f in logspace(-0.35, 0.35, 7)],
-          [nv0 * f for f in logspace(-0.6, 0.6, 5)])
-    return G.KernelParams(best[1], tuple(float(b * best[2]) for b in base), best[3])
+def select_kernel_grid(inputs, outputs, device: int = 0) -> G.KernelParams:
+    """Shared-kernel LML grid search, coarse 5x7x5 then a 5x7x5 refinement (gp.cpp:274-366):
+    every cell's Cholesky and LML on the device (gpmppi_select_kernel_grid, csrc/fit.cu)."""
+    X = np.ascontiguousarray(inputs, dtype=np.float64)
+    Y = np.ascontiguousarray(outputs, dtype=np.float64)
+    if X.ndim != 2 or X.shape[1] != 4 or Y.ndim != 2 or Y.shape[0] != X.shape[0]:
+        raise ValueError("select_kernel_grid: inputs n x 4 and outputs n x m required")
+    k = np.empty(6)
+    from . import _capi as A
+    A.check(A.lib().gpmppi_select_kernel_grid(A.dptr(X), A.dptr(Y), X.shape[0], Y.shape[1], device,
+                                              A.dptr(k), None))
+    return G.KernelParams(float(k[0]), tuple(float(v) for v in k[1:5]), float(k[5]))
 
 
 @dataclass
