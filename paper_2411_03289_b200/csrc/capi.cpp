@@ -671,7 +671,7 @@ struct gpmppi_planner {
   std::vector<gpmppi_diag> pending_diag;  // [B], completed by wait_tightening
 
   std::vector<void*> sample_allocs;  // per-sample buffers, reallocated by set_shard
-  static constexpr long long kNoiseMatMax = 1LL << 24;  // sample-steps (tuned by the config-5 sweep)
+  static constexpr long long kNoiseMatMax = 1LL << 31;  // sample-steps (config-5 sweep: materialise always)
   template <class T>
   T* dalloc(size_t count, std::vector<void*>* owner = nullptr) {
     void* p = nullptr;
@@ -731,9 +731,10 @@ struct gpmppi_planner {
     d_term = dalloc<uint8_t>(S, o);
     d_alive = dalloc<uint8_t>(S, o);
     // Philox noise materialised by the rollout for the reduce (16 B per sample-step written +
-    // read) while K*T is moderate; above kNoiseMatMax sample-steps the reduce regenerates it
-    // from the counter instead (no K*T*16-byte round trip through HBM).
-    // GPMPPI_NOISE_MAT=0/1 forces either.
+    // read) up to kNoiseMatMax sample-steps, else regenerated from the counter in the reduce.
+    // Measured (profiles/r02/config5_sweep.md): the FP64 Box-Muller regeneration costs more
+    // than the HBM round trip at every K up to 4M (reduce 4.46 vs 2.13 ms at K = 4M), so the
+    // bound is the 2^31 sample-step planner limit. GPMPPI_NOISE_MAT=0/1 forces either.
     static const int mat_env = getenv("GPMPPI_NOISE_MAT") ? atoi(getenv("GPMPPI_NOISE_MAT")) : -1;
     const bool mat = mat_env >= 0 ? mat_env != 0 : (long long)S * T <= kNoiseMatMax;
     d_noise = mat ? dalloc<double>((size_t)S * T * 2, o) : nullptr;
