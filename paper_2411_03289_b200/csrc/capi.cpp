@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -24,6 +25,13 @@
 #include "internal.hpp"
 
 namespace {
+
+// NVTX ranges (header-only NVTX3: free when no tool is attached) around the host phases of
+// a tick and the enqueue of each device phase, for nsys / ncu --nvtx.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 thread_local std::string g_err;
 
@@ -874,6 +882,7 @@ void finish_pending(gpmppi_planner* p, gpmppi_diag* diag);
 // mppi.cpp:235-248 ensure_thresholds + the per-tick staging of every robot's state,
 // task, variance weight and Philox key into pinned memory (enqueue_h2d copies them).
 void stage_tick(gpmppi_planner* p, const double* x0, const gpmppi_task* tasks) {
+  NvtxRange nv("gpmppi:stage tick");
   if (!x0 || !tasks) invalid("plan_step: null state or task");
   const int T = p->T;
   for (int b = 0; b < p->B; ++b) {
@@ -925,6 +934,7 @@ void enqueue_h2d(gpmppi_planner* p) {
 // Rollout + variance + reduce for every robot's sample range. finish=1 also
 // applies the update (single-rank solve).
 void enqueue_samples(gpmppi_planner* p, int finish, cudaEvent_t* evs) {
+  NvtxRange nv("gpmppi:enqueue rollout+variance+reduce");
   const int T = p->T;
   gpm::RolloutArgs a{};
   if (p->model) a.model = p->model->dev;
@@ -1035,6 +1045,7 @@ void enqueue_update(gpmppi_planner* p, cudaEvent_t* evs) {
 }
 
 void enqueue_tighten(gpmppi_planner* p) {
+  NvtxRange nv("gpmppi:enqueue tightening");
   gpm::TightenArgs t{};
   if (p->model) t.model = p->model->dev;
   t.model_kind = p->model_kind;
@@ -1281,6 +1292,7 @@ void capture_tick(gpmppi_planner* p, long long key) {
 void plan_tick(gpmppi_planner* p, const double* x0, const gpmppi_task* tasks, double* command,
                gpmppi_diag* diag) {
   const auto t0 = Clock::now();  // mppi.cpp:391
+  NvtxRange nv("gpmppi:plan_step");
   CK(cudaSetDevice(p->device));
   if (!command) invalid("plan_step: null command output");
   if (p->K_local != p->K_total && !p->comm)
@@ -1298,7 +1310,10 @@ void plan_tick(gpmppi_planner* p, const double* x0, const gpmppi_task* tasks, do
     enqueue_tick(p, false);
   }
   const double t_launch = ms_since(t0);
-  CK(cudaEventSynchronize(p->ev[0]));
+  {
+    NvtxRange wait("gpmppi:wait command");
+    CK(cudaEventSynchronize(p->ev[0]));
+  }
   const double t_cmd = ms_since(t0);
   if (p->command_first) {
     // command and diagnostics are on the host; the tightening (next tick's thresholds)
@@ -1313,7 +1328,10 @@ void plan_tick(gpmppi_planner* p, const double* x0, const gpmppi_task* tasks, do
       for (int b = 0; b < p->B; ++b) diag[b] = p->pending_diag[b];
     p->tightening_pending = true;
   } else {
-    CK(cudaStreamSynchronize(p->stream));
+    {
+      NvtxRange wait("gpmppi:wait tightening");
+      CK(cudaStreamSynchronize(p->stream));
+    }
     fill_diag(p, command, diag, t_cmd, ms_since(t0));
   }
   ++p->tick;  // mppi.cpp:460

@@ -53,7 +53,8 @@ __constant__ double kExp2Frac[32] = {
     0x1.d5818dcfba487p+0, 0x1.dfc97337b9b5fp+0, 0x1.ea4afa2a490dap+0, 0x1.f50765b6e4540p+0};
 
 // -------------------------------------------------------------------------
-// Rollout, GP ensemble model. NO = max outputs per kernel group (compile time).
+// Rollout, GP ensemble model (terrain-combined alpha: two sums per kernel group whatever the
+// output count). LPS lanes per sample group, SPG samples per group (compile time).
 size_t rollout_smem_bytes(const RolloutArgs& a) {
   size_t b = sizeof(TaskDev);
   b += sizeof(double) * (size_t)(2 * a.T + a.T + a.T * (a.n_obs_max > 0 ? a.n_obs_max : 1) + a.R + 2 + 32);
@@ -358,7 +359,7 @@ GPM_D void rollout_phase2(const RolloutArgs& a, const SmemView& sv, const TaskDe
 #endif
 }
 
-template <int NO, int LPS, int SPG>
+template <int LPS, int SPG>
 __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const RolloutArgs a) {
   pdl_trigger();  // single wave: the variance grid may be scheduled (it waits for this grid)
   extern __shared__ __align__(16) unsigned char smem[];
@@ -724,8 +725,6 @@ cudaError_t launch_rollout(const RolloutArgs& a, int num_sms, cudaStream_t st) {
   const size_t smem = rollout_smem_bytes(a);
   if (a.K_local <= 0 || a.B <= 0) return cudaSuccess;
   if (a.model_kind == MODEL_GP) {
-    int no = 0;
-    for (int g = 0; g < a.model.G; ++g) no = a.model.g[g].n_out > no ? a.model.g[g].n_out : no;
     int lps = 8, threads = 32, spg = 1;
     int spb = rollout_samples_per_block(a.K_local, a.B, num_sms, &lps, &threads, &spg);
     size_t smem_u = smem + sizeof(double2) * (size_t)(threads / lps) * spg * a.T;  // + control buffers
@@ -746,18 +745,12 @@ cudaError_t launch_rollout(const RolloutArgs& a, int num_sms, cudaStream_t st) {
     const long long cap = (long long)GPM_ROLLOUT_MINB * num_sms;
     const long long blocks = items < cap ? items : cap;
     using KF = void (*)(const RolloutArgs);
-#define GPM_ROW(NO, S) \
-  {rollout_gp_kernel<NO, 4, 1>, rollout_gp_kernel<NO, 8, S>, rollout_gp_kernel<NO, 16, S>, rollout_gp_kernel<NO, 32, S>}
-    KF table[2][4][4] = {{GPM_ROW(2, 1), GPM_ROW(4, 1), GPM_ROW(6, 1), GPM_ROW(8, 1)},
-                         {GPM_ROW(2, 2), GPM_ROW(4, 2), GPM_ROW(6, 2), GPM_ROW(8, 2)}};
-#undef GPM_ROW
-    // one 32-lane group per warp carrying four samples: no duplicate addresses inside a
-    // warp's Z/alpha loads, a quarter of the LDS instructions of the 8-lane layout
-    KF table4[4] = {rollout_gp_kernel<2, 32, 4>, rollout_gp_kernel<4, 32, 4>, rollout_gp_kernel<6, 32, 4>,
-                    rollout_gp_kernel<8, 32, 4>};
-    const int ni = no <= 2 ? 0 : no <= 4 ? 1 : no <= 6 ? 2 : 3;
+    KF table[2][4] = {{rollout_gp_kernel<4, 1>, rollout_gp_kernel<8, 1>, rollout_gp_kernel<16, 1>, rollout_gp_kernel<32, 1>},
+                      {rollout_gp_kernel<4, 1>, rollout_gp_kernel<8, 2>, rollout_gp_kernel<16, 2>, rollout_gp_kernel<32, 2>}};
     const int li = lps == 4 ? 0 : lps == 8 ? 1 : lps == 16 ? 2 : 3;
-    KF kern = spg == 4 ? table4[ni] : table[spg == 2 ? 1 : 0][ni][li];
+    // spg 4: one 32-lane group per warp carrying four samples (no duplicate addresses inside
+    // a warp's Z/alpha loads, a quarter of the LDS instructions of the 8-lane layout)
+    KF kern = spg == 4 ? rollout_gp_kernel<32, 4> : table[spg == 2 ? 1 : 0][li];
     static int scr_env = -1;  // GPMPPI_SCR_GLOBAL=1 keeps the trajectory scratch in global memory
     if (scr_env < 0) {
       const char* e = getenv("GPMPPI_SCR_GLOBAL");
