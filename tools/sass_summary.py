@@ -33,7 +33,11 @@ for line in out.splitlines():
 
 def short(name):
     d = subprocess.run(["c++filt", name], capture_output=True, text=True).stdout.strip()
-    return re.sub(r"\(.*", "", d)
+    d = re.sub(r"\(.*", "", d)
+    if not d:  # anonymous-namespace kernels (fit.cu): keep the plain name
+        m = re.search(r"\d+([a-z_]+_[a-z_]+)E", name)
+        d = "(fit.cu) " + (m.group(1) if m else name)
+    return d
 
 
 print("| kernel | " + " | ".join(OPS) + " | total |")
