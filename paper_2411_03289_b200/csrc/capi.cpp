@@ -641,6 +641,9 @@ struct gpmppi_planner {
   double *d_nom = nullptr, *d_tw = nullptr, *d_x0 = nullptr, *d_rbar = nullptr, *d_margins = nullptr;
   double* d_eps = nullptr;
   double* d_noise = nullptr;  // Philox noise drawn by the rollout, read back by the reduce [B][K][T][2]
+  gpm::RolloutGeom geom{};    // GP rollout geometry (query layout), fixed per sample-buffer set
+  long long q_slots = 0;      // item-major query / trace slots (gpm::query_slots)
+  unsigned long long* d_progress = nullptr;  // per lane group: query steps published (concurrent variance)
   gpm::TaskDev* d_task = nullptr;
   double *d_cost_mean = nullptr, *d_var = nullptr, *d_costs = nullptr, *d_e = nullptr;
   float4* d_queries = nullptr;
@@ -747,8 +750,11 @@ struct gpmppi_planner {
     const bool mat = mat_env >= 0 ? mat_env != 0 : (long long)S * T <= kNoiseMatMax;
     d_noise = mat ? dalloc<double>((size_t)S * T * 2, o) : nullptr;
     if (model_kind == GPMPPI_MODEL_GP_ENSEMBLE) {
-      d_queries = dalloc<float4>((size_t)S * T, o);
-      d_var = dalloc<double>((size_t)groups() * S * T, o);
+      geom = gpm::rollout_geometry((int)K_local, B, T, model->n, groups(), num_sms);
+      q_slots = gpm::query_slots(geom, B, T);  // item-major, padded to whole items
+      d_queries = dalloc<float4>((size_t)q_slots, o);
+      d_var = dalloc<double>((size_t)groups() * q_slots, o);
+      d_progress = dalloc<unsigned long long>((size_t)B * geom.chunks * (geom.threads / geom.lps), o);
       if (!d_scratch) d_scratch = dalloc<double>(gpm::rollout_scratch_doubles(T, num_sms));
     }
     reduce_blocks = gpm::reduce_blocks_for((int)K_local, B, num_sms, T);
@@ -971,11 +977,13 @@ void enqueue_samples(gpmppi_planner* p, int finish, cudaEvent_t* evs) {
   a.alive = p->d_alive;
   a.words = p->words;
   a.scratch = p->d_scratch;
+  a.geom = p->geom;
+  a.progress = nullptr;
   if (evs) CK(cudaEventRecord(evs[0], p->stream));
   check(gpm::launch_rollout(a, p->num_sms, p->stream), "rollout kernel");
   if (evs) CK(cudaEventRecord(evs[1], p->stream));
   const bool gp = p->model_kind == GPMPPI_MODEL_GP_ENSEMBLE;
-  const long long KT = p->slots() * T;
+  const long long KT = p->q_slots;  // item-major query / trace slots
   if (gp) {
     for (int g = 0; g < p->groups(); ++g) {  // raw variances; the reduce applies Σ w² per robot
       gpm::VarianceArgs v{};
@@ -991,6 +999,7 @@ void enqueue_samples(gpmppi_planner* p, int finish, cudaEvent_t* evs) {
   }
   if (evs) CK(cudaEventRecord(evs[2], p->stream));
   gpm::ReduceArgs r{};
+  r.geom = p->geom;
   r.B = p->B;
   r.K_local = (int)p->K_local;
   r.K_total = p->K_total;

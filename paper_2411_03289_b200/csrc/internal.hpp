@@ -55,6 +55,22 @@ struct BatchStrides {
   GPM_HD static int marg(int T) { return T * kMaxObstacles; }  // [T][n_obs] inside
 };
 
+// Lane-group geometry of the GP rollout, fixed per planner (rollout_geometry): LPS lanes
+// per sample group, SPG samples per group, `threads` per block, spb samples per work item
+// (one block's chunk of one robot), chunks = items per robot.
+struct RolloutGeom {
+  int lps, spg, threads, spb, chunks;
+};
+// Query / variance-trace slot of (robot-major sample slot sl, step k): item-major, so the
+// block working on an item writes its step-k queries contiguously ([item][k][spb]) and the
+// variance tiles of early steps are complete while the chains are still running.
+GPM_HD long long query_slot(long long sl, int k, int K_local, int T, int spb, int chunks) {
+  const long long b = sl / K_local;
+  const int ls = (int)(sl - b * K_local);
+  const long long item = b * chunks + ls / spb;
+  return (item * T + k) * spb + ls % spb;
+}
+
 struct RolloutArgs {
   ModelDev model;
   int model_kind;
@@ -87,6 +103,9 @@ struct RolloutArgs {
   int words;  // ceil(T/32)
   double* scratch;  // per lane-group trajectory scratch (rollout_scratch_doubles)
   int scratch_smem;  // set by launch_rollout: the trajectory scratch fits in shared memory (after ubuf)
+  RolloutGeom geom;  // rollout_geometry of the planner (query layout, query_slot)
+  unsigned long long* progress;  // [items * groups per block]: steps whose queries a group has
+                                 // written (release), read by the concurrent variance kernel; null: off
 };
 
 struct VarianceArgs {
@@ -100,6 +119,7 @@ struct VarianceArgs {
 };
 
 struct ReduceArgs {
+  RolloutGeom geom;  // the trace is in query_slot order
   int B;
   int K_local;
   long long K_total;
@@ -169,6 +189,16 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 #if defined(__CUDACC__)
+// release / acquire at GPU scope: the rollout publishes how many steps of queries a lane
+// group has written; the concurrent variance kernel acquires before reading them
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 #endif
@@ -180,7 +210,9 @@ cudaError_t launch_reduce(const ReduceArgs& a, int blocks, cudaStream_t st);
 cudaError_t launch_finish(const double* tuples, int n, int T, double lambda, double* nominal_seq,
                           const double lo[2], const double hi[2], double* out, long long K_total,
                           double* combined, cudaStream_t st);
-int rollout_samples_per_block(int K_local, int B, int num_sms, int* lps, int* threads, int* spg);
+RolloutGeom rollout_geometry(int K_local, int B, int T, int n_pts, int G, int num_sms);
+// slots of the item-major query / trace arrays (>= B*K_local*T: the last chunk of a robot is padded)
+GPM_HD long long query_slots(const RolloutGeom& g, int B, int T) { return (long long)B * g.chunks * T * g.spb; }
 cudaError_t launch_tighten(const TightenArgs& a, cudaStream_t st);
 cudaError_t launch_predict(const ModelDev& m, const double* q, long long S, double* mean,
                            double* var, cudaStream_t st);

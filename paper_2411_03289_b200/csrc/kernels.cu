@@ -398,8 +398,8 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
   const double av = a.nom.dt / a.nom.tau_v, aw = a.nom.dt / a.nom.tau_omega;
   // work items: (robot, chunk of groups_per_block*SPG samples); every lane of the block
   // runs the same item sequence (samples beyond K are masked, never early-exit)
-  const int spb = groups_per_block * SPG;
-  const int chunks = (a.K_local + spb - 1) / spb;
+  const int spb = groups_per_block * SPG;  // == a.geom.spb
+  const int chunks = a.geom.chunks;
   const long long items = (long long)a.B * chunks;
   int loaded = -1;
 
@@ -490,9 +490,12 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
         const double2 u = ubuf[j * T + k];
         u0[j] = u.x;
         u1[j] = u.y;
-        if (valid[j] && gl == 0)
-          a.queries[(size_t)sl[j] * T + k] = make_float4((float)v[j], (float)w[j], (float)u0[j], (float)u1[j]);
+        if (valid[j] && gl == 0)  // item-major slot: (item, k, sample within the item)
+          a.queries[(size_t)((item * T + k) * spb + ls0 + j - (item % chunks) * spb)] =
+              make_float4((float)v[j], (float)w[j], (float)u0[j], (float)u1[j]);
       }
+      if (a.progress && gl == 0)  // steps < k+1 of this group's queries are published
+        st_release_u64(a.progress + (size_t)item * groups_per_block + gib, (unsigned long long)(k + 1));
       double cm0[SPG], cm1[SPG];  // combine_terrains (mppi.cpp:34-49)
 #pragma unroll
       for (int j = 0; j < SPG; ++j) cm0[j] = cm1[j] = 0.0;
@@ -705,41 +708,46 @@ size_t rollout_scratch_doubles(int T, int num_sms) {
   return (size_t)GPM_ROLLOUT_MINB * num_sms * kMaxSampleSlotsPerBlock * SCR_ARRAYS * (size_t)(T + 1);
 }
 
-// samples per block for the GP rollout: spread one robot's samples over every SM in a
-// single wave when possible (one block per SM)
-int rollout_samples_per_block(int K_local, int B, int num_sms, int* lps_out, int* threads_out, int* spg_out) {
+// Geometry of the GP rollout: spread all robots' samples over every SM in a single wave
+// when possible (one block per SM); wider lane groups when n*T leaves no room for the
+// control buffers (the shared-memory estimate assumes the maximum obstacle count, so the
+// geometry -- and with it the query layout -- is fixed for the planner's lifetime).
+RolloutGeom rollout_geometry(int K_local, int B, int T, int n_pts, int G, int num_sms) {
   const long long total = (long long)K_local * B;
   int lps = 8, spg = 1;
   rollout_layout(total, num_sms, &lps, &spg);
-  const int spw = 32 / lps * spg;
-  const long long warps = (total + spw - 1) / spw;  // all robots' samples share the wave
-  int wpb = (int)((warps + num_sms - 1) / num_sms);
-  wpb = wpb < 1 ? 1 : (wpb > 8 ? 8 : wpb);
-  if (lps_out) *lps_out = lps;
-  if (threads_out) *threads_out = wpb * 32;
-  if (spg_out) *spg_out = spg;
-  return wpb * spw;
+  auto shape = [&](int* threads, int* spb) {
+    const int spw = 32 / lps * spg;
+    const long long warps = (total + spw - 1) / spw;  // all robots' samples share the wave
+    int wpb = (int)((warps + num_sms - 1) / num_sms);
+    wpb = wpb < 1 ? 1 : (wpb > 8 ? 8 : wpb);
+    *threads = wpb * 32;
+    *spb = wpb * spw;
+  };
+  int threads = 32, spb = 1;
+  shape(&threads, &spb);
+  size_t base = sizeof(TaskDev) + sizeof(double) * (size_t)(2 * T + T + T * kMaxObstacles + kMaxTerrains + 2 + 32);
+  base = ((base + 15) & ~(size_t)15) + sizeof(double) * (size_t)7 * ((n_pts + 1) & ~1) * (G > 0 ? G : 1);
+  while (base + sizeof(double2) * (size_t)(threads / lps) * spg * T > 227 * 1024 && lps < 32) {
+    lps *= 2;  // large n*T: wider groups, fewer control buffers
+    shape(&threads, &spb);
+  }
+  RolloutGeom g;
+  g.lps = lps;
+  g.spg = spg;
+  g.threads = threads;
+  g.spb = spb;
+  g.chunks = (K_local + spb - 1) / spb;
+  return g;
 }
 
 cudaError_t launch_rollout(const RolloutArgs& a, int num_sms, cudaStream_t st) {
   const size_t smem = rollout_smem_bytes(a);
   if (a.K_local <= 0 || a.B <= 0) return cudaSuccess;
   if (a.model_kind == MODEL_GP) {
-    int lps = 8, threads = 32, spg = 1;
-    int spb = rollout_samples_per_block(a.K_local, a.B, num_sms, &lps, &threads, &spg);
+    const int lps = a.geom.lps, threads = a.geom.threads, spg = a.geom.spg;
     size_t smem_u = smem + sizeof(double2) * (size_t)(threads / lps) * spg * a.T;  // + control buffers
-    while (smem_u > 227 * 1024 && lps < 32) {  // large n*T: wider groups, fewer control buffers
-      lps *= 2;
-      const int spw = 32 / lps * spg;
-      const long long total = (long long)a.K_local * a.B;
-      const long long warps = (total + spw - 1) / spw;
-      int wpb = (int)((warps + num_sms - 1) / num_sms);
-      wpb = wpb < 1 ? 1 : (wpb > 8 ? 8 : wpb);
-      threads = wpb * 32;
-      spb = wpb * spw;
-      smem_u = smem + sizeof(double2) * (size_t)(threads / lps) * spg * a.T;
-    }
-    const long long items = (long long)a.B * ((a.K_local + spb - 1) / spb);
+    const long long items = (long long)a.B * a.geom.chunks;
     // one block per SM: capping registers for a second resident block (122 instead of
     // ~200) costs more ILP than the extra warps recover (config2 0.34 -> 0.52 ms)
     const long long cap = (long long)GPM_ROLLOUT_MINB * num_sms;
@@ -960,11 +968,6 @@ GPM_D void apply_tuple(const double* tup, int T, double lambda, double* nominal_
 // grid = B * bpr; block (b, j) reduces robot b's samples [j*per, (j+1)*per);
 // the last block of each robot combines that robot's bpr tuples in block order.
 // samples per pass-1 trace slab of the reduction (<= 96 KB of shared memory)
-GPM_HD int reduce_slab_samples(int T, int threads) {
-  const int cap = (int)(96 * 1024 / (sizeof(double) * (T + 1)));
-  return cap < threads ? (cap < 1 ? 1 : cap) : threads;
-}
-
 __global__ void __launch_bounds__(256, 1) reduce_kernel(const ReduceArgs a) {
   pdl_wait();
   pdl_trigger();
@@ -985,7 +988,7 @@ __global__ void __launch_bounds__(256, 1) reduce_kernel(const ReduceArgs a) {
   const int b0 = j * per;
   const int b1 = min(a.K_local, b0 + per);
   const int W = tuple_doubles(T);
-  const long long KT = (long long)a.B * a.K_local * T;
+  const long long KT = query_slots(a.geom, a.B, T);  // per-group trace stride (item-major slots)
   const double* rt = a.x0 + (size_t)b * BatchStrides::X0;
   const double var_w = rt[5];
   const uint64_t key = (uint64_t)__double_as_longlong(rt[6]);
@@ -993,48 +996,36 @@ __global__ void __launch_bounds__(256, 1) reduce_kernel(const ReduceArgs a) {
 #pragma unroll
   for (int g = 0; g < kMaxGroups; ++g) cg[g] = g < a.G ? a.tw[(size_t)b * BatchStrides::TW + BatchStrides::TW_COEF + g] : 0.0;
   // pass 1: costs (cost_mean + var_w * Σ_k Σ_g coef_g var_g), block min over finite.
-  // Per chunk of <= kReduceSlab samples, the trace slab of each group is staged into
-  // shared memory by one coalesced sweep (row stride T+1: conflict-free), then every
-  // sample sums its T values in step order (mppi.cpp:34-49 combine, costs.cpp:141).
-  const int chunk = reduce_slab_samples(T, blockDim.x);
+  // Thread = sample; every sample sums its T traces in step order (mppi.cpp:34-49 combine,
+  // costs.cpp:141). The traces are item-major (query_slot): for a fixed step the samples of
+  // one rollout item are adjacent, so each step's loads coalesce across the warp; 8 steps
+  // in flight per thread.
   double lmin = INFINITY;
-  for (int c0 = b0; c0 < b1; c0 += chunk) {
-    const int nc = min(chunk, b1 - c0);
+  for (int s = b0 + (int)threadIdx.x; s < b1; s += blockDim.x) {
+    const long long sl = base + s;
     double vsum = 0.0;
     if (a.var) {
+      const long long q0 = query_slot(sl, 0, a.K_local, T, a.geom.spb, a.geom.chunks);
+      const int spb = a.geom.spb;
       for (int g = 0; g < a.G; ++g) {
-        const double* src = a.var + (size_t)g * KT + (size_t)(base + c0) * T;
-        const int cnt = nc * T;
-        __syncthreads();
-        for (int i0 = threadIdx.x; i0 < cnt; i0 += 8 * blockDim.x) {
+        const double* src = a.var + (size_t)g * KT + q0;
+        double gsum = 0.0;
+        int k = 0;
+        for (; k + 8 <= T; k += 8) {
           double x[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int i = i0 + u * blockDim.x;
-            x[u] = i < cnt ? __ldcg(src + i) : 0.0;
-          }
+          for (int u = 0; u < 8; ++u) x[u] = __ldcg(src + (size_t)(k + u) * spb);
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int i = i0 + u * blockDim.x;
-            if (i < cnt) dsm[(i / T) * (T + 1) + i % T] = x[u];
-          }
+          for (int u = 0; u < 8; ++u) gsum += x[u];
         }
-        __syncthreads();
-        if ((int)threadIdx.x < nc) {
-          const double* row = dsm + (size_t)threadIdx.x * (T + 1);
-          double gsum = 0.0;
-          for (int k = 0; k < T; ++k) gsum += row[k];
-          vsum += cg[g] * gsum;
-        }
+        for (; k < T; ++k) gsum += __ldcg(src + (size_t)k * spb);
+        vsum += cg[g] * gsum;
       }
     }
-    if ((int)threadIdx.x < nc) {
-      const long long q = base + c0 + threadIdx.x;
-      double c = a.cost_mean[q];
-      if (a.var) c += var_w * vsum;
-      a.costs_out[q] = c;
-      if (isfinite(c)) lmin = fmin(lmin, c);
-    }
+    double c = a.cost_mean[sl];
+    if (a.var) c += var_w * vsum;
+    a.costs_out[sl] = c;
+    if (isfinite(c)) lmin = fmin(lmin, c);
   }
   __syncthreads();  // the slab area is reused below
   lmin = warp_min(lmin);
@@ -1213,10 +1204,6 @@ cudaError_t launch_reduce(const ReduceArgs& a, int blocks, cudaStream_t st) {
   const int threads = 256;
   const int nsl = threads / a.T > 1 ? threads / a.T : 1;
   size_t smem = sizeof(double) * (size_t)nsl * a.T * 2;
-  const int per = (a.K_local + a.bpr - 1) / a.bpr;
-  const int ch = reduce_slab_samples(a.T, threads);
-  const size_t slab = sizeof(double) * (size_t)(per < ch ? per : ch) * (a.T + 1);  // pass-1 trace slab
-  if (smem < slab) smem = slab;
   const size_t need = sizeof(double) * ((size_t)a.bpr * tuple_doubles(a.T) + a.bpr + 2 * a.T);
   if (smem < need) smem = need;
   cudaFuncSetAttribute(reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
