@@ -644,6 +644,9 @@ struct gpmppi_planner {
   gpm::RolloutGeom geom{};    // GP rollout geometry (query layout), fixed per sample-buffer set
   long long q_slots = 0;      // item-major query / trace slots (gpm::query_slots)
   unsigned long long* d_progress = nullptr;  // per lane group: query steps published (concurrent variance)
+  long long progress_words = 0;
+  bool coop_ok = false;  // the variance runs concurrently with the rollout (variance_coop_kernel)
+  int coop_budget = 0;   // rollout block shared-memory cap that leaves room for it
   gpm::TaskDev* d_task = nullptr;
   double *d_cost_mean = nullptr, *d_var = nullptr, *d_costs = nullptr, *d_e = nullptr;
   float4* d_queries = nullptr;
@@ -750,11 +753,36 @@ struct gpmppi_planner {
     const bool mat = mat_env >= 0 ? mat_env != 0 : (long long)S * T <= kNoiseMatMax;
     d_noise = mat ? dalloc<double>((size_t)S * T * 2, o) : nullptr;
     if (model_kind == GPMPPI_MODEL_GP_ENSEMBLE) {
-      geom = gpm::rollout_geometry((int)K_local, B, T, model->n, groups(), num_sms);
+      // the co-resident variance (variance_coop_kernel) needs one kernel group with the
+      // 3xFP16 operand, a rollout block of <= 7 warps (registers) and room for both blocks'
+      // shared memory on an SM; GPMPPI_COOP=0 turns it off
+      static const int coop_env = getenv("GPMPPI_COOP") ? atoi(getenv("GPMPPI_COOP")) : 1;
+      const gpm::GroupDev& g0 = model->dev.g[0];
+      const bool coop_possible = coop_env != 0 && groups() == 1 && g0.tc_h && g0.tc_hmeta && g0.tc_np <= 256;
+      geom = gpm::rollout_geometry((int)K_local, B, T, model->n, groups(), num_sms, coop_possible ? 7 : 8);
+      coop_ok = false;
+      if (coop_possible) {
+        gpm::RolloutArgs ra{};
+        ra.model = model->dev;
+        ra.model_kind = model_kind;
+        ra.T = T;
+        ra.n_obs_max = gpm::kMaxObstacles;  // the worst per-tick robot view
+        ra.R = R;
+        ra.geom = geom;
+        for (int st = 3; st >= 2 && !coop_ok; --st) {
+          ra.smem_budget = (int)(228 * 1024 - 2048 - gpm::coop_smem_bytes(g0, st));
+          ra.smem_budget = std::min(ra.smem_budget, 227 * 1024);
+          if (gpm::rollout_launch_smem(ra, nullptr) <= (size_t)ra.smem_budget) {
+            coop_ok = true;
+            coop_budget = ra.smem_budget;
+          }
+        }
+      }
       q_slots = gpm::query_slots(geom, B, T);  // item-major, padded to whole items
       d_queries = dalloc<float4>((size_t)q_slots, o);
       d_var = dalloc<double>((size_t)groups() * q_slots, o);
-      d_progress = dalloc<unsigned long long>((size_t)B * geom.chunks * (geom.threads / geom.lps), o);
+      progress_words = (long long)B * geom.chunks * (geom.threads / geom.lps);
+      d_progress = dalloc<unsigned long long>((size_t)progress_words, o);
       if (!d_scratch) d_scratch = dalloc<double>(gpm::rollout_scratch_doubles(T, num_sms));
     }
     reduce_blocks = gpm::reduce_blocks_for((int)K_local, B, num_sms, T);
@@ -978,13 +1006,30 @@ void enqueue_samples(gpmppi_planner* p, int finish, cudaEvent_t* evs) {
   a.words = p->words;
   a.scratch = p->d_scratch;
   a.geom = p->geom;
-  a.progress = nullptr;
+  const bool gp = p->model_kind == GPMPPI_MODEL_GP_ENSEMBLE;
+  // concurrent variance: the rollout publishes its query progress, the variance kernel
+  // launches as its programmatic dependent and shares the SMs (phase events would split
+  // them, so the per-phase timing pass keeps the sequential path)
+  const bool coop = gp && p->coop_ok && p->var_path == GPMPPI_VAR_TC_3XF16 && !evs;
+  a.progress = coop ? p->d_progress : nullptr;
+  a.smem_budget = coop ? p->coop_budget : 0;
   if (evs) CK(cudaEventRecord(evs[0], p->stream));
   check(gpm::launch_rollout(a, p->num_sms, p->stream), "rollout kernel");
   if (evs) CK(cudaEventRecord(evs[1], p->stream));
-  const bool gp = p->model_kind == GPMPPI_MODEL_GP_ENSEMBLE;
   const long long KT = p->q_slots;  // item-major query / trace slots
-  if (gp) {
+  if (coop) {
+    gpm::VarianceArgs v{};
+    v.queries = p->d_queries;
+    v.KT = KT;
+    v.n = p->model->n;
+    v.g = p->model->dev.g[0];
+    v.coef = 1.0;
+    v.accumulate = 0;
+    v.trace = p->d_var;
+    check(gpm::launch_variance_coop(v, p->d_progress, p->progress_words, T, p->geom,
+                                    gpm::rollout_launch_smem(a, nullptr), p->num_sms, p->stream),
+          "co-resident variance kernel");
+  } else if (gp) {
     for (int g = 0; g < p->groups(); ++g) {  // raw variances; the reduce applies Σ w² per robot
       gpm::VarianceArgs v{};
       v.queries = p->d_queries;

@@ -104,6 +104,7 @@ struct RolloutArgs {
   double* scratch;  // per lane-group trajectory scratch (rollout_scratch_doubles)
   int scratch_smem;  // set by launch_rollout: the trajectory scratch fits in shared memory (after ubuf)
   RolloutGeom geom;  // rollout_geometry of the planner (query layout, query_slot)
+  int smem_budget;   // dynamic shared memory cap of the rollout block (0: 227 KB)
   unsigned long long* progress;  // [items * groups per block]: steps whose queries a group has
                                  // written (release), read by the concurrent variance kernel; null: off
 };
@@ -210,7 +211,13 @@ cudaError_t launch_reduce(const ReduceArgs& a, int blocks, cudaStream_t st);
 cudaError_t launch_finish(const double* tuples, int n, int T, double lambda, double* nominal_seq,
                           const double lo[2], const double hi[2], double* out, long long K_total,
                           double* combined, cudaStream_t st);
-RolloutGeom rollout_geometry(int K_local, int B, int T, int n_pts, int G, int num_sms);
+// max_warps: warps per rollout block (8; 7 leaves the registers of a co-resident variance block)
+RolloutGeom rollout_geometry(int K_local, int B, int T, int n_pts, int G, int num_sms, int max_warps = 8);
+size_t rollout_launch_smem(const RolloutArgs& a, int* scratch_smem);
+// kernels_tc.cu: the co-resident variance (variance_coop_kernel) and its shared memory
+size_t coop_smem_bytes(const GroupDev& g, int stages);
+cudaError_t launch_variance_coop(const VarianceArgs& v, const unsigned long long* progress, long long progress_words,
+                                 int T, const RolloutGeom& geom, size_t rollout_smem, int num_sms, cudaStream_t st);
 // slots of the item-major query / trace arrays (>= B*K_local*T: the last chunk of a robot is padded)
 GPM_HD long long query_slots(const RolloutGeom& g, int B, int T) { return (long long)B * g.chunks * T * g.spb; }
 cudaError_t launch_tighten(const TightenArgs& a, cudaStream_t st);

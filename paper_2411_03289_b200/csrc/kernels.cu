@@ -712,7 +712,7 @@ size_t rollout_scratch_doubles(int T, int num_sms) {
 // when possible (one block per SM); wider lane groups when n*T leaves no room for the
 // control buffers (the shared-memory estimate assumes the maximum obstacle count, so the
 // geometry -- and with it the query layout -- is fixed for the planner's lifetime).
-RolloutGeom rollout_geometry(int K_local, int B, int T, int n_pts, int G, int num_sms) {
+RolloutGeom rollout_geometry(int K_local, int B, int T, int n_pts, int G, int num_sms, int max_warps) {
   const long long total = (long long)K_local * B;
   int lps = 8, spg = 1;
   rollout_layout(total, num_sms, &lps, &spg);
@@ -720,7 +720,7 @@ RolloutGeom rollout_geometry(int K_local, int B, int T, int n_pts, int G, int nu
     const int spw = 32 / lps * spg;
     const long long warps = (total + spw - 1) / spw;  // all robots' samples share the wave
     int wpb = (int)((warps + num_sms - 1) / num_sms);
-    wpb = wpb < 1 ? 1 : (wpb > 8 ? 8 : wpb);
+    wpb = wpb < 1 ? 1 : (wpb > max_warps ? max_warps : wpb);
     *threads = wpb * 32;
     *spb = wpb * spw;
   };
@@ -741,12 +741,29 @@ RolloutGeom rollout_geometry(int K_local, int B, int T, int n_pts, int G, int nu
   return g;
 }
 
+// Dynamic shared memory of the GP rollout block: robot view + Z/alpha + control buffers,
+// plus the trajectory scratch when it fits under a.smem_budget (bytes; 0 = the 227 KB
+// per-block maximum -- the co-resident variance lowers it to leave room for its ring).
+size_t rollout_launch_smem(const RolloutArgs& a, int* scratch_smem) {
+  static int scr_env = -1;  // GPMPPI_SCR_GLOBAL=1 keeps the trajectory scratch in global memory
+  if (scr_env < 0) {
+    const char* e = getenv("GPMPPI_SCR_GLOBAL");
+    scr_env = e ? atoi(e) : 0;
+  }
+  const size_t budget = a.smem_budget > 0 ? (size_t)a.smem_budget : 227 * 1024;
+  const int lps = a.geom.lps, threads = a.geom.threads, spg = a.geom.spg;
+  size_t smem_u = rollout_smem_bytes(a) + sizeof(double2) * (size_t)(threads / lps) * spg * a.T;
+  const size_t scr_bytes = sizeof(double) * (size_t)(threads / lps) * spg * SCR_ARRAYS * (a.T + 1);
+  const int in_smem = (!scr_env && smem_u + scr_bytes <= budget) ? 1 : 0;
+  if (scratch_smem) *scratch_smem = in_smem;
+  return smem_u + (in_smem ? scr_bytes : 0);
+}
+
 cudaError_t launch_rollout(const RolloutArgs& a, int num_sms, cudaStream_t st) {
   const size_t smem = rollout_smem_bytes(a);
   if (a.K_local <= 0 || a.B <= 0) return cudaSuccess;
   if (a.model_kind == MODEL_GP) {
     const int lps = a.geom.lps, threads = a.geom.threads, spg = a.geom.spg;
-    size_t smem_u = smem + sizeof(double2) * (size_t)(threads / lps) * spg * a.T;  // + control buffers
     const long long items = (long long)a.B * a.geom.chunks;
     // one block per SM: capping registers for a second resident block (122 instead of
     // ~200) costs more ILP than the extra warps recover (config2 0.34 -> 0.52 ms)
@@ -759,15 +776,8 @@ cudaError_t launch_rollout(const RolloutArgs& a, int num_sms, cudaStream_t st) {
     // spg 4: one 32-lane group per warp carrying four samples (no duplicate addresses inside
     // a warp's Z/alpha loads, a quarter of the LDS instructions of the 8-lane layout)
     KF kern = spg == 4 ? rollout_gp_kernel<32, 4> : table[spg == 2 ? 1 : 0][li];
-    static int scr_env = -1;  // GPMPPI_SCR_GLOBAL=1 keeps the trajectory scratch in global memory
-    if (scr_env < 0) {
-      const char* e = getenv("GPMPPI_SCR_GLOBAL");
-      scr_env = e ? atoi(e) : 0;
-    }
     RolloutArgs ra = a;
-    const size_t scr_bytes = sizeof(double) * (size_t)(threads / lps) * spg * SCR_ARRAYS * (a.T + 1);
-    ra.scratch_smem = (!scr_env && smem_u + scr_bytes <= 227 * 1024) ? 1 : 0;
-    if (ra.scratch_smem) smem_u += scr_bytes;
+    const size_t smem_u = rollout_launch_smem(a, &ra.scratch_smem);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_u);
     if (e != cudaSuccess) return e;
     e = launch_pdl(kern, dim3((unsigned)blocks), dim3(threads), smem_u, st, ra);

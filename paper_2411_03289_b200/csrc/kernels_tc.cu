@@ -1286,6 +1286,282 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const Vari
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512) : "memory");
 }
 
+// ---------------------------------------------------------------------------
+// Co-resident 3xFP16 variance (default in the tick when it fits next to the rollout):
+// the same tcgen05 kind::f16 3-product math as variance_f16_kernel, but launched as the
+// rollout's programmatic dependent and sized to share every SM with the rollout's block
+// (320 threads at <= 48 registers, a shallow ring), so the FP64 rollout and the tensor /
+// XU variance run at the same time on different pipes. A query tile is consumed as soon
+// as the rollout lane groups that own its rows have published (st.release) that many steps
+// (RolloutArgs::progress, item-major query slots). At the end the kernel waits for the
+// rollout grid (griddepcontrol.wait: its completion then implies the rollout's, which the
+// reduce relies on) and re-arms the progress words for the next tick.
+// Roles: w0 lane 0 bulk-copies L^{-T} hi/lo chunks, w1 issues the MMAs, w2-5 drain TMEM
+// (quarter = warp % 4), w6-9 produce A (lane = one query row of the tile).
+namespace tc {
+constexpr int COOP_THREADS = 320;
+struct CoopArgs {
+  VarianceArgs v;
+  const unsigned long long* progress;  // [items * gpb]
+  unsigned long long* progress_rw;
+  long long progress_words;
+  int T, spb, spg, gpb;  // rollout geometry: steps, samples per item, samples per group, groups per block
+};
+}  // namespace tc
+
+__global__ void __maxnreg__(48)
+    variance_coop_kernel(const tc::CoopArgs c, int S) {
+  using namespace tc;
+  pdl_trigger();
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const VarianceArgs& a = c.v;
+  const GroupDev& G = a.g;
+  const int n = a.n, n_pad = G.tc_npad, NP = G.tc_np, n_pass = G.tc_npass;
+  constexpr int A_BYTES = 2 * H_TILE_BYTES;  // one tile x (hi, lo)
+  const int stage_bytes = A_BYTES + 2 * NP * KC * 2;
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char* stg = base;
+  float* zs = reinterpret_cast<float*>(stg + (size_t)S * stage_bytes);  // [5][n_pad]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(zs + 5 * n_pad);
+  uint64_t* full = bars;
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;  // [2] accumulator slots
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const long long n_tiles = (a.KT + M - 1) / M;
+  const float L2E = 1.4426950408889634f;
+  for (int i = threadIdx.x; i < n_pad; i += blockDim.x) {
+    float z[4], sq = 0.f;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      z[d] = i < n ? G.zs32[(size_t)d * n + i] : 0.f;
+      sq += z[d] * z[d];
+    }
+#pragma unroll
+    for (int d = 0; d < 4; ++d) zs[d * n_pad + i] = L2E * z[d];
+    zs[4 * n_pad + i] = i < n ? L2E * (-0.5f * sq) : -1e30f;
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(smem_u32(&full[s]), 4 + 1);  // four A warps + the B copy's expect_tx arrival
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(smem_u32(&tfull[s]), 1);
+      mbar_init(smem_u32(&tempty[s]), 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- B producer
+      Ring r(S);
+      for (long long t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        int m = 0;
+        for (int p = 0; p < n_pass; ++p) {
+          const int nk = pass_chunks(p, NP, n_pad);
+          for (int kb = 0; kb < nk; ++kb, ++m, r.next()) {
+            const int4 meta = G.tc_hmeta[m];
+            mbar_wait(smem_u32(&empty[r.s]), r.ph ^ 1);
+            const uint32_t bytes = (uint32_t)meta.y * KC * 2 * 2;
+            const uint32_t fb = smem_u32(&full[r.s]);
+            mbar_arrive_tx(fb, bytes);
+            bulk_g2s(smem_u32(stg + (size_t)r.s * stage_bytes + A_BYTES), G.tc_h + meta.x, bytes, fb);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {  // ---------------- MMA issuer (converged warp, elect.sync inside)
+    Ring r(S);
+    uint32_t uc = 0;
+    for (long long t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      for (int p = 0; p < n_pass; ++p, ++uc) {
+        const uint32_t slot = uc & 1;
+        mbar_wait(smem_u32(&tempty[slot]), ((uc >> 1) & 1) ^ 1);
+        tc_after();
+        const int nk = pass_chunks(p, NP, n_pad);
+        const int npw = min(NP, n_pad - p * NP);
+        for (int kb = 0; kb < nk; ++kb, r.next()) {
+          mbar_wait(smem_u32(&full[r.s]), r.ph);
+          tc_after();
+          const int col0 = max(0, kb * KC - p * NP);
+          const int ncols = npw - col0;
+          const uint32_t st = smem_u32(stg + (size_t)r.s * stage_bytes);
+          const uint32_t bh = st + A_BYTES;
+          const uint32_t bl = bh + (uint32_t)ncols * KC * 2;
+          mma_f16_single_3x(tmem_base + slot * (uint32_t)NP + (uint32_t)col0, smem_desc(st, H_SBO),
+                            smem_desc(st + H_TILE_BYTES, H_SBO), smem_desc(bh, H_SBO), smem_desc(bl, H_SBO),
+                            instr_desc_f16(ncols), kb > 0 ? 1u : 0u, smem_u32(&empty[r.s]));
+        }
+        mma_commit(smem_u32(&tfull[slot]));
+      }
+    }
+  } else if (warp >= 6) {  // ---------------- A producers: lane = one row of the tile
+    const int row = (warp - 6) * 32 + lane;
+    Ring r(S);
+    const long long per_item = (long long)c.T * c.spb;
+    for (long long t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const long long q = t * M + row;
+      float qq[5];
+      bool valid = q < a.KT;
+      if (valid) {  // wait until the lane group owning this query slot has written step k
+        const long long item = q / per_item;
+        const long long rem = q - item * per_item;
+        const int k = (int)(rem / c.spb), i = (int)(rem - (long long)k * c.spb);
+        const unsigned long long* flag = c.progress + item * c.gpb + i / c.spg;
+        unsigned ns = 32, spins = 0;
+        while (ld_acquire_u64(flag) < (unsigned long long)(k + 1)) {
+          __nanosleep(ns);
+          ns = ns < 1024 ? 2 * ns : ns;
+          if (++spins > (1u << 23)) __trap();  // ~8 s without progress: fail loudly, never hang
+        }
+        const float4 qv = __ldcg(reinterpret_cast<const float4*>(a.queries) + q);
+        qq[0] = qv.x / (float)G.ls[0];
+        qq[1] = qv.y / (float)G.ls[1];
+        qq[2] = qv.z / (float)G.ls[2];
+        qq[3] = qv.w / (float)G.ls[3];
+        qq[4] = -0.5f * L2E * (qq[0] * qq[0] + qq[1] * qq[1] + qq[2] * qq[2] + qq[3] * qq[3]);
+        valid = isfinite(qq[4]);
+      }
+      if (!valid) qq[0] = qq[1] = qq[2] = qq[3] = 0.f, qq[4] = -1e30f;
+      for (int p = 0; p < n_pass; ++p) {
+        const int nk = pass_chunks(p, NP, n_pad);
+        for (int kb = 0; kb < nk; ++kb, r.next()) {
+          if (lane == 0) mbar_wait(smem_u32(&empty[r.s]), r.ph ^ 1);
+          __syncwarp();
+          unsigned char* ahi = stg + (size_t)r.s * stage_bytes;
+          unsigned char* alo = ahi + H_TILE_BYTES;
+          const int off0 = (row >> 3) * H_SBO + (row & 7) * 16;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {  // points kb*16 + 8h .. +7: one core matrix each
+            const int i0 = kb * KC + 8 * h;
+            float kv[8];
+#pragma unroll
+            for (int u = 0; u < 8; u += 4) {
+              const float4 z0 = *reinterpret_cast<const float4*>(zs + i0 + u);
+              const float4 z1 = *reinterpret_cast<const float4*>(zs + n_pad + i0 + u);
+              const float4 z2 = *reinterpret_cast<const float4*>(zs + 2 * n_pad + i0 + u);
+              const float4 z3 = *reinterpret_cast<const float4*>(zs + 3 * n_pad + i0 + u);
+              const float4 zq = *reinterpret_cast<const float4*>(zs + 4 * n_pad + i0 + u);
+              kv[u] = exp2f_approx(fmaf(qq[0], z0.x, fmaf(qq[1], z1.x, fmaf(qq[2], z2.x, fmaf(qq[3], z3.x, qq[4] + zq.x)))));
+              kv[u + 1] = exp2f_approx(fmaf(qq[0], z0.y, fmaf(qq[1], z1.y, fmaf(qq[2], z2.y, fmaf(qq[3], z3.y, qq[4] + zq.y)))));
+              kv[u + 2] = exp2f_approx(fmaf(qq[0], z0.z, fmaf(qq[1], z1.z, fmaf(qq[2], z2.z, fmaf(qq[3], z3.z, qq[4] + zq.z)))));
+              kv[u + 3] = exp2f_approx(fmaf(qq[0], z0.w, fmaf(qq[1], z1.w, fmaf(qq[2], z2.w, fmaf(qq[3], z3.w, qq[4] + zq.w)))));
+            }
+            uint32_t hi[4], lo[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const __half2 hh = __floats2half2_rn(kv[2 * u], kv[2 * u + 1]);
+              const float2 hf = __half22float2(hh);
+              hi[u] = half2_bits(hh);
+              lo[u] = half2_bits(__floats2half2_rn(kv[2 * u] - hf.x, kv[2 * u + 1] - hf.y));
+            }
+            *reinterpret_cast<uint4*>(ahi + off0 + h * 128) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+            *reinterpret_cast<uint4*>(alo + off0 + h * 128) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+          }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&full[r.s]));
+        }
+      }
+    }
+  } else {  // ---------------- epilogue (warps 2-5): TMEM -> Σ D^2 -> var
+    const int quarter = warp & 3;
+    const int m = quarter * 32 + lane;
+    uint32_t uc = 0;
+    for (long long t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      double ssq = 0.0;
+      for (int p = 0; p < n_pass; ++p, ++uc) {
+        const uint32_t slot = uc & 1;
+        const int npw = min(NP, n_pad - p * NP);
+        if (lane == 0) mbar_wait(smem_u32(&tfull[slot]), (uc >> 1) & 1);
+        __syncwarp();
+        tc_after();
+        const uint32_t trow = tmem_base + ((uint32_t)(quarter * 32) << 16) + slot * (uint32_t)NP;
+        for (int cc = 0; cc < npw; cc += 16) {
+          float v[16];
+          tmem_ld16(trow + cc, v);
+          float p0 = 0.f, p1 = 0.f, p2 = 0.f, p3 = 0.f;
+#pragma unroll
+          for (int i = 0; i < 16; i += 4) {
+            p0 = fmaf(v[i], v[i], p0);
+            p1 = fmaf(v[i + 1], v[i + 1], p1);
+            p2 = fmaf(v[i + 2], v[i + 2], p2);
+            p3 = fmaf(v[i + 3], v[i + 3], p3);
+          }
+          ssq += (double)((p0 + p1) + (p2 + p3));
+        }
+        tc_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&tempty[slot]));
+      }
+      const long long q = t * M + m;
+      if (q < a.KT) {
+        double var = G.sv - G.tc_hfac * ssq;  // gp.cpp:187-191
+        var = var > 0.0 ? var : 0.0;
+        const double cv = a.coef * var;
+        a.trace[q] = a.accumulate ? a.trace[q] + cv : cv;
+      }
+    }
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512) : "memory");
+  // the rollout grid has finished (its queries, costs and flags are visible to whoever
+  // waits on this grid); re-arm the progress words for the next tick
+  pdl_wait();
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < c.progress_words;
+       i += (long long)gridDim.x * blockDim.x)
+    c.progress_rw[i] = 0ull;
+}
+
+size_t coop_smem_bytes(const GroupDev& g, int stages) {
+  return 1024 + (size_t)stages * (2 * tc::H_TILE_BYTES + 2 * (size_t)g.tc_np * tc::KC * 2) +
+         sizeof(float) * 5 * (size_t)g.tc_npad + sizeof(uint64_t) * (2 * stages + 4) + 16;
+}
+
+// Launch the co-resident variance as the rollout's programmatic dependent, or return
+// cudaErrorNotSupported (the caller then runs the ordinary variance path) when the model /
+// shared memory does not allow it next to the rollout block.
+cudaError_t launch_variance_coop(const VarianceArgs& v, const unsigned long long* progress, long long progress_words,
+                                 int T, const RolloutGeom& geom, size_t rollout_smem, int num_sms, cudaStream_t st) {
+  if (!v.g.tc_h || !v.g.tc_hmeta || v.g.tc_np > 256 || !progress) return cudaErrorNotSupported;
+  constexpr size_t kSmSmem = 228 * 1024;  // per SM, both blocks + 1 KB reserved each
+  int stages = 4;
+  while (stages >= 2 && rollout_smem + coop_smem_bytes(v.g, stages) + 2048 > kSmSmem) --stages;
+  if (stages < 2) return cudaErrorNotSupported;
+  const size_t sm = coop_smem_bytes(v.g, stages);
+  cudaError_t e = cudaFuncSetAttribute(variance_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  tc::CoopArgs c;
+  c.v = v;
+  c.progress = progress;
+  c.progress_rw = const_cast<unsigned long long*>(progress);
+  c.progress_words = progress_words;
+  c.T = T;
+  c.spb = geom.spb;
+  c.spg = geom.spg;
+  c.gpb = geom.threads / geom.lps;
+  const long long tiles = (v.KT + tc::M - 1) / tc::M;
+  const int grid = (int)(tiles < num_sms ? tiles : num_sms);
+  e = launch_pdl(variance_coop_kernel, dim3(grid), dim3(tc::COOP_THREADS), sm, st, c, stages);
+  if (e != cudaSuccess) return e;
+  count_launch();
+  return cudaGetLastError();
+}
+
 size_t f16_smem_bytes(const GroupDev& g, int stages) {
   return 1024 + (size_t)stages * (2 * 2 * tc::H_TILE_BYTES + 2 * (size_t)g.tc_np * tc::KC * 2) +
          sizeof(float) * 5 * (size_t)g.tc_npad + sizeof(uint64_t) * (2 * stages + 2) + 16;
