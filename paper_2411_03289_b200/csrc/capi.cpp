@@ -753,10 +753,11 @@ struct gpmppi_planner {
     const bool mat = mat_env >= 0 ? mat_env != 0 : (long long)S * T <= kNoiseMatMax;
     d_noise = mat ? dalloc<double>((size_t)S * T * 2, o) : nullptr;
     if (model_kind == GPMPPI_MODEL_GP_ENSEMBLE) {
-      // the co-resident variance (variance_coop_kernel) needs one kernel group with the
-      // 3xFP16 operand, a rollout block of <= 7 warps (registers) and room for both blocks'
-      // shared memory on an SM; GPMPPI_COOP=0 turns it off
-      static const int coop_env = getenv("GPMPPI_COOP") ? atoi(getenv("GPMPPI_COOP")) : 1;
+      // The co-resident variance (variance_coop_kernel, GPMPPI_COOP=1) needs one kernel group
+      // with the 3xFP16 operand, a rollout block of <= 7 warps (registers) and room for both
+      // blocks' shared memory on an SM. Off by default: measured slower than the sequential
+      // rollout -> variance_f16_kernel sequence (profiles/r02/coop_variance.md).
+      static const int coop_env = getenv("GPMPPI_COOP") ? atoi(getenv("GPMPPI_COOP")) : 0;
       const gpm::GroupDev& g0 = model->dev.g[0];
       const bool coop_possible = coop_env != 0 && groups() == 1 && g0.tc_h && g0.tc_hmeta && g0.tc_np <= 256;
       geom = gpm::rollout_geometry((int)K_local, B, T, model->n, groups(), num_sms, coop_possible ? 7 : 8);
@@ -905,6 +906,11 @@ void fill_task(gpm::TaskDev& d, const gpmppi_task* t) {
 
 void check(cudaError_t e, const char* where) {
   if (e != cudaSuccess) throw CudaError{e, where};
+  static const int dbg_sync = getenv("GPMPPI_DEBUG_SYNC") ? atoi(getenv("GPMPPI_DEBUG_SYNC")) : 0;  // diagnostics
+  if (dbg_sync) {
+    const cudaError_t se = cudaDeviceSynchronize();
+    if (se != cudaSuccess) throw CudaError{se, where};
+  }
 }
 
 double task_var_weight(const gpmppi_task* t) {
@@ -1045,6 +1051,8 @@ void enqueue_samples(gpmppi_planner* p, int finish, cudaEvent_t* evs) {
   if (evs) CK(cudaEventRecord(evs[2], p->stream));
   gpm::ReduceArgs r{};
   r.geom = p->geom;
+  r.progress = coop ? p->d_progress : nullptr;
+  r.progress_words = p->progress_words;
   r.B = p->B;
   r.K_local = (int)p->K_local;
   r.K_total = p->K_total;

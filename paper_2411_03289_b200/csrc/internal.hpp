@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <utility>
 #include <vector>
 
@@ -121,6 +122,8 @@ struct VarianceArgs {
 
 struct ReduceArgs {
   RolloutGeom geom;  // the trace is in query_slot order
+  unsigned long long* progress;  // rollout query-progress words to re-arm (null: none)
+  long long progress_words;
   int B;
   int K_local;
   long long K_total;
@@ -185,8 +188,9 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  static const int no_pdl = getenv("GPMPPI_NO_PDL") ? atoi(getenv("GPMPPI_NO_PDL")) : 0;  // diagnostics
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = no_pdl ? 0 : 1;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 #if defined(__CUDACC__)

@@ -981,6 +981,12 @@ GPM_D void apply_tuple(const double* tup, int T, double lambda, double* nominal_
 __global__ void __launch_bounds__(256, 1) reduce_kernel(const ReduceArgs a) {
   pdl_wait();
   pdl_trigger();
+  // re-arm the rollout's query-progress words for the next tick: the co-resident variance
+  // (the predecessor this grid waited for) has finished reading them
+  if (a.progress)
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.progress_words;
+         i += (long long)gridDim.x * blockDim.x)
+      a.progress[i] = 0ull;
   extern __shared__ __align__(16) double dsm[];
   __shared__ double red[32 * 5];
   __shared__ unsigned int s_last;

@@ -25,6 +25,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <vector>
 
@@ -1306,7 +1307,31 @@ struct CoopArgs {
   unsigned long long* progress_rw;
   long long progress_words;
   int T, spb, spg, gpb;  // rollout geometry: steps, samples per item, samples per group, groups per block
+  long long items;
+  int tiles_per_item;    // ceil(T * spb / 128): an item's tiles never straddle another item
 };
+// Tile t = (item, j): rows [j*128, min(j*128 + 128, T*spb)) of the item's [T][spb] slots. CTA c
+// walks items c, c + grid, ... -- the rollout blocks' item order -- and each item's tiles in
+// step order, so it consumes the queries in the order the chains produce them.
+__device__ __forceinline__ long long first_tile(const CoopArgs& c, int cta) {
+  return cta < c.items ? (long long)cta * c.tiles_per_item : -1;
+}
+__device__ __forceinline__ long long next_tile(const CoopArgs& c, long long t, int grid) {
+  const long long item = t / c.tiles_per_item;
+  const int j = (int)(t - item * c.tiles_per_item);
+  if (j + 1 < c.tiles_per_item) return t + 1;
+  const long long ni = item + grid;
+  return ni < c.items ? ni * c.tiles_per_item : -1;
+}
+__device__ __forceinline__ long long tile_slot(const CoopArgs& c, long long t) {
+  const long long item = t / c.tiles_per_item;
+  return item * c.T * c.spb + (t - item * c.tiles_per_item) * M;
+}
+__device__ __forceinline__ int tile_rows(const CoopArgs& c, long long t) {
+  const long long item = t / c.tiles_per_item;
+  const int r = c.T * c.spb - (int)(t - item * c.tiles_per_item) * M;
+  return r < M ? r : M;
+}
 }  // namespace tc
 
 __global__ void __maxnreg__(48)
@@ -1329,7 +1354,6 @@ __global__ void __maxnreg__(48)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
-  const long long n_tiles = (a.KT + M - 1) / M;
   const float L2E = 1.4426950408889634f;
   for (int i = threadIdx.x; i < n_pad; i += blockDim.x) {
     float z[4], sq = 0.f;
@@ -1366,7 +1390,7 @@ __global__ void __maxnreg__(48)
   if (warp == 0) {
     if (lane == 0) {  // ---------------- B producer
       Ring r(S);
-      for (long long t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      for (long long t = first_tile(c, blockIdx.x); t >= 0; t = next_tile(c, t, gridDim.x)) {
         int m = 0;
         for (int p = 0; p < n_pass; ++p) {
           const int nk = pass_chunks(p, NP, n_pad);
@@ -1384,7 +1408,7 @@ __global__ void __maxnreg__(48)
   } else if (warp == 1) {  // ---------------- MMA issuer (converged warp, elect.sync inside)
     Ring r(S);
     uint32_t uc = 0;
-    for (long long t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    for (long long t = first_tile(c, blockIdx.x); t >= 0; t = next_tile(c, t, gridDim.x)) {
       for (int p = 0; p < n_pass; ++p, ++uc) {
         const uint32_t slot = uc & 1;
         mbar_wait(smem_u32(&tempty[slot]), ((uc >> 1) & 1) ^ 1);
@@ -1410,10 +1434,10 @@ __global__ void __maxnreg__(48)
     const int row = (warp - 6) * 32 + lane;
     Ring r(S);
     const long long per_item = (long long)c.T * c.spb;
-    for (long long t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-      const long long q = t * M + row;
+    for (long long t = first_tile(c, blockIdx.x); t >= 0; t = next_tile(c, t, gridDim.x)) {
+      const long long q = tile_slot(c, t) + row;
       float qq[5];
-      bool valid = q < a.KT;
+      bool valid = row < tile_rows(c, t);
       if (valid) {  // wait until the lane group owning this query slot has written step k
         const long long item = q / per_item;
         const long long rem = q - item * per_item;
@@ -1423,7 +1447,11 @@ __global__ void __maxnreg__(48)
         while (ld_acquire_u64(flag) < (unsigned long long)(k + 1)) {
           __nanosleep(ns);
           ns = ns < 1024 ? 2 * ns : ns;
-          if (++spins > (1u << 23)) __trap();  // ~8 s without progress: fail loudly, never hang
+          if (++spins > (1u << 22)) {  // seconds without progress: fail loudly, never hang
+            printf("variance_coop: no progress cta %d row %d tile %lld item %lld k %d flag %llu\n", blockIdx.x, row, t,
+                   item, k, ld_acquire_u64(flag));
+            __trap();
+          }
         }
         const float4 qv = __ldcg(reinterpret_cast<const float4*>(a.queries) + q);
         qq[0] = qv.x / (float)G.ls[0];
@@ -1479,7 +1507,7 @@ __global__ void __maxnreg__(48)
     const int quarter = warp & 3;
     const int m = quarter * 32 + lane;
     uint32_t uc = 0;
-    for (long long t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    for (long long t = first_tile(c, blockIdx.x); t >= 0; t = next_tile(c, t, gridDim.x)) {
       double ssq = 0.0;
       for (int p = 0; p < n_pass; ++p, ++uc) {
         const uint32_t slot = uc & 1;
@@ -1505,8 +1533,8 @@ __global__ void __maxnreg__(48)
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&tempty[slot]));
       }
-      const long long q = t * M + m;
-      if (q < a.KT) {
+      const long long q = tile_slot(c, t) + m;
+      if (m < tile_rows(c, t)) {
         double var = G.sv - G.tc_hfac * ssq;  // gp.cpp:187-191
         var = var > 0.0 ? var : 0.0;
         const double cv = a.coef * var;
@@ -1519,12 +1547,9 @@ __global__ void __maxnreg__(48)
   tc_after();
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512) : "memory");
-  // the rollout grid has finished (its queries, costs and flags are visible to whoever
-  // waits on this grid); re-arm the progress words for the next tick
+  // wait for the rollout grid: this grid's completion then implies the rollout's, which the
+  // reduce (waiting on this grid) relies on; the reduce re-arms the progress words
   pdl_wait();
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < c.progress_words;
-       i += (long long)gridDim.x * blockDim.x)
-    c.progress_rw[i] = 0ull;
 }
 
 size_t coop_smem_bytes(const GroupDev& g, int stages) {
@@ -1542,7 +1567,12 @@ cudaError_t launch_variance_coop(const VarianceArgs& v, const unsigned long long
   int stages = 4;
   while (stages >= 2 && rollout_smem + coop_smem_bytes(v.g, stages) + 2048 > kSmSmem) --stages;
   if (stages < 2) return cudaErrorNotSupported;
-  const size_t sm = coop_smem_bytes(v.g, stages);
+  // diagnostics: GPMPPI_COOP_PAD adds shared memory (fewer blocks per SM), GPMPPI_COOP_GRID forces the
+  // grid, GPMPPI_COOP_NOPDL launches after the rollout (no overlap), GPMPPI_COOP_PRINT logs the launch
+  static const int pad_env = getenv("GPMPPI_COOP_PAD") ? atoi(getenv("GPMPPI_COOP_PAD")) : 0;
+  static const int grid_env = getenv("GPMPPI_COOP_GRID") ? atoi(getenv("GPMPPI_COOP_GRID")) : 0;
+  static const int nopdl_env = getenv("GPMPPI_COOP_NOPDL") ? atoi(getenv("GPMPPI_COOP_NOPDL")) : 0;
+  const size_t sm = coop_smem_bytes(v.g, stages) + pad_env;
   cudaError_t e = cudaFuncSetAttribute(variance_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   tc::CoopArgs c;
@@ -1554,9 +1584,18 @@ cudaError_t launch_variance_coop(const VarianceArgs& v, const unsigned long long
   c.spb = geom.spb;
   c.spg = geom.spg;
   c.gpb = geom.threads / geom.lps;
-  const long long tiles = (v.KT + tc::M - 1) / tc::M;
-  const int grid = (int)(tiles < num_sms ? tiles : num_sms);
-  e = launch_pdl(variance_coop_kernel, dim3(grid), dim3(tc::COOP_THREADS), sm, st, c, stages);
+  c.items = v.KT / ((long long)T * geom.spb);
+  c.tiles_per_item = (T * geom.spb + tc::M - 1) / tc::M;
+  const long long tiles = c.items * c.tiles_per_item;
+  int grid = (int)(c.items < num_sms ? c.items : num_sms);
+  if (grid_env > 0) grid = grid_env;
+  if (getenv("GPMPPI_COOP_PRINT"))
+    fprintf(stderr, "coop: KT %lld tiles %lld grid %d stages %d smem %zu rollout_smem %zu np %d npass %d npad %d words %lld\n",
+            v.KT, tiles, grid, stages, sm, rollout_smem, v.g.tc_np, v.g.tc_npass, v.g.tc_npad, progress_words);
+  if (nopdl_env)
+    variance_coop_kernel<<<grid, tc::COOP_THREADS, sm, st>>>(c, stages);
+  else
+    e = launch_pdl(variance_coop_kernel, dim3(grid), dim3(tc::COOP_THREADS), sm, st, c, stages);
   if (e != cudaSuccess) return e;
   count_launch();
   return cudaGetLastError();
