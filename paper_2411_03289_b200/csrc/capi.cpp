@@ -759,7 +759,8 @@ struct gpmppi_planner {
       // rollout -> variance_f16_kernel sequence (profiles/r02/coop_variance.md).
       static const int coop_env = getenv("GPMPPI_COOP") ? atoi(getenv("GPMPPI_COOP")) : 0;
       const gpm::GroupDev& g0 = model->dev.g[0];
-      const bool coop_possible = coop_env != 0 && groups() == 1 && g0.tc_h && g0.tc_hmeta && g0.tc_np <= 256;
+      const bool coop_possible =
+          GPM_COOP && coop_env != 0 && groups() == 1 && g0.tc_h && g0.tc_hmeta && g0.tc_np <= 256;
       geom = gpm::rollout_geometry((int)K_local, B, T, model->n, groups(), num_sms, coop_possible ? 7 : 8);
       coop_ok = false;
       if (coop_possible) {

@@ -56,6 +56,13 @@ struct BatchStrides {
   GPM_HD static int marg(int T) { return T * kMaxObstacles; }  // [T][n_obs] inside
 };
 
+// GPM_COOP=1 compiles the co-resident variance experiment's query-progress publication into
+// the rollout (an A/B build: python -m paper_2411_03289_b200.build --variant=coop -DGPM_COOP=1,
+// then GPMPPI_LIB=.../libgpmppi_b200_coop.so GPMPPI_COOP=1); the default build leaves it out.
+#ifndef GPM_COOP
+#define GPM_COOP 0
+#endif
+
 // Lane-group geometry of the GP rollout, fixed per planner (rollout_geometry): LPS lanes
 // per sample group, SPG samples per group, `threads` per block, spb samples per work item
 // (one block's chunk of one robot), chunks = items per robot.

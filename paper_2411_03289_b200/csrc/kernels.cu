@@ -494,8 +494,10 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
           a.queries[(size_t)((item * T + k) * spb + ls0 + j - (item % chunks) * spb)] =
               make_float4((float)v[j], (float)w[j], (float)u0[j], (float)u1[j]);
       }
+#if GPM_COOP
       if (a.progress && gl == 0)  // steps < k+1 of this group's queries are published
         st_release_u64(a.progress + (size_t)item * groups_per_block + gib, (unsigned long long)(k + 1));
+#endif
       double cm0[SPG], cm1[SPG];  // combine_terrains (mppi.cpp:34-49)
 #pragma unroll
       for (int j = 0; j < SPG; ++j) cm0[j] = cm1[j] = 0.0;
