@@ -980,6 +980,8 @@ GPM_D void apply_tuple(const double* tup, int T, double lambda, double* nominal_
 // grid = B * bpr; block (b, j) reduces robot b's samples [j*per, (j+1)*per);
 // the last block of each robot combines that robot's bpr tuples in block order.
 // samples per pass-1 trace slab of the reduction (<= 96 KB of shared memory)
+constexpr int kEpsDepth = 8;  // pass-3 noise loads in flight per thread
+
 __global__ void __launch_bounds__(256, 1) reduce_kernel(const ReduceArgs a) {
   pdl_wait();
   pdl_trigger();
@@ -1029,12 +1031,12 @@ __global__ void __launch_bounds__(256, 1) reduce_kernel(const ReduceArgs a) {
         const double* src = a.var + (size_t)g * KT + q0;
         double gsum = 0.0;
         int k = 0;
-        for (; k + 8 <= T; k += 8) {
-          double x[8];
+        for (; k + 16 <= T; k += 16) {  // 16 steps' loads in flight (HBM-bound at large K)
+          double x[16];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) x[u] = __ldcg(src + (size_t)(k + u) * spb);
+          for (int u = 0; u < 16; ++u) x[u] = __ldcs(src + (size_t)(k + u) * spb);
 #pragma unroll
-          for (int u = 0; u < 8; ++u) gsum += x[u];
+          for (int u = 0; u < 16; ++u) gsum += x[u];
         }
         for (; k < T; ++k) gsum += __ldcg(src + (size_t)k * spb);
         vsum += cg[g] * gsum;
@@ -1081,19 +1083,19 @@ __global__ void __launch_bounds__(256, 1) reduce_kernel(const ReduceArgs a) {
   for (int idx = threadIdx.x; idx < T * nsl; idx += blockDim.x) {
     const int k = idx % T, sl = idx / T;
     double s0 = 0.0, s1 = 0.0;
-    if (a.noise_mode == NOISE_INJECTED) {  // 4 samples' loads in flight per thread
+    if (a.noise_mode == NOISE_INJECTED) {  // kEpsDepth samples' loads in flight per thread
       const double2* eps2 = reinterpret_cast<const double2*>(a.eps);
-      for (int s = b0 + sl; s < b1; s += 4 * nsl) {
-        double ev[4];
-        double2 ep[4];
+      for (int s = b0 + sl; s < b1; s += kEpsDepth * nsl) {
+        double ev[kEpsDepth];
+        double2 ep[kEpsDepth];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kEpsDepth; ++u) {
           const int su = s + u * nsl;
-          ev[u] = su < b1 ? a.e_out[base + su] : 0.0;
-          ep[u] = su < b1 ? eps2[(size_t)(base + su) * T + k] : make_double2(0.0, 0.0);
+          ev[u] = su < b1 ? __ldcg(a.e_out + base + su) : 0.0;
+          ep[u] = su < b1 ? __ldcs(eps2 + (size_t)(base + su) * T + k) : make_double2(0.0, 0.0);
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {  // multiplied even when e = 0: a non-finite injected eps
+        for (int u = 0; u < kEpsDepth; ++u) {  // multiplied even when e = 0: a non-finite injected eps
           s0 += ev[u] * ep[u].x;       // poisons the update exactly as mppi.cpp:157-160 does
           s1 += ev[u] * ep[u].y;
         }
