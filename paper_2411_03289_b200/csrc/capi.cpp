@@ -661,8 +661,16 @@ struct gpmppi_planner {
   // pinned staging
   gpm::TaskDev* h_task = nullptr;  // [B]
   double* h_x0 = nullptr;          // [B][8] robot tick blocks
-  double* h_out = nullptr;         // [B][16]
+  double* h_out = nullptr;         // [B][16], mapped: the reduce writes command + diag + sequence here
   int* h_infeasible = nullptr;     // [B]
+  double* h_done = nullptr;        // [B][2], mapped: tightening infeasibility + sequence
+  double *d_out_host = nullptr, *d_done_host = nullptr;  // their device addresses
+  // zero-copy completion (default; GPMPPI_ZEROCOPY=0 restores the D2H copies + events): the
+  // kernels publish the command and the tightening result into mapped pinned memory behind a
+  // per-tick sequence number that plan_step polls
+  bool zero_copy = !(getenv("GPMPPI_ZEROCOPY") && atoi(getenv("GPMPPI_ZEROCOPY")) == 0);
+  bool zc_tick = false;   // set while the plan_step tick is enqueued / captured
+  double seq = 0.0;       // sequence number of the tick being planned
   cudaEvent_t ev[8] = {};
   // one CUDA graph per tick configuration: H2D staging, the six kernels, the command
   // and diagnostics D2H (GPMPPI_NO_GRAPH=1 launches them one by one instead)
@@ -711,6 +719,7 @@ struct gpmppi_planner {
     if (h_x0) cudaFreeHost(h_x0);
     if (h_out) cudaFreeHost(h_out);
     if (h_infeasible) cudaFreeHost(h_infeasible);
+    if (h_done) cudaFreeHost(h_done);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     if (tick_exec) cudaGraphExecDestroy(tick_exec);
@@ -960,8 +969,9 @@ void stage_tick(gpmppi_planner* p, const double* x0, const gpmppi_task* tasks) {
     blk[5] = task_var_weight(&tasks[b]);
     const uint64_t key = gpm::philox_key(p->seeds[b], p->tick);
     std::memcpy(&blk[6], &key, sizeof key);
-    blk[7] = 0.0;
+    blk[7] = p->seq + 1.0;  // this tick's sequence number (zero-copy completion words)
   }
+  p->seq += 1.0;
   p->n_obs_max = omax;
 }
 
@@ -1083,6 +1093,7 @@ void enqueue_samples(gpmppi_planner* p, int finish, cudaEvent_t* evs) {
   r.hi[0] = p->cfg.hi[0];
   r.hi[1] = p->cfg.hi[1];
   r.out = p->d_out;
+  r.out_host = p->zc_tick ? p->d_out_host : nullptr;
   check(gpm::launch_reduce(r, p->B * p->reduce_blocks, p->stream), "reduce kernel");
   if (evs) CK(cudaEventRecord(evs[3], p->stream));
 }
@@ -1102,7 +1113,8 @@ void enqueue_update(gpmppi_planner* p, cudaEvent_t* evs) {
   nccl_check(nccl_api().all_gather(p->d_rank_tuple, p->d_gathered, (size_t)W, ncclDouble, p->comm, p->stream),
              "ncclAllGather");
   check(gpm::launch_finish(p->d_gathered, p->n_ranks, p->T, p->cfg.lambda, p->d_nom, p->cfg.lo, p->cfg.hi,
-                           p->d_out, p->K_total, p->d_combined, p->stream),
+                           p->d_out, p->K_total, p->d_combined, p->stream, p->zc_tick ? p->d_out_host : nullptr,
+                           p->d_x0),
         "finish kernel");
   if (evs) CK(cudaEventRecord(evs[3], p->stream));  // the exchange counts to the reduce phase
 }
@@ -1130,6 +1142,7 @@ void enqueue_tighten(gpmppi_planner* p) {
   t.tmu = p->d_tmu;
   t.tJ = p->d_tJ;
   t.tvar_part = p->d_tvar;
+  t.done_host = p->zc_tick ? p->d_done_host : nullptr;
   check(gpm::launch_tighten(t, p->stream), "tighten kernel");
 }
 
@@ -1150,7 +1163,7 @@ void fill_diag(gpmppi_planner* p, double* command, gpmppi_diag* diag, double t_c
       d.ess = o[4];
       d.weight_entropy = o[5];
       d.nonfinite_samples = (int)o[6];
-      d.tightening_infeasible = p->h_infeasible[b];
+      d.tightening_infeasible = p->zero_copy ? (int)p->h_done[2 * b] : p->h_infeasible[b];
       d.plan_ms = t_all;
       d.command_ms = t_cmd;
     }
@@ -1273,7 +1286,12 @@ gpmppi_planner* create_planner(const gpmppi_mppi_config* cfg, const gpmppi_predi
     p->alloc_sample_buffers();
     CK(cudaMallocHost(&p->h_task, sizeof(gpm::TaskDev) * B));
     CK(cudaMallocHost(&p->h_x0, sizeof(double) * gpm::BatchStrides::X0 * B));
-    CK(cudaMallocHost(&p->h_out, sizeof(double) * gpm::BatchStrides::OUT * B));
+    CK(cudaHostAlloc(&p->h_out, sizeof(double) * gpm::BatchStrides::OUT * B, cudaHostAllocMapped));
+    CK(cudaHostAlloc(&p->h_done, sizeof(double) * 2 * B, cudaHostAllocMapped));
+    std::memset(p->h_out, 0, sizeof(double) * gpm::BatchStrides::OUT * B);
+    std::memset(p->h_done, 0, sizeof(double) * 2 * B);
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&p->d_out_host), p->h_out, 0));
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&p->d_done_host), p->h_done, 0));
     CK(cudaMallocHost(&p->h_infeasible, sizeof(int) * B));
     for (auto& e : p->ev) CK(cudaEventCreate(&e));
     CK(cudaStreamSynchronize(p->stream));
@@ -1295,6 +1313,21 @@ void enqueue_tick(gpmppi_planner* p, bool capturing) {
   };
   rec(p->ev[1], p->stream);  // device start of the tick (plan_ms in command-first mode)
   enqueue_h2d(p);
+  if (p->zero_copy) {
+    // the reduce (or finish) kernel and the covariance kernel publish into mapped pinned
+    // memory; no copies or events sit between the tick's kernels and the host
+    p->zc_tick = true;
+    try {
+      enqueue_update(p, nullptr);
+      enqueue_tighten(p);
+    } catch (...) {
+      p->zc_tick = false;
+      throw;
+    }
+    p->zc_tick = false;
+    rec(p->ev[2], p->stream);
+    return;
+  }
   enqueue_update(p, nullptr);
   // the command / diagnostics readback forks off onto the side stream, so the tightening
   // follows the reduction directly on the main stream (no copy on its critical path)
@@ -1302,15 +1335,36 @@ void enqueue_tick(gpmppi_planner* p, bool capturing) {
   CK(cudaStreamWaitEvent(p->side, p->fork_ev, 0));
   CK(cudaMemcpyAsync(p->h_out, p->d_out, sizeof(double) * gpm::BatchStrides::OUT * p->B, cudaMemcpyDeviceToHost,
                      p->side));
-  if (capturing)
-    CK(cudaEventRecordWithFlags(p->ev[0], p->side, cudaEventRecordExternal));
-  else
-    CK(cudaEventRecord(p->ev[0], p->side));
+  rec(p->ev[0], p->side);
   CK(cudaEventRecord(p->join_ev, p->side));
   enqueue_tighten(p);
   CK(cudaStreamWaitEvent(p->stream, p->join_ev, 0));
   CK(cudaMemcpyAsync(p->h_infeasible, p->d_infeasible, sizeof(int) * p->B, cudaMemcpyDeviceToHost, p->stream));
   rec(p->ev[2], p->stream);  // tightening and its readback done
+}
+
+// Spin until every robot's completion word (stride doubles apart, at `slot`) carries this
+// tick's sequence number. The stream is queried every few thousand spins so a failed
+// kernel surfaces as its CUDA error instead of a hang.
+void wait_host_words(gpmppi_planner* p, const double* words, int stride, int slot, const char* what) {
+  const volatile double* w = words;
+  for (unsigned it = 1;; ++it) {
+    bool all = true;
+    for (int b = 0; b < p->B && all; ++b) all = w[(size_t)b * stride + slot] == p->seq;
+    if (all) return;
+    if ((it & 4095u) == 0) {
+      const cudaError_t e = cudaStreamQuery(p->stream);
+      if (e != cudaSuccess && e != cudaErrorNotReady) throw CudaError{e, what};
+      if (e == cudaSuccess) {  // stream drained: the words must be there now
+        for (int b = 0; b < p->B; ++b)
+          if (w[(size_t)b * stride + slot] != p->seq) runtime(std::string(what) + ": completion word missing");
+        return;
+      }
+    }
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+  }
 }
 
 // Capture the tick into a graph (one launch instead of eight stream operations). Any
@@ -1375,7 +1429,10 @@ void plan_tick(gpmppi_planner* p, const double* x0, const gpmppi_task* tasks, do
   const double t_launch = ms_since(t0);
   {
     NvtxRange wait("gpmppi:wait command");
-    CK(cudaEventSynchronize(p->ev[0]));
+    if (p->zero_copy)
+      wait_host_words(p, p->h_out, gpm::BatchStrides::OUT, gpm::BatchStrides::OUT - 1, "plan_step (command)");
+    else
+      CK(cudaEventSynchronize(p->ev[0]));
   }
   const double t_cmd = ms_since(t0);
   if (p->command_first) {
@@ -1393,7 +1450,10 @@ void plan_tick(gpmppi_planner* p, const double* x0, const gpmppi_task* tasks, do
   } else {
     {
       NvtxRange wait("gpmppi:wait tightening");
-      CK(cudaStreamSynchronize(p->stream));
+      if (p->zero_copy)
+        wait_host_words(p, p->h_done, 2, 1, "plan_step (tightening)");
+      else
+        CK(cudaStreamSynchronize(p->stream));
     }
     fill_diag(p, command, diag, t_cmd, ms_since(t0));
   }
@@ -1410,7 +1470,7 @@ void finish_pending(gpmppi_planner* p, gpmppi_diag* diag) {
   if (cudaEventElapsedTime(&dev_ms, p->ev[1], p->ev[2]) != cudaSuccess) dev_ms = 0.f;
   for (int b = 0; b < p->B; ++b) {
     gpmppi_diag& d = p->pending_diag[b];
-    d.tightening_infeasible = p->h_infeasible[b];
+    d.tightening_infeasible = p->zero_copy ? (int)p->h_done[2 * b] : p->h_infeasible[b];
     d.plan_ms = std::max(d.plan_ms + (double)dev_ms, d.command_ms);
     if (diag) diag[b] = d;
   }

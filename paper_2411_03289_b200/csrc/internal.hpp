@@ -44,7 +44,8 @@ enum { NOISE_PHILOX = 0, NOISE_INJECTED = 1 };
 // with stride S starts at b*S.
 struct BatchStrides {
   // per-robot tick block: x0[0..4], [5] variance weight of the task, [6] Philox key
-  // (bit pattern), [7] pad -- one H2D copy stages everything a robot's tick needs
+  // (bit pattern), [7] the tick's sequence number (zero-copy completion words) -- one H2D
+  // copy stages everything a robot's tick needs
   static constexpr int X0 = 8;
   // terrain weights [kMaxTerrains], then the per-group variance coefficients
   // Σ_o w(o)² over each kernel group's outputs [kMaxGroups] (mppi.cpp:34-49; host-computed)
@@ -155,6 +156,7 @@ struct ReduceArgs {
   double* nominal_seq;    // [B][2T]
   double lo[2], hi[2];
   double* out;            // [B][16]: command, best, mean, ess, entropy, nonfinite, N
+  double* out_host;       // null, or mapped pinned [B][16]: the same + the tick's sequence in [15]
 };
 
 struct TightenArgs {
@@ -173,6 +175,7 @@ struct TightenArgs {
   double* r_bar;        // [B][T]
   double* margins;      // [B][T*kMaxObstacles]
   int* infeasible;      // [B]
+  double* done_host;    // null, or mapped pinned [B][2]: infeasible, tick sequence (x0 block [7])
   // scratch of the three-phase pass
   double* tq;         // [B][T][4] GP queries at the belief means
   double* tmu;        // [B][T+1][5] belief means
@@ -221,7 +224,8 @@ cudaError_t launch_variance(const VarianceArgs& a, int path, cudaStream_t st);
 cudaError_t launch_reduce(const ReduceArgs& a, int blocks, cudaStream_t st);
 cudaError_t launch_finish(const double* tuples, int n, int T, double lambda, double* nominal_seq,
                           const double lo[2], const double hi[2], double* out, long long K_total,
-                          double* combined, cudaStream_t st);
+                          double* combined, cudaStream_t st, double* out_host = nullptr,
+                          const double* x0_block = nullptr);
 // max_warps: warps per rollout block (8; 7 leaves the registers of a co-resident variance block)
 RolloutGeom rollout_geometry(int K_local, int B, int T, int n_pts, int G, int num_sms, int max_warps = 8);
 size_t rollout_launch_smem(const RolloutArgs& a, int* scratch_smem);

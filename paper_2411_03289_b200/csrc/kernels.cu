@@ -950,9 +950,18 @@ GPM_D void block_reduce_5(double v[5], double* red /*[32*5]*/) {
 
 // Apply a combined tuple: update + clamp (mppi.cpp:147-164), command (:430),
 // shift (:166-173), diagnostics (:435-455). Executed by one block.
+// Zero-copy completion word: the values land in pinned host memory (mapped), then -- after a
+// system-scope fence -- word `seq_slot` receives the tick's sequence number, which the host
+// polls instead of waiting on a copy and an event (latency of the command readback).
+GPM_D void publish_host(double* host, const double* v, int nv, int seq_slot, double seq) {
+  for (int i = 0; i < nv; ++i) host[i] = v[i];
+  __threadfence_system();
+  *reinterpret_cast<volatile double*>(host + seq_slot) = seq;
+}
+
 GPM_D void apply_tuple(const double* tup, int T, double lambda, double* nominal_seq,
                        const double lo[2], const double hi[2], double* out, long long K_total,
-                       double* tmp /*2T*/) {
+                       double* tmp /*2T*/, double* out_host = nullptr, double seq = 0.0) {
   const double Z = tup[1];
   for (int r = threadIdx.x; r < 2 * T; r += blockDim.x) {
     const double dv = Z > 0.0 ? tup[kTupleHead + r] / Z : 0.0;
@@ -973,6 +982,7 @@ GPM_D void apply_tuple(const double* tup, int T, double lambda, double* nominal_
     out[5] = Z > 0.0 ? log(Z) + H / (lambda * Z) : 0.0;                    // -Σ w ln w
     out[6] = (double)K_total - N;                                           // nonfinite
     out[7] = N;
+    if (out_host) publish_host(out_host, out, 8, BatchStrides::OUT - 1, seq);
   }
   __syncthreads();
 }
@@ -1212,7 +1222,8 @@ __global__ void __launch_bounds__(256, 1) reduce_kernel(const ReduceArgs a) {
   double* tmp = sc + BP;  // 2T doubles
   if (a.finish)
     apply_tuple(tup, T, a.lambda, a.nominal_seq + (size_t)b * BatchStrides::nom(T), a.lo, a.hi,
-                a.out + (size_t)b * BatchStrides::OUT, a.K_total, tmp);
+                a.out + (size_t)b * BatchStrides::OUT, a.K_total, tmp,
+                a.out_host ? a.out_host + (size_t)b * BatchStrides::OUT : nullptr, rt[7]);
 #ifdef GPM_REDUCE_TRACE
   RTR(7);
   if (threadIdx.x == 0)
@@ -1236,21 +1247,22 @@ cudaError_t launch_reduce(const ReduceArgs& a, int blocks, cudaStream_t st) {
 // Combine rank tuples (multi-GPU) and apply: one block.
 __global__ void finish_kernel(const double* tuples, int n, int T, double lambda,
                               double* nominal_seq, double lo0, double lo1, double hi0, double hi1,
-                              double* out, long long K_total, double* combined) {
+                              double* out, long long K_total, double* combined, double* out_host,
+                              const double* x0_block) {
   extern __shared__ __align__(16) double tmp[];
   if (threadIdx.x == 0) combine_tuples(tuples, n, T, lambda, combined);
   __syncthreads();
   __threadfence_block();
   const double lo[2] = {lo0, lo1}, hi[2] = {hi0, hi1};
-  apply_tuple(combined, T, lambda, nominal_seq, lo, hi, out, K_total, tmp);
+  apply_tuple(combined, T, lambda, nominal_seq, lo, hi, out, K_total, tmp, out_host, out_host ? x0_block[7] : 0.0);
 }
 
 cudaError_t launch_finish(const double* tuples, int n, int T, double lambda, double* nominal_seq,
                           const double lo[2], const double hi[2], double* out, long long K_total,
-                          double* combined, cudaStream_t st) {
+                          double* combined, cudaStream_t st, double* out_host, const double* x0_block) {
   finish_kernel<<<1, 128, sizeof(double) * 2 * T, st>>>(tuples, n, T, lambda, nominal_seq, lo[0],
                                                           lo[1], hi[0], hi[1], out, K_total,
-                                                          combined);
+                                                          combined, out_host, x0_block);
   count_launch();
   return cudaGetLastError();
 }
@@ -1858,7 +1870,13 @@ __global__ void __launch_bounds__(256, 1) tighten_cov_kernel(const TightenArgs a
       if (dbar <= 0.0) atomicOr(&infeasible, 1);
     }
   __syncthreads();
-  if (l == 0) a.infeasible[rb] = infeasible;
+  if (l == 0) {
+    a.infeasible[rb] = infeasible;
+    if (a.done_host) {  // zero-copy: infeasibility, then the tick's sequence number
+      const double v = (double)infeasible;
+      publish_host(a.done_host + 2 * (size_t)rb, &v, 1, 1, a.x0[(size_t)rb * BatchStrides::X0 + 7]);
+    }
+  }
 #ifdef GPM_TCOV_TRACE
   if (l == 0) printf("tcov: staging+cv %lld recursion %lld thresholds %lld\n", ct[1] - ct[0], ct[2] - ct[1], clock64() - ct[2]);
 #endif
