@@ -659,8 +659,9 @@ struct gpmppi_planner {
   double *d_tq = nullptr, *d_tmu = nullptr, *d_tJ = nullptr, *d_tvar = nullptr;
   double* d_scratch = nullptr;
   // pinned staging
-  gpm::TaskDev* h_task = nullptr;  // [B]
-  double* h_x0 = nullptr;          // [B][8] robot tick blocks
+  gpm::TaskDev* h_task = nullptr;  // [B] (inside the h_x0 block)
+  double* h_x0 = nullptr;          // [B][8] robot tick blocks, then the tasks
+  size_t tick_bytes = 0;
   double* h_out = nullptr;         // [B][16], mapped: the reduce writes command + diag + sequence here
   int* h_infeasible = nullptr;     // [B]
   double* h_done = nullptr;        // [B][2], mapped: tightening infeasibility + sequence
@@ -715,8 +716,7 @@ struct gpmppi_planner {
     if (stream) cudaStreamSynchronize(stream);
     for (void* p : allocs) cudaFree(p);
     for (void* p : sample_allocs) cudaFree(p);
-    if (h_task) cudaFreeHost(h_task);
-    if (h_x0) cudaFreeHost(h_x0);
+    if (h_x0) cudaFreeHost(h_x0);  // h_task lives in the same pinned block
     if (h_out) cudaFreeHost(h_out);
     if (h_infeasible) cudaFreeHost(h_infeasible);
     if (h_done) cudaFreeHost(h_done);
@@ -976,10 +976,8 @@ void stage_tick(gpmppi_planner* p, const double* x0, const gpmppi_task* tasks) {
 }
 
 // the tick's two H2D copies from the pinned staging buffers (captured in the tick graph)
-void enqueue_h2d(gpmppi_planner* p) {
-  CK(cudaMemcpyAsync(p->d_task, p->h_task, sizeof(gpm::TaskDev) * p->B, cudaMemcpyHostToDevice, p->stream));
-  CK(cudaMemcpyAsync(p->d_x0, p->h_x0, sizeof(double) * gpm::BatchStrides::X0 * p->B,
-                     cudaMemcpyHostToDevice, p->stream));
+void enqueue_h2d(gpmppi_planner* p) {  // tick blocks + tasks: one copy (contiguous on both sides)
+  CK(cudaMemcpyAsync(p->d_x0, p->h_x0, p->tick_bytes, cudaMemcpyHostToDevice, p->stream));
 }
 
 // Rollout + variance + reduce for every robot's sample range. finish=1 also
@@ -1265,10 +1263,15 @@ gpmppi_planner* create_planner(const gpmppi_mppi_config* cfg, const gpmppi_predi
     CK(cudaMemcpyAsync(p->d_nom, nom0.data(), sizeof(double) * nom0.size(), cudaMemcpyHostToDevice, p->stream));
     p->d_tw = p->dalloc<double>((size_t)B * gpm::BatchStrides::TW);
     upload_terrain_weights(p);
-    p->d_x0 = p->dalloc<double>((size_t)B * gpm::BatchStrides::X0);
+    // tick blocks [B][8] and tasks [B] in one device block (and one pinned block): the tick's
+    // inputs move in a single H2D copy
+    const size_t x0_bytes = sizeof(double) * gpm::BatchStrides::X0 * B;
+    p->tick_bytes = x0_bytes + sizeof(gpm::TaskDev) * B;
+    unsigned char* dblk = p->dalloc<unsigned char>(p->tick_bytes);
+    p->d_x0 = reinterpret_cast<double*>(dblk);
     p->d_rbar = p->dalloc<double>((size_t)B * gpm::BatchStrides::rbar(T));
     p->d_margins = p->dalloc<double>((size_t)B * gpm::BatchStrides::marg(T));
-    p->d_task = p->dalloc<gpm::TaskDev>(B);
+    p->d_task = reinterpret_cast<gpm::TaskDev*>(dblk + x0_bytes);
     p->d_rank_tuple = p->dalloc<double>((size_t)B * gpm::tuple_doubles(T));
     p->d_combined = p->dalloc<double>(gpm::tuple_doubles(T));
     p->d_out = p->dalloc<double>((size_t)B * gpm::BatchStrides::OUT);
@@ -1284,8 +1287,8 @@ gpmppi_planner* create_planner(const gpmppi_mppi_config* cfg, const gpmppi_predi
       p->d_tvar = p->dalloc<double>((size_t)B * T * G * ns);
     }
     p->alloc_sample_buffers();
-    CK(cudaMallocHost(&p->h_task, sizeof(gpm::TaskDev) * B));
-    CK(cudaMallocHost(&p->h_x0, sizeof(double) * gpm::BatchStrides::X0 * B));
+    CK(cudaMallocHost(&p->h_x0, p->tick_bytes));
+    p->h_task = reinterpret_cast<gpm::TaskDev*>(reinterpret_cast<unsigned char*>(p->h_x0) + x0_bytes);
     CK(cudaHostAlloc(&p->h_out, sizeof(double) * gpm::BatchStrides::OUT * B, cudaHostAllocMapped));
     CK(cudaHostAlloc(&p->h_done, sizeof(double) * 2 * B, cudaHostAllocMapped));
     std::memset(p->h_out, 0, sizeof(double) * gpm::BatchStrides::OUT * B);
