@@ -1466,11 +1466,75 @@ __global__ void __launch_bounds__(TMEAN_THREADS, 1) tighten_mean_kernel(const Ti
 #else
 #define TRC(i)
 #endif
+  // One kernel group and n <= 4 * TMEAN_THREADS (configs 1, 2, 4, 5): every thread keeps its
+  // four points' Z / alpha in registers for the whole chain, and the control-dependent part of
+  // each exponent, q2 z2 + q3 z3 + zn - (q2^2 + q3^2)/2, is formed for step k+1 while step k's
+  // partial sums cross the barrier -- the serial path per step is 2 FMAs + the exp per point.
+  const bool reg_path = G == 1 && n <= 4 * TMEAN_THREADS;
+  double rz0[4], rz1[4], rz2[4], rz3[4], rzn[4], rav[4], raw[4], e_cur[4];
+  if (reg_path) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int j = threadIdx.x + i * TMEAN_THREADS;
+      const bool in = j < n;
+      rz0[i] = in ? pts[j] : 0.0;
+      rz1[i] = in ? pts[ns + j] : 0.0;
+      rz2[i] = in ? pts[2 * ns + j] : 0.0;
+      rz3[i] = in ? pts[3 * ns + j] : 0.0;
+      rzn[i] = in ? pts[4 * ns + j] : -1e300;  // exp_tab flushes to 0
+      rav[i] = in ? pts[5 * ns + j] : 0.0;
+      raw[i] = in ? pts[6 * ns + j] : 0.0;
+    }
+    const double q2 = nom[0] * gil[0][2], q3 = nom[1] * gil[0][3];
+    const double qu = -0.5 * (q2 * q2 + q3 * q3);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) e_cur[i] = fma(q2, rz2[i], fma(q3, rz3[i], rzn[i] + qu));
+  }
   for (int k = 0; k < T; ++k) {
     TRC(0);
     const double u0 = nom[2 * k], u1 = nom[2 * k + 1];
     double c0 = 0.0, c1 = 0.0;
-    if (G > 0) {
+    if (reg_path) {
+      const double q0 = v * gil[0][0], q1 = om * gil[0][1];
+      const double qv = -0.5 * (q0 * q0 + q1 * q1);
+      double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double kj = exp_tab(fma(q0, rz0[i], fma(q1, rz1[i], e_cur[i] + qv)), etab);
+        acc0 = fma(kj, rav[i], acc0);
+        acc1 = fma(kj, raw[i], acc1);
+      }
+      TRC(1);
+      {  // transpose-reduce the two sums across the warp (5 shuffles), as below
+        const bool b4 = lane & 16;
+        double y = (b4 ? acc1 : acc0) + __shfl_xor_sync(0xffffffffu, b4 ? acc0 : acc1, 16);
+        y += __shfl_xor_sync(0xffffffffu, y, 8);
+        y += __shfl_xor_sync(0xffffffffu, y, 4);
+        y += __shfl_xor_sync(0xffffffffu, y, 2);
+        y += __shfl_xor_sync(0xffffffffu, y, 1);
+        if ((lane & 15) == 0) red[k & 1][0][w][lane >> 4] = y;
+      }
+      TRC(2);
+      if (k + 1 < T) {  // next step's control part, in the shadow of the barrier
+        const double q2 = nom[2 * k + 2] * gil[0][2], q3 = nom[2 * k + 3] * gil[0][3];
+        const double qu = -0.5 * (q2 * q2 + q3 * q3);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) e_cur[i] = fma(q2, rz2[i], fma(q3, rz3[i], rzn[i] + qu));
+      }
+      __syncthreads();
+      TRC(3);
+      double2 pr[TMEAN_THREADS / 32];
+#pragma unroll
+      for (int q = 0; q < TMEAN_THREADS / 32; ++q) pr[q] = *reinterpret_cast<const double2*>(&red[k & 1][0][q][0]);
+      double x0 = pr[0].x, x1 = pr[0].y;
+#pragma unroll
+      for (int q = 1; q < TMEAN_THREADS / 32; ++q) {
+        x0 += pr[q].x;
+        x1 += pr[q].y;
+      }
+      c0 = x0;
+      c1 = x1;
+    } else if (G > 0) {
       const double* p = pts;
       for (int g = 0; g < G; ++g) {
         const double q0 = v * gil[g][0], q1 = om * gil[g][1];
