@@ -156,8 +156,13 @@ def roofline_block(w, phase, steps, peaks, peaks_kind, var_path=3):
     tick_ms = sum(phase) / steps
     # 3xFP16 / 3xTF32 issue three tensor products per algorithmic MAC; FP16 runs at the bf16
     # dense rate, TF32 at half of it
-    if var_path == 3:
-        var = {"kernel": "variance_f16_kernel", "bound": "tensor", "peak": bf16, "unit": "TFLOP/s",
+    if var_path in (3, 4):
+        # the CTA-pair kernel (tcgen05 cta_group::2) is path 4, and path 3's choice at n_pad >= 1024
+        # or at <= 16 super-tiles (256 queries) per CTA pair (kernels_tc.cu launch_tc_variance)
+        n_pad = (n + 15) // 16 * 16
+        pair = var_path == 4 or n_pad >= 1024 or (n_pad > 256 and -(-units // 256) <= 16 * 74)
+        var = {"kernel": "variance_f16x2_kernel" if pair else "variance_f16_kernel", "bound": "tensor",
+               "peak": bf16, "unit": "TFLOP/s",
                "peak_kind": f"{peaks_kind} fp16 dense = bf16 dense burst (MEASURED_PEAKS.json)"}
     elif var_path in (1, 2):
         var = {"kernel": "variance_tc2u_kernel", "bound": "tensor", "peak": bf16 / 2, "unit": "TFLOP/s",
@@ -167,7 +172,7 @@ def roofline_block(w, phase, steps, peaks, peaks_kind, var_path=3):
                "peak": 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12,
                "peak_kind": "fp32 spec (148 SM x 128 FFMA x 2 x max clock)"}
     var.update({"launch_ms": var_ms, "flop_per_launch": units * (n * n + 3 * n),
-                "tensor_issue_factor": 3 if var_path in (1, 3) else 1})
+                "tensor_issue_factor": 3 if var_path in (1, 3, 4) else 1})
     roll = {"kernel": "rollout_gp_kernel", "bound": "fp64", "peak": fp64, "unit": "TFLOP/s",
             "peak_kind": fp64_kind, "launch_ms": roll_ms, "flop_per_launch": units * 22 * n,
             "binding_resource": "FP64 pipe + shared-memory wavefronts + issue (ncu at config2: FP64 51%, "

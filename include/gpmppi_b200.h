@@ -220,7 +220,13 @@ int gpmppi_planner_flags(const gpmppi_planner* p, uint8_t* viol, uint8_t* coll,
  * TC_1XTF32: one TF32 product (not a parity path). TC_3XF16 (default): tcgen05 kind::f16
  * on scaled hi/lo FP16 operands -- the same 22-bit splits at twice the TF32 rate.
  * Measured bounds: tests/test_gpu_variance_paths.py. */
-enum { GPMPPI_VAR_FFMA = 0, GPMPPI_VAR_TC_3XTF32 = 1, GPMPPI_VAR_TC_1XTF32 = 2, GPMPPI_VAR_TC_3XF16 = 3 };
+enum {
+  GPMPPI_VAR_FFMA = 0,
+  GPMPPI_VAR_TC_3XTF32 = 1,
+  GPMPPI_VAR_TC_1XTF32 = 2,
+  GPMPPI_VAR_TC_3XF16 = 3,
+  GPMPPI_VAR_TC_3XF16_PAIR = 4 /* CTA pairs (tcgen05 cta_group::2, M = 256) */
+};
 int gpmppi_planner_set_variance_path(gpmppi_planner* p, int path);
 int gpmppi_planner_variance_path(const gpmppi_planner* p);
 

@@ -9,7 +9,8 @@ from .gpmppi import (  # noqa: F401
     kernel_launches, nccl_unique_id, shard_range, tuple_doubles, RolloutResult, rollout, sample_perturbations,
     trajectory_weights, update_controls, shift_horizon, TrainedModels, load_models, save_models)
 from ._capi import (  # noqa: F401
-    NOISE_INJECTED, NOISE_PHILOX, VAR_FFMA, VAR_TC_1XTF32, VAR_TC_3XF16, VAR_TC_3XTF32, CudaError)
+    NOISE_INJECTED, NOISE_PHILOX, VAR_FFMA, VAR_TC_1XTF32, VAR_TC_3XF16, VAR_TC_3XF16_PAIR, VAR_TC_3XTF32,
+    CudaError)
 
 from .harness import (  # noqa: F401
     ExperimentConfig, HistoryBuffer, RunMetrics, Scenario, TerrainProfile, WeightSolverConfig,

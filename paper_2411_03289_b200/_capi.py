@@ -21,7 +21,7 @@ OK, INVALID_ARGUMENT, RUNTIME_ERROR, LOGIC_ERROR, CUDA_ERROR = 0, 1, 2, 3, 4
 MODEL_GP_ENSEMBLE, MODEL_EDD5, MODEL_UNICYCLE, MODEL_NOMINAL = 0, 1, 2, 3
 TASK_TRACKING, TASK_AVOIDANCE, TASK_COMBINED = 0, 1, 2
 NOISE_PHILOX, NOISE_INJECTED = 0, 1
-VAR_FFMA, VAR_TC_3XTF32, VAR_TC_1XTF32, VAR_TC_3XF16 = 0, 1, 2, 3
+VAR_FFMA, VAR_TC_3XTF32, VAR_TC_1XTF32, VAR_TC_3XF16, VAR_TC_3XF16_PAIR = 0, 1, 2, 3, 4
 MAX_WAYPOINTS = 64
 MAX_OBSTACLES = 64
 MAX_TERRAINS = 16

@@ -396,6 +396,9 @@ gpmppi_model* build_model(const double* X, const double* Y, int64_t n64, int64_t
         gpm::build_tc_operand_f16(G.ilt.data(), n, G.kernel[0], D.tc_npad, D.tc_np, D.tc_npass, tch, tchm, D.tc_hfac);
         D.tc_h = M->upload(tch);
         D.tc_hmeta = M->upload(tchm);
+        gpm::build_tc_operand_f16x2(G.ilt.data(), n, G.kernel[0], D.tc_npad, tch, tchm, D.tc_npass2);
+        D.tc_h2 = M->upload(tch);
+        D.tc_h2meta = M->upload(tchm);
       }
       for (int d = 0; d < 4; ++d) D.ls[d] = G.kernel[1 + d];
       D.sv = G.kernel[0];
@@ -574,7 +577,7 @@ int gpmppi_model_predict_batch(const gpmppi_model* M, const double* q, int64_t S
 int gpmppi_model_variance_batch(const gpmppi_model* M, const double* q, int64_t S, int path,
                                 double* var) {
   if (!M) return fail(GPMPPI_LOGIC_ERROR, "GpModel::predict_batch: model not fitted");
-  if (S < 0 || path < 0 || path > 3) return fail(GPMPPI_INVALID_ARGUMENT, "variance_batch: bad arguments");
+  if (S < 0 || path < 0 || path > 4) return fail(GPMPPI_INVALID_ARGUMENT, "variance_batch: bad arguments");
   if (S == 0) return GPMPPI_OK;
   return guarded([&] {
     CK(cudaSetDevice(M->device));
@@ -1716,7 +1719,7 @@ int gpmppi_planner_flags(const gpmppi_planner* p, uint8_t* viol, uint8_t* coll, 
 
 int gpmppi_planner_set_variance_path(gpmppi_planner* p, int path) {
   if (!p) return fail(GPMPPI_INVALID_ARGUMENT, "null planner");
-  if (path < 0 || path > 3) return fail(GPMPPI_INVALID_ARGUMENT, "unknown variance path");
+  if (path < 0 || path > 4) return fail(GPMPPI_INVALID_ARGUMENT, "unknown variance path");
   p->var_path = path;
   return GPMPPI_OK;
 }

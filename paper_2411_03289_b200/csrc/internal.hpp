@@ -26,6 +26,9 @@ struct GroupDev {
   const uint16_t* tc_h;  // 3xFP16 operand: scaled L^{-T} hi/lo FP16 blocks (build_tc_operand_f16)
   const int4* tc_hmeta;  // per (pass, chunk): fp16 offset, ncols, col0
   double tc_hfac;        // (sf2 / operand scale)^2
+  const uint16_t* tc_h2;   // CTA-pair 3xFP16 operand (build_tc_operand_f16x2): per (512-column pass,
+  const int4* tc_h2meta;   // chunk) one record [CTA0 part | CTA1 part]; meta .x offset, .w part size
+  int tc_npass2;           // 512-column passes
   double ls[4];
   double sv, log_sv;
   int n_out;
@@ -252,6 +255,29 @@ size_t rollout_smem_bytes(const RolloutArgs& a);
 size_t rollout_scratch_doubles(int T, int num_sms);
 int reduce_blocks_for(int K_local, int B, int num_sms, int T);
 int tighten_splits(int n, int B);
+// CTA-pair variance columns: pass p covers columns [512p, 512p + 512) as two halves of
+// <= 256 (TMEM columns [0, 256) and [256, 512)); chunk kb (points [16kb, 16kb + 16))
+// reaches the columns from its diagonal on, rounded down to 32 so each CTA of the pair
+// holds a multiple of 16 B rows. c0[h] = first column of half h, nc[h] = N of its MMA
+// (0 = the chunk does not reach the half). Shared by the host builder and the kernel.
+#ifndef GPM_PAIR_GRAN
+#define GPM_PAIR_GRAN 32  // column granularity of the triangle skip (a compile-time power of two)
+#endif
+GPM_HD void pair2_cols(int p, int kb, int n_pad, int* c0, int* nc) {
+  const int npw = n_pad - 512 * p < 512 ? n_pad - 512 * p : 512;
+  const int rel = 16 * kb - 512 * p;
+  for (int h = 0; h < 2; ++h) {
+    int w = npw - 256 * h;
+    w = w < 0 ? 0 : (w > 256 ? 256 : w);
+    const int r = rel - 256 * h;
+    const int c = r <= 0 ? 0 : (r & ~(GPM_PAIR_GRAN - 1));
+    const int wr = (w + 31) & ~31;
+    c0[h] = c;
+    nc[h] = (w > 0 && c < w) ? wr - c : 0;
+  }
+}
+void build_tc_operand_f16x2(const double* ilt, int n, double sv, int n_pad, std::vector<uint16_t>& data,
+                            std::vector<int4>& meta, int& n_pass2);
 void build_tc_operand_f16(const double* ilt, int n, double sv, int n_pad, int np, int n_pass,
                           std::vector<uint16_t>& data, std::vector<int4>& meta, double& hfac);
 void build_tc_operand(const double* ilt, int n, std::vector<float>& data, std::vector<int4>& meta,

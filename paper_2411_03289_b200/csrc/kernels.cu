@@ -904,7 +904,7 @@ cudaError_t launch_tc_variance(const VarianceArgs& a, int mode, cudaStream_t st)
 
 cudaError_t launch_variance(const VarianceArgs& a, int path, cudaStream_t st) {
   if (a.KT <= 0) return cudaSuccess;
-  if (path != 0) return launch_tc_variance(a, path == 3 ? 2 : path == 2 ? 1 : 0, st);
+  if (path != 0) return launch_tc_variance(a, path == 4 ? 3 : path == 3 ? 2 : path == 2 ? 1 : 0, st);
   const long long blocks = (a.KT + VQ - 1) / VQ;
   variance_ffma_kernel<<<(unsigned)blocks, 256, 0, st>>>(a);
   count_launch();

@@ -42,6 +42,12 @@ constexpr int KB = 8;       // points per B block (one K=8 TF32 MMA step)
 constexpr int STAGES_B = 4; // L^{-T} ring (<= 32 KB per stage), 5 when shared memory allows
 constexpr int PRODUCER_WARPS = 8;
 constexpr int THREADS = 256 + 32 * PRODUCER_WARPS;
+#ifndef GPM_F16_PW
+#define GPM_F16_PW 8
+#endif
+constexpr int F16_PW = GPM_F16_PW;             // variance_f16_kernel producer warps (8 or 16)
+constexpr int F16_RPL = 32 / F16_PW;           // rows per producer lane (4 or 2)
+constexpr int F16_THREADS = 256 + 32 * F16_PW;
 constexpr int A_STAGE_FLOATS = M * KC;       // per hi or lo
 constexpr int SBO = (KC / 4) * 128;          // A: bytes between 8-row groups
 constexpr int SBO_B = (KB / 4) * 128;        // B: bytes between 8-row groups
@@ -328,14 +334,22 @@ __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t* r) {
 // per-role cycle counters (diagnostics, env GPMPPI_TC_DEBUG bit 512)
 __device__ unsigned long long g_prof[16];
 __device__ unsigned long long g_trace[64];  // CTA 0 timeline (dbg 4096)
+// Diagnostic switches of the tensor-core variance kernels (GPMPPI_TC_DEBUG bits) exist only
+// in a -DGPM_TC_DIAG build: every runtime test on the MMA issuer's path is measurable (one
+// integer division per stage there cost the CTA-pair kernel 30%).
+#ifdef GPM_TC_DIAG
+#define GPM_DIAG(x) (x)
+#else
+#define GPM_DIAG(x) false
+#endif
 __device__ __forceinline__ void trace_at(int i, int dbg) {
-  if ((dbg & 4096) && blockIdx.x == 0 && i < 64) g_trace[i] = clock64();
+  if (GPM_DIAG(dbg & 4096) && blockIdx.x == 0 && i < 64) g_trace[i] = clock64();
 }
 __device__ __forceinline__ void prof_add(int slot, unsigned long long v, int dbg) {
-  if (dbg & 512) atomicAdd(&g_prof[slot], v);
+  if (GPM_DIAG(dbg & 512)) atomicAdd(&g_prof[slot], v);
 }
 __device__ __forceinline__ void mbar_wait_prof(uint32_t bar, uint32_t parity, int slot, int dbg) {
-  if (!(dbg & 512)) {
+  if (!GPM_DIAG(dbg & 512)) {
     mbar_wait(bar, parity);
     return;
   }
@@ -984,12 +998,21 @@ __device__ __forceinline__ void mma_f16_pair_3x(uint32_t d, uint32_t dt, uint64_
       "add.u32 d1, %0, %1;\n\t"
       "setp.ne.b32 p, %9, 0;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
+#ifdef GPM_MMA_INTERLEAVE  // alternate the two tiles' accumulators between dependent MMAs
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %6, %8, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [d1], %4, %6, %8, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %7, %8, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [d1], %4, %7, %8, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %3, %6, %8, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [d1], %5, %6, %8, 1;\n\t"
+#else
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %6, %8, p;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %7, %8, 1;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %3, %6, %8, 1;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [d1], %4, %6, %8, p;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [d1], %4, %7, %8, 1;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [d1], %5, %6, %8, 1;\n\t"
+#endif
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%10];\n\t}" ::"r"(d),
       "r"(dt), "l"(a0h), "l"(a0l), "l"(a1h), "l"(a1l), "l"(bh), "l"(bl), "r"(idesc), "r"(acc), "r"(bar)
       : "memory");
@@ -1028,7 +1051,7 @@ __device__ __forceinline__ uint32_t half2_bits(__half2 h) {
 }
 }  // namespace tc
 
-__global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const VarianceArgs a, int dbg, int S) {
+__global__ void __launch_bounds__(tc::F16_THREADS, 1) variance_f16_kernel(const VarianceArgs a, int dbg, int S) {
   using namespace tc;
   pdl_trigger();
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -1064,7 +1087,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const Vari
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(smem_u32(&full[s]), PRODUCER_WARPS + 1);
+      mbar_init(smem_u32(&full[s]), F16_PW + 1);
       mbar_init(smem_u32(&empty[s]), 1);
     }
     mbar_init(smem_u32(tfull), 1);
@@ -1097,7 +1120,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const Vari
           mbar_wait(smem_u32(&empty[r.s]), r.ph ^ 1);
           const uint32_t bytes = (uint32_t)meta.y * KC * 2 * 2;
           const uint32_t fb = smem_u32(&full[r.s]);
-          if (dbg & 1) {  // diagnostics: no operand copy
+          if (GPM_DIAG(dbg & 1)) {  // diagnostics: no operand copy
             mbar_arrive(fb);
           } else {
             mbar_arrive_tx(fb, bytes);
@@ -1120,13 +1143,13 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const Vari
         const int npw = min(NP, n_pad - p * NP);
         for (int kb = 0; kb < nk; ++kb, r.next()) {
           mbar_wait(smem_u32(&full[r.s]), r.ph);
-          const int col0 = max(0, kb * KC - p * NP);
+          const int col0 = GPM_DIAG(dbg & 16) ? 0 : max(0, kb * KC - p * NP);  // dbg 16: full-width MMAs
           const int ncols = npw - col0;
           const uint32_t st = smem_u32(stg + (size_t)r.s * stage_bytes);
           const uint32_t bh = st + A_BYTES;
           const uint32_t bl = bh + (uint32_t)ncols * KC * 2;
           const uint32_t bar = smem_u32(&empty[r.s]);
-          if (dbg & 4) {
+          if (GPM_DIAG(dbg & 4)) {
             mma_commit(bar);
             continue;
           }
@@ -1146,20 +1169,22 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const Vari
     }
     if (lane == 0) trace_at(60, dbg);
   } else if (warp >= 8) {
-    // ---------------- A producers (lane = 4 rows x 4 points, as variance_tc2u_kernel):
-    // k*/sf2 split into FP16 hi + lo, 8-byte stores covering 256 contiguous bytes per warp
+    // ---------------- A producers: k*/sf2 split into FP16 hi + lo, 8-byte stores covering 256
+    // contiguous bytes per warp; F16_PW / 2 warps per tile, lane = F16_RPL rows x 4 points
+    constexpr int WPT = F16_PW / 2;            // warps per tile
+    constexpr int RPW = M / WPT;               // rows per warp (32 or 16)
     const int pw = warp - 8;
-    const int t = pw >> 2;
+    const int t = pw / WPT;
     const int qi = lane & 7, pg = lane >> 3;
-    const int mb = (pw & 3) * 32 + qi;
+    const int mb = (pw % WPT) * RPW + qi;
     Ring r(S);
     int ti = 0;
     for (int t0 = tb; t0 < te; t0 += 2, ++ti) {
       if (pw == 0 && lane == 0 && ti < 10) trace_at(36 + ti, dbg);
       const bool present = t0 + t < te;
-      float qq[4][5];
+      float qq[F16_RPL][5];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < F16_RPL; ++j) {
         const long long q = (long long)(t0 + t) * M + mb + 8 * j;
         const bool valid = present && q < a.KT;
         const float4 qv = valid ? a.queries[q] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1171,9 +1196,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const Vari
                                           qq[j][3] * qq[j][3])
                          : -1e30f;
       }
-      unsigned long long qp[4][5];  // query terms duplicated into both halves of a pair
+      unsigned long long qp[F16_RPL][5];  // query terms duplicated into both halves of a pair
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < F16_RPL; ++j)
 #pragma unroll
         for (int c = 0; c < 5; ++c) qp[j][c] = f2_pack(qq[j][c], qq[j][c]);
       for (int p = 0; p < n_pass; ++p) {
@@ -1181,7 +1206,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const Vari
         for (int kb = 0; kb < nk; ++kb, r.next()) {
           if (lane == 0) mbar_wait(smem_u32(&empty[r.s]), r.ph ^ 1);
           __syncwarp();
-          if (present && !(dbg & 256)) {
+          if (present && !GPM_DIAG(dbg & 256)) {
             unsigned char* ahi = stg + (size_t)r.s * stage_bytes + (size_t)t * 2 * H_TILE_BYTES;
             unsigned char* alo = ahi + H_TILE_BYTES;
             const int i0 = kb * KC + pg * 4;
@@ -1195,7 +1220,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const Vari
                 {f2_pack(z0.x, z0.y), f2_pack(z1.x, z1.y), f2_pack(z2.x, z2.y), f2_pack(z3.x, z3.y), f2_pack(zq.x, zq.y)},
                 {f2_pack(z0.z, z0.w), f2_pack(z1.z, z1.w), f2_pack(z2.z, z2.w), f2_pack(z3.z, z3.w), f2_pack(zq.z, zq.w)}};
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < F16_RPL; ++j) {
               float kv[4];
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
@@ -1212,7 +1237,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const Vari
               const __half2 l01 = __floats2half2_rn(kv[0] - f01.x, kv[1] - f01.y);
               const __half2 l23 = __floats2half2_rn(kv[2] - f23.x, kv[3] - f23.y);
               // row m = mb + 8j, points 4pg..4pg+3: byte (m>>3)*256 + (pg>>1)*128 + (m&7)*16 + (pg&1)*8
-              const int off = (((pw & 3) * 32 + 8 * j) >> 3) * H_SBO + (pg >> 1) * 128 + qi * 16 + (pg & 1) * 8;
+              const int off = (((pw % WPT) * RPW + 8 * j) >> 3) * H_SBO + (pg >> 1) * 128 + qi * 16 + (pg & 1) * 8;
               *reinterpret_cast<uint2*>(ahi + off) = make_uint2(half2_bits(h01), half2_bits(h23));
               *reinterpret_cast<uint2*>(alo + off) = make_uint2(half2_bits(l01), half2_bits(l23));
             }
@@ -1237,7 +1262,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const Vari
         if (lane == 0 && e == 0 && uc < 10) trace_at(24 + (int)uc, dbg);
         __syncwarp();
         tc_after();
-        for (int tt = 0; tt < ntile; ++tt) {
+        for (int tt = 0; tt < (GPM_DIAG(dbg & 8) ? 0 : ntile); ++tt) {  // dbg 8: no TMEM drain
           const uint32_t trow = tmem_base + ((uint32_t)(e * 32) << 16) + (uint32_t)(tt * NP);
           double ssq = 0.0;
           int c = 0;
@@ -1285,6 +1310,399 @@ __global__ void __launch_bounds__(tc::THREADS, 1) variance_f16_kernel(const Vari
   if (threadIdx.x == 0) trace_at(63, dbg);
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// CTA-pair 3xFP16 variance (tcgen05.mma.cta_group::2, UMMA M = 256). Two CTAs of a
+// cluster form one 256-row super-tile: each generates k*/sf2 for its own 128 query rows
+// (the A operand is M-split across the pair) and holds half of every L^{-T} column block
+// (the B operand is N-split), so one pass reaches 512 columns -- two N <= 256 MMAs into
+// TMEM columns [0, 256) and [256, 512) of each CTA -- where the single-CTA kernel stops
+// at 256. At n = 512 the k* chunks are generated once per tile instead of 1.5 times (48 ->
+// 32 chunks), at n = 2048 320 instead of 576: the exponential producers, which bound the
+// single-CTA kernel, do 33-44% less work for the same tensor work.
+// Roles (both CTAs): w0 lane 0 bulk-copies the CTA's half of each L^{-T} chunk, w1 issues
+// the MMAs (leader) or relays the CTA's stage-full to the leader (peer), w2 owns TMEM,
+// w4-7 drain TMEM, w8-15 produce A (lane = 2 rows x 4 points). The leader's full barrier
+// counts its own producers + copy + the peer relay; MMA completion is multicast to both
+// CTAs' empty / tfull barriers; both CTAs' epilogues arrive on the leader's tempty.
+namespace tc {
+constexpr int P2_PRODUCER_WARPS = 8;
+constexpr int P2_THREADS = 256 + 32 * P2_PRODUCER_WARPS;
+constexpr int P2_A_BYTES = 2 * H_TILE_BYTES;         // this CTA's 128 rows: hi, lo
+constexpr int P2_B_BYTES = 2 * 2 * (M / 1) * KC * 2;  // two halves x (hi, lo) x <= 128 rows
+constexpr int P2_STAGE = P2_A_BYTES + P2_B_BYTES;      // 24 KB
+__device__ __forceinline__ uint32_t instr_desc_f16_m256(int n) {
+  return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t map_rank(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// a wait that outlives ~2^26 polls (seconds) is a protocol bug: trap instead of hanging
+// the device
+__device__ __forceinline__ void mbar_wait_x(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  for (uint32_t spins = 0;; ++spins) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (spins > (1u << 26)) {
+      printf("variance_f16x2_kernel: barrier wait timed out (block %d thread %d)\n", blockIdx.x, threadIdx.x);
+      __trap();
+    }
+  }
+}
+__device__ __forceinline__ void mbar_wait_xp(uint32_t bar, uint32_t parity, int slot, int dbg) {
+  if (!GPM_DIAG(dbg & 512)) {
+    mbar_wait_x(bar, parity);
+    return;
+  }
+  const unsigned long long t0 = clock64();
+  mbar_wait_x(bar, parity);
+  if ((threadIdx.x & 31) == 0) prof_add(slot, clock64() - t0, dbg);
+}
+__device__ __forceinline__ void mma2_f16_3x(uint32_t d, uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl,
+                                            uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %3, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %4, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %2, %3, %5, 1;\n\t}" ::"r"(d),
+      "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_f16_3x_pair(uint32_t d0, uint32_t d1, uint64_t ah, uint64_t al, uint64_t bh0,
+                                                 uint64_t bl0, uint64_t bh1, uint64_t bl1, uint32_t id0, uint32_t id1,
+                                                 uint32_t acc) {  // both halves, accumulators alternating
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %10, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %2, %4, %8, p;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%1], %2, %6, %9, p;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %2, %5, %8, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%1], %2, %7, %9, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %3, %4, %8, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%1], %3, %6, %9, 1;\n\t}" ::"r"(d0),
+      "r"(d1), "l"(ah), "l"(al), "l"(bh0), "l"(bl0), "l"(bh1), "l"(bl1), "r"(id0), "r"(id1), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_commit_both(uint32_t bar) {  // arrive on `bar` in both CTAs
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .b16 m;\n\t"
+      "mov.b16 m, 3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+          bar)
+      : "memory");
+}
+__device__ __forceinline__ double drain_ssq(uint32_t trow, int w) {  // Σ D^2 over TMEM columns [0, w)
+  double ssq = 0.0;
+  int c = 0;
+  for (; c + 64 <= w; c += 64) {
+    uint32_t rr[64];
+    tmem_ld16_nowait(trow + c, rr);
+    tmem_ld16_nowait(trow + c + 16, rr + 16);
+    tmem_ld16_nowait(trow + c + 32, rr + 32);
+    tmem_ld16_nowait(trow + c + 48, rr + 48);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    float pp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int i = 0; i < 64; ++i) pp[i & 7] = fmaf(__uint_as_float(rr[i]), __uint_as_float(rr[i]), pp[i & 7]);
+    ssq += (double)(((pp[0] + pp[1]) + (pp[2] + pp[3])) + ((pp[4] + pp[5]) + (pp[6] + pp[7])));
+  }
+  for (; c < w; c += 16) {
+    float v[16];
+    tmem_ld16(trow + c, v);
+    float part = 0.f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) part = fmaf(v[i], v[i], part);
+    ssq += (double)part;
+  }
+  return ssq;
+}
+}  // namespace tc
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::P2_THREADS, 1)
+    variance_f16x2_kernel(const VarianceArgs a, int S, int dbg) {
+  using namespace tc;
+  pdl_trigger();
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const GroupDev& G = a.g;
+  const int n = a.n, n_pad = G.tc_npad, n_pass = G.tc_npass2;
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char* stg = base;                                          // [S][A | B]
+  float* zs = reinterpret_cast<float*>(stg + (size_t)S * P2_STAGE);  // [5][n_pad]
+  uint64_t* full = reinterpret_cast<uint64_t*>(zs + 5 * n_pad);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  if (threadIdx.x == 0) trace_at(0, dbg);
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const long long n_super = (a.KT + 2 * M - 1) / (2 * M);
+  const int n_cl = gridDim.x >> 1, cl = blockIdx.x >> 1;
+  const long long sb = (long long)cl * n_super / n_cl, se = (long long)(cl + 1) * n_super / n_cl;
+  const float L2E = 1.4426950408889634f;
+  for (int i = threadIdx.x; i < n_pad; i += blockDim.x) {
+    float z[4], sq = 0.f;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      z[d] = i < n ? G.zs32[(size_t)d * n + i] : 0.f;
+      sq += z[d] * z[d];
+    }
+#pragma unroll
+    for (int d = 0; d < 4; ++d) zs[d * n_pad + i] = L2E * z[d];
+    zs[4 * n_pad + i] = i < n ? L2E * (-0.5f * sq) : -1e30f;  // k*/sf2: no ln sf2 term
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(smem_u32(&full[s]), P2_PRODUCER_WARPS + 1 + (leader ? 1 : 0));
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    mbar_init(smem_u32(tfull), 1);
+    mbar_init(smem_u32(tempty), 8);  // leader: four local + four peer epilogue warps
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_before();
+  cluster_sync_all();  // both CTAs' barriers initialised and TMEM allocated before any remote arrive
+  tc_after();
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  pdl_wait();  // prologue overlapped the producer kernel's tail; the queries are read below
+  const unsigned long long t_role = GPM_DIAG(dbg & 512) ? clock64() : 0ull;
+  if (threadIdx.x == 0) trace_at(1, dbg);
+  if (GPM_DIAG(dbg & 512) && threadIdx.x == 0) prof_add(11, 1, dbg);
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- B copy: this CTA's half of every chunk
+      Ring r(S);
+      for (long long st = sb; st < se; ++st) {
+        if (st - sb < 10) trace_at(48 + (int)(st - sb), dbg);
+        int m = 0;
+        for (int p = 0; p < n_pass; ++p) {
+          const int nk = min(n_pad, (p + 1) * 512) / KC;
+          for (int kb = 0; kb < nk; ++kb, ++m, r.next()) {
+            const int4 meta = G.tc_h2meta[m];
+            mbar_wait_xp(smem_u32(&empty[r.s]), r.ph ^ 1, 0, dbg);
+            const uint32_t bytes = (uint32_t)meta.w * 2;
+            const uint32_t fb = smem_u32(&full[r.s]);
+            if (GPM_DIAG(dbg & 1)) {  // diagnostics: no operand copy
+              mbar_arrive(fb);
+              continue;
+            }
+            mbar_arrive_tx(fb, bytes);
+            bulk_g2s(smem_u32(stg + (size_t)r.s * P2_STAGE + P2_A_BYTES), G.tc_h2 + meta.x + (size_t)rank * meta.w,
+                     bytes, fb);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {  // ---------------- MMA issuer for the pair
+      Ring r(S);
+      uint32_t uc = 0;
+      for (long long st = sb; st < se; ++st) {
+        for (int p = 0; p < n_pass; ++p, ++uc) {
+          mbar_wait_xp(smem_u32(tempty), (uc & 1) ^ 1, 1, dbg);
+          tc_after();
+          if (lane == 0 && uc < 10) trace_at(2 + 2 * (int)uc, dbg);
+          const int nk = min(n_pad, (p + 1) * 512) / KC;
+          for (int kb = 0; kb < nk; ++kb, r.next()) {
+            int c0[2], nc[2];
+            pair2_cols(p, GPM_DIAG(dbg & 16) ? 0 : kb, n_pad, c0, nc);  // dbg 16: full-width MMAs
+            mbar_wait_xp(smem_u32(&full[r.s]), r.ph, 2, dbg);
+            tc_after();
+            const uint32_t sa = smem_u32(stg + (size_t)r.s * P2_STAGE);
+            const uint64_t ah = smem_desc(sa, H_SBO), al = smem_desc(sa + H_TILE_BYTES, H_SBO);
+            uint32_t bo = sa + P2_A_BYTES;
+#ifdef GPM_MMA_INTERLEAVE
+            if (nc[0] && nc[1] && !GPM_DIAG(dbg & 4)) {
+              const uint32_t b1 = bo + (uint32_t)nc[0] * KC * 2;
+              mma2_f16_3x_pair(tmem_base + (uint32_t)c0[0], tmem_base + (uint32_t)(256 + c0[1]), ah, al,
+                               smem_desc(bo, H_SBO), smem_desc(bo + (uint32_t)nc[0] * KC, H_SBO), smem_desc(b1, H_SBO),
+                               smem_desc(b1 + (uint32_t)nc[1] * KC, H_SBO), instr_desc_f16_m256(nc[0]),
+                               instr_desc_f16_m256(nc[1]), kb > 0 ? 1u : 0u);
+            } else
+#endif
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              if (nc[h] == 0 || GPM_DIAG(dbg & 4)) continue;  // dbg 4: no MMA (commit only)
+              mma2_f16_3x(tmem_base + (uint32_t)(256 * h + c0[h]), ah, al, smem_desc(bo, H_SBO),
+                          smem_desc(bo + (uint32_t)nc[h] * KC, H_SBO), instr_desc_f16_m256(nc[h]), kb > 0 ? 1u : 0u);
+              bo += (uint32_t)nc[h] * KC * 2;
+            }
+            mma2_commit_both(smem_u32(&empty[r.s]));
+          }
+          mma2_commit_both(smem_u32(tfull));
+          if (lane == 0 && uc < 10) trace_at(3 + 2 * (int)uc, dbg);
+        }
+      }
+    } else if (lane == 0) {  // ---------------- peer: relay stage-full to the leader
+      Ring r(S);
+      const uint32_t lead_full = map_rank(smem_u32(full), 0);
+      for (long long st = sb; st < se; ++st)
+        for (int p = 0; p < n_pass; ++p) {
+          const int nk = min(n_pad, (p + 1) * 512) / KC;
+          for (int kb = 0; kb < nk; ++kb, r.next()) {
+            mbar_wait_xp(smem_u32(&full[r.s]), r.ph, 12, dbg);
+            mbar_arrive_remote(lead_full + 8u * (uint32_t)r.s);
+          }
+        }
+    }
+  } else if (warp >= 8) {
+    // ---------------- A producers: k*/sf2 for this CTA's 128 rows, FP16 hi + lo
+    const int pw = warp - 8;
+    const int qi = lane & 7, pg = lane >> 3;
+    Ring r(S);
+    for (long long st = sb; st < se; ++st) {
+      if (pw == 0 && lane == 0 && st - sb < 10) trace_at(36 + (int)(st - sb), dbg);
+      float qq[2][5];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const long long q = st * (2 * M) + (long long)rank * M + pw * 16 + 8 * j + qi;
+        const bool valid = q < a.KT;
+        const float4 qv = valid ? a.queries[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+        qq[j][0] = qv.x / (float)G.ls[0];
+        qq[j][1] = qv.y / (float)G.ls[1];
+        qq[j][2] = qv.z / (float)G.ls[2];
+        qq[j][3] = qv.w / (float)G.ls[3];
+        qq[j][4] = valid ? -0.5f * L2E * (qq[j][0] * qq[j][0] + qq[j][1] * qq[j][1] + qq[j][2] * qq[j][2] +
+                                          qq[j][3] * qq[j][3])
+                         : -1e30f;
+      }
+      unsigned long long qp[2][5];
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int c = 0; c < 5; ++c) qp[j][c] = f2_pack(qq[j][c], qq[j][c]);
+      for (int p = 0; p < n_pass; ++p) {
+        const int nk = min(n_pad, (p + 1) * 512) / KC;
+        for (int kb = 0; kb < nk; ++kb, r.next()) {
+          if (lane == 0) mbar_wait_xp(smem_u32(&empty[r.s]), r.ph ^ 1, 4, dbg);
+          __syncwarp();
+          if (GPM_DIAG(dbg & 256)) {  // diagnostics: no A production
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&full[r.s]));
+            continue;
+          }
+          unsigned char* ahi = stg + (size_t)r.s * P2_STAGE;
+          unsigned char* alo = ahi + H_TILE_BYTES;
+          const int i0 = kb * KC + pg * 4;
+          const float4 z0 = *reinterpret_cast<const float4*>(zs + i0);
+          const float4 z1 = *reinterpret_cast<const float4*>(zs + n_pad + i0);
+          const float4 z2 = *reinterpret_cast<const float4*>(zs + 2 * n_pad + i0);
+          const float4 z3 = *reinterpret_cast<const float4*>(zs + 3 * n_pad + i0);
+          const float4 zq = *reinterpret_cast<const float4*>(zs + 4 * n_pad + i0);
+          const unsigned long long zp[2][5] = {
+              {f2_pack(z0.x, z0.y), f2_pack(z1.x, z1.y), f2_pack(z2.x, z2.y), f2_pack(z3.x, z3.y), f2_pack(zq.x, zq.y)},
+              {f2_pack(z0.z, z0.w), f2_pack(z1.z, z1.w), f2_pack(z2.z, z2.w), f2_pack(z3.z, z3.w), f2_pack(zq.z, zq.w)}};
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            float kv[4];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              unsigned long long d = fadd2(qp[j][4], zp[h][4]);
+              d = ffma2(qp[j][3], zp[h][3], d);
+              d = ffma2(qp[j][2], zp[h][2], d);
+              d = ffma2(qp[j][1], zp[h][1], d);
+              d = ffma2(qp[j][0], zp[h][0], d);
+              kv[2 * h] = exp2f_approx(__uint_as_float((uint32_t)d));
+              kv[2 * h + 1] = exp2f_approx(__uint_as_float((uint32_t)(d >> 32)));
+            }
+            const __half2 h01 = __floats2half2_rn(kv[0], kv[1]), h23 = __floats2half2_rn(kv[2], kv[3]);
+            const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+            const __half2 l01 = __floats2half2_rn(kv[0] - f01.x, kv[1] - f01.y);
+            const __half2 l23 = __floats2half2_rn(kv[2] - f23.x, kv[3] - f23.y);
+            // row m = pw*16 + 8j + qi, points 4pg..4pg+3 (K-major canonical, as variance_f16_kernel)
+            const int off = (2 * pw + j) * H_SBO + (pg >> 1) * 128 + qi * 16 + (pg & 1) * 8;
+            *reinterpret_cast<uint2*>(ahi + off) = make_uint2(half2_bits(h01), half2_bits(h23));
+            *reinterpret_cast<uint2*>(alo + off) = make_uint2(half2_bits(l01), half2_bits(l23));
+          }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&full[r.s]));
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: this CTA's 128 rows, Σ D^2 over both halves of every pass
+    const int e = warp - 4;
+    const int m = e * 32 + lane;
+    const uint32_t lead_tempty = map_rank(smem_u32(tempty), 0);
+    uint32_t uc = 0;
+    for (long long st = sb; st < se; ++st) {
+      double ssq = 0.0;
+      for (int p = 0; p < n_pass; ++p, ++uc) {
+        const int npw = min(512, n_pad - p * 512);
+        const int w0 = (min(256, npw) + 31) & ~31, w1 = npw > 256 ? ((npw - 256 + 31) & ~31) : 0;
+        if (lane == 0) mbar_wait_xp(smem_u32(tfull), uc & 1, 5, dbg);
+        if (lane == 0 && e == 0 && uc < 10) trace_at(24 + (int)uc, dbg);
+        __syncwarp();
+        tc_after();
+        const uint32_t trow = tmem_base + ((uint32_t)(e * 32) << 16);
+        if (!GPM_DIAG(dbg & 8)) {  // dbg 8: no TMEM drain
+          ssq += drain_ssq(trow, w0);
+          if (w1) ssq += drain_ssq(trow + 256, w1);
+        }
+        tc_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader)
+            mbar_arrive(smem_u32(tempty));
+          else
+            mbar_arrive_remote(lead_tempty);
+        }
+      }
+      const long long q = st * (2 * M) + (long long)rank * M + m;
+      if (q < a.KT) {
+        double var = G.sv - G.tc_hfac * ssq;  // gp.cpp:187-191
+        var = var > 0.0 ? var : 0.0;
+        const double c = a.coef * var;
+        a.trace[q] = a.accumulate ? a.trace[q] + c : c;
+      }
+    }
+  }
+  if (GPM_DIAG(dbg & 512) && lane == 0) {
+    const unsigned long long dt = clock64() - t_role;
+    if (warp == 0) prof_add(6, dt, dbg);
+    else if (warp == 1) prof_add(leader ? 7 : 13, dt, dbg);
+    else if (warp >= 8) prof_add(8, dt, dbg);
+    else if (warp >= 4) prof_add(9, dt, dbg);
+  }
+  if (warp == 1 && lane == 0) trace_at(60, dbg);
+  tc_before();
+  cluster_sync_all();  // the pair's MMAs, copies and remote arrivals are complete
+  tc_after();
+  if (threadIdx.x == 0) trace_at(63, dbg);
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512) : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -1606,6 +2024,11 @@ size_t f16_smem_bytes(const GroupDev& g, int stages) {
          sizeof(float) * 5 * (size_t)g.tc_npad + sizeof(uint64_t) * (2 * stages + 2) + 16;
 }
 
+size_t f16x2_smem_bytes(const GroupDev& g, int stages) {
+  return 1024 + (size_t)stages * tc::P2_STAGE + sizeof(float) * 5 * (size_t)g.tc_npad +
+         sizeof(uint64_t) * (2 * stages + 2) + 16;
+}
+
 size_t tc2u_smem_bytes(const GroupDev& g, int stages) {
   return 1024 + sizeof(float) * ((size_t)stages * (2 * 2 * tc::A_STAGE_FLOATS + 2 * 2 * g.tc_np * tc::KB) + 5 * (size_t)g.tc_npad) +
          sizeof(uint64_t) * (2 * stages + 2) + 16;
@@ -1644,6 +2067,67 @@ cudaError_t launch_tc_variance(const VarianceArgs& a, int mode, cudaStream_t st)
     const char* e = getenv("GPMPPI_TC_DEBUG");
     dbg_h = e ? atoi(e) : 0;
   }
+  // The CTA-pair kernel: mode 3, or mode 2 when (measured) it is ahead:
+  //  - n_pad >= 1024: its 512-column passes regenerate k* 320 instead of 576 times per tile at
+  //    n = 2048 (config 3: 8.15 -> 7.87 ms);
+  //  - short launches (<= 16 super-tiles per CTA pair): one 128-row tile per SM per step
+  //    balances the tail better than the single-CTA kernel's two-tile units (config 2:
+  //    151 -> 146 us), while at long launches the single-CTA kernel's stages are cheaper
+  //    (config 5, 138 super-tiles per pair: 1.87 vs 1.97 ms).
+  // GPMPPI_VAR2CTA=0/1 forces the choice for mode 2 (A/B).
+  static int pair_env = -2;
+  if (pair_env == -2) {
+    const char* e = getenv("GPMPPI_VAR2CTA");
+    pair_env = e ? atoi(e) : -1;
+  }
+  int dev_sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const long long supers_all = (a.KT + 2 * tc::M - 1) / (2 * tc::M);
+  const bool pair_auto = a.g.tc_npad >= 1024 || (a.g.tc_npad > 256 && supers_all <= 16LL * (dev_sms / 2));
+  const bool pair = mode == 3 || (mode == 2 && (pair_env == 1 || (pair_env < 0 && pair_auto)));
+  if (pair && a.g.tc_h2 && a.g.tc_h2meta) {
+    int stages = 8;
+    while (stages > 3 && f16x2_smem_bytes(a.g, stages) > kSmemMax) --stages;
+    if (f16x2_smem_bytes(a.g, stages) <= kSmemMax) {
+      const size_t psm = f16x2_smem_bytes(a.g, stages);
+      cudaError_t ep = cudaFuncSetAttribute(variance_f16x2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
+      if (ep != cudaSuccess) return ep;
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const long long supers = (a.KT + 2 * tc::M - 1) / (2 * tc::M);
+      // co-resident CTA pairs: a TPC-paired cluster needs both SMs of a TPC, and the floor-swept
+      // GPCs of a B200 hold fewer than sms / 2 of them (a second wave would double the tail)
+      static int max_pairs = 0;
+      if (max_pairs == 0) {
+        cudaLaunchConfig_t qc = {};
+        qc.gridDim = dim3(sms);
+        qc.blockDim = dim3(tc::P2_THREADS);
+        qc.dynamicSmemBytes = psm;
+        int nc = 0;
+        max_pairs = cudaOccupancyMaxActiveClusters(&nc, variance_f16x2_kernel, &qc) == cudaSuccess && nc > 0
+                        ? nc
+                        : sms / 2;
+        if (getenv("GPMPPI_TC_PRINT")) printf("variance_f16x2_kernel: %d co-resident CTA pairs\n", max_pairs);
+      }
+      const int cap = max_pairs < sms / 2 ? max_pairs : sms / 2;
+      const int pairs = (int)(supers < cap ? supers : cap);
+      static int dbg_p = -1;
+      if (dbg_p < 0) {
+        const char* e = getenv("GPMPPI_TC_DEBUG");
+        dbg_p = e ? atoi(e) : 0;
+      }
+      cudaError_t el = launch_pdl(variance_f16x2_kernel, dim3(2 * pairs), dim3(tc::P2_THREADS), psm, st, a, stages, dbg_p);
+      if (el != cudaSuccess) return el;
+      count_launch();
+      return cudaGetLastError();
+    }
+  }
+  if (mode == 3) mode = 2;  // pair operand absent or shared memory short: the single-CTA kernel
   if (mode == 2 && a.g.tc_h && a.g.tc_hmeta && a.g.tc_np <= 256) {
     int stages = 8;
     while (stages > 3 && f16_smem_bytes(a.g, stages) > kSmemMax) --stages;
@@ -1656,7 +2140,7 @@ cudaError_t launch_tc_variance(const VarianceArgs& a, int mode, cudaStream_t st)
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       const long long units = ((a.KT + tc::M - 1) / tc::M + 1) / 2;
       const int grid = (int)(units < sms ? units : sms);
-      cudaError_t el = launch_pdl(variance_f16_kernel, dim3(grid), dim3(tc::THREADS), hsm, st, a, dbg_h, stages);
+      cudaError_t el = launch_pdl(variance_f16_kernel, dim3(grid), dim3(tc::F16_THREADS), hsm, st, a, dbg_h, stages);
       if (el != cudaSuccess) return el;
       count_launch();
       return cudaGetLastError();
@@ -1784,6 +2268,61 @@ void build_tc_operand(const double* ilt, int n, std::vector<float>& data, std::v
 // per (pass, 16-point chunk) a hi block then a lo block of ncols x 16 FP16 in the
 // K-major canonical layout (8-row groups of two 128-byte core matrices: SBO 256 B,
 // LBO 128 B). hfac = (sf2 / 2^-e)^2 undoes both scales on Σ D^2 in the epilogue.
+// Host: the CTA-pair operand (variance_f16x2_kernel). Same power-of-two scale and FP16
+// hi/lo split as build_tc_operand_f16; per (512-column pass p, 16-point chunk kb) one
+// record [CTA0 part | CTA1 part], each part = for each active half h (pair2_cols): hi then
+// lo block of nc[h]/2 rows x 16 FP16 (K-major canonical, SBO 256 B), CTA r holding columns
+// 512p + 256h + c0[h] + r·nc[h]/2 + [0, nc[h]/2). meta = {offset, 0, 0, part size} (FP16 units).
+void build_tc_operand_f16x2(const double* ilt, int n, double sv, int n_pad, std::vector<uint16_t>& data,
+                            std::vector<int4>& meta, int& n_pass2) {
+  (void)sv;
+  const int KC = tc::KC;
+  double mx = 0.0;
+  for (size_t i = 0; i < (size_t)n * n; ++i) mx = std::max(mx, std::fabs(ilt[i]));
+  const double scale = mx > 0.0 ? std::ldexp(1.0, -(int)std::ceil(std::log2(mx))) : 1.0;
+  auto bits = [](__half h) {
+    uint16_t u;
+    std::memcpy(&u, &h, 2);
+    return u;
+  };
+  n_pass2 = (n_pad + 511) / 512;
+  data.clear();
+  meta.clear();
+  for (int p = 0; p < n_pass2; ++p) {
+    const int nk = std::min(n_pad, (p + 1) * 512) / KC;
+    for (int kb = 0; kb < nk; ++kb) {
+      int c0[2], nc[2];
+      pair2_cols(p, kb, n_pad, c0, nc);
+      const int part = (nc[0] + nc[1]) * KC;
+      const size_t off = data.size();
+      data.resize(off + (size_t)2 * part, 0);
+      for (int r = 0; r < 2; ++r) {
+        size_t o0 = off + (size_t)r * part;
+        for (int h = 0; h < 2; ++h) {
+          if (nc[h] == 0) continue;
+          const int rows = nc[h] / 2;
+          uint16_t* hi = data.data() + o0;
+          uint16_t* lo = hi + (size_t)rows * KC;
+          for (int rr = 0; rr < rows; ++rr) {
+            const int j = 512 * p + 256 * h + c0[h] + r * rows + rr;
+            for (int k = 0; k < KC; ++k) {
+              const int i = kb * KC + k;
+              const double v = (i < n && j < n) ? ilt[(size_t)i * n + j] * scale : 0.0;
+              const __half hv = __float2half_rn((float)v);
+              const __half lv = __float2half_rn((float)(v - (double)__half2float(hv)));
+              const size_t o = (size_t)(rr >> 3) * 128 + (size_t)(k >> 3) * 64 + (rr & 7) * 8 + (k & 7);
+              hi[o] = bits(hv);
+              lo[o] = bits(lv);
+            }
+          }
+          o0 += (size_t)2 * rows * KC;
+        }
+      }
+      meta.push_back(make_int4((int)off, 0, 0, part));
+    }
+  }
+}
+
 void build_tc_operand_f16(const double* ilt, int n, double sv, int n_pad, int np, int n_pass,
                           std::vector<uint16_t>& data, std::vector<int4>& meta, double& hfac) {
   const int KC = tc::KC;

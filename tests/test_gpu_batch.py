@@ -61,7 +61,7 @@ def _setup(K=512, T=20, n=256, var_path=None):
     return G, gp, (X, Y, Kp), bp, singles, tasks, x0, weights, obs
 
 
-@pytest.mark.parametrize("var_path", [0, 1, 3])
+@pytest.mark.parametrize("var_path", [0, 1, 3, 4])
 def test_batch_matches_independent_planners(var_path):
     G, gp, _, bp, singles, tasks, x0, weights, _ = _setup(var_path=var_path)
     B = bp.B

@@ -69,7 +69,7 @@ CASES = {
 
 
 @pytest.mark.parametrize("case", sorted(CASES))
-@pytest.mark.parametrize("var_path", [0, 1, 3])
+@pytest.mark.parametrize("var_path", [0, 1, 3, 4])
 def test_edge_case_parity(case, var_path):
     import paper_2411_03289_b200 as G
     K, T, n, R, kind, track, n_obs, split, x0 = CASES[case]

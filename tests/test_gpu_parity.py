@@ -116,13 +116,13 @@ def test_config2_shape_reduced_K_injected_reference_noise(task):
     _run_ticks(w, ticks=3, samples=512)
 
 
-@pytest.mark.parametrize("var_path", [0, 1, 3])
+@pytest.mark.parametrize("var_path", [0, 1, 3, 4])
 def test_config2_variance_paths_parity(var_path):
     """FFMA and tcgen05 3xTF32 variance paths both meet the stated cost tolerance."""
     _run_ticks(W.CONFIGS["config2"], ticks=2, samples=2048, var_path=var_path)
 
 
-@pytest.mark.parametrize("var_path", [1, 3])
+@pytest.mark.parametrize("var_path", [1, 3, 4])
 def test_config3_shape_parity_tc(var_path):
     """n=2048, T=60 multi-terrain (BASELINE config 3 shape) at reduced K: 3xTF32 and the
     default 3xFP16 variance through plan_step."""

@@ -5,6 +5,9 @@ import sys
 import numpy as np
 
 sys.path.insert(0, os.getcwd())
+# the GPMPPI_TC_DEBUG switches exist only in the diagnostics build:
+#   python -m paper_2411_03289_b200.build --variant=diag -DGPM_TC_DIAG
+os.environ.setdefault("GPMPPI_LIB", os.path.join(os.getcwd(), "paper_2411_03289_b200", "lib", "libgpmppi_b200_diag.so"))
 os.environ["GPMPPI_TC_DEBUG"] = str(4096 | int(os.environ.get("TC_EXTRA", "0")))
 import paper_2411_03289_b200 as G  # noqa: E402
 from paper_2411_03289_b200 import _capi as A  # noqa: E402
