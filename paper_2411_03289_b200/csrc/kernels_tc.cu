@@ -70,9 +70,25 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+__device__ __forceinline__ bool mbar_test_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+#ifdef GPM_SPIN_WAIT  // A/B: non-suspending polls
+  while (!mbar_test_wait(bar, parity)) {
+  }
+#else
   while (!mbar_try_wait(bar, parity)) {
   }
+#endif
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
@@ -998,23 +1014,42 @@ __device__ __forceinline__ void mma_f16_pair_3x(uint32_t d, uint32_t dt, uint64_
       "add.u32 d1, %0, %1;\n\t"
       "setp.ne.b32 p, %9, 0;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
-#ifdef GPM_MMA_INTERLEAVE  // alternate the two tiles' accumulators between dependent MMAs
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %6, %8, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [d1], %4, %6, %8, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %7, %8, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [d1], %4, %7, %8, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %3, %6, %8, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [d1], %5, %6, %8, 1;\n\t"
-#else
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %6, %8, p;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %7, %8, 1;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %3, %6, %8, 1;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [d1], %4, %6, %8, p;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [d1], %4, %7, %8, 1;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [d1], %5, %6, %8, 1;\n\t"
-#endif
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%10];\n\t}" ::"r"(d),
       "r"(dt), "l"(a0h), "l"(a0l), "l"(a1h), "l"(a1l), "l"(bh), "l"(bl), "r"(idesc), "r"(acc), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mma_f16_pair_3x_nc(uint32_t d, uint32_t dt, uint64_t a0h, uint64_t a0l, uint64_t a1h,
+                                                   uint64_t a1l, uint64_t bh, uint64_t bl, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 d1;\n\t"
+      "add.u32 d1, %0, %1;\n\t"
+      "setp.ne.b32 p, %9, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %6, %8, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %7, %8, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %3, %6, %8, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [d1], %4, %6, %8, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [d1], %4, %7, %8, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [d1], %5, %6, %8, 1;\n\t}" ::"r"(d),
+      "r"(dt), "l"(a0h), "l"(a0l), "l"(a1h), "l"(a1l), "l"(bh), "l"(bl), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_f16_single_3x_nc(uint32_t d, uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl,
+                                                     uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %3, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %4, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %3, %5, 1;\n\t}" ::"r"(d),
+      "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(acc)
       : "memory");
 }
 __device__ __forceinline__ void mma_f16_single_3x(uint32_t d, uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl,
@@ -1051,6 +1086,7 @@ __device__ __forceinline__ uint32_t half2_bits(__half2 h) {
 }
 }  // namespace tc
 
+template <int CPS>  // 16-point chunks per ring stage (one barrier round trip, one commit per stage)
 __global__ void __launch_bounds__(tc::F16_THREADS, 1) variance_f16_kernel(const VarianceArgs a, int dbg, int S) {
   using namespace tc;
   pdl_trigger();
@@ -1058,7 +1094,8 @@ __global__ void __launch_bounds__(tc::F16_THREADS, 1) variance_f16_kernel(const 
   const GroupDev& G = a.g;
   const int n = a.n, n_pad = G.tc_npad, NP = G.tc_np, n_pass = G.tc_npass;
   constexpr int A_BYTES = 2 * 2 * H_TILE_BYTES;  // two tiles x (hi, lo)
-  const int stage_bytes = A_BYTES + 2 * NP * KC * 2;
+  const int b_bytes = 2 * NP * KC * 2;               // one chunk's L^{-T} hi + lo, at most
+  const int stage_bytes = CPS * (A_BYTES + b_bytes);  // [CPS x A][CPS x B]
   unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   unsigned char* stg = base;                                            // [S][A | B]
   float* zs = reinterpret_cast<float*>(stg + (size_t)S * stage_bytes);  // [5][n_pad]
@@ -1115,16 +1152,28 @@ __global__ void __launch_bounds__(tc::F16_THREADS, 1) variance_f16_kernel(const 
       int m = 0;
       for (int p = 0; p < n_pass; ++p) {
         const int nk = pass_chunks(p, NP, n_pad);
-        for (int kb = 0; kb < nk; ++kb, ++m, r.next()) {
-          const int4 meta = G.tc_hmeta[m];
+        for (int kb0 = 0; kb0 < nk; kb0 += CPS, r.next()) {
+          const int nc = min(CPS, nk - kb0);
+          int4 meta[CPS];
+          uint32_t total = 0;
+#pragma unroll
+          for (int c = 0; c < CPS; ++c)
+            if (c < nc) {
+              meta[c] = G.tc_hmeta[m + c];
+              total += (uint32_t)meta[c].y * KC * 2 * 2;
+            }
+          m += nc;
           mbar_wait(smem_u32(&empty[r.s]), r.ph ^ 1);
-          const uint32_t bytes = (uint32_t)meta.y * KC * 2 * 2;
           const uint32_t fb = smem_u32(&full[r.s]);
           if (GPM_DIAG(dbg & 1)) {  // diagnostics: no operand copy
             mbar_arrive(fb);
           } else {
-            mbar_arrive_tx(fb, bytes);
-            bulk_g2s(smem_u32(stg + (size_t)r.s * stage_bytes + A_BYTES), G.tc_h + meta.x, bytes, fb);
+            mbar_arrive_tx(fb, total);
+#pragma unroll
+            for (int c = 0; c < CPS; ++c)
+              if (c < nc)
+                bulk_g2s(smem_u32(stg + (size_t)r.s * stage_bytes + CPS * A_BYTES + c * b_bytes), G.tc_h + meta[c].x,
+                         (uint32_t)meta[c].y * KC * 2 * 2, fb);
           }
         }
       }
@@ -1141,27 +1190,46 @@ __global__ void __launch_bounds__(tc::F16_THREADS, 1) variance_f16_kernel(const 
         if (lane == 0 && uc < 10) trace_at(2 + 2 * (int)uc, dbg);
         const int nk = pass_chunks(p, NP, n_pad);
         const int npw = min(NP, n_pad - p * NP);
-        for (int kb = 0; kb < nk; ++kb, r.next()) {
+        for (int kb0 = 0; kb0 < nk; kb0 += CPS, r.next()) {
           mbar_wait(smem_u32(&full[r.s]), r.ph);
-          const int col0 = GPM_DIAG(dbg & 16) ? 0 : max(0, kb * KC - p * NP);  // dbg 16: full-width MMAs
-          const int ncols = npw - col0;
-          const uint32_t st = smem_u32(stg + (size_t)r.s * stage_bytes);
-          const uint32_t bh = st + A_BYTES;
-          const uint32_t bl = bh + (uint32_t)ncols * KC * 2;
+          const uint32_t st0 = smem_u32(stg + (size_t)r.s * stage_bytes);
           const uint32_t bar = smem_u32(&empty[r.s]);
           if (GPM_DIAG(dbg & 4)) {
             mma_commit(bar);
             continue;
           }
-          if (two)
-            mma_f16_pair_3x(tmem_base + (uint32_t)col0, (uint32_t)NP, smem_desc(st, H_SBO),
-                            smem_desc(st + H_TILE_BYTES, H_SBO), smem_desc(st + 2 * H_TILE_BYTES, H_SBO),
-                            smem_desc(st + 3 * H_TILE_BYTES, H_SBO), smem_desc(bh, H_SBO), smem_desc(bl, H_SBO),
-                            instr_desc_f16(ncols), kb > 0 ? 1u : 0u, bar);
-          else
-            mma_f16_single_3x(tmem_base + (uint32_t)col0, smem_desc(st, H_SBO), smem_desc(st + H_TILE_BYTES, H_SBO),
-                              smem_desc(bh, H_SBO), smem_desc(bl, H_SBO), instr_desc_f16(ncols), kb > 0 ? 1u : 0u,
-                              bar);
+#pragma unroll
+          for (int c = 0; c < CPS; ++c) {
+            const int kb = kb0 + c;
+            if (kb >= nk) break;
+            const int col0 = GPM_DIAG(dbg & 16) ? 0 : max(0, kb * KC - p * NP);  // dbg 16: full-width MMAs
+            const int ncols = npw - col0;
+            const uint32_t st = st0 + (uint32_t)(c * A_BYTES);
+            const uint32_t bh = st0 + (uint32_t)(CPS * A_BYTES + c * b_bytes);
+            const uint32_t bl = bh + (uint32_t)ncols * KC * 2;
+            if (CPS == 1) {
+              if (two)
+                mma_f16_pair_3x(tmem_base + (uint32_t)col0, (uint32_t)NP, smem_desc(st, H_SBO),
+                                smem_desc(st + H_TILE_BYTES, H_SBO), smem_desc(st + 2 * H_TILE_BYTES, H_SBO),
+                                smem_desc(st + 3 * H_TILE_BYTES, H_SBO), smem_desc(bh, H_SBO), smem_desc(bl, H_SBO),
+                                instr_desc_f16(ncols), kb > 0 ? 1u : 0u, bar);
+              else
+                mma_f16_single_3x(tmem_base + (uint32_t)col0, smem_desc(st, H_SBO),
+                                  smem_desc(st + H_TILE_BYTES, H_SBO), smem_desc(bh, H_SBO), smem_desc(bl, H_SBO),
+                                  instr_desc_f16(ncols), kb > 0 ? 1u : 0u, bar);
+            } else {
+              if (two)
+                mma_f16_pair_3x_nc(tmem_base + (uint32_t)col0, (uint32_t)NP, smem_desc(st, H_SBO),
+                                   smem_desc(st + H_TILE_BYTES, H_SBO), smem_desc(st + 2 * H_TILE_BYTES, H_SBO),
+                                   smem_desc(st + 3 * H_TILE_BYTES, H_SBO), smem_desc(bh, H_SBO), smem_desc(bl, H_SBO),
+                                   instr_desc_f16(ncols), kb > 0 ? 1u : 0u);
+              else
+                mma_f16_single_3x_nc(tmem_base + (uint32_t)col0, smem_desc(st, H_SBO),
+                                     smem_desc(st + H_TILE_BYTES, H_SBO), smem_desc(bh, H_SBO), smem_desc(bl, H_SBO),
+                                     instr_desc_f16(ncols), kb > 0 ? 1u : 0u);
+            }
+          }
+          if (CPS > 1) mma_commit(bar);
         }
         mma_commit(smem_u32(tfull));
         if (lane == 0 && uc < 10) trace_at(3 + 2 * (int)uc, dbg);
@@ -1203,11 +1271,15 @@ __global__ void __launch_bounds__(tc::F16_THREADS, 1) variance_f16_kernel(const 
         for (int c = 0; c < 5; ++c) qp[j][c] = f2_pack(qq[j][c], qq[j][c]);
       for (int p = 0; p < n_pass; ++p) {
         const int nk = pass_chunks(p, NP, n_pad);
-        for (int kb = 0; kb < nk; ++kb, r.next()) {
+        for (int kb0 = 0; kb0 < nk; kb0 += CPS, r.next()) {
           if (lane == 0) mbar_wait(smem_u32(&empty[r.s]), r.ph ^ 1);
           __syncwarp();
           if (present && !GPM_DIAG(dbg & 256)) {
-            unsigned char* ahi = stg + (size_t)r.s * stage_bytes + (size_t)t * 2 * H_TILE_BYTES;
+#pragma unroll
+           for (int c = 0; c < CPS; ++c) {
+            const int kb = kb0 + c;
+            if (kb >= nk) break;
+            unsigned char* ahi = stg + (size_t)r.s * stage_bytes + (size_t)c * A_BYTES + (size_t)t * 2 * H_TILE_BYTES;
             unsigned char* alo = ahi + H_TILE_BYTES;
             const int i0 = kb * KC + pg * 4;
             const float4 z0 = *reinterpret_cast<const float4*>(zs + i0);
@@ -1241,6 +1313,7 @@ __global__ void __launch_bounds__(tc::F16_THREADS, 1) variance_f16_kernel(const 
               *reinterpret_cast<uint2*>(ahi + off) = make_uint2(half2_bits(h01), half2_bits(h23));
               *reinterpret_cast<uint2*>(alo + off) = make_uint2(half2_bits(l01), half2_bits(l23));
             }
+           }
             fence_proxy_async();
           }
           __syncwarp();
@@ -1358,7 +1431,11 @@ __device__ __forceinline__ void mbar_wait_x(uint32_t bar, uint32_t parity) {
   for (uint32_t spins = 0;; ++spins) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
+#ifdef GPM_SPIN_WAIT
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+#else
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+#endif
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
         : "r"(bar), "r"(parity)
@@ -1389,22 +1466,6 @@ __device__ __forceinline__ void mma2_f16_3x(uint32_t d, uint64_t ah, uint64_t al
       "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %4, %5, 1;\n\t"
       "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %2, %3, %5, 1;\n\t}" ::"r"(d),
       "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(acc)
-      : "memory");
-}
-__device__ __forceinline__ void mma2_f16_3x_pair(uint32_t d0, uint32_t d1, uint64_t ah, uint64_t al, uint64_t bh0,
-                                                 uint64_t bl0, uint64_t bh1, uint64_t bl1, uint32_t id0, uint32_t id1,
-                                                 uint32_t acc) {  // both halves, accumulators alternating
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
-      "setp.ne.b32 p, %10, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %2, %4, %8, p;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%1], %2, %6, %9, p;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %2, %5, %8, 1;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%1], %2, %7, %9, 1;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %3, %4, %8, 1;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%1], %3, %6, %9, 1;\n\t}" ::"r"(d0),
-      "r"(d1), "l"(ah), "l"(al), "l"(bh0), "l"(bl0), "l"(bh1), "l"(bl1), "r"(id0), "r"(id1), "r"(acc)
       : "memory");
 }
 __device__ __forceinline__ void mma2_commit_both(uint32_t bar) {  // arrive on `bar` in both CTAs
@@ -1443,6 +1504,7 @@ __device__ __forceinline__ double drain_ssq(uint32_t trow, int w) {  // Σ D^2 o
 }
 }  // namespace tc
 
+template <int CPS>  // 16-point chunks per ring stage
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::P2_THREADS, 1)
     variance_f16x2_kernel(const VarianceArgs a, int S, int dbg) {
   using namespace tc;
@@ -1451,8 +1513,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::P2_THREADS, 1)
   const GroupDev& G = a.g;
   const int n = a.n, n_pad = G.tc_npad, n_pass = G.tc_npass2;
   unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  unsigned char* stg = base;                                          // [S][A | B]
-  float* zs = reinterpret_cast<float*>(stg + (size_t)S * P2_STAGE);  // [5][n_pad]
+  constexpr int STAGE = CPS * P2_STAGE;                             // [CPS x A][CPS x B]
+  unsigned char* stg = base;
+  float* zs = reinterpret_cast<float*>(stg + (size_t)S * STAGE);  // [5][n_pad]
   uint64_t* full = reinterpret_cast<uint64_t*>(zs + 5 * n_pad);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
@@ -1508,18 +1571,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::P2_THREADS, 1)
         int m = 0;
         for (int p = 0; p < n_pass; ++p) {
           const int nk = min(n_pad, (p + 1) * 512) / KC;
-          for (int kb = 0; kb < nk; ++kb, ++m, r.next()) {
-            const int4 meta = G.tc_h2meta[m];
+          for (int kb0 = 0; kb0 < nk; kb0 += CPS, r.next()) {
+            const int ncs = min(CPS, nk - kb0);
+            int4 meta[CPS];
+            uint32_t total = 0;
+#pragma unroll
+            for (int c = 0; c < CPS; ++c)
+              if (c < ncs) {
+                meta[c] = G.tc_h2meta[m + c];
+                total += (uint32_t)meta[c].w * 2;
+              }
+            m += ncs;
             mbar_wait_xp(smem_u32(&empty[r.s]), r.ph ^ 1, 0, dbg);
-            const uint32_t bytes = (uint32_t)meta.w * 2;
             const uint32_t fb = smem_u32(&full[r.s]);
             if (GPM_DIAG(dbg & 1)) {  // diagnostics: no operand copy
               mbar_arrive(fb);
               continue;
             }
-            mbar_arrive_tx(fb, bytes);
-            bulk_g2s(smem_u32(stg + (size_t)r.s * P2_STAGE + P2_A_BYTES), G.tc_h2 + meta.x + (size_t)rank * meta.w,
-                     bytes, fb);
+            mbar_arrive_tx(fb, total);
+#pragma unroll
+            for (int c = 0; c < CPS; ++c)
+              if (c < ncs)
+                bulk_g2s(smem_u32(stg + (size_t)r.s * STAGE + CPS * P2_A_BYTES + c * P2_B_BYTES),
+                         G.tc_h2 + meta[c].x + (size_t)rank * meta[c].w, (uint32_t)meta[c].w * 2, fb);
           }
         }
       }
@@ -1534,29 +1608,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::P2_THREADS, 1)
           tc_after();
           if (lane == 0 && uc < 10) trace_at(2 + 2 * (int)uc, dbg);
           const int nk = min(n_pad, (p + 1) * 512) / KC;
-          for (int kb = 0; kb < nk; ++kb, r.next()) {
-            int c0[2], nc[2];
-            pair2_cols(p, GPM_DIAG(dbg & 16) ? 0 : kb, n_pad, c0, nc);  // dbg 16: full-width MMAs
+          for (int kb0 = 0; kb0 < nk; kb0 += CPS, r.next()) {
             mbar_wait_xp(smem_u32(&full[r.s]), r.ph, 2, dbg);
             tc_after();
-            const uint32_t sa = smem_u32(stg + (size_t)r.s * P2_STAGE);
-            const uint64_t ah = smem_desc(sa, H_SBO), al = smem_desc(sa + H_TILE_BYTES, H_SBO);
-            uint32_t bo = sa + P2_A_BYTES;
-#ifdef GPM_MMA_INTERLEAVE
-            if (nc[0] && nc[1] && !GPM_DIAG(dbg & 4)) {
-              const uint32_t b1 = bo + (uint32_t)nc[0] * KC * 2;
-              mma2_f16_3x_pair(tmem_base + (uint32_t)c0[0], tmem_base + (uint32_t)(256 + c0[1]), ah, al,
-                               smem_desc(bo, H_SBO), smem_desc(bo + (uint32_t)nc[0] * KC, H_SBO), smem_desc(b1, H_SBO),
-                               smem_desc(b1 + (uint32_t)nc[1] * KC, H_SBO), instr_desc_f16_m256(nc[0]),
-                               instr_desc_f16_m256(nc[1]), kb > 0 ? 1u : 0u);
-            } else
-#endif
+            const uint32_t s0 = smem_u32(stg + (size_t)r.s * STAGE);
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              if (nc[h] == 0 || GPM_DIAG(dbg & 4)) continue;  // dbg 4: no MMA (commit only)
-              mma2_f16_3x(tmem_base + (uint32_t)(256 * h + c0[h]), ah, al, smem_desc(bo, H_SBO),
-                          smem_desc(bo + (uint32_t)nc[h] * KC, H_SBO), instr_desc_f16_m256(nc[h]), kb > 0 ? 1u : 0u);
-              bo += (uint32_t)nc[h] * KC * 2;
+            for (int c = 0; c < CPS; ++c) {
+              const int kb = kb0 + c;
+              if (kb >= nk) break;
+              int c0[2], nc[2];
+              pair2_cols(p, GPM_DIAG(dbg & 16) ? 0 : kb, n_pad, c0, nc);  // dbg 16: full-width MMAs
+              const uint32_t sa = s0 + (uint32_t)(c * P2_A_BYTES);
+              const uint64_t ah = smem_desc(sa, H_SBO), al = smem_desc(sa + H_TILE_BYTES, H_SBO);
+              uint32_t bo = s0 + (uint32_t)(CPS * P2_A_BYTES + c * P2_B_BYTES);
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                if (nc[h] == 0 || GPM_DIAG(dbg & 4)) continue;  // dbg 4: no MMA (commit only)
+                mma2_f16_3x(tmem_base + (uint32_t)(256 * h + c0[h]), ah, al, smem_desc(bo, H_SBO),
+                            smem_desc(bo + (uint32_t)nc[h] * KC, H_SBO), instr_desc_f16_m256(nc[h]), kb > 0 ? 1u : 0u);
+                bo += (uint32_t)nc[h] * KC * 2;
+              }
             }
             mma2_commit_both(smem_u32(&empty[r.s]));
           }
@@ -1570,7 +1641,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::P2_THREADS, 1)
       for (long long st = sb; st < se; ++st)
         for (int p = 0; p < n_pass; ++p) {
           const int nk = min(n_pad, (p + 1) * 512) / KC;
-          for (int kb = 0; kb < nk; ++kb, r.next()) {
+          for (int kb0 = 0; kb0 < nk; kb0 += CPS, r.next()) {
             mbar_wait_xp(smem_u32(&full[r.s]), r.ph, 12, dbg);
             mbar_arrive_remote(lead_full + 8u * (uint32_t)r.s);
           }
@@ -1604,7 +1675,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::P2_THREADS, 1)
         for (int c = 0; c < 5; ++c) qp[j][c] = f2_pack(qq[j][c], qq[j][c]);
       for (int p = 0; p < n_pass; ++p) {
         const int nk = min(n_pad, (p + 1) * 512) / KC;
-        for (int kb = 0; kb < nk; ++kb, r.next()) {
+        for (int kb0 = 0; kb0 < nk; kb0 += CPS, r.next()) {
           if (lane == 0) mbar_wait_xp(smem_u32(&empty[r.s]), r.ph ^ 1, 4, dbg);
           __syncwarp();
           if (GPM_DIAG(dbg & 256)) {  // diagnostics: no A production
@@ -1612,7 +1683,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::P2_THREADS, 1)
             if (lane == 0) mbar_arrive(smem_u32(&full[r.s]));
             continue;
           }
-          unsigned char* ahi = stg + (size_t)r.s * P2_STAGE;
+#pragma unroll
+          for (int c = 0; c < CPS; ++c) {
+          const int kb = kb0 + c;
+          if (kb >= nk) break;
+          unsigned char* ahi = stg + (size_t)r.s * STAGE + (size_t)c * P2_A_BYTES;
           unsigned char* alo = ahi + H_TILE_BYTES;
           const int i0 = kb * KC + pg * 4;
           const float4 z0 = *reinterpret_cast<const float4*>(zs + i0);
@@ -1644,6 +1719,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::P2_THREADS, 1)
             const int off = (2 * pw + j) * H_SBO + (pg >> 1) * 128 + qi * 16 + (pg & 1) * 8;
             *reinterpret_cast<uint2*>(ahi + off) = make_uint2(half2_bits(h01), half2_bits(h23));
             *reinterpret_cast<uint2*>(alo + off) = make_uint2(half2_bits(l01), half2_bits(l23));
+          }
           }
           fence_proxy_async();
           __syncwarp();
@@ -2019,13 +2095,13 @@ cudaError_t launch_variance_coop(const VarianceArgs& v, const unsigned long long
   return cudaGetLastError();
 }
 
-size_t f16_smem_bytes(const GroupDev& g, int stages) {
-  return 1024 + (size_t)stages * (2 * 2 * tc::H_TILE_BYTES + 2 * (size_t)g.tc_np * tc::KC * 2) +
+size_t f16_smem_bytes(const GroupDev& g, int stages, int cps = 1) {
+  return 1024 + (size_t)stages * cps * (2 * 2 * tc::H_TILE_BYTES + 2 * (size_t)g.tc_np * tc::KC * 2) +
          sizeof(float) * 5 * (size_t)g.tc_npad + sizeof(uint64_t) * (2 * stages + 2) + 16;
 }
 
-size_t f16x2_smem_bytes(const GroupDev& g, int stages) {
-  return 1024 + (size_t)stages * tc::P2_STAGE + sizeof(float) * 5 * (size_t)g.tc_npad +
+size_t f16x2_smem_bytes(const GroupDev& g, int stages, int cps = 1) {
+  return 1024 + (size_t)stages * cps * tc::P2_STAGE + sizeof(float) * 5 * (size_t)g.tc_npad +
          sizeof(uint64_t) * (2 * stages + 2) + 16;
 }
 
@@ -2067,13 +2143,14 @@ cudaError_t launch_tc_variance(const VarianceArgs& a, int mode, cudaStream_t st)
     const char* e = getenv("GPMPPI_TC_DEBUG");
     dbg_h = e ? atoi(e) : 0;
   }
-  // The CTA-pair kernel: mode 3, or mode 2 when (measured) it is ahead:
+  // The CTA-pair kernel: mode 3, or mode 2 when (measured; both kernels with
+  // two chunks per ring stage) it is ahead:
   //  - n_pad >= 1024: its 512-column passes regenerate k* 320 instead of 576 times per tile at
-  //    n = 2048 (config 3: 8.15 -> 7.87 ms);
+  //    n = 2048, and its stages still fit twice-deep (config 3: 8.40 -> 7.85 ms);
   //  - short launches (<= 16 super-tiles per CTA pair): one 128-row tile per SM per step
   //    balances the tail better than the single-CTA kernel's two-tile units (config 2:
-  //    151 -> 146 us), while at long launches the single-CTA kernel's stages are cheaper
-  //    (config 5, 138 super-tiles per pair: 1.87 vs 1.97 ms).
+  //    139 -> 129 us); at long launches the two are level (config 5, 138 super-tiles per
+  //    pair: 1.74 single vs 1.76 ms pair).
   // GPMPPI_VAR2CTA=0/1 forces the choice for mode 2 (A/B).
   static int pair_env = -2;
   if (pair_env == -2) {
@@ -2089,39 +2166,39 @@ cudaError_t launch_tc_variance(const VarianceArgs& a, int mode, cudaStream_t st)
   const long long supers_all = (a.KT + 2 * tc::M - 1) / (2 * tc::M);
   const bool pair_auto = a.g.tc_npad >= 1024 || (a.g.tc_npad > 256 && supers_all <= 16LL * (dev_sms / 2));
   const bool pair = mode == 3 || (mode == 2 && (pair_env == 1 || (pair_env < 0 && pair_auto)));
+  static int cps_env = -1;  // GPMPPI_F16_CPS=1/2 forces the chunks per ring stage (A/B)
+  if (cps_env < 0) {
+    const char* e = getenv("GPMPPI_F16_CPS");
+    cps_env = e ? atoi(e) : 0;
+  }
   if (pair && a.g.tc_h2 && a.g.tc_h2meta) {
+    // two chunks per ring stage when three such stages fit
+    int cps = cps_env >= 1 && cps_env <= 3 ? cps_env : 2;
+    while (cps > 1 && f16x2_smem_bytes(a.g, 3, cps) > kSmemMax) --cps;
     int stages = 8;
-    while (stages > 3 && f16x2_smem_bytes(a.g, stages) > kSmemMax) --stages;
-    if (f16x2_smem_bytes(a.g, stages) <= kSmemMax) {
-      const size_t psm = f16x2_smem_bytes(a.g, stages);
-      cudaError_t ep = cudaFuncSetAttribute(variance_f16x2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
+    while (stages > 3 && f16x2_smem_bytes(a.g, stages, cps) > kSmemMax) --stages;
+    if (f16x2_smem_bytes(a.g, stages, cps) <= kSmemMax) {
+      const size_t psm = f16x2_smem_bytes(a.g, stages, cps);
+      void (*kern)(const VarianceArgs, int, int) =
+          cps == 3 ? variance_f16x2_kernel<3> : cps == 2 ? variance_f16x2_kernel<2> : variance_f16x2_kernel<1>;
+      cudaError_t ep = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
       if (ep != cudaSuccess) return ep;
-      int dev = 0, sms = 148;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       const long long supers = (a.KT + 2 * tc::M - 1) / (2 * tc::M);
-      // co-resident CTA pairs: a TPC-paired cluster needs both SMs of a TPC, and the floor-swept
-      // GPCs of a B200 hold fewer than sms / 2 of them (a second wave would double the tail)
-      static int max_pairs = 0;
-      if (max_pairs == 0) {
+      // co-resident CTA pairs: a TPC-paired cluster needs both SMs of a TPC; a floor-swept GPU
+      // may hold fewer than sms / 2 of them (a second wave would double the tail)
+      static int max_pairs[3] = {0, 0, 0};
+      if (max_pairs[cps - 1] == 0) {
         cudaLaunchConfig_t qc = {};
-        qc.gridDim = dim3(sms);
+        qc.gridDim = dim3(dev_sms);
         qc.blockDim = dim3(tc::P2_THREADS);
         qc.dynamicSmemBytes = psm;
         int nc = 0;
-        max_pairs = cudaOccupancyMaxActiveClusters(&nc, variance_f16x2_kernel, &qc) == cudaSuccess && nc > 0
-                        ? nc
-                        : sms / 2;
-        if (getenv("GPMPPI_TC_PRINT")) printf("variance_f16x2_kernel: %d co-resident CTA pairs\n", max_pairs);
+        max_pairs[cps - 1] = cudaOccupancyMaxActiveClusters(&nc, kern, &qc) == cudaSuccess && nc > 0 ? nc : dev_sms / 2;
+        if (getenv("GPMPPI_TC_PRINT")) printf("variance_f16x2_kernel: %d co-resident CTA pairs\n", max_pairs[cps - 1]);
       }
-      const int cap = max_pairs < sms / 2 ? max_pairs : sms / 2;
+      const int cap = max_pairs[cps - 1] < dev_sms / 2 ? max_pairs[cps - 1] : dev_sms / 2;
       const int pairs = (int)(supers < cap ? supers : cap);
-      static int dbg_p = -1;
-      if (dbg_p < 0) {
-        const char* e = getenv("GPMPPI_TC_DEBUG");
-        dbg_p = e ? atoi(e) : 0;
-      }
-      cudaError_t el = launch_pdl(variance_f16x2_kernel, dim3(2 * pairs), dim3(tc::P2_THREADS), psm, st, a, stages, dbg_p);
+      cudaError_t el = launch_pdl(kern, dim3(2 * pairs), dim3(tc::P2_THREADS), psm, st, a, stages, dbg_h);
       if (el != cudaSuccess) return el;
       count_launch();
       return cudaGetLastError();
@@ -2129,18 +2206,22 @@ cudaError_t launch_tc_variance(const VarianceArgs& a, int mode, cudaStream_t st)
   }
   if (mode == 3) mode = 2;  // pair operand absent or shared memory short: the single-CTA kernel
   if (mode == 2 && a.g.tc_h && a.g.tc_hmeta && a.g.tc_np <= 256) {
+    // two chunks per ring stage when three such stages fit
+    int cps = cps_env == 1 ? 1 : 2;
+    if (cps == 2 && f16_smem_bytes(a.g, 3, 2) > kSmemMax) cps = 1;
     int stages = 8;
-    while (stages > 3 && f16_smem_bytes(a.g, stages) > kSmemMax) --stages;
-    if (f16_smem_bytes(a.g, stages) <= kSmemMax) {
-      const size_t hsm = f16_smem_bytes(a.g, stages);
-      cudaError_t eh = cudaFuncSetAttribute(variance_f16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
+    while (stages > 3 && f16_smem_bytes(a.g, stages, cps) > kSmemMax) --stages;
+    if (f16_smem_bytes(a.g, stages, cps) <= kSmemMax) {
+      const size_t hsm = f16_smem_bytes(a.g, stages, cps);
+      void (*kern)(const VarianceArgs, int, int) = cps == 2 ? variance_f16_kernel<2> : variance_f16_kernel<1>;
+      cudaError_t eh = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
       if (eh != cudaSuccess) return eh;
       int dev = 0, sms = 148;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       const long long units = ((a.KT + tc::M - 1) / tc::M + 1) / 2;
       const int grid = (int)(units < sms ? units : sms);
-      cudaError_t el = launch_pdl(variance_f16_kernel, dim3(grid), dim3(tc::F16_THREADS), hsm, st, a, dbg_h, stages);
+      cudaError_t el = launch_pdl(kern, dim3(grid), dim3(tc::F16_THREADS), hsm, st, a, dbg_h, stages);
       if (el != cudaSuccess) return el;
       count_launch();
       return cudaGetLastError();
