@@ -664,6 +664,7 @@ struct gpmppi_planner {
   // pinned staging
   gpm::TaskDev* h_task = nullptr;  // [B] (inside the h_x0 block)
   double* h_x0 = nullptr;          // [B][8] robot tick blocks, then the tasks
+  const double* dh_x0 = nullptr;   // its mapped device address (stage_tick_kernel), null: copy node
   size_t tick_bytes = 0;
   double* h_out = nullptr;         // [B][16], mapped: the reduce writes command + diag + sequence here
   int* h_infeasible = nullptr;     // [B]
@@ -980,7 +981,10 @@ void stage_tick(gpmppi_planner* p, const double* x0, const gpmppi_task* tasks) {
 
 // the tick's two H2D copies from the pinned staging buffers (captured in the tick graph)
 void enqueue_h2d(gpmppi_planner* p) {  // tick blocks + tasks: one copy (contiguous on both sides)
-  CK(cudaMemcpyAsync(p->d_x0, p->h_x0, p->tick_bytes, cudaMemcpyHostToDevice, p->stream));
+  if (p->dh_x0)  // a staging kernel reads the mapped block (GPMPPI_H2D_COPY=1: a copy node)
+    check(gpm::launch_stage_tick(p->dh_x0, p->d_x0, p->tick_bytes, p->stream), "stage tick");
+  else
+    CK(cudaMemcpyAsync(p->d_x0, p->h_x0, p->tick_bytes, cudaMemcpyHostToDevice, p->stream));
 }
 
 // Rollout + variance + reduce for every robot's sample range. finish=1 also
@@ -1290,7 +1294,14 @@ gpmppi_planner* create_planner(const gpmppi_mppi_config* cfg, const gpmppi_predi
       p->d_tvar = p->dalloc<double>((size_t)B * T * G * ns);
     }
     p->alloc_sample_buffers();
-    CK(cudaMallocHost(&p->h_x0, p->tick_bytes));
+    CK(cudaHostAlloc(&p->h_x0, p->tick_bytes, cudaHostAllocMapped));
+    {
+      static const int copy_env = getenv("GPMPPI_H2D_COPY") ? atoi(getenv("GPMPPI_H2D_COPY")) : 0;
+      double* dp = nullptr;
+      if (!copy_env && cudaHostGetDevicePointer(reinterpret_cast<void**>(&dp), p->h_x0, 0) == cudaSuccess)
+        p->dh_x0 = dp;
+      cudaGetLastError();
+    }
     p->h_task = reinterpret_cast<gpm::TaskDev*>(reinterpret_cast<unsigned char*>(p->h_x0) + x0_bytes);
     CK(cudaHostAlloc(&p->h_out, sizeof(double) * gpm::BatchStrides::OUT * B, cudaHostAllocMapped));
     CK(cudaHostAlloc(&p->h_done, sizeof(double) * 2 * B, cudaHostAllocMapped));

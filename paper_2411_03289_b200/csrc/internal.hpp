@@ -222,6 +222,9 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 #endif
 
 // launchers (kernels.cu); all enqueue on `st` and return cudaGetLastError()
+// copies the tick's staged inputs (mapped pinned memory) into device memory: the tick graph's
+// first node (a copy-engine node costs ~9 us more between the launch and the first kernel)
+cudaError_t launch_stage_tick(const void* src_mapped, void* dst, size_t bytes, cudaStream_t st);
 cudaError_t launch_rollout(const RolloutArgs& a, int num_sms, cudaStream_t st);
 cudaError_t launch_variance(const VarianceArgs& a, int path, cudaStream_t st);
 cudaError_t launch_reduce(const ReduceArgs& a, int blocks, cudaStream_t st);

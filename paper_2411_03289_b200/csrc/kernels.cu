@@ -761,6 +761,26 @@ size_t rollout_launch_smem(const RolloutArgs& a, int* scratch_smem) {
   return smem_u + (in_smem ? scr_bytes : 0);
 }
 
+__global__ void __launch_bounds__(256) stage_tick_kernel(const ulonglong2* __restrict__ src, ulonglong2* dst, int n16,
+                                                         const unsigned long long* __restrict__ src8,
+                                                         unsigned long long* dst8, int n8) {
+  pdl_trigger();  // the rollout's model staging may start; it waits for this grid's writes
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  for (int i = tid; i < n16; i += nt) dst[i] = src[i];  // PCIe reads of the mapped block
+  for (int i = 2 * n16 + tid; i < n8; i += nt) dst8[i] = src8[i];
+}
+
+cudaError_t launch_stage_tick(const void* src_mapped, void* dst, size_t bytes, cudaStream_t st) {
+  const int n8 = (int)(bytes / 8), n16 = n8 / 2;
+  const int blocks = n16 / 256 < 1 ? 1 : (n16 / 256 > 148 ? 148 : n16 / 256);  // one 16-byte read per thread per round trip
+  stage_tick_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const ulonglong2*>(src_mapped),
+                                       reinterpret_cast<ulonglong2*>(dst), n16,
+                                       reinterpret_cast<const unsigned long long*>(src_mapped),
+                                       reinterpret_cast<unsigned long long*>(dst), n8);
+  count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_rollout(const RolloutArgs& a, int num_sms, cudaStream_t st) {
   const size_t smem = rollout_smem_bytes(a);
   if (a.K_local <= 0 || a.B <= 0) return cudaSuccess;

@@ -52,6 +52,12 @@ __global__ void bell_kernel(const volatile double* bell, const double* h_in, dou
   (void)seen;
 }
 
+// copies the mapped (host) input block into device memory: the first node instead of a copy
+__global__ void stage_kernel(const double* h_in, double* d_in, int words) {
+  pdl_trigger();
+  for (int i = threadIdx.x; i < words; i += blockDim.x) d_in[i] = ((const volatile double*)h_in)[i];
+}
+
 template <class... KArgs, class... Args>
 cudaError_t launch(void (*k)(KArgs...), int grid, int block, cudaStream_t st, bool pdl, Args... args) {
   cudaLaunchConfig_t c = {};
@@ -139,7 +145,46 @@ int main() {
     if (it + 1 < iters) CK(cudaGraphLaunch(gbe, st));  // arm the next tick (outside the timed span)
   }
   CK(cudaStreamSynchronize(st));
+  // (c) graph: a staging kernel reading the mapped input block (no copy node) + chain
+  cudaGraph_t gc;
+  cudaGraphExec_t gce;
+  CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  CK(launch(stage_kernel, 1, 256, st, false, (const double*)dh_in, d_in, words));
+  for (int k = 0; k < chain; ++k)
+    CK(launch(link_kernel, 148, 256, st, true, (const double*)d_in, d_scr, dh_done, k == chain - 1 ? 1 : 0));
+  CK(cudaStreamEndCapture(st, &gc));
+  CK(cudaGraphInstantiate(&gce, gc, 0));
+  std::vector<double> tc;
+  for (int it = 0; it < iters; ++it) {
+    seq += 1;
+    const auto t0 = Clk::now();
+    h_in[7] = seq;
+    CK(cudaGraphLaunch(gce, st));
+    spin(seq);
+    tc.push_back(std::chrono::duration<double, std::micro>(Clk::now() - t0).count());
+  }
+  CK(cudaStreamSynchronize(st));
+  // (d) graph: the chain alone (input already on the device: the launch-path floor)
+  cudaGraph_t gd;
+  cudaGraphExec_t gde;
+  CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  for (int k = 0; k < chain; ++k)
+    CK(launch(link_kernel, 148, 256, st, k > 0, (const double*)dh_in, d_scr, dh_done, k == chain - 1 ? 1 : 0));
+  CK(cudaStreamEndCapture(st, &gd));
+  CK(cudaGraphInstantiate(&gde, gd, 0));
+  std::vector<double> td;
+  for (int it = 0; it < iters; ++it) {
+    seq += 1;
+    const auto t0 = Clk::now();
+    h_in[7] = seq;
+    CK(cudaGraphLaunch(gde, st));
+    spin(seq);
+    td.push_back(std::chrono::duration<double, std::micro>(Clk::now() - t0).count());
+  }
+  CK(cudaStreamSynchronize(st));
   stats("graph launch (H2D node + 6 PDL kernels)", ta);
+  stats("graph launch (staging kernel + 6 PDL kernels)", tc);
+  stats("graph launch (6 PDL kernels, mapped input)", td);
   stats("pre-launched doorbell (+ 6 PDL kernels)", tb);
   return 0;
 }
