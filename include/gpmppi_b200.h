@@ -218,8 +218,9 @@ int gpmppi_planner_flags(const gpmppi_planner* p, uint8_t* viol, uint8_t* coll,
 /* ---- variance path (north star: tensor cores only where tolerance allows) ----
  * FFMA: FP32 CUDA cores. TC_3XTF32: tcgen05 kind::tf32, hi/lo splits, three products.
  * TC_1XTF32: one TF32 product (not a parity path). TC_3XF16 (default): tcgen05 kind::f16
- * on scaled hi/lo FP16 operands -- the same 22-bit splits at twice the TF32 rate.
- * Measured bounds: tests/test_gpu_variance_paths.py. */
+ * on scaled hi/lo FP16 operands -- the same 22-bit splits at twice the TF32 rate; the
+ * library runs it on single CTAs or CTA pairs by shape.
+ * TC_3XF16_PAIR forces the CTA-pair kernel. Measured bounds: tests/test_gpu_variance_paths.py. */
 enum {
   GPMPPI_VAR_FFMA = 0,
   GPMPPI_VAR_TC_3XTF32 = 1,
