@@ -2193,15 +2193,19 @@ cudaError_t launch_tc_variance(const VarianceArgs& a, int mode, cudaStream_t st)
         qc.blockDim = dim3(tc::P2_THREADS);
         qc.dynamicSmemBytes = psm;
         int nc = 0;
-        max_pairs[cps - 1] = cudaOccupancyMaxActiveClusters(&nc, kern, &qc) == cudaSuccess && nc > 0 ? nc : dev_sms / 2;
+        const cudaError_t eo = cudaOccupancyMaxActiveClusters(&nc, kern, &qc);
+        cudaGetLastError();
+        max_pairs[cps - 1] = eo == cudaSuccess ? (nc > 0 ? nc : -1) : dev_sms / 2;  // -1: no pair fits
         if (getenv("GPMPPI_TC_PRINT")) printf("variance_f16x2_kernel: %d co-resident CTA pairs\n", max_pairs[cps - 1]);
       }
-      const int cap = max_pairs[cps - 1] < dev_sms / 2 ? max_pairs[cps - 1] : dev_sms / 2;
-      const int pairs = (int)(supers < cap ? supers : cap);
-      cudaError_t el = launch_pdl(kern, dim3(2 * pairs), dim3(tc::P2_THREADS), psm, st, a, stages, dbg_h);
-      if (el != cudaSuccess) return el;
-      count_launch();
-      return cudaGetLastError();
+      if (max_pairs[cps - 1] > 0) {  // else: the single-CTA kernel below
+        const int cap = max_pairs[cps - 1] < dev_sms / 2 ? max_pairs[cps - 1] : dev_sms / 2;
+        const int pairs = (int)(supers < cap ? supers : cap);
+        cudaError_t el = launch_pdl(kern, dim3(2 * pairs), dim3(tc::P2_THREADS), psm, st, a, stages, dbg_h);
+        if (el != cudaSuccess) return el;
+        count_launch();
+        return cudaGetLastError();
+      }
     }
   }
   if (mode == 3) mode = 2;  // pair operand absent or shared memory short: the single-CTA kernel
