@@ -660,6 +660,7 @@ struct gpmppi_planner {
   unsigned int* d_ticket = nullptr;
   int* d_infeasible = nullptr;
   double *d_tq = nullptr, *d_tmu = nullptr, *d_tJ = nullptr, *d_tvar = nullptr;
+  unsigned int* d_tflags = nullptr;  // pipelined single-robot tightening (TightenArgs::tflags)
   double* d_scratch = nullptr;
   // pinned staging
   gpm::TaskDev* h_task = nullptr;  // [B] (inside the h_x0 block)
@@ -1148,6 +1149,8 @@ void enqueue_tighten(gpmppi_planner* p) {
   t.tJ = p->d_tJ;
   t.tvar_part = p->d_tvar;
   t.done_host = p->zc_tick ? p->d_done_host : nullptr;
+  static const int seq_env = getenv("GPMPPI_TIGHTEN_SEQUENTIAL") ? atoi(getenv("GPMPPI_TIGHTEN_SEQUENTIAL")) : 0;
+  t.tflags = (p->B == 1 && p->model_kind == GPMPPI_MODEL_GP_ENSEMBLE && !seq_env) ? p->d_tflags : nullptr;
   check(gpm::launch_tighten(t, p->stream), "tighten kernel");
 }
 
@@ -1286,6 +1289,8 @@ gpmppi_planner* create_planner(const gpmppi_mppi_config* cfg, const gpmppi_predi
     p->d_ticket = p->dalloc<unsigned int>(B);
     p->d_infeasible = p->dalloc<int>(B);
     p->d_tq = p->dalloc<double>((size_t)B * T * 4);
+    p->d_tflags = p->dalloc<unsigned int>(2);
+    CK(cudaMemsetAsync(p->d_tflags, 0, 2 * sizeof(unsigned int), p->stream));
     p->d_tmu = p->dalloc<double>((size_t)B * (T + 1) * 5);
     p->d_tJ = p->dalloc<double>((size_t)B * T * 25);
     {

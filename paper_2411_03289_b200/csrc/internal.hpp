@@ -184,6 +184,11 @@ struct TightenArgs {
   double* tmu;        // [B][T+1][5] belief means
   double* tJ;         // [B][T][25] Jacobians
   double* tvar_part;  // [B][T][G][splits] partial ||L^{-1}k*||^2
+  // single-robot pipelining: the mean kernel raises flag 0 when its chain (the GP queries)
+  // is done and flag 1 when the Jacobians / belief means are; the variance grid starts on
+  // flag 0 instead of the mean grid's completion (it overlaps the mean kernel's tail), the
+  // covariance kernel waits for flag 1 and lowers both at its end. Null: grid ordering only.
+  unsigned int* tflags;  // [2]
 };
 
 // Programmatic dependent launch: the kernel may be scheduled while its stream

@@ -1385,6 +1385,24 @@ cudaError_t launch_predict(const ModelDev& m, const double* q, long long S, doub
 // rows of L^{-1} per tightening-variance block: short slices (more, shorter blocks: the
 // per-warp row loop is L2-latency bound) while the per-block k* recomputation is cheap
 // (one robot only: with many robots the grid is already wide and 64-row slices recompute less)
+__device__ __forceinline__ void st_release_u32(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// a flag wait that outlives ~2 s is a protocol bug: trap instead of hanging the device
+__device__ void spin_until_flag(const unsigned int* f, const char* who) {
+  for (unsigned it = 0; ld_acquire_u32(f) == 0u; ++it) {
+    __nanosleep(64);
+    if (it > (1u << 25)) {
+      printf("%s: tightening flag wait timed out\n", who);
+      __trap();
+    }
+  }
+}
 GPM_HD int tight_rows(int n, int B) { return (B == 1 && n <= 1024) ? 16 : 64; }
 
 // Belief-mean chain. The GP query of step k needs only (v_k, omega_k, u_k) and
@@ -1398,7 +1416,7 @@ GPM_HD int tight_rows(int n, int B) { return (B == 1 && n <= 1024) ? 16 : 64; }
 constexpr int TMEAN_THREADS = GPM_TMEAN_THREADS;
 template <int NO>
 __global__ void __launch_bounds__(TMEAN_THREADS, 1) tighten_mean_kernel(const TightenArgs a) {
-  pdl_trigger();
+  if (!a.tflags) pdl_trigger();  // pipelined: the variance grid is released after the reduction
   const int rb = blockIdx.x;  // robot
 #ifdef GPM_TMEAN_TRACE
   const long long tk0 = clock64();
@@ -1459,6 +1477,7 @@ __global__ void __launch_bounds__(TMEAN_THREADS, 1) tighten_mean_kernel(const Ti
     }
   }
   pdl_wait();  // the nominal sequence comes from the reduction
+  if (a.tflags) pdl_trigger();
   for (int i = threadIdx.x; i < 2 * T; i += blockDim.x) nom[i] = a.nominal_seq[(size_t)rb * BatchStrides::nom(T) + i];
   if (threadIdx.x == 0) {
     vv[0] = ax0[3];
@@ -1632,6 +1651,7 @@ __global__ void __launch_bounds__(TMEAN_THREADS, 1) tighten_mean_kernel(const Ti
       ww[k + 1] = om;
     }
   }
+  if (a.tflags && threadIdx.x == 0) st_release_u32(a.tflags, 1u);  // every query (thread 0's writes) is out
   __syncthreads();
 #ifdef GPM_TMEAN_TRACE
   const long long tk2 = clock64();
@@ -1691,6 +1711,13 @@ __global__ void __launch_bounds__(TMEAN_THREADS, 1) tighten_mean_kernel(const Ti
         }
     }
   }
+  if (a.tflags) {  // Jacobians and belief means are out
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      st_release_u32(a.tflags + 1, 1u);
+    }
+  }
 #ifdef GPM_TMEAN_TRACE
   if (threadIdx.x == 0) {
     const long long tk3 = clock64();
@@ -1703,8 +1730,14 @@ __global__ void __launch_bounds__(TMEAN_THREADS, 1) tighten_mean_kernel(const Ti
 // L^{-1}. One warp per row: a_j = sum_{i<=j} k_i L^{-1}[j][i] with the lanes striding
 // the contiguous row (coalesced), then a_j^2 (gp.cpp:184-191).
 __global__ void __launch_bounds__(256) tighten_var_kernel(const TightenArgs a) {
-  pdl_wait();
-  pdl_trigger();
+  if (a.tflags) {  // pipelined: start when the mean chain's queries are out (flag 0)
+    pdl_trigger();
+    if (threadIdx.x == 0) spin_until_flag(a.tflags, "tighten_var_kernel");
+    __syncthreads();
+  } else {
+    pdl_wait();
+    pdl_trigger();
+  }
   extern __shared__ __align__(16) double kst[];
   __shared__ double red[8];
   const int k = blockIdx.x, g = blockIdx.y % a.model.G, rb = blockIdx.y / a.model.G, c = blockIdx.z;
@@ -1807,6 +1840,10 @@ __global__ void __launch_bounds__(256, 1) tighten_cov_kernel(const TightenArgs a
   // guarantees their visibility only after this grid's own griddepcontrol.wait, so the
   // staging follows it (it does not rely on the variance grid's wait-before-trigger order)
   pdl_wait();
+  if (a.tflags) {  // pipelined: the mean kernel's tail may still be running
+    if (l == 0) spin_until_flag(a.tflags + 1, "tighten_cov_kernel");
+    __syncthreads();
+  }
   for (int i = l; i < 25 * T; i += nt) Js[i] = atJ[i];
   for (int i = l; i < 5 * (T + 1); i += nt) mus[i] = atmu[i];
   __syncthreads();
@@ -1955,6 +1992,10 @@ __global__ void __launch_bounds__(256, 1) tighten_cov_kernel(const TightenArgs a
     }
   __syncthreads();
   if (l == 0) {
+    if (a.tflags) {  // every reader of this tick's flags is done (the variance grid completed)
+      a.tflags[0] = 0u;
+      a.tflags[1] = 0u;
+    }
     a.infeasible[rb] = infeasible;
     if (a.done_host) {  // zero-copy: infeasibility, then the tick's sequence number
       const double v = (double)infeasible;
