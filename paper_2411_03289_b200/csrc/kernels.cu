@@ -1394,8 +1394,8 @@ __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
   return v;
 }
 // a flag wait that outlives ~2 s is a protocol bug: trap instead of hanging the device
-__device__ void spin_until_flag(const unsigned int* f, const char* who) {
-  for (unsigned it = 0; ld_acquire_u32(f) == 0u; ++it) {
+__device__ void spin_until_flag(const unsigned int* f, unsigned int at_least, const char* who) {
+  for (unsigned it = 0; ld_acquire_u32(f) < at_least; ++it) {
     __nanosleep(64);
     if (it > (1u << 25)) {
       printf("%s: tightening flag wait timed out\n", who);
@@ -1415,7 +1415,7 @@ GPM_HD int tight_rows(int n, int B) { return (B == 1 && n <= 1024) ? 16 : 64; }
 #endif
 constexpr int TMEAN_THREADS = GPM_TMEAN_THREADS;
 template <int NO>
-__global__ void __launch_bounds__(TMEAN_THREADS, 1) tighten_mean_kernel(const TightenArgs a) {
+__global__ void __launch_bounds__(TMEAN_THREADS + 32, 1) tighten_mean_kernel(const TightenArgs a) {
   if (!a.tflags) pdl_trigger();  // pipelined: the variance grid is released after the reduction
   const int rb = blockIdx.x;  // robot
 #ifdef GPM_TMEAN_TRACE
@@ -1492,7 +1492,11 @@ __global__ void __launch_bounds__(TMEAN_THREADS, 1) tighten_mean_kernel(const Ti
   // reference's division) to keep FP64 divides off the serial path.
   __shared__ __align__(16) double red[2][kMaxGroups][TMEAN_THREADS / 32][2];  // [parity][group][warp][v, omega]
   __shared__ double gil[kMaxGroups][4];  // reciprocal lengthscales
-  const int nwarps = blockDim.x >> 5;
+  // pipelined (a.tflags): warp TMEAN_THREADS / 32 publishes each step's query (and raises the
+  // query counter, flag 0) while the chain warps run on: its fences stay off the serial path
+  __shared__ volatile int prog;  // chain steps done (thread 0, after vv / ww)
+  const bool pub = a.tflags != nullptr && threadIdx.x >= TMEAN_THREADS;
+  if (threadIdx.x == 0) prog = 0;
   const int ns = a.model.ns;
   const int G = a.model_kind == MODEL_GP ? a.model.G : 0;
   if (threadIdx.x < 4 * G) gil[threadIdx.x >> 2][threadIdx.x & 3] = 1.0 / a.model.g[threadIdx.x >> 2].ls[threadIdx.x & 3];
@@ -1529,6 +1533,27 @@ __global__ void __launch_bounds__(TMEAN_THREADS, 1) tighten_mean_kernel(const Ti
 #pragma unroll
     for (int i = 0; i < 4; ++i) e_cur[i] = fma(q2, rz2[i], fma(q3, rz3[i], rzn[i] + qu));
   }
+  if (pub) {  // the whole warp walks the loop (convergent), lane 0 stores and publishes
+    for (int k = 0; k < T;) {
+      int done;
+      for (unsigned it = 0; (done = prog) < k; ++it)
+        if (it > (1u << 28)) __trap();
+      done = __shfl_sync(0xffffffffu, done, 0);
+      const int k1 = done + 1 < T ? done + 1 : T;  // query k = (v_k, omega_k, u_k): known once step k-1 is done
+      if (lane == 0) {
+        for (int kk = k; kk < k1; ++kk) {
+          atq[kk * 4 + 0] = vv[kk];
+          atq[kk * 4 + 1] = ww[kk];
+          atq[kk * 4 + 2] = nom[2 * kk];
+          atq[kk * 4 + 3] = nom[2 * kk + 1];
+        }
+        __threadfence();
+        st_release_u32(a.tflags, (unsigned)k1);  // queries [0, k1) are out
+      }
+      k = k1;
+      __syncwarp();
+    }
+  } else
   for (int k = 0; k < T; ++k) {
     TRC(0);
     const double u0 = nom[2 * k], u1 = nom[2 * k + 1];
@@ -1560,7 +1585,7 @@ __global__ void __launch_bounds__(TMEAN_THREADS, 1) tighten_mean_kernel(const Ti
 #pragma unroll
         for (int i = 0; i < 4; ++i) e_cur[i] = fma(q2, rz2[i], fma(q3, rz3[i], rzn[i] + qu));
       }
-      __syncthreads();
+      asm volatile("bar.sync 1, %0;" ::"n"(TMEAN_THREADS) : "memory");  // the chain warps
       TRC(3);
       double2 pr[TMEAN_THREADS / 32];
 #pragma unroll
@@ -1613,7 +1638,7 @@ __global__ void __launch_bounds__(TMEAN_THREADS, 1) tighten_mean_kernel(const Ti
         TRC(2);
         p += (size_t)7 * ns;
       }
-      __syncthreads();
+      asm volatile("bar.sync 1, %0;" ::"n"(TMEAN_THREADS) : "memory");  // the chain warps
       TRC(3);
       for (int g = 0; g < G; ++g) {
         // every thread sums the per-warp partials in warp order (identical bits everywhere)
@@ -1631,7 +1656,7 @@ __global__ void __launch_bounds__(TMEAN_THREADS, 1) tighten_mean_kernel(const Ti
       }
     }
     TRC(4);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && !a.tflags) {
       atq[k * 4 + 0] = v;
       atq[k * 4 + 1] = om;
       atq[k * 4 + 2] = u0;
@@ -1649,9 +1674,12 @@ __global__ void __launch_bounds__(TMEAN_THREADS, 1) tighten_mean_kernel(const Ti
     if (threadIdx.x == 0) {
       vv[k + 1] = v;
       ww[k + 1] = om;
+      if (a.tflags) {
+        __threadfence_block();
+        prog = k + 1;
+      }
     }
   }
-  if (a.tflags && threadIdx.x == 0) st_release_u32(a.tflags, 1u);  // every query (thread 0's writes) is out
   __syncthreads();
 #ifdef GPM_TMEAN_TRACE
   const long long tk2 = clock64();
@@ -1732,7 +1760,7 @@ __global__ void __launch_bounds__(TMEAN_THREADS, 1) tighten_mean_kernel(const Ti
 __global__ void __launch_bounds__(256) tighten_var_kernel(const TightenArgs a) {
   if (a.tflags) {  // pipelined: start when the mean chain's queries are out (flag 0)
     pdl_trigger();
-    if (threadIdx.x == 0) spin_until_flag(a.tflags, "tighten_var_kernel");
+    if (threadIdx.x == 0) spin_until_flag(a.tflags, (unsigned)blockIdx.x + 1u, "tighten_var_kernel");
     __syncthreads();
   } else {
     pdl_wait();
@@ -1841,7 +1869,7 @@ __global__ void __launch_bounds__(256, 1) tighten_cov_kernel(const TightenArgs a
   // staging follows it (it does not rely on the variance grid's wait-before-trigger order)
   pdl_wait();
   if (a.tflags) {  // pipelined: the mean kernel's tail may still be running
-    if (l == 0) spin_until_flag(a.tflags + 1, "tighten_cov_kernel");
+    if (l == 0) spin_until_flag(a.tflags + 1, 1u, "tighten_cov_kernel");
     __syncthreads();
   }
   for (int i = l; i < 25 * T; i += nt) Js[i] = atJ[i];
@@ -2019,7 +2047,7 @@ cudaError_t launch_tighten(const TightenArgs& a, cudaStream_t st) {
   void (*mk)(const TightenArgs) = no <= 2 ? tighten_mean_kernel<2> : no <= 4 ? tighten_mean_kernel<4>
                                   : no <= 6 ? tighten_mean_kernel<6> : tighten_mean_kernel<8>;
   cudaFuncSetAttribute(mk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm);  // static + dynamic may exceed 48 KB
-  cudaError_t el = launch_pdl(mk, dim3(a.B), dim3(TMEAN_THREADS), msm, st, a);
+  cudaError_t el = launch_pdl(mk, dim3(a.B), dim3(TMEAN_THREADS + (a.tflags ? 32 : 0)), msm, st, a);
   if (el != cudaSuccess) return el;
   const int G = a.model_kind == MODEL_GP ? a.model.G : 1;
   const int ns = a.model_kind == MODEL_GP ? tighten_splits(a.model.n, a.B) : 1;
