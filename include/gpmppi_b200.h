@@ -257,6 +257,9 @@ int gpmppi_debug_tc_profile(double* out16);
 /* diagnostics: clock64 timeline of CTA 0 of the last tensor-core variance launch
  * (GPMPPI_TC_DEBUG bit 4096): entry, role tile starts, accumulator hand-offs */
 int gpmppi_debug_tc_trace(double* out64);
+/* diagnostics: %globaltimer stamps (ns) at fixed points of the last tick, filled by a
+ * -DGPM_TIMELINE build (tools/timeline.py); zeros otherwise; read-and-reset */
+int gpmppi_debug_timeline(double* out32);
 int gpmppi_tuple_doubles(int horizon);
 int gpmppi_planner_set_shard(gpmppi_planner* p, int64_t begin, int64_t count);
 int gpmppi_planner_plan_partial(gpmppi_planner* p, const double x0[5], const gpmppi_task* task,

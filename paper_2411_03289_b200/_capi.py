@@ -134,6 +134,7 @@ SIGNATURES = [
     ("gpmppi_planner_io_bytes", C.c_int, [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("gpmppi_debug_tc_profile", C.c_int, [_dp]),
     ("gpmppi_debug_tc_trace", C.c_int, [_dp]),
+    ("gpmppi_debug_timeline", C.c_int, [_dp]),
     ("gpmppi_tuple_doubles", C.c_int, [C.c_int]),
     ("gpmppi_planner_set_shard", C.c_int, [_vp, C.c_int64, C.c_int64]),
     ("gpmppi_planner_plan_partial", C.c_int, [_vp, _dp, C.POINTER(TaskC), _vp]),

@@ -661,6 +661,7 @@ struct gpmppi_planner {
   int* d_infeasible = nullptr;
   double *d_tq = nullptr, *d_tmu = nullptr, *d_tJ = nullptr, *d_tvar = nullptr;
   unsigned int* d_tflags = nullptr;  // pipelined single-robot tightening (TightenArgs::tflags)
+  double* d_tcv = nullptr;            // its per-step combined correction variances
   double* d_scratch = nullptr;
   // pinned staging
   gpm::TaskDev* h_task = nullptr;  // [B] (inside the h_x0 block)
@@ -1151,6 +1152,7 @@ void enqueue_tighten(gpmppi_planner* p) {
   t.done_host = p->zc_tick ? p->d_done_host : nullptr;
   static const int seq_env = getenv("GPMPPI_TIGHTEN_SEQUENTIAL") ? atoi(getenv("GPMPPI_TIGHTEN_SEQUENTIAL")) : 0;
   t.tflags = (p->B == 1 && p->model_kind == GPMPPI_MODEL_GP_ENSEMBLE && !seq_env) ? p->d_tflags : nullptr;
+  t.tcv = p->d_tcv;
   check(gpm::launch_tighten(t, p->stream), "tighten kernel");
 }
 
@@ -1289,8 +1291,9 @@ gpmppi_planner* create_planner(const gpmppi_mppi_config* cfg, const gpmppi_predi
     p->d_ticket = p->dalloc<unsigned int>(B);
     p->d_infeasible = p->dalloc<int>(B);
     p->d_tq = p->dalloc<double>((size_t)B * T * 4);
-    p->d_tflags = p->dalloc<unsigned int>(2);
-    CK(cudaMemsetAsync(p->d_tflags, 0, 2 * sizeof(unsigned int), p->stream));
+    p->d_tflags = p->dalloc<unsigned int>((size_t)T + 2);  // query count, J count, per-step variance counts
+    CK(cudaMemsetAsync(p->d_tflags, 0, sizeof(unsigned int) * ((size_t)T + 2), p->stream));
+    p->d_tcv = p->dalloc<double>((size_t)2 * T);
     p->d_tmu = p->dalloc<double>((size_t)B * (T + 1) * 5);
     p->d_tJ = p->dalloc<double>((size_t)B * T * 25);
     {
@@ -1830,6 +1833,10 @@ int gpmppi_debug_tc_profile(double* out16) {
 
 int gpmppi_debug_tc_trace(double* out64) {
   return guarded([&] { gpm::tc_trace_read(out64); });
+}
+
+int gpmppi_debug_timeline(double* out32) {
+  return guarded([&] { gpm::timeline_read(out32); });
 }
 
 int gpmppi_tuple_doubles(int horizon) { return gpm::tuple_doubles(horizon); }

@@ -184,11 +184,13 @@ struct TightenArgs {
   double* tmu;        // [B][T+1][5] belief means
   double* tJ;         // [B][T][25] Jacobians
   double* tvar_part;  // [B][T][G][splits] partial ||L^{-1}k*||^2
-  // single-robot pipelining: the mean kernel raises flag 0 when its chain (the GP queries)
-  // is done and flag 1 when the Jacobians / belief means are; the variance grid starts on
-  // flag 0 instead of the mean grid's completion (it overlaps the mean kernel's tail), the
-  // covariance kernel waits for flag 1 and lowers both at its end. Null: grid ordering only.
-  unsigned int* tflags;  // [2]
+  // single-robot pipelining: the mean kernel's publisher warp counts the steps whose GP query
+  // (flag 0) and Jacobian / belief mean (flag 1) are out; the variance block of step k starts
+  // at query k and counts step k's finished slices (flags[2 + k]); the covariance kernel runs
+  // the recursion and thresholds step by step behind them and lowers every flag at its end.
+  // Null: grid ordering only (batched planners).
+  unsigned int* tflags;  // [T + 2]: queries out, J / belief means out, per-step variance slices done
+  double* tcv;           // [T][2] combined correction variances of the pipelined pass
 };
 
 // Programmatic dependent launch: the kernel may be scheduled while its stream
@@ -223,6 +225,21 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
   return v;
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// tick timeline (diagnostics, -DGPM_TIMELINE): %globaltimer at fixed points, slot i keeps the
+// latest (even i) or the earliest (odd i) stamp of the tick
+#ifdef GPM_TIMELINE
+static __device__ unsigned long long g_tl[32];  // one per translation unit (timeline_read merges them)
+__device__ __forceinline__ void tl_stamp(int i) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (i & 1)
+    atomicMin(&g_tl[i], t);
+  else
+    atomicMax(&g_tl[i], t);
+}
+#else
+__device__ __forceinline__ void tl_stamp(int) {}
+#endif
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 #endif
 
@@ -292,6 +309,8 @@ void build_tc_operand(const double* ilt, int n, std::vector<float>& data, std::v
                       int& n_pad, int& np, int& n_pass);
 void tc_profile_read(double* out);
 void tc_trace_read(double* out);  // 64 clock64 stamps of CTA 0 (GPMPPI_TC_DEBUG bit 4096)
+void timeline_read(double* out);  // 32 %globaltimer stamps of the last tick (-DGPM_TIMELINE builds), read-and-reset
+void timeline_read_unit(unsigned long long* h);  // kernels_tc.cu's copy of the stamps, read-and-reset
 void count_launch(int n = 1);
 // fit.cu: device Cholesky (jitter ladder) + L^{-1} for GpModel::fit at large n.
 cudaError_t device_factor(const double* K, int n, double noise_var, double* L_out, double* X_out,

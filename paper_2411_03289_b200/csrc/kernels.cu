@@ -361,6 +361,7 @@ GPM_D void rollout_phase2(const RolloutArgs& a, const SmemView& sv, const TaskDe
 
 template <int LPS, int SPG>
 __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const RolloutArgs a) {
+  if (threadIdx.x == 0) tl_stamp(1);
   pdl_trigger();  // single wave: the variance grid may be scheduled (it waits for this grid)
   extern __shared__ __align__(16) unsigned char smem[];
   const SmemView sv = carve_smem(a, smem);
@@ -600,6 +601,7 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
       }
     }
   }
+  if (threadIdx.x == 0) tl_stamp(0);
 }
 
 // GP-free models (mppi.cpp:351-368): one thread per sample; block = one robot chunk.
@@ -764,10 +766,30 @@ size_t rollout_launch_smem(const RolloutArgs& a, int* scratch_smem) {
 __global__ void __launch_bounds__(256) stage_tick_kernel(const ulonglong2* __restrict__ src, ulonglong2* dst, int n16,
                                                          const unsigned long long* __restrict__ src8,
                                                          unsigned long long* dst8, int n8) {
+  if (threadIdx.x == 0) tl_stamp(17);
   pdl_trigger();  // the rollout's model staging may start; it waits for this grid's writes
   const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
   for (int i = tid; i < n16; i += nt) dst[i] = src[i];  // PCIe reads of the mapped block
   for (int i = 2 * n16 + tid; i < n8; i += nt) dst8[i] = src8[i];
+  if (threadIdx.x == 0) tl_stamp(16);
+}
+
+void timeline_read(double* out) {
+#ifdef GPM_TIMELINE
+  unsigned long long h[32], u[32];
+  cudaMemcpyFromSymbol(h, g_tl, sizeof h);
+  timeline_read_unit(u);
+  for (int i = 0; i < 32; ++i) {
+    const bool hv = (i & 1) ? h[i] != ~0ull && h[i] != 0ull : h[i] != 0ull;
+    const bool uv = (i & 1) ? u[i] != ~0ull && u[i] != 0ull : u[i] != 0ull;
+    const unsigned long long m = !hv ? u[i] : !uv ? h[i] : ((i & 1) ? (h[i] < u[i] ? h[i] : u[i]) : (h[i] > u[i] ? h[i] : u[i]));
+    out[i] = (hv || uv) ? (double)m : 0.0;
+  }
+  for (int i = 0; i < 32; ++i) h[i] = (i & 1) ? ~0ull : 0ull;
+  cudaMemcpyToSymbol(g_tl, h, sizeof h);
+#else
+  for (int i = 0; i < 32; ++i) out[i] = 0.0;
+#endif
 }
 
 cudaError_t launch_stage_tick(const void* src_mapped, void* dst, size_t bytes, cudaStream_t st) {
@@ -1014,6 +1036,7 @@ constexpr int kEpsDepth = 8;  // pass-3 noise loads in flight per thread
 
 __global__ void __launch_bounds__(256, 1) reduce_kernel(const ReduceArgs a) {
   pdl_wait();
+  if (threadIdx.x == 0) tl_stamp(5);
   pdl_trigger();
   // re-arm the rollout's query-progress words for the next tick: the co-resident variance
   // (the predecessor this grid waited for) has finished reading them
@@ -1249,6 +1272,7 @@ __global__ void __launch_bounds__(256, 1) reduce_kernel(const ReduceArgs a) {
   if (threadIdx.x == 0)
     printf("reduce last: heads %lld combine+S %lld apply %lld\n", rt_[5] - rt_[4], rt_[6] - rt_[5], rt_[7] - rt_[6]);
 #endif
+  if (threadIdx.x == 0) tl_stamp(4);
 }
 
 cudaError_t launch_reduce(const ReduceArgs& a, int blocks, cudaStream_t st) {
@@ -1388,6 +1412,11 @@ cudaError_t launch_predict(const ModelDev& m, const double* q, long long S, doub
 __device__ __forceinline__ void st_release_u32(unsigned int* p, unsigned int v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ unsigned int ld_relaxed_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
   unsigned int v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -1395,15 +1424,23 @@ __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
 }
 // a flag wait that outlives ~2 s is a protocol bug: trap instead of hanging the device
 __device__ void spin_until_flag(const unsigned int* f, unsigned int at_least, const char* who) {
-  for (unsigned it = 0; ld_acquire_u32(f) < at_least; ++it) {
-    __nanosleep(64);
+  // counter flags advance about once per chain step (~0.5 us): a waiter far behind sleeps in
+  // proportion, so ~a thousand waiting blocks do not hammer one L2 line
+  // relaxed polls (an acquire per poll invalidates L1 each time), one fence once it is seen
+  for (unsigned it = 0, v; (v = ld_relaxed_u32(f)) < at_least; ++it) {
+    const unsigned gap = at_least - v;
+    __nanosleep(gap > 8u ? 2048u : 64u + 256u * (gap - 1u));
     if (it > (1u << 25)) {
       printf("%s: tightening flag wait timed out\n", who);
       __trap();
     }
   }
+  __threadfence();  // acquire: the data published before the flag
 }
-GPM_HD int tight_rows(int n, int B) { return (B == 1 && n <= 1024) ? 16 : 64; }
+#ifndef GPM_TIGHT_ROWS1
+#define GPM_TIGHT_ROWS1 16
+#endif
+GPM_HD int tight_rows(int n, int B) { return (B == 1 && n <= 1024) ? GPM_TIGHT_ROWS1 : 64; }
 
 // Belief-mean chain. The GP query of step k needs only (v_k, omega_k, u_k) and
 // the lag update of (v, omega) is cheap, so the serial part carries (v, omega)
@@ -1415,7 +1452,7 @@ GPM_HD int tight_rows(int n, int B) { return (B == 1 && n <= 1024) ? 16 : 64; }
 #endif
 constexpr int TMEAN_THREADS = GPM_TMEAN_THREADS;
 template <int NO>
-__global__ void __launch_bounds__(TMEAN_THREADS + 32, 1) tighten_mean_kernel(const TightenArgs a) {
+__global__ void __launch_bounds__(TMEAN_THREADS + 96, 1) tighten_mean_kernel(const TightenArgs a) {
   if (!a.tflags) pdl_trigger();  // pipelined: the variance grid is released after the reduction
   const int rb = blockIdx.x;  // robot
 #ifdef GPM_TMEAN_TRACE
@@ -1477,6 +1514,7 @@ __global__ void __launch_bounds__(TMEAN_THREADS + 32, 1) tighten_mean_kernel(con
     }
   }
   pdl_wait();  // the nominal sequence comes from the reduction
+  if (threadIdx.x == 0) tl_stamp(9);
   if (a.tflags) pdl_trigger();
   for (int i = threadIdx.x; i < 2 * T; i += blockDim.x) nom[i] = a.nominal_seq[(size_t)rb * BatchStrides::nom(T) + i];
   if (threadIdx.x == 0) {
@@ -1495,8 +1533,31 @@ __global__ void __launch_bounds__(TMEAN_THREADS + 32, 1) tighten_mean_kernel(con
   // pipelined (a.tflags): warp TMEAN_THREADS / 32 publishes each step's query (and raises the
   // query counter, flag 0) while the chain warps run on: its fences stay off the serial path
   __shared__ volatile int prog;  // chain steps done (thread 0, after vv / ww)
-  const bool pub = a.tflags != nullptr && threadIdx.x >= TMEAN_THREADS;
-  if (threadIdx.x == 0) prog = 0;
+  // pipelined roles of the three warps after the chain's: 0 publisher, 1 cv stager, 2 covariance
+  // recursion (tighten_cov_kernel's, step by step behind the chain); the thresholds follow the
+  // final barrier on every thread
+  const int role = a.tflags != nullptr && threadIdx.x >= TMEAN_THREADS ? (int)(threadIdx.x - TMEAN_THREADS) >> 5 : -1;
+  const bool pub = role == 0;
+  __shared__ volatile int j_ready, mu_ready, s_done;
+  __shared__ int infeasible, gof[2 * kMaxTerrains];
+  double* const pJ = pts + (size_t)7 * a.model.ns * (a.model.G > 0 ? a.model.G : 1);  // [T][9] sparse J
+  double* const pcv = pJ + 9 * T;         // [T][2] combined correction variances
+  double* const pS = pcv + 2 * T;         // [T][25] propagated covariances
+  double* const pxy = pS + 25 * T;        // [T+1][2] belief-mean positions
+  volatile int* const cv_ready = reinterpret_cast<volatile int*>(pxy + 2 * (T + 1));  // [T]
+  if (threadIdx.x == 0) {
+    prog = 0;
+    j_ready = 0;
+    mu_ready = 0;
+    s_done = 0;
+    infeasible = 0;
+  }
+  if (a.tflags) {
+    for (int i = threadIdx.x; i < T; i += blockDim.x) cv_ready[i] = 0;
+    if (threadIdx.x == 0)
+      for (int g = 0; g < a.model.G; ++g)
+        for (int o = 0; o < a.model.g[g].n_out; ++o) gof[a.model.g[g].out_idx[o]] = g;
+  }
   const int ns = a.model.ns;
   const int G = a.model_kind == MODEL_GP ? a.model.G : 0;
   if (threadIdx.x < 4 * G) gil[threadIdx.x >> 2][threadIdx.x & 3] = 1.0 / a.model.g[threadIdx.x >> 2].ls[threadIdx.x & 3];
@@ -1533,14 +1594,21 @@ __global__ void __launch_bounds__(TMEAN_THREADS + 32, 1) tighten_mean_kernel(con
 #pragma unroll
     for (int i = 0; i < 4; ++i) e_cur[i] = fma(q2, rz2[i], fma(q3, rz3[i], rzn[i] + qu));
   }
-  if (pub) {  // the whole warp walks the loop (convergent), lane 0 stores and publishes
+  if (pub) {
+    // the publisher warp walks the chain's steps as they complete (convergent): per batch of
+    // newly known steps, lane 0 advances the heading recursion, one lane per step evaluates the
+    // arc increment and the Jacobian (as the sequential tail below), lane 0 writes the queries,
+    // the belief means (positions summed in step order) and raises the query counter; after
+    // the last step, the final belief mean and flag 1
+    double px = ax0[0], py = ax0[1];  // lane 0: position prefix sums
+    double t = th[0];                 // lane 0: heading recursion
     for (int k = 0; k < T;) {
       int done;
       for (unsigned it = 0; (done = prog) < k; ++it)
         if (it > (1u << 28)) __trap();
       done = __shfl_sync(0xffffffffu, done, 0);
       const int k1 = done + 1 < T ? done + 1 : T;  // query k = (v_k, omega_k, u_k): known once step k-1 is done
-      if (lane == 0) {
+      if (lane == 0) {  // the queries first: the variance blocks of these steps wait for them
         for (int kk = k; kk < k1; ++kk) {
           atq[kk * 4 + 0] = vv[kk];
           atq[kk * 4 + 1] = ww[kk];
@@ -1550,9 +1618,157 @@ __global__ void __launch_bounds__(TMEAN_THREADS + 32, 1) tighten_mean_kernel(con
         __threadfence();
         st_release_u32(a.tflags, (unsigned)k1);  // queries [0, k1) are out
       }
-      k = k1;
+      if (lane == 0)
+        for (int kk = k; kk < k1; ++kk) {  // arc_advance: theta = wrap(theta + omega dt)
+          t = t + ww[kk] * a.nom.dt;
+          if (!(t > -kPi && t <= kPi)) t = wrap_angle_fast(t);
+          th[kk + 1] = t;
+        }
       __syncwarp();
+      for (int kk = k + lane; kk < k1; kk += 32) {
+        const double m0[5] = {0.0, 0.0, th[kk], vv[kk], ww[kk]};
+        double s0, c0;
+        sincos(th[kk], &s0, &c0);
+        double x = 0.0, y = 0.0, t2 = th[kk];
+        arc_advance(x, y, t2, vv[kk], 0.0, ww[kk], a.nom.dt, s0, c0);
+        dx[kk] = x;
+        dy[kk] = y;
+        double J[25];
+        jacobian_nominal(m0, a.nom, J);
+        for (int i = 0; i < 25; ++i) atJ[kk * 25 + i] = J[i];
+        double* Jk = pJ + 9 * kk;  // J = [1 0 a b c; 0 1 d e f; 0 0 1 0 g; 0 0 0 h 0; 0 0 0 0 i]
+        Jk[0] = J[2], Jk[1] = J[3], Jk[2] = J[4], Jk[3] = J[7], Jk[4] = J[8], Jk[5] = J[9];
+        Jk[6] = J[14], Jk[7] = J[18], Jk[8] = J[24];
+      }
+      __syncwarp();
+      if (lane == 0) {
+        for (int kk = k; kk < k1; ++kk) {  // belief mean before step kk
+          atmu[kk * 5 + 0] = px;
+          atmu[kk * 5 + 1] = py;
+          atmu[kk * 5 + 2] = th[kk];
+          atmu[kk * 5 + 3] = vv[kk];
+          atmu[kk * 5 + 4] = ww[kk];
+          pxy[2 * kk] = px;
+          pxy[2 * kk + 1] = py;
+          px += dx[kk];
+          py += dy[kk];
+        }
+        __threadfence_block();
+        j_ready = k1;
+        mu_ready = k1;
+      }
+      __syncwarp();
+      __threadfence();  // every lane's Jacobians, lane 0's belief means
+      __syncwarp();
+      if (lane == 0) st_release_u32(a.tflags + 1, (unsigned)k1);  // J_k and mu_k out for k < k1
+      k = k1;
     }
+    for (unsigned it = 0; prog < T; ++it)  // the final belief mean needs the last step's (v, omega)
+      if (it > (1u << 28)) __trap();
+    if (lane == 0) {
+      pxy[2 * T] = px;
+      pxy[2 * T + 1] = py;
+      __threadfence_block();
+      mu_ready = T + 1;
+      atmu[T * 5 + 0] = px;
+      atmu[T * 5 + 1] = py;
+      atmu[T * 5 + 2] = th[T];
+      atmu[T * 5 + 3] = vv[T];
+      atmu[T * 5 + 4] = ww[T];
+    }
+    __syncwarp();
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) {
+      st_release_u32(a.tflags + 1, (unsigned)T + 1u);  // and the final belief mean
+      tl_stamp(8);
+    }
+  } else if (role == 1) {  // ---- cv stager: lanes watch a window of 32 steps' flags (the variance
+    // grid's last slice block of step k writes cv_k and raises flags[2 + k] to 0x40000000)
+    int base = 0;
+    unsigned it = 0;
+    while (base < T) {
+      const int kk = base + lane;
+      bool ready = kk >= T;
+      if (!ready && !cv_ready[kk] && ld_relaxed_u32(a.tflags + 2 + kk) == 0x40000000u) {
+        __threadfence();  // acquire for cv_k
+        pcv[2 * kk] = __ldcg(a.tcv + 2 * kk);
+        pcv[2 * kk + 1] = __ldcg(a.tcv + 2 * kk + 1);
+        __threadfence_block();
+        cv_ready[kk] = 1;
+        if (kk == 0) tl_stamp(15);
+        if (kk == T / 2) tl_stamp(19);
+        if (kk == T - 1) tl_stamp(23);
+      }
+      if (!ready) ready = cv_ready[kk] != 0;
+      const unsigned all = __ballot_sync(0xffffffffu, ready);
+      const int adv = all == 0xffffffffu ? 32 : __ffs(~all) - 1;  // leading run of ready steps
+      base += adv;
+      if (adv == 0) {
+        __nanosleep(64);
+        if (++it > (1u << 25)) {
+          printf("tighten_mean_kernel: variance wait timed out\n");
+          __trap();
+        }
+      }
+    }
+  } else if (role == 2) {  // ---- the covariance recursion (tighten_cov_kernel's), step by step
+    if (lane == 0) {
+      double s00 = 0, s01 = 0, s02 = 0, s03 = 0, s04 = 0, s11 = 0, s12 = 0, s13 = 0, s14 = 0;
+      double s22 = 0, s23 = 0, s24 = 0, s33 = 0, s34 = 0, s44 = 0;
+      for (int kk = 0; kk < T; ++kk) {
+        for (unsigned it = 0; j_ready <= kk || !cv_ready[kk]; ++it) {
+          __nanosleep(16);
+          if (it > (1u << 27)) __trap();
+        }
+        __threadfence_block();
+        if (kk == 0) tl_stamp(18);
+        if (kk == T / 4) tl_stamp(14);
+        if (kk == T / 2) tl_stamp(22);
+        if (kk == 3 * T / 4) tl_stamp(28);
+        if (kk == T - 1) tl_stamp(26);
+        const double* Jk = pJ + 9 * kk;
+        const double ja = Jk[0], jb = Jk[1], jc = Jk[2], jd = Jk[3], je = Jk[4], jf = Jk[5], jg = Jk[6], jh = Jk[7],
+                     ji = Jk[8];
+        const double cv0 = pcv[2 * kk], cv1 = pcv[2 * kk + 1];
+        const double p00 = fma(jc, s04, fma(jb, s03, fma(ja, s02, s00)));
+        const double p01 = fma(jc, s14, fma(jb, s13, fma(ja, s12, s01)));
+        const double p02 = fma(jc, s24, fma(jb, s23, fma(ja, s22, s02)));
+        const double p03 = fma(jc, s34, fma(jb, s33, fma(ja, s23, s03)));
+        const double p04 = fma(jc, s44, fma(jb, s34, fma(ja, s24, s04)));
+        const double p11 = fma(jf, s14, fma(je, s13, fma(jd, s12, s11)));
+        const double p12 = fma(jf, s24, fma(je, s23, fma(jd, s22, s12)));
+        const double p13 = fma(jf, s34, fma(je, s33, fma(jd, s23, s13)));
+        const double p14 = fma(jf, s44, fma(je, s34, fma(jd, s24, s14)));
+        const double p22 = fma(jg, s24, s22), p23 = fma(jg, s34, s23), p24 = fma(jg, s44, s24);
+        const double p33 = jh * s33, p34 = jh * s34, p44 = ji * s44;
+        s00 = fma(jc, p04, fma(jb, p03, fma(ja, p02, p00)));
+        s01 = fma(jf, p04, fma(je, p03, fma(jd, p02, p01)));
+        s02 = fma(jg, p04, p02);
+        s03 = jh * p03;
+        s04 = ji * p04;
+        s11 = fma(jf, p14, fma(je, p13, fma(jd, p12, p11)));
+        s12 = fma(jg, p14, p12);
+        s13 = jh * p13;
+        s14 = ji * p14;
+        s22 = fma(jg, p24, p22);
+        s23 = jh * p23;
+        s24 = ji * p24;
+        s33 = fma(jh, p33, cv0);
+        s34 = ji * p34;
+        s44 = fma(ji, p44, cv1);
+        double* Sk = pS + 25 * kk;
+        Sk[0] = s00, Sk[1] = s01, Sk[2] = s02, Sk[3] = s03, Sk[4] = s04;
+        Sk[5] = s01, Sk[6] = s11, Sk[7] = s12, Sk[8] = s13, Sk[9] = s14;
+        Sk[10] = s02, Sk[11] = s12, Sk[12] = s22, Sk[13] = s23, Sk[14] = s24;
+        Sk[15] = s03, Sk[16] = s13, Sk[17] = s23, Sk[18] = s33, Sk[19] = s34;
+        Sk[20] = s04, Sk[21] = s14, Sk[22] = s24, Sk[23] = s34, Sk[24] = s44;
+        __threadfence_block();
+        s_done = kk + 1;
+      }
+      tl_stamp(24);
+    }
+    __syncwarp();
   } else
   for (int k = 0; k < T; ++k) {
     TRC(0);
@@ -1680,10 +1896,58 @@ __global__ void __launch_bounds__(TMEAN_THREADS + 32, 1) tighten_mean_kernel(con
       }
     }
   }
+  if (threadIdx.x == 0) tl_stamp(6);
+  if (a.tflags && threadIdx.x < TMEAN_THREADS) {
+    // the chain warps, free now: step k's thresholds as soon as the recursion has Σ_k
+    // (tighten_lane_radius / tighten_obstacle_distance, uncertainty.cpp:90-116)
+    const TaskDev& tk = a.task[0];
+    for (int kk = w; kk < T; kk += TMEAN_THREADS / 32) {
+      for (unsigned it = 0; s_done <= kk || mu_ready <= kk + 1; ++it) {
+        __nanosleep(32);
+        if (it > (1u << 27)) __trap();
+      }
+      __threadfence_block();
+      const double* Sk = pS + 25 * kk;
+      if (lane < 25) a.horizon_cov[25 * kk + lane] = Sk[lane];
+      const double c00 = Sk[0], c01 = Sk[1], c10 = Sk[5], c11 = Sk[6];
+      if (lane == 0 && tk.kind != TASK_AVOIDANCE) {
+        const double half_tr = 0.5 * (c00 + c11);
+        const double disc = 0.25 * (c00 - c11) * (c00 - c11) + c01 * c10;
+        double lm = half_tr + sqrt(disc > 0.0 ? disc : 0.0);
+        lm = lm > 0.0 ? lm : 0.0;
+        const double r = tk.half_width - sqrt(a.chi2 * lm);
+        a.r_bar[kk] = r;
+        if (r <= 0.0) atomicOr(&infeasible, 1);
+      }
+      if (tk.kind != TASK_TRACKING)
+        for (int o = lane; o < tk.n_obs; o += 32) {
+          const double mx = pxy[2 * (kk + 1)], my = pxy[2 * (kk + 1) + 1];  // belief mean after step k
+          const double ddx = mx - tk.obs[o][0], ddy = my - tk.obs[o][1];
+          const double dist = sqrt(ddx * ddx + ddy * ddy);
+          double d, n0, n1;
+          if (dist < 1e-12) {
+            n0 = 1.0;
+            n1 = 0.0;
+            d = -tk.obs[o][2];
+          } else {
+            n0 = ddx / dist;
+            n1 = ddy / dist;
+            d = dist - tk.obs[o][2];
+          }
+          const double cn0 = c00 * n0 + c01 * n1, cn1 = c10 * n0 + c11 * n1;
+          double dv = n0 * cn0 + n1 * cn1;
+          dv = dv > 0.0 ? dv : 0.0;
+          const double dbar = d - a.z * sqrt(dv);
+          a.margins[(size_t)kk * tk.n_obs + o] = d - dbar;
+          if (dbar <= 0.0) atomicOr(&infeasible, 1);
+        }
+    }
+  }
   __syncthreads();
 #ifdef GPM_TMEAN_TRACE
   const long long tk2 = clock64();
 #endif
+  if (!a.tflags) {  // sequential tail (the publisher warp did this step by step when pipelined)
   if (threadIdx.x == 0) {  // heading recursion (arc_advance: theta = wrap(theta + omega dt))
     double t = th[0];
     for (int k0 = 0; k0 < T; k0 += 8) {  // omega read 8 steps ahead; wrap only off (-pi, pi]
@@ -1739,11 +2003,17 @@ __global__ void __launch_bounds__(TMEAN_THREADS + 32, 1) tighten_mean_kernel(con
         }
     }
   }
-  if (a.tflags) {  // Jacobians and belief means are out
-    __syncthreads();
+  }
+
+  if (a.tflags) {  // pipelined: every role is done (the barrier after the chain waited for them)
+    for (int i = threadIdx.x; i < T + 2; i += blockDim.x) a.tflags[i] = 0u;  // next tick's flags
     if (threadIdx.x == 0) {
-      __threadfence();
-      st_release_u32(a.tflags + 1, 1u);
+      a.infeasible[0] = infeasible;
+      if (a.done_host) {  // zero-copy: infeasibility, then the tick's sequence number
+        const double v = (double)infeasible;
+        publish_host(a.done_host, &v, 1, 1, a.x0[7]);
+      }
+      tl_stamp(12);
     }
   }
 #ifdef GPM_TMEAN_TRACE
@@ -1754,13 +2024,19 @@ __global__ void __launch_bounds__(TMEAN_THREADS + 32, 1) tighten_mean_kernel(con
 #endif
 }
 
-// grid (T, G*B, ceil(n / tight_rows(n, B))): partial ||L^{-1} k*||^2 over a slice of rows of
-// L^{-1}. One warp per row: a_j = sum_{i<=j} k_i L^{-1}[j][i] with the lanes striding
+// grid (ceil(n / tight_rows(n, B)), G*B, T): partial ||L^{-1} k*||^2 over a slice of rows of
+// L^{-1} (x = slice fastest, so the blocks are scheduled step by step, the order in which the
+// pipelined pass releases them). One warp per row: a_j = sum_{i<=j} k_i L^{-1}[j][i] with the lanes striding
 // the contiguous row (coalesced), then a_j^2 (gp.cpp:184-191).
 __global__ void __launch_bounds__(256) tighten_var_kernel(const TightenArgs a) {
+  if (threadIdx.x == 0) tl_stamp(11);
   if (a.tflags) {  // pipelined: start when the mean chain's queries are out (flag 0)
     pdl_trigger();
-    if (threadIdx.x == 0) spin_until_flag(a.tflags, (unsigned)blockIdx.x + 1u, "tighten_var_kernel");
+    if (threadIdx.x == 0) spin_until_flag(a.tflags, (unsigned)blockIdx.z + 1u, "tighten_var_kernel");
+    if (threadIdx.x == 0 && blockIdx.z == gridDim.z - 1) {
+      tl_stamp(21);
+      tl_stamp(20);
+    }
     __syncthreads();
   } else {
     pdl_wait();
@@ -1768,7 +2044,7 @@ __global__ void __launch_bounds__(256) tighten_var_kernel(const TightenArgs a) {
   }
   extern __shared__ __align__(16) double kst[];
   __shared__ double red[8];
-  const int k = blockIdx.x, g = blockIdx.y % a.model.G, rb = blockIdx.y / a.model.G, c = blockIdx.z;
+  const int k = blockIdx.z, g = blockIdx.y % a.model.G, rb = blockIdx.y / a.model.G, c = blockIdx.x;
   const int n = a.model.n;
   if (a.model_kind != MODEL_GP) return;
   const GroupDev& G = a.model.g[g];
@@ -1824,8 +2100,55 @@ __global__ void __launch_bounds__(256) tighten_var_kernel(const TightenArgs a) {
   if (threadIdx.x == 0) {
     double s = 0.0;
     for (int i = 0; i < 8; ++i) s += red[i];
-    a.tvar_part[(((size_t)rb * a.T + k) * a.model.G + g) * gridDim.z + c] = s;
+    a.tvar_part[(((size_t)rb * a.T + k) * a.model.G + g) * gridDim.x + c] = s;
+    if (a.tflags) {  // pipelined: the step's last slice block also combines the step (cv_k)
+      __threadfence();
+      const unsigned total = (unsigned)(gridDim.x * a.model.G);
+      if (atomicAdd(a.tflags + 2 + k, 1u) == total - 1u) {
+        __threadfence();
+        double vg[kMaxGroups];
+#pragma unroll
+        for (int gg = 0; gg < kMaxGroups; ++gg) vg[gg] = 0.0;
+        for (int gg = 0; gg < a.model.G; ++gg) {  // the slices summed in split order (tighten_cov_kernel)
+          const double* pv = a.tvar_part + ((size_t)k * a.model.G + gg) * gridDim.x;
+          double sum = 0.0;
+          for (int c0 = 0; c0 < (int)gridDim.x; c0 += 8) {
+            double x[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) x[u] = c0 + u < (int)gridDim.x ? __ldcg(pv + c0 + u) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (c0 + u < (int)gridDim.x) sum += x[u];
+          }
+          const double v = a.model.g[gg].sv - sum;
+          vg[gg] = v > 0.0 ? v : 0.0;
+        }
+        double c0 = 0.0, c1 = 0.0;  // ensemble_combine's Σ w² v per channel (gp.cpp:380-386)
+        for (int i = 0; i < a.R; ++i) {
+          const double wi = a.tw[i];
+          int g0 = 0, g1 = 0;
+          for (int gg = 0; gg < a.model.G; ++gg)
+            for (int o = 0; o < a.model.g[gg].n_out; ++o) {
+              if (a.model.g[gg].out_idx[o] == 2 * i) g0 = gg;
+              if (a.model.g[gg].out_idx[o] == 2 * i + 1) g1 = gg;
+            }
+          double v0 = vg[0], v1 = vg[0];
+#pragma unroll
+          for (int gg = 1; gg < kMaxGroups; ++gg) {
+            v0 = g0 == gg ? vg[gg] : v0;
+            v1 = g1 == gg ? vg[gg] : v1;
+          }
+          c0 += wi * wi * v0;
+          c1 += wi * wi * v1;
+        }
+        a.tcv[2 * k] = c0;
+        a.tcv[2 * k + 1] = c1;
+        __threadfence();
+        st_release_u32(a.tflags + 2 + k, 0x40000000u);  // cv_k is out
+      }
+    }
   }
+  if (threadIdx.x == 0) tl_stamp(10);
 }
 
 // 256 threads stage J / mu / the per-step correction variances, warp 0 runs the
@@ -1868,10 +2191,7 @@ __global__ void __launch_bounds__(256, 1) tighten_cov_kernel(const TightenArgs a
   // guarantees their visibility only after this grid's own griddepcontrol.wait, so the
   // staging follows it (it does not rely on the variance grid's wait-before-trigger order)
   pdl_wait();
-  if (a.tflags) {  // pipelined: the mean kernel's tail may still be running
-    if (l == 0) spin_until_flag(a.tflags + 1, 1u, "tighten_cov_kernel");
-    __syncthreads();
-  }
+  if (l == 0) tl_stamp(13);
   for (int i = l; i < 25 * T; i += nt) Js[i] = atJ[i];
   for (int i = l; i < 5 * (T + 1); i += nt) mus[i] = atmu[i];
   __syncthreads();
@@ -2020,10 +2340,6 @@ __global__ void __launch_bounds__(256, 1) tighten_cov_kernel(const TightenArgs a
     }
   __syncthreads();
   if (l == 0) {
-    if (a.tflags) {  // every reader of this tick's flags is done (the variance grid completed)
-      a.tflags[0] = 0u;
-      a.tflags[1] = 0u;
-    }
     a.infeasible[rb] = infeasible;
     if (a.done_host) {  // zero-copy: infeasibility, then the tick's sequence number
       const double v = (double)infeasible;
@@ -2033,6 +2349,7 @@ __global__ void __launch_bounds__(256, 1) tighten_cov_kernel(const TightenArgs a
 #ifdef GPM_TCOV_TRACE
   if (l == 0) printf("tcov: staging+cv %lld recursion %lld thresholds %lld\n", ct[1] - ct[0], ct[2] - ct[1], clock64() - ct[2]);
 #endif
+  if (threadIdx.x == 0) tl_stamp(12);
 }
 
 int tighten_splits(int n, int B) { return n > 0 ? (n + tight_rows(n, B) - 1) / tight_rows(n, B) : 1; }
@@ -2046,20 +2363,27 @@ cudaError_t launch_tighten(const TightenArgs& a, cudaStream_t st) {
     for (int g = 0; g < a.model.G; ++g) no = a.model.g[g].n_out > no ? a.model.g[g].n_out : no;
   void (*mk)(const TightenArgs) = no <= 2 ? tighten_mean_kernel<2> : no <= 4 ? tighten_mean_kernel<4>
                                   : no <= 6 ? tighten_mean_kernel<6> : tighten_mean_kernel<8>;
+  if (a.tflags)  // the pipelined roles' shared memory: J, cv, Σ, positions, cv-ready words
+    msm += sizeof(double) * (size_t)(9 * a.T + 2 * a.T + 25 * a.T + 2 * (a.T + 1)) + sizeof(int) * a.T;
   cudaFuncSetAttribute(mk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm);  // static + dynamic may exceed 48 KB
-  cudaError_t el = launch_pdl(mk, dim3(a.B), dim3(TMEAN_THREADS + (a.tflags ? 32 : 0)), msm, st, a);
+  cudaError_t el = launch_pdl(mk, dim3(a.B), dim3(TMEAN_THREADS + (a.tflags ? 96 : 0)), msm, st, a);
   if (el != cudaSuccess) return el;
   const int G = a.model_kind == MODEL_GP ? a.model.G : 1;
   const int ns = a.model_kind == MODEL_GP ? tighten_splits(a.model.n, a.B) : 1;
   const size_t smem = sizeof(double) * (size_t)(a.model.n > 0 ? a.model.n : 1);
   cudaFuncSetAttribute(tighten_var_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (a.model_kind == MODEL_GP) {
-    el = launch_pdl(tighten_var_kernel, dim3(a.T, G * a.B, ns), dim3(256), smem, st, a);
+    el = launch_pdl(tighten_var_kernel, dim3(ns, G * a.B, a.T), dim3(256), smem, st, a);
     if (el != cudaSuccess) return el;
   }
-  const size_t csmem = sizeof(double) * (size_t)(25 * a.T + 2 * a.T + 5 * (a.T + 1) + 25 * a.T);
-  cudaFuncSetAttribute(tighten_cov_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem);
-  el = launch_pdl(tighten_cov_kernel, dim3(a.B), dim3(256), csmem, st, a, ns);
+  if (a.tflags) {  // the mean kernel's extra warps did the covariance pass
+    count_launch(2);
+    return cudaGetLastError();
+  } else {
+    const size_t csmem = sizeof(double) * (size_t)(25 * a.T + 2 * a.T + 5 * (a.T + 1) + 25 * a.T);
+    cudaFuncSetAttribute(tighten_cov_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem);
+    el = launch_pdl(tighten_cov_kernel, dim3(a.B), dim3(256), csmem, st, a, ns);
+  }
   if (el != cudaSuccess) return el;
   count_launch(3);
   return cudaGetLastError();

@@ -1088,6 +1088,7 @@ __device__ __forceinline__ uint32_t half2_bits(__half2 h) {
 
 template <int CPS>  // 16-point chunks per ring stage (one barrier round trip, one commit per stage)
 __global__ void __launch_bounds__(tc::F16_THREADS, 1) variance_f16_kernel(const VarianceArgs a, int dbg, int S) {
+  if (threadIdx.x == 0) tl_stamp(3);
   using namespace tc;
   pdl_trigger();
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -1383,6 +1384,7 @@ __global__ void __launch_bounds__(tc::F16_THREADS, 1) variance_f16_kernel(const 
   if (threadIdx.x == 0) trace_at(63, dbg);
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512) : "memory");
+  if (threadIdx.x == 0) tl_stamp(2);
 }
 
 // ---------------------------------------------------------------------------
@@ -1507,6 +1509,7 @@ __device__ __forceinline__ double drain_ssq(uint32_t trow, int w) {  // Σ D^2 o
 template <int CPS>  // 16-point chunks per ring stage
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::P2_THREADS, 1)
     variance_f16x2_kernel(const VarianceArgs a, int S, int dbg) {
+  if (threadIdx.x == 0) tl_stamp(3);
   using namespace tc;
   pdl_trigger();
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -1779,6 +1782,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::P2_THREADS, 1)
   if (threadIdx.x == 0) trace_at(63, dbg);
   if (warp == 2)
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512) : "memory");
+  if (threadIdx.x == 0) tl_stamp(2);
 }
 
 // ---------------------------------------------------------------------------
@@ -2123,6 +2127,17 @@ void tc_trace_read(double* out) {
   unsigned long long h[64];
   cudaMemcpyFromSymbol(h, tc::g_trace, sizeof h);
   for (int i = 0; i < 64; ++i) out[i] = (double)h[i];
+}
+
+void timeline_read_unit(unsigned long long* h) {
+#ifdef GPM_TIMELINE
+  cudaMemcpyFromSymbol(h, g_tl, 32 * sizeof(unsigned long long));
+  unsigned long long z[32];
+  for (int i = 0; i < 32; ++i) z[i] = (i & 1) ? ~0ull : 0ull;
+  cudaMemcpyToSymbol(g_tl, z, sizeof z);
+#else
+  for (int i = 0; i < 32; ++i) h[i] = 0ull;
+#endif
 }
 
 void tc_profile_read(double* out) {
