@@ -1615,8 +1615,7 @@ __global__ void __launch_bounds__(TMEAN_THREADS + 96, 1) tighten_mean_kernel(con
           atq[kk * 4 + 2] = nom[2 * kk];
           atq[kk * 4 + 3] = nom[2 * kk + 1];
         }
-        __threadfence();
-        st_release_u32(a.tflags, (unsigned)k1);  // queries [0, k1) are out
+        st_release_u32(a.tflags, (unsigned)k1);  // queries [0, k1) are out (release: lane 0's stores first)
       }
       if (lane == 0)
         for (int kk = k; kk < k1; ++kk) {  // arc_advance: theta = wrap(theta + omega dt)
@@ -1657,10 +1656,6 @@ __global__ void __launch_bounds__(TMEAN_THREADS + 96, 1) tighten_mean_kernel(con
         j_ready = k1;
         mu_ready = k1;
       }
-      __syncwarp();
-      __threadfence();  // every lane's Jacobians, lane 0's belief means
-      __syncwarp();
-      if (lane == 0) st_release_u32(a.tflags + 1, (unsigned)k1);  // J_k and mu_k out for k < k1
       k = k1;
     }
     for (unsigned it = 0; prog < T; ++it)  // the final belief mean needs the last step's (v, omega)
@@ -1676,13 +1671,7 @@ __global__ void __launch_bounds__(TMEAN_THREADS + 96, 1) tighten_mean_kernel(con
       atmu[T * 5 + 3] = vv[T];
       atmu[T * 5 + 4] = ww[T];
     }
-    __syncwarp();
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) {
-      st_release_u32(a.tflags + 1, (unsigned)T + 1u);  // and the final belief mean
-      tl_stamp(8);
-    }
+    if (lane == 0) tl_stamp(8);
   } else if (role == 1) {  // ---- cv stager: lanes watch a window of 32 steps' flags (the variance
     // grid's last slice block of step k writes cv_k and raises flags[2 + k] to 0x40000000)
     int base = 0;
@@ -1723,7 +1712,6 @@ __global__ void __launch_bounds__(TMEAN_THREADS + 96, 1) tighten_mean_kernel(con
         }
         __threadfence_block();
         if (kk == 0) tl_stamp(18);
-        if (kk == T / 4) tl_stamp(14);
         if (kk == T / 2) tl_stamp(22);
         if (kk == 3 * T / 4) tl_stamp(28);
         if (kk == T - 1) tl_stamp(26);
@@ -2037,6 +2025,7 @@ __global__ void __launch_bounds__(256) tighten_var_kernel(const TightenArgs a) {
       tl_stamp(21);
       tl_stamp(20);
     }
+    if (threadIdx.x == 0 && blockIdx.z == 0) tl_stamp(29);
     __syncthreads();
   } else {
     pdl_wait();
@@ -2097,55 +2086,63 @@ __global__ void __launch_bounds__(256) tighten_var_kernel(const TightenArgs a) {
   }
   if (lane == 0) red[w] = ssq;
   __syncthreads();
+  __shared__ int s_last;
   if (threadIdx.x == 0) {
     double s = 0.0;
     for (int i = 0; i < 8; ++i) s += red[i];
     a.tvar_part[(((size_t)rb * a.T + k) * a.model.G + g) * gridDim.x + c] = s;
+    if (k == 0) {
+      tl_stamp(31);
+      tl_stamp(14);
+    }
+    s_last = 0;
     if (a.tflags) {  // pipelined: the step's last slice block also combines the step (cv_k)
-      __threadfence();
-      const unsigned total = (unsigned)(gridDim.x * a.model.G);
-      if (atomicAdd(a.tflags + 2 + k, 1u) == total - 1u) {
-        __threadfence();
-        double vg[kMaxGroups];
+      unsigned prev;  // acq_rel: releases this slice's partial, acquires every earlier slice's
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(a.tflags + 2 + k) : "memory");
+      s_last = prev == (unsigned)(gridDim.x * a.model.G) - 1u;
+    }
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x < 32) {  // warp 0: every slice in flight at once, summed in split order
+    if (k == 0 && lane == 0) tl_stamp(27);
+    __syncwarp();
+    double vg[kMaxGroups];
 #pragma unroll
-        for (int gg = 0; gg < kMaxGroups; ++gg) vg[gg] = 0.0;
-        for (int gg = 0; gg < a.model.G; ++gg) {  // the slices summed in split order (tighten_cov_kernel)
-          const double* pv = a.tvar_part + ((size_t)k * a.model.G + gg) * gridDim.x;
-          double sum = 0.0;
-          for (int c0 = 0; c0 < (int)gridDim.x; c0 += 8) {
-            double x[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) x[u] = c0 + u < (int)gridDim.x ? __ldcg(pv + c0 + u) : 0.0;
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-              if (c0 + u < (int)gridDim.x) sum += x[u];
-          }
-          const double v = a.model.g[gg].sv - sum;
-          vg[gg] = v > 0.0 ? v : 0.0;
-        }
-        double c0 = 0.0, c1 = 0.0;  // ensemble_combine's Σ w² v per channel (gp.cpp:380-386)
-        for (int i = 0; i < a.R; ++i) {
-          const double wi = a.tw[i];
-          int g0 = 0, g1 = 0;
-          for (int gg = 0; gg < a.model.G; ++gg)
-            for (int o = 0; o < a.model.g[gg].n_out; ++o) {
-              if (a.model.g[gg].out_idx[o] == 2 * i) g0 = gg;
-              if (a.model.g[gg].out_idx[o] == 2 * i + 1) g1 = gg;
-            }
-          double v0 = vg[0], v1 = vg[0];
-#pragma unroll
-          for (int gg = 1; gg < kMaxGroups; ++gg) {
-            v0 = g0 == gg ? vg[gg] : v0;
-            v1 = g1 == gg ? vg[gg] : v1;
-          }
-          c0 += wi * wi * v0;
-          c1 += wi * wi * v1;
-        }
-        a.tcv[2 * k] = c0;
-        a.tcv[2 * k + 1] = c1;
-        __threadfence();
-        st_release_u32(a.tflags + 2 + k, 0x40000000u);  // cv_k is out
+    for (int gg = 0; gg < kMaxGroups; ++gg) vg[gg] = 0.0;
+    for (int gg = 0; gg < a.model.G; ++gg) {
+      const double* pv = a.tvar_part + ((size_t)k * a.model.G + gg) * gridDim.x;
+      double sum = 0.0;
+      for (int c0 = 0; c0 < (int)gridDim.x; c0 += 32) {
+        const double x = c0 + lane < (int)gridDim.x ? __ldcg(pv + c0 + lane) : 0.0;
+        const int cn = (int)gridDim.x - c0 < 32 ? (int)gridDim.x - c0 : 32;
+        for (int cc = 0; cc < cn; ++cc) sum += __shfl_sync(0xffffffffu, x, cc);
       }
+      const double v = a.model.g[gg].sv - sum;
+      vg[gg] = v > 0.0 ? v : 0.0;
+    }
+    if (lane == 0) {
+      double c0 = 0.0, c1 = 0.0;  // ensemble_combine's Σ w² v per channel (gp.cpp:380-386)
+      for (int i = 0; i < a.R; ++i) {
+        const double wi = a.tw[i];
+        int g0 = 0, g1 = 0;
+        for (int gg = 0; gg < a.model.G; ++gg)
+          for (int o = 0; o < a.model.g[gg].n_out; ++o) {
+            if (a.model.g[gg].out_idx[o] == 2 * i) g0 = gg;
+            if (a.model.g[gg].out_idx[o] == 2 * i + 1) g1 = gg;
+          }
+        double v0 = vg[0], v1 = vg[0];
+#pragma unroll
+        for (int gg = 1; gg < kMaxGroups; ++gg) {
+          v0 = g0 == gg ? vg[gg] : v0;
+          v1 = g1 == gg ? vg[gg] : v1;
+        }
+        c0 += wi * wi * v0;
+        c1 += wi * wi * v1;
+      }
+      a.tcv[2 * k] = c0;
+      a.tcv[2 * k + 1] = c1;
+      st_release_u32(a.tflags + 2 + k, 0x40000000u);  // cv_k is out (release: the stores above first)
+      if (k == 0) tl_stamp(25);
     }
   }
   if (threadIdx.x == 0) tl_stamp(10);
