@@ -1451,6 +1451,9 @@ GPM_HD int tight_rows(int n, int B) { return (B == 1 && n <= 1024) ? GPM_TIGHT_R
 #define GPM_TMEAN_THREADS 128
 #endif
 constexpr int TMEAN_THREADS = GPM_TMEAN_THREADS;
+#ifndef GPM_PUB_SLEEP
+#define GPM_PUB_SLEEP 32
+#endif
 template <int NO>
 __global__ void __launch_bounds__(TMEAN_THREADS + 96, 1) tighten_mean_kernel(const TightenArgs a) {
   if (!a.tflags) pdl_trigger();  // pipelined: the variance grid is released after the reduction
@@ -1604,8 +1607,10 @@ __global__ void __launch_bounds__(TMEAN_THREADS + 96, 1) tighten_mean_kernel(con
     double t = th[0];                 // lane 0: heading recursion
     for (int k = 0; k < T;) {
       int done;
-      for (unsigned it = 0; (done = prog) < k; ++it)
-        if (it > (1u << 28)) __trap();
+      for (unsigned it = 0; (done = prog) < k; ++it) {  // sleep between polls: the chain shares this scheduler
+        __nanosleep(GPM_PUB_SLEEP);
+        if (it > (1u << 27)) __trap();
+      }
       done = __shfl_sync(0xffffffffu, done, 0);
       const int k1 = done + 1 < T ? done + 1 : T;  // query k = (v_k, omega_k, u_k): known once step k-1 is done
       if (lane == 0) {  // the queries first: the variance blocks of these steps wait for them
