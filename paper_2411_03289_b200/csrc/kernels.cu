@@ -1455,7 +1455,7 @@ constexpr int TMEAN_THREADS = GPM_TMEAN_THREADS;
 #define GPM_PUB_SLEEP 32
 #endif
 template <int NO>
-__global__ void __launch_bounds__(TMEAN_THREADS + 96, 1) tighten_mean_kernel(const TightenArgs a) {
+__global__ void __launch_bounds__(TMEAN_THREADS + 32, 1) tighten_mean_kernel(const TightenArgs a) {
   if (!a.tflags) pdl_trigger();  // pipelined: the variance grid is released after the reduction
   const int rb = blockIdx.x;  // robot
 #ifdef GPM_TMEAN_TRACE
@@ -1536,31 +1536,11 @@ __global__ void __launch_bounds__(TMEAN_THREADS + 96, 1) tighten_mean_kernel(con
   // pipelined (a.tflags): warp TMEAN_THREADS / 32 publishes each step's query (and raises the
   // query counter, flag 0) while the chain warps run on: its fences stay off the serial path
   __shared__ volatile int prog;  // chain steps done (thread 0, after vv / ww)
-  // pipelined roles of the three warps after the chain's: 0 publisher, 1 cv stager, 2 covariance
-  // recursion (tighten_cov_kernel's, step by step behind the chain); the thresholds follow the
-  // final barrier on every thread
-  const int role = a.tflags != nullptr && threadIdx.x >= TMEAN_THREADS ? (int)(threadIdx.x - TMEAN_THREADS) >> 5 : -1;
-  const bool pub = role == 0;
-  __shared__ volatile int j_ready, mu_ready, s_done;
-  __shared__ int infeasible, gof[2 * kMaxTerrains];
-  double* const pJ = pts + (size_t)7 * a.model.ns * (a.model.G > 0 ? a.model.G : 1);  // [T][9] sparse J
-  double* const pcv = pJ + 9 * T;         // [T][2] combined correction variances
-  double* const pS = pcv + 2 * T;         // [T][25] propagated covariances
-  double* const pxy = pS + 25 * T;        // [T+1][2] belief-mean positions
-  volatile int* const cv_ready = reinterpret_cast<volatile int*>(pxy + 2 * (T + 1));  // [T]
-  if (threadIdx.x == 0) {
-    prog = 0;
-    j_ready = 0;
-    mu_ready = 0;
-    s_done = 0;
-    infeasible = 0;
-  }
-  if (a.tflags) {
-    for (int i = threadIdx.x; i < T; i += blockDim.x) cv_ready[i] = 0;
-    if (threadIdx.x == 0)
-      for (int g = 0; g < a.model.G; ++g)
-        for (int o = 0; o < a.model.g[g].n_out; ++o) gof[a.model.g[g].out_idx[o]] = g;
-  }
+  // pipelined (a.tflags): the warp after the chain's publishes, per batch of finished steps, the
+  // queries (flag 0), then the Jacobians and belief means (flag 1) -- tighten_cov_pipe_kernel
+  // and the variance grid, launched after this kernel, consume them step by step
+  const bool pub = a.tflags != nullptr && threadIdx.x >= TMEAN_THREADS;
+  if (threadIdx.x == 0) prog = 0;
   const int ns = a.model.ns;
   const int G = a.model_kind == MODEL_GP ? a.model.G : 0;
   if (threadIdx.x < 4 * G) gil[threadIdx.x >> 2][threadIdx.x & 3] = 1.0 / a.model.g[threadIdx.x >> 2].ls[threadIdx.x & 3];
@@ -1640,9 +1620,6 @@ __global__ void __launch_bounds__(TMEAN_THREADS + 96, 1) tighten_mean_kernel(con
         double J[25];
         jacobian_nominal(m0, a.nom, J);
         for (int i = 0; i < 25; ++i) atJ[kk * 25 + i] = J[i];
-        double* Jk = pJ + 9 * kk;  // J = [1 0 a b c; 0 1 d e f; 0 0 1 0 g; 0 0 0 h 0; 0 0 0 0 i]
-        Jk[0] = J[2], Jk[1] = J[3], Jk[2] = J[4], Jk[3] = J[7], Jk[4] = J[8], Jk[5] = J[9];
-        Jk[6] = J[14], Jk[7] = J[18], Jk[8] = J[24];
       }
       __syncwarp();
       if (lane == 0) {
@@ -1652,116 +1629,27 @@ __global__ void __launch_bounds__(TMEAN_THREADS + 96, 1) tighten_mean_kernel(con
           atmu[kk * 5 + 2] = th[kk];
           atmu[kk * 5 + 3] = vv[kk];
           atmu[kk * 5 + 4] = ww[kk];
-          pxy[2 * kk] = px;
-          pxy[2 * kk + 1] = py;
           px += dx[kk];
           py += dy[kk];
         }
-        __threadfence_block();
-        j_ready = k1;
-        mu_ready = k1;
       }
+      __syncwarp();  // every lane's Jacobians before lane 0's release
+      if (lane == 0) st_release_u32(a.tflags + 1, (unsigned)k1);  // J_k and mu_k out for k < k1
       k = k1;
     }
     for (unsigned it = 0; prog < T; ++it)  // the final belief mean needs the last step's (v, omega)
       if (it > (1u << 28)) __trap();
     if (lane == 0) {
-      pxy[2 * T] = px;
-      pxy[2 * T + 1] = py;
-      __threadfence_block();
-      mu_ready = T + 1;
       atmu[T * 5 + 0] = px;
       atmu[T * 5 + 1] = py;
       atmu[T * 5 + 2] = th[T];
       atmu[T * 5 + 3] = vv[T];
       atmu[T * 5 + 4] = ww[T];
     }
-    if (lane == 0) tl_stamp(8);
-  } else if (role == 1) {  // ---- cv stager: lanes watch a window of 32 steps' flags (the variance
-    // grid's last slice block of step k writes cv_k and raises flags[2 + k] to 0x40000000)
-    int base = 0;
-    unsigned it = 0;
-    while (base < T) {
-      const int kk = base + lane;
-      bool ready = kk >= T;
-      if (!ready && !cv_ready[kk] && ld_relaxed_u32(a.tflags + 2 + kk) == 0x40000000u) {
-        __threadfence();  // acquire for cv_k
-        pcv[2 * kk] = __ldcg(a.tcv + 2 * kk);
-        pcv[2 * kk + 1] = __ldcg(a.tcv + 2 * kk + 1);
-        __threadfence_block();
-        cv_ready[kk] = 1;
-        if (kk == 0) tl_stamp(15);
-        if (kk == T / 2) tl_stamp(19);
-        if (kk == T - 1) tl_stamp(23);
-      }
-      if (!ready) ready = cv_ready[kk] != 0;
-      const unsigned all = __ballot_sync(0xffffffffu, ready);
-      const int adv = all == 0xffffffffu ? 32 : __ffs(~all) - 1;  // leading run of ready steps
-      base += adv;
-      if (adv == 0) {
-        __nanosleep(64);
-        if (++it > (1u << 25)) {
-          printf("tighten_mean_kernel: variance wait timed out\n");
-          __trap();
-        }
-      }
-    }
-  } else if (role == 2) {  // ---- the covariance recursion (tighten_cov_kernel's), step by step
     if (lane == 0) {
-      double s00 = 0, s01 = 0, s02 = 0, s03 = 0, s04 = 0, s11 = 0, s12 = 0, s13 = 0, s14 = 0;
-      double s22 = 0, s23 = 0, s24 = 0, s33 = 0, s34 = 0, s44 = 0;
-      for (int kk = 0; kk < T; ++kk) {
-        for (unsigned it = 0; j_ready <= kk || !cv_ready[kk]; ++it) {
-          __nanosleep(16);
-          if (it > (1u << 27)) __trap();
-        }
-        __threadfence_block();
-        if (kk == 0) tl_stamp(18);
-        if (kk == T / 2) tl_stamp(22);
-        if (kk == 3 * T / 4) tl_stamp(28);
-        if (kk == T - 1) tl_stamp(26);
-        const double* Jk = pJ + 9 * kk;
-        const double ja = Jk[0], jb = Jk[1], jc = Jk[2], jd = Jk[3], je = Jk[4], jf = Jk[5], jg = Jk[6], jh = Jk[7],
-                     ji = Jk[8];
-        const double cv0 = pcv[2 * kk], cv1 = pcv[2 * kk + 1];
-        const double p00 = fma(jc, s04, fma(jb, s03, fma(ja, s02, s00)));
-        const double p01 = fma(jc, s14, fma(jb, s13, fma(ja, s12, s01)));
-        const double p02 = fma(jc, s24, fma(jb, s23, fma(ja, s22, s02)));
-        const double p03 = fma(jc, s34, fma(jb, s33, fma(ja, s23, s03)));
-        const double p04 = fma(jc, s44, fma(jb, s34, fma(ja, s24, s04)));
-        const double p11 = fma(jf, s14, fma(je, s13, fma(jd, s12, s11)));
-        const double p12 = fma(jf, s24, fma(je, s23, fma(jd, s22, s12)));
-        const double p13 = fma(jf, s34, fma(je, s33, fma(jd, s23, s13)));
-        const double p14 = fma(jf, s44, fma(je, s34, fma(jd, s24, s14)));
-        const double p22 = fma(jg, s24, s22), p23 = fma(jg, s34, s23), p24 = fma(jg, s44, s24);
-        const double p33 = jh * s33, p34 = jh * s34, p44 = ji * s44;
-        s00 = fma(jc, p04, fma(jb, p03, fma(ja, p02, p00)));
-        s01 = fma(jf, p04, fma(je, p03, fma(jd, p02, p01)));
-        s02 = fma(jg, p04, p02);
-        s03 = jh * p03;
-        s04 = ji * p04;
-        s11 = fma(jf, p14, fma(je, p13, fma(jd, p12, p11)));
-        s12 = fma(jg, p14, p12);
-        s13 = jh * p13;
-        s14 = ji * p14;
-        s22 = fma(jg, p24, p22);
-        s23 = jh * p23;
-        s24 = ji * p24;
-        s33 = fma(jh, p33, cv0);
-        s34 = ji * p34;
-        s44 = fma(ji, p44, cv1);
-        double* Sk = pS + 25 * kk;
-        Sk[0] = s00, Sk[1] = s01, Sk[2] = s02, Sk[3] = s03, Sk[4] = s04;
-        Sk[5] = s01, Sk[6] = s11, Sk[7] = s12, Sk[8] = s13, Sk[9] = s14;
-        Sk[10] = s02, Sk[11] = s12, Sk[12] = s22, Sk[13] = s23, Sk[14] = s24;
-        Sk[15] = s03, Sk[16] = s13, Sk[17] = s23, Sk[18] = s33, Sk[19] = s34;
-        Sk[20] = s04, Sk[21] = s14, Sk[22] = s24, Sk[23] = s34, Sk[24] = s44;
-        __threadfence_block();
-        s_done = kk + 1;
-      }
-      tl_stamp(24);
+      st_release_u32(a.tflags + 1, (unsigned)T + 1u);  // and the final belief mean
+      tl_stamp(8);
     }
-    __syncwarp();
   } else
   for (int k = 0; k < T; ++k) {
     TRC(0);
@@ -1890,52 +1778,6 @@ __global__ void __launch_bounds__(TMEAN_THREADS + 96, 1) tighten_mean_kernel(con
     }
   }
   if (threadIdx.x == 0) tl_stamp(6);
-  if (a.tflags && threadIdx.x < TMEAN_THREADS) {
-    // the chain warps, free now: step k's thresholds as soon as the recursion has Σ_k
-    // (tighten_lane_radius / tighten_obstacle_distance, uncertainty.cpp:90-116)
-    const TaskDev& tk = a.task[0];
-    for (int kk = w; kk < T; kk += TMEAN_THREADS / 32) {
-      for (unsigned it = 0; s_done <= kk || mu_ready <= kk + 1; ++it) {
-        __nanosleep(32);
-        if (it > (1u << 27)) __trap();
-      }
-      __threadfence_block();
-      const double* Sk = pS + 25 * kk;
-      if (lane < 25) a.horizon_cov[25 * kk + lane] = Sk[lane];
-      const double c00 = Sk[0], c01 = Sk[1], c10 = Sk[5], c11 = Sk[6];
-      if (lane == 0 && tk.kind != TASK_AVOIDANCE) {
-        const double half_tr = 0.5 * (c00 + c11);
-        const double disc = 0.25 * (c00 - c11) * (c00 - c11) + c01 * c10;
-        double lm = half_tr + sqrt(disc > 0.0 ? disc : 0.0);
-        lm = lm > 0.0 ? lm : 0.0;
-        const double r = tk.half_width - sqrt(a.chi2 * lm);
-        a.r_bar[kk] = r;
-        if (r <= 0.0) atomicOr(&infeasible, 1);
-      }
-      if (tk.kind != TASK_TRACKING)
-        for (int o = lane; o < tk.n_obs; o += 32) {
-          const double mx = pxy[2 * (kk + 1)], my = pxy[2 * (kk + 1) + 1];  // belief mean after step k
-          const double ddx = mx - tk.obs[o][0], ddy = my - tk.obs[o][1];
-          const double dist = sqrt(ddx * ddx + ddy * ddy);
-          double d, n0, n1;
-          if (dist < 1e-12) {
-            n0 = 1.0;
-            n1 = 0.0;
-            d = -tk.obs[o][2];
-          } else {
-            n0 = ddx / dist;
-            n1 = ddy / dist;
-            d = dist - tk.obs[o][2];
-          }
-          const double cn0 = c00 * n0 + c01 * n1, cn1 = c10 * n0 + c11 * n1;
-          double dv = n0 * cn0 + n1 * cn1;
-          dv = dv > 0.0 ? dv : 0.0;
-          const double dbar = d - a.z * sqrt(dv);
-          a.margins[(size_t)kk * tk.n_obs + o] = d - dbar;
-          if (dbar <= 0.0) atomicOr(&infeasible, 1);
-        }
-    }
-  }
   __syncthreads();
 #ifdef GPM_TMEAN_TRACE
   const long long tk2 = clock64();
@@ -1998,17 +1840,6 @@ __global__ void __launch_bounds__(TMEAN_THREADS + 96, 1) tighten_mean_kernel(con
   }
   }
 
-  if (a.tflags) {  // pipelined: every role is done (the barrier after the chain waited for them)
-    for (int i = threadIdx.x; i < T + 2; i += blockDim.x) a.tflags[i] = 0u;  // next tick's flags
-    if (threadIdx.x == 0) {
-      a.infeasible[0] = infeasible;
-      if (a.done_host) {  // zero-copy: infeasibility, then the tick's sequence number
-        const double v = (double)infeasible;
-        publish_host(a.done_host, &v, 1, 1, a.x0[7]);
-      }
-      tl_stamp(12);
-    }
-  }
 #ifdef GPM_TMEAN_TRACE
   if (threadIdx.x == 0) {
     const long long tk3 = clock64();
@@ -2356,6 +2187,197 @@ __global__ void __launch_bounds__(256, 1) tighten_cov_kernel(const TightenArgs a
 
 int tighten_splits(int n, int B) { return n > 0 ? (n + tight_rows(n, B) - 1) / tight_rows(n, B) : 1; }
 
+// Pipelined single-robot covariance pass (a.tflags), launched after the variance grid: it only
+// waits on work launched before it (serialisation-safe: under a profiler that runs kernels one
+// at a time every flag is already up). Warp 1 stages J_k / mu_k as the mean kernel's publisher
+// raises flag 1, warp 2 collects cv_k as the variance grid raises the per-step flags, warp 0
+// lane 0 runs the recursion (tighten_cov_kernel's arithmetic) as both arrive, warps 3-7
+// evaluate step k's thresholds as soon as Σ_k is known; at the end every flag is lowered.
+__global__ void __launch_bounds__(256, 1) tighten_cov_pipe_kernel(const TightenArgs a) {
+  pdl_trigger();
+  const int T = a.T, l = threadIdx.x, lane = l & 31, w = l >> 5;
+  extern __shared__ __align__(16) double psm[];  // [T][9] J, [T][2] cv, [T][25] Σ, [T+1][2] xy, int[T]
+  double* const pJ = psm;
+  double* const pcv = pJ + 9 * T;
+  double* const pS = pcv + 2 * T;
+  double* const pxy = pS + 25 * T;
+  volatile int* const cv_ready = reinterpret_cast<volatile int*>(pxy + 2 * (T + 1));
+  __shared__ volatile int j_ready, mu_ready, s_done;
+  __shared__ int infeasible;
+  if (l == 0) {
+    j_ready = 0;
+    mu_ready = 0;
+    s_done = 0;
+    infeasible = 0;
+  }
+  for (int i = l; i < T; i += blockDim.x) cv_ready[i] = 0;
+  __syncthreads();
+  if (w == 1) {  // ---- J / belief-mean stager
+    int staged = 0;
+    unsigned it = 0;
+    while (staged < T + 1) {
+      unsigned avail = ld_relaxed_u32(a.tflags + 1);
+      avail = __shfl_sync(0xffffffffu, avail, 0);
+      if ((int)avail <= staged) {
+        __nanosleep(64);
+        if (++it > (1u << 25)) {
+          printf("tighten_cov_pipe_kernel: Jacobian wait timed out\n");
+          __trap();
+        }
+        continue;
+      }
+      __threadfence();  // acquire: the rows published before the counter
+      const int j0 = staged < T ? staged : T, jt = (int)avail < T ? (int)avail : T;
+      for (int i = lane; i < 9 * (jt - j0); i += 32) {  // J = [1 0 a b c; 0 1 d e f; 0 0 1 0 g; 0 0 0 h 0; 0 0 0 0 i]
+        const int kk = j0 + i / 9, e = i % 9;
+        const int src = e < 3 ? 2 + e : e < 6 ? 4 + e : e == 6 ? 14 : e == 7 ? 18 : 24;
+        pJ[kk * 9 + e] = __ldcg(a.tJ + kk * 25 + src);
+      }
+      for (int i = lane; i < 2 * ((int)avail - staged); i += 32) {
+        const int kk = staged + i / 2;
+        pxy[2 * kk + (i & 1)] = __ldcg(a.tmu + kk * 5 + (i & 1));
+      }
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        j_ready = jt;
+        mu_ready = (int)avail;
+      }
+      staged = (int)avail;
+    }
+  } else if (w == 2) {  // ---- cv stager: lanes watch a window of 32 steps' flags
+    int base = 0;
+    unsigned it = 0;
+    while (base < T) {
+      const int kk = base + lane;
+      bool ready = kk >= T;
+      if (!ready && !cv_ready[kk] && ld_relaxed_u32(a.tflags + 2 + kk) == 0x40000000u) {
+        __threadfence();  // acquire for cv_k
+        pcv[2 * kk] = __ldcg(a.tcv + 2 * kk);
+        pcv[2 * kk + 1] = __ldcg(a.tcv + 2 * kk + 1);
+        __threadfence_block();
+        cv_ready[kk] = 1;
+      }
+      if (!ready) ready = cv_ready[kk] != 0;
+      const unsigned all = __ballot_sync(0xffffffffu, ready);
+      const int adv = all == 0xffffffffu ? 32 : __ffs(~all) - 1;  // leading run of ready steps
+      base += adv;
+      if (adv == 0) {
+        __nanosleep(64);
+        if (++it > (1u << 25)) {
+          printf("tighten_cov_pipe_kernel: variance wait timed out\n");
+          __trap();
+        }
+      }
+    }
+  } else if (w == 0) {  // ---- the covariance recursion (tighten_cov_kernel's), step by step
+    if (lane == 0) {
+      double s00 = 0, s01 = 0, s02 = 0, s03 = 0, s04 = 0, s11 = 0, s12 = 0, s13 = 0, s14 = 0;
+      double s22 = 0, s23 = 0, s24 = 0, s33 = 0, s34 = 0, s44 = 0;
+      for (int kk = 0; kk < T; ++kk) {
+        for (unsigned it = 0; j_ready <= kk || !cv_ready[kk]; ++it) {
+          __nanosleep(16);
+          if (it > (1u << 27)) __trap();
+        }
+        __threadfence_block();
+        const double* Jk = pJ + 9 * kk;
+        const double ja = Jk[0], jb = Jk[1], jc = Jk[2], jd = Jk[3], je = Jk[4], jf = Jk[5], jg = Jk[6], jh = Jk[7],
+                     ji = Jk[8];
+        const double cv0 = pcv[2 * kk], cv1 = pcv[2 * kk + 1];
+        const double p00 = fma(jc, s04, fma(jb, s03, fma(ja, s02, s00)));
+        const double p01 = fma(jc, s14, fma(jb, s13, fma(ja, s12, s01)));
+        const double p02 = fma(jc, s24, fma(jb, s23, fma(ja, s22, s02)));
+        const double p03 = fma(jc, s34, fma(jb, s33, fma(ja, s23, s03)));
+        const double p04 = fma(jc, s44, fma(jb, s34, fma(ja, s24, s04)));
+        const double p11 = fma(jf, s14, fma(je, s13, fma(jd, s12, s11)));
+        const double p12 = fma(jf, s24, fma(je, s23, fma(jd, s22, s12)));
+        const double p13 = fma(jf, s34, fma(je, s33, fma(jd, s23, s13)));
+        const double p14 = fma(jf, s44, fma(je, s34, fma(jd, s24, s14)));
+        const double p22 = fma(jg, s24, s22), p23 = fma(jg, s34, s23), p24 = fma(jg, s44, s24);
+        const double p33 = jh * s33, p34 = jh * s34, p44 = ji * s44;
+        s00 = fma(jc, p04, fma(jb, p03, fma(ja, p02, p00)));
+        s01 = fma(jf, p04, fma(je, p03, fma(jd, p02, p01)));
+        s02 = fma(jg, p04, p02);
+        s03 = jh * p03;
+        s04 = ji * p04;
+        s11 = fma(jf, p14, fma(je, p13, fma(jd, p12, p11)));
+        s12 = fma(jg, p14, p12);
+        s13 = jh * p13;
+        s14 = ji * p14;
+        s22 = fma(jg, p24, p22);
+        s23 = jh * p23;
+        s24 = ji * p24;
+        s33 = fma(jh, p33, cv0);
+        s34 = ji * p34;
+        s44 = fma(ji, p44, cv1);
+        double* Sk = pS + 25 * kk;
+        Sk[0] = s00, Sk[1] = s01, Sk[2] = s02, Sk[3] = s03, Sk[4] = s04;
+        Sk[5] = s01, Sk[6] = s11, Sk[7] = s12, Sk[8] = s13, Sk[9] = s14;
+        Sk[10] = s02, Sk[11] = s12, Sk[12] = s22, Sk[13] = s23, Sk[14] = s24;
+        Sk[15] = s03, Sk[16] = s13, Sk[17] = s23, Sk[18] = s33, Sk[19] = s34;
+        Sk[20] = s04, Sk[21] = s14, Sk[22] = s24, Sk[23] = s34, Sk[24] = s44;
+        __threadfence_block();
+        s_done = kk + 1;
+      }
+      tl_stamp(24);
+    }
+    __syncwarp();
+  } else {  // ---- warps 3-7: step k's covariance out, lane radius and obstacle margins
+    const TaskDev& tk = a.task[0];
+    for (int kk = w - 3; kk < T; kk += 5) {
+      for (unsigned it = 0; s_done <= kk || mu_ready <= kk + 1; ++it) {
+        __nanosleep(32);
+        if (it > (1u << 27)) __trap();
+      }
+      __threadfence_block();
+      const double* Sk = pS + 25 * kk;
+      if (lane < 25) a.horizon_cov[25 * kk + lane] = Sk[lane];
+      const double c00 = Sk[0], c01 = Sk[1], c10 = Sk[5], c11 = Sk[6];
+      if (lane == 0 && tk.kind != TASK_AVOIDANCE) {  // tighten_lane_radius (uncertainty.cpp:90-96)
+        const double half_tr = 0.5 * (c00 + c11);
+        const double disc = 0.25 * (c00 - c11) * (c00 - c11) + c01 * c10;
+        double lm = half_tr + sqrt(disc > 0.0 ? disc : 0.0);
+        lm = lm > 0.0 ? lm : 0.0;
+        const double r = tk.half_width - sqrt(a.chi2 * lm);
+        a.r_bar[kk] = r;
+        if (r <= 0.0) atomicOr(&infeasible, 1);
+      }
+      if (tk.kind != TASK_TRACKING)  // tighten_obstacle_distance (uncertainty.cpp:98-116)
+        for (int o = lane; o < tk.n_obs; o += 32) {
+          const double mx = pxy[2 * (kk + 1)], my = pxy[2 * (kk + 1) + 1];  // belief mean after step k
+          const double ddx = mx - tk.obs[o][0], ddy = my - tk.obs[o][1];
+          const double dist = sqrt(ddx * ddx + ddy * ddy);
+          double d, n0, n1;
+          if (dist < 1e-12) {
+            n0 = 1.0;
+            n1 = 0.0;
+            d = -tk.obs[o][2];
+          } else {
+            n0 = ddx / dist;
+            n1 = ddy / dist;
+            d = dist - tk.obs[o][2];
+          }
+          const double cn0 = c00 * n0 + c01 * n1, cn1 = c10 * n0 + c11 * n1;
+          double dv = n0 * cn0 + n1 * cn1;
+          dv = dv > 0.0 ? dv : 0.0;
+          const double dbar = d - a.z * sqrt(dv);
+          a.margins[(size_t)kk * tk.n_obs + o] = d - dbar;
+          if (dbar <= 0.0) atomicOr(&infeasible, 1);
+        }
+    }
+  }
+  __syncthreads();
+  for (int i = l; i < T + 2; i += blockDim.x) a.tflags[i] = 0u;  // every reader of this tick's flags is done
+  if (l == 0) {
+    a.infeasible[0] = infeasible;
+    if (a.done_host) {  // zero-copy: infeasibility, then the tick's sequence number
+      const double v = (double)infeasible;
+      publish_host(a.done_host, &v, 1, 1, a.x0[7]);
+    }
+    tl_stamp(12);
+  }
+}
+
 cudaError_t launch_tighten(const TightenArgs& a, cudaStream_t st) {
   size_t msm = sizeof(double) * (size_t)(2 * a.T + 3 * (a.T + 1) + 2 * a.T + 1);
   if (a.model_kind == MODEL_GP)
@@ -2365,10 +2387,8 @@ cudaError_t launch_tighten(const TightenArgs& a, cudaStream_t st) {
     for (int g = 0; g < a.model.G; ++g) no = a.model.g[g].n_out > no ? a.model.g[g].n_out : no;
   void (*mk)(const TightenArgs) = no <= 2 ? tighten_mean_kernel<2> : no <= 4 ? tighten_mean_kernel<4>
                                   : no <= 6 ? tighten_mean_kernel<6> : tighten_mean_kernel<8>;
-  if (a.tflags)  // the pipelined roles' shared memory: J, cv, Σ, positions, cv-ready words
-    msm += sizeof(double) * (size_t)(9 * a.T + 2 * a.T + 25 * a.T + 2 * (a.T + 1)) + sizeof(int) * a.T;
   cudaFuncSetAttribute(mk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm);  // static + dynamic may exceed 48 KB
-  cudaError_t el = launch_pdl(mk, dim3(a.B), dim3(TMEAN_THREADS + (a.tflags ? 96 : 0)), msm, st, a);
+  cudaError_t el = launch_pdl(mk, dim3(a.B), dim3(TMEAN_THREADS + (a.tflags ? 32 : 0)), msm, st, a);
   if (el != cudaSuccess) return el;
   const int G = a.model_kind == MODEL_GP ? a.model.G : 1;
   const int ns = a.model_kind == MODEL_GP ? tighten_splits(a.model.n, a.B) : 1;
@@ -2378,9 +2398,10 @@ cudaError_t launch_tighten(const TightenArgs& a, cudaStream_t st) {
     el = launch_pdl(tighten_var_kernel, dim3(ns, G * a.B, a.T), dim3(256), smem, st, a);
     if (el != cudaSuccess) return el;
   }
-  if (a.tflags) {  // the mean kernel's extra warps did the covariance pass
-    count_launch(2);
-    return cudaGetLastError();
+  if (a.tflags) {
+    const size_t psm = sizeof(double) * (size_t)(9 * a.T + 2 * a.T + 25 * a.T + 2 * (a.T + 1)) + sizeof(int) * a.T;
+    cudaFuncSetAttribute(tighten_cov_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
+    el = launch_pdl(tighten_cov_pipe_kernel, dim3(1), dim3(256), psm, st, a);
   } else {
     const size_t csmem = sizeof(double) * (size_t)(25 * a.T + 2 * a.T + 5 * (a.T + 1) + 25 * a.T);
     cudaFuncSetAttribute(tighten_cov_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem);
