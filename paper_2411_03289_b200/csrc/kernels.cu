@@ -1984,6 +1984,80 @@ __global__ void __launch_bounds__(256) tighten_var_kernel(const TightenArgs a) {
   if (threadIdx.x == 0) tl_stamp(10);
 }
 
+// One step of the belief covariance recursion Σ' = J Σ Jᵀ + diag(0,0,0,cv0,cv1)
+// (uncertainty.cpp:83-87) in registers. jacobian_nominal (dynamics.cpp:68-98) is structurally
+// sparse, J = [1 0 a b c; 0 1 d e f; 0 0 1 0 g; 0 0 0 h 0; 0 0 0 0 i] (j[0..8] = a..i), so a
+// step is P = JΣ (3-FMA rows) then the 15 upper entries of PJᵀ: a 6-FMA-deep chain. Σ stays
+// exactly symmetric, so the reference's symmetrisation is the identity here. s[15] holds the
+// upper triangle row by row (00 01 02 03 04 11 12 13 14 22 23 24 33 34 44); Sk gets all 25.
+GPM_D void cov_step(const double j[9], double cv0, double cv1, double s[15], double* Sk) {
+  const double ja = j[0], jb = j[1], jc = j[2], jd = j[3], je = j[4], jf = j[5], jg = j[6], jh = j[7], ji = j[8];
+  const double s00 = s[0], s01 = s[1], s02 = s[2], s03 = s[3], s04 = s[4], s11 = s[5], s12 = s[6], s13 = s[7];
+  const double s14 = s[8], s22 = s[9], s23 = s[10], s24 = s[11], s33 = s[12], s34 = s[13], s44 = s[14];
+  const double p00 = fma(jc, s04, fma(jb, s03, fma(ja, s02, s00)));
+  const double p01 = fma(jc, s14, fma(jb, s13, fma(ja, s12, s01)));
+  const double p02 = fma(jc, s24, fma(jb, s23, fma(ja, s22, s02)));
+  const double p03 = fma(jc, s34, fma(jb, s33, fma(ja, s23, s03)));
+  const double p04 = fma(jc, s44, fma(jb, s34, fma(ja, s24, s04)));
+  const double p11 = fma(jf, s14, fma(je, s13, fma(jd, s12, s11)));
+  const double p12 = fma(jf, s24, fma(je, s23, fma(jd, s22, s12)));
+  const double p13 = fma(jf, s34, fma(je, s33, fma(jd, s23, s13)));
+  const double p14 = fma(jf, s44, fma(je, s34, fma(jd, s24, s14)));
+  const double p22 = fma(jg, s24, s22), p23 = fma(jg, s34, s23), p24 = fma(jg, s44, s24);
+  const double p33 = jh * s33, p34 = jh * s34, p44 = ji * s44;
+  s[0] = fma(jc, p04, fma(jb, p03, fma(ja, p02, p00)));
+  s[1] = fma(jf, p04, fma(je, p03, fma(jd, p02, p01)));
+  s[2] = fma(jg, p04, p02);
+  s[3] = jh * p03;
+  s[4] = ji * p04;
+  s[5] = fma(jf, p14, fma(je, p13, fma(jd, p12, p11)));
+  s[6] = fma(jg, p14, p12);
+  s[7] = jh * p13;
+  s[8] = ji * p14;
+  s[9] = fma(jg, p24, p22);
+  s[10] = jh * p23;
+  s[11] = ji * p24;
+  s[12] = fma(jh, p33, cv0);
+  s[13] = ji * p34;
+  s[14] = fma(ji, p44, cv1);
+  Sk[0] = s[0], Sk[1] = s[1], Sk[2] = s[2], Sk[3] = s[3], Sk[4] = s[4];
+  Sk[5] = s[1], Sk[6] = s[5], Sk[7] = s[6], Sk[8] = s[7], Sk[9] = s[8];
+  Sk[10] = s[2], Sk[11] = s[6], Sk[12] = s[9], Sk[13] = s[10], Sk[14] = s[11];
+  Sk[15] = s[3], Sk[16] = s[7], Sk[17] = s[10], Sk[18] = s[12], Sk[19] = s[13];
+  Sk[20] = s[4], Sk[21] = s[8], Sk[22] = s[11], Sk[23] = s[13], Sk[24] = s[14];
+}
+// tighten_lane_radius (uncertainty.cpp:90-96) from Σ's (x, y) block
+GPM_D double lane_radius(const double* Sk, double half_width, double chi2) {
+  const double c00 = Sk[0], c01 = Sk[1], c10 = Sk[5], c11 = Sk[6];
+  const double half_tr = 0.5 * (c00 + c11);
+  const double disc = 0.25 * (c00 - c11) * (c00 - c11) + c01 * c10;
+  double lm = half_tr + sqrt(disc > 0.0 ? disc : 0.0);
+  lm = lm > 0.0 ? lm : 0.0;
+  return half_width - sqrt(chi2 * lm);
+}
+// tighten_obstacle_distance (uncertainty.cpp:98-116): margin d - d̄ of one obstacle; *tight = d̄
+GPM_D double obstacle_margin(const double* Sk, double mx, double my, const double obs[3], double z, double* tight) {
+  const double c00 = Sk[0], c01 = Sk[1], c10 = Sk[5], c11 = Sk[6];
+  const double dx = mx - obs[0], dy = my - obs[1];
+  const double dist = sqrt(dx * dx + dy * dy);
+  double d, n0, n1;
+  if (dist < 1e-12) {
+    n0 = 1.0;
+    n1 = 0.0;
+    d = -obs[2];
+  } else {
+    n0 = dx / dist;
+    n1 = dy / dist;
+    d = dist - obs[2];
+  }
+  const double cn0 = c00 * n0 + c01 * n1, cn1 = c10 * n0 + c11 * n1;
+  double dv = n0 * cn0 + n1 * cn1;
+  dv = dv > 0.0 ? dv : 0.0;
+  const double dbar = d - z * sqrt(dv);
+  *tight = dbar;
+  return d - dbar;
+}
+
 // 256 threads stage J / mu / the per-step correction variances, warp 0 runs the
 // serial recursion Σ_{k+1} = J Σ Jᵀ + diag(0,0,0,cv0,cv1) (symmetrised), then all
 // threads evaluate r̄_k and the margins in parallel.
@@ -2073,60 +2147,23 @@ __global__ void __launch_bounds__(256, 1) tighten_cov_kernel(const TightenArgs a
 #ifdef GPM_TCOV_TRACE
   ct[1] = clock64();
 #endif
-  if (l == 0) {
-    // The serial recursion Σ' = J Σ Jᵀ + diag(0,0,0,cv0,cv1) (uncertainty.cpp:83-87) in one
-    // thread's registers. jacobian_nominal (dynamics.cpp:68-98) is structurally sparse:
-    //   J = [1 0 a b c; 0 1 d e f; 0 0 1 0 g; 0 0 0 h 0; 0 0 0 0 i],
-    // so one step is P = JΣ (3-FMA rows) then the 15 upper entries of PJᵀ: a 6-FMA-deep
-    // chain with no shuffles. Σ stays exactly symmetric, so the reference's
-    // symmetrisation is the identity here. J and cv of step k+1 load during step k.
-    double s00 = 0, s01 = 0, s02 = 0, s03 = 0, s04 = 0, s11 = 0, s12 = 0, s13 = 0, s14 = 0;
-    double s22 = 0, s23 = 0, s24 = 0, s33 = 0, s34 = 0, s44 = 0;
-    double na = Js[2], nb = Js[3], nc = Js[4], nd = Js[7], ne = Js[8], nf = Js[9];
-    double ng = Js[14], nh = Js[18], ni = Js[24], ncv0 = cvs[0], ncv1 = cvs[1];
+  if (l == 0) {  // the serial recursion (cov_step) in one thread's registers; J and cv of
+                 // step k+1 load during step k
+    double sg[15] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    double nj[9] = {Js[2], Js[3], Js[4], Js[7], Js[8], Js[9], Js[14], Js[18], Js[24]};
+    double ncv0 = cvs[0], ncv1 = cvs[1];
     for (int k = 0; k < T; ++k) {
-      const double ja = na, jb = nb, jc = nc, jd = nd, je = ne, jf = nf, jg = ng, jh = nh, ji = ni;
+      double j[9];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) j[e] = nj[e];
       const double cv0 = ncv0, cv1 = ncv1;
       if (k + 1 < T) {
         const double* Jn = Js + 25 * (k + 1);
-        na = Jn[2], nb = Jn[3], nc = Jn[4], nd = Jn[7], ne = Jn[8], nf = Jn[9];
-        ng = Jn[14], nh = Jn[18], ni = Jn[24];
+        nj[0] = Jn[2], nj[1] = Jn[3], nj[2] = Jn[4], nj[3] = Jn[7], nj[4] = Jn[8], nj[5] = Jn[9];
+        nj[6] = Jn[14], nj[7] = Jn[18], nj[8] = Jn[24];
         ncv0 = cvs[2 * k + 2], ncv1 = cvs[2 * k + 3];
       }
-      // P = J Σ (rows 0..4; only the entries P Jᵀ's upper triangle reads)
-      const double p00 = fma(jc, s04, fma(jb, s03, fma(ja, s02, s00)));
-      const double p01 = fma(jc, s14, fma(jb, s13, fma(ja, s12, s01)));
-      const double p02 = fma(jc, s24, fma(jb, s23, fma(ja, s22, s02)));
-      const double p03 = fma(jc, s34, fma(jb, s33, fma(ja, s23, s03)));
-      const double p04 = fma(jc, s44, fma(jb, s34, fma(ja, s24, s04)));
-      const double p11 = fma(jf, s14, fma(je, s13, fma(jd, s12, s11)));
-      const double p12 = fma(jf, s24, fma(je, s23, fma(jd, s22, s12)));
-      const double p13 = fma(jf, s34, fma(je, s33, fma(jd, s23, s13)));
-      const double p14 = fma(jf, s44, fma(je, s34, fma(jd, s24, s14)));
-      const double p22 = fma(jg, s24, s22), p23 = fma(jg, s34, s23), p24 = fma(jg, s44, s24);
-      const double p33 = jh * s33, p34 = jh * s34, p44 = ji * s44;
-      // Σ' = P Jᵀ (+ the correction variances on the (3,3), (4,4) diagonal)
-      s00 = fma(jc, p04, fma(jb, p03, fma(ja, p02, p00)));
-      s01 = fma(jf, p04, fma(je, p03, fma(jd, p02, p01)));
-      s02 = fma(jg, p04, p02);
-      s03 = jh * p03;
-      s04 = ji * p04;
-      s11 = fma(jf, p14, fma(je, p13, fma(jd, p12, p11)));
-      s12 = fma(jg, p14, p12);
-      s13 = jh * p13;
-      s14 = ji * p14;
-      s22 = fma(jg, p24, p22);
-      s23 = jh * p23;
-      s24 = ji * p24;
-      s33 = fma(jh, p33, cv0);
-      s34 = ji * p34;
-      s44 = fma(ji, p44, cv1);
-      double* Sk = Ss + 25 * k;
-      Sk[0] = s00, Sk[1] = s01, Sk[2] = s02, Sk[3] = s03, Sk[4] = s04;
-      Sk[5] = s01, Sk[6] = s11, Sk[7] = s12, Sk[8] = s13, Sk[9] = s14;
-      Sk[10] = s02, Sk[11] = s12, Sk[12] = s22, Sk[13] = s23, Sk[14] = s24;
-      Sk[15] = s03, Sk[16] = s13, Sk[17] = s23, Sk[18] = s33, Sk[19] = s34;
-      Sk[20] = s04, Sk[21] = s14, Sk[22] = s24, Sk[23] = s34, Sk[24] = s44;
+      cov_step(j, cv0, cv1, sg, Ss + 25 * k);
     }
   }
   __syncthreads();
@@ -2136,39 +2173,16 @@ __global__ void __launch_bounds__(256, 1) tighten_cov_kernel(const TightenArgs a
   for (int i = l; i < 25 * T; i += nt) ahcov[i] = Ss[i];
   for (int k = l; k < T; k += nt) {  // tighten_lane_radius (uncertainty.cpp:90-96), parallel in k
     if (t.kind == TASK_AVOIDANCE) break;
-    const double* Sk = Ss + 25 * k;
-    const double c00 = Sk[0], c01 = Sk[1], c10 = Sk[5], c11 = Sk[6];
-    const double half_tr = 0.5 * (c00 + c11);
-    const double disc = 0.25 * (c00 - c11) * (c00 - c11) + c01 * c10;
-    double lm = half_tr + sqrt(disc > 0.0 ? disc : 0.0);
-    lm = lm > 0.0 ? lm : 0.0;
-    const double r = t.half_width - sqrt(a.chi2 * lm);
+    const double r = lane_radius(Ss + 25 * k, t.half_width, a.chi2);
     arbar[k] = r;
     if (r <= 0.0) atomicOr(&infeasible, 1);
   }
   if (t.kind != TASK_TRACKING)  // tighten_obstacle_distance (uncertainty.cpp:98-116), parallel in (k, o)
     for (int idx = l; idx < T * t.n_obs; idx += nt) {
       const int k = idx / t.n_obs, o = idx % t.n_obs;
-      const double* Sk = Ss + 25 * k;
-      const double c00 = Sk[0], c01 = Sk[1], c10 = Sk[5], c11 = Sk[6];
       const double* mu = mus + (k + 1) * 5;  // belief mean after step k
-      const double dx = mu[0] - t.obs[o][0], dy = mu[1] - t.obs[o][1];
-      const double dist = sqrt(dx * dx + dy * dy);
-      double d, n0, n1;
-      if (dist < 1e-12) {
-        n0 = 1.0;
-        n1 = 0.0;
-        d = -t.obs[o][2];
-      } else {
-        n0 = dx / dist;
-        n1 = dy / dist;
-        d = dist - t.obs[o][2];
-      }
-      const double cn0 = c00 * n0 + c01 * n1, cn1 = c10 * n0 + c11 * n1;
-      double dv = n0 * cn0 + n1 * cn1;
-      dv = dv > 0.0 ? dv : 0.0;
-      const double dbar = d - a.z * sqrt(dv);
-      amarg[(size_t)k * t.n_obs + o] = d - dbar;
+      double dbar;
+      amarg[(size_t)k * t.n_obs + o] = obstacle_margin(Ss + 25 * k, mu[0], mu[1], t.obs[o], a.z, &dbar);
       if (dbar <= 0.0) atomicOr(&infeasible, 1);
     }
   __syncthreads();
@@ -2272,50 +2286,17 @@ __global__ void __launch_bounds__(256, 1) tighten_cov_pipe_kernel(const TightenA
     }
   } else if (w == 0) {  // ---- the covariance recursion (tighten_cov_kernel's), step by step
     if (lane == 0) {
-      double s00 = 0, s01 = 0, s02 = 0, s03 = 0, s04 = 0, s11 = 0, s12 = 0, s13 = 0, s14 = 0;
-      double s22 = 0, s23 = 0, s24 = 0, s33 = 0, s34 = 0, s44 = 0;
+      double sg[15] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
       for (int kk = 0; kk < T; ++kk) {
         for (unsigned it = 0; j_ready <= kk || !cv_ready[kk]; ++it) {
           __nanosleep(16);
           if (it > (1u << 27)) __trap();
         }
         __threadfence_block();
-        const double* Jk = pJ + 9 * kk;
-        const double ja = Jk[0], jb = Jk[1], jc = Jk[2], jd = Jk[3], je = Jk[4], jf = Jk[5], jg = Jk[6], jh = Jk[7],
-                     ji = Jk[8];
-        const double cv0 = pcv[2 * kk], cv1 = pcv[2 * kk + 1];
-        const double p00 = fma(jc, s04, fma(jb, s03, fma(ja, s02, s00)));
-        const double p01 = fma(jc, s14, fma(jb, s13, fma(ja, s12, s01)));
-        const double p02 = fma(jc, s24, fma(jb, s23, fma(ja, s22, s02)));
-        const double p03 = fma(jc, s34, fma(jb, s33, fma(ja, s23, s03)));
-        const double p04 = fma(jc, s44, fma(jb, s34, fma(ja, s24, s04)));
-        const double p11 = fma(jf, s14, fma(je, s13, fma(jd, s12, s11)));
-        const double p12 = fma(jf, s24, fma(je, s23, fma(jd, s22, s12)));
-        const double p13 = fma(jf, s34, fma(je, s33, fma(jd, s23, s13)));
-        const double p14 = fma(jf, s44, fma(je, s34, fma(jd, s24, s14)));
-        const double p22 = fma(jg, s24, s22), p23 = fma(jg, s34, s23), p24 = fma(jg, s44, s24);
-        const double p33 = jh * s33, p34 = jh * s34, p44 = ji * s44;
-        s00 = fma(jc, p04, fma(jb, p03, fma(ja, p02, p00)));
-        s01 = fma(jf, p04, fma(je, p03, fma(jd, p02, p01)));
-        s02 = fma(jg, p04, p02);
-        s03 = jh * p03;
-        s04 = ji * p04;
-        s11 = fma(jf, p14, fma(je, p13, fma(jd, p12, p11)));
-        s12 = fma(jg, p14, p12);
-        s13 = jh * p13;
-        s14 = ji * p14;
-        s22 = fma(jg, p24, p22);
-        s23 = jh * p23;
-        s24 = ji * p24;
-        s33 = fma(jh, p33, cv0);
-        s34 = ji * p34;
-        s44 = fma(ji, p44, cv1);
-        double* Sk = pS + 25 * kk;
-        Sk[0] = s00, Sk[1] = s01, Sk[2] = s02, Sk[3] = s03, Sk[4] = s04;
-        Sk[5] = s01, Sk[6] = s11, Sk[7] = s12, Sk[8] = s13, Sk[9] = s14;
-        Sk[10] = s02, Sk[11] = s12, Sk[12] = s22, Sk[13] = s23, Sk[14] = s24;
-        Sk[15] = s03, Sk[16] = s13, Sk[17] = s23, Sk[18] = s33, Sk[19] = s34;
-        Sk[20] = s04, Sk[21] = s14, Sk[22] = s24, Sk[23] = s34, Sk[24] = s44;
+        double j[9];
+#pragma unroll
+        for (int e = 0; e < 9; ++e) j[e] = pJ[9 * kk + e];
+        cov_step(j, pcv[2 * kk], pcv[2 * kk + 1], sg, pS + 25 * kk);
         __threadfence_block();
         s_done = kk + 1;
       }
@@ -2332,36 +2313,16 @@ __global__ void __launch_bounds__(256, 1) tighten_cov_pipe_kernel(const TightenA
       __threadfence_block();
       const double* Sk = pS + 25 * kk;
       if (lane < 25) a.horizon_cov[25 * kk + lane] = Sk[lane];
-      const double c00 = Sk[0], c01 = Sk[1], c10 = Sk[5], c11 = Sk[6];
       if (lane == 0 && tk.kind != TASK_AVOIDANCE) {  // tighten_lane_radius (uncertainty.cpp:90-96)
-        const double half_tr = 0.5 * (c00 + c11);
-        const double disc = 0.25 * (c00 - c11) * (c00 - c11) + c01 * c10;
-        double lm = half_tr + sqrt(disc > 0.0 ? disc : 0.0);
-        lm = lm > 0.0 ? lm : 0.0;
-        const double r = tk.half_width - sqrt(a.chi2 * lm);
+        const double r = lane_radius(Sk, tk.half_width, a.chi2);
         a.r_bar[kk] = r;
         if (r <= 0.0) atomicOr(&infeasible, 1);
       }
       if (tk.kind != TASK_TRACKING)  // tighten_obstacle_distance (uncertainty.cpp:98-116)
-        for (int o = lane; o < tk.n_obs; o += 32) {
-          const double mx = pxy[2 * (kk + 1)], my = pxy[2 * (kk + 1) + 1];  // belief mean after step k
-          const double ddx = mx - tk.obs[o][0], ddy = my - tk.obs[o][1];
-          const double dist = sqrt(ddx * ddx + ddy * ddy);
-          double d, n0, n1;
-          if (dist < 1e-12) {
-            n0 = 1.0;
-            n1 = 0.0;
-            d = -tk.obs[o][2];
-          } else {
-            n0 = ddx / dist;
-            n1 = ddy / dist;
-            d = dist - tk.obs[o][2];
-          }
-          const double cn0 = c00 * n0 + c01 * n1, cn1 = c10 * n0 + c11 * n1;
-          double dv = n0 * cn0 + n1 * cn1;
-          dv = dv > 0.0 ? dv : 0.0;
-          const double dbar = d - a.z * sqrt(dv);
-          a.margins[(size_t)kk * tk.n_obs + o] = d - dbar;
+        for (int o = lane; o < tk.n_obs; o += 32) {  // belief mean after step k
+          double dbar;
+          a.margins[(size_t)kk * tk.n_obs + o] =
+              obstacle_margin(Sk, pxy[2 * (kk + 1)], pxy[2 * (kk + 1) + 1], tk.obs[o], a.z, &dbar);
           if (dbar <= 0.0) atomicOr(&infeasible, 1);
         }
     }
