@@ -19,7 +19,11 @@ sys.path.insert(0, {root!r})
 import paper_2411_03289_b200 as G
 from paper_2411_03289_b200 import workloads as W
 from tests.helpers import build_pair
-w = W.CONFIGS[sys.argv[1]]
+import dataclasses
+name, _, horizon = sys.argv[1].partition(":")
+w = W.CONFIGS[name]
+if horizon:
+    w = dataclasses.replace(w, horizon=int(horizon))
 _, pd, _, td, _ = build_pair(w, samples=int(sys.argv[3]))
 x = np.array(w.x0)
 out = {{}}
@@ -36,13 +40,15 @@ np.savez(sys.argv[2], **out)
 """
 
 
-@pytest.mark.parametrize("cfg,samples", [("config2", 1024), ("config3", 512), ("config1", 512)])
+@pytest.mark.parametrize("cfg,samples", [("config2", 1024), ("config3", 512), ("config1", 512),
+                                         ("config2:1", 256), ("config2:2", 256), ("config2:33", 256),
+                                         ("config2:97", 256)])
 def test_pipelined_tightening_matches_sequential(tmp_path, cfg, samples):
     script = tmp_path / "arm.py"
     script.write_text(_ARM.format(root=ROOT))
     res = {}
     for seq in ("0", "1"):
-        f = str(tmp_path / f"{cfg}_{seq}.npz")
+        f = str(tmp_path / f"{cfg.replace(':', '_')}_{seq}.npz")
         env = {**os.environ, "GPMPPI_TIGHTEN_SEQUENTIAL": seq}
         r = subprocess.run([sys.executable, str(script), cfg, f, str(samples)], env=env, capture_output=True,
                            text=True, timeout=600)
