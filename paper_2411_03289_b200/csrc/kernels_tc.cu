@@ -1397,10 +1397,11 @@ __global__ void __launch_bounds__(tc::F16_THREADS, 1) variance_f16_kernel(const 
 // 32 chunks), at n = 2048 320 instead of 576: the exponential producers, which bound the
 // single-CTA kernel, do 33-44% less work for the same tensor work.
 // Roles (both CTAs): w0 lane 0 bulk-copies the CTA's half of each L^{-T} chunk, w1 issues
-// the MMAs (leader) or relays the CTA's stage-full to the leader (peer), w2 owns TMEM,
-// w4-7 drain TMEM, w8-15 produce A (lane = 2 rows x 4 points). The leader's full barrier
-// counts its own producers + copy + the peer relay; MMA completion is multicast to both
-// CTAs' empty / tfull barriers; both CTAs' epilogues arrive on the leader's tempty.
+// the MMAs (leader) or relays the completion of the CTA's copy to the leader (peer), w2 owns
+// TMEM, w4-7 drain TMEM, w8-15 produce A (lane = 2 rows x 4 points). The leader's full
+// barrier counts both CTAs' producer warps (the peer's arrive remotely, `mapa`), its own copy
+// and the relayed peer copy; MMA completion is multicast to both CTAs' empty / tfull
+// barriers; both CTAs' epilogues arrive on the leader's tempty.
 namespace tc {
 constexpr int P2_PRODUCER_WARPS = 8;
 constexpr int P2_THREADS = 256 + 32 * P2_PRODUCER_WARPS;
@@ -1545,7 +1546,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::P2_THREADS, 1)
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(smem_u32(&full[s]), P2_PRODUCER_WARPS + 1 + (leader ? 1 : 0));
+      // leader: both CTAs' producer warps (the peer's arrive remotely), its own copy, the peer's
+      // copy relayed; peer: its copy's bytes only
+      mbar_init(smem_u32(&full[s]), leader ? 2 * P2_PRODUCER_WARPS + 2 : 1);
       mbar_init(smem_u32(&empty[s]), 1);
     }
     mbar_init(smem_u32(tfull), 1);
@@ -1638,7 +1641,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::P2_THREADS, 1)
           if (lane == 0 && uc < 10) trace_at(3 + 2 * (int)uc, dbg);
         }
       }
-    } else if (lane == 0) {  // ---------------- peer: relay stage-full to the leader
+    } else if (lane == 0) {  // ---------------- peer: relay its operand copy's completion to the leader
       Ring r(S);
       const uint32_t lead_full = map_rank(smem_u32(full), 0);
       for (long long st = sb; st < se; ++st)
@@ -1653,6 +1656,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::P2_THREADS, 1)
   } else if (warp >= 8) {
     // ---------------- A producers: k*/sf2 for this CTA's 128 rows, FP16 hi + lo
     const int pw = warp - 8;
+    const uint32_t lead_full_p = map_rank(smem_u32(full), 0);
     const int qi = lane & 7, pg = lane >> 3;
     Ring r(S);
     for (long long st = sb; st < se; ++st) {
@@ -1683,7 +1687,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::P2_THREADS, 1)
           __syncwarp();
           if (GPM_DIAG(dbg & 256)) {  // diagnostics: no A production
             __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&full[r.s]));
+            if (lane == 0) {
+              if (leader)
+                mbar_arrive(smem_u32(&full[r.s]));
+              else
+                mbar_arrive_remote(lead_full_p + 8u * (uint32_t)r.s);
+            }
             continue;
           }
 #pragma unroll
@@ -1726,7 +1735,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::P2_THREADS, 1)
           }
           fence_proxy_async();
           __syncwarp();
-          if (lane == 0) mbar_arrive(smem_u32(&full[r.s]));
+          if (lane == 0) {  // the peer's producers arrive on the leader's barrier directly
+            if (leader)
+              mbar_arrive(smem_u32(&full[r.s]));
+            else
+              mbar_arrive_remote(lead_full_p + 8u * (uint32_t)r.s);
+          }
         }
       }
     }
