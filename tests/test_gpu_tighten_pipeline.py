@@ -58,3 +58,22 @@ def test_pipelined_tightening_matches_sequential(tmp_path, cfg, samples):
     assert sorted(a.files) == sorted(b.files)
     for k in a.files:
         np.testing.assert_array_equal(a[k], b[k], err_msg=f"{cfg}: {k}")
+
+
+@pytest.mark.parametrize("serialise", [{"GPMPPI_NO_PDL": "1"}, {"GPMPPI_NO_GRAPH": "1", "GPMPPI_DEBUG_SYNC": "1"}])
+def test_pipelined_tightening_survives_serialised_kernels(tmp_path, serialise):
+    """The pipelined pass only waits on kernels launched before the waiter, so it completes (with
+    the same results) when the kernels cannot overlap: no programmatic dependent launch, or a
+    synchronisation after every launch (as under a serialising profiler)."""
+    script = tmp_path / "arm.py"
+    script.write_text(_ARM.format(root=ROOT))
+    res = {}
+    for tag, extra in (("overlap", {}), ("serial", serialise)):
+        f = str(tmp_path / f"{tag}.npz")
+        env = {**os.environ, "GPMPPI_TIGHTEN_SEQUENTIAL": "0", **extra}
+        r = subprocess.run([sys.executable, str(script), "config2", f, "512"], env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        res[tag] = np.load(f)
+    for k in res["overlap"].files:
+        np.testing.assert_array_equal(res["overlap"][k], res["serial"][k], err_msg=k)
