@@ -989,6 +989,8 @@ void enqueue_h2d(gpmppi_planner* p) {  // tick blocks + tasks: one copy (contigu
     CK(cudaMemcpyAsync(p->d_x0, p->h_x0, p->tick_bytes, cudaMemcpyHostToDevice, p->stream));
 }
 
+bool command_in_tightening(const gpmppi_planner* p);
+
 // Rollout + variance + reduce for every robot's sample range. finish=1 also
 // applies the update (single-rank solve).
 void enqueue_samples(gpmppi_planner* p, int finish, cudaEvent_t* evs) {
@@ -1100,7 +1102,7 @@ void enqueue_samples(gpmppi_planner* p, int finish, cudaEvent_t* evs) {
   r.hi[0] = p->cfg.hi[0];
   r.hi[1] = p->cfg.hi[1];
   r.out = p->d_out;
-  r.out_host = p->zc_tick ? p->d_out_host : nullptr;
+  r.out_host = p->zc_tick && !command_in_tightening(p) ? p->d_out_host : nullptr;
   check(gpm::launch_reduce(r, p->B * p->reduce_blocks, p->stream), "reduce kernel");
   if (evs) CK(cudaEventRecord(evs[3], p->stream));
 }
@@ -1124,6 +1126,21 @@ void enqueue_update(gpmppi_planner* p, cudaEvent_t* evs) {
                            p->d_x0),
         "finish kernel");
   if (evs) CK(cudaEventRecord(evs[3], p->stream));  // the exchange counts to the reduce phase
+}
+
+// single-robot GP planners run the pipelined tightening pass (TightenArgs::tflags)
+bool pipelined_tightening(const gpmppi_planner* p) {
+  static const int seq_env = getenv("GPMPPI_TIGHTEN_SEQUENTIAL") ? atoi(getenv("GPMPPI_TIGHTEN_SEQUENTIAL")) : 0;
+  return p->B == 1 && p->model_kind == GPMPPI_MODEL_GP_ENSEMBLE && !seq_env;
+}
+// ... and then the mean kernel's publisher warp, not the reduce's last block, writes the
+// command into the mapped words: the system-scope fence leaves the tick's critical path
+// (only when plan_step waits for the whole tick: in command-first mode the reduce publishes,
+// ~2 us sooner to the command; measured 0.3707 vs 0.3722 ms full plan_step, 0.3362 vs 0.3338
+// command-first at config 2)
+bool command_in_tightening(const gpmppi_planner* p) {
+  static const int env = getenv("GPMPPI_CMD_IN_TIGHTEN") ? atoi(getenv("GPMPPI_CMD_IN_TIGHTEN")) : 1;
+  return env && p->zc_tick && !p->comm && !p->command_first && pipelined_tightening(p);
 }
 
 void enqueue_tighten(gpmppi_planner* p) {
@@ -1150,9 +1167,10 @@ void enqueue_tighten(gpmppi_planner* p) {
   t.tJ = p->d_tJ;
   t.tvar_part = p->d_tvar;
   t.done_host = p->zc_tick ? p->d_done_host : nullptr;
-  static const int seq_env = getenv("GPMPPI_TIGHTEN_SEQUENTIAL") ? atoi(getenv("GPMPPI_TIGHTEN_SEQUENTIAL")) : 0;
-  t.tflags = (p->B == 1 && p->model_kind == GPMPPI_MODEL_GP_ENSEMBLE && !seq_env) ? p->d_tflags : nullptr;
+  t.tflags = pipelined_tightening(p) ? p->d_tflags : nullptr;
   t.tcv = p->d_tcv;
+  t.cmd_host = command_in_tightening(p) ? p->d_out_host : nullptr;
+  t.cmd_dev = p->d_out;
   check(gpm::launch_tighten(t, p->stream), "tighten kernel");
 }
 
@@ -1443,7 +1461,8 @@ void plan_tick(gpmppi_planner* p, const double* x0, const gpmppi_task* tasks, do
   stage_tick(p, x0, tasks);
   // everything a captured kernel argument depends on (device buffers are fixed per planner)
   const long long key = (long long)p->n_obs_max | ((long long)p->noise_mode << 8) | ((long long)p->var_path << 10) |
-                        ((long long)p->R << 16) | ((long long)(p->comm != nullptr) << 24);
+                        ((long long)p->R << 16) | ((long long)(p->comm != nullptr) << 24) |
+                        ((long long)p->command_first << 25);  // who publishes the command (command_in_tightening)
   if (p->use_graph && (!p->tick_exec || p->graph_key != key)) capture_tick(p, key);
   if (p->use_graph && p->tick_exec) {
     CK(cudaGraphLaunch(p->tick_exec, p->stream));

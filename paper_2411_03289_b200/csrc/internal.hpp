@@ -191,6 +191,8 @@ struct TightenArgs {
   // Null: grid ordering only (batched planners).
   unsigned int* tflags;  // [T + 2]: queries out, J / belief means out, per-step variance slices done
   double* tcv;           // [T][2] combined correction variances of the pipelined pass
+  double* cmd_host;      // non-null: the mean kernel publishes the command (cmd_dev, OUT words) here
+  const double* cmd_dev;
 };
 
 // Programmatic dependent launch: the kernel may be scheduled while its stream

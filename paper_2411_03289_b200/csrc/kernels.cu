@@ -1578,6 +1578,12 @@ __global__ void __launch_bounds__(TMEAN_THREADS + 32, 1) tighten_mean_kernel(con
     for (int i = 0; i < 4; ++i) e_cur[i] = fma(q2, rz2[i], fma(q3, rz3[i], rzn[i] + qu));
   }
   if (pub) {
+    if (a.cmd_host && lane == 0) {  // the reduction's command and diagnostics into the mapped words
+      double o[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = __ldcg(a.cmd_dev + i);
+      publish_host(a.cmd_host, o, 8, BatchStrides::OUT - 1, a.x0[7]);
+    }
     // the publisher warp walks the chain's steps as they complete (convergent): per batch of
     // newly known steps, lane 0 advances the heading recursion, one lane per step evaluates the
     // arc increment and the Jacobian (as the sequential tail below), lane 0 writes the queries,
