@@ -59,8 +59,24 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
+// Suspend-time hint (ns) of the single-CTA kernels' mbarrier waits: a failed poll becomes
+// NANOSLEEP.SYNCS (woken by barrier activity) instead of an immediate re-poll. Config 5
+// (variance_f16_kernel) 1.745 -> 1.726 ms. The CTA-pair kernel does not use it (mbar_wait_x).
+// 0 = no hint (A/B).
+#ifndef GPM_WAIT_HINT_NS
+#define GPM_WAIT_HINT_NS 10000000
+#endif
 __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
   uint32_t ok;
+#if GPM_WAIT_HINT_NS > 0
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity), "n"(GPM_WAIT_HINT_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -68,6 +84,7 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
       : "=r"(ok)
       : "r"(bar), "r"(parity)
       : "memory");
+#endif
   return ok != 0;
 }
 __device__ __forceinline__ bool mbar_test_wait(uint32_t bar, uint32_t parity) {
@@ -1427,8 +1444,12 @@ __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-// a wait that outlives ~2^26 polls (seconds) is a protocol bug: trap instead of hanging
-// the device
+// The CTA pair's waits poll without the suspend-time hint: with it (NANOSLEEP.SYNCS after a
+// failed poll) the pair kernel ran 45% slower at config 2 (its barriers complete through remote
+// arrivals and multicast commits). Its epilogue warps' polls are ~45% of the kernel's executed
+// instructions (ncu source view), but a __nanosleep back-off in that wait (64 / 128 / 256 ns) or
+// in the producers' did not change the kernel's time (it is not issue-bound). A wait that
+// outlives ~2^26 polls (seconds) is a protocol bug: trap instead of hanging the device.
 __device__ __forceinline__ void mbar_wait_x(uint32_t bar, uint32_t parity) {
   uint32_t ok = 0;
   for (uint32_t spins = 0;; ++spins) {
