@@ -2221,12 +2221,18 @@ cudaError_t launch_tc_variance(const VarianceArgs& a, int mode, cudaStream_t st)
     const char* e = getenv("GPMPPI_F16_CPS");
     cps_env = e ? atoi(e) : 0;
   }
+  static int stages_env = -1;  // GPMPPI_F16_STAGES caps the ring depth (A/B)
+  if (stages_env < 0) {
+    const char* e = getenv("GPMPPI_F16_STAGES");
+    stages_env = e ? atoi(e) : 0;
+  }
+  const int max_stages = stages_env >= 2 && stages_env <= 8 ? stages_env : 8;
   if (pair && a.g.tc_h2 && a.g.tc_h2meta) {
     // two chunks per ring stage when three such stages fit
     int cps = cps_env >= 1 && cps_env <= 3 ? cps_env : 2;
     while (cps > 1 && f16x2_smem_bytes(a.g, 3, cps) > kSmemMax) --cps;
-    int stages = 8;
-    while (stages > 3 && f16x2_smem_bytes(a.g, stages, cps) > kSmemMax) --stages;
+    int stages = max_stages;
+    while (stages > 2 && f16x2_smem_bytes(a.g, stages, cps) > kSmemMax) --stages;
     if (f16x2_smem_bytes(a.g, stages, cps) <= kSmemMax) {
       const size_t psm = f16x2_smem_bytes(a.g, stages, cps);
       void (*kern)(const VarianceArgs, int, int) =
@@ -2263,8 +2269,8 @@ cudaError_t launch_tc_variance(const VarianceArgs& a, int mode, cudaStream_t st)
     // two chunks per ring stage when three such stages fit
     int cps = cps_env == 1 ? 1 : 2;
     if (cps == 2 && f16_smem_bytes(a.g, 3, 2) > kSmemMax) cps = 1;
-    int stages = 8;
-    while (stages > 3 && f16_smem_bytes(a.g, stages, cps) > kSmemMax) --stages;
+    int stages = max_stages;
+    while (stages > 2 && f16_smem_bytes(a.g, stages, cps) > kSmemMax) --stages;
     if (f16_smem_bytes(a.g, stages, cps) <= kSmemMax) {
       const size_t hsm = f16_smem_bytes(a.g, stages, cps);
       void (*kern)(const VarianceArgs, int, int) = cps == 2 ? variance_f16_kernel<2> : variance_f16_kernel<1>;
