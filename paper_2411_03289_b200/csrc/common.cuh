@@ -113,6 +113,35 @@ GPM_HD double exp_tab(double x, const double* tab) {
   return x < -700.0 ? 0.0 : scaled;
 }
 
+// exp_tab of an argument already scaled by 32/ln2 (t = 32x/ln2; the rollout folds the scale
+// into its staged kernel points): n = rint(t), s = t - n is exact (Sterbenz), and
+// e^(s·ln2/32) - 1 is exp_tab's polynomial with the scale folded into its coefficients
+// (b_i = c_i·(ln2/32)^i, Horner in s). 10 FP64 ops instead of 11: the reduction is one
+// DADD instead of two DFMAs. Within 2 ulp of exp(t·ln2/32) (tests/cpp/exp_tab_check.cpp);
+// t below -700·32/ln2 flushes to 0, as exp_tab.
+constexpr double kLn2d32 = 0x1.62e42fefa39efp-6;
+constexpr double kExpTB1 = kLn2d32;
+constexpr double kExpTB2 = 0x1.ffffffffe5bc7p-2 * kLn2d32 * kLn2d32;
+constexpr double kExpTB3 = 0x1.5555555541cedp-3 * kLn2d32 * kLn2d32 * kLn2d32;
+constexpr double kExpTB4 = 0x1.5555c2a9cb753p-5 * kLn2d32 * kLn2d32 * kLn2d32 * kLn2d32;
+constexpr double kExpTB5 = 0x1.1111688fec18cp-7 * kLn2d32 * kLn2d32 * kLn2d32 * kLn2d32 * kLn2d32;
+constexpr double kExpTMin = -700.0 * kInvLn2x32;
+GPM_HD double exp_tab_t(double t, const double* tab) {
+  const double magic = 6755399441055744.0;
+  const double tt = t + magic;
+  const int n = dbl_lo(tt);
+  const double s = t - (tt - magic);
+  double u = fma(kExpTB5, s, kExpTB4);
+  u = fma(u, s, kExpTB3);
+  u = fma(u, s, kExpTB2);
+  u = fma(u, s, kExpTB1);
+  const double p = u * s;  // e^(s·ln2/32) - 1
+  const double tj = tab[n & 31];
+  const double res = fma(tj, p, tj);
+  const double scaled = dbl_from(dbl_hi(res) + ((n >> 5) << 20), dbl_lo(res));
+  return t < kExpTMin ? 0.0 : scaled;
+}
+
 GPM_HD double wrap_angle(double a) {
   double r = remainder(a, 2.0 * kPi);
   if (r <= -kPi) r += 2.0 * kPi;

@@ -359,6 +359,9 @@ GPM_D void rollout_phase2(const RolloutArgs& a, const SmemView& sv, const TaskDe
 #endif
 }
 
+#ifndef GPM_EXP_PRESCALE
+#define GPM_EXP_PRESCALE 1
+#endif
 template <int LPS, int SPG>
 __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const RolloutArgs a) {
   if (threadIdx.x == 0) tl_stamp(1);
@@ -379,7 +382,14 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
       const double2* src = reinterpret_cast<const double2*>(a.model.g[g].pts);
       double2* d2 = reinterpret_cast<double2*>(dst);
 #pragma unroll 4
-      for (int i = threadIdx.x; i < cnt / 2; i += blockDim.x) d2[i] = __ldg(src + i);
+      for (int i = threadIdx.x; i < cnt / 2; i += blockDim.x) {
+        double2 z = __ldg(src + i);
+#if GPM_EXP_PRESCALE  // the exponent rows carry exp_tab_t's 32/ln2 (padding: -1e300·46 stays finite)
+        z.x *= kInvLn2x32;
+        z.y *= kInvLn2x32;
+#endif
+        d2[i] = z;
+      }
       dst += 7 * ns;
     }
     ubuf = reinterpret_cast<double2*>(dst) + (size_t)gib * SPG * T;
@@ -514,6 +524,9 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
           q2[j] = u0[j] * gil[g][2];
           q3[j] = u1[j] * gil[g][3];
           qn[j] = -0.5 * (q0[j] * q0[j] + q1[j] * q1[j] + q2[j] * q2[j] + q3[j] * q3[j]);
+#if GPM_EXP_PRESCALE
+          qn[j] *= kInvLn2x32;
+#endif
           acc[j][0] = acc[j][1] = 0.0;
         }
         // two adjacent points per lane and load (LDS.128): the 32/LPS sample groups of a
@@ -536,7 +549,11 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
             // q·z + (qn + zn) as one DADD and four DFMAs (gp.cpp:177-179)
             const double d0 = fma(q0[j], a0.x, fma(q1[j], a1.x, fma(q2[j], a2.x, fma(q3[j], a3.x, qn[j] + an.x))));
             const double d1 = fma(q0[j], a0.y, fma(q1[j], a1.y, fma(q2[j], a2.y, fma(q3[j], a3.y, qn[j] + an.y))));
+#if GPM_EXP_PRESCALE  // d = 32/ln2 · (q·z + qn + zn): the reduction is one DADD (exp_tab_t)
+            const double k0 = exp_tab_t(d0, sv.etab), k1 = exp_tab_t(d1, sv.etab);
+#else
             const double k0 = exp_tab(d0, sv.etab), k1 = exp_tab(d1, sv.etab);
+#endif
             acc[j][0] = fma(k1, av.y, fma(k0, av.x, acc[j][0]));  // gp.cpp:181-182, terrain-combined
             acc[j][1] = fma(k1, aw.y, fma(k0, aw.x, acc[j][1]));
           }
