@@ -282,26 +282,47 @@ size_t rollout_smem_bytes(const RolloutArgs& a);
 size_t rollout_scratch_doubles(int T, int num_sms);
 int reduce_blocks_for(int K_local, int B, int num_sms, int T);
 int tighten_splits(int n, int B);
-// CTA-pair variance columns: pass p covers columns [512p, 512p + 512) as two halves of
-// <= 256 (TMEM columns [0, 256) and [256, 512)); chunk kb (points [16kb, 16kb + 16))
-// reaches the columns from its diagonal on, rounded down to 32 so each CTA of the pair
-// holds a multiple of 16 B rows. c0[h] = first column of half h, nc[h] = N of its MMA
-// (0 = the chunk does not reach the half). Shared by the host builder and the kernel.
+// CTA-pair variance (variance_f16x2_kernel): the MMAs of 512-column pass p, 16-point chunk kb.
+// The chunk's active columns (triangle skip at GPM_PAIR_GRAN granularity, widths rounded to 32
+// so each CTA's N/2 rows stay whole 8-row groups) form one contiguous range of pass-relative
+// TMEM columns; it is issued as at most two M = 256 MMAs: c0[s] = first TMEM column, nc[s] =
+// N (0 = no MMA), split at the 256-column boundary. GPM_PAIR_BALANCE=1 splits a range wider
+// than 256 columns into two near-equal MMAs instead (the microbenchmark's max(75, N/2)-cycle
+// pair MMA favours it), but measured slower: config 2 variance 0.132 -> 0.139 ms, config 3
+// 7.73 -> 7.95 ms. Shared by the kernel and the host operand builder, which must agree.
 #ifndef GPM_PAIR_GRAN
 #define GPM_PAIR_GRAN 32  // column granularity of the triangle skip (a compile-time power of two)
+#endif
+#ifndef GPM_PAIR_BALANCE
+#define GPM_PAIR_BALANCE 0
 #endif
 GPM_HD void pair2_cols(int p, int kb, int n_pad, int* c0, int* nc) {
   const int npw = n_pad - 512 * p < 512 ? n_pad - 512 * p : 512;
   const int rel = 16 * kb - 512 * p;
+  int lo = -1, hi = 0;  // active range [lo, hi) of pass-relative TMEM columns
   for (int h = 0; h < 2; ++h) {
     int w = npw - 256 * h;
     w = w < 0 ? 0 : (w > 256 ? 256 : w);
     const int r = rel - 256 * h;
     const int c = r <= 0 ? 0 : (r & ~(GPM_PAIR_GRAN - 1));
     const int wr = (w + 31) & ~31;
-    c0[h] = c;
+    c0[h] = 256 * h + c;
     nc[h] = (w > 0 && c < w) ? wr - c : 0;
+    if (nc[h] > 0) {
+      if (lo < 0) lo = c0[h];
+      hi = c0[h] + nc[h];
+    }
   }
+#if GPM_PAIR_BALANCE
+  if (nc[0] > 0 && nc[1] > 0) {  // contiguous: half 0 then runs to column 256 (w = 256 there)
+    const int total = hi - lo;
+    const int na = ((total >> 1) + 31) & ~31;
+    c0[0] = lo;
+    nc[0] = na;
+    c0[1] = lo + na;
+    nc[1] = total - na;
+  }
+#endif
 }
 void build_tc_operand_f16x2(const double* ilt, int n, double sv, int n_pad, std::vector<uint16_t>& data,
                             std::vector<int4>& meta, int& n_pass2);

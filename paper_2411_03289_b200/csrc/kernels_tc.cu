@@ -1651,7 +1651,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::P2_THREADS, 1)
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 if (nc[h] == 0 || GPM_DIAG(dbg & 4)) continue;  // dbg 4: no MMA (commit only)
-                mma2_f16_3x(tmem_base + (uint32_t)(256 * h + c0[h]), ah, al, smem_desc(bo, H_SBO),
+                mma2_f16_3x(tmem_base + (uint32_t)c0[h], ah, al, smem_desc(bo, H_SBO),
                             smem_desc(bo + (uint32_t)nc[h] * KC, H_SBO), instr_desc_f16_m256(nc[h]), kb > 0 ? 1u : 0u);
                 bo += (uint32_t)nc[h] * KC * 2;
               }
@@ -2411,9 +2411,9 @@ void build_tc_operand(const double* ilt, int n, std::vector<float>& data, std::v
 // LBO 128 B). hfac = (sf2 / 2^-e)^2 undoes both scales on Σ D^2 in the epilogue.
 // Host: the CTA-pair operand (variance_f16x2_kernel). Same power-of-two scale and FP16
 // hi/lo split as build_tc_operand_f16; per (512-column pass p, 16-point chunk kb) one
-// record [CTA0 part | CTA1 part], each part = for each active half h (pair2_cols): hi then
-// lo block of nc[h]/2 rows x 16 FP16 (K-major canonical, SBO 256 B), CTA r holding columns
-// 512p + 256h + c0[h] + r·nc[h]/2 + [0, nc[h]/2). meta = {offset, 0, 0, part size} (FP16 units).
+// record [CTA0 part | CTA1 part], each part = for each MMA s of the chunk (pair2_cols): hi then
+// lo block of nc[s]/2 rows x 16 FP16 (K-major canonical, SBO 256 B), CTA r holding columns
+// 512p + c0[s] + r·nc[s]/2 + [0, nc[s]/2). meta = {offset, 0, 0, part size} (FP16 units).
 void build_tc_operand_f16x2(const double* ilt, int n, double sv, int n_pad, std::vector<uint16_t>& data,
                             std::vector<int4>& meta, int& n_pass2) {
   (void)sv;
@@ -2445,7 +2445,7 @@ void build_tc_operand_f16x2(const double* ilt, int n, double sv, int n_pad, std:
           uint16_t* hi = data.data() + o0;
           uint16_t* lo = hi + (size_t)rows * KC;
           for (int rr = 0; rr < rows; ++rr) {
-            const int j = 512 * p + 256 * h + c0[h] + r * rows + rr;
+            const int j = 512 * p + c0[h] + r * rows + rr;
             for (int k = 0; k < KC; ++k) {
               const int i = kb * KC + k;
               const double v = (i < n && j < n) ? ilt[(size_t)i * n + j] * scale : 0.0;
