@@ -175,8 +175,9 @@ def roofline_block(w, phase, steps, peaks, peaks_kind, var_path=3):
                 "tensor_issue_factor": 3 if var_path in (1, 3, 4) else 1})
     roll = {"kernel": "rollout_gp_kernel", "bound": "fp64", "peak": fp64, "unit": "TFLOP/s",
             "peak_kind": fp64_kind, "launch_ms": roll_ms, "flop_per_launch": units * 22 * n,
-            "binding_resource": "FP64 pipe + shared-memory wavefronts + issue (ncu at config2: FP64 51%, "
-                                "LSU shared 60%; 7 warps/SM, latency-bound; config5: FP64 60%)"}
+            "binding_resource": "FP64 pipe + shared-memory wavefronts + issue (ncu at config2, "
+                                "profiles/r02/r2y: FP64 50%, LSU shared 63%, issue 52%; 7 warps/SM, "
+                                "latency-bound)"}
     for k in (var, roll):
         k["achieved"] = k["flop_per_launch"] / (k["launch_ms"] / 1e3) / 1e12
         k["frac"] = k["achieved"] / k["peak"]
