@@ -1419,6 +1419,9 @@ __global__ void __launch_bounds__(tc::F16_THREADS, 1) variance_f16_kernel(const 
 // barrier counts both CTAs' producer warps (the peer's arrive remotely, `mapa`), its own copy
 // and the relayed peer copy; MMA completion is multicast to both CTAs' empty / tfull
 // barriers; both CTAs' epilogues arrive on the leader's tempty.
+#ifndef GPM_MMA_IFELECT
+#define GPM_MMA_IFELECT 1
+#endif
 namespace tc {
 constexpr int P2_PRODUCER_WARPS = 8;
 constexpr int P2_THREADS = 256 + 32 * P2_PRODUCER_WARPS;
@@ -1480,8 +1483,28 @@ __device__ __forceinline__ void mbar_wait_xp(uint32_t bar, uint32_t parity, int 
   mbar_wait_x(bar, parity);
   if ((threadIdx.x & 31) == 0) prof_add(slot, clock64() - t0, dbg);
 }
+__device__ __forceinline__ uint32_t elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .b32 rx;\n\t.reg .pred px;\n\t"
+      "elect.sync rx|px, 0xffffffff;\n\t"
+      "@px mov.s32 %0, 1;\n\t}"
+      : "+r"(pred));
+  return pred;
+}
 __device__ __forceinline__ void mma2_f16_3x(uint32_t d, uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl,
                                             uint32_t idesc, uint32_t acc) {
+#if GPM_MMA_IFELECT
+  if (elect_one())
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %3, %5, p;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %4, %5, 1;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %2, %3, %5, 1;\n\t}" ::"r"(d),
+        "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(acc)
+        : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred p, e;\n\t"
       "setp.ne.b32 p, %6, 0;\n\t"
@@ -1491,6 +1514,7 @@ __device__ __forceinline__ void mma2_f16_3x(uint32_t d, uint64_t ah, uint64_t al
       "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %2, %3, %5, 1;\n\t}" ::"r"(d),
       "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(acc)
       : "memory");
+#endif
 }
 __device__ __forceinline__ void mma2_commit_both(uint32_t bar) {  // arrive on `bar` in both CTAs
   asm volatile(
@@ -1547,7 +1571,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::P2_THREADS, 1)
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
   if (threadIdx.x == 0) trace_at(0, dbg);
-  const uint32_t rank = cluster_rank();
+  // warp-uniform in the compiler's view (a lane-0 shuffle): the leader's MMA branch then keeps its
+  // descriptors on the uniform datapath instead of a per-MMA elect / R2UR.BROADCAST waterfall
+  const uint32_t rank = __shfl_sync(0xffffffffu, cluster_rank(), 0);
   const bool leader = rank == 0;
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const long long n_super = (a.KT + 2 * M - 1) / (2 * M);
