@@ -139,14 +139,27 @@ __device__ __forceinline__ uint32_t instr_desc(int n) {
   // N>>3 at [17,23), M>>4 at [24,29)
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
-// Issued by the whole (converged) MMA warp; elect.sync lets exactly one lane issue.
+// One lane of a converged warp, as a C++ branch condition (CUTLASS's elect_one_sync). The
+// tcgen05.mma / tcgen05.commit statements below are issued inside `if (elect_one())` with no
+// predicate of their own: an elect predicate inside the asm made ptxas wrap every UTCHMMA in
+// an R2UR.BROADCAST / BRA.U.ANY waterfall (CTA-pair kernel at config 2: 0.133 vs 0.125 ms).
+__device__ __forceinline__ uint32_t elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .b32 rx;\n\t.reg .pred px;\n\t"
+      "elect.sync rx|px, 0xffffffff;\n\t"
+      "@px mov.s32 %0, 1;\n\t}"
+      : "+r"(pred));
+  return pred;
+}
+// Issued by the whole (converged) MMA warp; elect_one() picks the lane that issues.
 __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
                                          uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
+  if (elect_one())
+    asm volatile(
+      "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
       : "memory");
 }
@@ -156,31 +169,31 @@ __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b
 __device__ __forceinline__ void mma_block_3x(uint32_t d, uint64_t ahi, uint64_t alo, uint64_t bhi, uint64_t blo,
                                              uint32_t idesc0, uint32_t idesc1, uint32_t acc, int two) {
   if (two) {
-    asm volatile(
-        "{\n\t.reg .pred p, e;\n\t.reg .b32 d1;\n\t.reg .b64 bh1, bl1;\n\t"
-        "add.u32 d1, %0, 256;\n\t"
-        "add.s64 bh1, %3, 512;\n\t"
-        "add.s64 bl1, %4, 512;\n\t"
-        "setp.ne.b32 p, %7, 0;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %3, %5, p;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %4, %5, 1;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %5, 1;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], %1, bh1, %6, p;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], %1, bl1, %6, 1;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], %2, bh1, %6, 1;\n\t}" ::"r"(d),
-        "l"(ahi), "l"(alo), "l"(bhi), "l"(blo), "r"(idesc0), "r"(idesc1), "r"(acc)
-        : "memory");
+    if (elect_one())
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t.reg .b32 d1;\n\t.reg .b64 bh1, bl1;\n\t"
+          "add.u32 d1, %0, 256;\n\t"
+          "add.s64 bh1, %3, 512;\n\t"
+          "add.s64 bl1, %4, 512;\n\t"
+          "setp.ne.b32 p, %7, 0;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %3, %5, p;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %4, %5, 1;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %5, 1;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [d1], %1, bh1, %6, p;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [d1], %1, bl1, %6, 1;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [d1], %2, bh1, %6, 1;\n\t}" ::"r"(d),
+          "l"(ahi), "l"(alo), "l"(bhi), "l"(blo), "r"(idesc0), "r"(idesc1), "r"(acc)
+          : "memory");
   } else {
-    asm volatile(
-        "{\n\t.reg .pred p, e;\n\t"
-        "setp.ne.b32 p, %6, 0;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %3, %5, p;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %4, %5, 1;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %5, 1;\n\t}" ::"r"(d),
-        "l"(ahi), "l"(alo), "l"(bhi), "l"(blo), "r"(idesc0), "r"(acc)
-        : "memory");
+    if (elect_one())
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t"
+          "setp.ne.b32 p, %6, 0;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %3, %5, p;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %4, %5, 1;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %5, 1;\n\t}" ::"r"(d),
+          "l"(ahi), "l"(alo), "l"(bhi), "l"(blo), "r"(idesc0), "r"(acc)
+          : "memory");
   }
 }
 // One 16-point A chunk: two K=8 steps (B blocks b0/b1) x 3xTF32 x one or two
@@ -192,54 +205,54 @@ __device__ __forceinline__ void mma_chunk_3x(uint32_t d, uint64_t ahi, uint64_t 
                                              uint32_t acc, int two, uint32_t bar_b0, uint32_t bar_b1,
                                              uint32_t bar_a) {
   if (two) {
-    asm volatile(
-        "{\n\t.reg .pred p, e;\n\t.reg .b32 d1;\n\t.reg .b64 ah1, al1, x0, y0, x1, y1;\n\t"
-        "add.u32 d1, %0, 256;\n\t"
-        "add.s64 ah1, %1, 16;\n\t"
-        "add.s64 al1, %2, 16;\n\t"
-        "add.s64 x0, %3, 512;\n\t"
-        "add.s64 y0, %4, 512;\n\t"
-        "add.s64 x1, %5, 512;\n\t"
-        "add.s64 y1, %6, 512;\n\t"
-        "setp.ne.b32 p, %9, 0;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %3, %7, p;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %4, %7, 1;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %7, 1;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], %1, x0, %8, p;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], %1, y0, %8, 1;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], %2, x0, %8, 1;\n\t"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%10];\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah1, %5, %7, 1;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah1, %6, %7, 1;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al1, %5, %7, 1;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], ah1, x1, %8, 1;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], ah1, y1, %8, 1;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], al1, x1, %8, 1;\n\t"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%11];\n\t"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%12];\n\t}" ::"r"(d),
-        "l"(ahi), "l"(alo), "l"(bh0), "l"(bl0), "l"(bh1), "l"(bl1), "r"(idesc0), "r"(idesc1), "r"(acc),
-        "r"(bar_b0), "r"(bar_b1), "r"(bar_a)
-        : "memory");
+    if (elect_one())
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t.reg .b32 d1;\n\t.reg .b64 ah1, al1, x0, y0, x1, y1;\n\t"
+          "add.u32 d1, %0, 256;\n\t"
+          "add.s64 ah1, %1, 16;\n\t"
+          "add.s64 al1, %2, 16;\n\t"
+          "add.s64 x0, %3, 512;\n\t"
+          "add.s64 y0, %4, 512;\n\t"
+          "add.s64 x1, %5, 512;\n\t"
+          "add.s64 y1, %6, 512;\n\t"
+          "setp.ne.b32 p, %9, 0;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %3, %7, p;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %4, %7, 1;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %7, 1;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [d1], %1, x0, %8, p;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [d1], %1, y0, %8, 1;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [d1], %2, x0, %8, 1;\n\t"
+          "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%10];\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [%0], ah1, %5, %7, 1;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [%0], ah1, %6, %7, 1;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [%0], al1, %5, %7, 1;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [d1], ah1, x1, %8, 1;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [d1], ah1, y1, %8, 1;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [d1], al1, x1, %8, 1;\n\t"
+          "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%11];\n\t"
+          "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%12];\n\t}" ::"r"(d),
+          "l"(ahi), "l"(alo), "l"(bh0), "l"(bl0), "l"(bh1), "l"(bl1), "r"(idesc0), "r"(idesc1), "r"(acc),
+          "r"(bar_b0), "r"(bar_b1), "r"(bar_a)
+          : "memory");
   } else {
-    asm volatile(
-        "{\n\t.reg .pred p, e;\n\t.reg .b64 ah1, al1;\n\t"
-        "add.s64 ah1, %1, 16;\n\t"
-        "add.s64 al1, %2, 16;\n\t"
-        "setp.ne.b32 p, %8, 0;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %3, %7, p;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %4, %7, 1;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %7, 1;\n\t"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%9];\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah1, %5, %7, 1;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah1, %6, %7, 1;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al1, %5, %7, 1;\n\t"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%10];\n\t"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%11];\n\t}" ::"r"(d),
-        "l"(ahi), "l"(alo), "l"(bh0), "l"(bl0), "l"(bh1), "l"(bl1), "r"(idesc0), "r"(acc), "r"(bar_b0),
-        "r"(bar_b1), "r"(bar_a)
-        : "memory");
+    if (elect_one())
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t.reg .b64 ah1, al1;\n\t"
+          "add.s64 ah1, %1, 16;\n\t"
+          "add.s64 al1, %2, 16;\n\t"
+          "setp.ne.b32 p, %8, 0;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %3, %7, p;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %4, %7, 1;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %7, 1;\n\t"
+          "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%9];\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [%0], ah1, %5, %7, 1;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [%0], ah1, %6, %7, 1;\n\t"
+          "tcgen05.mma.cta_group::1.kind::tf32 [%0], al1, %5, %7, 1;\n\t"
+          "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%10];\n\t"
+          "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%11];\n\t}" ::"r"(d),
+          "l"(ahi), "l"(alo), "l"(bh0), "l"(bl0), "l"(bh1), "l"(bl1), "r"(idesc0), "r"(acc), "r"(bar_b0),
+          "r"(bar_b1), "r"(bar_a)
+          : "memory");
   }
 }
 // Two M tiles (TMEM columns d and d + dt) share one 16-point B chunk of <= 256
@@ -248,30 +261,30 @@ __device__ __forceinline__ void mma_chunk_pair_3x(uint32_t d, uint32_t dt, uint6
                                                   uint64_t a1hi, uint64_t a1lo, uint64_t bh0, uint64_t bl0,
                                                   uint64_t bh1, uint64_t bl1, uint32_t idesc, uint32_t acc,
                                                   uint32_t bar_b0, uint32_t bar_b1, uint32_t bar_a) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t.reg .b32 d1;\n\t.reg .b64 x0h, x0l, x1h, x1l;\n\t"
+  if (elect_one())
+    asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b32 d1;\n\t.reg .b64 x0h, x0l, x1h, x1l;\n\t"
       "add.u32 d1, %0, %1;\n\t"
       "add.s64 x0h, %2, 16;\n\t"
       "add.s64 x0l, %3, 16;\n\t"
       "add.s64 x1h, %4, 16;\n\t"
       "add.s64 x1l, %5, 16;\n\t"
       "setp.ne.b32 p, %11, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %6, %10, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %7, %10, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %3, %6, %10, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], %4, %6, %10, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], %4, %7, %10, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], %5, %6, %10, 1;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%12];\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], x0h, %8, %10, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], x0h, %9, %10, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], x0l, %8, %10, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], x1h, %8, %10, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], x1h, %9, %10, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], x1l, %8, %10, 1;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%13];\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%14];\n\t}" ::"r"(d),
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %6, %10, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %7, %10, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %3, %6, %10, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [d1], %4, %6, %10, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [d1], %4, %7, %10, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [d1], %5, %6, %10, 1;\n\t"
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%12];\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], x0h, %8, %10, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], x0h, %9, %10, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], x0l, %8, %10, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [d1], x1h, %8, %10, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [d1], x1h, %9, %10, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [d1], x1l, %8, %10, 1;\n\t"
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%13];\n\t"
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%14];\n\t}" ::"r"(d),
       "r"(dt), "l"(a0hi), "l"(a0lo), "l"(a1hi), "l"(a1lo), "l"(bh0), "l"(bl0), "l"(bh1), "l"(bl1), "r"(idesc),
       "r"(acc), "r"(bar_b0), "r"(bar_b1), "r"(bar_a)
       : "memory");
@@ -282,28 +295,28 @@ __device__ __forceinline__ void mma_stage_pair_3x(uint32_t d, uint32_t dt, uint6
                                                   uint64_t a1hi, uint64_t a1lo, uint64_t bh0, uint64_t bl0,
                                                   uint64_t bh1, uint64_t bl1, uint32_t idesc, uint32_t acc,
                                                   uint32_t bar) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t.reg .b32 d1;\n\t.reg .b64 x0h, x0l, x1h, x1l;\n\t"
+  if (elect_one())
+    asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b32 d1;\n\t.reg .b64 x0h, x0l, x1h, x1l;\n\t"
       "add.u32 d1, %0, %1;\n\t"
       "add.s64 x0h, %2, 16;\n\t"
       "add.s64 x0l, %3, 16;\n\t"
       "add.s64 x1h, %4, 16;\n\t"
       "add.s64 x1l, %5, 16;\n\t"
       "setp.ne.b32 p, %11, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %6, %10, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %7, %10, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %3, %6, %10, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], %4, %6, %10, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], %4, %7, %10, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], %5, %6, %10, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], x0h, %8, %10, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], x0h, %9, %10, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], x0l, %8, %10, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], x1h, %8, %10, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], x1h, %9, %10, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], x1l, %8, %10, 1;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%12];\n\t}" ::"r"(d),
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %6, %10, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %7, %10, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %3, %6, %10, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [d1], %4, %6, %10, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [d1], %4, %7, %10, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [d1], %5, %6, %10, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], x0h, %8, %10, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], x0h, %9, %10, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], x0l, %8, %10, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [d1], x1h, %8, %10, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [d1], x1h, %9, %10, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [d1], x1l, %8, %10, 1;\n\t"
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%12];\n\t}" ::"r"(d),
       "r"(dt), "l"(a0hi), "l"(a0lo), "l"(a1hi), "l"(a1lo), "l"(bh0), "l"(bl0), "l"(bh1), "l"(bl1), "r"(idesc),
       "r"(acc), "r"(bar)
       : "memory");
@@ -311,27 +324,27 @@ __device__ __forceinline__ void mma_stage_pair_3x(uint32_t d, uint32_t dt, uint6
 __device__ __forceinline__ void mma_stage_single_3x(uint32_t d, uint64_t ahi, uint64_t alo, uint64_t bh0,
                                                     uint64_t bl0, uint64_t bh1, uint64_t bl1, uint32_t idesc,
                                                     uint32_t acc, uint32_t bar) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t.reg .b64 ah1, al1;\n\t"
+  if (elect_one())
+    asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 ah1, al1;\n\t"
       "add.s64 ah1, %1, 16;\n\t"
       "add.s64 al1, %2, 16;\n\t"
       "setp.ne.b32 p, %8, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %3, %7, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %4, %7, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %7, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah1, %5, %7, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah1, %6, %7, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al1, %5, %7, 1;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%9];\n\t}" ::"r"(d),
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %3, %7, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %4, %7, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %7, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], ah1, %5, %7, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], ah1, %6, %7, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], al1, %5, %7, 1;\n\t"
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%9];\n\t}" ::"r"(d),
       "l"(ahi), "l"(alo), "l"(bh0), "l"(bl0), "l"(bh1), "l"(bl1), "r"(idesc), "r"(acc), "r"(bar)
       : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
-  asm volatile(
-      "{\n\t.reg .pred e;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
+  if (elect_one())
+    asm volatile(
+      "{\n\t"
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
       : "memory");
 }
 __device__ __forceinline__ float exp2f_approx(float x) {  // MUFU.EX2, ~2 ulp
@@ -1026,59 +1039,59 @@ __device__ __forceinline__ uint32_t instr_desc_f16(int n) {
 __device__ __forceinline__ void mma_f16_pair_3x(uint32_t d, uint32_t dt, uint64_t a0h, uint64_t a0l, uint64_t a1h,
                                                 uint64_t a1l, uint64_t bh, uint64_t bl, uint32_t idesc, uint32_t acc,
                                                 uint32_t bar) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t.reg .b32 d1;\n\t"
+  if (elect_one())
+    asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b32 d1;\n\t"
       "add.u32 d1, %0, %1;\n\t"
       "setp.ne.b32 p, %9, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %6, %8, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %7, %8, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %3, %6, %8, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [d1], %4, %6, %8, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [d1], %4, %7, %8, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [d1], %5, %6, %8, 1;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%10];\n\t}" ::"r"(d),
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %6, %8, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %7, %8, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %3, %6, %8, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [d1], %4, %6, %8, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [d1], %4, %7, %8, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [d1], %5, %6, %8, 1;\n\t"
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%10];\n\t}" ::"r"(d),
       "r"(dt), "l"(a0h), "l"(a0l), "l"(a1h), "l"(a1l), "l"(bh), "l"(bl), "r"(idesc), "r"(acc), "r"(bar)
       : "memory");
 }
 __device__ __forceinline__ void mma_f16_pair_3x_nc(uint32_t d, uint32_t dt, uint64_t a0h, uint64_t a0l, uint64_t a1h,
                                                    uint64_t a1l, uint64_t bh, uint64_t bl, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t.reg .b32 d1;\n\t"
+  if (elect_one())
+    asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b32 d1;\n\t"
       "add.u32 d1, %0, %1;\n\t"
       "setp.ne.b32 p, %9, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %6, %8, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %7, %8, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %3, %6, %8, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [d1], %4, %6, %8, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [d1], %4, %7, %8, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [d1], %5, %6, %8, 1;\n\t}" ::"r"(d),
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %6, %8, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %7, %8, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %3, %6, %8, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [d1], %4, %6, %8, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [d1], %4, %7, %8, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [d1], %5, %6, %8, 1;\n\t}" ::"r"(d),
       "r"(dt), "l"(a0h), "l"(a0l), "l"(a1h), "l"(a1l), "l"(bh), "l"(bl), "r"(idesc), "r"(acc)
       : "memory");
 }
 __device__ __forceinline__ void mma_f16_single_3x_nc(uint32_t d, uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl,
                                                      uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
+  if (elect_one())
+    asm volatile(
+      "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %6, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %3, %5, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %4, %5, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %3, %5, 1;\n\t}" ::"r"(d),
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %3, %5, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %4, %5, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %3, %5, 1;\n\t}" ::"r"(d),
       "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(acc)
       : "memory");
 }
 __device__ __forceinline__ void mma_f16_single_3x(uint32_t d, uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl,
                                                   uint32_t idesc, uint32_t acc, uint32_t bar) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
+  if (elect_one())
+    asm volatile(
+      "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %6, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %3, %5, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %4, %5, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %3, %5, 1;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n\t}" ::"r"(d),
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %3, %5, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %4, %5, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %3, %5, 1;\n\t"
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n\t}" ::"r"(d),
       "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(acc), "r"(bar)
       : "memory");
 }
@@ -1419,9 +1432,6 @@ __global__ void __launch_bounds__(tc::F16_THREADS, 1) variance_f16_kernel(const 
 // barrier counts both CTAs' producer warps (the peer's arrive remotely, `mapa`), its own copy
 // and the relayed peer copy; MMA completion is multicast to both CTAs' empty / tfull
 // barriers; both CTAs' epilogues arrive on the leader's tempty.
-#ifndef GPM_MMA_IFELECT
-#define GPM_MMA_IFELECT 1
-#endif
 namespace tc {
 constexpr int P2_PRODUCER_WARPS = 8;
 constexpr int P2_THREADS = 256 + 32 * P2_PRODUCER_WARPS;
@@ -1483,18 +1493,8 @@ __device__ __forceinline__ void mbar_wait_xp(uint32_t bar, uint32_t parity, int 
   mbar_wait_x(bar, parity);
   if ((threadIdx.x & 31) == 0) prof_add(slot, clock64() - t0, dbg);
 }
-__device__ __forceinline__ uint32_t elect_one() {
-  uint32_t pred = 0;
-  asm volatile(
-      "{\n\t.reg .b32 rx;\n\t.reg .pred px;\n\t"
-      "elect.sync rx|px, 0xffffffff;\n\t"
-      "@px mov.s32 %0, 1;\n\t}"
-      : "+r"(pred));
-  return pred;
-}
 __device__ __forceinline__ void mma2_f16_3x(uint32_t d, uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl,
                                             uint32_t idesc, uint32_t acc) {
-#if GPM_MMA_IFELECT
   if (elect_one())
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -1504,24 +1504,13 @@ __device__ __forceinline__ void mma2_f16_3x(uint32_t d, uint64_t ah, uint64_t al
         "tcgen05.mma.cta_group::2.kind::f16 [%0], %2, %3, %5, 1;\n\t}" ::"r"(d),
         "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(acc)
         : "memory");
-#else
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
-      "setp.ne.b32 p, %6, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %3, %5, p;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %4, %5, 1;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %2, %3, %5, 1;\n\t}" ::"r"(d),
-      "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(acc)
-      : "memory");
-#endif
 }
 __device__ __forceinline__ void mma2_commit_both(uint32_t bar) {  // arrive on `bar` in both CTAs
-  asm volatile(
-      "{\n\t.reg .pred e;\n\t.reg .b16 m;\n\t"
+  if (elect_one())
+    asm volatile(
+      "{\n\t.reg .b16 m;\n\t"
       "mov.b16 m, 3;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
           bar)
       : "memory");
 }
