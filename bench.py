@@ -157,10 +157,10 @@ def roofline_block(w, phase, steps, peaks, peaks_kind, var_path=3):
     # 3xFP16 / 3xTF32 issue three tensor products per algorithmic MAC; FP16 runs at the bf16
     # dense rate, TF32 at half of it
     if var_path in (3, 4):
-        # the CTA-pair kernel (tcgen05 cta_group::2) is path 4, and path 3's choice at n_pad >= 1024
-        # or at <= 16 super-tiles (256 queries) per CTA pair (kernels_tc.cu launch_tc_variance)
+        # the CTA-pair kernel (tcgen05 cta_group::2) is path 4, and path 3's choice at n_pad > 256
+        # (kernels_tc.cu launch_tc_variance)
         n_pad = (n + 15) // 16 * 16
-        pair = var_path == 4 or n_pad >= 1024 or (n_pad > 256 and -(-units // 256) <= 16 * 74)
+        pair = var_path == 4 or n_pad > 256
         var = {"kernel": "variance_f16x2_kernel" if pair else "variance_f16_kernel", "bound": "tensor",
                "peak": bf16, "unit": "TFLOP/s",
                "peak_kind": f"{peaks_kind} fp16 dense = bf16 dense burst (MEASURED_PEAKS.json)"}

@@ -2208,14 +2208,12 @@ cudaError_t launch_tc_variance(const VarianceArgs& a, int mode, cudaStream_t st)
     const char* e = getenv("GPMPPI_TC_DEBUG");
     dbg_h = e ? atoi(e) : 0;
   }
-  // The CTA-pair kernel: mode 3, or mode 2 when (measured; both kernels with
-  // two chunks per ring stage) it is ahead:
-  //  - n_pad >= 1024: its 512-column passes regenerate k* 320 instead of 576 times per tile at
-  //    n = 2048, and its stages still fit twice-deep (config 3: 8.40 -> 7.85 ms);
-  //  - short launches (<= 16 super-tiles per CTA pair): one 128-row tile per SM per step
-  //    balances the tail better than the single-CTA kernel's two-tile units (config 2:
-  //    139 -> 129 us); at long launches the two are level (config 5, 138 super-tiles per
-  //    pair: 1.74 single vs 1.76 ms pair).
+  // The CTA-pair kernel: mode 3, or mode 2 whenever n_pad > 256 (measured, with
+  // both kernels issuing their MMAs under a C++ elect_one() branch): config 5 1.648 vs 1.720 ms,
+  // config 4 26.4 vs 27.1 ms; configs 2 and 3 already ran the pair (0.129 vs 0.139 ms, 7.85 vs
+  // 8.40 ms before that change). Its 512-column passes regenerate k* less often and one
+  // 128-row tile per SM per step balances the tail.
+  // n_pad <= 256 keeps the single-CTA kernel (two tiles share each B chunk there).
   // GPMPPI_VAR2CTA=0/1 forces the choice for mode 2 (A/B).
   static int pair_env = -2;
   if (pair_env == -2) {
@@ -2228,8 +2226,7 @@ cudaError_t launch_tc_variance(const VarianceArgs& a, int mode, cudaStream_t st)
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const long long supers_all = (a.KT + 2 * tc::M - 1) / (2 * tc::M);
-  const bool pair_auto = a.g.tc_npad >= 1024 || (a.g.tc_npad > 256 && supers_all <= 16LL * (dev_sms / 2));
+  const bool pair_auto = a.g.tc_npad > 256;
   const bool pair = mode == 3 || (mode == 2 && (pair_env == 1 || (pair_env < 0 && pair_auto)));
   static int cps_env = -1;  // GPMPPI_F16_CPS=1/2 forces the chunks per ring stage (A/B)
   if (cps_env < 0) {

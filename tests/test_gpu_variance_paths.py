@@ -57,8 +57,8 @@ def test_pair_variance_shapes(n):
 
 
 def test_path3_kernel_choice_both_regimes():
-    """Path 3 runs the CTA-pair kernel on short launches and the single-CTA kernel on long ones
-    (> 16 super-tiles of 256 queries per CTA pair, n_pad < 1024): both within the path bound."""
+    """Path 3 on a short and a long launch (3000 queries; > 16 super-tiles of 256 queries per
+    CTA pair): within the path bound either way (it runs the CTA-pair kernel for n_pad > 256)."""
     import paper_2411_03289_b200 as G
     from paper_2411_03289_b200 import workloads as W
     X, Y, K = W.gp_training_set(512, 1, seed=5)
@@ -73,3 +73,41 @@ def test_path3_kernel_choice_both_regimes():
         v4 = m.variance_batch(q32, 4)[:, 0]
         assert np.abs(v3 - v64[:, 0]).max() <= TOL[3], S
         assert np.abs(v4 - v64[:, 0]).max() <= TOL[4], S
+
+
+_SINGLE = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2411_03289_b200 as G
+from paper_2411_03289_b200 import workloads as W
+TOL = {tol!r}
+for n in (300, 513, 1100, 2048):
+    X, Y, K = W.gp_training_set(n, 1, seed=n + 3)
+    m = G.GpModel.fit(X, Y, K)
+    rng = np.random.default_rng(n)
+    for S in (1, 257, 3000):
+        q = np.column_stack([rng.uniform(-0.5, 2, S), rng.uniform(-2, 2, S),
+                             rng.uniform(-0.5, 2, S), rng.uniform(-2, 2, S)])
+        q32 = q.astype(np.float32).astype(np.float64)
+        _, v64 = m.predict_batch(q32)
+        v3 = m.variance_batch(q32, 3)[:, 0]
+        v4 = m.variance_batch(q32, 4)[:, 0]
+        assert np.abs(v3 - v64[:, 0]).max() <= TOL, (n, S, np.abs(v3 - v64[:, 0]).max())
+        assert np.abs(v3 - v4).max() <= 1e-8, (n, S)
+print("ok")
+"""
+
+
+def test_single_cta_kernel_above_256_points(tmp_path):
+    """The single-CTA 3xFP16 kernel (path 3 with GPMPPI_VAR2CTA=0; the default picks the CTA
+    pair for n_pad > 256) against FP64 and against the pair kernel, n = 300 ... 2048. The switch
+    is read once per process, hence a subprocess."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "single.py"
+    script.write_text(_SINGLE.format(root=root, tol=TOL[3]))
+    r = subprocess.run([sys.executable, str(script)], env={**os.environ, "GPMPPI_VAR2CTA": "0"},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-3000:]
