@@ -1109,6 +1109,11 @@ __device__ __forceinline__ unsigned long long fadd2(unsigned long long a, unsign
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
+__device__ __forceinline__ unsigned long long fsub2(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
 __device__ __forceinline__ uint32_t half2_bits(__half2 h) {
   uint32_t u;
   memcpy(&u, &h, 4);
@@ -1433,7 +1438,17 @@ __global__ void __launch_bounds__(tc::F16_THREADS, 1) variance_f16_kernel(const 
 // and the relayed peer copy; MMA completion is multicast to both CTAs' empty / tfull
 // barriers; both CTAs' epilogues arrive on the leader's tempty.
 namespace tc {
-constexpr int P2_PRODUCER_WARPS = 8;
+#ifndef GPM_P2_PRODUCER_WARPS
+#define GPM_P2_PRODUCER_WARPS 8
+#endif
+constexpr int P2_PRODUCER_WARPS = GPM_P2_PRODUCER_WARPS;  // 8: a lane owns 2 rows x 4 points; 16: 1 row
+constexpr int P2_RPL = 16 / P2_PRODUCER_WARPS;            // rows per producer lane
+#ifndef GPM_P2_ZHOIST
+#define GPM_P2_ZHOIST 1
+#endif
+#ifndef GPM_P2_FADD2
+#define GPM_P2_FADD2 1
+#endif
 constexpr int P2_THREADS = 256 + 32 * P2_PRODUCER_WARPS;
 constexpr int P2_A_BYTES = 2 * H_TILE_BYTES;         // this CTA's 128 rows: hi, lo
 constexpr int P2_B_BYTES = 2 * 2 * (M / 1) * KC * 2;  // two halves x (hi, lo) x <= 128 rows
@@ -1697,10 +1712,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::P2_THREADS, 1)
     Ring r(S);
     for (long long st = sb; st < se; ++st) {
       if (pw == 0 && lane == 0 && st - sb < 10) trace_at(36 + (int)(st - sb), dbg);
-      float qq[2][5];
+      float qq[P2_RPL][5];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const long long q = st * (2 * M) + (long long)rank * M + pw * 16 + 8 * j + qi;
+      for (int j = 0; j < P2_RPL; ++j) {
+        const long long q = st * (2 * M) + (long long)rank * M + pw * (8 * P2_RPL) + 8 * j + qi;
         const bool valid = q < a.KT;
         const float4 qv = valid ? a.queries[q] : make_float4(0.f, 0.f, 0.f, 0.f);
         qq[j][0] = qv.x / (float)G.ls[0];
@@ -1711,9 +1726,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::P2_THREADS, 1)
                                           qq[j][3] * qq[j][3])
                          : -1e30f;
       }
-      unsigned long long qp[2][5];
+      unsigned long long qp[P2_RPL][5];
 #pragma unroll
-      for (int j = 0; j < 2; ++j)
+      for (int j = 0; j < P2_RPL; ++j)
 #pragma unroll
         for (int c = 0; c < 5; ++c) qp[j][c] = f2_pack(qq[j][c], qq[j][c]);
       for (int p = 0; p < n_pass; ++p) {
@@ -1731,23 +1746,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::P2_THREADS, 1)
             }
             continue;
           }
+#if GPM_P2_ZHOIST
+          float4 zc[CPS][5];  // every chunk's point terms ahead of the stage's stores
+#pragma unroll
+          for (int c = 0; c < CPS; ++c) {
+            const int i0 = min(kb0 + c, nk - 1) * KC + pg * 4;
+#pragma unroll
+            for (int d = 0; d < 5; ++d) zc[c][d] = *reinterpret_cast<const float4*>(zs + d * n_pad + i0);
+          }
+#endif
 #pragma unroll
           for (int c = 0; c < CPS; ++c) {
           const int kb = kb0 + c;
           if (kb >= nk) break;
           unsigned char* ahi = stg + (size_t)r.s * STAGE + (size_t)c * P2_A_BYTES;
           unsigned char* alo = ahi + H_TILE_BYTES;
+#if GPM_P2_ZHOIST
+          const float4 z0 = zc[c][0], z1 = zc[c][1], z2 = zc[c][2], z3 = zc[c][3], zq = zc[c][4];
+#else
           const int i0 = kb * KC + pg * 4;
           const float4 z0 = *reinterpret_cast<const float4*>(zs + i0);
           const float4 z1 = *reinterpret_cast<const float4*>(zs + n_pad + i0);
           const float4 z2 = *reinterpret_cast<const float4*>(zs + 2 * n_pad + i0);
           const float4 z3 = *reinterpret_cast<const float4*>(zs + 3 * n_pad + i0);
           const float4 zq = *reinterpret_cast<const float4*>(zs + 4 * n_pad + i0);
+#endif
           const unsigned long long zp[2][5] = {
               {f2_pack(z0.x, z0.y), f2_pack(z1.x, z1.y), f2_pack(z2.x, z2.y), f2_pack(z3.x, z3.y), f2_pack(zq.x, zq.y)},
               {f2_pack(z0.z, z0.w), f2_pack(z1.z, z1.w), f2_pack(z2.z, z2.w), f2_pack(z3.z, z3.w), f2_pack(zq.z, zq.w)}};
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
+          for (int j = 0; j < P2_RPL; ++j) {
             float kv[4];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -1761,10 +1789,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::P2_THREADS, 1)
             }
             const __half2 h01 = __floats2half2_rn(kv[0], kv[1]), h23 = __floats2half2_rn(kv[2], kv[3]);
             const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+#if GPM_P2_FADD2  // residuals as packed FP32 pairs (exact: Sterbenz), one instruction per two
+            const unsigned long long r01 = fsub2(f2_pack(kv[0], kv[1]), f2_pack(f01.x, f01.y));
+            const unsigned long long r23 = fsub2(f2_pack(kv[2], kv[3]), f2_pack(f23.x, f23.y));
+            const __half2 l01 = __floats2half2_rn(__uint_as_float((uint32_t)r01), __uint_as_float((uint32_t)(r01 >> 32)));
+            const __half2 l23 = __floats2half2_rn(__uint_as_float((uint32_t)r23), __uint_as_float((uint32_t)(r23 >> 32)));
+#else
             const __half2 l01 = __floats2half2_rn(kv[0] - f01.x, kv[1] - f01.y);
             const __half2 l23 = __floats2half2_rn(kv[2] - f23.x, kv[3] - f23.y);
+#endif
             // row m = pw*16 + 8j + qi, points 4pg..4pg+3 (K-major canonical, as variance_f16_kernel)
-            const int off = (2 * pw + j) * H_SBO + (pg >> 1) * 128 + qi * 16 + (pg & 1) * 8;
+            const int off = (P2_RPL * pw + j) * H_SBO + (pg >> 1) * 128 + qi * 16 + (pg & 1) * 8;
             *reinterpret_cast<uint2*>(ahi + off) = make_uint2(half2_bits(h01), half2_bits(h23));
             *reinterpret_cast<uint2*>(alo + off) = make_uint2(half2_bits(l01), half2_bits(l23));
           }
