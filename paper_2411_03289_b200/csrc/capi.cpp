@@ -356,6 +356,13 @@ gpmppi_model* build_model(const double* X, const double* Y, int64_t n64, int64_t
     M->dev.m = m;
     M->dev.G = (int)M->groups.size();
     M->dev.ns = (n + 1) & ~1;
+    M->dev.fold_zn = 1;
+    for (const HostGroup& G : M->groups) {
+      if (!(std::fabs(std::log(G.kernel[0])) <= 50.0)) M->dev.fold_zn = 0;
+      for (int j = 0; j < n; ++j)
+        if (!(std::fabs(G.aug[(size_t)j * 6 + 5]) <= 600.0)) M->dev.fold_zn = 0;
+    }
+    if (const char* e = getenv("GPMPPI_FOLD_ZN")) M->dev.fold_zn = M->dev.fold_zn && atoi(e) != 0;
     for (int gi = 0; gi < M->dev.G; ++gi) {
       const HostGroup& G = M->groups[gi];
       gpm::GroupDev& D = M->dev.g[gi];

@@ -37,6 +37,10 @@ struct GroupDev {
 struct ModelDev {
   int n, m, G;
   int ns;  // stride of the pts SoA arrays: n rounded up to even (padded points contribute 0)
+  // 1 when every real point's exponent row zn (= -|z|^2/2 + ln sv) lies in [-600, 600] and
+  // |ln sv| <= 50: the rollout then folds exp(zn_j) into its combined alpha rows and forms
+  // the kernel-row exponent without zn (q·z + qn <= |z|^2/2 stays far from FP64 overflow)
+  int fold_zn;
   GroupDev g[kMaxGroups];
 };
 

@@ -138,6 +138,11 @@ GPM_D void load_robot_smem(const RolloutArgs& a, const SmemView& v, int b) {
             }
           }
         }
+        if (a.model.fold_zn) {  // exp(zn_j) folded into the combined rows (ModelDev::fold_zn)
+          const double ez = exp(__ldg(G.pts + (size_t)4 * ns + j));
+          s0 *= ez;
+          s1 *= ez;
+        }
         gp[5 * ns + j] = s0;
         gp[6 * ns + j] = s1;
       }
@@ -362,7 +367,7 @@ GPM_D void rollout_phase2(const RolloutArgs& a, const SmemView& sv, const TaskDe
 #ifndef GPM_EXP_PRESCALE
 #define GPM_EXP_PRESCALE 1
 #endif
-template <int LPS, int SPG>
+template <int LPS, int SPG, bool FOLD>
 __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const RolloutArgs a) {
   if (threadIdx.x == 0) tl_stamp(1);
   pdl_trigger();  // single wave: the variance grid may be scheduled (it waits for this grid)
@@ -542,13 +547,17 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
 #pragma unroll(kRollUnroll / SPG)
         for (int jp = gl; jp < half; jp += LPS) {
           // gp.cpp:177-179: k*_j = exp(q_aug · inputs_aug_j)
-          const double2 a0 = z0[jp], a1 = z1[jp], a2 = z2[jp], a3 = z3[jp], an = zn[jp];
+          const double2 a0 = z0[jp], a1 = z1[jp], a2 = z2[jp], a3 = z3[jp];
+          const double2 an = FOLD ? make_double2(0.0, 0.0) : zn[jp];
           const double2 av = cv[jp], aw = cw[jp];
 #pragma unroll
           for (int j = 0; j < SPG; ++j) {
-            // q·z + (qn + zn) as one DADD and four DFMAs (gp.cpp:177-179)
-            const double d0 = fma(q0[j], a0.x, fma(q1[j], a1.x, fma(q2[j], a2.x, fma(q3[j], a3.x, qn[j] + an.x))));
-            const double d1 = fma(q0[j], a0.y, fma(q1[j], a1.y, fma(q2[j], a2.y, fma(q3[j], a3.y, qn[j] + an.y))));
+            // q·z + (qn + zn) as one DADD and four DFMAs (gp.cpp:177-179); with FOLD the zn
+            // factor rides in the alpha rows and the exponent is q·z + qn (four DFMAs, one
+            // load fewer per point pair)
+            const double e0 = FOLD ? qn[j] : qn[j] + an.x, e1 = FOLD ? qn[j] : qn[j] + an.y;
+            const double d0 = fma(q0[j], a0.x, fma(q1[j], a1.x, fma(q2[j], a2.x, fma(q3[j], a3.x, e0))));
+            const double d1 = fma(q0[j], a0.y, fma(q1[j], a1.y, fma(q2[j], a2.y, fma(q3[j], a3.y, e1))));
 #if GPM_EXP_PRESCALE  // d = 32/ln2 · (q·z + qn + zn): the reduction is one DADD (exp_tab_t)
             const double k0 = exp_tab_t(d0, sv.etab), k1 = exp_tab_t(d1, sv.etab);
 #else
@@ -831,12 +840,22 @@ cudaError_t launch_rollout(const RolloutArgs& a, int num_sms, cudaStream_t st) {
     const long long cap = (long long)GPM_ROLLOUT_MINB * num_sms;
     const long long blocks = items < cap ? items : cap;
     using KF = void (*)(const RolloutArgs);
-    KF table[2][4] = {{rollout_gp_kernel<4, 1>, rollout_gp_kernel<8, 1>, rollout_gp_kernel<16, 1>, rollout_gp_kernel<32, 1>},
-                      {rollout_gp_kernel<4, 1>, rollout_gp_kernel<8, 2>, rollout_gp_kernel<16, 2>, rollout_gp_kernel<32, 2>}};
+    // [fold zn][spg 1/2][lps]
+    KF table[2][2][4] = {
+        {{rollout_gp_kernel<4, 1, false>, rollout_gp_kernel<8, 1, false>, rollout_gp_kernel<16, 1, false>,
+          rollout_gp_kernel<32, 1, false>},
+         {rollout_gp_kernel<4, 1, false>, rollout_gp_kernel<8, 2, false>, rollout_gp_kernel<16, 2, false>,
+          rollout_gp_kernel<32, 2, false>}},
+        {{rollout_gp_kernel<4, 1, true>, rollout_gp_kernel<8, 1, true>, rollout_gp_kernel<16, 1, true>,
+          rollout_gp_kernel<32, 1, true>},
+         {rollout_gp_kernel<4, 1, true>, rollout_gp_kernel<8, 2, true>, rollout_gp_kernel<16, 2, true>,
+          rollout_gp_kernel<32, 2, true>}}};
     const int li = lps == 4 ? 0 : lps == 8 ? 1 : lps == 16 ? 2 : 3;
+    const int fz = a.model.fold_zn ? 1 : 0;
     // spg 4: one 32-lane group per warp carrying four samples (no duplicate addresses inside
     // a warp's Z/alpha loads, a quarter of the LDS instructions of the 8-lane layout)
-    KF kern = spg == 4 ? rollout_gp_kernel<32, 4> : table[spg == 2 ? 1 : 0][li];
+    KF kern = spg == 4 ? (fz ? rollout_gp_kernel<32, 4, true> : rollout_gp_kernel<32, 4, false>)
+                       : table[fz][spg == 2 ? 1 : 0][li];
     RolloutArgs ra = a;
     const size_t smem_u = rollout_launch_smem(a, &ra.scratch_smem);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_u);
