@@ -176,7 +176,7 @@ def roofline_block(w, phase, steps, peaks, peaks_kind, var_path=3):
     roll = {"kernel": "rollout_gp_kernel", "bound": "fp64", "peak": fp64, "unit": "TFLOP/s",
             "peak_kind": fp64_kind, "launch_ms": roll_ms, "flop_per_launch": units * 22 * n,
             "binding_resource": "FP64 pipe + shared-memory wavefronts + issue (ncu at config2, "
-                                "profiles/r02/r2y: FP64 50%, LSU shared 63%, issue 52%; 7 warps/SM, "
+                                "profiles/r02/r2f: FP64 48%, LSU shared 58%, issue 51%; 7 warps/SM, "
                                 "latency-bound)"}
     for k in (var, roll):
         k["achieved"] = k["flop_per_launch"] / (k["launch_ms"] / 1e3) / 1e12
