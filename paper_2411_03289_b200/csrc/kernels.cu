@@ -367,6 +367,9 @@ GPM_D void rollout_phase2(const RolloutArgs& a, const SmemView& sv, const TaskDe
 #ifndef GPM_EXP_PRESCALE
 #define GPM_EXP_PRESCALE 1
 #endif
+#ifndef GPM_QUERY_BULK
+#define GPM_QUERY_BULK 1
+#endif
 template <int LPS, int SPG, bool FOLD>
 __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const RolloutArgs a) {
   if (threadIdx.x == 0) tl_stamp(1);
@@ -506,9 +509,11 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
         const double2 u = ubuf[j * T + k];
         u0[j] = u.x;
         u1[j] = u.y;
+#if GPM_COOP || !GPM_QUERY_BULK
         if (valid[j] && gl == 0)  // item-major slot: (item, k, sample within the item)
           a.queries[(size_t)((item * T + k) * spb + ls0 + j - (item % chunks) * spb)] =
               make_float4((float)v[j], (float)w[j], (float)u0[j], (float)u1[j]);
+#endif
       }
 #if GPM_COOP
       if (a.progress && gl == 0)  // steps < k+1 of this group's queries are published
@@ -601,6 +606,23 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
       }
     }
     __syncwarp();
+#if !GPM_COOP && GPM_QUERY_BULK
+    // the variance queries of every step, written after the chain from its state record (the
+    // same doubles the chain used): the conversions and stores leave the serial path, and the
+    // group's lanes split the (sample, step) pairs. Item-major slot: (item, k, sample in item).
+    for (int idx = gl; idx < SPG * T; idx += LPS) {
+      const int j = SPG == 1 ? 0 : idx / T, k = SPG == 1 ? idx : idx - j * T;
+      bool vj = valid[0];
+#pragma unroll
+      for (int q = 1; q < SPG; ++q) vj = j == q ? valid[q] : vj;
+      if (vj) {
+        const double* scr = scr0 + (size_t)j * SCR_ARRAYS * stride;
+        const double2 u = ubuf[j * T + k];
+        a.queries[(size_t)((item * T + k) * spb + ls0 + j - (item % chunks) * spb)] =
+            make_float4((float)scr[2 * stride + k], (float)scr[3 * stride + k], (float)u.x, (float)u.y);
+      }
+    }
+#endif
 #ifdef GPM_ROLLOUT_TRACE
     if (blockIdx.x == 0 && threadIdx.x == 0)
       printf("rollout item %lld: prologue %lld phase1 %lld (per step %lld)\n", item, t_p1 - t_item, clock64() - t_p1,
