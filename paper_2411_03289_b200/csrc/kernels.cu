@@ -653,6 +653,7 @@ __global__ void __launch_bounds__(256, GPM_ROLLOUT_MINB) rollout_gp_kernel(const
 }
 
 // GP-free models (mppi.cpp:351-368): one thread per sample; block = one robot chunk.
+constexpr int kBaseSteps = 40;  // steps of controls drawn ahead of the GP-free chain (80 KB at 128 threads)
 __global__ void __launch_bounds__(128) rollout_base_kernel(const RolloutArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const SmemView sv = carve_smem(a, smem);
@@ -681,12 +682,25 @@ __global__ void __launch_bounds__(128) rollout_base_kernel(const RolloutArgs a) 
     bool alive = true;
     double cost = 0.0, decay = 1.0;
     uint32_t vb = 0, cb = 0;
+    // the noise and clamped controls of a chunk of kBaseSteps steps first (mppi.cpp:298-308):
+    // they do not depend on the state chain, so the draws of consecutive steps overlap
+    // instead of sitting on its serial path; [k][thread] in shared memory after the robot view
+    double2* ub = reinterpret_cast<double2*>(sv.pts);
     for (int k = 0; k < T; ++k) {
-      double e0, e1;
-      sample_noise(a, key, sl, s, k, &e0, &e1);
-      if (a.noise_out) reinterpret_cast<double2*>(a.noise_out)[(size_t)sl * T + k] = make_double2(e0, e1);
-      const double u[2] = {clampd(sv.nom[2 * k] + e0, a.lo[0], a.hi[0]),
-                           clampd(sv.nom[2 * k + 1] + e1, a.lo[1], a.hi[1])};
+      if (k % kBaseSteps == 0) {
+        const int k1 = min(T, k + kBaseSteps);
+        for (int kk = k; kk < k1; ++kk) {
+          double e0, e1;
+          sample_noise(a, key, sl, s, kk, &e0, &e1);
+          if (a.noise_out) reinterpret_cast<double2*>(a.noise_out)[(size_t)sl * T + kk] = make_double2(e0, e1);
+          ub[(size_t)(kk - k) * blockDim.x + threadIdx.x] = make_double2(
+              clampd(sv.nom[2 * kk] + e0, a.lo[0], a.hi[0]), clampd(sv.nom[2 * kk + 1] + e1, a.lo[1], a.hi[1]));
+        }
+      }
+      const double2 uk = ub[(size_t)(k % kBaseSteps) * blockDim.x + threadIdx.x];
+      const double u[2] = {uk.x, uk.y};
+      double sp, cp;  // heading of the step's start state: the dynamics and the cost share it
+      sincos(st[2], &sp, &cp);
       double nx[5];
       if (alive) {
         if (a.model_kind == MODEL_EDD5) {
@@ -694,9 +708,7 @@ __global__ void __launch_bounds__(128) rollout_base_kernel(const RolloutArgs a) 
         } else if (a.model_kind == MODEL_UNICYCLE) {
           step_kinematic(st, u, a.nom.dt, nx);
         } else {
-          double sp0, cp0;
-          sincos(st[2], &sp0, &cp0);
-          step_nominal(st, u, a.nom, nx, sp0, cp0);
+          step_nominal(st, u, a.nom, nx, sp, cp);
         }
         if (!finite5(nx)) {
           alive = false;
@@ -705,8 +717,6 @@ __global__ void __launch_bounds__(128) rollout_base_kernel(const RolloutArgs a) 
       } else {
         for (int i = 0; i < 5; ++i) nx[i] = st[i];
       }
-      double sp, cp;
-      sincos(st[2], &sp, &cp);
       const StepCost c = step_cost(task, st, nx, sp, cp, sv.rbar[k], sv.marg + (size_t)k * O, u[0], decay);
       cost += c.cost;
       decay *= 0.9;
@@ -888,9 +898,10 @@ cudaError_t launch_rollout(const RolloutArgs& a, int num_sms, cudaStream_t st) {
     const int threads = 128;
     const long long items = (long long)a.B * ((a.K_local + threads - 1) / threads);
     const long long blocks = items < (long long)num_sms * 8 ? items : (long long)num_sms * 8;
-    cudaError_t e = cudaFuncSetAttribute(rollout_base_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem_b = smem + sizeof(double2) * (size_t)threads * kBaseSteps;  // + the controls chunk
+    cudaError_t e = cudaFuncSetAttribute(rollout_base_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b);
     if (e != cudaSuccess) return e;
-    rollout_base_kernel<<<(unsigned)blocks, threads, smem, st>>>(a);
+    rollout_base_kernel<<<(unsigned)blocks, threads, smem_b, st>>>(a);
   }
   count_launch();
   return cudaGetLastError();
