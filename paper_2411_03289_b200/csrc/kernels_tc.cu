@@ -1446,6 +1446,9 @@ constexpr int P2_RPL = 16 / P2_PRODUCER_WARPS;            // rows per producer l
 #ifndef GPM_P2_ZHOIST
 #define GPM_P2_ZHOIST 1
 #endif
+#ifndef GPM_P2_EARLY_DRAIN
+#define GPM_P2_EARLY_DRAIN 1
+#endif
 #ifndef GPM_P2_FADD2
 #define GPM_P2_FADD2 1
 #endif
@@ -1573,7 +1576,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::P2_THREADS, 1)
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  uint64_t* tfull0 = tempty + 1;  // GPM_P2_EARLY_DRAIN: the lower TMEM half of a pass is final
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull0 + 1);
   if (threadIdx.x == 0) trace_at(0, dbg);
   // warp-uniform in the compiler's view (a lane-0 shuffle): the leader's MMA branch then keeps its
   // descriptors on the uniform datapath instead of a per-MMA elect / R2UR.BROADCAST waterfall
@@ -1603,6 +1607,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::P2_THREADS, 1)
       mbar_init(smem_u32(&empty[s]), 1);
     }
     mbar_init(smem_u32(tfull), 1);
+    mbar_init(smem_u32(tfull0), 1);
     mbar_init(smem_u32(tempty), 8);  // leader: four local + four peer epilogue warps
     fence_barrier_init();
   }
@@ -1685,6 +1690,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::P2_THREADS, 1)
                             smem_desc(bo + (uint32_t)nc[h] * KC, H_SBO), instr_desc_f16_m256(nc[h]), kb > 0 ? 1u : 0u);
                 bo += (uint32_t)nc[h] * KC * 2;
               }
+#if GPM_P2_EARLY_DRAIN
+              // the pass's last chunk that reaches the lower half: its columns are final once
+              // these MMAs complete, so the epilogue drains them under the remaining chunks
+              if (n_pad - p * 512 > 256 && kb == min(nk - 1, 32 * p + 15)) mma2_commit_both(smem_u32(tfull0));
+#endif
             }
             mma2_commit_both(smem_u32(&empty[r.s]));
           }
@@ -1820,20 +1830,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::P2_THREADS, 1)
     const int e = warp - 4;
     const int m = e * 32 + lane;
     const uint32_t lead_tempty = map_rank(smem_u32(tempty), 0);
-    uint32_t uc = 0;
+    uint32_t uc = 0, uc0 = 0;
     for (long long st = sb; st < se; ++st) {
       double ssq = 0.0;
       for (int p = 0; p < n_pass; ++p, ++uc) {
         const int npw = min(512, n_pad - p * 512);
         const int w0 = (min(256, npw) + 31) & ~31, w1 = npw > 256 ? ((npw - 256 + 31) & ~31) : 0;
+        const uint32_t trow = tmem_base + ((uint32_t)(e * 32) << 16);
+#if GPM_P2_EARLY_DRAIN
+        if (w1) {  // the lower half as soon as its last chunk's MMAs complete
+          if (lane == 0) mbar_wait_xp(smem_u32(tfull0), uc0 & 1, 5, dbg);
+          ++uc0;
+          __syncwarp();
+          tc_after();
+          if (!GPM_DIAG(dbg & 8)) ssq += drain_ssq(trow, w0);
+        }
+#endif
         if (lane == 0) mbar_wait_xp(smem_u32(tfull), uc & 1, 5, dbg);
         if (lane == 0 && e == 0 && uc < 10) trace_at(24 + (int)uc, dbg);
         __syncwarp();
         tc_after();
-        const uint32_t trow = tmem_base + ((uint32_t)(e * 32) << 16);
         if (!GPM_DIAG(dbg & 8)) {  // dbg 8: no TMEM drain
+#if GPM_P2_EARLY_DRAIN
+          if (w1)
+            ssq += drain_ssq(trow + 256, w1);
+          else
+            ssq += drain_ssq(trow, w0);
+#else
           ssq += drain_ssq(trow, w0);
           if (w1) ssq += drain_ssq(trow + 256, w1);
+#endif
         }
         tc_before();
         __syncwarp();
@@ -2191,7 +2217,7 @@ size_t f16_smem_bytes(const GroupDev& g, int stages, int cps = 1) {
 
 size_t f16x2_smem_bytes(const GroupDev& g, int stages, int cps = 1) {
   return 1024 + (size_t)stages * cps * tc::P2_STAGE + sizeof(float) * 5 * (size_t)g.tc_npad +
-         sizeof(uint64_t) * (2 * stages + 2) + 16;
+         sizeof(uint64_t) * (2 * stages + 3) + 16;
 }
 
 size_t tc2u_smem_bytes(const GroupDev& g, int stages) {
